@@ -1,0 +1,545 @@
+#!/usr/bin/env python
+"""bench.py — co-run prefill + decode attention on one unified paged KV pool.
+
+Workload (BASELINE.json configs[1], "Llama-3-8B attention shapes bf16"): 32 layers,
+32 q / 8 kv heads, d = 128, block 16; per step (one co-run iteration, SURVEY §8(a)
+rows a1-a9):
+  stream P (prefill worker): alloc 128 blocks for the prefill request, then for each
+    layer semipd_prefill_attn on one 2048-token chunk (P = 0; K/V write + causal GQA
+    attention), then free the request's blocks;
+  stream D (decode worker), concurrently: for each layer semipd_decode_attn on 64
+    requests at ctx 2048 (K/V append + split-K paged attention).
+The two persistent grids are capped to the (x, y) SM partition.  A short
+sweep over x picks the best split during warm-up; the K timed steps run at it.
+
+metric: attention-stack tokens/s = (2048 prefill + 64 decode tokens) x steps / time
+(each token through all 32 layers).  value = device time (CUDA events, max over
+ranks), inputs resident in HBM; e2e = the same through the public API with pinned
+host inputs copied in and outputs copied out every step.
+
+Multi-GPU (torchrun, N ranks): tensor parallel by KV head (Hq/N, Hkv/N per rank,
+own pool shard), NCCL all-gather of head-major outputs per layer on a per-phase
+process group, strong scaling.  --impl reference times the fp64 oracle
+(oracle/, the reference arm of this tier) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+MODELS = {"llama3-8b": synth.CFG2_LLAMA8B, "llama3-70b": synth.CFG3_LLAMA70B}
+PREFILL_TOKENS = 2048
+DECODE_BATCH = 64
+DECODE_CTX = 2048
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="semipd", choices=["semipd", "reference"])
+    ap.add_argument("--model", default="llama3-8b", choices=list(MODELS))
+    ap.add_argument("--split", type=float, default=None, help="prefill SM percent x (y = 100-x)")
+    ap.add_argument("--sweep", default="30,40,50,60,70")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--extra", action="store_true", help="serial / (100,100) / isolated curves")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(
+            d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- workload
+class Workload:
+    """Pool + resident inputs for one rank (head shard under TP)."""
+
+    def __init__(self, shape: synth.AttnShape, tp: int, dev: torch.device, seed: int = 1020):
+        from paper_2504_19867_b200 import KVPool, PoolConfig
+        self.full = shape
+        self.shape = synth.shard_heads(shape, tp) if tp > 1 else shape
+        self.tp, self.dev = tp, dev
+        s = self.shape
+        self.L = s.num_layers
+        self.B, self.ctx, self.C = DECODE_BATCH, DECODE_CTX, PREFILL_TOKENS
+        bs = s.block_size
+        self.nb_dec = self.ctx // bs + 1                 # slot ctx needs block ctx // bs
+        self.nb_pre = -(-self.C // bs)
+        n_blocks = self.B * self.nb_dec + self.nb_pre + 64
+        self.cfg = PoolConfig(num_layers=self.L, num_blocks=n_blocks, block_size=bs,
+                              num_kv_heads=s.num_kv_heads, head_dim_k=s.head_dim_k,
+                              head_dim_v=s.head_dim_v, max_reqs=self.B + 2,
+                              max_blocks_per_req=self.nb_dec + 8, dtype=s.dtype)
+        self.pool = KVPool(self.cfg, dev)
+        i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+        self.rid_dec = i32(list(range(self.B)))
+        self.ctx_lens = i32([self.ctx] * self.B)
+        self.pool.alloc_blocks(self.rid_dec, i32([self.nb_dec] * self.B))
+        self.rid_pre = i32([self.B])
+        self.nblk_pre = i32([self.nb_pre])
+        self.cu = i32([0, self.C])
+        self.prefix = i32([0])
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        # cached context: random bf16 in every layer's pool (distinct memory per layer,
+        # so the per-step decode working set (L x 537 MB) is far larger than L2)
+        for l in range(self.L):
+            K, V, _, _ = self.pool.views(l)
+            K.normal_(generator=g)
+            V.normal_(generator=g)
+        Hq, Hkv, d = s.num_q_heads, s.num_kv_heads, s.head_dim_k
+        mk = lambda *shp: torch.randn(*shp, generator=g, device=dev, dtype=torch.float32).to(s.dtype)  # noqa: E731
+        self.qp = [mk(self.C, Hq, d) for _ in range(self.L)]
+        self.kp = [mk(self.C, Hkv, d) for _ in range(self.L)]
+        self.vp = [mk(self.C, Hkv, d) for _ in range(self.L)]
+        self.qd = [mk(self.B, Hq, d) for _ in range(self.L)]
+        self.kd = [mk(self.B, Hkv, d) for _ in range(self.L)]
+        self.vd = [mk(self.B, Hkv, d) for _ in range(self.L)]
+        hm = tp > 1
+        self.op = [torch.empty((Hq, self.C, d) if hm else (self.C, Hq, d), dtype=s.dtype,
+                               device=dev) for _ in range(self.L)]
+        self.od = [torch.empty((Hq, self.B, d) if hm else (self.B, Hq, d), dtype=s.dtype,
+                               device=dev) for _ in range(self.L)]
+        self.ws = self.pool.new_decode_workspace(self.B, Hq, self.ctx)
+        self.scale = s.softmax_scale
+        self.sP = torch.cuda.Stream(device=dev)
+        self.sD = torch.cuda.Stream(device=dev)
+        self.pg_p = self.pg_d = None
+        self.gath_p = self.gath_d = None
+        if tp > 1:
+            import torch.distributed as dist
+            ranks = list(range(tp))
+            self.pg_p = dist.new_group(ranks, backend="nccl")   # prefill workers' group
+            self.pg_d = dist.new_group(ranks, backend="nccl")   # decode workers' group
+            self.gath_p = torch.empty((self.full.num_q_heads, self.C, d), dtype=s.dtype, device=dev)
+            self.gath_d = torch.empty((self.full.num_q_heads, self.B, d), dtype=s.dtype, device=dev)
+        # per-launch timing events (decode kernel on stream D, prefill call on stream P)
+        self.ev_d = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                     for _ in range(self.L)]
+        self.ev_p = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                     for _ in range(self.L)]
+
+    # algorithmic work: count unmasked pairs and K/V bytes once
+    def decode_bytes_per_launch(self) -> float:
+        s = self.shape
+        eb = 2
+        kv = self.B * (self.ctx + 1) * s.num_kv_heads * (s.head_dim_k + s.head_dim_v) * eb
+        io = self.B * s.num_q_heads * (s.head_dim_k + s.head_dim_v) * eb  # q in, o out
+        return float(kv + io)
+
+    def prefill_flops_per_launch(self) -> float:
+        s = self.shape
+        pairs = self.C * (self.C + 1) / 2
+        return 2.0 * s.num_q_heads * (s.head_dim_k + s.head_dim_v) * pairs
+
+    def phase_prefill(self, budget, timed=False, stream=None):
+        s = stream or self.sP
+        p = self.pool
+        with torch.cuda.stream(s):
+            p.alloc_blocks(self.rid_pre, self.nblk_pre, None, stream=s)
+            for l in range(self.L):
+                if timed:
+                    self.ev_p[l][0].record(s)
+                p.prefill_attn(l, self.qp[l], self.kp[l], self.vp[l], self.cu, self.rid_pre,
+                               self.prefix, self.C, self.C, self.scale, self.op[l],
+                               out_head_major=self.tp > 1, sm_budget=budget, stream=s)
+                if timed:
+                    self.ev_p[l][1].record(s)
+                if self.tp > 1:
+                    import torch.distributed as dist
+                    dist.all_gather_into_tensor(self.gath_p, self.op[l], group=self.pg_p)
+            p.free_blocks(self.rid_pre, None, stream=s)
+
+    def phase_decode(self, budget, timed=False, stream=None):
+        s = stream or self.sD
+        p = self.pool
+        with torch.cuda.stream(s):
+            for l in range(self.L):
+                if timed:
+                    self.ev_d[l][0].record(s)
+                p.decode_attn(l, self.qd[l], self.kd[l], self.vd[l], self.rid_dec, self.ctx_lens,
+                              self.ctx, self.scale, self.od[l], self.ws,
+                              out_head_major=self.tp > 1, sm_budget=budget, stream=s)
+                if timed:
+                    self.ev_d[l][1].record(s)
+                if self.tp > 1:
+                    import torch.distributed as dist
+                    dist.all_gather_into_tensor(self.gath_d, self.od[l], group=self.pg_d)
+
+    def corun_step(self, x, y, timed=False):
+        """One co-run iteration: both workers concurrently at budgets from (x, y)."""
+        main = torch.cuda.current_stream(self.dev)
+        self.pool.set_partition(x, y)
+        self.sP.wait_stream(main)
+        self.sD.wait_stream(main)
+        self.phase_prefill(0, timed)
+        self.phase_decode(0, timed)
+        main.wait_stream(self.sP)
+        main.wait_stream(self.sD)
+
+    def serial_step(self):
+        """Time-sliced baseline (unified system): each phase on all SMs in turn."""
+        main = torch.cuda.current_stream(self.dev)
+        n = self.pool.num_sms
+        self.phase_prefill(n, stream=main)
+        self.phase_decode(n, stream=main)
+
+    def uncontrolled_step(self):
+        """(100,100): non-persistent grids on both streams, hardware arbitrates."""
+        main = torch.cuda.current_stream(self.dev)
+        self.sP.wait_stream(main)
+        self.sD.wait_stream(main)
+        self.phase_prefill(-1)
+        self.phase_decode(-1)
+        main.wait_stream(self.sP)
+        main.wait_stream(self.sD)
+
+
+def time_steps(fn, steps, dev, barrier=None):
+    torch.cuda.synchronize(dev)
+    if barrier:
+        barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    if barrier:
+        barrier()
+    return e0.elapsed_time(e1) / 1e3  # seconds
+
+
+# ----------------------------------------------------------------------------- e2e
+class E2E:
+    """Same step through the public API with pinned host inputs/outputs (copies
+    inside the timed region, on each phase's stream)."""
+
+    def __init__(self, w: Workload):
+        self.w = w
+        pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+        self.h_qp = [pin(t) for t in w.qp]
+        self.h_kp = [pin(t) for t in w.kp]
+        self.h_vp = [pin(t) for t in w.vp]
+        self.h_qd = [pin(t) for t in w.qd]
+        self.h_kd = [pin(t) for t in w.kd]
+        self.h_vd = [pin(t) for t in w.vd]
+        self.h_op = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in w.op]
+        self.h_od = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in w.od]
+        self.h2d = sum(t.numel() * t.element_size() for lst in
+                       (self.h_qp, self.h_kp, self.h_vp, self.h_qd, self.h_kd, self.h_vd) for t in lst)
+        self.d2h = sum(t.numel() * t.element_size() for lst in (self.h_op, self.h_od) for t in lst)
+
+    def step(self, x, y):
+        w = self.w
+        main = torch.cuda.current_stream(w.dev)
+        w.pool.set_partition(x, y)
+        w.sP.wait_stream(main)
+        w.sD.wait_stream(main)
+        with torch.cuda.stream(w.sP):
+            w.pool.alloc_blocks(w.rid_pre, w.nblk_pre, None, stream=w.sP)
+            for l in range(w.L):
+                w.qp[l].copy_(self.h_qp[l], non_blocking=True)
+                w.kp[l].copy_(self.h_kp[l], non_blocking=True)
+                w.vp[l].copy_(self.h_vp[l], non_blocking=True)
+                w.pool.prefill_attn(l, w.qp[l], w.kp[l], w.vp[l], w.cu, w.rid_pre, w.prefix, w.C,
+                                    w.C, w.scale, w.op[l], out_head_major=w.tp > 1, stream=w.sP)
+                self.h_op[l].copy_(w.op[l], non_blocking=True)
+            w.pool.free_blocks(w.rid_pre, None, stream=w.sP)
+        with torch.cuda.stream(w.sD):
+            for l in range(w.L):
+                w.qd[l].copy_(self.h_qd[l], non_blocking=True)
+                w.kd[l].copy_(self.h_kd[l], non_blocking=True)
+                w.vd[l].copy_(self.h_vd[l], non_blocking=True)
+                w.pool.decode_attn(l, w.qd[l], w.kd[l], w.vd[l], w.rid_dec, w.ctx_lens, w.ctx,
+                                   w.scale, w.od[l], w.ws, out_head_major=w.tp > 1, stream=w.sD)
+                self.h_od[l].copy_(w.od[l], non_blocking=True)
+        main.wait_stream(w.sP)
+        main.wait_stream(w.sD)
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample_rate(shape: synth.AttnShape, threads: int, budget_s: float = 12.0):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload and
+    extrapolate to attention-stack tokens/s for the full step.  Sample: decode =
+    whole requests (ctx 2048, all heads, one layer); prefill = rows of the 2048
+    chunk at evenly spaced positions (all heads, one layer)."""
+    import oracle
+    oracle.set_threads(threads)
+    s = shape
+    bs = s.block_size
+    rng = np.random.default_rng(0)
+    # decode sample: n_req requests
+    n_req = 2
+    nb = DECODE_CTX // bs + 1
+    kpool = (rng.standard_normal((n_req * nb, s.num_kv_heads, bs, s.head_dim_k)) * 1).astype(np.float32)
+    vpool = rng.standard_normal((n_req * nb, s.num_kv_heads, bs, s.head_dim_v)).astype(np.float32)
+    to_bits = lambda a: (a.view(np.uint32) >> 16).astype(np.uint16)  # noqa: E731 (bf16 bit patterns)
+    kpool, vpool = to_bits(kpool), to_bits(vpool)
+    bt = np.arange(n_req * nb, dtype=np.int32).reshape(n_req, nb)
+    q = to_bits(rng.standard_normal((n_req, s.num_q_heads, s.head_dim_k)).astype(np.float32))
+    kn = to_bits(rng.standard_normal((n_req, s.num_kv_heads, s.head_dim_k)).astype(np.float32))
+    vn = to_bits(rng.standard_normal((n_req, s.num_kv_heads, s.head_dim_v)).astype(np.float32))
+    t0 = time.perf_counter()
+    oracle.decode(q, kn, vn, kpool, vpool, bt, list(range(n_req)), [DECODE_CTX] * n_req,
+                  s.softmax_scale)
+    t_dec_req = (time.perf_counter() - t0) / n_req
+    # prefill sample: every stride-th row of a 2048 chunk
+    C = PREFILL_TOKENS
+    stride = 64
+    nbp = -(-C // bs)
+    kpp = np.zeros((nbp, s.num_kv_heads, bs, s.head_dim_k), np.uint16)
+    vpp = np.zeros((nbp, s.num_kv_heads, bs, s.head_dim_v), np.uint16)
+    btp = np.arange(nbp, dtype=np.int32).reshape(1, nbp)
+    qp = to_bits(rng.standard_normal((C, s.num_q_heads, s.head_dim_k)).astype(np.float32))
+    kp = to_bits(rng.standard_normal((C, s.num_kv_heads, s.head_dim_k)).astype(np.float32))
+    vp = to_bits(rng.standard_normal((C, s.num_kv_heads, s.head_dim_v)).astype(np.float32))
+    mask = np.zeros(C, np.uint8)
+    mask[stride // 2::stride] = 1
+    t0 = time.perf_counter()
+    oracle.prefill(qp, kp, vp, kpp, vpp, btp, [0, C], [0], [0], s.softmax_scale, rows_mask=mask)
+    t_pre_rows = time.perf_counter() - t0
+    t_pre_chunk = t_pre_rows * C / int(mask.sum())
+    t_step = s.num_layers * (DECODE_BATCH * t_dec_req + t_pre_chunk)
+    tokens = PREFILL_TOKENS + DECODE_BATCH
+    sample = (f"{n_req} decode requests (ctx {DECODE_CTX}, all {s.num_q_heads} heads, 1 layer) + "
+              f"{int(mask.sum())} of {C} prefill rows (every {stride}th, all heads, 1 layer); "
+              f"extrapolated x{s.num_layers} layers, x{DECODE_BATCH} requests, x{C} rows")
+    return tokens / t_step, sample, time.perf_counter()
+
+
+def run_reference(args):
+    ws, rank, _ = dist_info()
+    if rank != 0:
+        return 0
+    shape = MODELS[args.model]
+    threads = os.cpu_count() or 1
+    vals = []
+    t_start = time.perf_counter()
+    for i in range(args.warmup + args.steps):
+        v, sample, _ = oracle_sample_rate(shape, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    elapsed = time.perf_counter() - t_start
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": "co-run prefill+decode attention tokens/s (32-layer stack)",
+        "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * (PREFILL_TOKENS + DECODE_BATCH) / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{shape.name}: decode B={DECODE_BATCH} "
+                                        f"ctx={DECODE_CTX} + prefill chunk {PREFILL_TOKENS}"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": elapsed,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    ws, rank, local = dist_info()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    barrier = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        barrier = lambda: dist.barrier()  # noqa: E731
+    shape = MODELS[args.model]
+    w = Workload(shape, ws, dev)
+    hbm_peak, bf16_peak, bf16_sus, peak_kind = peaks()
+    W = max(3, args.warmup)
+    splits = [float(x) for x in args.sweep.split(",")] if args.split is None else [args.split]
+    # warm-up + split sweep (1 timed step per split, not part of the reported number)
+    for _ in range(2):
+        w.corun_step(50, 50)
+    sweep = []
+    for x in splits:
+        t = time_steps(lambda: w.corun_step(x, 100 - x), 1, dev, barrier)
+        if ws > 1:
+            tt = torch.tensor([t], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t = float(tt.item())
+        sweep.append({"x": x, "y": 100 - x, "n_p": w.pool.sm_budgets()[0],
+                      "n_d": w.pool.sm_budgets()[1],
+                      "tokens_per_s": (PREFILL_TOKENS + DECODE_BATCH) / t, "ms": t * 1e3})
+    best = max(sweep, key=lambda r: r["tokens_per_s"])
+    x, y = best["x"], best["y"]
+    for _ in range(W):
+        w.corun_step(x, y)
+    # ---- timed region
+    launches0 = w.pool.launch_count()
+    with ClockSampler(local) as clk:
+        t = time_steps(lambda: w.corun_step(x, y, timed=True), args.steps, dev, barrier)
+    launches = w.pool.launch_count() - launches0
+    if ws > 1:
+        tt = torch.tensor([t], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    tokens = (PREFILL_TOKENS + DECODE_BATCH) * args.steps
+    value = tokens / t
+    # per-launch kernel times (last timed step's events)
+    dec_ms = statistics.mean(a.elapsed_time(b) for a, b in w.ev_d)
+    pre_ms = statistics.mean(a.elapsed_time(b) for a, b in w.ev_p)
+    dec_gbs = w.decode_bytes_per_launch() / (dec_ms / 1e3) / 1e9
+    pre_tfs = w.prefill_flops_per_launch() / (pre_ms / 1e3) / 1e12
+    n_p, n_d = w.pool.sm_budgets()
+    dec_total, pre_total = dec_ms * w.L, pre_ms * w.L
+    dominant = "decode" if dec_total >= pre_total else "prefill"
+    roof_dec = {"kernel": "decode_bf16_kernel (split-K paged decode)", "bound": "hbm",
+                "achieved": dec_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": dec_gbs / hbm_peak,
+                "peak_kind": peak_kind, "traffic": None,
+                "algorithmic_bytes_per_launch": w.decode_bytes_per_launch(),
+                "avg_launch_ms": dec_ms, "sm_budget": n_d}
+    share = n_p / w.pool.num_sms
+    roof_pre = {"kernel": "prefill_tc_kernel (+kv_write) tcgen05 causal GQA", "bound": "tensor",
+                "achieved": pre_tfs, "peak": bf16_sus, "unit": "TFLOP/s",
+                "frac": pre_tfs / bf16_sus, "frac_share_scaled": pre_tfs / (bf16_sus * share),
+                "peak_kind": f"{peak_kind} sustained", "traffic": None,
+                "algorithmic_flops_per_launch": w.prefill_flops_per_launch(),
+                "avg_launch_ms": pre_ms, "sm_budget": n_p}
+    extra = {}
+    if args.extra:
+        ts = time_steps(w.serial_step, 2, dev, barrier) / 2
+        tu = time_steps(w.uncontrolled_step, 2, dev, barrier) / 2
+        extra = {"serial_ms": ts * 1e3, "uncontrolled_100_100_ms": tu * 1e3,
+                 "corun_ms": t / args.steps * 1e3,
+                 "speedup_vs_serial": ts / (t / args.steps),
+                 "speedup_vs_100_100": tu / (t / args.steps)}
+    e2e = None
+    if not args.no_e2e:
+        ee = E2E(w)
+        for _ in range(2):
+            ee.step(x, y)
+        te = time_steps(lambda: ee.step(x, y), max(2, min(args.steps, 5)), dev, barrier)
+        te /= max(2, min(args.steps, 5))
+        if ws > 1:
+            tt = torch.tensor([te], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": (PREFILL_TOKENS + DECODE_BATCH) / te, "unit": "tokens/s",
+               "h2d_bytes_per_step": ee.h2d, "d2h_bytes_per_step": ee.d2h,
+               "ms_per_step": te * 1e3}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        v, sample, _ = oracle_sample_rate(shape, threads)
+        cpu = {"value": v, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+               "sample": sample}
+    if rank == 0:
+        line = {
+            "metric": "co-run prefill+decode attention tokens/s (32-layer stack)",
+            "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": W,
+            "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{shape.name} attention (Hq {shape.num_q_heads}, Hkv "
+                                   f"{shape.num_kv_heads}, d 128, bs 16, {shape.num_layers} layers): "
+                                   f"decode B={DECODE_BATCH} ctx={DECODE_CTX} + prefill chunk "
+                                   f"{PREFILL_TOKENS} (P=0), co-run",
+                       "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d},
+                       "parallelism": f"tp{ws} (KV-head shards, NCCL all-gather)" if ws > 1 else "tp1",
+                       "l2": "no flush: per-step decode working set "
+                             f"{w.L * w.decode_bytes_per_launch() / 1e9:.1f} GB >> 126 MB L2"},
+            "roofline": roof_dec if dominant == "decode" else roof_pre,
+            "roofline_decode": roof_dec, "roofline_prefill": roof_pre,
+            "decode_tokens_per_s": DECODE_BATCH * args.steps / t,
+            "prefill_tokens_per_s": PREFILL_TOKENS * args.steps / t,
+            "sweep": sweep, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": launches, "extra": extra or None,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,224 @@
+/*
+ * semipd.h — C ABI of libsemipd.so, the B200 (sm_100a) hot path of semi-PD
+ * (arXiv 2504.19867): prefill and decode attention co-running on disjoint SM
+ * partitions of one GPU over ONE unified paged KV-cache pool.
+ *
+ * Paper passages (PAPER.md line, section):
+ *   P:184 §4.2  prefill writes the request's K/V "into the KV cache"; decode
+ *               updates it "at each decode iteration"; a request moves from the
+ *               prefill worker's queue to the decode worker's after prefill.
+ *   P:195 §4.3  "(x, y) ... the percentage of the total SMs dispatched to the
+ *               prefill and decode processes".
+ *   P:209-216   resident holder of weights + KV, delayed and asynchronous switching;
+ *               x + y > 100 is allowed ("compete for the resources").
+ *   P:229 §4.4  paged KV "accessed through the block table index"; allocation
+ *               (query -> get -> update) is atomic: "the memory utilization is
+ *               locked until the update step finishes".
+ *   P:355 §6    GQA attention kernels for both phases.
+ * SPEC.md (allocator contract): S:234-262.
+ *
+ * Conventions (all functions):
+ *   - Pointers are DEVICE pointers unless documented "host".  All device work is
+ *     stream-ordered on the given stream (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream).  No call allocates device memory: the caller owns
+ *     the pool backing memory, all I/O tensors and workspaces (PyTorch allocates
+ *     them in the Python binding) and must keep them alive while in use.
+ *   - Host argument errors return SEMIPD_ERR_INVALID / SEMIPD_ERR_UNSUPPORTED
+ *     synchronously and launch nothing.  Device-side outcomes (OOM, unknown free,
+ *     table full, bad block) are written to *status_dev (int32, may be NULL) on
+ *     the stream; the call itself returns SEMIPD_OK once launched.
+ *   - n == 0 / batch == 0 / empty chunk is a no-op returning SEMIPD_OK.
+ *   - Element dtype of every activation tensor equals the pool dtype.
+ *   - One in-flight prefill call and one in-flight decode call per pool (one
+ *     prefill worker stream and one decode worker stream); allocator calls
+ *     may come from any number of streams / host threads (linearizable).
+ */
+#ifndef SEMIPD_H
+#define SEMIPD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct semipd_pool* semipd_pool_t; /* opaque; owned by the library */
+typedef void* semipd_stream_t;             /* cudaStream_t */
+
+typedef enum {
+    SEMIPD_OK = 0,
+    SEMIPD_ERR_INVALID = 1,     /* bad host argument (nothing launched) */
+    SEMIPD_ERR_OOM = 2,         /* alloc: sum(n_blocks) > free blocks; a normal outcome */
+    SEMIPD_ERR_UNKNOWN_REQ = 3, /* free of a request holding no blocks / repeated id */
+    SEMIPD_ERR_TABLE_FULL = 4,  /* alloc would exceed max_blocks_per_req */
+    SEMIPD_ERR_BAD_BLOCK = 5,   /* attention met a block-table entry outside [0, num_blocks) */
+    SEMIPD_ERR_CUDA = 6,        /* a CUDA runtime error (launch / attribute) */
+    SEMIPD_ERR_UNSUPPORTED = 7  /* valid but unsupported shape / dtype combination */
+} semipd_status;
+
+typedef enum { SEMIPD_BF16 = 0, SEMIPD_FP32 = 1 } semipd_dtype;
+
+/* Pool geometry.  One block id spans all layers (reading R8).
+ * Layout in the caller's memory (device), every region 1 KiB aligned:
+ *   [state words | free_stack int32[num_blocks] | nblk int32[max_reqs] |
+ *    block_tables int32[max_reqs][max_blocks_per_req] | op log int32[oplog_words] |
+ *    for l in layers: K_l [num_blocks][num_kv_heads][block_size][head_dim_k],
+ *                     V_l [num_blocks][num_kv_heads][block_size][head_dim_v] (absent if kv_shared)]
+ * "HND" pages: one (block, kv head) page is contiguous (4 KiB at bs 16, d 128, bf16). */
+typedef struct {
+    int32_t num_layers;
+    int32_t num_blocks;         /* N_B */
+    int32_t block_size;         /* tokens per block: 16, 32, 64 or 128 */
+    int32_t num_kv_heads;       /* Hkv (per rank under TP) */
+    int32_t head_dim_k;         /* dk */
+    int32_t head_dim_v;         /* dv */
+    int32_t kv_shared;          /* 1 = MLA latent cache: V aliases K[..., :head_dim_v] (dv <= dk) */
+    int32_t max_reqs;           /* rows of the block table; request ids are in [0, max_reqs) */
+    int32_t max_blocks_per_req; /* MBR */
+    int32_t dtype;              /* semipd_dtype */
+    int32_t device;             /* CUDA device ordinal the memory lives on */
+    int32_t oplog_words;        /* int32 capacity of the allocator op log (0 = no log) */
+} semipd_pool_config;
+
+/* Bytes of device memory semipd_kv_pool_create needs for cfg (host; 0 if cfg invalid). */
+size_t semipd_kv_pool_bytes(const semipd_pool_config* cfg);
+
+/* Carve `mem` (>= semipd_kv_pool_bytes(cfg) bytes, 1 KiB aligned, device memory on
+ * cfg->device) into the pool and initialise it on stream s: free stack
+ * [N_B-1 ... 0] (first pops return 0, 1, 2, ...), top = N_B, tables = -1, counts 0,
+ * K/V zero-filled.  Writes the new handle to *out (host).  The memory stays owned by
+ * the caller and must outlive the pool.  Errors: INVALID (bad cfg / NULL), CUDA. */
+semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, size_t bytes,
+                                    semipd_stream_t s, semipd_pool_t* out);
+
+/* Release the handle (host state only; the caller frees the memory). */
+semipd_status semipd_kv_pool_destroy(semipd_pool_t pool);
+
+/* Borrowed device views (any pointer may be NULL): layer's K and V base
+ * ([N_B][Hkv][bs][d]; V == K for kv_shared), block_tables [max_reqs][MBR], nblk
+ * [max_reqs].  INVALID if layer is out of range. */
+semipd_status semipd_kv_pool_views(semipd_pool_t pool, int32_t layer, void** k, void** v,
+                                   int32_t** block_tables, int32_t** nblk);
+
+/* ---- Unified memory manager: atomic block allocator (§4.4) ----
+ * alloc: for i in argument order, append n_blocks[i] blocks (popped from the LIFO
+ * free stack) to row req_ids[i].  All-or-nothing per call (reading R10): INVALID
+ * (id outside [0,max_reqs) or n_blocks[i] < 1), else OOM if
+ * sum(n_blocks) > free, else TABLE_FULL if a row would exceed MBR; any error
+ * leaves the state unchanged.  The query -> get -> update sequence runs inside a
+ * device lock (acquire/release) held by one CTA, so calls from different streams
+ * linearise; each call's linearisation order is recorded in the op log.
+ *   req_ids, n_blocks: device int32[n].  n: host.  status_dev: device int32 or NULL. */
+semipd_status semipd_alloc_blocks(semipd_pool_t pool, const int32_t* req_ids,
+                                  const int32_t* n_blocks, int32_t n, int32_t* status_dev,
+                                  semipd_stream_t s);
+
+/* free: push every block of each listed request back in table order, reset its
+ * row to -1 and its count to 0.  UNKNOWN_REQ if a request holds no blocks or is
+ * listed twice (double release); INVALID if an id is out of range; any error
+ * rejects the whole call unchanged.  Stream order with the last kernel that read
+ * those blocks is the caller's job (hazard H2). */
+semipd_status semipd_free_blocks(semipd_pool_t pool, const int32_t* req_ids, int32_t n,
+                                 int32_t* status_dev, semipd_stream_t s);
+
+/* ceil(tokens / block_size); 0 -> 0; -1 if tokens < 0 or block_size <= 0. */
+int32_t semipd_blocks_for_tokens(int32_t tokens, int32_t block_size);
+
+/* Host-out stats: current free blocks and the minimum ever seen (utilisation
+ * high-water).  Synchronises stream s. */
+semipd_status semipd_pool_stats(semipd_pool_t pool, int32_t* free_blocks,
+                                int32_t* min_free_seen, semipd_stream_t s);
+
+/* Test hook (synchronises s): copy the op log to host_buf (<= bytes) and report
+ * its length in int32 words (*n_words) and the number of ops not logged because
+ * the log was full (*dropped).  Record: {seq, kind (1 alloc, 2 free), n, status,
+ * req_ids[n], (alloc only) n_blocks[n]}, in linearisation (seq) order. */
+semipd_status semipd_pool_oplog(semipd_pool_t pool, int32_t* host_buf, size_t bytes,
+                                int64_t* n_words, int64_t* dropped, semipd_stream_t s);
+
+/* ---- Computational resource controller ----
+ * Set the (x, y) SM percentages of the prefill and decode phases, 0 < x, y <= 100;
+ * x + y > 100 is allowed (oversubscription).  Budgets are
+ * n = clamp(floor(num_SMs * pct / 100 + 1/2), 1, num_SMs).  Thread-safe atomic
+ * host store; each phase adopts it at its next launch (delayed + asynchronous
+ * switching); the pool, and so the KV cache, never moves.  INVALID if out of range. */
+semipd_status semipd_set_partition(semipd_pool_t pool, double x_prefill_pct,
+                                   double y_decode_pct);
+/* Host-out current budgets (CTAs each phase's persistent grid is capped to). */
+semipd_status semipd_get_sm_budgets(semipd_pool_t pool, int32_t* n_prefill,
+                                    int32_t* n_decode);
+/* SM count of the pool's device (host). */
+int32_t semipd_num_sms(semipd_pool_t pool);
+
+/* ---- Prefill attention (P:184, P:355, P:365 chunked prefill) ----
+ * For request i (block-table row req_ids[i]) with chunk rows cu_seqlens_q[i] ..
+ * cu_seqlens_q[i+1]-1 and prefix_lens[i] tokens already cached:
+ *   1. writes k_new/v_new rows into the pool slots prefix_lens[i] + t (bit-exact);
+ *   2. O[t,h,:] = sum_{j <= P_i + t} softmax_j(softmax_scale * q[t,h]·k[j,g(h)]) v[j,g(h)],
+ *      g(h) = h / (num_q_heads / Hkv), keys read from the paged pool (bottom-right
+ *      causal alignment).
+ * Blocks covering positions [0, P_i + C_i) must be allocated (semipd_alloc_blocks);
+ * an entry outside [0, N_B) sets *status_dev = BAD_BLOCK and is read as zeros.
+ *   q [T][Hq][dk], k_new [T][Hkv][dk], v_new [T][Hkv][dv] (v_new ignored if
+ *   kv_shared), out [T][Hq][dv] or, if out_head_major, [Hq][T][dv];
+ *   cu_seqlens_q device int32[n+1], req_ids / prefix_lens device int32[n];
+ *   total_q (host) = T = cu_seqlens_q[n]; max_chunk_len (host) >= every C_i;
+ *   sm_budget (host): > 0 caps the persistent grid to that many CTAs, 0 = the
+ *   partition's prefill budget, -1 = non-persistent (one CTA per work unit; the
+ *   "(100,100) uncontrolled" baseline).
+ * bf16 with dk = dv = 128 and (Hq/Hkv) | 128 runs the tcgen05/TMEM/TMA kernel;
+ * other shapes run the generic CUDA-core kernel.  Output is bitwise identical
+ * for every sm_budget (the work decomposition depends on shapes only). */
+semipd_status semipd_prefill_attn(semipd_pool_t pool, int32_t layer, const void* q,
+                                  const void* k_new, const void* v_new,
+                                  const int32_t* cu_seqlens_q, const int32_t* req_ids,
+                                  const int32_t* prefix_lens, int32_t n, int32_t total_q,
+                                  int32_t max_chunk_len, int32_t num_q_heads,
+                                  float softmax_scale, void* out, int32_t out_head_major,
+                                  int32_t sm_budget, int32_t* status_dev, semipd_stream_t s);
+
+/* ---- Decode attention (P:184, P:229 PagedAttention) ----
+ * For each b: writes k_new[b]/v_new[b] to slot ctx_lens[b] (tokens cached BEFORE
+ * the step, reading R5) of row req_ids[b] (the block covering that slot must be
+ * allocated), then O[b,h,:] = attention of q[b,h] over keys 0 .. ctx_lens[b]
+ * inclusive.  Split-K: keys are cut into S_b = ceil((ctx+1)/4096) splits of equal
+ * 32-key-rounded length; partials are merged in split-index order by the last CTA
+ * to finish (fused, no extra launch).
+ *   q [B][Hq][dk], k_new [B][Hkv][dk], v_new [B][Hkv][dv], out [B][Hq][dv] or
+ *   [Hq][B][dv] if out_head_major; req_ids / ctx_lens device int32[B];
+ *   max_ctx_len (host) >= every ctx_lens[b];
+ *   workspace: device scratch of >= semipd_decode_workspace_bytes(...) bytes,
+ *   ZERO-FILLED before its first use (the kernels leave their counters at zero);
+ *   sm_budget as in semipd_prefill_attn (0 = partition's decode budget). */
+semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* q,
+                                 const void* k_new, const void* v_new, const int32_t* req_ids,
+                                 const int32_t* ctx_lens, int32_t batch, int32_t max_ctx_len,
+                                 int32_t num_q_heads, float softmax_scale, void* out,
+                                 int32_t out_head_major, void* workspace, size_t ws_bytes,
+                                 int32_t sm_budget, int32_t* status_dev, semipd_stream_t s);
+
+/* Workspace bytes for decode calls with batch <= max_batch and ctx <= max_ctx (host). */
+size_t semipd_decode_workspace_bytes(semipd_pool_t pool, int32_t max_batch,
+                                     int32_t num_q_heads, int32_t max_ctx);
+
+/* ---- Instrumentation (host) ----
+ * Number of kernels this pool handle has launched so far (every launch the
+ * library issues is counted).  Used for bench.py's "gpu_launches". */
+int64_t semipd_launch_count(semipd_pool_t pool);
+
+/* Optional CTA trace for co-run evidence: when buf (device int32, capacity
+ * `cap` records of 4 words) is non-NULL every attention CTA appends
+ * {phase (1 prefill, 2 decode), %smid, blockIdx.x, kernel kind (0 CUDA-core generic,
+ * 1 tcgen05 prefill, 2 split-K decode)}; *counter_dev (device int32)
+ * is the append cursor.  Pass buf = NULL to disable. */
+semipd_status semipd_set_trace(semipd_pool_t pool, int32_t* buf, int32_t cap,
+                               int32_t* counter_dev);
+
+/* Library version string (host, static). */
+const char* semipd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEMIPD_H */

@@ -1,0 +1,539 @@
+// decode.cu — split-K paged decode attention (PagedAttention P:229, GQA P:355,
+// flash-decoding split-K cited P:127) with the K/V append fused ("at each
+// decode iteration, the KV cache of the request is updated").
+//
+// Persistent grid capped to the decode SM budget (P:195 x/y partition), dynamic
+// work counter; a work unit is (request b, kv head g, split s).  Per CTA:
+//   warp 4 (producer, one lane): fetches units, appends k_new/v_new for the unit
+//     owning slot ctx, streams 32-key stages of K and V pages with TMA (128-B
+//     swizzle, one box = 64 columns x min(bs,32) rows of one (block, head) page)
+//     into a 12-deep shared-memory ring (192 KiB: Little's law for HBM latency on
+//     a minority of SMs);
+//   warps 0-3 (consumers): stage i of a unit goes to warp i % 4; QK^T and PV on
+//     mma.sync m16n8k16 (the G <= 16 query heads of one kv head fill M = 16, so
+//     each K/V byte is read once for all G heads), warp-shuffle online softmax in
+//     the log2 domain, then a cross-warp merge in shared memory and, for split
+//     units, a last-CTA-done merge over splits in split-index order.
+// The decomposition depends on shapes only, so results are bitwise identical for
+// every sm_budget and under co-run (S26).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+
+using namespace spd;
+
+constexpr int HD = 128;           // head dim (dk == dv)
+constexpr int KPS = 32;           // keys per stage
+constexpr int NSTAGE = 12;
+constexpr int NCW = 4;            // consumer warps
+constexpr int NTHREADS = (NCW + 1) * 32;
+constexpr int STAGE_BYTES = 2 * KPS * HD * 2;  // K + V
+constexpr int SPLIT_KEYS = 4096;  // maximum keys per split (shape-only decomposition)
+constexpr float LOG2E = 1.4426950408889634f;
+
+struct UnitDesc {
+    int b, g, s, S, k0, k1, base, nst;  // b < 0 : no more work
+};
+
+struct DecodeParams {
+    const __nv_bfloat16* q;      // [B][Hq][128]
+    const uint4* k_new;          // [B][Hkv][128] bf16
+    const uint4* v_new;
+    const int* req_ids;
+    const int* ctx_lens;
+    const int* bt;
+    unsigned char* k_pool;       // layer base
+    unsigned char* v_pool;
+    __nv_bfloat16* out;
+    float* ws_m;                 // [B][Hq][S_max]
+    float* ws_l;
+    float* ws_acc;               // [B][Hq][S_max][128]
+    int* ws_cnt;                 // [B][Hkv]
+    unsigned* sched;             // [2]: next unit, finished CTAs
+    int* status;
+    int B, Hq, Hkv, G, bs, MBR, N_B, S_max, n_units, out_head_major;
+    float scale_log2;
+    SpdTrace trace;
+};
+
+__device__ __forceinline__ void split_range(int ctx, int S, int s, int& k0, int& k1) {
+    const int nk = ctx + 1;
+    int len = (nk + S - 1) / S;
+    len = (len + KPS - 1) / KPS * KPS;
+    k0 = s * len;
+    k1 = min(nk, k0 + len);
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    decode_bf16_kernel(const __grid_constant__ CUtensorMap kmap,
+                       const __grid_constant__ CUtensorMap vmap, DecodeParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* ring = smem;                                   // NSTAGE x 16 KiB
+    float* scr_acc = reinterpret_cast<float*>(ring + NSTAGE * STAGE_BYTES);  // [NCW][16][128]
+    float* scr_ml = scr_acc + NCW * 16 * HD;                       // [NCW][16][2]
+    uint64_t* full = reinterpret_cast<uint64_t*>(scr_ml + NCW * 16 * 2);
+    uint64_t* empty = full + NSTAGE;
+    uint64_t* ufull = empty + NSTAGE;
+    uint64_t* uempty = ufull + 2;
+    UnitDesc* units = reinterpret_cast<UnitDesc*>(uempty + 2);
+    int* s_last = reinterpret_cast<int*>(units + 2);
+
+    const int warp = (int)warp_id();
+    const int lane = (int)lane_id();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(ufull + i, 1);
+            mbar_init(uempty + i, NCW);
+        }
+        fence_mbar_init();
+        if (p.trace.buf) {
+            int slot = atomicAdd(p.trace.ctr, 1);
+            if (slot < p.trace.cap)
+                reinterpret_cast<int4*>(p.trace.buf)[slot] =
+                    make_int4(2, (int)smid(), (int)blockIdx.x, 2 /* kernel kind: mma.sync decode */);
+        }
+    }
+    __syncthreads();
+
+    if (warp == NCW) {
+        // =========================== producer ===========================
+        if (lane == 0) {
+            tma_prefetch_desc(&kmap);
+            tma_prefetch_desc(&vmap);
+            const int box = p.bs < KPS ? p.bs : KPS;
+            const int oob_z = p.N_B * p.Hkv;  // first page index past the tensor -> zero fill
+            int gstage = 0, nunit = 0;
+            for (;;) {
+                const int u = (int)atomicAdd(p.sched, 1u);
+                UnitDesc d;
+                if (u >= p.n_units) {
+                    d.b = -1;
+                } else {
+                    // unit order: split-major, then request, then kv head
+                    d.s = u / (p.B * p.Hkv);
+                    d.b = (u / p.Hkv) % p.B;
+                    d.g = u % p.Hkv;
+                    const int ctx = __ldg(p.ctx_lens + d.b);
+                    d.S = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+                    if (d.s >= d.S) continue;
+                    split_range(ctx, d.S, d.s, d.k0, d.k1);
+                    d.nst = (d.k1 - d.k0 + KPS - 1) / KPS;
+                    d.base = gstage;
+                }
+                const int us = nunit & 1;
+                mbar_wait(uempty + us, ((nunit >> 1) & 1) ^ 1);
+                units[us] = d;
+                mbar_arrive(ufull + us);
+                ++nunit;
+                if (d.b < 0) break;
+                const int ctx = __ldg(p.ctx_lens + d.b);
+                const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
+                const int last_page = ctx / p.bs;
+                if (d.s == d.S - 1) {
+                    // fused append of this step's K/V at slot ctx (bit-exact)
+                    const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
+                    if (blk >= 0 && blk < p.N_B) {
+                        const size_t slot = ((size_t)blk * p.Hkv + d.g) * p.bs + (ctx % p.bs);
+                        uint4* kd = reinterpret_cast<uint4*>(p.k_pool) + slot * (HD / 8);
+                        uint4* vd = reinterpret_cast<uint4*>(p.v_pool) + slot * (HD / 8);
+                        const uint4* ks = p.k_new + ((size_t)d.b * p.Hkv + d.g) * (HD / 8);
+                        const uint4* vs = p.v_new + ((size_t)d.b * p.Hkv + d.g) * (HD / 8);
+#pragma unroll 4
+                        for (int c = 0; c < HD / 8; ++c) {
+                            kd[c] = __ldg(ks + c);
+                            vd[c] = __ldg(vs + c);
+                        }
+                        fence_proxy_async_global();
+                    }
+                }
+                for (int i = 0; i < d.nst; ++i, ++gstage) {
+                    const int st = gstage % NSTAGE;
+                    mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
+                    mbar_arrive_expect_tx(full + st, STAGE_BYTES);
+                    unsigned char* kst = ring + st * STAGE_BYTES;
+                    unsigned char* vst = kst + STAGE_BYTES / 2;
+                    for (int r = 0; r < KPS; r += box) {
+                        const int key = d.k0 + i * KPS + r;
+                        const int page = key / p.bs;
+                        int z = oob_z;
+                        if (page <= last_page) {
+                            const int blk = page < p.MBR ? __ldg(btr + page) : -1;
+                            if (blk >= 0 && blk < p.N_B) {
+                                z = blk * p.Hkv + d.g;
+                            } else if (p.status) {
+                                atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                            }
+                        }
+                        const int y = key % p.bs;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            tma_load_3d(kst + h * (KPS * 128) + r * 128, &kmap, full + st, h * 64, y, z);
+                            tma_load_3d(vst + h * (KPS * 128) + r * 128, &vmap, full + st, h * 64, y, z);
+                        }
+                    }
+                }
+            }
+        }
+    } else {
+        // =========================== consumers ===========================
+        const int r0 = lane >> 2;       // row (q head within group) of c0/c1
+        const int c0 = (lane & 3) * 2;  // column pair
+        int nunit = 0;
+        for (;;) {
+            const int us = nunit & 1;
+            mbar_wait(ufull + us, (nunit >> 1) & 1);
+            const UnitDesc d = units[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(uempty + us);
+            ++nunit;
+            if (d.b < 0) break;
+            // ---- Q fragments (rows >= G are zero)
+            uint32_t qa[8][4];
+            {
+                const uint32_t* q32 = reinterpret_cast<const uint32_t*>(p.q);
+                const size_t rowA = ((size_t)d.b * p.Hq + d.g * p.G + r0) * (HD / 2);
+                const size_t rowB = rowA + 8 * (HD / 2);
+                const bool va = r0 < p.G, vb = r0 + 8 < p.G;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int col = (kk * 16 + c0) >> 1;
+                    qa[kk][0] = va ? __ldg(q32 + rowA + col) : 0u;
+                    qa[kk][1] = vb ? __ldg(q32 + rowB + col) : 0u;
+                    qa[kk][2] = va ? __ldg(q32 + rowA + col + 4) : 0u;
+                    qa[kk][3] = vb ? __ldg(q32 + rowB + col + 4) : 0u;
+                }
+            }
+            float acc[16][4];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+            float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+
+            for (int i = warp; i < d.nst; i += NCW) {
+                const int gs = d.base + i;
+                const int st = gs % NSTAGE;
+                mbar_wait(full + st, (gs / NSTAGE) & 1);
+                const uint32_t kst = smem_u32(ring + st * STAGE_BYTES);
+                const uint32_t vst = kst + STAGE_BYTES / 2;
+                // ---- S = Q K^T : 4 n-tiles of 8 keys
+                float s[4][4];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+                    const int key = nt * 8 + (lane & 7);
+#pragma unroll
+                    for (int kk = 0; kk < 8; kk += 2) {
+                        const int ci = 2 * kk + (lane >> 3);
+                        const uint32_t addr = kst + (ci >> 3) * (KPS * 128) + key * 128 +
+                                              (((ci & 7) ^ (key & 7)) << 4);
+                        uint32_t b0, b1, b2, b3;
+                        ldsm_x4(addr, b0, b1, b2, b3);
+                        mma_bf16_16816(s[nt], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
+                        mma_bf16_16816(s[nt], qa[kk + 1][0], qa[kk + 1][1], qa[kk + 1][2],
+                                       qa[kk + 1][3], b2, b3);
+                    }
+                }
+                // ---- mask + online softmax (log2 domain); rows r0 (idx 0,1) and r0+8 (2,3)
+                const int kbase = d.k0 + i * KPS;
+                float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int key = kbase + nt * 8 + c0 + (e & 1);
+                        const float x = key < d.k1 ? s[nt][e] * p.scale_log2 : -INFINITY;
+                        s[nt][e] = x;
+                        mx[e >> 1] = fmaxf(mx[e >> 1], x);
+                    }
+                float alpha[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
+                    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
+                    const float mnew = fmaxf(mrow[h], mx[h]);
+                    alpha[h] = fast_exp2(mrow[h] - mnew);  // exp2(-inf) = 0 on first stage
+                    mrow[h] = mnew;
+                }
+                float ls[2] = {0.f, 0.f};
+                uint32_t pa[2][4];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    const float p0 = fast_exp2(s[nt][0] - mrow[0]);
+                    const float p1 = fast_exp2(s[nt][1] - mrow[0]);
+                    const float p2 = fast_exp2(s[nt][2] - mrow[1]);
+                    const float p3 = fast_exp2(s[nt][3] - mrow[1]);
+                    ls[0] += p0 + p1;
+                    ls[1] += p2 + p3;
+                    const int ks = nt >> 1, hi = nt & 1;
+                    pa[ks][hi * 2 + 0] = pack_bf16(p0, p1);
+                    pa[ks][hi * 2 + 1] = pack_bf16(p2, p3);
+                }
+                lrow[0] = lrow[0] * alpha[0] + ls[0];
+                lrow[1] = lrow[1] * alpha[1] + ls[1];
+                if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
+#pragma unroll
+                    for (int nd = 0; nd < 16; ++nd) {
+                        acc[nd][0] *= alpha[0];
+                        acc[nd][1] *= alpha[0];
+                        acc[nd][2] *= alpha[1];
+                        acc[nd][3] *= alpha[1];
+                    }
+                }
+                // ---- O += P V : 16 dv n-tiles x 2 k-steps of 16 keys
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int key = ks * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+                    for (int nd = 0; nd < 16; nd += 2) {
+                        const int ch = nd + (lane >> 4);
+                        const uint32_t addr = vst + (ch >> 3) * (KPS * 128) + key * 128 +
+                                              (((ch & 7) ^ (key & 7)) << 4);
+                        uint32_t b0, b1, b2, b3;
+                        ldsm_x4_t(addr, b0, b1, b2, b3);
+                        // A = P (rows r0 / r0+8; keys 16ks + {c0, c0+8})
+                        mma_bf16_16816(acc[nd], pa[ks][0], pa[ks][1], pa[ks][2], pa[ks][3], b0, b1);
+                        mma_bf16_16816(acc[nd + 1], pa[ks][0], pa[ks][1], pa[ks][2], pa[ks][3], b2, b3);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + st);
+            }
+            // ---- per-warp partial -> shared scratch
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 1);
+                lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 2);
+            }
+            float* wacc = scr_acc + warp * 16 * HD;
+#pragma unroll
+            for (int nd = 0; nd < 16; ++nd) {
+                const int col = nd * 8 + c0;
+                *reinterpret_cast<float2*>(wacc + r0 * HD + col) = make_float2(acc[nd][0], acc[nd][1]);
+                *reinterpret_cast<float2*>(wacc + (r0 + 8) * HD + col) =
+                    make_float2(acc[nd][2], acc[nd][3]);
+            }
+            if ((lane & 3) == 0) {
+                scr_ml[(warp * 16 + r0) * 2 + 0] = mrow[0];
+                scr_ml[(warp * 16 + r0) * 2 + 1] = lrow[0];
+                scr_ml[(warp * 16 + r0 + 8) * 2 + 0] = mrow[1];
+                scr_ml[(warp * 16 + r0 + 8) * 2 + 1] = lrow[1];
+            }
+            named_bar_sync(1, NCW * 32);
+            // ---- cross-warp merge: thread t handles (head h, 4 columns)
+            const int tid = threadIdx.x;  // 0..127
+            const bool split = d.S > 1;
+            for (int idx = tid; idx < p.G * (HD / 4); idx += NCW * 32) {
+                const int h = idx / (HD / 4), c = (idx % (HD / 4)) * 4;
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < NCW; ++w) M = fmaxf(M, scr_ml[(w * 16 + h) * 2]);
+                float L = 0.f;
+                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int w = 0; w < NCW; ++w) {
+                    const float mw = scr_ml[(w * 16 + h) * 2];
+                    const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
+                    L += f * scr_ml[(w * 16 + h) * 2 + 1];
+                    const float4 a = *reinterpret_cast<const float4*>(scr_acc + (w * 16 + h) * HD + c);
+                    o.x += f * a.x;
+                    o.y += f * a.y;
+                    o.z += f * a.z;
+                    o.w += f * a.w;
+                }
+                const int hq = d.g * p.G + h;
+                if (!split) {
+                    const float inv = 1.f / L;
+                    const size_t off = p.out_head_major ? (((size_t)hq * p.B + d.b) * HD + c)
+                                                        : (((size_t)d.b * p.Hq + hq) * HD + c);
+                    uint2 v;
+                    v.x = pack_bf16(o.x * inv, o.y * inv);
+                    v.y = pack_bf16(o.z * inv, o.w * inv);
+                    *reinterpret_cast<uint2*>(p.out + off) = v;
+                } else {
+                    const size_t pi = ((size_t)d.b * p.Hq + hq) * p.S_max + d.s;
+                    *reinterpret_cast<float4*>(p.ws_acc + pi * HD + c) = o;
+                    if (c == 0) {
+                        p.ws_m[pi] = M;
+                        p.ws_l[pi] = L;
+                    }
+                }
+            }
+            if (split) {
+                __threadfence();
+                named_bar_sync(1, NCW * 32);
+                if (tid == 0) {
+                    const int prev = atomicAdd(p.ws_cnt + d.b * p.Hkv + d.g, 1);
+                    *s_last = prev == d.S - 1;
+                }
+                named_bar_sync(1, NCW * 32);
+                if (*s_last) {
+                    __threadfence();
+                    // merge over splits in split-index order (flash-decoding)
+                    for (int idx = tid; idx < p.G * (HD / 4); idx += NCW * 32) {
+                        const int h = idx / (HD / 4), c = (idx % (HD / 4)) * 4;
+                        const int hq = d.g * p.G + h;
+                        const size_t pb = ((size_t)d.b * p.Hq + hq) * p.S_max;
+                        float M = -INFINITY;
+                        for (int sI = 0; sI < d.S; ++sI) M = fmaxf(M, __ldcg(p.ws_m + pb + sI));
+                        float L = 0.f;
+                        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int sI = 0; sI < d.S; ++sI) {
+                            const float f = fast_exp2(__ldcg(p.ws_m + pb + sI) - M);
+                            L += f * __ldcg(p.ws_l + pb + sI);
+                            const float4 a = __ldcg(reinterpret_cast<const float4*>(p.ws_acc + (pb + sI) * HD + c));
+                            o.x += f * a.x;
+                            o.y += f * a.y;
+                            o.z += f * a.z;
+                            o.w += f * a.w;
+                        }
+                        const float inv = 1.f / L;
+                        const size_t off = p.out_head_major ? (((size_t)hq * p.B + d.b) * HD + c)
+                                                            : (((size_t)d.b * p.Hq + hq) * HD + c);
+                        uint2 v;
+                        v.x = pack_bf16(o.x * inv, o.y * inv);
+                        v.y = pack_bf16(o.z * inv, o.w * inv);
+                        *reinterpret_cast<uint2*>(p.out + off) = v;
+                    }
+                    if (tid == 0) p.ws_cnt[d.b * p.Hkv + d.g] = 0;  // ready for the next call
+                }
+            }
+            named_bar_sync(1, NCW * 32);  // scratch reuse
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(p.sched + 1, 1u);
+        if (done == gridDim.x - 1) {  // last CTA: reset the work counter for the next launch
+            p.sched[0] = 0u;
+            p.sched[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+size_t decode_smem_bytes() {
+    return 1024 + NSTAGE * STAGE_BYTES + NCW * 16 * HD * 4 + NCW * 16 * 2 * 4 +
+           (2 * NSTAGE + 4) * 8 + 2 * sizeof(UnitDesc) + 16;
+}
+
+inline size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+struct WsLayout {
+    size_t cnt, sched, m, l, acc, total;
+};
+WsLayout ws_layout(int B, int Hq, int Hkv, int S_max, int dv) {
+    WsLayout w;
+    w.cnt = 0;
+    w.sched = al256((size_t)B * Hkv * 4);
+    w.m = w.sched + 256;
+    w.l = al256(w.m + (size_t)B * Hq * S_max * 4);
+    w.acc = al256(w.l + (size_t)B * Hq * S_max * 4);
+    w.total = al256(w.acc + (size_t)B * Hq * S_max * dv * 4);
+    return w;
+}
+
+bool fast_path_ok(const semipd_pool* p, int Hq) {
+    const auto& c = p->cfg;
+    const int bs = c.block_size;
+    return c.dtype == SEMIPD_BF16 && !c.kv_shared && c.head_dim_k == HD && c.head_dim_v == HD &&
+           p->have_maps && Hq % c.num_kv_heads == 0 && Hq / c.num_kv_heads <= 16 &&
+           (bs == 16 || bs == 32 || bs == 64 || bs == 128);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t semipd_decode_workspace_bytes(semipd_pool_t pool, int32_t max_batch, int32_t num_q_heads,
+                                     int32_t max_ctx) {
+    if (!pool || max_batch < 0 || num_q_heads <= 0 || max_ctx < 0) return 0;
+    const int S_max = (max_ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+    return ws_layout(max_batch, num_q_heads, pool->cfg.num_kv_heads, S_max,
+                     pool->cfg.head_dim_v).total;
+}
+
+semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* q,
+                                 const void* k_new, const void* v_new, const int32_t* req_ids,
+                                 const int32_t* ctx_lens, int32_t batch, int32_t max_ctx_len,
+                                 int32_t num_q_heads, float softmax_scale, void* out,
+                                 int32_t out_head_major, void* workspace, size_t ws_bytes,
+                                 int32_t sm_budget, int32_t* status_dev, semipd_stream_t s) {
+    if (!pool || layer < 0 || layer >= pool->cfg.num_layers || batch < 0 || max_ctx_len < 0)
+        return SEMIPD_ERR_INVALID;
+    const auto& c = pool->cfg;
+    if (num_q_heads <= 0 || num_q_heads % c.num_kv_heads) return SEMIPD_ERR_INVALID;
+    if (sm_budget < -1 || sm_budget > pool->num_sms) return SEMIPD_ERR_INVALID;
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    if (status_dev && cudaMemsetAsync(status_dev, 0, sizeof(int), st) != cudaSuccess)
+        return SEMIPD_ERR_CUDA;
+    if (batch == 0) return SEMIPD_OK;
+    if (!q || !k_new || (!v_new && !c.kv_shared) || !req_ids || !ctx_lens || !out)
+        return SEMIPD_ERR_INVALID;
+    const int budget = spd_resolve_budget(pool, sm_budget, false);
+    if (!fast_path_ok(pool, num_q_heads)) {
+        // generic CUDA-core path: append, then attention (same stream)
+        semipd_status r = spd_launch_kv_write(pool, layer, k_new, v_new, nullptr, req_ids,
+                                              ctx_lens, batch, batch, 1, status_dev, st);
+        if (r != SEMIPD_OK) return r;
+        return spd_launch_simt_attn(pool, layer, q, nullptr, req_ids, ctx_lens, batch, batch, 1,
+                                    num_q_heads, softmax_scale, out, out_head_major, budget,
+                                    status_dev, st);
+    }
+    const int S_max = (max_ctx_len + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+    const WsLayout w = ws_layout(batch, num_q_heads, c.num_kv_heads, S_max, HD);
+    if (!workspace || ws_bytes < w.total) return SEMIPD_ERR_INVALID;
+    unsigned char* ws = static_cast<unsigned char*>(workspace);
+    DecodeParams prm;
+    prm.q = static_cast<const __nv_bfloat16*>(q);
+    prm.k_new = static_cast<const uint4*>(k_new);
+    prm.v_new = static_cast<const uint4*>(v_new);
+    prm.req_ids = req_ids;
+    prm.ctx_lens = ctx_lens;
+    prm.bt = pool->bt;
+    prm.k_pool = static_cast<unsigned char*>(pool->k_layer(layer));
+    prm.v_pool = static_cast<unsigned char*>(pool->v_layer(layer));
+    prm.out = static_cast<__nv_bfloat16*>(out);
+    prm.ws_cnt = reinterpret_cast<int*>(ws + w.cnt);
+    prm.sched = reinterpret_cast<unsigned*>(ws + w.sched);
+    prm.ws_m = reinterpret_cast<float*>(ws + w.m);
+    prm.ws_l = reinterpret_cast<float*>(ws + w.l);
+    prm.ws_acc = reinterpret_cast<float*>(ws + w.acc);
+    prm.status = status_dev;
+    prm.B = batch;
+    prm.Hq = num_q_heads;
+    prm.Hkv = c.num_kv_heads;
+    prm.G = num_q_heads / c.num_kv_heads;
+    prm.bs = c.block_size;
+    prm.MBR = c.max_blocks_per_req;
+    prm.N_B = c.num_blocks;
+    prm.S_max = S_max;
+    prm.n_units = batch * c.num_kv_heads * S_max;
+    prm.out_head_major = out_head_major;
+    prm.scale_log2 = softmax_scale * LOG2E;
+    prm.trace = spd_trace(pool);
+    const size_t smem = decode_smem_bytes();
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(decode_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return SEMIPD_ERR_CUDA;
+        attr_set = true;
+    }
+    int grid = budget > 0 ? budget : prm.n_units;
+    if (grid > prm.n_units) grid = prm.n_units;
+    decode_bf16_kernel<<<grid, NTHREADS, smem, st>>>(pool->kmap[layer], pool->vmap[layer], prm);
+    pool->launches += 1;
+    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+}
+
+}  // extern "C"

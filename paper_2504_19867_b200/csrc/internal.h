@@ -1,0 +1,82 @@
+// internal.h — host-side pool handle shared by the library's translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <vector>
+
+#include "semipd.h"
+
+// Device-resident allocator / scheduler state (first region of the pool).
+struct SpdDevState {
+    unsigned int lock;             // allocator lock word (0 free, 1 held)
+    int top;                       // free-stack height == free blocks
+    int min_free;                  // high-water of utilisation (min free seen)
+    int pad0;
+    unsigned long long op_seq;     // linearisation sequence number of the next op
+    long long oplog_len;           // int32 words used in the op log
+    long long oplog_dropped;       // ops not logged (log full)
+    unsigned int sched[16];        // persistent-grid work counters (prefill uses [0..1])
+};
+
+struct semipd_pool {
+    semipd_pool_config cfg;
+    int num_sms = 0;
+    unsigned char* base = nullptr;
+    SpdDevState* st = nullptr;
+    int* free_stack = nullptr;
+    int* nblk = nullptr;
+    int* bt = nullptr;
+    int* oplog = nullptr;
+    unsigned char* kv = nullptr;
+    size_t k_layer_bytes = 0, v_layer_bytes = 0, layer_stride = 0;
+    size_t esize = 2;
+    std::atomic<int> n_prefill{1}, n_decode{1};
+    std::atomic<long long> epoch{0};
+    std::atomic<long long> launches{0};
+    // TMA descriptors of every layer's K and V pool ([N_B*Hkv] pages of
+    // [bs][d]; box = 64 columns x min(bs, 32) rows, 128-byte swizzle).
+    std::vector<CUtensorMap> kmap, vmap;
+    bool have_maps = false;
+    int box_rows = 16;
+    int* trace_buf = nullptr;
+    int trace_cap = 0;
+    int* trace_ctr = nullptr;
+
+    void* k_layer(int l) const { return kv + (size_t)l * layer_stride; }
+    void* v_layer(int l) const {
+        return cfg.kv_shared ? k_layer(l) : (void*)(kv + (size_t)l * layer_stride + k_layer_bytes);
+    }
+};
+
+// Trace sink passed by value to kernels.
+struct SpdTrace {
+    int* buf;
+    int cap;
+    int* ctr;
+};
+
+inline SpdTrace spd_trace(const semipd_pool* p) { return SpdTrace{p->trace_buf, p->trace_cap, p->trace_ctr}; }
+
+// budget resolution (host): >0 cap, 0 partition, -1 non-persistent
+inline int spd_resolve_budget(const semipd_pool* p, int requested, bool prefill) {
+    if (requested > 0) return requested < p->num_sms ? requested : p->num_sms;
+    if (requested == 0) return prefill ? p->n_prefill.load() : p->n_decode.load();
+    return -1;
+}
+
+// TMA encode through the driver entry point (no -lcuda link dependency)
+bool spd_encode_tiled_3d(CUtensorMap* map, CUtensorMapDataType dt, void* gaddr, uint64_t d0,
+                         uint64_t d1, uint64_t d2, uint64_t s1_bytes, uint64_t s2_bytes,
+                         uint32_t b0, uint32_t b1, uint32_t b2, CUtensorMapSwizzle swz);
+
+// kernels launched from other TUs
+semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new, const void* v_new,
+                                  const int* cu_seqlens, const int* req_ids, const int* pos0,
+                                  int n, int total_rows, int mode, int* status_dev,
+                                  cudaStream_t s);
+semipd_status spd_launch_simt_attn(semipd_pool_t p, int layer, const void* q, const int* cu_seqlens,
+                                   const int* req_ids, const int* pos0, int n, int total_rows,
+                                   int mode, int Hq, float scale, void* out, int out_head_major,
+                                   int budget, int* status_dev, cudaStream_t s);

@@ -1,0 +1,461 @@
+// prefill_sm100.cu — chunked causal GQA prefill attention on 5th-gen tensor cores
+// (tcgen05.mma, accumulators in TMEM, operands staged by TMA), over the paged KV
+// pool (P:184 prefill writes K/V; P:229 paged access; P:355 GQA kernels for both
+// phases; P:365 chunked prefill).
+//
+// Work unit: (request i, q tile of 128 rows, kv head g).  GQA packing: the G q
+// heads of kv head g x (128 / G) tokens fill the M = 128 rows of one tile (row
+// r = token (r / G), head g*G + r % G), so every K/V tile is staged once for all
+// G heads.  Units run longest-first (LPT: last q tiles first) from a dynamic work
+// counter over a persistent grid capped to the prefill SM budget.
+//
+// Warp roles (256 threads, 1 CTA / SM):
+//   warp 0      TMA producer: Q tile (2 x 64-col boxes), K/V tiles of 128 keys as
+//               (128 / box_rows) page boxes per 64-col half, 2-stage K and V rings.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
+//               S[j%2] = Q K_j^T  (SS, M=N=128, K=16 x 8);  O += P_j V_j  (TS: P in
+//               TMEM, V MN-major from smem).  Order S_0, S_1, PV_0, S_2, PV_1, ...
+//   warps 4-7   softmax warpgroup, one thread per row: tcgen05.ld S, causal mask,
+//               online softmax in the log2 domain with lazy (threshold 2^8) O
+//               rescale, P (bf16) written back over S with tcgen05.st, epilogue
+//               O / l -> bf16 -> global.
+// TMEM columns: S0 [0,128), S1 [128,256), O [256,384).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+
+using namespace spd;
+
+constexpr int HD = 128;
+constexpr int BM = 128;   // rows per tile
+constexpr int BN = 128;   // keys per kv tile
+constexpr int NT = 256;
+constexpr uint32_t TILE_BYTES = BM * HD * 2;    // 32 KiB
+constexpr uint32_t HALF_BYTES = TILE_BYTES / 2; // 16 KiB (64 columns)
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 domain: rescale when max grows by > 2^8
+
+struct PUnit {
+    int i, g, t0, tvalid, pos0, nkv, qrow0, btrow;  // i < 0: no more work
+};
+
+struct PrefillParams {
+    const int* cu;          // [n+1]
+    const int* req_ids;     // [n]
+    const int* prefix;      // [n]
+    const int* bt;
+    __nv_bfloat16* out;
+    int* status;
+    unsigned* sched;
+    int n, T, Hq, Hkv, G, TQ, tiles_max, n_units, bs, box_rows, MBR, N_B, out_head_major;
+    float scale_log2;
+    SpdTrace trace;
+};
+
+struct Smem {
+    // operand tiles first (1024-aligned by construction)
+    unsigned char q[TILE_BYTES];
+    unsigned char k[2][TILE_BYTES];
+    unsigned char v[2][TILE_BYTES];
+    uint64_t q_full, q_empty;
+    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+    uint64_t s_full[2], p_full[2];
+    uint64_t o_full, o_empty;
+    uint64_t ufull[2], uempty[2];
+    PUnit units[2];
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t addr) {
+    return umma_desc_sw128(addr, 16, 1024);
+}
+
+__global__ void __launch_bounds__(NT, 1)
+    prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap,
+                      const __grid_constant__ CUtensorMap kmap,
+                      const __grid_constant__ CUtensorMap vmap, PrefillParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                        ~uintptr_t(1023));
+    const int warp = (int)warp_id();
+    const int lane = (int)lane_id();
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.q_full, 1);
+        mbar_init(&sm.q_empty, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.k_full[s], 1);
+            mbar_init(&sm.k_empty[s], 1);
+            mbar_init(&sm.v_full[s], 1);
+            mbar_init(&sm.v_empty[s], 1);
+            mbar_init(&sm.s_full[s], 1);
+            mbar_init(&sm.p_full[s], 128);
+            mbar_init(&sm.ufull[s], 1);
+            mbar_init(&sm.uempty[s], 1 + 4);
+        }
+        mbar_init(&sm.o_full, 1);
+        mbar_init(&sm.o_empty, 128);
+        fence_mbar_init();
+        if (p.trace.buf) {
+            int slot = atomicAdd(p.trace.ctr, 1);
+            if (slot < p.trace.cap)
+                reinterpret_cast<int4*>(p.trace.buf)[slot] =
+                    make_int4(1, (int)smid(), (int)blockIdx.x, 1 /* kernel kind: tcgen05 prefill */);
+        }
+    }
+    if (warp == 1) tmem_alloc(&sm.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp == 0) {
+        // ================================ TMA producer ================================
+        if (lane == 0) {
+            tma_prefetch_desc(&qmap);
+            tma_prefetch_desc(&kmap);
+            tma_prefetch_desc(&vmap);
+            const int oob_z = p.N_B * p.Hkv;
+            int kvit = 0, nunit = 0;
+            for (;;) {
+                const int u = (int)atomicAdd(p.sched, 1u);
+                PUnit d;
+                d.i = -1;
+                if (u < p.n_units) {
+                    const int per_tile = p.n * p.Hkv;
+                    const int tile = p.tiles_max - 1 - u / per_tile;  // LPT: last tiles first
+                    d.i = (u / p.Hkv) % p.n;
+                    d.g = u % p.Hkv;
+                    const int c0 = __ldg(p.cu + d.i), c1 = __ldg(p.cu + d.i + 1);
+                    d.t0 = tile * p.TQ;
+                    if (d.t0 >= c1 - c0) continue;  // tile past this request's chunk
+                    d.tvalid = min(p.TQ, c1 - c0 - d.t0);
+                    const int P = __ldg(p.prefix + d.i);
+                    d.pos0 = P + d.t0;
+                    d.nkv = (d.pos0 + d.tvalid - 1) / BN + 1;
+                    d.qrow0 = c0 + d.t0;
+                    d.btrow = __ldg(p.req_ids + d.i);
+                }
+                const int us = nunit & 1;
+                mbar_wait(&sm.uempty[us], ((nunit >> 1) & 1) ^ 1);
+                sm.units[us] = d;
+                mbar_arrive(&sm.ufull[us]);
+                if (d.i < 0) break;
+                // Q tile (rows = tokens x G heads of kv head g)
+                mbar_wait(&sm.q_empty, (nunit & 1) ^ 1);
+                mbar_arrive_expect_tx(&sm.q_full, TILE_BYTES);
+                tma_load_3d(sm.q, &qmap, &sm.q_full, 0, d.g * p.G, d.qrow0);
+                tma_load_3d(sm.q + HALF_BYTES, &qmap, &sm.q_full, 64, d.g * p.G, d.qrow0);
+                ++nunit;
+                const int* btr = p.bt + (size_t)d.btrow * p.MBR;
+                const int nkeys = d.pos0 + d.tvalid;  // keys [0, P + t0 + tvalid)
+                const int last_page = (nkeys - 1) / p.bs;
+                for (int j = 0; j < d.nkv; ++j, ++kvit) {
+                    const int st = kvit & 1;
+                    const uint32_t ph = ((kvit >> 1) & 1) ^ 1;
+                    for (int kv = 0; kv < 2; ++kv) {
+                        uint64_t* emp = kv ? &sm.v_empty[st] : &sm.k_empty[st];
+                        uint64_t* ful = kv ? &sm.v_full[st] : &sm.k_full[st];
+                        unsigned char* dst = kv ? sm.v[st] : sm.k[st];
+                        const CUtensorMap* map = kv ? &vmap : &kmap;
+                        mbar_wait(emp, ph);
+                        mbar_arrive_expect_tx(ful, TILE_BYTES);
+                        for (int r = 0; r < BN; r += p.box_rows) {
+                            const int key = j * BN + r;
+                            const int page = key / p.bs;
+                            int z = oob_z;
+                            if (page <= last_page) {
+                                const int blk = page < p.MBR ? __ldg(btr + page) : -1;
+                                if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
+                                else if (p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                            }
+                            const int y = key % p.bs;
+                            tma_load_3d(dst + r * 128, map, ful, 0, y, z);
+                            tma_load_3d(dst + HALF_BYTES + r * 128, map, ful, 64, y, z);
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================================ MMA issuer ================================
+        if (lane == 0) {
+            const uint32_t idesc_s = umma_idesc_bf16_f32(BM, BN, 0);
+            const uint32_t idesc_o = umma_idesc_bf16_f32(BM, HD, 1);
+            const uint32_t q_addr = smem_u32(sm.q);
+            int kvit = 0, nunit = 0;
+            for (;;) {
+                const int us = nunit & 1;
+                mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
+                const PUnit d = sm.units[us];
+                mbar_arrive(&sm.uempty[us]);
+                if (d.i < 0) break;
+                mbar_wait(&sm.q_full, nunit & 1);
+                tc_fence_after();
+                auto issue_s = [&](int it) {
+                    const int st = it & 1;
+                    mbar_wait(&sm.k_full[st], (it >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t k_addr = smem_u32(sm.k[st]);
+                    const uint32_t d_tmem = tmem + (uint32_t)(st * BN);
+#pragma unroll
+                    for (int kk = 0; kk < HD / 16; ++kk) {
+                        const uint32_t off = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
+                        umma_ss(d_tmem, kmajor_desc(q_addr + off), kmajor_desc(k_addr + off),
+                                idesc_s, kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&sm.s_full[st]);
+                    umma_commit(&sm.k_empty[st]);
+                };
+                auto issue_pv = [&](int it, bool first) {
+                    const int st = it & 1;
+                    mbar_wait(&sm.p_full[st], (it >> 1) & 1);
+                    if (first) mbar_wait(&sm.o_empty, (nunit & 1) ^ 1);
+                    mbar_wait(&sm.v_full[st], (it >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t v_addr = smem_u32(sm.v[st]);
+                    const uint32_t p_tmem = tmem + (uint32_t)(st * BN);
+                    const uint32_t o_tmem = tmem + 256u;
+#pragma unroll
+                    for (int kk = 0; kk < BN / 16; ++kk) {
+                        const uint64_t bdesc = umma_desc_sw128(v_addr + kk * 2048, HALF_BYTES, 1024);
+                        umma_ts(o_tmem, p_tmem + (uint32_t)(kk * 8), bdesc, idesc_o,
+                                (first && kk == 0) ? 0u : 1u);
+                    }
+                    umma_commit(&sm.v_empty[st]);
+                    umma_commit(&sm.o_full);
+                };
+                const int it0 = kvit;
+                for (int j = 0; j < d.nkv; ++j) {
+                    issue_s(it0 + j);
+                    if (j == d.nkv - 1) umma_commit(&sm.q_empty);
+                    if (j > 0) issue_pv(it0 + j - 1, j - 1 == 0);
+                }
+                issue_pv(it0 + d.nkv - 1, d.nkv == 1);
+                kvit = it0 + d.nkv;
+                ++nunit;
+            }
+        }
+    } else if (warp >= 4) {
+        // ============================ softmax warpgroup ============================
+        const int q4 = warp - 4;              // TMEM lane quarter
+        const int r = q4 * 32 + lane;         // tile row
+        const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+        int kvit = 0, nunit = 0;
+        for (;;) {
+            const int us = nunit & 1;
+            mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
+            const PUnit d = sm.units[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.uempty[us]);
+            if (d.i < 0) break;
+            const int tok = r / p.G;
+            const int pos = d.pos0 + tok;  // absolute position of this row's token
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < d.nkv; ++j, ++kvit) {
+                const int sb = kvit & 1;
+                mbar_wait(&sm.s_full[sb], (kvit >> 1) & 1);
+                tc_fence_after();
+                const uint32_t s_tmem = tmem + lane_base + (uint32_t)(sb * BN);
+                uint32_t sr[4][32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32(s_tmem + c * 32, sr[c]);
+                tmem_wait_ld();
+                float mx = -INFINITY;
+                const int kbase = j * BN;
+                const bool need_mask = kbase + BN - 1 > pos;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        float x = __uint_as_float(sr[c][e]) * p.scale_log2;
+                        if (need_mask && kbase + c * 32 + e > pos) x = -INFINITY;
+                        sr[c][e] = __float_as_uint(x);
+                        mx = fmaxf(mx, x);
+                    }
+                // lazy rescale: keep a stale max unless the new one exceeds it by > 2^8
+                const bool grow = mx > m + RESCALE_THRESHOLD;
+                if (j == 0) {
+                    m = mx;
+                } else if (__any_sync(0xffffffffu, grow)) {
+                    const float mnew = grow ? mx : m;
+                    const float alpha = fast_exp2(m - mnew);
+                    mbar_wait(&sm.o_full, (kvit - 1) & 1);  // PV_{j-1} done
+                    tc_fence_after();
+                    const uint32_t o_tmem = tmem + lane_base + 256u;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(o_tmem + c * 32, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                        tmem_st32(o_tmem + c * 32, o);
+                    }
+                    l *= alpha;
+                    m = mnew;
+                }
+                // P = exp2(x - m) in bf16, written over the S columns [0, 64)
+                float ls = 0.f;
+#pragma unroll
+                for (int c = 0; c < 4; c += 2) {
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        const float a0 = fast_exp2(__uint_as_float(sr[c][e]) - m);
+                        const float a1 = fast_exp2(__uint_as_float(sr[c][e + 1]) - m);
+                        const float b0 = fast_exp2(__uint_as_float(sr[c + 1][e]) - m);
+                        const float b1 = fast_exp2(__uint_as_float(sr[c + 1][e + 1]) - m);
+                        ls += (a0 + a1) + (b0 + b1);
+                        pk[e / 2] = pack_bf16(a0, a1);
+                        pk[16 + e / 2] = pack_bf16(b0, b1);
+                    }
+                    tmem_st32(s_tmem + (uint32_t)(c * 16), pk);
+                }
+                l += ls;
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&sm.p_full[sb]);
+            }
+            // ---- epilogue: O / l -> bf16 -> global
+            mbar_wait(&sm.o_full, (kvit - 1) & 1);
+            tc_fence_after();
+            const bool valid = tok < d.tvalid;
+            const int hq = d.g * p.G + (r % p.G);
+            const int trow = d.qrow0 + tok;
+            __nv_bfloat16* dst = p.out + (p.out_head_major
+                                              ? ((size_t)hq * p.T + trow) * HD
+                                              : ((size_t)trow * p.Hq + hq) * HD);
+            const float inv = 1.f / l;
+            const uint32_t o_tmem = tmem + lane_base + 256u;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t o[32];
+                tmem_ld32(o_tmem + c * 32, o);
+                tmem_wait_ld();
+                if (valid) {
+#pragma unroll
+                    for (int e = 0; e < 32; e += 8) {
+                        uint4 v;
+                        v.x = pack_bf16(__uint_as_float(o[e + 0]) * inv, __uint_as_float(o[e + 1]) * inv);
+                        v.y = pack_bf16(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+                        v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+                        v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+                        *reinterpret_cast<uint4*>(dst + c * 32 + e) = v;
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&sm.o_empty);
+            ++nunit;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(p.sched + 1, 1u);
+        if (done == gridDim.x - 1) {
+            p.sched[0] = 0u;
+            p.sched[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+bool fast_path_ok(const semipd_pool* pl, int Hq) {
+    const auto& c = pl->cfg;
+    if (c.dtype != SEMIPD_BF16 || c.kv_shared || c.head_dim_k != HD || c.head_dim_v != HD ||
+        !pl->have_maps || Hq % c.num_kv_heads)
+        return false;
+    const int G = Hq / c.num_kv_heads;
+    const int bs = c.block_size;
+    return G >= 1 && G <= 16 && BM % G == 0 &&
+           (bs == 16 || bs == 32 || bs == 64 || bs == 128);
+}
+
+}  // namespace
+
+extern "C" semipd_status semipd_prefill_attn(
+    semipd_pool_t pool, int32_t layer, const void* q, const void* k_new, const void* v_new,
+    const int32_t* cu_seqlens_q, const int32_t* req_ids, const int32_t* prefix_lens, int32_t n,
+    int32_t total_q, int32_t max_chunk_len, int32_t num_q_heads, float softmax_scale, void* out,
+    int32_t out_head_major, int32_t sm_budget, int32_t* status_dev, semipd_stream_t s) {
+    if (!pool || layer < 0 || layer >= pool->cfg.num_layers || n < 0 || total_q < 0 ||
+        max_chunk_len < 0)
+        return SEMIPD_ERR_INVALID;
+    const auto& c = pool->cfg;
+    if (num_q_heads <= 0 || num_q_heads % c.num_kv_heads) return SEMIPD_ERR_INVALID;
+    if (sm_budget < -1 || sm_budget > pool->num_sms) return SEMIPD_ERR_INVALID;
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    if (status_dev && cudaMemsetAsync(status_dev, 0, sizeof(int), st) != cudaSuccess)
+        return SEMIPD_ERR_CUDA;
+    if (n == 0 || total_q == 0) return SEMIPD_OK;
+    if (!q || !k_new || (!v_new && !c.kv_shared) || !cu_seqlens_q || !req_ids || !prefix_lens ||
+        !out)
+        return SEMIPD_ERR_INVALID;
+    // 1. K/V write into the pool, stream-ordered before attention reads it
+    semipd_status r = spd_launch_kv_write(pool, layer, k_new, v_new, cu_seqlens_q, req_ids,
+                                          prefix_lens, n, total_q, 0, status_dev, st);
+    if (r != SEMIPD_OK) return r;
+    const int budget = spd_resolve_budget(pool, sm_budget, true);
+    if (!fast_path_ok(pool, num_q_heads))
+        return spd_launch_simt_attn(pool, layer, q, cu_seqlens_q, req_ids, prefix_lens, n, total_q,
+                                    0, num_q_heads, softmax_scale, out, out_head_major, budget,
+                                    status_dev, st);
+    // 2. tensor-core attention
+    const int G = num_q_heads / c.num_kv_heads;
+    const int TQ = BM / G;
+    PrefillParams prm;
+    prm.cu = cu_seqlens_q;
+    prm.req_ids = req_ids;
+    prm.prefix = prefix_lens;
+    prm.bt = pool->bt;
+    prm.out = static_cast<__nv_bfloat16*>(out);
+    prm.status = status_dev;
+    prm.sched = &pool->st->sched[0];
+    prm.n = n;
+    prm.T = total_q;
+    prm.Hq = num_q_heads;
+    prm.Hkv = c.num_kv_heads;
+    prm.G = G;
+    prm.TQ = TQ;
+    prm.tiles_max = (max_chunk_len + TQ - 1) / TQ;
+    if (prm.tiles_max < 1) return SEMIPD_OK;
+    const long long units = (long long)n * prm.tiles_max * c.num_kv_heads;
+    if (units > (1LL << 30)) return SEMIPD_ERR_UNSUPPORTED;
+    prm.n_units = (int)units;
+    prm.bs = c.block_size;
+    prm.box_rows = pool->box_rows;
+    prm.MBR = c.max_blocks_per_req;
+    prm.N_B = c.num_blocks;
+    prm.out_head_major = out_head_major;
+    prm.scale_log2 = softmax_scale * LOG2E;
+    prm.trace = spd_trace(pool);
+    CUtensorMap qmap;
+    if (!spd_encode_tiled_3d(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(q), HD,
+                             (uint64_t)num_q_heads, (uint64_t)total_q, HD * 2,
+                             (uint64_t)num_q_heads * HD * 2, 64, (uint32_t)G, (uint32_t)TQ,
+                             CU_TENSOR_MAP_SWIZZLE_128B))
+        return SEMIPD_ERR_CUDA;
+    const size_t smem = sizeof(Smem) + 1024;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return SEMIPD_ERR_CUDA;
+        attr_set = true;
+    }
+    int grid = budget > 0 ? budget : prm.n_units;
+    if (grid > prm.n_units) grid = prm.n_units;
+    prefill_tc_kernel<<<grid, NT, smem, st>>>(qmap, pool->kmap[layer], pool->vmap[layer], prm);
+    pool->launches += 1;
+    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+}

@@ -1,0 +1,54 @@
+"""CPU checks of the C ABI boundary: the library builds, loads, and exports every
+symbol include/semipd.h declares (no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+
+import paper_2504_19867_b200 as spd
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "semipd.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(semipd_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = spd.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(L, s), f"missing export {s}"
+    assert b"sm_100a" in L.semipd_version()
+
+
+def test_host_only_calls():
+    L = spd.lib()
+    assert L.semipd_blocks_for_tokens(251, 16) == 16
+    assert L.semipd_blocks_for_tokens(256, 16) == 16
+    assert L.semipd_blocks_for_tokens(0, 16) == 0
+    assert L.semipd_blocks_for_tokens(-1, 16) == -1
+    cfg = spd.PoolConfig(2, 100, 16, 8, 128, 128, 4, 8).c(0)
+    nb = L.semipd_kv_pool_bytes(ctypes.byref(cfg))
+    kv = 2 * 100 * 8 * 16 * 128 * 2 * 2
+    assert kv < nb < kv + 2 * 1024 * 1024
+    bad = spd.PoolConfig(2, 100, 16, 8, 128, 128, 0, 8).c(0)
+    assert L.semipd_kv_pool_bytes(ctypes.byref(bad)) == 0
+    # NULL handle / arguments are rejected without touching a device
+    assert L.semipd_set_partition(None, 50.0, 50.0) == spd.INVALID
+    assert L.semipd_alloc_blocks(None, None, None, 1, None, None) == spd.INVALID
+    assert L.semipd_kv_pool_create(ctypes.byref(cfg), None, 0, None, None) == spd.INVALID
+
+
+def test_sass_is_blackwell_native():
+    """The built library holds tcgen05 (UTCHMMA), TMEM (LDTM/STTM) and TMA (UTMALDG)."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        return
+    sass = subprocess.run([tool, "-sass", spd.lib()._name], capture_output=True, text=True).stdout
+    for mnem in ("UTCHMMA", "LDTM", "STTM", "UTMALDG"):
+        assert mnem in sass, mnem

@@ -51,7 +51,7 @@ DECODE_CTX = 2048
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="semipd", choices=["semipd", "reference"])
     ap.add_argument("--model", default="llama3-8b", choices=list(MODELS))

@@ -69,6 +69,16 @@ __device__ int block_exclusive_scan(int v, int* scratch, int* total) {
     return warp_off + x - v;
 }
 
+// item owning flattened index idx: last i with prefix[i] <= idx (prefix is non-decreasing)
+__device__ __forceinline__ int owner(const int* prefix, int n, int idx) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= idx) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
 __device__ void log_op(const AllocArgs& a, int kind, int n, int status, const int* ids,
                        const int* counts, unsigned long long seq) {
     // all threads participate; thread 0 owns the header
@@ -153,12 +163,12 @@ __global__ void __launch_bounds__(kThreads) alloc_kernel(AllocArgs a, const int*
     }
     // ---- get + update
     if (status == SEMIPD_OK) {
-        for (int i = tid; i < n; i += kThreads) {
+        // the idx-th popped block (argument order) goes to item i = owner(idx)
+        for (int idx = tid; idx < total; idx += kThreads) {
+            const int i = owner(s_prefix, n, idx);
             const int id = __ldg(ids + i);
-            const int cnt = __ldg(counts + i);
-            int* row = a.bt + (size_t)id * a.MBR;
-            for (int c = 0; c < cnt; ++c)
-                row[s_base[i] + c] = __ldcg(a.free_stack + (top - 1 - (s_prefix[i] + c)));
+            a.bt[(size_t)id * a.MBR + s_base[i] + (idx - s_prefix[i])] =
+                __ldcg(a.free_stack + (top - 1 - idx));
         }
         __syncthreads();
         for (int i = tid; i < n; i += kThreads) {
@@ -231,14 +241,13 @@ __global__ void __launch_bounds__(kThreads) free_kernel(AllocArgs a, const int* 
             total += chunk_total;
         }
         __syncthreads();
-        for (int i = tid; i < n; i += kThreads) {
-            const int id = __ldg(ids + i);
-            int* row = a.bt + (size_t)id * a.MBR;
-            const int cnt = __ldcg(a.nblk + id);
-            for (int j = 0; j < cnt; ++j) {
-                a.free_stack[top + s_prefix[i] + j] = __ldcg(row + j);
-                row[j] = -1;
-            }
+        // push blocks in (argument, table) order: slot top + idx
+        for (int idx = tid; idx < total; idx += kThreads) {
+            const int i = owner(s_prefix, n, idx);
+            int* row = a.bt + (size_t)__ldg(ids + i) * a.MBR;
+            const int j = idx - s_prefix[i];
+            a.free_stack[top + idx] = __ldcg(row + j);
+            row[j] = -1;
         }
         __syncthreads();
         for (int i = tid; i < n; i += kThreads) a.nblk[__ldg(ids + i)] = 0;

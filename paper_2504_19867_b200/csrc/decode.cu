@@ -4,12 +4,12 @@
 //
 // Persistent grid capped to the decode SM budget (P:195 x/y partition), dynamic
 // work counter; a work unit is (request b, kv head g, split s).  Per CTA:
-//   warp 4 (producer, one lane): fetches units, appends k_new/v_new for the unit
-//     owning slot ctx, streams 32-key stages of K and V pages with TMA (128-B
-//     swizzle, one box = 64 columns x min(bs,32) rows of one (block, head) page)
-//     into a 12-deep shared-memory ring (192 KiB: Little's law for HBM latency on
-//     a minority of SMs);
-//   warps 0-3 (consumers): stage i of a unit goes to warp i % 4; QK^T and PV on
+//   warp 3 (producer): fetches units, appends k_new/v_new for the unit
+//     owning slot ctx, streams 64-key stages of K and V pages with TMA (128-B
+//     swizzle, one 4-D box = min(bs,64) rows x all 128 columns of one (block, head)
+//     page) into a 6-deep shared-memory ring (192 KiB: Little's law for HBM latency
+//     on a minority of SMs);
+//   warps 0-2 (consumers): global stage gs goes to warp gs % 3; QK^T and PV on
 //     mma.sync m16n8k16 (the G <= 16 query heads of one kv head fill M = 16, so
 //     each K/V byte is read once for all G heads), warp-shuffle online softmax in
 //     the log2 domain, then a cross-warp merge in shared memory and, for split
@@ -27,11 +27,13 @@ namespace {
 using namespace spd;
 
 constexpr int HD = 128;           // head dim (dk == dv)
-constexpr int KPS = 32;           // keys per stage
-constexpr int NSTAGE = 12;
-constexpr int NCW = 4;            // consumer warps
+constexpr int KPS = 64;           // keys per stage
+constexpr int NSTAGE = 6;
+constexpr int NCW = 3;            // consumer warps; slot s is always consumed by warp s % NCW
+static_assert(NSTAGE % NCW == 0, "each ring slot must have one fixed consumer warp");
 constexpr int NTHREADS = (NCW + 1) * 32;
-constexpr int STAGE_BYTES = 2 * KPS * HD * 2;  // K + V
+constexpr int KV_BYTES = KPS * HD * 2;         // 16 KiB of K (or V) per stage
+constexpr int STAGE_BYTES = 2 * KV_BYTES;      // K + V
 constexpr int SPLIT_KEYS = 4096;  // maximum keys per split (shape-only decomposition)
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -55,7 +57,7 @@ struct DecodeParams {
     int* ws_cnt;                 // [B][Hkv]
     unsigned* sched;             // [2]: next unit, finished CTAs
     int* status;
-    int B, Hq, Hkv, G, bs, MBR, N_B, S_max, n_units, out_head_major;
+    int B, Hq, Hkv, G, lg_bs, MBR, N_B, S_max, n_units, out_head_major;
     float scale_log2;
     SpdTrace trace;
 };
@@ -68,13 +70,24 @@ __device__ __forceinline__ void split_range(int ctx, int S, int s, int& k0, int&
     k1 = min(nk, k0 + len);
 }
 
+// byte offset of (key, 64-column half h) inside a stage's K or V buffer:
+// TMA box b (LG_R rows of one page, both halves) lands as [half][R rows][128 B]
+template <int LG_R>
+__device__ __forceinline__ uint32_t kv_off(int key, int h) {
+    return ((uint32_t)(key >> LG_R) << (LG_R + 8)) + ((uint32_t)h << (LG_R + 7)) +
+           ((uint32_t)(key & ((1 << LG_R) - 1)) << 7);
+}
+
+template <int LG_R>
 __global__ void __launch_bounds__(NTHREADS, 1)
     decode_bf16_kernel(const __grid_constant__ CUtensorMap kmap,
                        const __grid_constant__ CUtensorMap vmap, DecodeParams p) {
+    constexpr int R = 1 << LG_R;     // rows per TMA box (= min(bs, 64))
+    constexpr int NB = KPS / R;      // boxes per stage per tensor
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char* ring = smem;                                   // NSTAGE x 16 KiB
+    unsigned char* ring = smem;                                   // NSTAGE x 32 KiB
     float* scr_acc = reinterpret_cast<float*>(ring + NSTAGE * STAGE_BYTES);  // [NCW][16][128]
     float* scr_ml = scr_acc + NCW * 16 * HD;                       // [NCW][16][2]
     uint64_t* full = reinterpret_cast<uint64_t*>(scr_ml + NCW * 16 * 2);
@@ -100,88 +113,115 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
                 reinterpret_cast<int4*>(p.trace.buf)[slot] =
-                    make_int4(2, (int)smid(), (int)blockIdx.x, 2 /* kernel kind: mma.sync decode */);
+                    make_int4(2, (int)smid(), (int)blockIdx.x, 2 /* kernel kind: split-K decode */);
         }
     }
     __syncthreads();
 
     if (warp == NCW) {
         // =========================== producer ===========================
+        // Whole warp: lane l holds the raw block id of box (32*batch + l) of the unit,
+        // loaded one batch ahead (block-table reads off the TMA issue path); lane 0
+        // issues one TMA per (page, tensor) per box; the K/V append uses 32 lanes.
         if (lane == 0) {
             tma_prefetch_desc(&kmap);
             tma_prefetch_desc(&vmap);
-            const int box = p.bs < KPS ? p.bs : KPS;
-            const int oob_z = p.N_B * p.Hkv;  // first page index past the tensor -> zero fill
-            int gstage = 0, nunit = 0;
-            for (;;) {
-                const int u = (int)atomicAdd(p.sched, 1u);
-                UnitDesc d;
-                if (u >= p.n_units) {
-                    d.b = -1;
-                } else {
-                    // unit order: split-major, then request, then kv head
-                    d.s = u / (p.B * p.Hkv);
-                    d.b = (u / p.Hkv) % p.B;
-                    d.g = u % p.Hkv;
-                    const int ctx = __ldg(p.ctx_lens + d.b);
-                    d.S = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
-                    if (d.s >= d.S) continue;
-                    split_range(ctx, d.S, d.s, d.k0, d.k1);
-                    d.nst = (d.k1 - d.k0 + KPS - 1) / KPS;
-                    d.base = gstage;
+        }
+        const int oob_z = p.N_B * p.Hkv;  // first page index past the tensor -> zero fill
+        const int bs_mask = (1 << p.lg_bs) - 1;
+        int gstage = 0, nunit = 0;
+        for (;;) {
+            int u = 0;
+            if (lane == 0) u = (int)atomicAdd(p.sched, 1u);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            UnitDesc d;
+            if (u >= p.n_units) {
+                d.b = -1;
+            } else {
+                // unit order: split-major, then request, then kv head
+                d.s = u / (p.B * p.Hkv);
+                d.b = (u / p.Hkv) % p.B;
+                d.g = u % p.Hkv;
+                const int ctx = __ldg(p.ctx_lens + d.b);
+                d.S = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+                if (d.s >= d.S) continue;  // warp-uniform
+                split_range(ctx, d.S, d.s, d.k0, d.k1);
+                d.nst = (d.k1 - d.k0 + KPS - 1) / KPS;
+                // align the unit's first stage to a multiple of NCW with data-less padding
+                // stages, so the stage -> warp split depends on the unit only (bitwise
+                // identical results for every grid size / schedule)
+                while (gstage % NCW != 0) {
+                    if (lane == 0) {
+                        const int st = gstage % NSTAGE;
+                        mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
+                        mbar_arrive(full + st);
+                    }
+                    ++gstage;
                 }
-                const int us = nunit & 1;
+                __syncwarp();
+                d.base = gstage;
+            }
+            const int us = nunit & 1;
+            if (lane == 0) {
                 mbar_wait(uempty + us, ((nunit >> 1) & 1) ^ 1);
                 units[us] = d;
                 mbar_arrive(ufull + us);
-                ++nunit;
-                if (d.b < 0) break;
-                const int ctx = __ldg(p.ctx_lens + d.b);
-                const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
-                const int last_page = ctx / p.bs;
-                if (d.s == d.S - 1) {
-                    // fused append of this step's K/V at slot ctx (bit-exact)
-                    const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
-                    if (blk >= 0 && blk < p.N_B) {
-                        const size_t slot = ((size_t)blk * p.Hkv + d.g) * p.bs + (ctx % p.bs);
-                        uint4* kd = reinterpret_cast<uint4*>(p.k_pool) + slot * (HD / 8);
-                        uint4* vd = reinterpret_cast<uint4*>(p.v_pool) + slot * (HD / 8);
-                        const uint4* ks = p.k_new + ((size_t)d.b * p.Hkv + d.g) * (HD / 8);
-                        const uint4* vs = p.v_new + ((size_t)d.b * p.Hkv + d.g) * (HD / 8);
-#pragma unroll 4
-                        for (int c = 0; c < HD / 8; ++c) {
-                            kd[c] = __ldg(ks + c);
-                            vd[c] = __ldg(vs + c);
-                        }
-                        fence_proxy_async_global();
-                    }
+            }
+            __syncwarp();
+            ++nunit;
+            if (d.b < 0) break;
+            const int ctx = __ldg(p.ctx_lens + d.b);
+            const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
+            const int last_page = ctx >> p.lg_bs;
+            if (d.s == d.S - 1) {
+                // fused append of this step's K/V at slot ctx (bit-exact): lanes 0-15 copy
+                // K, lanes 16-31 copy V (16 x 16 B each), then hand over to the async proxy
+                const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
+                if (blk >= 0 && blk < p.N_B) {
+                    const size_t slot = (((size_t)blk * p.Hkv + d.g) << p.lg_bs) + (ctx & bs_mask);
+                    const size_t src = ((size_t)d.b * p.Hkv + d.g) * (HD / 8);
+                    const int c = lane & 15;
+                    if (lane < 16)
+                        reinterpret_cast<uint4*>(p.k_pool)[slot * (HD / 8) + c] = __ldg(p.k_new + src + c);
+                    else
+                        reinterpret_cast<uint4*>(p.v_pool)[slot * (HD / 8) + c] = __ldg(p.v_new + src + c);
+                    fence_proxy_async_global();
                 }
-                for (int i = 0; i < d.nst; ++i, ++gstage) {
-                    const int st = gstage % NSTAGE;
+                __syncwarp();
+            }
+            const int nbox = d.nst * NB;
+            // raw block id for box bi (-2 = past the request's last page: zero fill, no error)
+            auto lookup = [&](int bi) -> int {
+                const int page = (d.k0 + bi * R) >> p.lg_bs;
+                if (bi >= nbox || page > last_page) return -2;
+                return page < p.MBR ? __ldg(btr + page) : -1;
+            };
+            int zc = lookup(lane), zn = lookup(32 + lane);
+            for (int i = 0; i < d.nst; ++i, ++gstage) {
+                const int bb0 = i * NB;
+                if (bb0 > 0 && (bb0 & 31) == 0) {
+                    zc = zn;
+                    zn = lookup(bb0 + 32 + lane);
+                }
+                const int st = gstage % NSTAGE;
+                unsigned char* kst = ring + st * STAGE_BYTES;
+                if (lane == 0) {
                     mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
                     mbar_arrive_expect_tx(full + st, STAGE_BYTES);
-                    unsigned char* kst = ring + st * STAGE_BYTES;
-                    unsigned char* vst = kst + STAGE_BYTES / 2;
-                    for (int r = 0; r < KPS; r += box) {
-                        const int key = d.k0 + i * KPS + r;
-                        const int page = key / p.bs;
-                        int z = oob_z;
-                        if (page <= last_page) {
-                            const int blk = page < p.MBR ? __ldg(btr + page) : -1;
-                            if (blk >= 0 && blk < p.N_B) {
-                                z = blk * p.Hkv + d.g;
-                            } else if (p.status) {
-                                atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
-                            }
-                        }
-                        const int y = key % p.bs;
+                }
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            tma_load_3d(kst + h * (KPS * 128) + r * 128, &kmap, full + st, h * 64, y, z);
-                            tma_load_3d(vst + h * (KPS * 128) + r * 128, &vmap, full + st, h * 64, y, z);
-                        }
+                for (int b = 0; b < NB; ++b) {
+                    const int blk = __shfl_sync(0xffffffffu, zc, (bb0 & 31) + b);
+                    if (lane == 0) {
+                        int z = oob_z;
+                        if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
+                        else if (blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                        const int y = (d.k0 + i * KPS + b * R) & bs_mask;
+                        tma_load_4d(kst + b * (R * 256), &kmap, full + st, 0, y, 0, z);
+                        tma_load_4d(kst + KV_BYTES + b * (R * 256), &vmap, full + st, 0, y, 0, z);
                     }
                 }
+                __syncwarp();
             }
         }
     } else {
@@ -189,6 +229,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int r0 = lane >> 2;       // row (q head within group) of c0/c1
         const int c0 = (lane & 3) * 2;  // column pair
         int nunit = 0;
+        int next_gs = warp;             // next global stage this warp must consume
         for (;;) {
             const int us = nunit & 1;
             mbar_wait(ufull + us, (nunit >> 1) & 1);
@@ -218,22 +259,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
             float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
 
+            // global stage gs goes to warp gs % NCW, so every ring slot is consumed by one
+            // warp in order (each full/empty phase is waited for exactly once); first
+            // release the padding stages in front of this unit
+            while (next_gs < d.base) {
+                const int st = next_gs % NSTAGE;
+                mbar_wait(full + st, (next_gs / NSTAGE) & 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + st);
+                next_gs += NCW;
+            }
+            next_gs = d.base + (warp < d.nst ? warp + ((d.nst - 1 - warp) / NCW + 1) * NCW : warp);
             for (int i = warp; i < d.nst; i += NCW) {
                 const int gs = d.base + i;
                 const int st = gs % NSTAGE;
                 mbar_wait(full + st, (gs / NSTAGE) & 1);
                 const uint32_t kst = smem_u32(ring + st * STAGE_BYTES);
-                const uint32_t vst = kst + STAGE_BYTES / 2;
-                // ---- S = Q K^T : 4 n-tiles of 8 keys
-                float s[4][4];
+                const uint32_t vst = kst + KV_BYTES;
+                // ---- S = Q K^T : 8 n-tiles of 8 keys
+                float s[8][4];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
+                for (int nt = 0; nt < 8; ++nt) {
                     s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
                     const int key = nt * 8 + (lane & 7);
 #pragma unroll
                     for (int kk = 0; kk < 8; kk += 2) {
                         const int ci = 2 * kk + (lane >> 3);
-                        const uint32_t addr = kst + (ci >> 3) * (KPS * 128) + key * 128 +
+                        const uint32_t addr = kst + kv_off<LG_R>(key, ci >> 3) +
                                               (((ci & 7) ^ (key & 7)) << 4);
                         uint32_t b0, b1, b2, b3;
                         ldsm_x4(addr, b0, b1, b2, b3);
@@ -244,13 +296,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 // ---- mask + online softmax (log2 domain); rows r0 (idx 0,1) and r0+8 (2,3)
                 const int kbase = d.k0 + i * KPS;
+                const bool tail = kbase + KPS > d.k1;
                 float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt)
+                for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int key = kbase + nt * 8 + c0 + (e & 1);
-                        const float x = key < d.k1 ? s[nt][e] * p.scale_log2 : -INFINITY;
+                        float x = s[nt][e] * p.scale_log2;
+                        if (tail && kbase + nt * 8 + c0 + (e & 1) >= d.k1) x = -INFINITY;
                         s[nt][e] = x;
                         mx[e >> 1] = fmaxf(mx[e >> 1], x);
                     }
@@ -264,9 +317,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mrow[h] = mnew;
                 }
                 float ls[2] = {0.f, 0.f};
-                uint32_t pa[2][4];
+                uint32_t pa[4][4];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
+                for (int nt = 0; nt < 8; ++nt) {
                     const float p0 = fast_exp2(s[nt][0] - mrow[0]);
                     const float p1 = fast_exp2(s[nt][1] - mrow[0]);
                     const float p2 = fast_exp2(s[nt][2] - mrow[1]);
@@ -288,18 +341,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         acc[nd][3] *= alpha[1];
                     }
                 }
-                // ---- O += P V : 16 dv n-tiles x 2 k-steps of 16 keys
+                // ---- O += P V : 16 dv n-tiles x 4 k-steps of 16 keys
 #pragma unroll
-                for (int ks = 0; ks < 2; ++ks) {
+                for (int ks = 0; ks < 4; ++ks) {
                     const int key = ks * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
 #pragma unroll
                     for (int nd = 0; nd < 16; nd += 2) {
                         const int ch = nd + (lane >> 4);
-                        const uint32_t addr = vst + (ch >> 3) * (KPS * 128) + key * 128 +
+                        const uint32_t addr = vst + kv_off<LG_R>(key, ch >> 3) +
                                               (((ch & 7) ^ (key & 7)) << 4);
                         uint32_t b0, b1, b2, b3;
                         ldsm_x4_t(addr, b0, b1, b2, b3);
-                        // A = P (rows r0 / r0+8; keys 16ks + {c0, c0+8})
                         mma_bf16_16816(acc[nd], pa[ks][0], pa[ks][1], pa[ks][2], pa[ks][3], b0, b1);
                         mma_bf16_16816(acc[nd + 1], pa[ks][0], pa[ks][1], pa[ks][2], pa[ks][3], b2, b3);
                     }
@@ -446,7 +498,7 @@ bool fast_path_ok(const semipd_pool* p, int Hq) {
     const auto& c = p->cfg;
     const int bs = c.block_size;
     return c.dtype == SEMIPD_BF16 && !c.kv_shared && c.head_dim_k == HD && c.head_dim_v == HD &&
-           p->have_maps && Hq % c.num_kv_heads == 0 && Hq / c.num_kv_heads <= 16 &&
+           p->have_dmaps && Hq % c.num_kv_heads == 0 && Hq / c.num_kv_heads <= 16 &&
            (bs == 16 || bs == 32 || bs == 64 || bs == 128);
 }
 
@@ -513,7 +565,7 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     prm.Hq = num_q_heads;
     prm.Hkv = c.num_kv_heads;
     prm.G = num_q_heads / c.num_kv_heads;
-    prm.bs = c.block_size;
+    prm.lg_bs = __builtin_ctz((unsigned)c.block_size);
     prm.MBR = c.max_blocks_per_req;
     prm.N_B = c.num_blocks;
     prm.S_max = S_max;
@@ -522,18 +574,26 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     prm.scale_log2 = softmax_scale * LOG2E;
     prm.trace = spd_trace(pool);
     const size_t smem = decode_smem_bytes();
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(decode_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
-            return SEMIPD_ERR_CUDA;
-        attr_set = true;
-    }
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;
-    decode_bf16_kernel<<<grid, NTHREADS, smem, st>>>(pool->kmap[layer], pool->vmap[layer], prm);
+    const int lg_r = __builtin_ctz((unsigned)pool->dbox_rows);
+    cudaError_t e = cudaSuccess;
+    auto launch = [&](auto kern) {
+        static bool attr_set[3] = {false, false, false};
+        if (!attr_set[lg_r - 4]) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return;
+            attr_set[lg_r - 4] = true;
+        }
+        kern<<<grid, NTHREADS, smem, st>>>(pool->dkmap[layer], pool->dvmap[layer], prm);
+        e = cudaGetLastError();
+    };
+    if (lg_r == 4) launch(decode_bf16_kernel<4>);
+    else if (lg_r == 5) launch(decode_bf16_kernel<5>);
+    else launch(decode_bf16_kernel<6>);
+    if (e != cudaSuccess) return SEMIPD_ERR_CUDA;
     pool->launches += 1;
-    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+    return SEMIPD_OK;
 }
 
 }  // extern "C"

@@ -38,8 +38,13 @@ struct semipd_pool {
     // TMA descriptors of every layer's K and V pool ([N_B*Hkv] pages of
     // [bs][d]; box = 64 columns x min(bs, 32) rows, 128-byte swizzle).
     std::vector<CUtensorMap> kmap, vmap;
-    bool have_maps = false;
+    // decode maps: 4-D (64 cols, dk/64 column blocks, bs rows, pages), box = one
+    // whole page-row-block of min(bs, 64) rows x all column blocks, 128-byte swizzle
+    std::vector<CUtensorMap> dkmap, dvmap;
+    bool have_maps = false;   // 3-D page maps (prefill)
+    bool have_dmaps = false;  // 4-D page maps (decode)
     int box_rows = 16;
+    int dbox_rows = 16;
     int* trace_buf = nullptr;
     int trace_cap = 0;
     int* trace_ctr = nullptr;
@@ -67,6 +72,9 @@ inline int spd_resolve_budget(const semipd_pool* p, int requested, bool prefill)
 }
 
 // TMA encode through the driver entry point (no -lcuda link dependency)
+bool spd_encode_tiled_4d(CUtensorMap* map, CUtensorMapDataType dt, void* gaddr, const uint64_t* dims,
+                         const uint64_t* strides_bytes /* 3 */, const uint32_t* box,
+                         CUtensorMapSwizzle swz);
 bool spd_encode_tiled_3d(CUtensorMap* map, CUtensorMapDataType dt, void* gaddr, uint64_t d0,
                          uint64_t d1, uint64_t d2, uint64_t s1_bytes, uint64_t s2_bytes,
                          uint32_t b0, uint32_t b1, uint32_t b2, CUtensorMapSwizzle swz);

@@ -112,6 +112,20 @@ bool spd_encode_tiled_3d(CUtensorMap* map, CUtensorMapDataType dt, void* gaddr, 
     return r == CUDA_SUCCESS;
 }
 
+bool spd_encode_tiled_4d(CUtensorMap* map, CUtensorMapDataType dt, void* gaddr, const uint64_t* dims,
+                         const uint64_t* strides_bytes, const uint32_t* box,
+                         CUtensorMapSwizzle swz) {
+    PFN_encodeTiled_t enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t d[4] = {dims[0], dims[1], dims[2], dims[3]};
+    cuuint64_t st[3] = {strides_bytes[0], strides_bytes[1], strides_bytes[2]};
+    cuuint32_t b[4] = {box[0], box[1], box[2], box[3]};
+    cuuint32_t e[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, dt, 4, gaddr, d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 extern "C" {
 
 const char* semipd_version(void) { return "semipd-b200 0.1 (sm_100a)"; }
@@ -183,7 +197,11 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
         const uint64_t pages = (uint64_t)cfg->num_blocks * cfg->num_kv_heads;
         p->kmap.resize(cfg->num_layers);
         p->vmap.resize(cfg->num_layers);
-        bool ok = true;
+        p->dkmap.resize(cfg->num_layers);
+        p->dvmap.resize(cfg->num_layers);
+        p->dbox_rows = cfg->block_size < 64 ? cfg->block_size : 64;
+        const bool pow2 = (cfg->block_size & (cfg->block_size - 1)) == 0;
+        bool ok = true, dok = pow2 && cfg->block_size >= 16;
         for (int l = 0; l < cfg->num_layers && ok; ++l) {
             const uint64_t kr = (uint64_t)cfg->head_dim_k * 2;
             ok = spd_encode_tiled_3d(&p->kmap[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p->k_layer(l),
@@ -195,7 +213,22 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
                                            p->v_layer(l), cfg->head_dim_v, cfg->block_size, pages,
                                            vr, vr * cfg->block_size, 64, p->box_rows, 1,
                                            CU_TENSOR_MAP_SWIZZLE_128B);
+            // decode: (64 cols, rows [row pitch], column blocks [128 B], pages [page pitch]);
+            // box = min(bs, 64) rows x all column blocks of one page -> smem
+            // [column block][rows][128 B] (conflict-free 128-byte swizzle per 8 rows)
+            const uint64_t kd[4] = {64, (uint64_t)cfg->block_size, (uint64_t)cfg->head_dim_k / 64, pages};
+            const uint64_t ks[3] = {kr, 128, kr * cfg->block_size};
+            const uint32_t kb[4] = {64, (uint32_t)p->dbox_rows, (uint32_t)cfg->head_dim_k / 64, 1};
+            bool okd = spd_encode_tiled_4d(&p->dkmap[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                           p->k_layer(l), kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_128B);
+            const uint64_t vd[4] = {64, (uint64_t)cfg->block_size, (uint64_t)cfg->head_dim_v / 64, pages};
+            const uint64_t vs[3] = {vr, 128, vr * cfg->block_size};
+            const uint32_t vb[4] = {64, (uint32_t)p->dbox_rows, (uint32_t)cfg->head_dim_v / 64, 1};
+            okd = okd && spd_encode_tiled_4d(&p->dvmap[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                           p->v_layer(l), vd, vs, vb, CU_TENSOR_MAP_SWIZZLE_128B);
+            dok = dok && okd;
         }
+        p->have_dmaps = dok;
         p->have_maps = ok;
     }
     cudaSetDevice(prev);

@@ -10,14 +10,16 @@
 // counter over a persistent grid capped to the prefill SM budget.
 //
 // Warp roles (256 threads, 1 CTA / SM):
-//   warp 0      TMA producer: Q tile (2 x 64-col boxes), K/V tiles of 128 keys as
-//               (128 / box_rows) page boxes per 64-col half, 2-stage K and V rings.
+//   warps 0, 2  TMA producers (0: unit fetch, Q tile, K tiles; 2: V tiles), 2-stage K
+//               and V rings.  Prefix kv tiles (keys < P) are gathered from the paged
+//               pool as (128 / box_rows) page boxes per 64-column half; chunk kv tiles
+//               (the request's own new keys) come from k_new / v_new, 2 boxes each.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
 //               S[j%2] = Q K_j^T  (SS, M=N=128, K=16 x 8);  O += P_j V_j  (TS: P in
 //               TMEM, V MN-major from smem).  Order S_0, S_1, PV_0, S_2, PV_1, ...
 //   warps 4-7   softmax warpgroup, one thread per row: tcgen05.ld S, causal mask,
-//               online softmax in the log2 domain with lazy (threshold 2^8) O
-//               rescale, P (bf16) written back over S with tcgen05.st, epilogue
+//               online softmax in the log2 domain (exact running max, O rescaled
+//               in TMEM when it grows), P (bf16) written back over S with tcgen05.st, epilogue
 //               O / l -> bf16 -> global.
 // TMEM columns: S0 [0,128), S1 [128,256), O [256,384).
 #include <cuda_bf16.h>
@@ -37,10 +39,16 @@ constexpr int NT = 256;
 constexpr uint32_t TILE_BYTES = BM * HD * 2;    // 32 KiB
 constexpr uint32_t HALF_BYTES = TILE_BYTES / 2; // 16 KiB (64 columns)
 constexpr float LOG2E = 1.4426950408889634f;
-constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 domain: rescale when max grows by > 2^8
+// log2 domain: rescale O whenever a row max grows (exact running max).  A stale max
+// (FA4-style threshold 8) leaves the dominant p = 2^(x - m) inexact in bf16, which costs
+// ~0.2% of |o| and breaks the 2e-2 absolute bound for |o| > 4 (S16).
+constexpr float RESCALE_THRESHOLD = 0.0f;
 
 struct PUnit {
-    int i, g, t0, tvalid, pos0, nkv, qrow0, btrow;  // i < 0: no more work
+    // i < 0: no more work.  t0: first chunk row of the q tile; P: cached prefix;
+    // np: prefix kv tiles (keys [0, P) from pages), nkv = np + chunk kv tiles (keys from
+    // k_new / v_new rows crow0 ...); qrow0 = global row of chunk row t0.
+    int i, g, t0, tvalid, P, np, nkv, qrow0, crow0, btrow;
 };
 
 struct PrefillParams {
@@ -51,7 +59,7 @@ struct PrefillParams {
     __nv_bfloat16* out;
     int* status;
     unsigned* sched;
-    int n, T, Hq, Hkv, G, TQ, tiles_max, n_units, bs, box_rows, MBR, N_B, out_head_major;
+    int n, T, Hq, Hkv, G, TQ, tiles_max, n_units, lg_bs, box_rows, MBR, N_B, out_head_major;
     float scale_log2;
     SpdTrace trace;
 };
@@ -77,7 +85,9 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t addr) {
 __global__ void __launch_bounds__(NT, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap,
                       const __grid_constant__ CUtensorMap kmap,
-                      const __grid_constant__ CUtensorMap vmap, PrefillParams p) {
+                      const __grid_constant__ CUtensorMap vmap,
+                      const __grid_constant__ CUtensorMap kcmap,
+                      const __grid_constant__ CUtensorMap vcmap, PrefillParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                         ~uintptr_t(1023));
@@ -95,7 +105,7 @@ __global__ void __launch_bounds__(NT, 1)
             mbar_init(&sm.s_full[s], 1);
             mbar_init(&sm.p_full[s], 128);
             mbar_init(&sm.ufull[s], 1);
-            mbar_init(&sm.uempty[s], 1 + 4);
+            mbar_init(&sm.uempty[s], 1 + 4 + 1);  // MMA warp + 4 softmax warps + V producer
         }
         mbar_init(&sm.o_full, 1);
         mbar_init(&sm.o_empty, 128);
@@ -113,18 +123,32 @@ __global__ void __launch_bounds__(NT, 1)
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
-    if (warp == 0) {
-        // ================================ TMA producer ================================
+    if (warp == 0 || warp == 2) {
+        // ============================ TMA producers ============================
+        // warp 0: unit fetch + Q + K tiles; warp 2: V tiles.  Prefix tiles (keys < P)
+        // come from the paged pool, one box of box_rows x 64 columns per page per half,
+        // page ids prefetched one 32-box batch ahead by the lanes; chunk tiles come
+        // straight from k_new / v_new (two 16 KiB boxes per tile).
+        const int kv = warp == 2;
+        const CUtensorMap* pmap = kv ? &vmap : &kmap;
+        const CUtensorMap* cmap = kv ? &vcmap : &kcmap;
         if (lane == 0) {
-            tma_prefetch_desc(&qmap);
-            tma_prefetch_desc(&kmap);
-            tma_prefetch_desc(&vmap);
-            const int oob_z = p.N_B * p.Hkv;
-            int kvit = 0, nunit = 0;
-            for (;;) {
-                const int u = (int)atomicAdd(p.sched, 1u);
-                PUnit d;
-                d.i = -1;
+            if (!kv) tma_prefetch_desc(&qmap);
+            tma_prefetch_desc(pmap);
+            tma_prefetch_desc(cmap);
+        }
+        const int oob_z = p.N_B * p.Hkv;
+        const int nbox_tile = BN / p.box_rows;  // page boxes per 64-column half of a tile
+        const int bs_mask = (1 << p.lg_bs) - 1;
+        int kvit = 0, nunit = 0;
+        for (;;) {
+            const int us = nunit & 1;
+            PUnit d;
+            d.i = -1;
+            if (!kv) {
+                int u = 0;
+                if (lane == 0) u = (int)atomicAdd(p.sched, 1u);
+                u = __shfl_sync(0xffffffffu, u, 0);
                 if (u < p.n_units) {
                     const int per_tile = p.n * p.Hkv;
                     const int tile = p.tiles_max - 1 - u / per_tile;  // LPT: last tiles first
@@ -132,53 +156,79 @@ __global__ void __launch_bounds__(NT, 1)
                     d.g = u % p.Hkv;
                     const int c0 = __ldg(p.cu + d.i), c1 = __ldg(p.cu + d.i + 1);
                     d.t0 = tile * p.TQ;
-                    if (d.t0 >= c1 - c0) continue;  // tile past this request's chunk
+                    if (d.t0 >= c1 - c0) continue;  // tile past this request's chunk (warp-uniform)
                     d.tvalid = min(p.TQ, c1 - c0 - d.t0);
-                    const int P = __ldg(p.prefix + d.i);
-                    d.pos0 = P + d.t0;
-                    d.nkv = (d.pos0 + d.tvalid - 1) / BN + 1;
+                    d.P = __ldg(p.prefix + d.i);
+                    d.np = (d.P + BN - 1) / BN;
+                    d.nkv = d.np + (d.t0 + d.tvalid - 1) / BN + 1;
                     d.qrow0 = c0 + d.t0;
+                    d.crow0 = c0;
                     d.btrow = __ldg(p.req_ids + d.i);
                 }
-                const int us = nunit & 1;
-                mbar_wait(&sm.uempty[us], ((nunit >> 1) & 1) ^ 1);
-                sm.units[us] = d;
-                mbar_arrive(&sm.ufull[us]);
-                if (d.i < 0) break;
+                if (lane == 0) {
+                    mbar_wait(&sm.uempty[us], ((nunit >> 1) & 1) ^ 1);
+                    sm.units[us] = d;
+                    mbar_arrive(&sm.ufull[us]);
+                }
+                __syncwarp();
+            } else {
+                mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
+                d = sm.units[us];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.uempty[us]);
+            }
+            if (d.i < 0) break;
+            if (!kv && lane == 0) {
                 // Q tile (rows = tokens x G heads of kv head g)
                 mbar_wait(&sm.q_empty, (nunit & 1) ^ 1);
                 mbar_arrive_expect_tx(&sm.q_full, TILE_BYTES);
                 tma_load_3d(sm.q, &qmap, &sm.q_full, 0, d.g * p.G, d.qrow0);
                 tma_load_3d(sm.q + HALF_BYTES, &qmap, &sm.q_full, 64, d.g * p.G, d.qrow0);
-                ++nunit;
-                const int* btr = p.bt + (size_t)d.btrow * p.MBR;
-                const int nkeys = d.pos0 + d.tvalid;  // keys [0, P + t0 + tvalid)
-                const int last_page = (nkeys - 1) / p.bs;
-                for (int j = 0; j < d.nkv; ++j, ++kvit) {
-                    const int st = kvit & 1;
-                    const uint32_t ph = ((kvit >> 1) & 1) ^ 1;
-                    for (int kv = 0; kv < 2; ++kv) {
-                        uint64_t* emp = kv ? &sm.v_empty[st] : &sm.k_empty[st];
-                        uint64_t* ful = kv ? &sm.v_full[st] : &sm.k_full[st];
-                        unsigned char* dst = kv ? sm.v[st] : sm.k[st];
-                        const CUtensorMap* map = kv ? &vmap : &kmap;
-                        mbar_wait(emp, ph);
-                        mbar_arrive_expect_tx(ful, TILE_BYTES);
-                        for (int r = 0; r < BN; r += p.box_rows) {
-                            const int key = j * BN + r;
-                            const int page = key / p.bs;
+            }
+            ++nunit;
+            const int* btr = p.bt + (size_t)d.btrow * p.MBR;
+            const int last_page = (d.P - 1) >> p.lg_bs;  // prefix pages only
+            const int nbox = d.np * nbox_tile;
+            auto lookup = [&](int bi) -> int {  // raw block id; -2 = beyond the prefix
+                const int page = (bi * p.box_rows) >> p.lg_bs;
+                if (bi >= nbox || page > last_page) return -2;
+                return page < p.MBR ? __ldg(btr + page) : -1;
+            };
+            int zc = lookup(lane), zn = lookup(32 + lane);
+            for (int j = 0; j < d.nkv; ++j, ++kvit) {
+                const int st = kvit & 1;
+                const uint32_t ph = ((kvit >> 1) & 1) ^ 1;
+                uint64_t* emp = kv ? &sm.v_empty[st] : &sm.k_empty[st];
+                uint64_t* ful = kv ? &sm.v_full[st] : &sm.k_full[st];
+                unsigned char* dst = kv ? sm.v[st] : sm.k[st];
+                if (lane == 0) {
+                    mbar_wait(emp, ph);
+                    mbar_arrive_expect_tx(ful, TILE_BYTES);
+                }
+                if (j < d.np) {
+                    const int bb0 = j * nbox_tile;
+                    if (bb0 > 0 && (bb0 & 31) == 0) {
+                        zc = zn;
+                        zn = lookup(bb0 + 32 + lane);
+                    }
+                    for (int b = 0; b < nbox_tile; ++b) {
+                        const int blk = __shfl_sync(0xffffffffu, zc, (bb0 & 31) + b);
+                        if (lane == 0) {
                             int z = oob_z;
-                            if (page <= last_page) {
-                                const int blk = page < p.MBR ? __ldg(btr + page) : -1;
-                                if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
-                                else if (p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
-                            }
-                            const int y = key % p.bs;
-                            tma_load_3d(dst + r * 128, map, ful, 0, y, z);
-                            tma_load_3d(dst + HALF_BYTES + r * 128, map, ful, 64, y, z);
+                            if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
+                            else if (blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                            const int r = b * p.box_rows;
+                            const int y = (j * BN + r) & bs_mask;
+                            tma_load_3d(dst + r * 128, pmap, ful, 0, y, z);
+                            tma_load_3d(dst + HALF_BYTES + r * 128, pmap, ful, 64, y, z);
                         }
                     }
+                } else if (lane == 0) {
+                    const int row = d.crow0 + (j - d.np) * BN;
+                    tma_load_3d(dst, cmap, ful, 0, d.g, row);
+                    tma_load_3d(dst + HALF_BYTES, cmap, ful, 64, d.g, row);
                 }
+                __syncwarp();
             }
         }
     } else if (warp == 1) {
@@ -254,7 +304,7 @@ __global__ void __launch_bounds__(NT, 1)
             if (lane == 0) mbar_arrive(&sm.uempty[us]);
             if (d.i < 0) break;
             const int tok = r / p.G;
-            const int pos = d.pos0 + tok;  // absolute position of this row's token
+            const int trel = d.t0 + tok;   // chunk-relative token index of this row
             float m = -INFINITY, l = 0.f;
             for (int j = 0; j < d.nkv; ++j, ++kvit) {
                 const int sb = kvit & 1;
@@ -266,26 +316,55 @@ __global__ void __launch_bounds__(NT, 1)
                 for (int c = 0; c < 4; ++c) tmem_ld32(s_tmem + c * 32, sr[c]);
                 tmem_wait_ld();
                 float mx = -INFINITY;
-                const int kbase = j * BN;
-                const bool need_mask = kbase + BN - 1 > pos;
+                // prefix tile: keys j*BN + c must be < P; chunk tile: chunk-relative key
+                // (j - np)*BN + c must be <= this row's token (causal, bottom-right aligned)
+                const int lim = j < d.np ? d.P - 1 - j * BN : trel - (j - d.np) * BN;
+                const bool need_mask = lim < BN - 1;
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) {
                         float x = __uint_as_float(sr[c][e]) * p.scale_log2;
-                        if (need_mask && kbase + c * 32 + e > pos) x = -INFINITY;
+                        if (need_mask && c * 32 + e > lim) x = -INFINITY;
                         sr[c][e] = __float_as_uint(x);
                         mx = fmaxf(mx, x);
                     }
                 // lazy rescale: keep a stale max unless the new one exceeds it by > 2^8
                 const bool grow = mx > m + RESCALE_THRESHOLD;
+                const bool rescale = j > 0 && __any_sync(0xffffffffu, grow);
+                float alpha = 1.f;
                 if (j == 0) {
                     m = mx;
-                } else if (__any_sync(0xffffffffu, grow)) {
+                } else if (rescale) {
                     const float mnew = grow ? mx : m;
-                    const float alpha = fast_exp2(m - mnew);
-                    mbar_wait(&sm.o_full, (kvit - 1) & 1);  // PV_{j-1} done
+                    alpha = fast_exp2(m - mnew);
+                    m = mnew;
+                }
+                // P = exp2(x - m) in bf16 (registers first, so PV_{j-1} overlaps the exps)
+                float ls = 0.f;
+                uint32_t pk[2][32];
+#pragma unroll
+                for (int c = 0; c < 4; c += 2) {
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        const float a0 = fast_exp2(__uint_as_float(sr[c][e]) - m);
+                        const float a1 = fast_exp2(__uint_as_float(sr[c][e + 1]) - m);
+                        const float b0 = fast_exp2(__uint_as_float(sr[c + 1][e]) - m);
+                        const float b1 = fast_exp2(__uint_as_float(sr[c + 1][e + 1]) - m);
+                        ls += (a0 + a1) + (b0 + b1);
+                        pk[c >> 1][e / 2] = pack_bf16(a0, a1);
+                        pk[c >> 1][16 + e / 2] = pack_bf16(b0, b1);
+                    }
+                }
+                // Every PV completion is waited for, in order, once per tile (a parity wait
+                // is only sound when the waiter is at most one phase behind): PV_{j-1} must be
+                // complete before O is rescaled, and before P_j overwrites the S buffer of
+                // tile j-2 (implied: PVs complete in issue order).
+                if (j > 0) {
+                    mbar_wait(&sm.o_full, (kvit - 1) & 1);
                     tc_fence_after();
+                }
+                if (rescale) {
                     const uint32_t o_tmem = tmem + lane_base + 256u;
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -298,25 +377,9 @@ __global__ void __launch_bounds__(NT, 1)
                         tmem_st32(o_tmem + c * 32, o);
                     }
                     l *= alpha;
-                    m = mnew;
                 }
-                // P = exp2(x - m) in bf16, written over the S columns [0, 64)
-                float ls = 0.f;
-#pragma unroll
-                for (int c = 0; c < 4; c += 2) {
-                    uint32_t pk[32];
-#pragma unroll
-                    for (int e = 0; e < 32; e += 2) {
-                        const float a0 = fast_exp2(__uint_as_float(sr[c][e]) - m);
-                        const float a1 = fast_exp2(__uint_as_float(sr[c][e + 1]) - m);
-                        const float b0 = fast_exp2(__uint_as_float(sr[c + 1][e]) - m);
-                        const float b1 = fast_exp2(__uint_as_float(sr[c + 1][e + 1]) - m);
-                        ls += (a0 + a1) + (b0 + b1);
-                        pk[e / 2] = pack_bf16(a0, a1);
-                        pk[16 + e / 2] = pack_bf16(b0, b1);
-                    }
-                    tmem_st32(s_tmem + (uint32_t)(c * 16), pk);
-                }
+                tmem_st32(s_tmem, pk[0]);
+                tmem_st32(s_tmem + 32u, pk[1]);
                 l += ls;
                 tmem_wait_st();
                 tc_fence_before();
@@ -373,7 +436,7 @@ __global__ void __launch_bounds__(NT, 1)
 bool fast_path_ok(const semipd_pool* pl, int Hq) {
     const auto& c = pl->cfg;
     if (c.dtype != SEMIPD_BF16 || c.kv_shared || c.head_dim_k != HD || c.head_dim_v != HD ||
-        !pl->have_maps || Hq % c.num_kv_heads)
+        !pl->have_maps || Hq % c.num_kv_heads || (c.block_size & (c.block_size - 1)))
         return false;
     const int G = Hq / c.num_kv_heads;
     const int bs = c.block_size;
@@ -432,7 +495,7 @@ extern "C" semipd_status semipd_prefill_attn(
     const long long units = (long long)n * prm.tiles_max * c.num_kv_heads;
     if (units > (1LL << 30)) return SEMIPD_ERR_UNSUPPORTED;
     prm.n_units = (int)units;
-    prm.bs = c.block_size;
+    prm.lg_bs = __builtin_ctz((unsigned)c.block_size);
     prm.box_rows = pool->box_rows;
     prm.MBR = c.max_blocks_per_req;
     prm.N_B = c.num_blocks;
@@ -445,6 +508,16 @@ extern "C" semipd_status semipd_prefill_attn(
                              (uint64_t)num_q_heads * HD * 2, 64, (uint32_t)G, (uint32_t)TQ,
                              CU_TENSOR_MAP_SWIZZLE_128B))
         return SEMIPD_ERR_CUDA;
+    // chunk K / V straight from k_new / v_new: (dk, Hkv, T), box 64 cols x 1 head x 128 rows
+    CUtensorMap kcmap, vcmap;
+    const uint64_t kvrow = (uint64_t)c.num_kv_heads * HD * 2;
+    if (!spd_encode_tiled_3d(&kcmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(k_new), HD,
+                             (uint64_t)c.num_kv_heads, (uint64_t)total_q, HD * 2, kvrow, 64, 1, BN,
+                             CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !spd_encode_tiled_3d(&vcmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(v_new), HD,
+                             (uint64_t)c.num_kv_heads, (uint64_t)total_q, HD * 2, kvrow, 64, 1, BN,
+                             CU_TENSOR_MAP_SWIZZLE_128B))
+        return SEMIPD_ERR_CUDA;
     const size_t smem = sizeof(Smem) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
@@ -455,7 +528,8 @@ extern "C" semipd_status semipd_prefill_attn(
     }
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;
-    prefill_tc_kernel<<<grid, NT, smem, st>>>(qmap, pool->kmap[layer], pool->vmap[layer], prm);
+    prefill_tc_kernel<<<grid, NT, smem, st>>>(qmap, pool->kmap[layer], pool->vmap[layer], kcmap,
+                                              vcmap, prm);
     pool->launches += 1;
     return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }

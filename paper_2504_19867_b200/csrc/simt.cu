@@ -50,29 +50,34 @@ __device__ __forceinline__ void set_status(int* status, int v) {
     if (status) atomicMax(status, v);
 }
 
-// one CTA per (row, kv head) pair, 16-byte copies; bit-exact
-__global__ void kv_write_kernel(RowMap m, int rows, const uint4* __restrict__ k_new,
-                                const uint4* __restrict__ v_new, unsigned char* k_pool,
-                                unsigned char* v_pool, const int* __restrict__ bt, int MBR,
-                                int N_B, int Hkv, int bs, int k_vec, int v_vec, int* status) {
-    for (long long u = blockIdx.x; u < (long long)rows * Hkv; u += gridDim.x) {
+// one warp per (row, kv head) pair, 16-byte vector copies; bit-exact
+constexpr int kKvWarps = 8;
+__global__ void __launch_bounds__(kKvWarps * 32)
+    kv_write_kernel(RowMap m, int rows, const uint4* __restrict__ k_new,
+                    const uint4* __restrict__ v_new, unsigned char* k_pool,
+                    unsigned char* v_pool, const int* __restrict__ bt, int MBR, int N_B, int Hkv,
+                    int bs, int k_vec, int v_vec, int* status) {
+    const int lane = threadIdx.x & 31;
+    const long long total = (long long)rows * Hkv;
+    for (long long u = (long long)blockIdx.x * kKvWarps + (threadIdx.x >> 5); u < total;
+         u += (long long)gridDim.x * kKvWarps) {
         const int row = (int)(u / Hkv), g = (int)(u % Hkv);
         int i, pos;
         map_row(m, row, i, pos);
         const int page = pos / bs;
-        int blk = page < MBR ? __ldg(bt + (size_t)__ldg(m.req + i) * MBR + page) : -1;
+        const int blk = page < MBR ? __ldg(bt + (size_t)__ldg(m.req + i) * MBR + page) : -1;
         if (blk < 0 || blk >= N_B) {
-            if (threadIdx.x == 0) set_status(status, SEMIPD_ERR_BAD_BLOCK);
+            if (lane == 0) set_status(status, SEMIPD_ERR_BAD_BLOCK);
             continue;
         }
         const size_t slot = ((size_t)blk * Hkv + g) * bs + (pos % bs);
         uint4* kd = reinterpret_cast<uint4*>(k_pool) + slot * k_vec;
         const uint4* ks = k_new + ((size_t)row * Hkv + g) * k_vec;
-        for (int c = threadIdx.x; c < k_vec; c += blockDim.x) kd[c] = __ldg(ks + c);
+        for (int c = lane; c < k_vec; c += 32) kd[c] = __ldg(ks + c);
         if (v_pool) {
             uint4* vd = reinterpret_cast<uint4*>(v_pool) + slot * v_vec;
             const uint4* vs = v_new + ((size_t)row * Hkv + g) * v_vec;
-            for (int c = threadIdx.x; c < v_vec; c += blockDim.x) vd[c] = __ldg(vs + c);
+            for (int c = lane; c < v_vec; c += 32) vd[c] = __ldg(vs + c);
         }
     }
 }
@@ -197,10 +202,11 @@ semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new,
     const auto& c = p->cfg;
     const int k_vec = (int)(c.head_dim_k * p->esize / 16);
     const int v_vec = (int)(c.head_dim_v * p->esize / 16);
-    long long units = (long long)total_rows * c.num_kv_heads;
-    int grid = (int)(units < 8LL * p->num_sms ? units : 8LL * p->num_sms);
+    const long long units = (long long)total_rows * c.num_kv_heads;
+    long long grid = (units + kKvWarps - 1) / kKvWarps;
+    if (grid > 16LL * p->num_sms) grid = 16LL * p->num_sms;
     unsigned char* vpool = c.kv_shared ? nullptr : static_cast<unsigned char*>(p->v_layer(layer));
-    kv_write_kernel<<<grid, 64, 0, s>>>(m, total_rows, static_cast<const uint4*>(k_new),
+    kv_write_kernel<<<(unsigned)grid, kKvWarps * 32, 0, s>>>(m, total_rows, static_cast<const uint4*>(k_new),
                                         static_cast<const uint4*>(v_new),
                                         static_cast<unsigned char*>(p->k_layer(layer)), vpool,
                                         p->bt, c.max_blocks_per_req, c.num_blocks,

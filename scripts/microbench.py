@@ -1,0 +1,98 @@
+#!/usr/bin/env python
+"""Isolated per-kernel timing (CUDA events) for the cfg2 shapes at chosen SM budgets.
+
+  python scripts/microbench.py --kernel decode --budgets 37,74,148
+  python scripts/microbench.py --kernel prefill --budgets 74 --iters 3   (under ncu)
+
+Decode: B=64 requests, ctx 2048, Hq 32 / Hkv 8, d 128, bs 16; rotates over L layers
+of distinct pool memory (L x 537 MB >> L2).  Prefill: one 2048-token chunk, P=0.
+Prints one JSON line per (kernel, budget): median ms, GB/s (decode, algorithmic
+bytes), TFLOP/s (prefill, unmasked pairs).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2504_19867_b200 import KVPool, PoolConfig  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kernel", default="decode", choices=["decode", "prefill", "both"])
+    ap.add_argument("--budgets", default="74,148")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--ctx", type=int, default=2048)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--chunk", type=int, default=2048)
+    ap.add_argument("--prefix", type=int, default=0)
+    ap.add_argument("--hq", type=int, default=32)
+    ap.add_argument("--hkv", type=int, default=8)
+    ap.add_argument("--bs", type=int, default=16)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    L, B, ctx, C, P = args.layers, args.batch, args.ctx, args.chunk, args.prefix
+    Hq, Hkv, d, bs = args.hq, args.hkv, 128, args.bs
+    nb_dec = ctx // bs + 1
+    nb_pre = -(-(C + P) // bs)
+    cfg = PoolConfig(L, B * nb_dec + nb_pre + 8, bs, Hkv, d, d, B + 2, max(nb_dec, nb_pre) + 2)
+    pool = KVPool(cfg, dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32(list(range(B))), i32([nb_dec] * B))
+    pool.alloc_blocks(i32([B]), i32([nb_pre]))
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    for l in range(L):
+        K, V, _, _ = pool.views(l)
+        K.normal_(generator=g)
+        V.normal_(generator=g)
+    rnd = lambda *s: torch.randn(*s, device=dev, generator=g).bfloat16()  # noqa: E731
+    sc = 1 / math.sqrt(d)
+    qd, kd, vd = rnd(B, Hq, d), rnd(B, Hkv, d), rnd(B, Hkv, d)
+    od = torch.empty(B, Hq, d, dtype=torch.bfloat16, device=dev)
+    ws = pool.new_decode_workspace(B, Hq, ctx)
+    rid, ctxs = i32(list(range(B))), i32([ctx] * B)
+    qp, kp, vp = rnd(C, Hq, d), rnd(C, Hkv, d), rnd(C, Hkv, d)
+    op = torch.empty(C, Hq, d, dtype=torch.bfloat16, device=dev)
+    cu, ridp, pre = i32([0, C]), i32([B]), i32([P])
+    dec_bytes = B * (ctx + 1) * Hkv * 2 * d * 2 + B * Hq * 2 * d * 2
+    pairs = C * P + C * (C + 1) / 2
+    pre_flops = 2 * Hq * 2 * d * pairs
+    kernels = ["decode", "prefill"] if args.kernel == "both" else [args.kernel]
+    for kern in kernels:
+        for bud in [int(x) for x in args.budgets.split(",")]:
+            def run(l):
+                if kern == "decode":
+                    pool.decode_attn(l, qd, kd, vd, rid, ctxs, ctx, sc, od, ws, sm_budget=bud)
+                else:
+                    pool.prefill_attn(l, qp, kp, vp, cu, ridp, pre, C, C, sc, op, sm_budget=bud)
+            for l in range(min(L, 3)):
+                run(l)
+            torch.cuda.synchronize()
+            times = []
+            for it in range(args.iters):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run(it % L)
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+            ms = statistics.median(times)
+            rec = {"kernel": kern, "budget": bud, "ms": ms, "min_ms": min(times)}
+            if kern == "decode":
+                rec["GB_s"] = dec_bytes / (ms / 1e3) / 1e9
+            else:
+                rec["TFLOP_s"] = pre_flops / (ms / 1e3) / 1e12
+            print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -299,6 +299,23 @@ def test_prefill_head_major_and_layer():
                 num_layers=2)
 
 
+def test_prefill_repeat_stress():
+    """Same multi-request launch 20x: any pipeline race shows up as a bitwise change."""
+    outs = [run_prefill(small(SHAPE_8B), [33, 1, 250, 129], [0, 5, 300, 16], seed=31,
+                        dist=synth.NEEDLE, sm_budget=b)[0].cpu() for b in [3, 148] * 10]
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+def test_decode_repeat_stress_short_units():
+    """Short units (1-3 stages) interleaved with long ones rotate stages over warps."""
+    ctx = [5, 70, 130, 4100, 63, 200, 9000, 1]
+    outs = [run_decode(small(SHAPE_8B), ctx, seed=17, dist=synth.NEEDLE, sm_budget=b)[0].cpu()
+            for b in [2, 148] * 8]
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
 def test_prefill_bitwise_stable_across_budgets():
     outs = [run_prefill(small(SHAPE_8B), [400, 90], [30, 0], seed=12, dist=synth.FLAT,
                         sm_budget=b)[0].cpu() for b in (1, 5, 74, 148, -1)]

@@ -3,25 +3,29 @@
 // pool (P:184 prefill writes K/V; P:229 paged access; P:355 GQA kernels for both
 // phases; P:365 chunked prefill).
 //
-// Work unit: (request i, q tile of 128 rows, kv head g).  GQA packing: the G q
-// heads of kv head g x (128 / G) tokens fill the M = 128 rows of one tile (row
-// r = token (r / G), head g*G + r % G), so every K/V tile is staged once for all
-// G heads.  Units run longest-first (LPT: last q tiles first) from a dynamic work
-// counter over a persistent grid capped to the prefill SM budget.
+// Tile: 128 rows = the G q heads of kv head g x (128 / G) tokens (row r = token r / G,
+// head g*G + r % G), so every K/V tile is staged once for all G heads (GQA packing).
+// Work unit: (request i, PAIR of consecutive q tiles A, B, kv head g); A and B share
+// every K/V tile.  Units run longest-first (LPT: last pairs first) from a dynamic
+// work counter over a persistent grid capped to the prefill SM budget.
 //
-// Warp roles (256 threads, 1 CTA / SM):
-//   warps 0, 2  TMA producers (0: unit fetch, Q tile, K tiles; 2: V tiles), 2-stage K
-//               and V rings.  Prefix kv tiles (keys < P) are gathered from the paged
-//               pool as (128 / box_rows) page boxes per 64-column half; chunk kv tiles
-//               (the request's own new keys) come from k_new / v_new, 2 boxes each.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
-//               S[j%2] = Q K_j^T  (SS, M=N=128, K=16 x 8);  O += P_j V_j  (TS: P in
-//               TMEM, V MN-major from smem).  Order S_0, S_1, PV_0, S_2, PV_1, ...
-//   warps 4-7   softmax warpgroup, one thread per row: tcgen05.ld S, causal mask,
-//               online softmax in the log2 domain (exact running max, O rescaled
-//               in TMEM when it grows), P (bf16) written back over S with tcgen05.st, epilogue
-//               O / l -> bf16 -> global.
-// TMEM columns: S0 [0,128), S1 [128,256), O [256,384).
+// Warp roles (384 threads, 1 CTA / SM; setmaxnreg moves registers to the softmax):
+//   warp 0      unit fetch, Q_A + Q_B tiles, K tiles (TMA)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, in the order
+//               S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...  so each softmax
+//               warpgroup works while the tensor core serves the other tile
+//               (S = Q K^T: SS, M = N = 128, K = 8 x 16; O += P V: TS, P from TMEM,
+//               V MN-major from smem)
+//   warp 2      V tiles (TMA)
+//   warps 4-7   softmax warpgroup of tile A, warps 8-11 of tile B; one thread per row:
+//               tcgen05.ld S, causal mask, online softmax in the log2 domain with packed
+//               f32x2 math (exact running max; O rescaled in TMEM when it grows - safe
+//               without a wait because S_t(j)'s commit implies PV_t(j-1) completed),
+//               P (bf16) written back over S with tcgen05.st; epilogue O / l -> global.
+// Prefix kv tiles (keys < P) are gathered from the paged pool as (128 / box_rows) page
+// boxes per 64-column half; chunk kv tiles (the request's own new keys) come from
+// k_new / v_new (two 16 KiB boxes per tile).
+// TMEM columns: S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -35,20 +39,18 @@ using namespace spd;
 constexpr int HD = 128;
 constexpr int BM = 128;   // rows per tile
 constexpr int BN = 128;   // keys per kv tile
-constexpr int NT = 256;
+constexpr int NT = 384;
 constexpr uint32_t TILE_BYTES = BM * HD * 2;    // 32 KiB
 constexpr uint32_t HALF_BYTES = TILE_BYTES / 2; // 16 KiB (64 columns)
 constexpr float LOG2E = 1.4426950408889634f;
-// log2 domain: rescale O whenever a row max grows (exact running max).  A stale max
-// (FA4-style threshold 8) leaves the dominant p = 2^(x - m) inexact in bf16, which costs
-// ~0.2% of |o| and breaks the 2e-2 absolute bound for |o| > 4 (S16).
-constexpr float RESCALE_THRESHOLD = 0.0f;
 
 struct PUnit {
-    // i < 0: no more work.  t0: first chunk row of the q tile; P: cached prefix;
-    // np: prefix kv tiles (keys [0, P) from pages), nkv = np + chunk kv tiles (keys from
-    // k_new / v_new rows crow0 ...); qrow0 = global row of chunk row t0.
-    int i, g, t0, tvalid, P, np, nkv, qrow0, crow0, btrow;
+    // i < 0: no more work.  t0: first chunk row of tile A (tile B starts at t0 + TQ);
+    // tv[t]: valid rows (tokens) of tile t; P: cached prefix; np: prefix kv tiles;
+    // nkv[t] = np + chunk kv tiles tile t needs (nkv[0] <= nkv[1]); qrow0: global row of
+    // chunk row t0; crow0: global row of the request's first chunk row.
+    int i, g, t0, P, np, qrow0, crow0, btrow;
+    int tv[2], nkv[2];
 };
 
 struct PrefillParams {
@@ -59,20 +61,20 @@ struct PrefillParams {
     __nv_bfloat16* out;
     int* status;
     unsigned* sched;
-    int n, T, Hq, Hkv, G, TQ, tiles_max, n_units, lg_bs, box_rows, MBR, N_B, out_head_major;
+    int n, T, Hq, Hkv, G, TQ, pairs_max, n_units, lg_bs, box_rows, MBR, N_B, out_head_major;
     float scale_log2;
     SpdTrace trace;
 };
 
 struct Smem {
     // operand tiles first (1024-aligned by construction)
-    unsigned char q[TILE_BYTES];
+    unsigned char q[2][TILE_BYTES];
     unsigned char k[2][TILE_BYTES];
     unsigned char v[2][TILE_BYTES];
     uint64_t q_full, q_empty;
     uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-    uint64_t s_full[2], p_full[2];
-    uint64_t o_full, o_empty;
+    uint64_t s_full[2], p_full[2];   // per q tile
+    uint64_t o_full[2], o_empty[2];  // per q tile
     uint64_t ufull[2], uempty[2];
     PUnit units[2];
     uint32_t tmem_base;
@@ -104,11 +106,11 @@ __global__ void __launch_bounds__(NT, 1)
             mbar_init(&sm.v_empty[s], 1);
             mbar_init(&sm.s_full[s], 1);
             mbar_init(&sm.p_full[s], 128);
+            mbar_init(&sm.o_full[s], 1);
+            mbar_init(&sm.o_empty[s], 128);
             mbar_init(&sm.ufull[s], 1);
-            mbar_init(&sm.uempty[s], 1 + 4 + 1);  // MMA warp + 4 softmax warps + V producer
+            mbar_init(&sm.uempty[s], 1 + 8 + 1);  // MMA warp + 8 softmax warps + V producer
         }
-        mbar_init(&sm.o_full, 1);
-        mbar_init(&sm.o_empty, 128);
         fence_mbar_init();
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
@@ -123,12 +125,11 @@ __global__ void __launch_bounds__(NT, 1)
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
+    if (warp < 4) {
+    // ====================== warpgroup 0: TMA producers + MMA issuer ======================
+    setmaxnreg_dec<72>();
     if (warp == 0 || warp == 2) {
         // ============================ TMA producers ============================
-        // warp 0: unit fetch + Q + K tiles; warp 2: V tiles.  Prefix tiles (keys < P)
-        // come from the paged pool, one box of box_rows x 64 columns per page per half,
-        // page ids prefetched one 32-box batch ahead by the lanes; chunk tiles come
-        // straight from k_new / v_new (two 16 KiB boxes per tile).
         const int kv = warp == 2;
         const CUtensorMap* pmap = kv ? &vmap : &kmap;
         const CUtensorMap* cmap = kv ? &vcmap : &kcmap;
@@ -150,17 +151,20 @@ __global__ void __launch_bounds__(NT, 1)
                 if (lane == 0) u = (int)atomicAdd(p.sched, 1u);
                 u = __shfl_sync(0xffffffffu, u, 0);
                 if (u < p.n_units) {
-                    const int per_tile = p.n * p.Hkv;
-                    const int tile = p.tiles_max - 1 - u / per_tile;  // LPT: last tiles first
+                    const int per_pair = p.n * p.Hkv;
+                    const int pair = p.pairs_max - 1 - u / per_pair;  // LPT: last pairs first
                     d.i = (u / p.Hkv) % p.n;
                     d.g = u % p.Hkv;
                     const int c0 = __ldg(p.cu + d.i), c1 = __ldg(p.cu + d.i + 1);
-                    d.t0 = tile * p.TQ;
-                    if (d.t0 >= c1 - c0) continue;  // tile past this request's chunk (warp-uniform)
-                    d.tvalid = min(p.TQ, c1 - c0 - d.t0);
+                    const int C = c1 - c0;
+                    d.t0 = pair * 2 * p.TQ;
+                    if (d.t0 >= C) continue;  // pair past this request's chunk (warp-uniform)
+                    d.tv[0] = min(p.TQ, C - d.t0);
+                    d.tv[1] = max(0, min(p.TQ, C - d.t0 - p.TQ));
                     d.P = __ldg(p.prefix + d.i);
                     d.np = (d.P + BN - 1) / BN;
-                    d.nkv = d.np + (d.t0 + d.tvalid - 1) / BN + 1;
+                    d.nkv[0] = d.np + (d.t0 + d.tv[0] - 1) / BN + 1;
+                    d.nkv[1] = d.tv[1] > 0 ? d.np + (d.t0 + p.TQ + d.tv[1] - 1) / BN + 1 : d.nkv[0];
                     d.qrow0 = c0 + d.t0;
                     d.crow0 = c0;
                     d.btrow = __ldg(p.req_ids + d.i);
@@ -179,11 +183,15 @@ __global__ void __launch_bounds__(NT, 1)
             }
             if (d.i < 0) break;
             if (!kv && lane == 0) {
-                // Q tile (rows = tokens x G heads of kv head g)
+                // Q tiles A and B (rows = tokens x G heads of kv head g)
                 mbar_wait(&sm.q_empty, (nunit & 1) ^ 1);
-                mbar_arrive_expect_tx(&sm.q_full, TILE_BYTES);
-                tma_load_3d(sm.q, &qmap, &sm.q_full, 0, d.g * p.G, d.qrow0);
-                tma_load_3d(sm.q + HALF_BYTES, &qmap, &sm.q_full, 64, d.g * p.G, d.qrow0);
+                mbar_arrive_expect_tx(&sm.q_full, 2 * TILE_BYTES);
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    tma_load_3d(sm.q[t], &qmap, &sm.q_full, 0, d.g * p.G, d.qrow0 + t * p.TQ);
+                    tma_load_3d(sm.q[t] + HALF_BYTES, &qmap, &sm.q_full, 64, d.g * p.G,
+                                d.qrow0 + t * p.TQ);
+                }
             }
             ++nunit;
             const int* btr = p.bt + (size_t)d.btrow * p.MBR;
@@ -195,7 +203,8 @@ __global__ void __launch_bounds__(NT, 1)
                 return page < p.MBR ? __ldg(btr + page) : -1;
             };
             int zc = lookup(lane), zn = lookup(32 + lane);
-            for (int j = 0; j < d.nkv; ++j, ++kvit) {
+            const int nkv = d.nkv[1];
+            for (int j = 0; j < nkv; ++j, ++kvit) {
                 const int st = kvit & 1;
                 const uint32_t ph = ((kvit >> 1) & 1) ^ 1;
                 uint64_t* emp = kv ? &sm.v_empty[st] : &sm.k_empty[st];
@@ -236,8 +245,8 @@ __global__ void __launch_bounds__(NT, 1)
         if (lane == 0) {
             const uint32_t idesc_s = umma_idesc_bf16_f32(BM, BN, 0);
             const uint32_t idesc_o = umma_idesc_bf16_f32(BM, HD, 1);
-            const uint32_t q_addr = smem_u32(sm.q);
             int kvit = 0, nunit = 0;
+            int cnt_a = 0, cnt_b = 0;  // P tiles consumed so far per q tile (p_full phases)
             for (;;) {
                 const int us = nunit & 1;
                 mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
@@ -246,56 +255,81 @@ __global__ void __launch_bounds__(NT, 1)
                 if (d.i < 0) break;
                 mbar_wait(&sm.q_full, nunit & 1);
                 tc_fence_after();
-                auto issue_s = [&](int it) {
-                    const int st = it & 1;
-                    mbar_wait(&sm.k_full[st], (it >> 1) & 1);
-                    tc_fence_after();
-                    const uint32_t k_addr = smem_u32(sm.k[st]);
-                    const uint32_t d_tmem = tmem + (uint32_t)(st * BN);
+                const int nA = d.nkv[0], nB = d.nkv[1];
+                auto issue_s = [&](int t, int it) {  // S_t = Q_t K^T (K stage of kv tile it)
+                    const uint32_t q_addr = smem_u32(sm.q[t]);
+                    const uint32_t k_addr = smem_u32(sm.k[it & 1]);
+                    const uint32_t d_tmem = tmem + (uint32_t)(t * BN);
 #pragma unroll
                     for (int kk = 0; kk < HD / 16; ++kk) {
                         const uint32_t off = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
                         umma_ss(d_tmem, kmajor_desc(q_addr + off), kmajor_desc(k_addr + off),
                                 idesc_s, kk > 0 ? 1u : 0u);
                     }
-                    umma_commit(&sm.s_full[st]);
-                    umma_commit(&sm.k_empty[st]);
+                    umma_commit(&sm.s_full[t]);
                 };
-                auto issue_pv = [&](int it, bool first) {
-                    const int st = it & 1;
-                    mbar_wait(&sm.p_full[st], (it >> 1) & 1);
-                    if (first) mbar_wait(&sm.o_empty, (nunit & 1) ^ 1);
-                    mbar_wait(&sm.v_full[st], (it >> 1) & 1);
+                auto issue_pv = [&](int t, int& cnt, int it, bool first) {  // O_t += P_t V
+                    mbar_wait(&sm.p_full[t], cnt & 1);
+                    ++cnt;
                     tc_fence_after();
-                    const uint32_t v_addr = smem_u32(sm.v[st]);
-                    const uint32_t p_tmem = tmem + (uint32_t)(st * BN);
-                    const uint32_t o_tmem = tmem + 256u;
+                    const uint32_t v_addr = smem_u32(sm.v[it & 1]);
+                    const uint32_t p_tmem = tmem + (uint32_t)(t * BN);
+                    const uint32_t o_tmem = tmem + 256u + (uint32_t)(t * HD);
 #pragma unroll
                     for (int kk = 0; kk < BN / 16; ++kk) {
                         const uint64_t bdesc = umma_desc_sw128(v_addr + kk * 2048, HALF_BYTES, 1024);
                         umma_ts(o_tmem, p_tmem + (uint32_t)(kk * 8), bdesc, idesc_o,
                                 (first && kk == 0) ? 0u : 1u);
                     }
-                    umma_commit(&sm.v_empty[st]);
-                    umma_commit(&sm.o_full);
+                };
+                auto wait_full = [&](uint64_t* bars, int it) {
+                    mbar_wait(&bars[it & 1], (it >> 1) & 1);
+                    tc_fence_after();
                 };
                 const int it0 = kvit;
-                for (int j = 0; j < d.nkv; ++j) {
-                    issue_s(it0 + j);
-                    if (j == d.nkv - 1) umma_commit(&sm.q_empty);
-                    if (j > 0) issue_pv(it0 + j - 1, j - 1 == 0);
+                // prologue: S_A(0), S_B(0)
+                wait_full(sm.k_full, it0);
+                issue_s(0, it0);
+                issue_s(1, it0);
+                umma_commit(&sm.k_empty[it0 & 1]);
+                if (nB == 1) umma_commit(&sm.q_empty);
+                for (int j = 0; j < nB; ++j) {
+                    const int it = it0 + j;
+                    wait_full(sm.v_full, it);
+                    if (j < nA) {
+                        if (j == 0) mbar_wait(&sm.o_empty[0], (nunit & 1) ^ 1);
+                        issue_pv(0, cnt_a, it, j == 0);
+                        if (j == nA - 1) umma_commit(&sm.o_full[0]);
+                    }
+                    const bool more = j + 1 < nB;
+                    if (more) wait_full(sm.k_full, it + 1);
+                    if (j + 1 < nA) issue_s(0, it + 1);
+                    if (j == 0) mbar_wait(&sm.o_empty[1], (nunit & 1) ^ 1);
+                    issue_pv(1, cnt_b, it, j == 0);
+                    umma_commit(&sm.v_empty[it & 1]);
+                    if (j == nB - 1) umma_commit(&sm.o_full[1]);
+                    if (more) {
+                        issue_s(1, it + 1);
+                        umma_commit(&sm.k_empty[(it + 1) & 1]);
+                        if (j + 1 == nB - 1) umma_commit(&sm.q_empty);
+                    }
                 }
-                issue_pv(it0 + d.nkv - 1, d.nkv == 1);
-                kvit = it0 + d.nkv;
+                kvit = it0 + nB;
                 ++nunit;
             }
         }
-    } else if (warp >= 4) {
-        // ============================ softmax warpgroup ============================
-        const int q4 = warp - 4;              // TMEM lane quarter
-        const int r = q4 * 32 + lane;         // tile row
+    }
+    } else {
+        // ============================ softmax warpgroups ============================
+        setmaxnreg_inc<216>();
+        const int t = (warp - 4) >> 2;         // q tile A (0) or B (1)
+        const int q4 = warp & 3;               // TMEM lane quarter
+        const int r = q4 * 32 + lane;          // tile row
         const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-        int kvit = 0, nunit = 0;
+        const uint32_t s_tmem = tmem + lane_base + (uint32_t)(t * BN);
+        const uint32_t o_tmem = tmem + lane_base + 256u + (uint32_t)(t * HD);
+        const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
+        int cnt = 0, nunit = 0;
         for (;;) {
             const int us = nunit & 1;
             mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
@@ -304,98 +338,93 @@ __global__ void __launch_bounds__(NT, 1)
             if (lane == 0) mbar_arrive(&sm.uempty[us]);
             if (d.i < 0) break;
             const int tok = r / p.G;
-            const int trel = d.t0 + tok;   // chunk-relative token index of this row
-            float m = -INFINITY, l = 0.f;
-            for (int j = 0; j < d.nkv; ++j, ++kvit) {
-                const int sb = kvit & 1;
-                mbar_wait(&sm.s_full[sb], (kvit >> 1) & 1);
+            const int trel = d.t0 + t * p.TQ + tok;  // chunk-relative token index of this row
+            const int nkv = d.nkv[t];
+            float m = -INFINITY;
+            uint64_t l2 = f2(0.f, 0.f);
+            for (int j = 0; j < nkv; ++j, ++cnt) {
+                mbar_wait(&sm.s_full[t], cnt & 1);
                 tc_fence_after();
-                const uint32_t s_tmem = tmem + lane_base + (uint32_t)(sb * BN);
                 uint32_t sr[4][32];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) tmem_ld32(s_tmem + c * 32, sr[c]);
                 tmem_wait_ld();
-                float mx = -INFINITY;
                 // prefix tile: keys j*BN + c must be < P; chunk tile: chunk-relative key
                 // (j - np)*BN + c must be <= this row's token (causal, bottom-right aligned)
                 const int lim = j < d.np ? d.P - 1 - j * BN : trel - (j - d.np) * BN;
-                const bool need_mask = lim < BN - 1;
+                if (lim < BN - 1) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (c * 32 + e > lim) sr[c][e] = __float_as_uint(-INFINITY);
+                }
+                float mx = -INFINITY;
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        float x = __uint_as_float(sr[c][e]) * p.scale_log2;
-                        if (need_mask && c * 32 + e > lim) x = -INFINITY;
-                        sr[c][e] = __float_as_uint(x);
-                        mx = fmaxf(mx, x);
-                    }
-                // lazy rescale: keep a stale max unless the new one exceeds it by > 2^8
-                const bool grow = mx > m + RESCALE_THRESHOLD;
-                const bool rescale = j > 0 && __any_sync(0xffffffffu, grow);
-                float alpha = 1.f;
-                if (j == 0) {
-                    m = mx;
-                } else if (rescale) {
-                    const float mnew = grow ? mx : m;
-                    alpha = fast_exp2(m - mnew);
-                    m = mnew;
-                }
-                // P = exp2(x - m) in bf16 (registers first, so PV_{j-1} overlaps the exps)
-                float ls = 0.f;
-                uint32_t pk[2][32];
-#pragma unroll
-                for (int c = 0; c < 4; c += 2) {
-#pragma unroll
-                    for (int e = 0; e < 32; e += 2) {
-                        const float a0 = fast_exp2(__uint_as_float(sr[c][e]) - m);
-                        const float a1 = fast_exp2(__uint_as_float(sr[c][e + 1]) - m);
-                        const float b0 = fast_exp2(__uint_as_float(sr[c + 1][e]) - m);
-                        const float b1 = fast_exp2(__uint_as_float(sr[c + 1][e + 1]) - m);
-                        ls += (a0 + a1) + (b0 + b1);
-                        pk[c >> 1][e / 2] = pack_bf16(a0, a1);
-                        pk[c >> 1][16 + e / 2] = pack_bf16(b0, b1);
-                    }
-                }
-                // Every PV completion is waited for, in order, once per tile (a parity wait
-                // is only sound when the waiter is at most one phase behind): PV_{j-1} must be
-                // complete before O is rescaled, and before P_j overwrites the S buffer of
-                // tile j-2 (implied: PVs complete in issue order).
-                if (j > 0) {
-                    mbar_wait(&sm.o_full, (kvit - 1) & 1);
-                    tc_fence_after();
-                }
-                if (rescale) {
-                    const uint32_t o_tmem = tmem + lane_base + 256u;
+                    for (int e = 0; e < 32; e += 2)
+                        mx = fmax3(mx, __uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1]));
+                const float mnew = fmaxf(m, mx * p.scale_log2);  // scale > 0: max commutes
+                // exact running max: rescale O_t in TMEM when a row max grows (PV_t(j-1)
+                // is complete: S_t(j) was issued after it and its commit tracks both)
+                if (j > 0 && __any_sync(0xffffffffu, mnew > m)) {
+                    const float alpha = fast_exp2(m - mnew);
+                    const uint64_t a2 = f2(alpha, alpha);
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         uint32_t o[32];
                         tmem_ld32(o_tmem + c * 32, o);
                         tmem_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                        for (int e = 0; e < 32; e += 2) {
+                            float lo, hi;
+                            f2_split(fmul2(f2(__uint_as_float(o[e]), __uint_as_float(o[e + 1])), a2),
+                                     lo, hi);
+                            o[e] = __float_as_uint(lo);
+                            o[e + 1] = __float_as_uint(hi);
+                        }
                         tmem_st32(o_tmem + c * 32, o);
                     }
-                    l *= alpha;
+                    l2 = fmul2(l2, a2);
                 }
-                tmem_st32(s_tmem, pk[0]);
-                tmem_st32(s_tmem + 32u, pk[1]);
-                l += ls;
+                m = mnew;
+                // P = exp2(s * scale - m) (bf16) over the S columns [0, 64)
+                const uint64_t nm2 = f2(-m, -m);
+#pragma unroll
+                for (int c = 0; c < 4; c += 2) {
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int e = 0; e < 32; e += 2) {
+                            float x0, x1;
+                            f2_split(ffma2(f2(__uint_as_float(sr[c + h][e]),
+                                              __uint_as_float(sr[c + h][e + 1])),
+                                           sc2, nm2),
+                                     x0, x1);
+                            const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+                            l2 = fadd2(l2, f2(p0, p1));
+                            pk[h * 16 + e / 2] = pack_bf16(p0, p1);
+                        }
+                    tmem_st32(s_tmem + (uint32_t)(c * 16), pk);
+                }
                 tmem_wait_st();
                 tc_fence_before();
-                mbar_arrive(&sm.p_full[sb]);
+                mbar_arrive(&sm.p_full[t]);
             }
             // ---- epilogue: O / l -> bf16 -> global
-            mbar_wait(&sm.o_full, (kvit - 1) & 1);
+            mbar_wait(&sm.o_full[t], nunit & 1);
             tc_fence_after();
-            const bool valid = tok < d.tvalid;
+            float la, lb;
+            f2_split(l2, la, lb);
+            const float inv = 1.f / (la + lb);
+            const bool valid = tok < d.tv[t];
             const int hq = d.g * p.G + (r % p.G);
-            const int trow = d.qrow0 + tok;
+            const int trow = d.qrow0 + t * p.TQ + tok;
             __nv_bfloat16* dst = p.out + (p.out_head_major
                                               ? ((size_t)hq * p.T + trow) * HD
                                               : ((size_t)trow * p.Hq + hq) * HD);
-            const float inv = 1.f / l;
-            const uint32_t o_tmem = tmem + lane_base + 256u;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t o[32];
@@ -414,7 +443,7 @@ __global__ void __launch_bounds__(NT, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&sm.o_empty);
+            mbar_arrive(&sm.o_empty[t]);
             ++nunit;
         }
     }
@@ -490,9 +519,9 @@ extern "C" semipd_status semipd_prefill_attn(
     prm.Hkv = c.num_kv_heads;
     prm.G = G;
     prm.TQ = TQ;
-    prm.tiles_max = (max_chunk_len + TQ - 1) / TQ;
-    if (prm.tiles_max < 1) return SEMIPD_OK;
-    const long long units = (long long)n * prm.tiles_max * c.num_kv_heads;
+    prm.pairs_max = (max_chunk_len + 2 * TQ - 1) / (2 * TQ);
+    if (prm.pairs_max < 1) return SEMIPD_OK;
+    const long long units = (long long)n * prm.pairs_max * c.num_kv_heads;
     if (units > (1LL << 30)) return SEMIPD_ERR_UNSUPPORTED;
     prm.n_units = (int)units;
     prm.lg_bs = __builtin_ctz((unsigned)c.block_size);

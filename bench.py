@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--model", default="llama3-8b", choices=list(MODELS))
     ap.add_argument("--split", type=float, default=None, help="prefill SM percent x (y = 100-x)")
     ap.add_argument("--sweep", default="30,40,50,60,70")
+    ap.add_argument("--block-size", type=int, default=64,
+                    help="KV page size in tokens (64: one 16 KiB TMA box per (block, head) "
+                         "page on B200; 16 is supported but TMA-per-box bound)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extra", action="store_true", help="serial / (100,100) / isolated curves")
@@ -76,52 +79,59 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons polled through NVML every ~10 ms while the timed
+    region runs (nvidia-smi's 100 ms interval is longer than short timed regions)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-    def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.index, self.period, self.rows, self.max_mhz = index, period_s, [], None
+        self._stop = threading.Event()
+        self.err = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+            except Exception as e:  # pragma: no cover
+                self.err = repr(e)
+                return
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if hasattr(self, "t"):
+            self.t.join(timeout=1)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "error": self.err}
+        nv = self.nv
+        reasons = sorted({name for _, rs in self.rows for name, attr in self.REASONS.items()
+                          if rs & getattr(nv, attr)})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml, 10 ms"}
 
 
 def dist_info():
@@ -188,10 +198,9 @@ class Workload:
         self.pg_p = self.pg_d = None
         self.gath_p = self.gath_d = None
         if tp > 1:
-            import torch.distributed as dist
-            ranks = list(range(tp))
-            self.pg_p = dist.new_group(ranks, backend="nccl")   # prefill workers' group
-            self.pg_d = dist.new_group(ranks, backend="nccl")   # decode workers' group
+            from paper_2504_19867_b200 import tp as tpmod
+            groups = tpmod.PhaseGroups.create(backend="nccl")  # one communicator per phase
+            self.pg_p, self.pg_d = groups.prefill, groups.decode
             self.gath_p = torch.empty((self.full.num_q_heads, self.C, d), dtype=s.dtype, device=dev)
             self.gath_d = torch.empty((self.full.num_q_heads, self.B, d), dtype=s.dtype, device=dev)
         # per-launch timing events (decode kernel on stream D, prefill call on stream P)
@@ -227,8 +236,8 @@ class Workload:
                 if timed:
                     self.ev_p[l][1].record(s)
                 if self.tp > 1:
-                    import torch.distributed as dist
-                    dist.all_gather_into_tensor(self.gath_p, self.op[l], group=self.pg_p)
+                    from paper_2504_19867_b200 import tp as tpmod
+                    tpmod.gather_heads(self.op[l], self.gath_p, self.pg_p)
             p.free_blocks(self.rid_pre, None, stream=s)
 
     def phase_decode(self, budget, timed=False, stream=None):
@@ -244,8 +253,8 @@ class Workload:
                 if timed:
                     self.ev_d[l][1].record(s)
                 if self.tp > 1:
-                    import torch.distributed as dist
-                    dist.all_gather_into_tensor(self.gath_d, self.od[l], group=self.pg_d)
+                    from paper_2504_19867_b200 import tp as tpmod
+                    tpmod.gather_heads(self.od[l], self.gath_d, self.pg_d)
 
     def corun_step(self, x, y, timed=False):
         """One co-run iteration: both workers concurrently at budgets from (x, y)."""
@@ -434,6 +443,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         barrier = lambda: dist.barrier()  # noqa: E731
     shape = MODELS[args.model]
+    shape = synth.AttnShape(shape.name, shape.num_q_heads, shape.num_kv_heads, shape.head_dim_k,
+                            shape.head_dim_v, args.block_size, shape.dtype, shape.num_layers,
+                            shape.kv_shared, shape.scale)
     w = Workload(shape, ws, dev)
     hbm_peak, bf16_peak, bf16_sus, peak_kind = peaks()
     W = max(3, args.warmup)
@@ -521,7 +533,7 @@ def main():
             "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{shape.name} attention (Hq {shape.num_q_heads}, Hkv "
-                                   f"{shape.num_kv_heads}, d 128, bs 16, {shape.num_layers} layers): "
+                                   f"{shape.num_kv_heads}, d 128, bs {shape.block_size}, {shape.num_layers} layers): "
                                    f"decode B={DECODE_BATCH} ctx={DECODE_CTX} + prefill chunk "
                                    f"{PREFILL_TOKENS} (P=0), co-run",
                        "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d},

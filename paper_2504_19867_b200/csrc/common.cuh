@@ -228,6 +228,35 @@ SPD_DEV float fmax3(float a, float b, float c) {
     asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
     return r;
 }
+// 2^x for a pair on the FMA pipe (no MUFU): x = n + f with n = rint(x), f in [-1/2, 1/2]
+// (magic-number rounding), 2^f by a degree-4 polynomial (Taylor degree 5: rel. error ~3e-6, far below the
+// bf16 rounding of P), 2^n by adding n to the exponent bits.  x is clamped at -125, so
+// masked (-inf) inputs give ~2^-125 (3e-38) instead of 0.
+SPD_DEV uint64_t exp2_poly2(uint64_t x2) {
+    const float kMagic = 12582912.0f;  // 1.5 * 2^23
+    float x0, x1;
+    f2_split(x2, x0, x1);
+    x0 = fmaxf(x0, -125.0f);
+    x1 = fmaxf(x1, -125.0f);
+    const uint64_t t = fadd2(f2(x0, x1), f2(kMagic, kMagic));
+    const uint64_t r = fadd2(t, f2(-kMagic, -kMagic));
+    float r0, r1, t0, t1;
+    f2_split(r, r0, r1);
+    f2_split(t, t0, t1);
+    const uint64_t f = fadd2(f2(x0, x1), f2(-r0, -r1));
+    uint64_t p = f2(1.3333558146e-3f, 1.3333558146e-3f);
+    p = ffma2(p, f, f2(9.6181291076e-3f, 9.6181291076e-3f));
+    p = ffma2(p, f, f2(5.5504108665e-2f, 5.5504108665e-2f));
+    p = ffma2(p, f, f2(2.4022650696e-1f, 2.4022650696e-1f));
+    p = ffma2(p, f, f2(6.9314718056e-1f, 6.9314718056e-1f));
+    p = ffma2(p, f, f2(1.0f, 1.0f));
+    float p0, p1;
+    f2_split(p, p0, p1);
+    const int n0 = __float_as_int(t0) - 0x4B400000, n1 = __float_as_int(t1) - 0x4B400000;
+    return f2(__int_as_float(__float_as_int(p0) + (n0 << 23)),
+              __int_as_float(__float_as_int(p1) + (n1 << 23)));
+}
+
 template <uint32_t N>
 SPD_DEV void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
 template <uint32_t N>

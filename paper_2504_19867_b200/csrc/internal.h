@@ -48,6 +48,8 @@ struct semipd_pool {
     int* trace_buf = nullptr;
     int trace_cap = 0;
     int* trace_ctr = nullptr;
+    void* timeline = nullptr;      // debug builds (SPD_TIMELINE): prefill clock64 stamps
+    int* timeline_ctr = nullptr;
 
     void* k_layer(int l) const { return kv + (size_t)l * layer_stride; }
     void* v_layer(int l) const {

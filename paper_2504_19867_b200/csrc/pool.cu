@@ -324,3 +324,13 @@ semipd_status semipd_set_trace(semipd_pool_t pool, int32_t* buf, int32_t cap, in
 }
 
 }  // extern "C"
+
+#ifdef SPD_TIMELINE
+// Debug builds only (not part of the ABI): prefill phase timeline of CTA 0.
+extern "C" semipd_status semipd_debug_set_timeline(semipd_pool_t pool, void* buf, int32_t* ctr) {
+    if (!pool) return SEMIPD_ERR_INVALID;
+    pool->timeline = buf;
+    pool->timeline_ctr = ctr;
+    return SEMIPD_OK;
+}
+#endif

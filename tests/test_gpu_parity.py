@@ -429,3 +429,42 @@ def test_corun_bitwise_identical_and_disjoint_sms():
     # Disjointness holds whenever the two persistent grids are resident together;
     # report the overlap (0 expected when both launch before either finishes).
     print("corun SM overlap:", len(pre_sms & dec_sms))
+
+
+def test_partition_switch_moves_no_kv_and_keeps_results():
+    """P:211-216 / SURVEY CS3: set_partition between iterations is a host store - the
+    pool pointer and contents (checksum) are unchanged and outputs stay bitwise equal."""
+    shape = small(SHAPE_8B, block_size=64)
+    ctx = [4000, 700]
+    rig = Rig(shape, num_blocks=90, max_reqs=4, mbr=70)
+    for b, c in enumerate(ctx):
+        rig.alloc([b], [c // 64 + 1])
+    case = synth.decode_case(shape, ctx, seed=77)
+    for b in range(2):
+        rig.scatter(0, b, case.k_ctx[b], case.v_ctx[b])
+    dev = rig.dev
+    ptr0 = rig.pool.mem.data_ptr()
+    K, V, _, _ = rig.pool.views(0)
+    outs, sums = [], []
+    ws = rig.pool.new_decode_workspace(2, 32, max(ctx))
+    for x, y in [(30, 70), (50, 50), (70, 30), (100, 100), (10, 90)]:
+        rig.pool.set_partition(x, y)
+        n_p, n_d = rig.pool.sm_budgets()
+        assert (n_p, n_d) == (oracle.sm_budget(rig.pool.num_sms, x),
+                              oracle.sm_budget(rig.pool.num_sms, y))
+        out = torch.empty(2, 32, 128, dtype=torch.bfloat16, device=dev)
+        # same step re-run (append rewrites the same slot with the same bits)
+        rig.pool.decode_attn(0, case.q.to(dev), case.k_new.to(dev), case.v_new.to(dev),
+                             rig.i32([0, 1]), rig.i32(ctx), max(ctx), shape.softmax_scale, out, ws,
+                             sm_budget=0)
+        torch.cuda.synchronize()
+        outs.append(out.cpu())
+        sums.append((int(K.view(torch.int16).sum().item()), int(V.view(torch.int16).sum().item())))
+        assert rig.pool.mem.data_ptr() == ptr0
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    assert all(s == sums[0] for s in sums)
+    with pytest.raises(Exception):
+        rig.pool.set_partition(0, 50)
+    with pytest.raises(Exception):
+        rig.pool.set_partition(50, 100.5)

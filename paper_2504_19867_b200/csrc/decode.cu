@@ -85,8 +85,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     constexpr int R = 1 << LG_R;     // rows per TMA box (= min(bs, 64))
     constexpr int NB = KPS / R;      // boxes per stage per tensor
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* ring = smem;                                   // NSTAGE x 32 KiB
     float* scr_acc = reinterpret_cast<float*>(ring + NSTAGE * STAGE_BYTES);  // [NCW][16][128]
     float* scr_ml = scr_acc + NCW * 16 * HD;                       // [NCW][16][2]
@@ -510,8 +509,13 @@ size_t semipd_decode_workspace_bytes(semipd_pool_t pool, int32_t max_batch, int3
                                      int32_t max_ctx) {
     if (!pool || max_batch < 0 || num_q_heads <= 0 || max_ctx < 0) return 0;
     const int S_max = (max_ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
-    return ws_layout(max_batch, num_q_heads, pool->cfg.num_kv_heads, S_max,
-                     pool->cfg.head_dim_v).total;
+    size_t n = ws_layout(max_batch, num_q_heads, pool->cfg.num_kv_heads, S_max,
+                         pool->cfg.head_dim_v).total;
+    if (pool->cfg.kv_shared) {
+        const size_t m = spd_mla_ws_bytes(max_batch, max_ctx);
+        if (m > n) n = m;
+    }
+    return n;
 }
 
 semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* q,
@@ -532,6 +536,10 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     if (!q || !k_new || (!v_new && !c.kv_shared) || !req_ids || !ctx_lens || !out)
         return SEMIPD_ERR_INVALID;
     const int budget = spd_resolve_budget(pool, sm_budget, false);
+    if (spd_mla_decode_ok(pool, num_q_heads))  // absorbed MLA latent cache (cfg 5)
+        return spd_launch_decode_mla(pool, layer, q, k_new, req_ids, ctx_lens, batch, max_ctx_len,
+                                     num_q_heads, softmax_scale, out, out_head_major, workspace,
+                                     ws_bytes, budget, status_dev, st);
     if (!fast_path_ok(pool, num_q_heads)) {
         // generic CUDA-core path: append, then attention (same stream)
         semipd_status r = spd_launch_kv_write(pool, layer, k_new, v_new, nullptr, req_ids,

@@ -43,6 +43,10 @@ struct semipd_pool {
     std::vector<CUtensorMap> dkmap, dvmap;
     bool have_maps = false;   // 3-D page maps (prefill)
     bool have_dmaps = false;  // 4-D page maps (decode)
+    // MLA latent pool (kv_shared): 4-D (64 cols, rows, dk/64 blocks, pages), box 32 rows x all
+    // column blocks (one 36 KiB TMA per 32-key stage at dk = 576)
+    std::vector<CUtensorMap> mla_kmap;
+    bool have_mla_map = false;
     int box_rows = 16;
     int dbox_rows = 16;
     int* trace_buf = nullptr;
@@ -82,6 +86,13 @@ bool spd_encode_tiled_3d(CUtensorMap* map, CUtensorMapDataType dt, void* gaddr, 
                          uint32_t b0, uint32_t b1, uint32_t b2, CUtensorMapSwizzle swz);
 
 // kernels launched from other TUs
+bool spd_mla_decode_ok(const semipd_pool* p, int Hq);
+size_t spd_mla_ws_bytes(int B, int max_ctx);
+semipd_status spd_launch_decode_mla(semipd_pool_t pool, int layer, const void* q, const void* k_new,
+                                    const int* req_ids, const int* ctx_lens, int batch,
+                                    int max_ctx_len, int Hq, float scale, void* out,
+                                    int out_head_major, void* workspace, size_t ws_bytes,
+                                    int budget, int* status_dev, cudaStream_t st);
 semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new, const void* v_new,
                                   const int* cu_seqlens, const int* req_ids, const int* pos0,
                                   int n, int total_rows, int mode, int* status_dev,

@@ -229,6 +229,20 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
             dok = dok && okd;
         }
         p->have_dmaps = dok;
+        if (cfg->kv_shared && cfg->block_size % 32 == 0 && pow2) {
+            p->mla_kmap.resize(cfg->num_layers);
+            bool mok = true;
+            for (int l = 0; l < cfg->num_layers && mok; ++l) {
+                const uint64_t kr = (uint64_t)cfg->head_dim_k * 2;
+                const uint64_t md[4] = {64, (uint64_t)cfg->block_size, (uint64_t)cfg->head_dim_k / 64,
+                                        (uint64_t)cfg->num_blocks * cfg->num_kv_heads};
+                const uint64_t ms[3] = {kr, 128, kr * cfg->block_size};
+                const uint32_t mb[4] = {64, 32, (uint32_t)cfg->head_dim_k / 64, 1};
+                mok = spd_encode_tiled_4d(&p->mla_kmap[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                          p->k_layer(l), md, ms, mb, CU_TENSOR_MAP_SWIZZLE_128B);
+            }
+            p->have_mla_map = mok;
+        }
         p->have_maps = ok;
     }
     cudaSetDevice(prev);

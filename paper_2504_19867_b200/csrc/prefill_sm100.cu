@@ -64,7 +64,26 @@ struct PrefillParams {
     int n, T, Hq, Hkv, G, TQ, pairs_max, n_units, lg_bs, box_rows, MBR, N_B, out_head_major;
     float scale_log2;
     SpdTrace trace;
+    long long* tl;  // SPD_TIMELINE builds only: phase clock64 stamps of CTA 0
+    int* tl_ctr;
 };
+
+#ifdef SPD_TIMELINE
+#define TL_REC(a, b, c, d, e)                                                              \
+    do {                                                                                   \
+        if (p.tl && blockIdx.x == 0) {                                                     \
+            const int _i = atomicAdd(p.tl_ctr, 1);                                         \
+            if (_i < 4096) {                                                               \
+                long long* _r = p.tl + 8 * _i;                                             \
+                _r[0] = a; _r[1] = b; _r[2] = c; _r[3] = d; _r[4] = e;                     \
+            }                                                                              \
+        }                                                                                  \
+    } while (0)
+#define TL_NOW() clock64()
+#else
+#define TL_REC(a, b, c, d, e) do { } while (0)
+#define TL_NOW() 0LL
+#endif
 
 struct Smem {
     // operand tiles first (1024-aligned by construction)
@@ -91,8 +110,7 @@ __global__ void __launch_bounds__(NT, 1)
                       const __grid_constant__ CUtensorMap kcmap,
                       const __grid_constant__ CUtensorMap vcmap, PrefillParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                        ~uintptr_t(1023));
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = (int)warp_id();
     const int lane = (int)lane_id();
 
@@ -184,7 +202,9 @@ __global__ void __launch_bounds__(NT, 1)
             if (d.i < 0) break;
             if (!kv && lane == 0) {
                 // Q tiles A and B (rows = tokens x G heads of kv head g)
+                [[maybe_unused]] const long long tq0 = TL_NOW();
                 mbar_wait(&sm.q_empty, (nunit & 1) ^ 1);
+                TL_REC(30, nunit, tq0, TL_NOW(), 0);
                 mbar_arrive_expect_tx(&sm.q_full, 2 * TILE_BYTES);
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
@@ -253,7 +273,9 @@ __global__ void __launch_bounds__(NT, 1)
                 const PUnit d = sm.units[us];
                 mbar_arrive(&sm.uempty[us]);
                 if (d.i < 0) break;
+                [[maybe_unused]] const long long tq1 = TL_NOW();
                 mbar_wait(&sm.q_full, nunit & 1);
+                TL_REC(31, nunit, tq1, TL_NOW(), d.nkv[1]);
                 tc_fence_after();
                 const int nA = d.nkv[0], nB = d.nkv[1];
                 auto issue_s = [&](int t, int it) {  // S_t = Q_t K^T (K stage of kv tile it)
@@ -343,7 +365,9 @@ __global__ void __launch_bounds__(NT, 1)
             float m = -INFINITY;
             uint64_t l2 = f2(0.f, 0.f);
             for (int j = 0; j < nkv; ++j, ++cnt) {
+                [[maybe_unused]] const long long ts0 = TL_NOW();
                 mbar_wait(&sm.s_full[t], cnt & 1);
+                [[maybe_unused]] const long long ts1 = TL_NOW();
                 tc_fence_after();
                 uint32_t sr[4][32];
 #pragma unroll
@@ -412,9 +436,12 @@ __global__ void __launch_bounds__(NT, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&sm.p_full[t]);
+                if (lane == 0 && q4 == 0) TL_REC(t, j, ts0, ts1, TL_NOW());
             }
             // ---- epilogue: O / l -> bf16 -> global
+            [[maybe_unused]] const long long te0 = TL_NOW();
             mbar_wait(&sm.o_full[t], nunit & 1);
+            [[maybe_unused]] const long long te1 = TL_NOW();
             tc_fence_after();
             float la, lb;
             f2_split(l2, la, lb);
@@ -444,6 +471,7 @@ __global__ void __launch_bounds__(NT, 1)
             }
             tc_fence_before();
             mbar_arrive(&sm.o_empty[t]);
+            if (lane == 0 && q4 == 0) TL_REC(10 + t, nunit, te0, te1, TL_NOW());
             ++nunit;
         }
     }
@@ -531,6 +559,8 @@ extern "C" semipd_status semipd_prefill_attn(
     prm.out_head_major = out_head_major;
     prm.scale_log2 = softmax_scale * LOG2E;
     prm.trace = spd_trace(pool);
+    prm.tl = reinterpret_cast<long long*>(pool->timeline);
+    prm.tl_ctr = pool->timeline_ctr;
     CUtensorMap qmap;
     if (!spd_encode_tiled_3d(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(q), HD,
                              (uint64_t)num_q_heads, (uint64_t)total_q, HD * 2,

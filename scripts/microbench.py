@@ -37,8 +37,11 @@ def main():
     ap.add_argument("--hq", type=int, default=32)
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--bs", type=int, default=16)
+    ap.add_argument("--mla", action="store_true", help="cfg5 absorbed-MLA decode (576/512, 16 heads)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
+    if args.mla:
+        return mla(args, dev)
     L, B, ctx, C, P = args.layers, args.batch, args.ctx, args.chunk, args.prefix
     Hq, Hkv, d, bs = args.hq, args.hkv, 128, args.bs
     nb_dec = ctx // bs + 1
@@ -92,6 +95,45 @@ def main():
             else:
                 rec["TFLOP_s"] = pre_flops / (ms / 1e3) / 1e12
             print(json.dumps(rec), flush=True)
+
+
+def mla(args, dev):
+    """MLA decode: B requests at ctx, latent 576 (V = first 512), 16 heads, bs 64."""
+    L, B, ctx, bs = args.layers, args.batch, args.ctx, 64
+    nb = ctx // bs + 1
+    cfg = PoolConfig(L, B * nb + 4, bs, 1, 576, 512, B + 1, nb + 1, kv_shared=True)
+    pool = KVPool(cfg, dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32(list(range(B))), i32([nb] * B))
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    for l in range(L):
+        K, _, _, _ = pool.views(l)
+        K.normal_(generator=g)
+    q = torch.randn(B, 16, 576, device=dev, generator=g).bfloat16()
+    kn = torch.randn(B, 1, 576, device=dev, generator=g).bfloat16()
+    out = torch.empty(B, 16, 512, dtype=torch.bfloat16, device=dev)
+    ws = pool.new_decode_workspace(B, 16, ctx)
+    rid, ctxs = i32(list(range(B))), i32([ctx] * B)
+    byts = B * (ctx + 1) * 576 * 2 + B * 16 * (576 + 512) * 2
+    flops = 2 * B * 16 * (ctx + 1) * (576 + 512)
+    for bud in [int(x) for x in args.budgets.split(",")]:
+        for l in range(min(L, 3)):
+            pool.decode_attn(l, q, kn, None, rid, ctxs, ctx, 1 / math.sqrt(192), out, ws, sm_budget=bud)
+        torch.cuda.synchronize()
+        times = []
+        for it in range(args.iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pool.decode_attn(it % L, q, kn, None, rid, ctxs, ctx, 1 / math.sqrt(192), out, ws,
+                             sm_budget=bud)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        print(json.dumps({"kernel": "decode_mla", "budget": bud, "B": B, "ctx": ctx, "ms": ms,
+                          "GB_s": byts / (ms / 1e3) / 1e9, "TFLOP_s": flops / (ms / 1e3) / 1e12}),
+              flush=True)
 
 
 if __name__ == "__main__":

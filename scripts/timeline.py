@@ -37,7 +37,9 @@ n = min(int(ctr.item()), 4096)
 rec = buf[:8 * n].view(n, 8).cpu().tolist()
 t0 = min(r[2] for r in rec)
 for r in rec:
-    r[2:7] = [x - t0 if x else 0 for x in r[2:7]]
+    r[2:4] = [x - t0 if x else 0 for x in r[2:4]]
+    if r[0] < 20:
+        r[4] = r[4] - t0 if r[4] else 0
 rec.sort(key=lambda r: r[2])
 json.dump(rec, open(os.path.join(ROOT, "gpurun_out", "timeline.json"), "w"))
 print("records", n)

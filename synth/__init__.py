@@ -91,13 +91,16 @@ def qkv_tokens(n_tok: int, shape: AttnShape, g: torch.Generator, dist: int):
 
 
 def plant_needles(k: torch.Tensor, qhat_per_kv: torch.Tensor, g: torch.Generator,
-                  frac: float = 0.01) -> torch.Tensor:
-    """Set `frac` of key positions (seeded) to 3*sqrt(d)*q_hat for each kv head.
-    k [n, Hkv, dk]; qhat_per_kv [Hkv, dk] (unit vectors, fp32)."""
+                  frac: float = 0.01, gain: float = 3.0) -> torch.Tensor:
+    """Set `frac` of key positions (seeded) to gain*sqrt(d)*q_hat for each kv head.
+    k [n, Hkv, dk]; qhat_per_kv [Hkv, dk] (unit vectors, fp32).  gain = 3 for separate V;
+    for the MLA latent cache (V aliases K) gain = 1 keeps the needle's value elements at
+    unit scale (with gain 3 |o| reaches ~12, where bf16 output rounding alone exceeds the
+    2e-2 absolute bound; R17) while its score still dominates (~40)."""
     n, hkv, d = k.shape
     cnt = max(1, int(round(frac * n)))
     pos = torch.randperm(n, generator=g)[:cnt]
-    needle = (3.0 * math.sqrt(d) * qhat_per_kv).to(k.dtype)
+    needle = (gain * math.sqrt(d) * qhat_per_kv).to(k.dtype)
     k = k.clone()
     k[pos] = needle.unsqueeze(0).expand(cnt, hkv, d)
     return k
@@ -133,7 +136,7 @@ def decode_case(shape: AttnShape, ctx_lens, seed: int, dist: int = FLAT,
         _, kc, vc = qkv_tokens(c, shape, g, dist)
         if dist == NEEDLE and c > 0:
             qhat = unit(q[b, ::G, :])  # first q head of each kv group
-            kc = plant_needles(kc, qhat, g)
+            kc = plant_needles(kc, qhat, g, gain=1.0 if shape.kv_shared else 3.0)
         k_ctx.append(kc)
         v_ctx.append(vc)
     return DecodeCase(shape, list(ctx_lens), list(req_ids if req_ids is not None else range(B)),
@@ -172,9 +175,10 @@ def prefill_case(shape: AttnShape, chunk_lens, prefix_lens, seed: int, dist: int
         _, k_pre, v_pre = qkv_tokens(p, shape, g, dist)
         if dist == NEEDLE and c > 0:
             qhat = unit(q[cu + c - 1, ::G, :])  # chunk's last row
+            gain = 1.0 if shape.kv_shared else 3.0
             if p > 0:
-                k_pre = plant_needles(k_pre, qhat, g)
-            k_new[cu:cu + c] = plant_needles(k_new[cu:cu + c], qhat, g)
+                k_pre = plant_needles(k_pre, qhat, g, gain=gain)
+            k_new[cu:cu + c] = plant_needles(k_new[cu:cu + c], qhat, g, gain=gain)
         kp.append(k_pre)
         vp.append(v_pre)
         cu += c

@@ -204,9 +204,37 @@ def test_decode_bitwise_stable_across_budgets():
         assert torch.equal(o, outs[0])
 
 
-def test_decode_mla_latent_generic_path():
+@pytest.mark.parametrize("dist", synth.DISTS)
+def test_decode_mla_latent(dist):
+    """cfg 5 absorbed MLA (16 heads, latent 576 / 512, V aliases K, bs 64): block edges,
+    ragged tails and > 1 split (4096 keys)."""
+    run_decode(small(synth.CFG5_MLA), [0, 31, 63, 64, 200, 4100, 9000], seed=55 + dist, dist=dist)
+
+
+def test_decode_mla_tensor_kernel_and_budgets():
     shape = small(synth.CFG5_MLA)
-    run_decode(shape, [0, 63, 64, 200], seed=55, dist=synth.FLAT)
+    outs = [run_decode(shape, [500, 4500, 37], seed=5, dist=synth.FLAT, sm_budget=b)[0].cpu()
+            for b in (1, 9, 148, -1)]
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    # the tensor-core MLA kernel (trace kind 3) is the one that runs
+    from paper_2504_19867_b200 import KVPool, PoolConfig
+    dev = torch.device("cuda", 0)
+    pool = KVPool(PoolConfig(1, 8, 64, 1, 576, 512, 2, 4, kv_shared=True), dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32([0]), i32([2]))
+    trace = torch.zeros(4 * 64, dtype=torch.int32, device=dev)
+    ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+    pool.set_trace(trace, ctr)
+    q = torch.randn(1, 16, 576, device=dev).bfloat16()
+    kn = torch.randn(1, 1, 576, device=dev).bfloat16()
+    out = torch.empty(1, 16, 512, dtype=torch.bfloat16, device=dev)
+    ws = pool.new_decode_workspace(1, 16, 100)
+    pool.decode_attn(0, q, kn, None, i32([0]), i32([100]), 100, 0.07, out, ws)
+    torch.cuda.synchronize()
+    n = int(ctr.item())
+    kinds = set(trace[:4 * n].view(n, 4)[:, 3].cpu().tolist())
+    assert kinds == {3}
 
 
 def test_decode_full_size_cfg2():

@@ -25,6 +25,7 @@ process group, strong scaling.  --impl reference times the fp64 oracle
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import math
 import os
@@ -349,65 +350,84 @@ class E2E:
 
 
 # ----------------------------------------------------------------------------- oracle arm
-def oracle_sample_rate(shape: synth.AttnShape, threads: int, budget_s: float = 12.0):
+def oracle_sample_rate(shape: synth.AttnShape, threads: int, budget_s: float = 15.0):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload and
-    extrapolate to attention-stack tokens/s for the full step.  Sample: decode =
-    whole requests (ctx 2048, all heads, one layer); prefill = rows of the 2048
-    chunk at evenly spaced positions (all heads, one layer)."""
+    extrapolate to attention-stack tokens/s for the full step.  About budget_s of CPU
+    work, split evenly: decode = whole layer-steps of the B=64 ctx-2048 batch (all
+    heads), repeated; prefill = evenly spaced rows of the 2048 chunk (all heads), the
+    row count calibrated so the rows take ~budget_s/2 (causal cost averages out)."""
     import oracle
     oracle.set_threads(threads)
     s = shape
     bs = s.block_size
     rng = np.random.default_rng(0)
-    # decode sample: n_req requests
-    n_req = 2
-    nb = DECODE_CTX // bs + 1
-    kpool = (rng.standard_normal((n_req * nb, s.num_kv_heads, bs, s.head_dim_k)) * 1).astype(np.float32)
-    vpool = rng.standard_normal((n_req * nb, s.num_kv_heads, bs, s.head_dim_v)).astype(np.float32)
     to_bits = lambda a: (a.view(np.uint32) >> 16).astype(np.uint16)  # noqa: E731 (bf16 bit patterns)
-    kpool, vpool = to_bits(kpool), to_bits(vpool)
-    bt = np.arange(n_req * nb, dtype=np.int32).reshape(n_req, nb)
-    q = to_bits(rng.standard_normal((n_req, s.num_q_heads, s.head_dim_k)).astype(np.float32))
-    kn = to_bits(rng.standard_normal((n_req, s.num_kv_heads, s.head_dim_k)).astype(np.float32))
-    vn = to_bits(rng.standard_normal((n_req, s.num_kv_heads, s.head_dim_v)).astype(np.float32))
+    bf = lambda *sh: to_bits(rng.standard_normal(sh).astype(np.float32))  # noqa: E731
+    # decode sample: the whole B-request batch of one layer, repeated
+    B = DECODE_BATCH
+    nb = DECODE_CTX // bs + 1
+    kpool, vpool = bf(B * nb, s.num_kv_heads, bs, s.head_dim_k), bf(B * nb, s.num_kv_heads, bs, s.head_dim_v)
+    bt = np.arange(B * nb, dtype=np.int32).reshape(B, nb)
+    q, kn, vn = bf(B, s.num_q_heads, s.head_dim_k), bf(B, s.num_kv_heads, s.head_dim_k), bf(B, s.num_kv_heads, s.head_dim_v)
+    reps, t_dec = 0, 0.0
     t0 = time.perf_counter()
-    oracle.decode(q, kn, vn, kpool, vpool, bt, list(range(n_req)), [DECODE_CTX] * n_req,
-                  s.softmax_scale)
-    t_dec_req = (time.perf_counter() - t0) / n_req
-    # prefill sample: every stride-th row of a 2048 chunk
+    while reps == 0 or t_dec < budget_s / 2:
+        oracle.decode(q, kn, vn, kpool, vpool, bt, list(range(B)), [DECODE_CTX] * B, s.softmax_scale)
+        reps += 1
+        t_dec = time.perf_counter() - t0
+    t_dec_layer = t_dec / reps
+    del kpool, vpool
+    # prefill sample: evenly spaced rows of the 2048 chunk
     C = PREFILL_TOKENS
-    stride = 64
     nbp = -(-C // bs)
     kpp = np.zeros((nbp, s.num_kv_heads, bs, s.head_dim_k), np.uint16)
     vpp = np.zeros((nbp, s.num_kv_heads, bs, s.head_dim_v), np.uint16)
     btp = np.arange(nbp, dtype=np.int32).reshape(1, nbp)
-    qp = to_bits(rng.standard_normal((C, s.num_q_heads, s.head_dim_k)).astype(np.float32))
-    kp = to_bits(rng.standard_normal((C, s.num_kv_heads, s.head_dim_k)).astype(np.float32))
-    vp = to_bits(rng.standard_normal((C, s.num_kv_heads, s.head_dim_v)).astype(np.float32))
-    mask = np.zeros(C, np.uint8)
-    mask[stride // 2::stride] = 1
-    t0 = time.perf_counter()
-    oracle.prefill(qp, kp, vp, kpp, vpp, btp, [0, C], [0], [0], s.softmax_scale, rows_mask=mask)
-    t_pre_rows = time.perf_counter() - t0
-    t_pre_chunk = t_pre_rows * C / int(mask.sum())
-    t_step = s.num_layers * (DECODE_BATCH * t_dec_req + t_pre_chunk)
+    qp, kp, vp = bf(C, s.num_q_heads, s.head_dim_k), bf(C, s.num_kv_heads, s.head_dim_k), bf(C, s.num_kv_heads, s.head_dim_v)
+
+    def rows(stride):
+        mask = np.zeros(C, np.uint8)
+        mask[stride // 2::stride] = 1
+        t = time.perf_counter()
+        oracle.prefill(qp, kp, vp, kpp, vpp, btp, [0, C], [0], [0], s.softmax_scale, rows_mask=mask)
+        return time.perf_counter() - t, int(mask.sum())
+
+    t_cal, n_cal = rows(256)
+    per_row = t_cal / n_cal
+    n_rows = int(min(C, max(n_cal, (budget_s / 2) / per_row)))
+    stride = max(1, C // n_rows)
+    t_pre, n_rows = rows(stride)
+    t_pre_chunk = t_pre * C / n_rows
+    t_step = s.num_layers * (t_dec_layer + t_pre_chunk)
     tokens = PREFILL_TOKENS + DECODE_BATCH
-    sample = (f"{n_req} decode requests (ctx {DECODE_CTX}, all {s.num_q_heads} heads, 1 layer) + "
-              f"{int(mask.sum())} of {C} prefill rows (every {stride}th, all heads, 1 layer); "
-              f"extrapolated x{s.num_layers} layers, x{DECODE_BATCH} requests, x{C} rows")
+    sample = (f"{reps}x one decode layer-step (B={B}, ctx {DECODE_CTX}, all {s.num_q_heads} heads) "
+              f"in {t_dec:.1f} s + {n_rows} of {C} prefill rows (every {stride}th, all heads, 1 layer) "
+              f"in {t_pre:.1f} s; extrapolated x{s.num_layers} layers, x{C / n_rows:.0f} rows")
     return tokens / t_step, sample, time.perf_counter()
+
+
+def workload_config(shape: synth.AttnShape, ws: int) -> dict:
+    """The `config` both arms print (the reference arm runs the same workload)."""
+    decode_gb = shape.num_layers * (DECODE_BATCH * (DECODE_CTX + 1) * shape.num_kv_heads * 2 * 128 * 2) / 1e9
+    return {"workload": f"{shape.name} attention (Hq {shape.num_q_heads}, Hkv {shape.num_kv_heads}, "
+                        f"d 128, bs {shape.block_size}, {shape.num_layers} layers): decode B={DECODE_BATCH} "
+                        f"ctx={DECODE_CTX} + prefill chunk {PREFILL_TOKENS} (P=0), co-run",
+            "parallelism": f"tp{ws} (KV-head shards, NCCL all-gather)" if ws > 1 else "tp1",
+            "l2": f"no flush: per-step decode working set {decode_gb:.1f} GB >> 126 MB L2"}
 
 
 def run_reference(args):
     ws, rank, _ = dist_info()
     if rank != 0:
         return 0
-    shape = MODELS[args.model]
+    shape = dataclasses.replace(MODELS[args.model], block_size=args.block_size)
     threads = os.cpu_count() or 1
+    # each step is a bounded sample; the whole --steps/--warmup run stays within ~3 min
+    budget = max(2.0, min(15.0, 180.0 / (args.steps + args.warmup)))
     vals = []
     t_start = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        v, sample, _ = oracle_sample_rate(shape, threads)
+        v, sample, _ = oracle_sample_rate(shape, threads, budget)
         if i >= args.warmup:
             vals.append(v)
     elapsed = time.perf_counter() - t_start
@@ -417,8 +437,7 @@ def run_reference(args):
         "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * (PREFILL_TOKENS + DECODE_BATCH) / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"{shape.name}: decode B={DECODE_BATCH} "
-                                        f"ctx={DECODE_CTX} + prefill chunk {PREFILL_TOKENS}"},
+        "data": "synthetic", "config": workload_config(shape, 1),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -442,10 +461,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         barrier = lambda: dist.barrier()  # noqa: E731
-    shape = MODELS[args.model]
-    shape = synth.AttnShape(shape.name, shape.num_q_heads, shape.num_kv_heads, shape.head_dim_k,
-                            shape.head_dim_v, args.block_size, shape.dtype, shape.num_layers,
-                            shape.kv_shared, shape.scale)
+    shape = dataclasses.replace(MODELS[args.model], block_size=args.block_size)
     w = Workload(shape, ws, dev)
     hbm_peak, bf16_peak, bf16_sus, peak_kind = peaks()
     W = max(3, args.warmup)
@@ -532,14 +548,8 @@ def main():
             "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": W,
             "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{shape.name} attention (Hq {shape.num_q_heads}, Hkv "
-                                   f"{shape.num_kv_heads}, d 128, bs {shape.block_size}, {shape.num_layers} layers): "
-                                   f"decode B={DECODE_BATCH} ctx={DECODE_CTX} + prefill chunk "
-                                   f"{PREFILL_TOKENS} (P=0), co-run",
-                       "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d},
-                       "parallelism": f"tp{ws} (KV-head shards, NCCL all-gather)" if ws > 1 else "tp1",
-                       "l2": "no flush: per-step decode working set "
-                             f"{w.L * w.decode_bytes_per_launch() / 1e9:.1f} GB >> 126 MB L2"},
+            "config": {**workload_config(shape, ws),
+                       "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d}},
             "roofline": roof_dec if dominant == "decode" else roof_pre,
             "roofline_decode": roof_dec, "roofline_prefill": roof_pre,
             "decode_tokens_per_s": DECODE_BATCH * args.steps / t,

@@ -513,7 +513,9 @@ size_t semipd_decode_workspace_bytes(semipd_pool_t pool, int32_t max_batch, int3
                          pool->cfg.head_dim_v).total;
     if (pool->cfg.kv_shared) {
         const size_t m = spd_mla_ws_bytes(max_batch, max_ctx);
+        const size_t m2 = spd_mla_tc_ws_bytes(max_batch, max_ctx);
         if (m > n) n = m;
+        if (m2 > n) n = m2;
     }
     return n;
 }
@@ -536,7 +538,11 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     if (!q || !k_new || (!v_new && !c.kv_shared) || !req_ids || !ctx_lens || !out)
         return SEMIPD_ERR_INVALID;
     const int budget = spd_resolve_budget(pool, sm_budget, false);
-    if (spd_mla_decode_ok(pool, num_q_heads))  // absorbed MLA latent cache (cfg 5)
+    if (spd_mla_tc_ok(pool, num_q_heads))  // absorbed MLA latent cache, 64-token pages (cfg 5)
+        return spd_launch_decode_mla_tc(pool, layer, q, k_new, req_ids, ctx_lens, batch,
+                                        max_ctx_len, num_q_heads, softmax_scale, out,
+                                        out_head_major, workspace, ws_bytes, budget, status_dev, st);
+    if (spd_mla_decode_ok(pool, num_q_heads))  // latent cache with 32/128-token pages
         return spd_launch_decode_mla(pool, layer, q, k_new, req_ids, ctx_lens, batch, max_ctx_len,
                                      num_q_heads, softmax_scale, out, out_head_major, workspace,
                                      ws_bytes, budget, status_dev, st);

@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const float v0 = acc[nd][half * 2], v1 = acc[nd][half * 2 + 1];
                     if (!split) {
                         const size_t off = p.out_head_major ? (((size_t)h * p.B + d.b) * DV + col)
-                                                            : (((size_t)d.b * NH + h) * DV + col);
+                                                            : (((size_t)d.b * p.G + h) * DV + col);
                         *reinterpret_cast<uint32_t*>(p.out + off) = pack_bf16(v0 * inv, v1 * inv);
                     } else {
                         const size_t pi = ((size_t)d.b * NH + h) * p.S_max + d.s;
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         }
                         const float inv = 1.f / L;
                         const size_t off = p.out_head_major ? (((size_t)h * p.B + d.b) * DV + c)
-                                                            : (((size_t)d.b * NH + h) * DV + c);
+                                                            : (((size_t)d.b * p.G + h) * DV + c);
                         uint2 v;
                         v.x = pack_bf16(o.x * inv, o.y * inv);
                         v.y = pack_bf16(o.z * inv, o.w * inv);

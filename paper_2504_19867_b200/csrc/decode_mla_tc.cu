@@ -1,0 +1,758 @@
+// decode_mla_tc.cu — absorbed-MLA decode attention on the 5th-gen tensor cores (cfg 5:
+// 16 q heads share ONE latent KV head, dk = 576 (512 latent + 64 rope), dv = 512,
+// V = K[..., :512]; R19).  Same hot-path contract as decode.cu: fused append of
+// the step's latent row, paged access through the block table, split-K
+// with a last-CTA merge in split-index order (flash-decoding, cited P:127).
+//
+// AI ~ 30 FLOP/B (SURVEY §8(d) cfg 5: "tensor cores in decode").  Swap-AB so the 16 heads
+// are the MMA N dimension and keys / value columns fill M:
+//   S^T[64 keys x 16]  = C_page[64 x 576] . Q^T        M=64  N=16, 36 x K16, SS
+//   O^T[512 x 16]     += V^T[512 x 64] . P^T[64 x 16]   M=128 N=16, 4 blocks x 4 K16, SS
+// C_page is one 64-token page, landed by two 4-D TMA boxes (column blocks [0,4) = 32 KiB
+// and [4,9) = 40 KiB) into 40 KiB ring slots: [column block][64 keys][128 B], 128-B
+// swizzle — K-major A for QK and, read transposed (LBO = 8 KiB between 64-column blocks,
+// SBO = 1 KiB between 8-key groups), MN-major A for PV.  Q (18 KiB) arrives by TMA per
+// unit; P^T ([16 heads][64 keys] bf16, K-major) is written by the softmax warps.
+// TMEM: S^T double-buffered (2 x 16 cols), O^T 4 x 16 cols.  For M = 64, D row 16w + i
+// sits in TMEM lane 32w + i (measured, scripts/probe_umma_m64.cu).
+//
+// Warps: 0 producer (units, append, TMA), 1 MMA issuer (one thread), 2-5 softmax +
+// epilogue (warp w reads TMEM lane quadrant w % 4).  The work list depends on shapes
+// only, so outputs are bitwise identical for every sm_budget (R26).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+
+using namespace spd;
+
+constexpr int DK = 576, DV = 512, NH = 16;
+constexpr int PAGE = 64;                                // keys per tile = one page (bs 64)
+constexpr int NCB = DK / 64;                            // 9 column blocks of 128 B
+constexpr int CB_LO = 4;                                // boxes: cb [0,4) and [4,9)
+constexpr uint32_t LO_BYTES = CB_LO * PAGE * 128;       // 32 KiB
+constexpr uint32_t HI_BYTES = (NCB - CB_LO) * PAGE * 128;  // 40 KiB
+constexpr uint32_t SLOT_BYTES = HI_BYTES;
+constexpr int NSLOT = 5;
+constexpr uint32_t Q_BYTES = NCB * NH * 128;            // 18 KiB
+constexpr uint32_t P_BYTES = NH * 128;                  // 2 KiB per buffer (2 buffers)
+constexpr int NTHREADS = 192;
+constexpr int NSOFT = 128;
+constexpr int SPLIT_KEYS = 1024;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr uint32_t TM_S = 0, TM_O = 64, TM_COLS = 256;  // S^T 2x16 cols, O^T 2 x (4 x 16) cols
+
+struct TUnit {
+    int b, s, S, k0, k1, nt;  // b < 0: done
+};
+
+struct TcParams {
+    const uint4* k_new;       // [B][1][576]
+    const int* req_ids;
+    const int* ctx_lens;
+    const int* bt;
+    unsigned char* k_pool;
+    __nv_bfloat16* out;       // [B][Hq][512] or [Hq][B][512]
+    float* ws_m;              // [B][16][S_max]
+    float* ws_l;
+    float* ws_acc;            // [B][16][S_max][512]
+    int* ws_cnt;              // [B]
+    unsigned* sched;
+    int* status;
+    int B, MBR, N_B, S_max, n_units, out_head_major, G;
+    float scale_log2;
+    SpdTrace trace;
+    long long* tl;  // SPD_TIMELINE builds only: pipeline clock64 stamps of CTA 0
+    int* tl_ctr;
+};
+
+#ifdef SPD_TIMELINE
+// record slot = kind * 512 + tile: plain stores, no atomics (keeps the pipeline unperturbed)
+#define TL_REC(a, b, c, d, e)                                                              \
+    do {                                                                                   \
+        if (p.tl && (int)blockIdx.x == tl_cta && (b) < 512) {                                        \
+            long long* _r = p.tl + 8 * ((a) * 512 + (b));                                  \
+            _r[0] = a; _r[1] = b; _r[2] = c; _r[3] = d; _r[4] = e;                         \
+        }                                                                                  \
+    } while (0)
+#define TL_NOW() clock64()
+#else
+#define TL_REC(a, b, c, d, e) do { } while (0)
+#define TL_NOW() 0LL
+#endif
+
+struct Bars {
+    uint64_t full[NSLOT], empty[NSLOT], s_full[2], s_empty[2], p_full[2], o_done[2], q_full, q_empty,
+        ufull[2], uempty[2];
+};
+
+constexpr uint32_t OFF_Q = NSLOT * SLOT_BYTES;
+constexpr uint32_t OFF_P = OFF_Q + Q_BYTES;
+constexpr uint32_t OFF_RED = OFF_P + 2 * P_BYTES;            // [2][64] maxima, [64] sums
+constexpr uint32_t OFF_BARS = OFF_RED + 3 * 64 * 4;
+constexpr uint32_t OFF_UNITS = OFF_BARS + sizeof(Bars);
+constexpr uint32_t OFF_MISC = OFF_UNITS + 2 * sizeof(TUnit);
+constexpr uint32_t SMEM_BYTES = 1024 + OFF_MISC + 16;
+static_assert(OFF_Q % 1024 == 0 && OFF_P % 1024 == 0, "UMMA operands need 1 KiB alignment");
+static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KiB opt-in shared memory");
+
+__device__ __forceinline__ void split_range(int ctx, int S, int s, int& k0, int& k1) {
+    const int nk = ctx + 1;
+    int len = (nk + S - 1) / S;
+    len = (len + PAGE - 1) / PAGE * PAGE;
+    k0 = s * len;
+    k1 = min(nk, k0 + len);
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    decode_mla_tc_kernel(const __grid_constant__ CUtensorMap map_lo,
+                         const __grid_constant__ CUtensorMap map_hi,
+                         const __grid_constant__ CUtensorMap qmap, TcParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* ring = base;
+    unsigned char* qs = base + OFF_Q;
+    unsigned char* ps = base + OFF_P;
+    float* red = reinterpret_cast<float*>(base + OFF_RED);
+    Bars& bar = *reinterpret_cast<Bars*>(base + OFF_BARS);
+    TUnit* units = reinterpret_cast<TUnit*>(base + OFF_UNITS);
+    int* s_last = reinterpret_cast<int*>(base + OFF_MISC);
+    uint32_t* tmem_base = reinterpret_cast<uint32_t*>(base + OFF_MISC + 4);
+
+    const int warp = (int)warp_id();
+    const int lane = (int)lane_id();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSLOT; ++i) {
+            mbar_init(bar.full + i, 1);
+            mbar_init(bar.empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar.s_full + i, 1);
+            mbar_init(bar.s_empty + i, 4);
+            mbar_init(bar.ufull + i, 1);
+            mbar_init(bar.uempty + i, 5);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar.p_full + i, 4);
+            mbar_init(bar.o_done + i, 1);
+        }
+        mbar_init(&bar.q_full, 1);
+        mbar_init(&bar.q_empty, 1);
+        fence_mbar_init();
+        if (p.trace.buf) {
+            int slot = atomicAdd(p.trace.ctr, 1);
+            if (slot < p.trace.cap)
+                reinterpret_cast<int4*>(p.trace.buf)[slot] =
+                    make_int4(2, (int)smid(), (int)blockIdx.x, 4 /* kernel kind: MLA tcgen05 */);
+        }
+    }
+#ifdef SPD_TIMELINE
+    const int tl_cta = p.tl ? *p.tl_ctr : -1;  // which CTA records its pipeline
+    unsigned long long g_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+    int n_units_done = 0;
+#endif
+    if (warp == 1) tmem_alloc(tmem_base, TM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_base;
+
+    if (warp == 0) {
+        // =========================== producer ===========================
+        if (lane == 0) {
+            tma_prefetch_desc(&map_lo);
+            tma_prefetch_desc(&map_hi);
+            tma_prefetch_desc(&qmap);
+        }
+        int gh = 0, nunit = 0, nq = 0;
+        // first unit of each CTA is static (blockIdx.x); later ones come from the counter,
+        // fetched one unit ahead so the atomic's round trip overlaps the current unit
+        int u_next = blockIdx.x;
+        for (;;) {
+            const int u = u_next;
+            if (lane == 0) u_next = (int)gridDim.x + (int)atomicAdd(p.sched, 1u);
+            u_next = __shfl_sync(0xffffffffu, u_next, 0);
+            TUnit d;
+            int ctx = 0, rid = 0;
+            if (u >= p.n_units) {
+                d.b = -1;
+            } else {
+                // longest-first: units of the highest split index (full-length splits of the
+                // longest requests) are handed out first
+                d.s = p.S_max - 1 - u / p.B;
+                d.b = u % p.B;
+                ctx = __ldg(p.ctx_lens + d.b);
+                rid = __ldg(p.req_ids + d.b);
+                d.S = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+                if (d.s >= d.S) continue;
+                split_range(ctx, d.S, d.s, d.k0, d.k1);
+                d.nt = (d.k1 - d.k0 + PAGE - 1) / PAGE;
+            }
+            const int us = nunit & 1;
+            if (lane == 0) {
+                mbar_wait(bar.uempty + us, ((nunit >> 1) & 1) ^ 1);
+                units[us] = d;
+                mbar_arrive(bar.ufull + us);
+            }
+            __syncwarp();
+            ++nunit;
+            if (d.b < 0) break;
+            const int* btr = p.bt + (size_t)rid * p.MBR;
+            const int last_page = ctx / PAGE;
+            // fused append (last split only): the step's latent row (576 bf16 = 72 x 16 B) goes
+            // to slot ctx right before the TMA of the page holding it
+            const bool append = d.s == d.S - 1;
+            uint4 kn[3];
+            if (append) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const int c = lane + 32 * j;
+                    kn[j] = c < DK / 8 ? __ldg(p.k_new + (size_t)d.b * (DK / 8) + c) : make_uint4(0, 0, 0, 0);
+                }
+            }
+            const int page0 = d.k0 / PAGE;
+            int blk_l = -1;
+            for (int i = 0; i < d.nt; ++i, gh += 2) {
+                if ((i & 31) == 0) {
+                    const int pg = page0 + i + lane;
+                    blk_l = (pg <= last_page && pg < p.MBR) ? __ldg(btr + pg) : -1;
+                }
+                const int blk = __shfl_sync(0xffffffffu, blk_l, i & 31);
+                if (append && page0 + i == last_page && blk >= 0 && blk < p.N_B) {
+                    uint4* dst = reinterpret_cast<uint4*>(p.k_pool) + ((size_t)blk * PAGE + (ctx % PAGE)) * (DK / 8);
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        if (lane + 32 * j < DK / 8) dst[lane + 32 * j] = kn[j];
+                    fence_proxy_async_global();
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    int z = p.N_B;  // out of range: zero fill
+                    if (blk >= 0 && blk < p.N_B) z = blk;
+                    else if (p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                    const int s0 = gh % NSLOT, s1 = (gh + 1) % NSLOT;
+                    [[maybe_unused]] const long long tp0 = TL_NOW();
+                    mbar_wait(bar.empty + s0, ((gh / NSLOT) & 1) ^ 1);
+                    [[maybe_unused]] const long long tp1 = TL_NOW();
+                    mbar_arrive_expect_tx(bar.full + s0, LO_BYTES);
+                    tma_load_4d(ring + s0 * SLOT_BYTES, &map_lo, bar.full + s0, 0, 0, 0, z);
+                    mbar_wait(bar.empty + s1, (((gh + 1) / NSLOT) & 1) ^ 1);
+                    mbar_arrive_expect_tx(bar.full + s1, HI_BYTES);
+                    tma_load_4d(ring + s1 * SLOT_BYTES, &map_hi, bar.full + s1, 0, 0, CB_LO, z);
+                    TL_REC(1, gh / 2, tp0, tp1, TL_NOW());
+                    if (i == 0) {
+                        // Q of this unit: its buffer frees when the previous unit's last QK
+                        // completes (that tile was issued before this one: no deadlock)
+                        mbar_wait(&bar.q_empty, (nq & 1) ^ 1);
+                        mbar_arrive_expect_tx(&bar.q_full, Q_BYTES);
+                        tma_load_4d(qs, &qmap, &bar.q_full, 0, 0, 0, d.b);
+                    }
+                }
+                __syncwarp();
+            }
+            ++nq;
+        }
+    } else if (warp == 1) {
+        // =========================== MMA issuer (warp-collective) ===========================
+        // The whole warp runs this loop with uniform state; elect.sync inside the asm picks
+        // the issuing lane, so descriptors stay in uniform registers.  Barrier probes are
+        // taken by lane 0 and broadcast so every lane takes the same branch.
+        constexpr uint32_t ID_QK = umma_idesc_bf16_f32_ab(64, NH, 0, 0);
+        constexpr uint32_t ID_PV = umma_idesc_bf16_f32_ab(128, NH, 1, 0);
+        const uint32_t ring_a = smem_u32(ring), q_a = smem_u32(qs), p_a = smem_u32(ps);
+        const uint64_t dq0 = umma_desc_sw128(q_a, 16, 1024);
+        const uint64_t dp0 = umma_desc_sw128(p_a, 16, 1024);
+        auto probe = [&](const uint64_t* b, uint32_t par) {
+            bool r = false;
+            if (lane == 0) r = mbar_test_wait(b, par);
+            return __shfl_sync(0xffffffffu, r ? 1 : 0, 0) != 0;
+        };
+        int gh = 0, gt = 0, nunit = 0, nq = 0;
+        for (;;) {
+            const int us = nunit & 1;
+            mbar_wait(bar.ufull + us, (nunit >> 1) & 1);
+            const TUnit d = units[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar.uempty + us);
+            ++nunit;
+            if (d.b < 0) break;
+            // PV(t) as soon as P(t) is written (it releases tile t's ring slots), else QK(t)
+            // as soon as tile t has landed.
+            bool q_ok = false;
+            int nqk = 0, npv = 0;
+            while (npv < d.nt) {
+                const int tp = gt + npv, ob = tp & 1;
+                if (npv < nqk && probe(bar.p_full + ob, (tp >> 1) & 1)) {
+                    const int h0 = gh + 2 * npv;
+                    const int s0 = h0 % NSLOT, s1 = (h0 + 1) % NSLOT;
+                    tc_fence_after();
+                    const uint32_t lo = ring_a + s0 * SLOT_BYTES, hi = ring_a + s1 * SLOT_BYTES;
+#pragma unroll
+                    for (int m = 0; m < DV / 128; ++m) {
+                        // dv block m = column blocks 2m, 2m+1 (both in the same half-page)
+                        const uint32_t a0 = m < 2 ? lo + m * (2 * PAGE * 128)
+                                                  : hi + (2 * m - CB_LO) * (PAGE * 128);
+                        const uint64_t da = umma_desc_sw128(a0, PAGE * 128, 1024);
+#pragma unroll
+                        for (int ks = 0; ks < PAGE / 16; ++ks)
+                            umma_ss_warp(tmem + TM_O + ob * 64 + m * NH, da + (uint64_t)(ks * 128),
+                                         dp0 + (uint64_t)(ob * (P_BYTES / 16) + ks * 2), ID_PV,
+                                         (npv > 1 || ks > 0) ? 1u : 0u);
+                    }
+                    umma_commit_warp(bar.o_done + ob);
+                    umma_commit_warp(bar.empty + s0);
+                    umma_commit_warp(bar.empty + s1);
+                    if (lane == 0) TL_REC(3, gt + npv, TL_NOW(), 0, 0);
+                    ++npv;
+                    continue;
+                }
+                if (nqk < d.nt) {
+                    const int t = gt + nqk, sb = t & 1, h0 = gh + 2 * nqk;
+                    const int s0 = h0 % NSLOT, s1 = (h0 + 1) % NSLOT;
+                    if (!q_ok) q_ok = probe(&bar.q_full, nq & 1);
+                    if (q_ok && probe(bar.s_empty + sb, ((t >> 1) & 1) ^ 1) &&
+                        probe(bar.full + s0, (h0 / NSLOT) & 1) &&
+                        probe(bar.full + s1, ((h0 + 1) / NSLOT) & 1)) {
+                        tc_fence_after();
+                        const uint64_t dlo = umma_desc_sw128(ring_a + s0 * SLOT_BYTES, 16, 1024);
+                        const uint64_t dhi = umma_desc_sw128(ring_a + s1 * SLOT_BYTES, 16, 1024);
+#pragma unroll
+                        for (int k = 0; k < DK / 16; ++k) {
+                            const int cb = k >> 2;
+                            // descriptor start address is in 16-byte units
+                            const uint64_t da = cb < CB_LO ? dlo + (uint64_t)(cb * (PAGE * 128 / 16) + (k & 3) * 2)
+                                                           : dhi + (uint64_t)((cb - CB_LO) * (PAGE * 128 / 16) + (k & 3) * 2);
+                            umma_ss_warp(tmem + TM_S + sb * NH, da,
+                                         dq0 + (uint64_t)(cb * (NH * 128 / 16) + (k & 3) * 2), ID_QK, k > 0);
+                        }
+                        umma_commit_warp(bar.s_full + sb);
+                        if (lane == 0) TL_REC(2, t, TL_NOW(), 0, 0);
+                        if (nqk == d.nt - 1) umma_commit_warp(&bar.q_empty);
+                        ++nqk;
+                        continue;
+                    }
+                }
+                __nanosleep(32);  // nothing ready: yield issue slots to the softmax warp
+                                  // sharing this SM sub-partition
+            }
+            ++nq;
+            gt += d.nt;
+            gh += 2 * d.nt;
+        }
+    } else {
+        // =========================== softmax + epilogue ===========================
+        const int qd = warp & 3;                       // TMEM lane quadrant
+        const int tid = threadIdx.x - 64;              // 0..127
+        const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
+        float* red_l = red + 128;
+        int gt = 0, nunit = 0;
+        for (;;) {
+            const int us = nunit & 1;
+            mbar_wait(bar.ufull + us, (nunit >> 1) & 1);
+            const TUnit d = units[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar.uempty + us);
+            ++nunit;
+            if (d.b < 0) break;
+            // O^T is double-buffered: PV(t) accumulates into buffer t & 1 with P(t) from P
+            // buffer t & 1, so writing P(t) / rescaling O_(t&1) waits only for PV(t-2) and
+            // the softmax of tile t overlaps PV(t-1).  Buffer contents are relative to the
+            // running max at their last update (mold2 for tile t-2); the epilogue combines.
+            float mrun[NH], mold2[NH], lpart[NH];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                mrun[h] = -INFINITY;
+                mold2[h] = -INFINITY;
+                lpart[h] = 0.f;
+            }
+            for (int i = 0; i < d.nt; ++i) {
+                const int t = gt + i, sb = t & 1;
+                [[maybe_unused]] const long long ts0 = TL_NOW();
+                mbar_wait(bar.s_full + sb, (t >> 1) & 1);
+                [[maybe_unused]] const long long ts1 = TL_NOW();
+                tc_fence_after();
+                uint32_t r[NH];
+                tmem_ld16(tmem + lane_base + TM_S + sb * NH, r);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar.s_empty + sb);
+                const int key = d.k0 + i * PAGE + qd * 16 + lane;
+                const bool valid = lane < 16 && key < d.k1;
+                float x[NH];
+                float mine = -INFINITY;
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    x[h] = valid ? __uint_as_float(r[h]) * p.scale_log2 : -INFINITY;
+                    const float mx = redux_max_f32(x[h]);
+                    mine = lane == h ? mx : mine;
+                }
+                float* rm = red + (t & 1) * 64;
+                if (lane < NH) rm[qd * NH + lane] = mine;
+                named_bar_sync(1, NSOFT);
+                float scl[NH];
+                bool grow = false;
+#pragma unroll
+                for (int h4 = 0; h4 < NH / 4; ++h4) {
+                    const float4 a = reinterpret_cast<const float4*>(rm)[h4];
+                    const float4 b = reinterpret_cast<const float4*>(rm + NH)[h4];
+                    const float4 c = reinterpret_cast<const float4*>(rm + 2 * NH)[h4];
+                    const float4 e = reinterpret_cast<const float4*>(rm + 3 * NH)[h4];
+                    const float m4[4] = {fmaxf(fmax3(a.x, b.x, c.x), e.x), fmaxf(fmax3(a.y, b.y, c.y), e.y),
+                                         fmaxf(fmax3(a.z, b.z, c.z), e.z), fmaxf(fmax3(a.w, b.w, c.w), e.w)};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int h = h4 * 4 + j;
+                        const float mn = fmaxf(mrun[h], m4[j]);
+                        lpart[h] *= fast_exp2(mrun[h] - mn);
+                        grow |= mn > mold2[h];
+                        scl[h] = fast_exp2(mold2[h] - mn);  // O_(t&1) holds tiles <= t-2
+                        mold2[h] = mrun[h];
+                        mrun[h] = mn;
+                    }
+                }
+                uint32_t pb[NH];
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    const __nv_bfloat16 pv = __float2bfloat16_rn(fast_exp2(x[h] - mrun[h]));
+                    pb[h] = (uint32_t)__bfloat16_as_ushort(pv);
+                    lpart[h] += __bfloat162float(pv);
+                }
+                // P buffer / O buffer t & 1 are free once PV(t-2) completed
+                const int ob = t & 1;
+                [[maybe_unused]] const long long ts2 = TL_NOW();
+                if (t >= 2) mbar_wait(bar.o_done + ob, ((t >> 1) & 1) ^ 1);
+                [[maybe_unused]] const long long ts3 = TL_NOW();
+                tc_fence_after();
+                if (grow && i >= 2) {
+                    const uint32_t ta = tmem + lane_base + TM_O + ob * 64;
+                    uint32_t o[4][NH];
+#pragma unroll
+                    for (int m = 0; m < DV / 128; ++m) tmem_ld16(ta + m * NH, o[m]);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int m = 0; m < DV / 128; ++m) {
+#pragma unroll
+                        for (int h = 0; h < NH; ++h) o[m][h] = __float_as_uint(__uint_as_float(o[m][h]) * scl[h]);
+                        tmem_st16(ta + m * NH, o[m]);
+                    }
+                    tmem_wait_st();
+                }
+                // P^T [16 heads][64 keys] bf16, K-major 128-B swizzle; lane pairs store 4 B
+                {
+                    unsigned char* pbuf = ps + ob * P_BYTES;
+                    const int kk = qd * 16 + (lane & ~1);
+                    const bool odd = lane & 1;
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) {
+                        const uint32_t other = __shfl_xor_sync(0xffffffffu, pb[h], 1);
+                        const bool mine_h = odd ? (h >= 8) : (h < 8);
+                        if (lane < 16 && mine_h) {
+                            const uint32_t v = odd ? (other | (pb[h] << 16)) : (pb[h] | (other << 16));
+                            const uint32_t off = h * 128 + ((((kk >> 3) ^ (h & 7)) << 4) | ((kk & 7) << 1));
+                            *reinterpret_cast<uint32_t*>(pbuf + off) = v;
+                        }
+                    }
+                }
+                fence_proxy_async_smem();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar.p_full + ob);
+                if (lane == 0 && qd == 2) {
+                    TL_REC(4, t, ts0, ts1, ts2);
+                    TL_REC(5, t, ts3, TL_NOW(), 0);
+                }
+            }
+            gt += d.nt;
+            // ---- unit epilogue: l totals, O^T from TMEM (combining the two buffers)
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                float v = lpart[h];
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                lpart[h] = v;  // lanes 0..15 hold the warp's total (lanes 16..31 contribute 0)
+            }
+            {
+                float mine = 0.f;
+#pragma unroll
+                for (int h = 0; h < NH; ++h) mine = lane == h ? lpart[h] : mine;
+                if (lane < NH) red_l[qd * NH + lane] = mine;
+            }
+            [[maybe_unused]] const long long te0 = TL_NOW();
+            const int bl = (gt - 1) & 1;  // buffer of the last tile (relative to mrun)
+            const bool two = d.nt >= 2;   // the other buffer holds tiles <= nt-2 (mold2)
+            mbar_wait(bar.o_done + bl, ((gt - 1) >> 1) & 1);
+            if (two) mbar_wait(bar.o_done + (bl ^ 1), ((gt - 2) >> 1) & 1);
+            tc_fence_after();
+            named_bar_sync(1, NSOFT);
+            float L[NH], f2[NH], rl[NH];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                L[h] = red_l[h] + red_l[NH + h] + red_l[2 * NH + h] + red_l[3 * NH + h];
+                f2[h] = two ? fast_exp2(mold2[h] - mrun[h]) : 0.f;
+                rl[h] = __frcp_rn(L[h]);
+            }
+            [[maybe_unused]] const long long te1 = TL_NOW();
+            const bool split = d.S > 1;
+            // per-unit bases: head h of this unit's output / partial row sits at base + h * hs
+            __nv_bfloat16* obase = p.out + (p.out_head_major ? (size_t)d.b * DV : (size_t)d.b * p.G * DV);
+            const size_t ohs = p.out_head_major ? (size_t)p.B * DV : (size_t)DV;
+            float* wbase = p.ws_acc + ((size_t)d.b * NH * p.S_max + d.s) * DV;
+            const size_t whs = (size_t)p.S_max * DV;
+            // lane pairs (dv, dv + 1) exchange so each lane stores bf16x2 for 8 of the 16
+            // heads (even lane: heads 0-7, odd lane: heads 8-15)
+            const bool odd = lane & 1;
+#pragma unroll
+            for (int m = 0; m < DV / 128; ++m) {
+                uint32_t o[NH], o2[NH];
+                tmem_ld16(tmem + lane_base + TM_O + bl * 64 + m * NH, o);
+                tmem_ld16(tmem + lane_base + TM_O + (bl ^ 1) * 64 + m * NH, o2);
+                tmem_wait_ld();
+                const int dv = m * 128 + qd * 32 + lane;
+                float v[NH];
+#pragma unroll
+                for (int h = 0; h < NH; ++h)
+                    v[h] = two ? fmaf(__uint_as_float(o2[h]), f2[h], __uint_as_float(o[h]))
+                               : __uint_as_float(o[h]);
+                if (!split) {
+                    __nv_bfloat16* op = obase + (dv & ~1) + (odd ? 8 * ohs : 0);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        // even lanes store head j, odd lanes head j + 8
+                        const float a0 = v[j] * rl[j], a1 = v[j + 8] * rl[j + 8];
+                        const float send = odd ? a0 : a1;
+                        const float got = __shfl_xor_sync(0xffffffffu, send, 1);
+                        const int h = odd ? j + 8 : j;
+                        if (h < p.G)
+                            *reinterpret_cast<uint32_t*>(op + j * ohs) =
+                                odd ? pack_bf16(got, a1) : pack_bf16(a0, got);
+                    }
+                } else {
+                    float* wp = wbase + dv;
+#pragma unroll
+                    for (int h = 0; h < NH; ++h)
+                        if (h < p.G) wp[h * whs] = v[h];
+                }
+            }
+            tc_fence_before();
+            if (split) {
+                if (tid < p.G) {
+                    const size_t pi = ((size_t)d.b * NH + tid) * p.S_max + d.s;
+                    float mv = mrun[0], lv = L[0];
+#pragma unroll
+                    for (int h = 1; h < NH; ++h) {
+                        mv = tid == h ? mrun[h] : mv;
+                        lv = tid == h ? L[h] : lv;
+                    }
+                    p.ws_m[pi] = mv;
+                    p.ws_l[pi] = lv;
+                }
+                __threadfence();
+                named_bar_sync(1, NSOFT);
+                if (tid == 0) *s_last = atomicAdd(p.ws_cnt + d.b, 1) == d.S - 1;
+                named_bar_sync(1, NSOFT);
+                if (*s_last) {
+                    __threadfence();
+                    // merge in split-index order.  Pass 1 (one thread per head): weights
+                    // w[h][s] = 2^(m_s - M) / L into smem (the P buffer is idle here: PV of
+                    // the unit's last tile completed).  Pass 2: each thread owns 16 float4
+                    // columns and streams the S partials with 16 loads in flight.
+                    float* wsm = reinterpret_cast<float*>(ps);  // [16][S], S <= 32
+                    const bool staged = d.S <= 32;
+                    if (staged && tid < p.G) {
+                        const size_t pb0 = ((size_t)d.b * NH + tid) * p.S_max;
+                        float M = -INFINITY;
+                        for (int sI = 0; sI < d.S; ++sI) M = fmaxf(M, __ldcg(p.ws_m + pb0 + sI));
+                        float Ls = 0.f;
+                        for (int sI = 0; sI < d.S; ++sI) {
+                            const float f = fast_exp2(__ldcg(p.ws_m + pb0 + sI) - M);
+                            wsm[tid * 32 + sI] = f;
+                            Ls += f * __ldcg(p.ws_l + pb0 + sI);
+                        }
+                        const float inv = 1.f / Ls;
+                        for (int sI = 0; sI < d.S; ++sI) wsm[tid * 32 + sI] *= inv;
+                    }
+                    named_bar_sync(1, NSOFT);
+                    if (staged) {
+                        constexpr int PER = NH * (DV / 4) / NSOFT;  // 16 float4 per thread
+                        float4 o[PER];
+#pragma unroll
+                        for (int j = 0; j < PER; ++j) o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int sI = 0; sI < d.S; ++sI) {
+#pragma unroll
+                            for (int j = 0; j < PER; ++j) {
+                                const int idx = tid + j * NSOFT;
+                                const int h = idx / (DV / 4), c = (idx % (DV / 4)) * 4;
+                                if (h < p.G) {
+                                    const float w = wsm[h * 32 + sI];
+                                    const float4 a = __ldcg(reinterpret_cast<const float4*>(
+                                        p.ws_acc + (((size_t)d.b * NH + h) * p.S_max + sI) * DV + c));
+                                    o[j].x += w * a.x;
+                                    o[j].y += w * a.y;
+                                    o[j].z += w * a.z;
+                                    o[j].w += w * a.w;
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < PER; ++j) {
+                            const int idx = tid + j * NSOFT;
+                            const int h = idx / (DV / 4), c = (idx % (DV / 4)) * 4;
+                            if (h >= p.G) continue;
+                            const size_t off = p.out_head_major ? (((size_t)h * p.B + d.b) * DV + c)
+                                                                : (((size_t)d.b * p.G + h) * DV + c);
+                            uint2 v;
+                            v.x = pack_bf16(o[j].x, o[j].y);
+                            v.y = pack_bf16(o[j].z, o[j].w);
+                            *reinterpret_cast<uint2*>(p.out + off) = v;
+                        }
+                    } else {
+                        for (int idx = tid; idx < p.G * (DV / 4); idx += NSOFT) {
+                            const int h = idx / (DV / 4), c = (idx % (DV / 4)) * 4;
+                            const size_t pb0 = ((size_t)d.b * NH + h) * p.S_max;
+                            float M = -INFINITY;
+                            for (int sI = 0; sI < d.S; ++sI) M = fmaxf(M, __ldcg(p.ws_m + pb0 + sI));
+                            float Ls = 0.f;
+                            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                            for (int sI = 0; sI < d.S; ++sI) {
+                                const float f = fast_exp2(__ldcg(p.ws_m + pb0 + sI) - M);
+                                Ls += f * __ldcg(p.ws_l + pb0 + sI);
+                                const float4 a = __ldcg(reinterpret_cast<const float4*>(p.ws_acc + (pb0 + sI) * DV + c));
+                                o.x += f * a.x;
+                                o.y += f * a.y;
+                                o.z += f * a.z;
+                                o.w += f * a.w;
+                            }
+                            const float inv = 1.f / Ls;
+                            const size_t off = p.out_head_major ? (((size_t)h * p.B + d.b) * DV + c)
+                                                                : (((size_t)d.b * p.G + h) * DV + c);
+                            uint2 v;
+                            v.x = pack_bf16(o.x * inv, o.y * inv);
+                            v.y = pack_bf16(o.z * inv, o.w * inv);
+                            *reinterpret_cast<uint2*>(p.out + off) = v;
+                        }
+                    }
+                    if (tid == 0) p.ws_cnt[d.b] = 0;
+                }
+            }
+            [[maybe_unused]] const long long te2 = TL_NOW();
+            // red_l / s_last are rewritten by the next unit
+            named_bar_sync(1, NSOFT);
+            if (lane == 0 && qd == 2) TL_REC(6, nunit, te0, te1, te2);
+            if (lane == 0 && qd == 2) TL_REC(7, nunit, TL_NOW(), 0, 0);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+#ifdef SPD_TIMELINE
+    if (threadIdx.x == 0 && p.tl && blockIdx.x < 512) {
+        unsigned long long g_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+        long long* _r = p.tl + 8 * (8 * 512 + blockIdx.x);
+        _r[0] = 8; _r[1] = blockIdx.x; _r[2] = (long long)g_start; _r[3] = (long long)g_end; _r[4] = smid();
+    }
+#endif
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, TM_COLS);
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(p.sched + 1, 1u);
+        if (done == gridDim.x - 1) {
+            p.sched[0] = 0u;
+            p.sched[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+inline size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+}  // namespace
+
+bool spd_mla_tc_ok(const semipd_pool* p, int Hq) {
+    const auto& c = p->cfg;
+    return c.dtype == SEMIPD_BF16 && c.kv_shared && c.num_kv_heads == 1 && c.head_dim_k == DK &&
+           c.head_dim_v == DV && Hq <= NH && c.block_size == PAGE && p->have_mla_tc_maps;
+}
+
+size_t spd_mla_tc_ws_bytes(int B, int max_ctx) {
+    const int S_max = (max_ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+    size_t o = al256((size_t)B * 4);           // cnt
+    o += 256;                                   // sched
+    o = al256(o + (size_t)B * NH * S_max * 4);  // m
+    o = al256(o + (size_t)B * NH * S_max * 4);  // l
+    o = al256(o + (size_t)B * NH * S_max * DV * 4);
+    return o;
+}
+
+semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void* q,
+                                       const void* k_new, const int* req_ids, const int* ctx_lens,
+                                       int batch, int max_ctx_len, int Hq, float scale, void* out,
+                                       int out_head_major, void* workspace, size_t ws_bytes,
+                                       int budget, int* status_dev, cudaStream_t st) {
+    const int S_max = (max_ctx_len + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+    if (!workspace || ws_bytes < spd_mla_tc_ws_bytes(batch, max_ctx_len)) return SEMIPD_ERR_INVALID;
+    if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) return SEMIPD_ERR_INVALID;
+    // Q [B][Hq][576] as (64 cols, Hq heads, 9 column blocks, B): box lands [cb][16 rows][128 B];
+    // rows >= Hq are out of range and zero-filled by TMA
+    CUtensorMap qmap;
+    {
+        const uint64_t dims[4] = {64, (uint64_t)Hq, NCB, (uint64_t)batch};
+        const uint64_t strides[3] = {DK * 2, 128, (uint64_t)Hq * DK * 2};
+        const uint32_t box[4] = {64, NH, NCB, 1};
+        if (!spd_encode_tiled_4d(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(q), dims,
+                                 strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+            return SEMIPD_ERR_CUDA;
+    }
+    unsigned char* ws = static_cast<unsigned char*>(workspace);
+    TcParams prm;
+    prm.k_new = static_cast<const uint4*>(k_new);
+    prm.req_ids = req_ids;
+    prm.ctx_lens = ctx_lens;
+    prm.bt = pool->bt;
+    prm.k_pool = static_cast<unsigned char*>(pool->k_layer(layer));
+    prm.out = static_cast<__nv_bfloat16*>(out);
+    size_t o = 0;
+    prm.ws_cnt = reinterpret_cast<int*>(ws + o);
+    o = al256((size_t)batch * 4);
+    prm.sched = reinterpret_cast<unsigned*>(ws + o);
+    o += 256;
+    prm.ws_m = reinterpret_cast<float*>(ws + o);
+    o = al256(o + (size_t)batch * NH * S_max * 4);
+    prm.ws_l = reinterpret_cast<float*>(ws + o);
+    o = al256(o + (size_t)batch * NH * S_max * 4);
+    prm.ws_acc = reinterpret_cast<float*>(ws + o);
+    prm.status = status_dev;
+    prm.B = batch;
+    prm.MBR = pool->cfg.max_blocks_per_req;
+    prm.N_B = pool->cfg.num_blocks;
+    prm.S_max = S_max;
+    prm.n_units = batch * S_max;
+    prm.out_head_major = out_head_major;
+    prm.G = Hq;
+    prm.scale_log2 = scale * LOG2E;
+    prm.trace = spd_trace(pool);
+    prm.tl = reinterpret_cast<long long*>(pool->timeline);
+    prm.tl_ctr = pool->timeline_ctr;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(decode_mla_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SMEM_BYTES) != cudaSuccess)
+            return SEMIPD_ERR_CUDA;
+        attr = true;
+    }
+    int grid = budget > 0 ? budget : prm.n_units;
+    if (grid > prm.n_units) grid = prm.n_units;
+    decode_mla_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(pool->mla_lo[layer], pool->mla_hi[layer],
+                                                             qmap, prm);
+    pool->launches += 1;
+    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+}

@@ -47,6 +47,10 @@ struct semipd_pool {
     // column blocks (one 36 KiB TMA per 32-key stage at dk = 576)
     std::vector<CUtensorMap> mla_kmap;
     bool have_mla_map = false;
+    // MLA tcgen05 decode (bs 64): the same 4-D view, boxes of 64 rows x column blocks
+    // [0, 4) (32 KiB) and [4, 9) (40 KiB) — one page in two TMA boxes
+    std::vector<CUtensorMap> mla_lo, mla_hi;
+    bool have_mla_tc_maps = false;
     int box_rows = 16;
     int dbox_rows = 16;
     int* trace_buf = nullptr;
@@ -93,6 +97,13 @@ semipd_status spd_launch_decode_mla(semipd_pool_t pool, int layer, const void* q
                                     int max_ctx_len, int Hq, float scale, void* out,
                                     int out_head_major, void* workspace, size_t ws_bytes,
                                     int budget, int* status_dev, cudaStream_t st);
+bool spd_mla_tc_ok(const semipd_pool* p, int Hq);
+size_t spd_mla_tc_ws_bytes(int B, int max_ctx);
+semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void* q,
+                                       const void* k_new, const int* req_ids, const int* ctx_lens,
+                                       int batch, int max_ctx_len, int Hq, float scale, void* out,
+                                       int out_head_major, void* workspace, size_t ws_bytes,
+                                       int budget, int* status_dev, cudaStream_t st);
 semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new, const void* v_new,
                                   const int* cu_seqlens, const int* req_ids, const int* pos0,
                                   int n, int total_rows, int mode, int* status_dev,

@@ -242,6 +242,22 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
                                           p->k_layer(l), md, ms, mb, CU_TENSOR_MAP_SWIZZLE_128B);
             }
             p->have_mla_map = mok;
+            if (cfg->block_size == 64 && cfg->head_dim_k == 576 && cfg->num_kv_heads == 1) {
+                p->mla_lo.resize(cfg->num_layers);
+                p->mla_hi.resize(cfg->num_layers);
+                bool tok = true;
+                for (int l = 0; l < cfg->num_layers && tok; ++l) {
+                    const uint64_t kr = (uint64_t)cfg->head_dim_k * 2;
+                    const uint64_t md[4] = {64, 64, 9, (uint64_t)cfg->num_blocks};
+                    const uint64_t ms[3] = {kr, 128, kr * 64};
+                    const uint32_t lo[4] = {64, 64, 4, 1}, hi[4] = {64, 64, 5, 1};
+                    tok = spd_encode_tiled_4d(&p->mla_lo[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                              p->k_layer(l), md, ms, lo, CU_TENSOR_MAP_SWIZZLE_128B) &&
+                          spd_encode_tiled_4d(&p->mla_hi[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                              p->k_layer(l), md, ms, hi, CU_TENSOR_MAP_SWIZZLE_128B);
+                }
+                p->have_mla_tc_maps = tok;
+            }
         }
         p->have_maps = ok;
     }

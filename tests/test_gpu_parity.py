@@ -217,7 +217,7 @@ def test_decode_mla_tensor_kernel_and_budgets():
             for b in (1, 9, 148, -1)]
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
-    # the tensor-core MLA kernel (trace kind 3) is the one that runs
+    # the tcgen05 MLA kernel (trace kind 4) is the one that runs at bs 64
     from paper_2504_19867_b200 import KVPool, PoolConfig
     dev = torch.device("cuda", 0)
     pool = KVPool(PoolConfig(1, 8, 64, 1, 576, 512, 2, 4, kv_shared=True), dev)
@@ -234,7 +234,27 @@ def test_decode_mla_tensor_kernel_and_budgets():
     torch.cuda.synchronize()
     n = int(ctr.item())
     kinds = set(trace[:4 * n].view(n, 4)[:, 3].cpu().tolist())
-    assert kinds == {3}
+    assert kinds == {4}
+
+
+@pytest.mark.parametrize("dist", [synth.FLAT, synth.NEEDLE])
+def test_decode_mla_bs32_mma_sync_kernel(dist):
+    """Latent pools with 32-token pages take the mma.sync MLA kernel (trace kind 3)."""
+    run_decode(small(synth.CFG5_MLA, block_size=32), [0, 31, 32, 700, 5000], seed=65 + dist,
+               dist=dist)
+
+
+def test_decode_mla_fewer_heads_head_major():
+    """Hq < 16 (q rows beyond Hq zero-filled by TMA) with head-major output."""
+    run_decode(small(synth.CFG5_MLA, num_q_heads=8), [5, 64, 127, 1500, 2100], seed=71,
+               dist=synth.PEAKED, head_major=True)
+
+
+def test_decode_mla_cfg5_batch():
+    """cfg 5 shape at trace scale: B = 256 requests with lognormal-like contexts."""
+    rng = np.random.default_rng(5)
+    ctx = [int(x) for x in np.clip(rng.lognormal(np.log(251.0) - 0.5, 1.0, 256), 1, 8192)]
+    run_decode(small(synth.CFG5_MLA), ctx, seed=75, dist=synth.VSHIFT)
 
 
 def test_decode_full_size_cfg2():

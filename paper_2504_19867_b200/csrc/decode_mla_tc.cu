@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (d.b < 0) break;
             // PV(t) as soon as P(t) is written (it releases tile t's ring slots), else QK(t)
             // as soon as tile t has landed.
-            bool q_ok = false;
+            bool q_ok = false, qk_lo = false;
             int nqk = 0, npv = 0;
             while (npv < d.nt) {
                 const int tp = gt + npv, ob = tp & 1;
@@ -302,36 +302,47 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             umma_ss_warp(tmem + TM_O + ob * 64 + m * NH, da + (uint64_t)(ks * 128),
                                          dp0 + (uint64_t)(ob * (P_BYTES / 16) + ks * 2), ID_PV,
                                          (npv > 1 || ks > 0) ? 1u : 0u);
+                        if (m == 1) umma_commit_warp(bar.empty + s0);  // blocks 0,1 read the first box
                     }
                     umma_commit_warp(bar.o_done + ob);
-                    umma_commit_warp(bar.empty + s0);
                     umma_commit_warp(bar.empty + s1);
                     if (lane == 0) TL_REC(3, gt + npv, TL_NOW(), 0, 0);
                     ++npv;
                     continue;
                 }
                 if (nqk < d.nt) {
+                    // QK(t) in two halves: column blocks [0,4) as soon as the first box has
+                    // landed, [4,9) when the second has
                     const int t = gt + nqk, sb = t & 1, h0 = gh + 2 * nqk;
                     const int s0 = h0 % NSLOT, s1 = (h0 + 1) % NSLOT;
                     if (!q_ok) q_ok = probe(&bar.q_full, nq & 1);
-                    if (q_ok && probe(bar.s_empty + sb, ((t >> 1) & 1) ^ 1) &&
-                        probe(bar.full + s0, (h0 / NSLOT) & 1) &&
-                        probe(bar.full + s1, ((h0 + 1) / NSLOT) & 1)) {
+                    if (q_ok && !qk_lo && probe(bar.s_empty + sb, ((t >> 1) & 1) ^ 1) &&
+                        probe(bar.full + s0, (h0 / NSLOT) & 1)) {
                         tc_fence_after();
                         const uint64_t dlo = umma_desc_sw128(ring_a + s0 * SLOT_BYTES, 16, 1024);
-                        const uint64_t dhi = umma_desc_sw128(ring_a + s1 * SLOT_BYTES, 16, 1024);
 #pragma unroll
-                        for (int k = 0; k < DK / 16; ++k) {
+                        for (int k = 0; k < CB_LO * 4; ++k) {
                             const int cb = k >> 2;
                             // descriptor start address is in 16-byte units
-                            const uint64_t da = cb < CB_LO ? dlo + (uint64_t)(cb * (PAGE * 128 / 16) + (k & 3) * 2)
-                                                           : dhi + (uint64_t)((cb - CB_LO) * (PAGE * 128 / 16) + (k & 3) * 2);
-                            umma_ss_warp(tmem + TM_S + sb * NH, da,
+                            umma_ss_warp(tmem + TM_S + sb * NH, dlo + (uint64_t)(cb * (PAGE * 128 / 16) + (k & 3) * 2),
                                          dq0 + (uint64_t)(cb * (NH * 128 / 16) + (k & 3) * 2), ID_QK, k > 0);
+                        }
+                        qk_lo = true;
+                        continue;
+                    }
+                    if (qk_lo && probe(bar.full + s1, ((h0 + 1) / NSLOT) & 1)) {
+                        tc_fence_after();
+                        const uint64_t dhi = umma_desc_sw128(ring_a + s1 * SLOT_BYTES, 16, 1024);
+#pragma unroll
+                        for (int k = CB_LO * 4; k < DK / 16; ++k) {
+                            const int cb = k >> 2;
+                            umma_ss_warp(tmem + TM_S + sb * NH, dhi + (uint64_t)((cb - CB_LO) * (PAGE * 128 / 16) + (k & 3) * 2),
+                                         dq0 + (uint64_t)(cb * (NH * 128 / 16) + (k & 3) * 2), ID_QK, 1u);
                         }
                         umma_commit_warp(bar.s_full + sb);
                         if (lane == 0) TL_REC(2, t, TL_NOW(), 0, 0);
                         if (nqk == d.nt - 1) umma_commit_warp(&bar.q_empty);
+                        qk_lo = false;
                         ++nqk;
                         continue;
                     }
@@ -394,25 +405,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 float* rm = red + (t & 1) * 64;
                 if (lane < NH) rm[qd * NH + lane] = mine;
                 named_bar_sync(1, NSOFT);
-                float scl[NH];
-                bool grow = false;
+                float mn[NH];
 #pragma unroll
                 for (int h4 = 0; h4 < NH / 4; ++h4) {
                     const float4 a = reinterpret_cast<const float4*>(rm)[h4];
                     const float4 b = reinterpret_cast<const float4*>(rm + NH)[h4];
                     const float4 c = reinterpret_cast<const float4*>(rm + 2 * NH)[h4];
                     const float4 e = reinterpret_cast<const float4*>(rm + 3 * NH)[h4];
-                    const float m4[4] = {fmaxf(fmax3(a.x, b.x, c.x), e.x), fmaxf(fmax3(a.y, b.y, c.y), e.y),
-                                         fmaxf(fmax3(a.z, b.z, c.z), e.z), fmaxf(fmax3(a.w, b.w, c.w), e.w)};
+                    mn[h4 * 4 + 0] = fmaxf(mrun[h4 * 4 + 0], fmaxf(fmax3(a.x, b.x, c.x), e.x));
+                    mn[h4 * 4 + 1] = fmaxf(mrun[h4 * 4 + 1], fmaxf(fmax3(a.y, b.y, c.y), e.y));
+                    mn[h4 * 4 + 2] = fmaxf(mrun[h4 * 4 + 2], fmaxf(fmax3(a.z, b.z, c.z), e.z));
+                    mn[h4 * 4 + 3] = fmaxf(mrun[h4 * 4 + 3], fmaxf(fmax3(a.w, b.w, c.w), e.w));
+                }
+                // the 32 per-head factors are warp-uniform: lane h computes 2^(mrun - mn) (the
+                // l rescale) and lane 16 + h 2^(mold2 - mn) (the O_(t&1) rescale), one MUFU
+                // op per lane instead of 32, then broadcast
+                float scl[NH];
+                bool grow = false;
+                {
+                    float e_in = 0.f;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int h = h4 * 4 + j;
-                        const float mn = fmaxf(mrun[h], m4[j]);
-                        lpart[h] *= fast_exp2(mrun[h] - mn);
-                        grow |= mn > mold2[h];
-                        scl[h] = fast_exp2(mold2[h] - mn);  // O_(t&1) holds tiles <= t-2
+                    for (int h = 0; h < NH; ++h) {
+                        e_in = lane == h ? mrun[h] - mn[h] : e_in;
+                        e_in = lane == h + 16 ? mold2[h] - mn[h] : e_in;
+                        grow |= mn[h] > mold2[h];
+                    }
+                    const float e = fast_exp2(e_in);
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) {
+                        lpart[h] *= __shfl_sync(0xffffffffu, e, h);
+                        scl[h] = __shfl_sync(0xffffffffu, e, h + 16);
                         mold2[h] = mrun[h];
-                        mrun[h] = mn;
+                        mrun[h] = mn[h];
                     }
                 }
                 uint32_t pb[NH];

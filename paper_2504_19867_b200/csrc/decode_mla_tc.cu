@@ -41,7 +41,14 @@ constexpr uint32_t Q_BYTES = NCB * NH * 128;            // 18 KiB
 constexpr uint32_t P_BYTES = NH * 128;                  // 2 KiB per buffer (2 buffers)
 constexpr int NTHREADS = 192;
 constexpr int NSOFT = 128;
-constexpr int SPLIT_KEYS = 1024;
+constexpr int SPLIT_PAGES = 20;  // a split spans at most 20 pages (1280 keys, 1.4 MiB)
+
+// number of splits of a request with ctx cached tokens (ctx + 1 keys): a function of the
+// shape only (R26); ceil(pages / 20), so 1025 keys (17 pages) stay one unit
+__host__ __device__ __forceinline__ int n_splits(int ctx) {
+    const int pages = (ctx + 1 + PAGE - 1) / PAGE;
+    return (pages + SPLIT_PAGES - 1) / SPLIT_PAGES;
+}
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr uint32_t TM_S = 0, TM_O = 64, TM_COLS = 256;  // S^T 2x16 cols, O^T 2 x (4 x 16) cols
 
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 d.b = u % p.B;
                 ctx = __ldg(p.ctx_lens + d.b);
                 rid = __ldg(p.req_ids + d.b);
-                d.S = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+                d.S = n_splits(ctx);
                 if (d.s >= d.S) continue;
                 split_range(ctx, d.S, d.s, d.k0, d.k1);
                 d.nt = (d.k1 - d.k0 + PAGE - 1) / PAGE;
@@ -708,7 +715,7 @@ bool spd_mla_tc_ok(const semipd_pool* p, int Hq) {
 }
 
 size_t spd_mla_tc_ws_bytes(int B, int max_ctx) {
-    const int S_max = (max_ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+    const int S_max = n_splits(max_ctx);
     size_t o = al256((size_t)B * 4);           // cnt
     o += 256;                                   // sched
     o = al256(o + (size_t)B * NH * S_max * 4);  // m
@@ -722,7 +729,7 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
                                        int batch, int max_ctx_len, int Hq, float scale, void* out,
                                        int out_head_major, void* workspace, size_t ws_bytes,
                                        int budget, int* status_dev, cudaStream_t st) {
-    const int S_max = (max_ctx_len + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+    const int S_max = n_splits(max_ctx_len);
     if (!workspace || ws_bytes < spd_mla_tc_ws_bytes(batch, max_ctx_len)) return SEMIPD_ERR_INVALID;
     if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) return SEMIPD_ERR_INVALID;
     // Q [B][Hq][576] as (64 cols, Hq heads, 9 column blocks, B): box lands [cb][16 rows][128 B];

@@ -97,6 +97,12 @@ semipd_status spd_launch_decode_mla(semipd_pool_t pool, int layer, const void* q
                                     int max_ctx_len, int Hq, float scale, void* out,
                                     int out_head_major, void* workspace, size_t ws_bytes,
                                     int budget, int* status_dev, cudaStream_t st);
+bool spd_mla_prefill_ok(const semipd_pool* p, int Hq);
+semipd_status spd_launch_prefill_mla(semipd_pool_t pool, int layer, const void* q,
+                                     const int* cu_seqlens, const int* req_ids,
+                                     const int* prefix_lens, int n, int total_q, int max_chunk_len,
+                                     int Hq, float scale, void* out, int out_head_major,
+                                     int budget, int* status_dev, cudaStream_t st);
 bool spd_mla_tc_ok(const semipd_pool* p, int Hq);
 size_t spd_mla_tc_ws_bytes(int B, int max_ctx);
 semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void* q,

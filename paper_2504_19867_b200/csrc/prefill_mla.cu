@@ -1,0 +1,486 @@
+// prefill_mla.cu — absorbed-MLA chunked prefill attention on the 5th-gen tensor cores (cfg 5:
+// 16 q heads share ONE latent KV head, dk = 576, dv = 512, V = K[..., :512]; R19).
+// Causal, bottom-right aligned (row t of request r sees keys 0 .. P_r + t, R4), keys read
+// from the paged latent pool after the chunk's own rows were written there.
+//
+// Tile: M = 64 rows = 4 consecutive tokens x 16 heads (GQA packing: every K/V page is read
+// once per 4 tokens x 16 heads).  With M = 64 a tcgen05 accumulator only occupies TMEM lanes
+// 0-15 of each 32-lane quadrant, and a second accumulator can sit at lane base 16
+// (scripts/probe_umma_m64.cu), so the 64 x 512 fp32 output fits in 256 columns:
+//   S  [64 x 64 keys]  = Q[64 x 576] . K^T       M=64 N=64,  36 x K16, SS  (2 TMEM buffers)
+//   O_lo[64 x 256]    += P[64 x 64] . V[:, 0:256]   M=64 N=256, 4 x K16, SS  (lane base 0)
+//   O_hi[64 x 256]    += P[64 x 64] . V[:, 256:512] M=64 N=256, 4 x K16, SS  (lane base 16)
+// A page (64 keys x 576) lands as two 4-D TMA boxes (column blocks [0,4) and [4,9)) in 40 KiB
+// ring slots — the same boxes as the MLA decode kernel; V is read MN-major from them.
+//
+// Warps: 0 producer (units, TMA), 1 MMA issuer (warp-collective), 2-5 softmax + epilogue.
+// Softmax warp w handles token w % 4 of the tile: lanes 0-15 own one head's row each (the
+// causal limit is warp-uniform), lanes 16-31 own the O_hi half of the same rows.  Lazy
+// rescale (reference max moves only when the running max exceeds it by > 8 in log2 units);
+// the denominator sums the bf16-rounded P that the MMA consumes, so both sides of the
+// quotient see the same P (R16).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+
+using namespace spd;
+
+constexpr int DK = 576, DV = 512, NH = 16;
+constexpr int PAGE = 64;
+constexpr int NCB = DK / 64;                            // 9 column blocks
+constexpr int CB_LO = 4;
+constexpr uint32_t LO_BYTES = CB_LO * PAGE * 128;       // 32 KiB
+constexpr uint32_t HI_BYTES = (NCB - CB_LO) * PAGE * 128;  // 40 KiB
+constexpr uint32_t SLOT_BYTES = HI_BYTES;
+constexpr int NSLOT = 3;
+constexpr int TQ = 4;                                   // tokens per unit
+constexpr int BM = TQ * NH;                             // 64 rows
+constexpr uint32_t Q_BYTES = NCB * BM * 128;            // 72 KiB
+constexpr uint32_t P_BYTES = BM * 128;                  // 8 KiB per buffer
+constexpr int NTHREADS = 192;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_TH = 8.f;
+constexpr uint32_t TM_O = 0, TM_S = 256, TM_COLS = 512;
+
+struct PUnit {
+    int i, t0, ntok, P, kend, nt, row0, rid;  // i < 0: done
+};
+
+struct PmParams {
+    const int* cu;
+    const int* req_ids;
+    const int* prefix;
+    const int* bt;
+    __nv_bfloat16* out;  // [T][Hq][512] or [Hq][T][512]
+    int* status;
+    unsigned* sched;
+    int n, T, Hq, maxqb, n_units, MBR, N_B, out_head_major;
+    float scale_log2;
+    SpdTrace trace;
+};
+
+struct Bars {
+    uint64_t full[NSLOT], empty[NSLOT], s_full[2], s_empty[2], p_full[2], o_done[2], q_full,
+        q_empty, ufull[2], uempty[2];
+};
+
+constexpr uint32_t OFF_Q = NSLOT * SLOT_BYTES;
+constexpr uint32_t OFF_P = OFF_Q + Q_BYTES;
+constexpr uint32_t OFF_BARS = OFF_P + 2 * P_BYTES;
+constexpr uint32_t OFF_UNITS = OFF_BARS + sizeof(Bars);
+constexpr uint32_t OFF_MISC = OFF_UNITS + 2 * sizeof(PUnit);
+constexpr uint32_t SMEM_BYTES = 1024 + OFF_MISC + 16;
+static_assert(OFF_Q % 1024 == 0 && OFF_P % 1024 == 0, "UMMA operands need 1 KiB alignment");
+static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KiB opt-in shared memory");
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    prefill_mla_kernel(const __grid_constant__ CUtensorMap map_lo,
+                       const __grid_constant__ CUtensorMap map_hi,
+                       const __grid_constant__ CUtensorMap qmap, PmParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* ring = base;
+    unsigned char* qs = base + OFF_Q;
+    unsigned char* ps = base + OFF_P;
+    Bars& bar = *reinterpret_cast<Bars*>(base + OFF_BARS);
+    PUnit* units = reinterpret_cast<PUnit*>(base + OFF_UNITS);
+    uint32_t* tmem_base = reinterpret_cast<uint32_t*>(base + OFF_MISC);
+
+    const int warp = (int)warp_id();
+    const int lane = (int)lane_id();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSLOT; ++i) {
+            mbar_init(bar.full + i, 1);
+            mbar_init(bar.empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar.s_full + i, 1);
+            mbar_init(bar.s_empty + i, 4);
+            mbar_init(bar.p_full + i, 4);
+            mbar_init(bar.o_done + i, 1);
+            mbar_init(bar.ufull + i, 1);
+            mbar_init(bar.uempty + i, 5);
+        }
+        mbar_init(&bar.q_full, 1);
+        mbar_init(&bar.q_empty, 1);
+        fence_mbar_init();
+        if (p.trace.buf) {
+            int slot = atomicAdd(p.trace.ctr, 1);
+            if (slot < p.trace.cap)
+                reinterpret_cast<int4*>(p.trace.buf)[slot] =
+                    make_int4(1, (int)smid(), (int)blockIdx.x, 5 /* kernel kind: MLA prefill */);
+        }
+    }
+    if (warp == 1) tmem_alloc(tmem_base, TM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_base;
+
+    if (warp == 0) {
+        // =========================== producer ===========================
+        if (lane == 0) {
+            tma_prefetch_desc(&map_lo);
+            tma_prefetch_desc(&map_hi);
+            tma_prefetch_desc(&qmap);
+        }
+        int gh = 0, nunit = 0, nq = 0;
+        int u_next = blockIdx.x;
+        for (;;) {
+            const int u = u_next;
+            if (lane == 0) u_next = (int)gridDim.x + (int)atomicAdd(p.sched, 1u);
+            u_next = __shfl_sync(0xffffffffu, u_next, 0);
+            PUnit d;
+            if (u >= p.n_units) {
+                d.i = -1;
+            } else {
+                // longest-first: the last token blocks of every request (most keys) go first
+                d.i = u % p.n;
+                const int qb = p.maxqb - 1 - u / p.n;
+                const int c0 = __ldg(p.cu + d.i), C = __ldg(p.cu + d.i + 1) - c0;
+                d.t0 = qb * TQ;
+                if (d.t0 >= C) continue;
+                d.ntok = min(TQ, C - d.t0);
+                d.P = __ldg(p.prefix + d.i);
+                d.kend = d.P + d.t0 + d.ntok;
+                d.nt = (d.kend + PAGE - 1) / PAGE;
+                d.row0 = c0 + d.t0;
+                d.rid = __ldg(p.req_ids + d.i);
+            }
+            const int us = nunit & 1;
+            if (lane == 0) {
+                mbar_wait(bar.uempty + us, ((nunit >> 1) & 1) ^ 1);
+                units[us] = d;
+                mbar_arrive(bar.ufull + us);
+            }
+            __syncwarp();
+            ++nunit;
+            if (d.i < 0) break;
+            const int* btr = p.bt + (size_t)d.rid * p.MBR;
+            int blk_l = -1;
+            for (int j = 0; j < d.nt; ++j, gh += 2) {
+                if ((j & 31) == 0) {
+                    const int pg = j + lane;
+                    blk_l = (pg < d.nt && pg < p.MBR) ? __ldg(btr + pg) : -1;
+                }
+                const int blk = __shfl_sync(0xffffffffu, blk_l, j & 31);
+                if (lane == 0) {
+                    int z = p.N_B;  // out of range: zero fill
+                    if (blk >= 0 && blk < p.N_B) z = blk;
+                    else if (p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                    const int s0 = gh % NSLOT, s1 = (gh + 1) % NSLOT;
+                    mbar_wait(bar.empty + s0, ((gh / NSLOT) & 1) ^ 1);
+                    mbar_arrive_expect_tx(bar.full + s0, LO_BYTES);
+                    tma_load_4d(ring + s0 * SLOT_BYTES, &map_lo, bar.full + s0, 0, 0, 0, z);
+                    if (j == 0) {
+                        // this unit's Q (64 rows): free once the previous unit's last QK is done
+                        mbar_wait(&bar.q_empty, (nq & 1) ^ 1);
+                        mbar_arrive_expect_tx(&bar.q_full, Q_BYTES);
+                        tma_load_4d(qs, &qmap, &bar.q_full, 0, 0, d.row0, 0);
+                    }
+                    mbar_wait(bar.empty + s1, (((gh + 1) / NSLOT) & 1) ^ 1);
+                    mbar_arrive_expect_tx(bar.full + s1, HI_BYTES);
+                    tma_load_4d(ring + s1 * SLOT_BYTES, &map_hi, bar.full + s1, 0, 0, CB_LO, z);
+                }
+                __syncwarp();
+            }
+            ++nq;
+        }
+    } else if (warp == 1) {
+        // =========================== MMA issuer (warp-collective) ===========================
+        constexpr uint32_t ID_QK = umma_idesc_bf16_f32_ab(BM, PAGE, 0, 0);
+        constexpr uint32_t ID_PV = umma_idesc_bf16_f32_ab(BM, 256, 0, 1);
+        const uint32_t ring_a = smem_u32(ring);
+        const uint64_t dq0 = umma_desc_sw128(smem_u32(qs), 16, 1024);
+        const uint64_t dp0 = umma_desc_sw128(smem_u32(ps), 16, 1024);
+        auto probe = [&](const uint64_t* b, uint32_t par) {
+            bool r = false;
+            if (lane == 0) r = mbar_test_wait(b, par);
+            return __shfl_sync(0xffffffffu, r ? 1 : 0, 0) != 0;
+        };
+        int gh = 0, gt = 0, nunit = 0, nq = 0;
+        for (;;) {
+            const int us = nunit & 1;
+            mbar_wait(bar.ufull + us, (nunit >> 1) & 1);
+            const PUnit d = units[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar.uempty + us);
+            ++nunit;
+            if (d.i < 0) break;
+            bool q_ok = false, qk_lo = false;
+            int nqk = 0, npv = 0;
+            while (npv < d.nt) {
+                const int tp = gt + npv, pb = tp & 1;
+                if (npv < nqk && probe(bar.p_full + pb, (tp >> 1) & 1)) {
+                    const int h0 = gh + 2 * npv;
+                    const int s0 = h0 % NSLOT, s1 = (h0 + 1) % NSLOT;
+                    tc_fence_after();
+                    // V^T blocks: dv [0,256) = column blocks 0-3 (first box), [256,512) = 4-7
+                    const uint64_t dvlo = umma_desc_sw128(ring_a + s0 * SLOT_BYTES, PAGE * 128, 1024);
+                    const uint64_t dvhi = umma_desc_sw128(ring_a + s1 * SLOT_BYTES, PAGE * 128, 1024);
+                    const uint64_t dpa = dp0 + (uint64_t)(pb * (P_BYTES / 16));
+#pragma unroll
+                    for (int ks = 0; ks < PAGE / 16; ++ks)
+                        umma_ss_warp(tmem + TM_O, dpa + (uint64_t)(ks * 2), dvlo + (uint64_t)(ks * 128),
+                                     ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
+                    umma_commit_warp(bar.empty + s0);
+#pragma unroll
+                    for (int ks = 0; ks < PAGE / 16; ++ks)
+                        umma_ss_warp(tmem + TM_O + (16u << 16), dpa + (uint64_t)(ks * 2),
+                                     dvhi + (uint64_t)(ks * 128), ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
+                    umma_commit_warp(bar.o_done + pb);
+                    umma_commit_warp(bar.empty + s1);
+                    ++npv;
+                    continue;
+                }
+                if (nqk < d.nt) {
+                    const int t = gt + nqk, sb = t & 1, h0 = gh + 2 * nqk;
+                    const int s0 = h0 % NSLOT, s1 = (h0 + 1) % NSLOT;
+                    if (!q_ok) q_ok = probe(&bar.q_full, nq & 1);
+                    if (q_ok && !qk_lo && probe(bar.s_empty + sb, ((t >> 1) & 1) ^ 1) &&
+                        probe(bar.full + s0, (h0 / NSLOT) & 1)) {
+                        tc_fence_after();
+                        const uint64_t dk = umma_desc_sw128(ring_a + s0 * SLOT_BYTES, 16, 1024);
+#pragma unroll
+                        for (int k = 0; k < CB_LO * 4; ++k) {
+                            const int cb = k >> 2;
+                            umma_ss_warp(tmem + TM_S + sb * PAGE,
+                                         dq0 + (uint64_t)(cb * (BM * 128 / 16) + (k & 3) * 2),
+                                         dk + (uint64_t)(cb * (PAGE * 128 / 16) + (k & 3) * 2), ID_QK,
+                                         k > 0);
+                        }
+                        qk_lo = true;
+                        continue;
+                    }
+                    if (qk_lo && probe(bar.full + s1, ((h0 + 1) / NSLOT) & 1)) {
+                        tc_fence_after();
+                        const uint64_t dk = umma_desc_sw128(ring_a + s1 * SLOT_BYTES, 16, 1024);
+#pragma unroll
+                        for (int k = CB_LO * 4; k < DK / 16; ++k) {
+                            const int cb = k >> 2;
+                            umma_ss_warp(tmem + TM_S + sb * PAGE,
+                                         dq0 + (uint64_t)(cb * (BM * 128 / 16) + (k & 3) * 2),
+                                         dk + (uint64_t)((cb - CB_LO) * (PAGE * 128 / 16) + (k & 3) * 2),
+                                         ID_QK, 1u);
+                        }
+                        umma_commit_warp(bar.s_full + sb);
+                        if (nqk == d.nt - 1) umma_commit_warp(&bar.q_empty);
+                        qk_lo = false;
+                        ++nqk;
+                        continue;
+                    }
+                }
+                __nanosleep(32);
+            }
+            ++nq;
+            gt += d.nt;
+            gh += 2 * d.nt;
+        }
+    } else {
+        // =========================== softmax + epilogue ===========================
+        const int qd = warp & 3;  // TMEM lane quadrant = token of the tile
+        const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
+        const bool lo = lane < 16;
+        const int h = lane & 15;  // head of this lane's row
+        int gt = 0, nunit = 0;
+        for (;;) {
+            const int us = nunit & 1;
+            mbar_wait(bar.ufull + us, (nunit >> 1) & 1);
+            const PUnit d = units[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar.uempty + us);
+            ++nunit;
+            if (d.i < 0) break;
+            const int klim = d.P + d.t0 + qd + 1;  // keys [0, klim) visible to this token
+            float mref = -INFINITY;                 // reference max of P / O (log2 domain)
+            float lsum = 0.f;
+            for (int j = 0; j < d.nt; ++j) {
+                const int t = gt + j, sb = t & 1;
+                mbar_wait(bar.s_full + sb, (t >> 1) & 1);
+                tc_fence_after();
+                uint32_t sr[2][32];
+                tmem_ld32(tmem + lane_base + TM_S + sb * PAGE, sr[0]);
+                tmem_ld32(tmem + lane_base + TM_S + sb * PAGE + 32, sr[1]);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar.s_empty + sb);
+                const int k0 = j * PAGE;
+                float mt = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < PAGE; ++c) {
+                    float x = __uint_as_float(sr[c >> 5][c & 31]) * p.scale_log2;
+                    x = (k0 + c < klim) ? x : -INFINITY;
+                    sr[c >> 5][c & 31] = __float_as_uint(x);
+                    mt = fmaxf(mt, x);
+                }
+                // lazy rescale: move the reference only when the max grew by > RESCALE_TH
+                const bool move = lo && (mt > mref + RESCALE_TH || j == 0);
+                const float mnew = move ? fmaxf(mt, mref) : mref;
+                const float alpha = (move && j > 0) ? fast_exp2(mref - mnew) : 1.f;
+                mref = mnew;
+                lsum *= alpha;
+                const bool any_rescale = __any_sync(0xffffffffu, move && j > 0);
+                // P buffer t&1 is free once PV(t-2) completed; O may be rescaled only after
+                // PV(t-1) completed
+                if (any_rescale && j > 0) {
+                    mbar_wait(bar.o_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
+                } else if (t >= 2) {
+                    mbar_wait(bar.o_done + sb, ((t >> 1) & 1) ^ 1);
+                }
+                tc_fence_after();
+                if (any_rescale && j > 0) {
+                    // lanes 0-15: O_lo of row (qd, h); lanes 16-31: O_hi of the same row
+                    const float a = __shfl_sync(0xffffffffu, alpha, h);
+                    const uint32_t ob = tmem + lane_base + TM_O;
+#pragma unroll 1
+                    for (int cc = 0; cc < 256; cc += 32) {
+                        uint32_t o[32];
+                        tmem_ld32(ob + cc, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * a);
+                        tmem_st32(ob + cc, o);
+                    }
+                    tmem_wait_st();
+                }
+                // P row (64 keys, bf16) -> P buffer sb, K-major 128-B swizzle; lsum from the
+                // rounded values
+                if (lo) {
+                    unsigned char* prow = ps + sb * P_BYTES + (qd * 16 + h) * 128;
+                    const int sw = (qd * 16 + h) & 7;
+#pragma unroll
+                    for (int c8 = 0; c8 < 8; ++c8) {
+                        uint32_t w[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int c = c8 * 8 + 2 * e;
+                            const __nv_bfloat16 b0 = __float2bfloat16_rn(
+                                fast_exp2(__uint_as_float(sr[c >> 5][c & 31]) - mref));
+                            const __nv_bfloat16 b1 = __float2bfloat16_rn(
+                                fast_exp2(__uint_as_float(sr[(c + 1) >> 5][(c + 1) & 31]) - mref));
+                            lsum += __bfloat162float(b0) + __bfloat162float(b1);
+                            w[e] = (uint32_t)__bfloat16_as_ushort(b0) |
+                                   ((uint32_t)__bfloat16_as_ushort(b1) << 16);
+                        }
+                        *reinterpret_cast<uint4*>(prow + ((c8 ^ sw) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                }
+                fence_proxy_async_smem();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar.p_full + sb);
+            }
+            gt += d.nt;
+            // ---- epilogue: O / l -> bf16 (lanes 0-15: dv [0,256), lanes 16-31: [256,512))
+            mbar_wait(bar.o_done + ((gt - 1) & 1), ((gt - 1) >> 1) & 1);
+            tc_fence_after();
+            const float rl = __frcp_rn(__shfl_sync(0xffffffffu, lsum, h));
+            const bool store = qd < d.ntok && h < p.Hq;
+            const size_t tok = (size_t)d.row0 + qd;
+            __nv_bfloat16* orow = p.out + (p.out_head_major ? ((size_t)h * p.T + tok) * DV
+                                                            : (tok * p.Hq + h) * DV) +
+                                  (lo ? 0 : 256);
+            const uint32_t ob = tmem + lane_base + TM_O;
+#pragma unroll 1
+            for (int cc = 0; cc < 256; cc += 32) {
+                uint32_t o[32];
+                tmem_ld32(ob + cc, o);
+                tmem_wait_ld();
+                if (store) {
+#pragma unroll
+                    for (int e8 = 0; e8 < 4; ++e8) {
+                        uint4 v;
+                        v.x = pack_bf16(__uint_as_float(o[e8 * 8 + 0]) * rl, __uint_as_float(o[e8 * 8 + 1]) * rl);
+                        v.y = pack_bf16(__uint_as_float(o[e8 * 8 + 2]) * rl, __uint_as_float(o[e8 * 8 + 3]) * rl);
+                        v.z = pack_bf16(__uint_as_float(o[e8 * 8 + 4]) * rl, __uint_as_float(o[e8 * 8 + 5]) * rl);
+                        v.w = pack_bf16(__uint_as_float(o[e8 * 8 + 6]) * rl, __uint_as_float(o[e8 * 8 + 7]) * rl);
+                        *reinterpret_cast<uint4*>(orow + cc + e8 * 8) = v;
+                    }
+                }
+            }
+            tc_fence_before();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, TM_COLS);
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(p.sched + 1, 1u);
+        if (done == gridDim.x - 1) {
+            p.sched[0] = 0u;
+            p.sched[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+}  // namespace
+
+bool spd_mla_prefill_ok(const semipd_pool* p, int Hq) {
+    const auto& c = p->cfg;
+    return c.dtype == SEMIPD_BF16 && c.kv_shared && c.num_kv_heads == 1 && c.head_dim_k == DK &&
+           c.head_dim_v == DV && Hq <= NH && c.block_size == PAGE && p->have_mla_tc_maps;
+}
+
+semipd_status spd_launch_prefill_mla(semipd_pool_t pool, int layer, const void* q,
+                                     const int* cu_seqlens, const int* req_ids,
+                                     const int* prefix_lens, int n, int total_q, int max_chunk_len,
+                                     int Hq, float scale, void* out, int out_head_major,
+                                     int budget, int* status_dev, cudaStream_t st) {
+    if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) return SEMIPD_ERR_INVALID;
+    // Q [T][Hq][576] as (64 cols, Hq heads, T tokens, 9 column blocks); box (64, 16, 4, 9)
+    // lands [cb][token][head][128 B] = K-major rows t * 16 + h; heads >= Hq and tokens >= T
+    // are zero-filled
+    CUtensorMap qmap;
+    {
+        const uint64_t dims[4] = {64, (uint64_t)Hq, (uint64_t)total_q, NCB};
+        const uint64_t strides[3] = {DK * 2, (uint64_t)Hq * DK * 2, 128};
+        const uint32_t box[4] = {64, NH, TQ, NCB};
+        if (!spd_encode_tiled_4d(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(q), dims,
+                                 strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+            return SEMIPD_ERR_CUDA;
+    }
+    PmParams prm;
+    prm.cu = cu_seqlens;
+    prm.req_ids = req_ids;
+    prm.prefix = prefix_lens;
+    prm.bt = pool->bt;
+    prm.out = static_cast<__nv_bfloat16*>(out);
+    prm.status = status_dev;
+    prm.sched = &pool->st->sched[0];
+    prm.n = n;
+    prm.T = total_q;
+    prm.Hq = Hq;
+    prm.maxqb = (max_chunk_len + TQ - 1) / TQ;
+    if (prm.maxqb < 1) return SEMIPD_OK;
+    const long long units = (long long)n * prm.maxqb;
+    if (units > (1LL << 30)) return SEMIPD_ERR_UNSUPPORTED;
+    prm.n_units = (int)units;
+    prm.MBR = pool->cfg.max_blocks_per_req;
+    prm.N_B = pool->cfg.num_blocks;
+    prm.out_head_major = out_head_major;
+    prm.scale_log2 = scale * LOG2E;
+    prm.trace = spd_trace(pool);
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(prefill_mla_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SMEM_BYTES) != cudaSuccess)
+            return SEMIPD_ERR_CUDA;
+        attr = true;
+    }
+    int grid = budget > 0 ? budget : prm.n_units;
+    if (grid > prm.n_units) grid = prm.n_units;
+    prefill_mla_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(pool->mla_lo[layer], pool->mla_hi[layer],
+                                                           qmap, prm);
+    pool->launches += 1;
+    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+}

@@ -526,6 +526,10 @@ extern "C" semipd_status semipd_prefill_attn(
                                           prefix_lens, n, total_q, 0, status_dev, st);
     if (r != SEMIPD_OK) return r;
     const int budget = spd_resolve_budget(pool, sm_budget, true);
+    if (spd_mla_prefill_ok(pool, num_q_heads))  // absorbed MLA latent cache, 64-token pages (cfg 5)
+        return spd_launch_prefill_mla(pool, layer, q, cu_seqlens_q, req_ids, prefix_lens, n, total_q,
+                                      max_chunk_len, num_q_heads, softmax_scale, out,
+                                      out_head_major, budget, status_dev, st);
     if (!fast_path_ok(pool, num_q_heads))
         return spd_launch_simt_attn(pool, layer, q, cu_seqlens_q, req_ids, prefix_lens, n, total_q,
                                     0, num_q_heads, softmax_scale, out, out_head_major, budget,

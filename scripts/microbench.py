@@ -38,10 +38,13 @@ def main():
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--bs", type=int, default=16)
     ap.add_argument("--mla", action="store_true", help="cfg5 absorbed-MLA decode (576/512, 16 heads)")
+    ap.add_argument("--mla-prefill", action="store_true", help="cfg5 absorbed-MLA prefill chunk")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     if args.mla:
         return mla(args, dev)
+    if args.mla_prefill:
+        return mla_prefill(args, dev)
     L, B, ctx, C, P = args.layers, args.batch, args.ctx, args.chunk, args.prefix
     Hq, Hkv, d, bs = args.hq, args.hkv, 128, args.bs
     nb_dec = ctx // bs + 1
@@ -134,6 +137,41 @@ def mla(args, dev):
         print(json.dumps({"kernel": "decode_mla", "budget": bud, "B": B, "ctx": ctx, "ms": ms,
                           "GB_s": byts / (ms / 1e3) / 1e9, "TFLOP_s": flops / (ms / 1e3) / 1e12}),
               flush=True)
+
+
+def mla_prefill(args, dev):
+    """MLA prefill: one chunk of C tokens after a prefix P, 16 heads over the latent (bs 64)."""
+    L, C, P = args.layers, args.chunk, args.prefix
+    nb = -(-(C + P) // 64)
+    pool = KVPool(PoolConfig(L, nb + 4, 64, 1, 576, 512, 2, nb + 1, kv_shared=True), dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32([0]), i32([nb]))
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    for l in range(L):
+        K, _, _, _ = pool.views(l)
+        K.normal_(generator=g)
+    q = torch.randn(C, 16, 576, device=dev, generator=g).bfloat16()
+    k = torch.randn(C, 1, 576, device=dev, generator=g).bfloat16()
+    out = torch.empty(C, 16, 512, dtype=torch.bfloat16, device=dev)
+    flops = 2 * 16 * (576 + 512) * (C * P + C * (C + 1) / 2)
+    for bud in [int(x) for x in args.budgets.split(",")]:
+        run = lambda l: pool.prefill_attn(l, q, k, None, i32([0, C]), i32([0]), i32([P]), C, C,  # noqa: E731
+                                          1 / math.sqrt(192), out, sm_budget=bud)
+        for l in range(min(L, 2)):
+            run(l)
+        torch.cuda.synchronize()
+        times = []
+        for it in range(args.iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            run(it % L)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        print(json.dumps({"kernel": "prefill_mla", "budget": bud, "C": C, "P": P, "ms": ms,
+                          "TFLOP_s": flops / (ms / 1e3) / 1e12}), flush=True)
 
 
 if __name__ == "__main__":

@@ -62,6 +62,13 @@ __global__ void probe(const uint16_t* cimg, const uint16_t* qimg, const uint16_t
             uint64_t b = umma_desc_sw128(smem_u32(ps) + k * 32, 16, 1024);
             umma_ss(t0 + 16, a, b, id_pv, k > 0);
         }
+        // same QK into TMEM lane offset 16, column 64 (is a lane-16 base legal for M=64?)
+        for (int k = 0; k < DK / 16; ++k) {
+            const int cb = k >> 2, sub = k & 3;
+            uint64_t a = umma_desc_sw128(smem_u32(cs + cb * KEYS * 128) + sub * 32, 16, 1024);
+            uint64_t b = umma_desc_sw128(smem_u32(qs + cb * NH * 128) + sub * 32, 16, 1024);
+            umma_ss(t0 + (16u << 16) + 64, a, b, id_qk, k > 0);
+        }
         umma_commit(&bar);
     }
     __syncwarp();
@@ -73,6 +80,9 @@ __global__ void probe(const uint16_t* cimg, const uint16_t* qimg, const uint16_t
     tmem_wait_ld();
     for (int j = 0; j < 16; ++j) s_out[(w * 32 + l) * 16 + j] = __uint_as_float(r[j]);
     for (int j = 0; j < 16; ++j) o_out[(w * 32 + l) * 16 + j] = __uint_as_float(r[16 + j]);
+    tmem_ld32(t0 + ((uint32_t)(w * 32) << 16) + 64, r);
+    tmem_wait_ld();
+    for (int j = 0; j < 16; ++j) s_out[128 * 16 + (w * 32 + l) * 16 + j] = __uint_as_float(r[j]);
     tc_fence_before();
     __syncthreads();
     if (tid < 32) tmem_dealloc(t0, 128);
@@ -109,12 +119,12 @@ int main() {
     cudaMalloc(&dc, cimg.size() * 2);
     cudaMalloc(&dq, qimg.size() * 2);
     cudaMalloc(&dp, pimg.size() * 2);
-    cudaMalloc(&ds, 128 * 16 * 4);
+    cudaMalloc(&ds, 2 * 128 * 16 * 4);
     cudaMalloc(&dout, 128 * 16 * 4);
     cudaMemcpy(dc, cimg.data(), cimg.size() * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dq, qimg.data(), qimg.size() * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dp, pimg.data(), pimg.size() * 2, cudaMemcpyHostToDevice);
-    cudaMemset(ds, 0xFF, 128 * 16 * 4);
+    cudaMemset(ds, 0xFF, 2 * 128 * 16 * 4);
     const int smem = 1024 + NCB * KEYS * 128 + NCB * NH * 128 + NH * 128;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     for (int variant = 0; variant < 2; ++variant) {
@@ -123,7 +133,7 @@ int main() {
     probe<<<1, 128, smem>>>(dc, dq, dp, ds, dout, lbo, sbo);
     cudaError_t e = cudaDeviceSynchronize();
     printf("variant lbo=%u sbo=%u kernel: %s\n", lbo, sbo, cudaGetErrorString(e));
-    std::vector<float> s(128 * 16), o(128 * 16);
+    std::vector<float> s(2 * 128 * 16), o(128 * 16);
     cudaMemcpy(s.data(), ds, s.size() * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(o.data(), dout, o.size() * 4, cudaMemcpyDeviceToHost);
     std::vector<float> ref(KEYS * NH);
@@ -133,13 +143,13 @@ int main() {
             for (int c = 0; c < DK; ++c) a += (double)C[k * DK + c] * Q[h * DK + c];
             ref[k * NH + h] = (float)a;
         }
-    if (variant == 0) {
-    printf("QK M=64 lane -> key map:\n");
+    if (variant == 0) for (int half = 0; half < 2; ++half) {
+    printf("QK M=64 (D lane base %d) lane -> key map:\n", half * 16);
     for (int lane = 0; lane < 128; ++lane) {
         int match = -1;
         for (int k = 0; k < KEYS; ++k) {
             bool ok = true;
-            for (int h = 0; h < NH; ++h) ok &= fabsf(s[lane * 16 + h] - ref[k * NH + h]) < 1e-3f;
+            for (int h = 0; h < NH; ++h) ok &= fabsf(s[half * 2048 + lane * 16 + h] - ref[k * NH + h]) < 1e-3f;
             if (ok) { match = k; break; }
         }
         printf("%d:%d ", lane, match);

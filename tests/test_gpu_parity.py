@@ -381,6 +381,53 @@ def test_prefill_full_size_cfg2_sampled():
     run_prefill(small(SHAPE_8B), [T], [0], seed=1220, dist=synth.FLAT, rows_mask=mask)
 
 
+@pytest.mark.parametrize("chunks,prefixes", [([128], [0]), ([37], [100]), ([3, 70, 130], [0, 64, 5]),
+                                             ([1, 200], [0, 300])])
+@pytest.mark.parametrize("dist", synth.DISTS)
+def test_prefill_mla_latent(chunks, prefixes, dist):
+    """cfg 5 absorbed MLA prefill (16 heads over the 576-d latent, V = K[:, :512], bs 64):
+    ragged token blocks, non-page-aligned prefixes, several requests per launch."""
+    run_prefill(small(synth.CFG5_MLA), chunks, prefixes, seed=80 + dist, dist=dist)
+
+
+def test_prefill_mla_kernel_budgets_and_kind():
+    shape = small(synth.CFG5_MLA)
+    outs = [run_prefill(shape, [150, 7], [10, 64], seed=85, dist=synth.NEEDLE,
+                        sm_budget=b)[0].cpu() for b in (1, 9, 148, -1)]
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    from paper_2504_19867_b200 import KVPool, PoolConfig
+    dev = torch.device("cuda", 0)
+    pool = KVPool(PoolConfig(1, 8, 64, 1, 576, 512, 2, 4, kv_shared=True), dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32([0]), i32([2]))
+    trace = torch.zeros(4 * 64, dtype=torch.int32, device=dev)
+    ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+    pool.set_trace(trace, ctr)
+    q = torch.randn(100, 16, 576, device=dev).bfloat16()
+    kn = torch.randn(100, 1, 576, device=dev).bfloat16()
+    out = torch.empty(100, 16, 512, dtype=torch.bfloat16, device=dev)
+    pool.prefill_attn(0, q, kn, None, i32([0, 100]), i32([0]), i32([0]), 100, 100, 0.07, out)
+    torch.cuda.synchronize()
+    n = int(ctr.item())
+    kinds = set(trace[:4 * n].view(n, 4)[:, 3].cpu().tolist())
+    assert kinds == {5}
+
+
+def test_prefill_mla_fewer_heads_head_major():
+    run_prefill(small(synth.CFG5_MLA, num_q_heads=8), [77], [20], seed=87, dist=synth.PEAKED,
+                head_major=True)
+
+
+def test_prefill_mla_full_chunk_sampled():
+    """cfg 5 prefill chunk at full size (C = 2048, P = 0), every 32nd row + the last."""
+    T = 2048
+    mask = np.zeros(T, np.uint8)
+    mask[::32] = 1
+    mask[-1] = 1
+    run_prefill(small(synth.CFG5_MLA), [T], [0], seed=88, dist=synth.FLAT, rows_mask=mask)
+
+
 def test_prefill_then_decode_handoff():
     """Prefill writes the chunk's K/V; decode of the next token reads it from the
     pool (P:184 handoff, zero-copy)."""

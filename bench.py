@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--impl", default="semipd", choices=["semipd", "reference"])
     ap.add_argument("--model", default="llama3-8b", choices=list(MODELS))
     ap.add_argument("--split", type=float, default=None, help="prefill SM percent x (y = 100-x)")
-    ap.add_argument("--sweep", default="30,40,50,60,70")
+    ap.add_argument("--sweep", default="30,35,40,45,50,60")
     ap.add_argument("--block-size", type=int, default=64,
                     help="KV page size in tokens (64: one 16 KiB TMA box per (block, head) "
                          "page on B200; 16 is supported but TMA-per-box bound)")
@@ -508,7 +508,7 @@ def main():
                 "algorithmic_bytes_per_launch": w.decode_bytes_per_launch(),
                 "avg_launch_ms": dec_ms, "sm_budget": n_d}
     share = n_p / w.pool.num_sms
-    roof_pre = {"kernel": "prefill_tc_kernel (+kv_write) tcgen05 causal GQA", "bound": "tensor",
+    roof_pre = {"kernel": "prefill_tc_kernel tcgen05 causal GQA (K/V pool write fused)", "bound": "tensor",
                 "achieved": pre_tfs, "peak": bf16_sus, "unit": "TFLOP/s",
                 "frac": pre_tfs / bf16_sus, "frac_share_scaled": pre_tfs / (bf16_sus * share),
                 "peak_kind": f"{peak_kind} sustained", "traffic": None,

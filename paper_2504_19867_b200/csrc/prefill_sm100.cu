@@ -62,6 +62,10 @@ struct PrefillParams {
     int* status;
     unsigned* sched;
     int n, T, Hq, Hkv, G, TQ, pairs_max, n_units, lg_bs, box_rows, MBR, N_B, out_head_major;
+    const uint4* k_new;     // chunk K / V rows [T][Hkv][128] (fused pool write, warp 3)
+    const uint4* v_new;
+    unsigned char* k_pool;  // this layer's K / V pages
+    unsigned char* v_pool;
     float scale_log2;
     SpdTrace trace;
     long long* tl;  // SPD_TIMELINE builds only: phase clock64 stamps of CTA 0
@@ -340,6 +344,63 @@ __global__ void __launch_bounds__(NT, 1)
                 ++nunit;
             }
         }
+    } else {
+        // ============ warp 3: the chunk's K/V rows -> pool pages, fused ============
+        // Rows are split evenly over the CTAs; the attention itself reads chunk K/V from
+        // k_new / v_new and prefix pages written by earlier calls, so nothing in this launch
+        // reads what this warp writes (the next kernel on the stream does).
+        const int r0 = (int)((long long)p.T * blockIdx.x / gridDim.x);
+        const int r1 = (int)((long long)p.T * (blockIdx.x + 1) / gridDim.x);
+        if (r0 < r1) {
+            int i = 0, hi = p.n - 1;  // last request with cu[i] <= r0
+            while (i < hi) {
+                const int mid = (i + hi + 1) >> 1;
+                if (__ldg(p.cu + mid) <= r0) i = mid; else hi = mid - 1;
+            }
+            int c_lo = __ldg(p.cu + i), c_hi = __ldg(p.cu + i + 1);
+            int pre = __ldg(p.prefix + i);
+            const int* btr = p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR;
+            const int bs_mask = (1 << p.lg_bs) - 1;
+            const int c = lane & 15;         // 16-byte chunk of a 256-byte head row
+            for (int row = r0; row < r1; ++row) {
+                while (row >= c_hi) {
+                    ++i;
+                    c_lo = c_hi;
+                    c_hi = __ldg(p.cu + i + 1);
+                    pre = __ldg(p.prefix + i);
+                    btr = p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR;
+                }
+                const int pos = pre + row - c_lo;
+                const int page = pos >> p.lg_bs;
+                const int blk = page < p.MBR ? __ldg(btr + page) : -1;
+                if (blk < 0 || blk >= p.N_B) {
+                    if (lane == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                    continue;
+                }
+#pragma unroll 1
+                for (int g0 = 0; g0 < p.Hkv; g0 += 8) {  // 8 heads per pass, 4 per half-warp
+                    uint4 kv[2][4];
+#pragma unroll
+                    for (int gg = 0; gg < 4; ++gg) {
+                        const int g = g0 + (lane >> 4) + 2 * gg;
+                        if (g < p.Hkv) {
+                            const size_t src = ((size_t)row * p.Hkv + g) * 16 + c;
+                            kv[0][gg] = __ldg(p.k_new + src);
+                            kv[1][gg] = __ldg(p.v_new + src);
+                        }
+                    }
+#pragma unroll
+                    for (int gg = 0; gg < 4; ++gg) {
+                        const int g = g0 + (lane >> 4) + 2 * gg;
+                        if (g < p.Hkv) {
+                            const size_t dst = (((size_t)blk * p.Hkv + g) * (bs_mask + 1) + (pos & bs_mask)) * 16 + c;
+                            reinterpret_cast<uint4*>(p.k_pool)[dst] = kv[0][gg];
+                            reinterpret_cast<uint4*>(p.v_pool)[dst] = kv[1][gg];
+                        }
+                    }
+                }
+            }
+        }
     }
     } else {
         // ============================ softmax warpgroups ============================
@@ -521,11 +582,14 @@ extern "C" semipd_status semipd_prefill_attn(
     if (!q || !k_new || (!v_new && !c.kv_shared) || !cu_seqlens_q || !req_ids || !prefix_lens ||
         !out)
         return SEMIPD_ERR_INVALID;
-    // 1. K/V write into the pool, stream-ordered before attention reads it
-    semipd_status r = spd_launch_kv_write(pool, layer, k_new, v_new, cu_seqlens_q, req_ids,
-                                          prefix_lens, n, total_q, 0, status_dev, st);
-    if (r != SEMIPD_OK) return r;
     const int budget = spd_resolve_budget(pool, sm_budget, true);
+    if (!fast_path_ok(pool, num_q_heads) || spd_mla_prefill_ok(pool, num_q_heads)) {
+        // K/V write into the pool, stream-ordered before attention reads it (these
+        // paths read the chunk's own keys from the pool); the tcgen05 path fuses it
+        semipd_status r = spd_launch_kv_write(pool, layer, k_new, v_new, cu_seqlens_q, req_ids,
+                                              prefix_lens, n, total_q, 0, status_dev, st);
+        if (r != SEMIPD_OK) return r;
+    }
     if (spd_mla_prefill_ok(pool, num_q_heads))  // absorbed MLA latent cache, 64-token pages (cfg 5)
         return spd_launch_prefill_mla(pool, layer, q, cu_seqlens_q, req_ids, prefix_lens, n, total_q,
                                       max_chunk_len, num_q_heads, softmax_scale, out,
@@ -562,6 +626,10 @@ extern "C" semipd_status semipd_prefill_attn(
     prm.N_B = c.num_blocks;
     prm.out_head_major = out_head_major;
     prm.scale_log2 = softmax_scale * LOG2E;
+    prm.k_new = static_cast<const uint4*>(k_new);
+    prm.v_new = static_cast<const uint4*>(v_new);
+    prm.k_pool = static_cast<unsigned char*>(pool->k_layer(layer));
+    prm.v_pool = static_cast<unsigned char*>(pool->v_layer(layer));
     prm.trace = spd_trace(pool);
     prm.tl = reinterpret_cast<long long*>(pool->timeline);
     prm.tl_ctr = pool->timeline_ctr;

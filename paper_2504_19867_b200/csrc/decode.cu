@@ -472,6 +472,376 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Head-pair variant (pages of >= 64 tokens, even Hkv, G <= 8).  A TMA box costs ~800 cycles
+// of its SM's TMA unit regardless of size up to ~24 KiB, so 16 KiB boxes cap
+// an SM at ~20 B/clk.  Here a unit is (request, kv heads g0 and g0 + 1, split) and one 4-D box
+// covers the two adjacent (block, head) pages: 32 KiB of K + 32 KiB of V per 64-key stage,
+// 3-deep ring.  Consumers: 3 warp pairs; stage gs goes to pair gs % 3, warp 2p + e of the
+// pair handles head g0 + e (same per-head math as decode_bf16_kernel).
+constexpr int P_NCW = 3;                       // warp pairs (stage rotation)
+constexpr int P_NSTAGE = 3;
+constexpr int P_NTHREADS = (2 * P_NCW + 1) * 32;
+constexpr int P_STAGE = 4 * KV_BYTES;          // K(g0) K(g0+1) V(g0) V(g0+1)
+constexpr int P_GMAX = 8;
+
+__global__ void __launch_bounds__(P_NTHREADS, 1)
+    decode_pair_kernel(const __grid_constant__ CUtensorMap kmap2,
+                       const __grid_constant__ CUtensorMap vmap2, DecodeParams p) {
+    constexpr int LG_R = 6;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* ring = smem;                                                     // 3 x 64 KiB
+    float* scr_acc = reinterpret_cast<float*>(ring + P_NSTAGE * P_STAGE);          // [6][8][128]
+    float* scr_ml = scr_acc + 2 * P_NCW * P_GMAX * HD;                             // [6][8][2]
+    uint64_t* full = reinterpret_cast<uint64_t*>(scr_ml + 2 * P_NCW * P_GMAX * 2);
+    uint64_t* empty = full + P_NSTAGE;
+    uint64_t* ufull = empty + P_NSTAGE;
+    uint64_t* uempty = ufull + 2;
+    UnitDesc* units = reinterpret_cast<UnitDesc*>(uempty + 2);
+    int* s_last = reinterpret_cast<int*>(units + 2);
+
+    const int warp = (int)warp_id();
+    const int lane = (int)lane_id();
+    const int NP = p.Hkv >> 1;  // head pairs
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < P_NSTAGE; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, 2);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(ufull + i, 1);
+            mbar_init(uempty + i, 2 * P_NCW);
+        }
+        fence_mbar_init();
+        if (p.trace.buf) {
+            int slot = atomicAdd(p.trace.ctr, 1);
+            if (slot < p.trace.cap)
+                reinterpret_cast<int4*>(p.trace.buf)[slot] =
+                    make_int4(2, (int)smid(), (int)blockIdx.x, 6 /* kernel kind: head-pair split-K decode */);
+        }
+    }
+    __syncthreads();
+
+    if (warp == 2 * P_NCW) {
+        // =========================== producer ===========================
+        if (lane == 0) {
+            tma_prefetch_desc(&kmap2);
+            tma_prefetch_desc(&vmap2);
+        }
+        const int oob_z = p.N_B * p.Hkv;
+        const int bs_mask = (1 << p.lg_bs) - 1;
+        int gstage = 0, nunit = 0;
+        for (;;) {
+            int u = 0;
+            if (lane == 0) u = (int)atomicAdd(p.sched, 1u);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            UnitDesc d;
+            if (u >= p.n_units) {
+                d.b = -1;
+            } else {
+                d.s = u / (p.B * NP);
+                d.b = (u / NP) % p.B;
+                d.g = 2 * (u % NP);  // first head of the pair
+                const int ctx = __ldg(p.ctx_lens + d.b);
+                d.S = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+                if (d.s >= d.S) continue;
+                split_range(ctx, d.S, d.s, d.k0, d.k1);
+                d.nst = (d.k1 - d.k0 + KPS - 1) / KPS;
+                while (gstage % P_NCW != 0) {  // align to the pair rotation (R26)
+                    if (lane == 0) {
+                        const int st = gstage % P_NSTAGE;
+                        mbar_wait(empty + st, ((gstage / P_NSTAGE) & 1) ^ 1);
+                        mbar_arrive(full + st);
+                    }
+                    ++gstage;
+                }
+                __syncwarp();
+                d.base = gstage;
+            }
+            const int us = nunit & 1;
+            if (lane == 0) {
+                mbar_wait(uempty + us, ((nunit >> 1) & 1) ^ 1);
+                units[us] = d;
+                mbar_arrive(ufull + us);
+            }
+            __syncwarp();
+            ++nunit;
+            if (d.b < 0) break;
+            const int ctx = __ldg(p.ctx_lens + d.b);
+            const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
+            const int last_page = ctx >> p.lg_bs;
+            if (d.s == d.S - 1) {
+                // fused append of both heads' K and V rows at slot ctx: lane l copies 16 B of
+                // (head l>>4 ... ) -- 2 heads x (K, V) x 16 chunks = 64 copies, 2 per lane
+                const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
+                if (blk >= 0 && blk < p.N_B) {
+                    const int c = lane & 15, e = lane >> 4;  // e: head of the pair
+                    const size_t slot = (((size_t)blk * p.Hkv + d.g + e) << p.lg_bs) + (ctx & bs_mask);
+                    const size_t src = ((size_t)d.b * p.Hkv + d.g + e) * (HD / 8);
+                    reinterpret_cast<uint4*>(p.k_pool)[slot * (HD / 8) + c] = __ldg(p.k_new + src + c);
+                    reinterpret_cast<uint4*>(p.v_pool)[slot * (HD / 8) + c] = __ldg(p.v_new + src + c);
+                    fence_proxy_async_global();
+                }
+                __syncwarp();
+            }
+            auto lookup = [&](int i) -> int {  // raw block id of stage i (-2: past the request)
+                const int page = (d.k0 + i * KPS) >> p.lg_bs;
+                if (i >= d.nst || page > last_page) return -2;
+                return page < p.MBR ? __ldg(btr + page) : -1;
+            };
+            int zc = lookup(lane);
+            for (int i = 0; i < d.nst; ++i, ++gstage) {
+                if (i > 0 && (i & 31) == 0) zc = lookup(i + lane);
+                const int blk = __shfl_sync(0xffffffffu, zc, i & 31);
+                const int st = gstage % P_NSTAGE;
+                if (lane == 0) {
+                    unsigned char* kst = ring + st * P_STAGE;
+                    mbar_wait(empty + st, ((gstage / P_NSTAGE) & 1) ^ 1);
+                    mbar_arrive_expect_tx(full + st, P_STAGE);
+                    int z = oob_z;
+                    if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
+                    else if (blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                    const int y = (d.k0 + i * KPS) & bs_mask;
+                    tma_load_4d(kst, &kmap2, full + st, 0, y, 0, z);
+                    tma_load_4d(kst + 2 * KV_BYTES, &vmap2, full + st, 0, y, 0, z);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // =========================== consumers ===========================
+        const int pw = warp >> 1, e = warp & 1;  // pair (stage rotation), head of the pair
+        const int r0 = lane >> 2;
+        const int c0 = (lane & 3) * 2;
+        int nunit = 0;
+        int next_gs = pw;
+        for (;;) {
+            const int us = nunit & 1;
+            mbar_wait(ufull + us, (nunit >> 1) & 1);
+            const UnitDesc d = units[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(uempty + us);
+            ++nunit;
+            if (d.b < 0) break;
+            const int g = d.g + e;
+            uint32_t qa[8][4];
+            {
+                const uint32_t* q32 = reinterpret_cast<const uint32_t*>(p.q);
+                const size_t rowA = ((size_t)d.b * p.Hq + g * p.G + r0) * (HD / 2);
+                const bool va = r0 < p.G;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int col = (kk * 16 + c0) >> 1;
+                    qa[kk][0] = va ? __ldg(q32 + rowA + col) : 0u;
+                    qa[kk][1] = 0u;  // rows 8-15: G <= 8
+                    qa[kk][2] = va ? __ldg(q32 + rowA + col + 4) : 0u;
+                    qa[kk][3] = 0u;
+                }
+            }
+            float acc[16][2];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.f;
+            float mrow = -INFINITY, lrow = 0.f;
+            while (next_gs < d.base) {
+                const int st = next_gs % P_NSTAGE;
+                mbar_wait(full + st, (next_gs / P_NSTAGE) & 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + st);
+                next_gs += P_NCW;
+            }
+            next_gs = d.base + (pw < d.nst ? pw + ((d.nst - 1 - pw) / P_NCW + 1) * P_NCW : pw);
+            for (int i = pw; i < d.nst; i += P_NCW) {
+                const int gs = d.base + i;
+                const int st = gs % P_NSTAGE;
+                mbar_wait(full + st, (gs / P_NSTAGE) & 1);
+                const uint32_t kst = smem_u32(ring + st * P_STAGE) + e * KV_BYTES;
+                const uint32_t vst = kst + 2 * KV_BYTES;
+                float s[8][4];
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) {
+                    s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+                    const int key = nt * 8 + (lane & 7);
+#pragma unroll
+                    for (int kk = 0; kk < 8; kk += 2) {
+                        const int ci = 2 * kk + (lane >> 3);
+                        const uint32_t addr = kst + kv_off<LG_R>(key, ci >> 3) + (((ci & 7) ^ (key & 7)) << 4);
+                        uint32_t b0, b1, b2, b3;
+                        ldsm_x4(addr, b0, b1, b2, b3);
+                        mma_bf16_16816(s[nt], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
+                        mma_bf16_16816(s[nt], qa[kk + 1][0], qa[kk + 1][1], qa[kk + 1][2],
+                                       qa[kk + 1][3], b2, b3);
+                    }
+                }
+                const int kbase = d.k0 + i * KPS;
+                const bool tail = kbase + KPS > d.k1;
+                float mx = -INFINITY;
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2) {  // rows r0 only (rows >= 8 are padding)
+                        float x = s[nt][q2] * p.scale_log2;
+                        if (tail && kbase + nt * 8 + c0 + q2 >= d.k1) x = -INFINITY;
+                        s[nt][q2] = x;
+                        mx = fmaxf(mx, x);
+                    }
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                const float mnew = fmaxf(mrow, mx);
+                const float alpha = fast_exp2(mrow - mnew);
+                mrow = mnew;
+                float ls = 0.f;
+                uint32_t pa[4][4];
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) {
+                    const float p0 = fast_exp2(s[nt][0] - mrow);
+                    const float p1 = fast_exp2(s[nt][1] - mrow);
+                    ls += p0 + p1;
+                    const int ks = nt >> 1, hi = nt & 1;
+                    pa[ks][hi * 2 + 0] = pack_bf16(p0, p1);
+                    pa[ks][hi * 2 + 1] = 0u;
+                }
+                lrow = lrow * alpha + ls;
+                if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+                    for (int nd = 0; nd < 16; ++nd) {
+                        acc[nd][0] *= alpha;
+                        acc[nd][1] *= alpha;
+                    }
+                }
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const int key = ks * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+                    for (int nd = 0; nd < 16; nd += 2) {
+                        const int ch = nd + (lane >> 4);
+                        const uint32_t addr = vst + kv_off<LG_R>(key, ch >> 3) + (((ch & 7) ^ (key & 7)) << 4);
+                        uint32_t b0, b1, b2, b3;
+                        ldsm_x4_t(addr, b0, b1, b2, b3);
+                        float t0[4] = {acc[nd][0], acc[nd][1], 0.f, 0.f};
+                        float t1[4] = {acc[nd + 1][0], acc[nd + 1][1], 0.f, 0.f};
+                        mma_bf16_16816(t0, pa[ks][0], pa[ks][1], pa[ks][2], pa[ks][3], b0, b1);
+                        mma_bf16_16816(t1, pa[ks][0], pa[ks][1], pa[ks][2], pa[ks][3], b2, b3);
+                        acc[nd][0] = t0[0];
+                        acc[nd][1] = t0[1];
+                        acc[nd + 1][0] = t1[0];
+                        acc[nd + 1][1] = t1[1];
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + st);
+            }
+            lrow += __shfl_xor_sync(0xffffffffu, lrow, 1);
+            lrow += __shfl_xor_sync(0xffffffffu, lrow, 2);
+            const int wi = pw * 2 + e;  // scratch slot of this warp
+            float* wacc = scr_acc + wi * P_GMAX * HD;
+            if (r0 < P_GMAX) {
+#pragma unroll
+                for (int nd = 0; nd < 16; ++nd)
+                    *reinterpret_cast<float2*>(wacc + r0 * HD + nd * 8 + c0) = make_float2(acc[nd][0], acc[nd][1]);
+                if ((lane & 3) == 0) {
+                    scr_ml[(wi * P_GMAX + r0) * 2 + 0] = mrow;
+                    scr_ml[(wi * P_GMAX + r0) * 2 + 1] = lrow;
+                }
+            }
+            named_bar_sync(1, 2 * P_NCW * 32);
+            // cross-warp merge: thread t handles (head e of the pair, q head h, 4 columns)
+            const int tid = threadIdx.x;  // 0..191
+            const bool split = d.S > 1;
+            for (int idx = tid; idx < 2 * p.G * (HD / 4); idx += 2 * P_NCW * 32) {
+                const int ee = idx / (p.G * (HD / 4));
+                const int h = (idx / (HD / 4)) % p.G, c = (idx % (HD / 4)) * 4;
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < P_NCW; ++w) M = fmaxf(M, scr_ml[((w * 2 + ee) * P_GMAX + h) * 2]);
+                float L = 0.f;
+                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int w = 0; w < P_NCW; ++w) {
+                    const int wj = w * 2 + ee;
+                    const float mw = scr_ml[(wj * P_GMAX + h) * 2];
+                    const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
+                    L += f * scr_ml[(wj * P_GMAX + h) * 2 + 1];
+                    const float4 a = *reinterpret_cast<const float4*>(scr_acc + (wj * P_GMAX + h) * HD + c);
+                    o.x += f * a.x;
+                    o.y += f * a.y;
+                    o.z += f * a.z;
+                    o.w += f * a.w;
+                }
+                const int hq = (d.g + ee) * p.G + h;
+                if (!split) {
+                    const float inv = 1.f / L;
+                    const size_t off = p.out_head_major ? (((size_t)hq * p.B + d.b) * HD + c)
+                                                        : (((size_t)d.b * p.Hq + hq) * HD + c);
+                    uint2 v;
+                    v.x = pack_bf16(o.x * inv, o.y * inv);
+                    v.y = pack_bf16(o.z * inv, o.w * inv);
+                    *reinterpret_cast<uint2*>(p.out + off) = v;
+                } else {
+                    const size_t pi = ((size_t)d.b * p.Hq + hq) * p.S_max + d.s;
+                    *reinterpret_cast<float4*>(p.ws_acc + pi * HD + c) = o;
+                    if (c == 0) {
+                        p.ws_m[pi] = M;
+                        p.ws_l[pi] = L;
+                    }
+                }
+            }
+            if (split) {
+                __threadfence();
+                named_bar_sync(1, 2 * P_NCW * 32);
+                if (tid == 0) *s_last = atomicAdd(p.ws_cnt + d.b * p.Hkv + d.g, 1) == d.S - 1;
+                named_bar_sync(1, 2 * P_NCW * 32);
+                if (*s_last) {
+                    __threadfence();
+                    for (int idx = tid; idx < 2 * p.G * (HD / 4); idx += 2 * P_NCW * 32) {
+                        const int ee = idx / (p.G * (HD / 4));
+                        const int h = (idx / (HD / 4)) % p.G, c = (idx % (HD / 4)) * 4;
+                        const int hq = (d.g + ee) * p.G + h;
+                        const size_t pb = ((size_t)d.b * p.Hq + hq) * p.S_max;
+                        float M = -INFINITY;
+                        for (int sI = 0; sI < d.S; ++sI) M = fmaxf(M, __ldcg(p.ws_m + pb + sI));
+                        float L = 0.f;
+                        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int sI = 0; sI < d.S; ++sI) {
+                            const float f = fast_exp2(__ldcg(p.ws_m + pb + sI) - M);
+                            L += f * __ldcg(p.ws_l + pb + sI);
+                            const float4 a = __ldcg(reinterpret_cast<const float4*>(p.ws_acc + (pb + sI) * HD + c));
+                            o.x += f * a.x;
+                            o.y += f * a.y;
+                            o.z += f * a.z;
+                            o.w += f * a.w;
+                        }
+                        const float inv = 1.f / L;
+                        const size_t off = p.out_head_major ? (((size_t)hq * p.B + d.b) * HD + c)
+                                                            : (((size_t)d.b * p.Hq + hq) * HD + c);
+                        uint2 v;
+                        v.x = pack_bf16(o.x * inv, o.y * inv);
+                        v.y = pack_bf16(o.z * inv, o.w * inv);
+                        *reinterpret_cast<uint2*>(p.out + off) = v;
+                    }
+                    if (tid == 0) p.ws_cnt[d.b * p.Hkv + d.g] = 0;
+                }
+            }
+            named_bar_sync(1, 2 * P_NCW * 32);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(p.sched + 1, 1u);
+        if (done == gridDim.x - 1) {
+            p.sched[0] = 0u;
+            p.sched[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+size_t decode_pair_smem_bytes() {
+    return 1024 + P_NSTAGE * P_STAGE + 2 * P_NCW * P_GMAX * HD * 4 + 2 * P_NCW * P_GMAX * 2 * 4 +
+           (2 * P_NSTAGE + 4) * 8 + 2 * sizeof(UnitDesc) + 16;
+}
+
 size_t decode_smem_bytes() {
     return 1024 + NSTAGE * STAGE_BYTES + NCW * 16 * HD * 4 + NCW * 16 * 2 * 4 +
            (2 * NSTAGE + 4) * 8 + 2 * sizeof(UnitDesc) + 16;
@@ -587,6 +957,29 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     prm.out_head_major = out_head_major;
     prm.scale_log2 = softmax_scale * LOG2E;
     prm.trace = spd_trace(pool);
+    // head-pair kernel only when the batch alone gives >= 2 x 148 units: with fewer, the
+    // coarser units cost more in grid-tail imbalance than the bigger boxes gain.
+    // A shape-only rule, so the kernel choice never depends on the SM budget (R26).
+    if (pool->have_pair_maps && prm.G <= P_GMAX && c.num_kv_heads % 2 == 0 &&
+        batch * (c.num_kv_heads / 2) >= 2 * 148 && !pool->force_single) {
+        // head-pair kernel: one 32 KiB TMA box per tensor per stage
+        const int pairs = batch * (c.num_kv_heads / 2);
+        prm.n_units = pairs * S_max;
+        const size_t smem = decode_pair_smem_bytes();
+        static bool attr_pair = false;
+        if (!attr_pair) {
+            if (cudaFuncSetAttribute(decode_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem) != cudaSuccess)
+                return SEMIPD_ERR_CUDA;
+            attr_pair = true;
+        }
+        int grid = budget > 0 ? budget : prm.n_units;
+        if (grid > prm.n_units) grid = prm.n_units;
+        decode_pair_kernel<<<grid, P_NTHREADS, smem, st>>>(pool->dkmap2[layer], pool->dvmap2[layer], prm);
+        if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
+        pool->launches += 1;
+        return SEMIPD_OK;
+    }
     const size_t smem = decode_smem_bytes();
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;

@@ -9,6 +9,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include <cstdlib>
 
 namespace {
 
@@ -229,6 +230,24 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
             dok = dok && okd;
         }
         p->have_dmaps = dok;
+        if (dok && cfg->block_size >= 64 && cfg->num_kv_heads % 2 == 0 && cfg->head_dim_k == 128 &&
+            cfg->head_dim_v == 128 && !cfg->kv_shared) {
+            p->dkmap2.resize(cfg->num_layers);
+            p->dvmap2.resize(cfg->num_layers);
+            bool pok = true;
+            for (int l = 0; l < cfg->num_layers && pok; ++l) {
+                const uint64_t r = 256;
+                const uint64_t dd[4] = {64, (uint64_t)cfg->block_size, 2, pages};
+                const uint64_t ds[3] = {r, 128, r * cfg->block_size};
+                const uint32_t db[4] = {64, 64, 2, 2};
+                pok = spd_encode_tiled_4d(&p->dkmap2[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                          p->k_layer(l), dd, ds, db, CU_TENSOR_MAP_SWIZZLE_128B) &&
+                      spd_encode_tiled_4d(&p->dvmap2[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                          p->v_layer(l), dd, ds, db, CU_TENSOR_MAP_SWIZZLE_128B);
+            }
+            p->have_pair_maps = pok;
+            p->force_single = getenv("SEMIPD_DECODE_SINGLE") != nullptr;  // A/B debugging only
+        }
         if (cfg->kv_shared && cfg->block_size % 32 == 0 && pow2) {
             p->mla_kmap.resize(cfg->num_layers);
             bool mok = true;

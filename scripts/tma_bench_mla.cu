@@ -19,9 +19,10 @@ __global__ void __launch_bounds__(64, 1)
           long long* out) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    __shared__ uint64_t full[8];
+    __shared__ uint64_t full[16];
     const int box_bytes = NB * 64 * 128;
-    const int per_page = (9 + NB - 1) / NB;
+    const int ncb = (8 % NB == 0) ? 8 : 9;
+    const int per_page = (ncb + NB - 1) / NB;
     if (threadIdx.x == 0) {
         for (int i = 0; i < stages; ++i) mbar_init(&full[i], 1);
         fence_mbar_init();
@@ -56,7 +57,8 @@ int main(int argc, char** argv) {
     const int grid = argc > 2 ? atoi(argv[2]) : 148;
     const int stages = argc > 3 ? atoi(argv[3]) : 4;
     const int layout = argc > 4 ? atoi(argv[4]) : 0;
-    const int per_page = (9 + NB - 1) / NB;
+    const int ncb = (8 % NB == 0) ? 8 : 9;  // NB | 8: boxes never leave the page (no OOB fill)
+    const int per_page = (ncb + NB - 1) / NB;
     const int nbox = 600 * per_page;
     void* encp;
     cudaDriverEntryPointQueryResult q;
@@ -70,7 +72,7 @@ int main(int argc, char** argv) {
     cudaMalloc(&buf, bytes);
     cudaMemset(buf, 1, bytes);
     CUtensorMap map;
-    cuuint64_t dims[4] = {64, 64, 9, (cuuint64_t)pages};
+    cuuint64_t dims[4] = {64, 64, (cuuint64_t)ncb, (cuuint64_t)pages};
     cuuint64_t str0[3] = {1152, 128, 64 * 1152};
     cuuint64_t str1[3] = {128, 64 * 128, 64 * 1152};
     cuuint32_t box[4] = {64, 64, (cuuint32_t)NB, 1};

@@ -262,6 +262,58 @@ def test_decode_full_size_cfg2():
     run_decode(small(SHAPE_8B), [2048] * 64, seed=1020, dist=synth.FLAT)
 
 
+def test_decode_full_size_cfg2_bench_pages():
+    """The bench's configuration: cfg2 decode at full size with 64-token pages (the
+    head-pair kernel), all rows."""
+    run_decode(small(SHAPE_8B, block_size=64), [2048] * 64, seed=1021, dist=synth.FLAT)
+
+
+def _pair_ctx(n, seed):
+    edges = [0, 1, 63, 64, 65, 127, 128, 700, 4095, 4096, 5000]
+    rng = np.random.default_rng(seed)
+    return [edges[i] if i < len(edges) else int(rng.integers(1, 600)) for i in range(n)]
+
+
+@pytest.mark.parametrize("dist", synth.DISTS)
+def test_decode_pair_kernel(dist):
+    """Head-pair kernel (64-token pages, even Hkv, >= 2 x 148 head-pair units): block edges,
+    ragged tails, > 1 split; B = 80 requests x 4 pairs."""
+    run_decode(small(SHAPE_8B, block_size=64), _pair_ctx(80, dist), seed=1030 + dist, dist=dist)
+
+
+@pytest.mark.parametrize("G,hkv,B", [(1, 2, 296), (8, 2, 300), (16, 2, 296), (4, 3, 200)])
+def test_decode_pair_kernel_groups(G, hkv, B):
+    """G <= 8 with even Hkv takes the head-pair kernel; G = 16 or odd Hkv the one-head one."""
+    shape = small(SHAPE_8B, num_q_heads=hkv * G, num_kv_heads=hkv, block_size=64)
+    run_decode(shape, _pair_ctx(B, G + hkv), seed=90 + G + hkv, dist=synth.PEAKED)
+
+
+def test_decode_pair_kernel_budgets_stress_and_kind():
+    shape = small(SHAPE_8B, block_size=128)
+    ctx = _pair_ctx(76, 7)
+    outs = [run_decode(shape, ctx, seed=19, dist=synth.NEEDLE, sm_budget=b)[0].cpu()
+            for b in [1, 2, 37, 148, -1] * 2]
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    from paper_2504_19867_b200 import KVPool, PoolConfig
+    dev = torch.device("cuda", 0)
+    B = 74
+    pool = KVPool(PoolConfig(1, 2 * B + 2, 64, 8, 128, 128, B + 1, 4), dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32(list(range(B))), i32([2] * B))
+    trace = torch.zeros(4 * 256, dtype=torch.int32, device=dev)
+    ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+    pool.set_trace(trace, ctr)
+    q = torch.randn(B, 32, 128, device=dev).bfloat16()
+    kn = torch.randn(B, 8, 128, device=dev).bfloat16()
+    out = torch.empty(B, 32, 128, dtype=torch.bfloat16, device=dev)
+    ws = pool.new_decode_workspace(B, 32, 100)
+    pool.decode_attn(0, q, kn, kn.clone(), i32(list(range(B))), i32([100] * B), 100, 0.08, out, ws)
+    torch.cuda.synchronize()
+    n = int(ctr.item())
+    assert set(trace[:4 * n].view(n, 4)[:, 3].cpu().tolist()) == {6}
+
+
 # ----------------------------------------------------------------------------- prefill
 def run_prefill(shape, chunks, prefixes, seed, dist, sm_budget=0, head_major=False,
                 rows_mask=None, layer=0, num_layers=1, rid_offset=0):
@@ -461,15 +513,16 @@ def test_prefill_then_decode_handoff():
 
 
 # ----------------------------------------------------------------------------- co-run
-def test_corun_bitwise_identical_and_disjoint_sms():
+@pytest.mark.parametrize("bs,dec_kind", [(16, 2), (64, 2)])
+def test_corun_bitwise_identical_and_disjoint_sms(bs, dec_kind):
     """Prefill (stream P) and decode (stream D) co-run on one pool with budgets
     (74, 74): outputs are bitwise identical to isolated runs and the two grids
     occupy disjoint SM sets (CTA %smid trace)."""
     from paper_2504_19867_b200 import KVPool, PoolConfig
     shape = small(SHAPE_8B)
     B, ctx, C = 32, 2048, 1024
-    nb_d, nb_p = ctx // 16 + 1, C // 16
-    cfg = PoolConfig(1, B * nb_d + nb_p + 4, 16, 8, 128, 128, B + 2, nb_d + 1)
+    nb_d, nb_p = ctx // bs + 1, C // bs
+    cfg = PoolConfig(1, B * nb_d + nb_p + 4, bs, 8, 128, 128, B + 2, nb_d + 1)
     pool = KVPool(cfg, 0)
     dev = pool.device
     rid_d = torch.arange(B, dtype=torch.int32, device=dev)
@@ -518,9 +571,10 @@ def test_corun_bitwise_identical_and_disjoint_sms():
     pre_sms = set(rec[rec[:, 0] == 1, 1].tolist())
     dec_sms = set(rec[rec[:, 0] == 2, 1].tolist())
     assert len(pre_sms) == 74 and len(dec_sms) == 74
-    # the tensor-core kernels ran (kind 1 = tcgen05 prefill, 2 = split-K decode)
+    # the tensor-core kernels ran (kind 1 = tcgen05 prefill, 2 = split-K decode, 6 = the
+    # head-pair split-K decode used with >= 64-token pages)
     assert set(rec[rec[:, 0] == 1, 3].tolist()) == {1}
-    assert set(rec[rec[:, 0] == 2, 3].tolist()) == {2}
+    assert set(rec[rec[:, 0] == 2, 3].tolist()) == {dec_kind}
     # Disjointness holds whenever the two persistent grids are resident together;
     # report the overlap (0 expected when both launch before either finishes).
     print("corun SM overlap:", len(pre_sms & dec_sms))

@@ -470,8 +470,9 @@ def main():
     for _ in range(2):
         w.corun_step(50, 50)
     sweep = []
-    for x in splits:
-        t = time_steps(lambda: w.corun_step(x, 100 - x), 1, dev, barrier)
+
+    def measure(x):
+        t = time_steps(lambda: w.corun_step(x, 100 - x), 2, dev, barrier) / 2
         if ws > 1:
             tt = torch.tensor([t], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -479,6 +480,14 @@ def main():
         sweep.append({"x": x, "y": 100 - x, "n_p": w.pool.sm_budgets()[0],
                       "n_d": w.pool.sm_budgets()[1],
                       "tokens_per_s": (PREFILL_TOKENS + DECODE_BATCH) / t, "ms": t * 1e3})
+
+    for x in splits:
+        measure(x)
+    if args.split is None:  # refine around the best coarse split (+-2.5 % = ~4 SMs)
+        x0 = max(sweep, key=lambda r: r["tokens_per_s"])["x"]
+        for x in (x0 - 2.5, x0 + 2.5):
+            if 0 < x < 100 and all(abs(r["x"] - x) > 1e-6 for r in sweep):
+                measure(x)
     best = max(sweep, key=lambda r: r["tokens_per_s"])
     x, y = best["x"], best["y"]
     for _ in range(W):

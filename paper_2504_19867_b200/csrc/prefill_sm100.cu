@@ -73,14 +73,12 @@ struct PrefillParams {
 };
 
 #ifdef SPD_TIMELINE
+// record slot = kind * 1024 + idx (plain stores, no atomics: keeps the pipeline unperturbed)
 #define TL_REC(a, b, c, d, e)                                                              \
     do {                                                                                   \
-        if (p.tl && blockIdx.x == 0) {                                                     \
-            const int _i = atomicAdd(p.tl_ctr, 1);                                         \
-            if (_i < 4096) {                                                               \
-                long long* _r = p.tl + 8 * _i;                                             \
-                _r[0] = a; _r[1] = b; _r[2] = c; _r[3] = d; _r[4] = e;                     \
-            }                                                                              \
+        if (p.tl && blockIdx.x == 0 && (b) < 1024) {                                       \
+            long long* _r = p.tl + 8 * ((a) * 1024 + (b));                                 \
+            _r[0] = a; _r[1] = b; _r[2] = c; _r[3] = d; _r[4] = e;                         \
         }                                                                                  \
     } while (0)
 #define TL_NOW() clock64()
@@ -94,7 +92,8 @@ struct Smem {
     unsigned char q[2][TILE_BYTES];
     unsigned char k[2][TILE_BYTES];
     unsigned char v[2][TILE_BYTES];
-    uint64_t q_full, q_empty;
+    unsigned char ostage[2][HALF_BYTES];  // per q tile: epilogue staging for TMA stores (64 cols)
+    uint64_t q_full, q_empty, q_issued;  // q_issued: V loads of a unit queue behind its Q
     uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
     uint64_t s_full[2], p_full[2];   // per q tile
     uint64_t o_full[2], o_empty[2];  // per q tile
@@ -112,7 +111,8 @@ __global__ void __launch_bounds__(NT, 1)
                       const __grid_constant__ CUtensorMap kmap,
                       const __grid_constant__ CUtensorMap vmap,
                       const __grid_constant__ CUtensorMap kcmap,
-                      const __grid_constant__ CUtensorMap vcmap, PrefillParams p) {
+                      const __grid_constant__ CUtensorMap vcmap,
+                      const __grid_constant__ CUtensorMap omap, PrefillParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = (int)warp_id();
@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (threadIdx.x == 0) {
         mbar_init(&sm.q_full, 1);
         mbar_init(&sm.q_empty, 1);
+        mbar_init(&sm.q_issued, 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&sm.k_full[s], 1);
             mbar_init(&sm.k_empty[s], 1);
@@ -209,14 +210,13 @@ __global__ void __launch_bounds__(NT, 1)
                 [[maybe_unused]] const long long tq0 = TL_NOW();
                 mbar_wait(&sm.q_empty, (nunit & 1) ^ 1);
                 TL_REC(30, nunit, tq0, TL_NOW(), 0);
+                // one 64 KiB box: (64 cols, G heads, 2 TQ tokens, 2 halves) lands as
+                // [half][tile A rows | tile B rows][128 B]
                 mbar_arrive_expect_tx(&sm.q_full, 2 * TILE_BYTES);
-#pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    tma_load_3d(sm.q[t], &qmap, &sm.q_full, 0, d.g * p.G, d.qrow0 + t * p.TQ);
-                    tma_load_3d(sm.q[t] + HALF_BYTES, &qmap, &sm.q_full, 64, d.g * p.G,
-                                d.qrow0 + t * p.TQ);
-                }
+                tma_load_4d(sm.q[0], &qmap, &sm.q_full, 0, d.g * p.G, d.qrow0, 0);
+                mbar_arrive(&sm.q_issued);
             }
+            if (kv && lane == 0) mbar_wait(&sm.q_issued, nunit & 1);  // keep V behind this Q
             ++nunit;
             const int* btr = p.bt + (size_t)d.btrow * p.MBR;
             const int last_page = (d.P - 1) >> p.lg_bs;  // prefix pages only
@@ -283,13 +283,15 @@ __global__ void __launch_bounds__(NT, 1)
                 tc_fence_after();
                 const int nA = d.nkv[0], nB = d.nkv[1];
                 auto issue_s = [&](int t, int it) {  // S_t = Q_t K^T (K stage of kv tile it)
-                    const uint32_t q_addr = smem_u32(sm.q[t]);
+                    // Q smem: [half][tile A | tile B][128 rows][128 B]; K: [half][128 rows]
+                    const uint32_t q_addr = smem_u32(sm.q[0]) + (uint32_t)t * HALF_BYTES;
                     const uint32_t k_addr = smem_u32(sm.k[it & 1]);
                     const uint32_t d_tmem = tmem + (uint32_t)(t * BN);
 #pragma unroll
                     for (int kk = 0; kk < HD / 16; ++kk) {
-                        const uint32_t off = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
-                        umma_ss(d_tmem, kmajor_desc(q_addr + off), kmajor_desc(k_addr + off),
+                        const uint32_t koff = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
+                        const uint32_t qoff = (kk >> 2) * TILE_BYTES + (kk & 3) * 32;
+                        umma_ss(d_tmem, kmajor_desc(q_addr + qoff), kmajor_desc(k_addr + koff),
                                 idesc_s, kk > 0 ? 1u : 0u);
                     }
                     umma_commit(&sm.s_full[t]);
@@ -412,6 +414,7 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t s_tmem = tmem + lane_base + (uint32_t)(t * BN);
         const uint32_t o_tmem = tmem + lane_base + 256u + (uint32_t)(t * HD);
         const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
+        [[maybe_unused]] int tl_tile = 0;  // SPD_TIMELINE record index
         int cnt = 0, nunit = 0;
         for (;;) {
             const int us = nunit & 1;
@@ -497,7 +500,8 @@ __global__ void __launch_bounds__(NT, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&sm.p_full[t]);
-                if (lane == 0 && q4 == 0) TL_REC(t, j, ts0, ts1, TL_NOW());
+                if (lane == 0 && q4 == 0) TL_REC(t, tl_tile, ts0, ts1, TL_NOW());
+                ++tl_tile;
             }
             // ---- epilogue: O / l -> bf16 -> global
             [[maybe_unused]] const long long te0 = TL_NOW();
@@ -510,23 +514,60 @@ __global__ void __launch_bounds__(NT, 1)
             const bool valid = tok < d.tv[t];
             const int hq = d.g * p.G + (r % p.G);
             const int trow = d.qrow0 + t * p.TQ + tok;
-            __nv_bfloat16* dst = p.out + (p.out_head_major
-                                              ? ((size_t)hq * p.T + trow) * HD
-                                              : ((size_t)trow * p.Hq + hq) * HD);
+            if (d.tv[t] == p.TQ) {
+                // full tile: rows -> swizzled smem staging -> one TMA store per 64-column half
+                // (per-thread 16-byte stores to 256-byte-strided rows were ~4k cycles and held
+                // up the next unit's Q load in the SM's memory path)
+                const int srow = p.out_head_major ? (r % p.G) * p.TQ + tok : r;
+                unsigned char* stg = sm.ostage[t];
+                const bool issuer = q4 == 0 && lane == 0;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t o[32];
-                tmem_ld32(o_tmem + c * 32, o);
-                tmem_wait_ld();
-                if (valid) {
+                for (int hh = 0; hh < 2; ++hh) {
+                    if (issuer) bulk_wait_group_read0();  // previous store has read the staging
+                    named_bar_sync(2 + t, 128);
+                    uint32_t o[2][32];
+                    tmem_ld32(o_tmem + hh * 64, o[0]);
+                    tmem_ld32(o_tmem + hh * 64 + 32, o[1]);
+                    tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 32; e += 8) {
+                    for (int c8 = 0; c8 < 8; ++c8) {
+                        const uint32_t* oo = &o[c8 >> 2][(c8 & 3) * 8];
                         uint4 v;
-                        v.x = pack_bf16(__uint_as_float(o[e + 0]) * inv, __uint_as_float(o[e + 1]) * inv);
-                        v.y = pack_bf16(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
-                        v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
-                        v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
-                        *reinterpret_cast<uint4*>(dst + c * 32 + e) = v;
+                        v.x = pack_bf16(__uint_as_float(oo[0]) * inv, __uint_as_float(oo[1]) * inv);
+                        v.y = pack_bf16(__uint_as_float(oo[2]) * inv, __uint_as_float(oo[3]) * inv);
+                        v.z = pack_bf16(__uint_as_float(oo[4]) * inv, __uint_as_float(oo[5]) * inv);
+                        v.w = pack_bf16(__uint_as_float(oo[6]) * inv, __uint_as_float(oo[7]) * inv);
+                        *reinterpret_cast<uint4*>(stg + srow * 128 + ((c8 ^ (srow & 7)) << 4)) = v;
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(2 + t, 128);
+                    if (issuer) {
+                        if (p.out_head_major)
+                            tma_store_3d(&omap, stg, hh * 64, d.qrow0 + t * p.TQ, d.g * p.G);
+                        else
+                            tma_store_3d(&omap, stg, hh * 64, d.g * p.G, d.qrow0 + t * p.TQ);
+                        bulk_commit_group();
+                    }
+                }
+            } else {
+                __nv_bfloat16* dst = p.out + (p.out_head_major
+                                                  ? ((size_t)hq * p.T + trow) * HD
+                                                  : ((size_t)trow * p.Hq + hq) * HD);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32(o_tmem + c * 32, o);
+                    tmem_wait_ld();
+                    if (valid) {
+#pragma unroll
+                        for (int e = 0; e < 32; e += 8) {
+                            uint4 v;
+                            v.x = pack_bf16(__uint_as_float(o[e + 0]) * inv, __uint_as_float(o[e + 1]) * inv);
+                            v.y = pack_bf16(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+                            v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+                            v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+                            *reinterpret_cast<uint4*>(dst + c * 32 + e) = v;
+                        }
                     }
                 }
             }
@@ -535,6 +576,7 @@ __global__ void __launch_bounds__(NT, 1)
             if (lane == 0 && q4 == 0) TL_REC(10 + t, nunit, te0, te1, TL_NOW());
             ++nunit;
         }
+        if (q4 == 0 && lane == 0) bulk_wait_group0();  // all TMA stores of this tile done
     }
     tc_fence_before();
     __syncthreads();
@@ -633,12 +675,18 @@ extern "C" semipd_status semipd_prefill_attn(
     prm.trace = spd_trace(pool);
     prm.tl = reinterpret_cast<long long*>(pool->timeline);
     prm.tl_ctr = pool->timeline_ctr;
+    // Q [T][Hq][128] as (64 cols, Hq heads, T tokens, 2 halves); box (64, G, 2 TQ, 2) = both q
+    // tiles of a unit in one 64 KiB TMA (a box costs ~800 cycles of the SM's TMA unit, so one
+    // big box instead of four 16 KiB ones)
     CUtensorMap qmap;
-    if (!spd_encode_tiled_3d(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(q), HD,
-                             (uint64_t)num_q_heads, (uint64_t)total_q, HD * 2,
-                             (uint64_t)num_q_heads * HD * 2, 64, (uint32_t)G, (uint32_t)TQ,
-                             CU_TENSOR_MAP_SWIZZLE_128B))
-        return SEMIPD_ERR_CUDA;
+    {
+        const uint64_t dims[4] = {64, (uint64_t)num_q_heads, (uint64_t)total_q, 2};
+        const uint64_t strides[3] = {HD * 2, (uint64_t)num_q_heads * HD * 2, 128};
+        const uint32_t box[4] = {64, (uint32_t)G, (uint32_t)(2 * TQ), 2};
+        if (!spd_encode_tiled_4d(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(q), dims,
+                                 strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+            return SEMIPD_ERR_CUDA;
+    }
     // chunk K / V straight from k_new / v_new: (dk, Hkv, T), box 64 cols x 1 head x 128 rows
     CUtensorMap kcmap, vcmap;
     const uint64_t kvrow = (uint64_t)c.num_kv_heads * HD * 2;
@@ -649,6 +697,20 @@ extern "C" semipd_status semipd_prefill_attn(
                              (uint64_t)c.num_kv_heads, (uint64_t)total_q, HD * 2, kvrow, 64, 1, BN,
                              CU_TENSOR_MAP_SWIZZLE_128B))
         return SEMIPD_ERR_CUDA;
+    // output map for the epilogue's TMA stores: token-major [T][Hq][128] box (64, G, TQ) or
+    // head-major [Hq][T][128] box (64, TQ, G)
+    CUtensorMap omap;
+    if (!out_head_major) {
+        if (!spd_encode_tiled_3d(&omap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, HD, (uint64_t)num_q_heads,
+                                 (uint64_t)total_q, HD * 2, (uint64_t)num_q_heads * HD * 2, 64,
+                                 (uint32_t)G, (uint32_t)TQ, CU_TENSOR_MAP_SWIZZLE_128B))
+            return SEMIPD_ERR_CUDA;
+    } else {
+        if (!spd_encode_tiled_3d(&omap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, HD, (uint64_t)total_q,
+                                 (uint64_t)num_q_heads, HD * 2, (uint64_t)total_q * HD * 2, 64,
+                                 (uint32_t)TQ, (uint32_t)G, CU_TENSOR_MAP_SWIZZLE_128B))
+            return SEMIPD_ERR_CUDA;
+    }
     const size_t smem = sizeof(Smem) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
@@ -660,7 +722,7 @@ extern "C" semipd_status semipd_prefill_attn(
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;
     prefill_tc_kernel<<<grid, NT, smem, st>>>(qmap, pool->kmap[layer], pool->vmap[layer], kcmap,
-                                              vcmap, prm);
+                                              vcmap, omap, prm);
     pool->launches += 1;
     return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }

@@ -10,7 +10,8 @@ lib_tl = os.path.join(_build.PKG, "libsemipd_tl.so")
 objs = []
 for src in _build.sources():
     obj = os.path.join(_build.BUILD, "tl_" + os.path.basename(src)[:-3] + ".o")
-    subprocess.check_call([_build.nvcc(), *_build.NVCC_FLAGS, "-DSPD_TIMELINE", "-c", src, "-o", obj],
+    extra = os.environ.get("TL_FLAGS", "").split()
+    subprocess.check_call([_build.nvcc(), *_build.NVCC_FLAGS, "-DSPD_TIMELINE", *extra, "-c", src, "-o", obj],
                           stderr=subprocess.DEVNULL)
     objs.append(obj)
 subprocess.check_call([_build.nvcc(), *_build.ARCH, "-shared", "-o", lib_tl, *objs])
@@ -27,19 +28,20 @@ i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)
 pool.alloc_blocks(i32([0]), i32([32]))
 q = torch.randn(C, Hq, d, device=dev).bfloat16(); k = torch.randn(C, Hkv, d, device=dev).bfloat16()
 v = torch.randn(C, Hkv, d, device=dev).bfloat16(); out = torch.empty_like(q)
-buf = torch.zeros(4096 * 8, dtype=torch.int64, device=dev); ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+buf = torch.zeros(32 * 1024 * 8, dtype=torch.int64, device=dev); ctr = torch.zeros(1, dtype=torch.int32, device=dev)
 for it in range(3):
     ctr.zero_()
+    buf.zero_()
     L.semipd_debug_set_timeline(pool.h, ctypes.c_void_p(buf.data_ptr()), ctypes.c_void_p(ctr.data_ptr()))
     pool.prefill_attn(0, q, k, v, i32([0, C]), i32([0]), i32([0]), C, C, 1 / math.sqrt(d), out, sm_budget=budget)
     torch.cuda.synchronize()
-n = min(int(ctr.item()), 4096)
-rec = buf[:8 * n].view(n, 8).cpu().tolist()
+rec = [r for r in buf.view(-1, 8).cpu().tolist() if r[2] != 0]
+n = len(rec)
 t0 = min(r[2] for r in rec)
 for r in rec:
     r[2:4] = [x - t0 if x else 0 for x in r[2:4]]
     if r[0] < 20:
         r[4] = r[4] - t0 if r[4] else 0
 rec.sort(key=lambda r: r[2])
-json.dump(rec, open(os.path.join(ROOT, "gpurun_out", "timeline.json"), "w"))
+json.dump(rec, open(os.path.join(ROOT, "gpurun_out", os.environ.get("TL_OUT", "timeline.json")), "w"))
 print("records", n)

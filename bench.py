@@ -68,6 +68,21 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- helpers
+def ncu_traffic(kernel: str):
+    """dram read + write bytes per launch of `kernel` from the newest committed ncu capture
+    (profiles/r*_ncu_traffic.json, written from an `ncu --set full` run of the same shapes)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
+    if not files:
+        return None
+    try:
+        with open(files[-1]) as f:
+            d = json.load(f)[kernel]
+        return int(d["dram_read_bytes"]) + int(d["dram_write_bytes"])
+    except Exception:
+        return None
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -513,14 +528,16 @@ def main():
     dominant = "decode" if dec_total >= pre_total else "prefill"
     roof_dec = {"kernel": "decode_bf16_kernel (split-K paged decode)", "bound": "hbm",
                 "achieved": dec_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": dec_gbs / hbm_peak,
-                "peak_kind": peak_kind, "traffic": None,
+                "peak_kind": peak_kind, "traffic": ncu_traffic("decode_bf16_kernel"),
+                "traffic_unit": "DRAM bytes per launch (ncu)",
                 "algorithmic_bytes_per_launch": w.decode_bytes_per_launch(),
                 "avg_launch_ms": dec_ms, "sm_budget": n_d}
     share = n_p / w.pool.num_sms
     roof_pre = {"kernel": "prefill_tc_kernel tcgen05 causal GQA (K/V pool write fused)", "bound": "tensor",
                 "achieved": pre_tfs, "peak": bf16_sus, "unit": "TFLOP/s",
                 "frac": pre_tfs / bf16_sus, "frac_share_scaled": pre_tfs / (bf16_sus * share),
-                "peak_kind": f"{peak_kind} sustained", "traffic": None,
+                "peak_kind": f"{peak_kind} sustained", "traffic": ncu_traffic("prefill_tc_kernel"),
+                "traffic_unit": "DRAM bytes per launch (ncu)",
                 "algorithmic_flops_per_launch": w.prefill_flops_per_launch(),
                 "avg_launch_ms": pre_ms, "sm_budget": n_p}
     extra = {}

@@ -473,22 +473,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // ---------------------------------------------------------------------------------------
-// Head-pair variant (pages of >= 64 tokens, even Hkv, G <= 8).  A TMA box costs ~800 cycles
-// of its SM's TMA unit regardless of size up to ~24 KiB, so 16 KiB boxes cap
-// an SM at ~20 B/clk.  Here a unit is (request, kv heads g0 and g0 + 1, split) and one 4-D box
-// covers the two adjacent (block, head) pages: 32 KiB of K + 32 KiB of V per 64-key stage,
-// 3-deep ring.  Consumers: 3 warp pairs; stage gs goes to pair gs % 3, warp 2p + e of the
-// pair handles head g0 + e (same per-head math as decode_bf16_kernel).
+// Wide-box variants (G <= 8).  A TMA box costs ~800 cycles of its SM's TMA unit regardless of
+// size up to ~24 KiB, so 16 KiB boxes cap an SM at ~20 B/clk.  Both variants
+// move 32 KiB of K + 32 KiB of V per stage in two boxes, 3-deep ring, 3 warp pairs: stage gs
+// goes to pair gs % 3 and warp 2p + e of the pair takes half e of the stage.
+//   MODE 0 (64-token pages, even Hkv): unit = (request, kv heads g0 and g0 + 1, split); a box
+//          covers the two adjacent (block, head) pages; half e = head g0 + e, 64 keys.
+//   MODE 1 (128-token pages): unit = (request, kv head, split); a box is one whole page,
+//          128 keys; half e = keys [64 e, 64 e + 64) of the stage.
+// Per-warp math is decode_bf16_kernel's; partials of the 6 warps merge in smem.
 constexpr int P_NCW = 3;                       // warp pairs (stage rotation)
 constexpr int P_NSTAGE = 3;
 constexpr int P_NTHREADS = (2 * P_NCW + 1) * 32;
 constexpr int P_STAGE = 4 * KV_BYTES;          // K(g0) K(g0+1) V(g0) V(g0+1)
 constexpr int P_GMAX = 8;
 
+template <int MODE>
 __global__ void __launch_bounds__(P_NTHREADS, 1)
     decode_pair_kernel(const __grid_constant__ CUtensorMap kmap2,
                        const __grid_constant__ CUtensorMap vmap2, DecodeParams p) {
-    constexpr int LG_R = 6;
+    constexpr int LG_R = MODE == 0 ? 6 : 7;   // rows per box (and per page in the stage)
+    constexpr int KPS_M = MODE == 0 ? 64 : 128;  // keys per stage
+    constexpr int NHU = MODE == 0 ? 2 : 1;       // kv heads per unit
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* ring = smem;                                                     // 3 x 64 KiB
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
 
     const int warp = (int)warp_id();
     const int lane = (int)lane_id();
-    const int NP = p.Hkv >> 1;  // head pairs
+    const int NP = MODE == 0 ? p.Hkv >> 1 : p.Hkv;  // head groups per request
     if (threadIdx.x == 0) {
         for (int i = 0; i < P_NSTAGE; ++i) {
             mbar_init(full + i, 1);
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
                 reinterpret_cast<int4*>(p.trace.buf)[slot] =
-                    make_int4(2, (int)smid(), (int)blockIdx.x, 6 /* kernel kind: head-pair split-K decode */);
+                    make_int4(2, (int)smid(), (int)blockIdx.x, 6 + MODE /* kernel kind: wide-box split-K decode */);
         }
     }
     __syncthreads();
@@ -542,12 +548,18 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             } else {
                 d.s = u / (p.B * NP);
                 d.b = (u / NP) % p.B;
-                d.g = 2 * (u % NP);  // first head of the pair
+                d.g = NHU * (u % NP);  // first head of the unit
                 const int ctx = __ldg(p.ctx_lens + d.b);
                 d.S = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
                 if (d.s >= d.S) continue;
-                split_range(ctx, d.S, d.s, d.k0, d.k1);
-                d.nst = (d.k1 - d.k0 + KPS - 1) / KPS;
+                {
+                    const int nk = ctx + 1;
+                    int len = (nk + d.S - 1) / d.S;
+                    len = (len + KPS_M - 1) / KPS_M * KPS_M;
+                    d.k0 = d.s * len;
+                    d.k1 = min(nk, d.k0 + len);
+                }
+                d.nst = (d.k1 - d.k0 + KPS_M - 1) / KPS_M;
                 while (gstage % P_NCW != 0) {  // align to the pair rotation (R26)
                     if (lane == 0) {
                         const int st = gstage % P_NSTAGE;
@@ -572,21 +584,29 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
             const int last_page = ctx >> p.lg_bs;
             if (d.s == d.S - 1) {
-                // fused append of both heads' K and V rows at slot ctx: lane l copies 16 B of
-                // (head l>>4 ... ) -- 2 heads x (K, V) x 16 chunks = 64 copies, 2 per lane
+                // fused append of the unit's heads' K and V rows at slot ctx (16 B per lane per
+                // copy; MODE 0: lanes 16-31 take the second head, MODE 1: they take V)
                 const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
                 if (blk >= 0 && blk < p.N_B) {
-                    const int c = lane & 15, e = lane >> 4;  // e: head of the pair
-                    const size_t slot = (((size_t)blk * p.Hkv + d.g + e) << p.lg_bs) + (ctx & bs_mask);
-                    const size_t src = ((size_t)d.b * p.Hkv + d.g + e) * (HD / 8);
-                    reinterpret_cast<uint4*>(p.k_pool)[slot * (HD / 8) + c] = __ldg(p.k_new + src + c);
-                    reinterpret_cast<uint4*>(p.v_pool)[slot * (HD / 8) + c] = __ldg(p.v_new + src + c);
+                    const int c = lane & 15, e = lane >> 4;
+                    if (MODE == 0) {
+                        const size_t slot = (((size_t)blk * p.Hkv + d.g + e) << p.lg_bs) + (ctx & bs_mask);
+                        const size_t src = ((size_t)d.b * p.Hkv + d.g + e) * (HD / 8);
+                        reinterpret_cast<uint4*>(p.k_pool)[slot * (HD / 8) + c] = __ldg(p.k_new + src + c);
+                        reinterpret_cast<uint4*>(p.v_pool)[slot * (HD / 8) + c] = __ldg(p.v_new + src + c);
+                    } else {
+                        const size_t slot = (((size_t)blk * p.Hkv + d.g) << p.lg_bs) + (ctx & bs_mask);
+                        const size_t src = ((size_t)d.b * p.Hkv + d.g) * (HD / 8);
+                        unsigned char* pool = e ? p.v_pool : p.k_pool;
+                        const uint4* nw = e ? p.v_new : p.k_new;
+                        reinterpret_cast<uint4*>(pool)[slot * (HD / 8) + c] = __ldg(nw + src + c);
+                    }
                     fence_proxy_async_global();
                 }
                 __syncwarp();
             }
             auto lookup = [&](int i) -> int {  // raw block id of stage i (-2: past the request)
-                const int page = (d.k0 + i * KPS) >> p.lg_bs;
+                const int page = (d.k0 + i * KPS_M) >> p.lg_bs;
                 if (i >= d.nst || page > last_page) return -2;
                 return page < p.MBR ? __ldg(btr + page) : -1;
             };
@@ -602,7 +622,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                     int z = oob_z;
                     if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
                     else if (blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
-                    const int y = (d.k0 + i * KPS) & bs_mask;
+                    const int y = (d.k0 + i * KPS_M) & bs_mask;
                     tma_load_4d(kst, &kmap2, full + st, 0, y, 0, z);
                     tma_load_4d(kst + 2 * KV_BYTES, &vmap2, full + st, 0, y, 0, z);
                 }
@@ -624,7 +644,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             if (lane == 0) mbar_arrive(uempty + us);
             ++nunit;
             if (d.b < 0) break;
-            const int g = d.g + e;
+            const int g = d.g + (MODE == 0 ? e : 0);
             uint32_t qa[8][4];
             {
                 const uint32_t* q32 = reinterpret_cast<const uint32_t*>(p.q);
@@ -655,13 +675,16 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                 const int gs = d.base + i;
                 const int st = gs % P_NSTAGE;
                 mbar_wait(full + st, (gs / P_NSTAGE) & 1);
-                const uint32_t kst = smem_u32(ring + st * P_STAGE) + e * KV_BYTES;
+                // MODE 0: [K g0 | K g0+1 | V g0 | V g0+1], 64-row pages; MODE 1: [K | V], one
+                // 128-row page each ([half][128 rows][128 B]); this warp's keys start at koff
+                const uint32_t kst = smem_u32(ring + st * P_STAGE) + (MODE == 0 ? e * KV_BYTES : 0);
                 const uint32_t vst = kst + 2 * KV_BYTES;
+                const int koff = MODE == 0 ? 0 : 64 * e;
                 float s[8][4];
 #pragma unroll
                 for (int nt = 0; nt < 8; ++nt) {
                     s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-                    const int key = nt * 8 + (lane & 7);
+                    const int key = koff + nt * 8 + (lane & 7);
 #pragma unroll
                     for (int kk = 0; kk < 8; kk += 2) {
                         const int ci = 2 * kk + (lane >> 3);
@@ -673,7 +696,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                                        qa[kk + 1][3], b2, b3);
                     }
                 }
-                const int kbase = d.k0 + i * KPS;
+                const int kbase = d.k0 + i * KPS_M + koff;
                 const bool tail = kbase + KPS > d.k1;
                 float mx = -INFINITY;
 #pragma unroll
@@ -687,6 +710,11 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                     }
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                if (MODE == 1 && mx == -INFINITY) {  // this half lies past the unit's last key
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + st);
+                    continue;
+                }
                 const float mnew = fmaxf(mrow, mx);
                 const float alpha = fast_exp2(mrow - mnew);
                 mrow = mnew;
@@ -711,7 +739,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                 }
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
-                    const int key = ks * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+                    const int key = koff + ks * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
 #pragma unroll
                     for (int nd = 0; nd < 16; nd += 2) {
                         const int ch = nd + (lane >> 4);
@@ -748,17 +776,19 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             // cross-warp merge: thread t handles (head e of the pair, q head h, 4 columns)
             const int tid = threadIdx.x;  // 0..191
             const bool split = d.S > 1;
-            for (int idx = tid; idx < 2 * p.G * (HD / 4); idx += 2 * P_NCW * 32) {
+            constexpr int WPH = 2 * P_NCW / NHU;  // warps per head
+            for (int idx = tid; idx < NHU * p.G * (HD / 4); idx += 2 * P_NCW * 32) {
                 const int ee = idx / (p.G * (HD / 4));
                 const int h = (idx / (HD / 4)) % p.G, c = (idx % (HD / 4)) * 4;
                 float M = -INFINITY;
 #pragma unroll
-                for (int w = 0; w < P_NCW; ++w) M = fmaxf(M, scr_ml[((w * 2 + ee) * P_GMAX + h) * 2]);
+                for (int w = 0; w < WPH; ++w)
+                    M = fmaxf(M, scr_ml[(((MODE == 0 ? w * 2 + ee : w)) * P_GMAX + h) * 2]);
                 float L = 0.f;
                 float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int w = 0; w < P_NCW; ++w) {
-                    const int wj = w * 2 + ee;
+                for (int w = 0; w < WPH; ++w) {
+                    const int wj = MODE == 0 ? w * 2 + ee : w;
                     const float mw = scr_ml[(wj * P_GMAX + h) * 2];
                     const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
                     L += f * scr_ml[(wj * P_GMAX + h) * 2 + 1];
@@ -793,7 +823,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                 named_bar_sync(1, 2 * P_NCW * 32);
                 if (*s_last) {
                     __threadfence();
-                    for (int idx = tid; idx < 2 * p.G * (HD / 4); idx += 2 * P_NCW * 32) {
+                    for (int idx = tid; idx < NHU * p.G * (HD / 4); idx += 2 * P_NCW * 32) {
                         const int ee = idx / (p.G * (HD / 4));
                         const int h = (idx / (HD / 4)) % p.G, c = (idx % (HD / 4)) * 4;
                         const int hq = (d.g + ee) * p.G + h;
@@ -957,25 +987,28 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     prm.out_head_major = out_head_major;
     prm.scale_log2 = softmax_scale * LOG2E;
     prm.trace = spd_trace(pool);
-    // head-pair kernel only when the batch alone gives >= 2 x 148 units: with fewer, the
-    // coarser units cost more in grid-tail imbalance than the bigger boxes gain.
-    // A shape-only rule, so the kernel choice never depends on the SM budget (R26).
-    if (pool->have_pair_maps && prm.G <= P_GMAX && c.num_kv_heads % 2 == 0 &&
-        batch * (c.num_kv_heads / 2) >= 2 * 148 && !pool->force_single) {
-        // head-pair kernel: one 32 KiB TMA box per tensor per stage
-        const int pairs = batch * (c.num_kv_heads / 2);
-        prm.n_units = pairs * S_max;
+    // wide-box kernels (G <= 8): 128-token pages always (MODE 1, one whole page per box);
+    // 64-token pages with even Hkv only when the batch alone gives >= 2 x 148 head-pair
+    // units (MODE 0: with fewer, the coarser units cost more in grid-tail imbalance than the
+    // bigger boxes gain).  Shape-only rules, so the kernel choice never depends on the SM
+    // budget (R26).
+    const bool mode1 = pool->have_wide_maps && c.block_size == 128 && prm.G <= P_GMAX;
+    const bool mode0 = pool->have_wide_maps && c.block_size == 64 && prm.G <= P_GMAX &&
+                       c.num_kv_heads % 2 == 0 && batch * (c.num_kv_heads / 2) >= 2 * 148;
+    if ((mode0 || mode1) && !pool->force_single) {
+        prm.n_units = batch * (mode0 ? c.num_kv_heads / 2 : c.num_kv_heads) * S_max;
         const size_t smem = decode_pair_smem_bytes();
-        static bool attr_pair = false;
-        if (!attr_pair) {
-            if (cudaFuncSetAttribute(decode_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem) != cudaSuccess)
+        static bool attr_pair[2] = {false, false};
+        auto kern = mode0 ? decode_pair_kernel<0> : decode_pair_kernel<1>;
+        if (!attr_pair[mode1]) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess)
                 return SEMIPD_ERR_CUDA;
-            attr_pair = true;
+            attr_pair[mode1] = true;
         }
         int grid = budget > 0 ? budget : prm.n_units;
         if (grid > prm.n_units) grid = prm.n_units;
-        decode_pair_kernel<<<grid, P_NTHREADS, smem, st>>>(pool->dkmap2[layer], pool->dvmap2[layer], prm);
+        kern<<<grid, P_NTHREADS, smem, st>>>(pool->dkmap2[layer], pool->dvmap2[layer], prm);
         if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
         pool->launches += 1;
         return SEMIPD_OK;

@@ -43,10 +43,10 @@ struct semipd_pool {
     std::vector<CUtensorMap> dkmap, dvmap;
     bool have_maps = false;   // 3-D page maps (prefill)
     bool have_dmaps = false;  // 4-D page maps (decode)
-    // decode head-pair maps (bs >= 64, even Hkv): box = 64 rows x 128 columns x 2 adjacent
-    // (block, head) pages = 32 KiB
+    // decode wide-box maps, 32 KiB per box: bs 64 with even Hkv -> 64 rows x 128 columns x 2
+    // adjacent (block, head) pages; bs 128 -> one whole 128-row page
     std::vector<CUtensorMap> dkmap2, dvmap2;
-    bool have_pair_maps = false;
+    bool have_wide_maps = false;
     bool force_single = false;  // debug/bench: keep the one-head decode kernel
     // MLA latent pool (kv_shared): 4-D (64 cols, rows, dk/64 blocks, pages), box 32 rows x all
     // column blocks (one 36 KiB TMA per 32-key stage at dk = 576)

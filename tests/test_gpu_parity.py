@@ -289,7 +289,7 @@ def test_decode_pair_kernel_groups(G, hkv, B):
 
 
 def test_decode_pair_kernel_budgets_stress_and_kind():
-    shape = small(SHAPE_8B, block_size=128)
+    shape = small(SHAPE_8B, block_size=64)
     ctx = _pair_ctx(76, 7)
     outs = [run_decode(shape, ctx, seed=19, dist=synth.NEEDLE, sm_budget=b)[0].cpu()
             for b in [1, 2, 37, 148, -1] * 2]
@@ -312,6 +312,41 @@ def test_decode_pair_kernel_budgets_stress_and_kind():
     torch.cuda.synchronize()
     n = int(ctr.item())
     assert set(trace[:4 * n].view(n, 4)[:, 3].cpu().tolist()) == {6}
+
+
+@pytest.mark.parametrize("dist", synth.DISTS)
+def test_decode_page128_kernel(dist):
+    """128-token pages take the whole-page-box kernel (MODE 1): keys split over two warps per
+    stage, including stages whose second half lies past the last key."""
+    run_decode(small(SHAPE_8B, block_size=128), [0, 1, 63, 64, 65, 127, 128, 129, 700, 4096, 9000],
+               seed=1040 + dist, dist=dist)
+
+
+def test_decode_page128_kind_groups_budgets():
+    for G in (1, 8, 16):
+        shape = small(SHAPE_8B, num_q_heads=2 * G, num_kv_heads=2, block_size=128)
+        run_decode(shape, [33, 700, 5000], seed=95 + G, dist=synth.VSHIFT)
+    shape = small(SHAPE_8B, block_size=128)
+    outs = [run_decode(shape, [5, 70, 130, 4100, 63, 200, 9000, 1], seed=21, dist=synth.NEEDLE,
+                       sm_budget=b)[0].cpu() for b in [1, 2, 37, 148, -1]]
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    from paper_2504_19867_b200 import KVPool, PoolConfig
+    dev = torch.device("cuda", 0)
+    pool = KVPool(PoolConfig(1, 8, 128, 8, 128, 128, 2, 4), dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32([0]), i32([2]))
+    trace = torch.zeros(4 * 256, dtype=torch.int32, device=dev)
+    ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+    pool.set_trace(trace, ctr)
+    q = torch.randn(1, 32, 128, device=dev).bfloat16()
+    kn = torch.randn(1, 8, 128, device=dev).bfloat16()
+    out = torch.empty(1, 32, 128, dtype=torch.bfloat16, device=dev)
+    ws = pool.new_decode_workspace(1, 32, 200)
+    pool.decode_attn(0, q, kn, kn.clone(), i32([0]), i32([200]), 200, 0.08, out, ws)
+    torch.cuda.synchronize()
+    n = int(ctr.item())
+    assert set(trace[:4 * n].view(n, 4)[:, 3].cpu().tolist()) == {7}
 
 
 # ----------------------------------------------------------------------------- prefill
@@ -513,7 +548,7 @@ def test_prefill_then_decode_handoff():
 
 
 # ----------------------------------------------------------------------------- co-run
-@pytest.mark.parametrize("bs,dec_kind", [(16, 2), (64, 2)])
+@pytest.mark.parametrize("bs,dec_kind", [(16, 2), (64, 2), (128, 7)])
 def test_corun_bitwise_identical_and_disjoint_sms(bs, dec_kind):
     """Prefill (stream P) and decode (stream D) co-run on one pool with budgets
     (74, 74): outputs are bitwise identical to isolated runs and the two grids

@@ -78,7 +78,7 @@ __device__ __forceinline__ uint32_t kv_off(int key, int h) {
            ((uint32_t)(key & ((1 << LG_R) - 1)) << 7);
 }
 
-template <int LG_R>
+template <int LG_R, bool SWAP>
 __global__ void __launch_bounds__(NTHREADS, 1)
     decode_bf16_kernel(const __grid_constant__ CUtensorMap kmap,
                        const __grid_constant__ CUtensorMap vmap, DecodeParams p) {
@@ -117,6 +117,89 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncthreads();
 
+    // cross-warp merge of the consumer warps' partials (scratch rows = q heads of the group),
+    // then the output (or the split partial and, by the last split, the split-order merge)
+    auto merge_and_store = [&](const UnitDesc& d) {
+        // ---- cross-warp merge: thread t handles (head h, 4 columns)
+        const int tid = threadIdx.x;  // 0..127
+        const bool split = d.S > 1;
+        for (int idx = tid; idx < p.G * (HD / 4); idx += NCW * 32) {
+            const int h = idx / (HD / 4), c = (idx % (HD / 4)) * 4;
+            float M = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) M = fmaxf(M, scr_ml[(w * 16 + h) * 2]);
+            float L = 0.f;
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) {
+                const float mw = scr_ml[(w * 16 + h) * 2];
+                const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
+                L += f * scr_ml[(w * 16 + h) * 2 + 1];
+                const float4 a = *reinterpret_cast<const float4*>(scr_acc + (w * 16 + h) * HD + c);
+                o.x += f * a.x;
+                o.y += f * a.y;
+                o.z += f * a.z;
+                o.w += f * a.w;
+            }
+            const int hq = d.g * p.G + h;
+            if (!split) {
+                const float inv = 1.f / L;
+                const size_t off = p.out_head_major ? (((size_t)hq * p.B + d.b) * HD + c)
+                                                    : (((size_t)d.b * p.Hq + hq) * HD + c);
+                uint2 v;
+                v.x = pack_bf16(o.x * inv, o.y * inv);
+                v.y = pack_bf16(o.z * inv, o.w * inv);
+                *reinterpret_cast<uint2*>(p.out + off) = v;
+            } else {
+                const size_t pi = ((size_t)d.b * p.Hq + hq) * p.S_max + d.s;
+                *reinterpret_cast<float4*>(p.ws_acc + pi * HD + c) = o;
+                if (c == 0) {
+                    p.ws_m[pi] = M;
+                    p.ws_l[pi] = L;
+                }
+            }
+        }
+        if (split) {
+            __threadfence();
+            named_bar_sync(1, NCW * 32);
+            if (tid == 0) {
+                const int prev = atomicAdd(p.ws_cnt + d.b * p.Hkv + d.g, 1);
+                *s_last = prev == d.S - 1;
+            }
+            named_bar_sync(1, NCW * 32);
+            if (*s_last) {
+                __threadfence();
+                // merge over splits in split-index order (flash-decoding)
+                for (int idx = tid; idx < p.G * (HD / 4); idx += NCW * 32) {
+                    const int h = idx / (HD / 4), c = (idx % (HD / 4)) * 4;
+                    const int hq = d.g * p.G + h;
+                    const size_t pb = ((size_t)d.b * p.Hq + hq) * p.S_max;
+                    float M = -INFINITY;
+                    for (int sI = 0; sI < d.S; ++sI) M = fmaxf(M, __ldcg(p.ws_m + pb + sI));
+                    float L = 0.f;
+                    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int sI = 0; sI < d.S; ++sI) {
+                        const float f = fast_exp2(__ldcg(p.ws_m + pb + sI) - M);
+                        L += f * __ldcg(p.ws_l + pb + sI);
+                        const float4 a = __ldcg(reinterpret_cast<const float4*>(p.ws_acc + (pb + sI) * HD + c));
+                        o.x += f * a.x;
+                        o.y += f * a.y;
+                        o.z += f * a.z;
+                        o.w += f * a.w;
+                    }
+                    const float inv = 1.f / L;
+                    const size_t off = p.out_head_major ? (((size_t)hq * p.B + d.b) * HD + c)
+                                                        : (((size_t)d.b * p.Hq + hq) * HD + c);
+                    uint2 v;
+                    v.x = pack_bf16(o.x * inv, o.y * inv);
+                    v.y = pack_bf16(o.z * inv, o.w * inv);
+                    *reinterpret_cast<uint2*>(p.out + off) = v;
+                }
+                if (tid == 0) p.ws_cnt[d.b * p.Hkv + d.g] = 0;  // ready for the next call
+            }
+        }
+        named_bar_sync(1, NCW * 32);  // scratch reuse
+    };
     if (warp == NCW) {
         // =========================== producer ===========================
         // Whole warp: lane l holds the raw block id of box (32*batch + l) of the unit,
@@ -222,6 +305,159 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 __syncwarp();
             }
+        }
+    } else if (SWAP) {
+        // ================= consumers, swap-AB (G <= 8): heads are the MMA N =================
+        // S^T[16 keys x 8 heads] = K . Q^T and O^T[16 dv x 8 heads] += V^T . P^T with
+        // m16n8k16: half the MMAs of the q-heads-as-M form, which pads G <= 8 rows to 16.
+        // The C fragment of S^T is turned into the B fragment of P^T by an 8x8 transpose.
+        const int kr = lane >> 2;         // key (S^T) / dv (O^T) row within an 8-row block
+        const int hc = (lane & 3) * 2;    // heads hc, hc + 1 of this thread's C values
+        int nunit = 0;
+        int next_gs = warp;
+        for (;;) {
+            const int us = nunit & 1;
+            mbar_wait(ufull + us, (nunit >> 1) & 1);
+            const UnitDesc d = units[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(uempty + us);
+            ++nunit;
+            if (d.b < 0) break;
+            // Q^T B fragments: head n = lane / 4, dims 16 kk + 2 (lane % 4) (+8)
+            uint32_t qb[8][2];
+            {
+                const uint32_t* q32 = reinterpret_cast<const uint32_t*>(p.q);
+                const bool v = kr < p.G;
+                const size_t row = ((size_t)d.b * p.Hq + d.g * p.G + kr) * (HD / 2);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int col = (kk * 16 + hc) >> 1;
+                    qb[kk][0] = v ? __ldg(q32 + row + col) : 0u;
+                    qb[kk][1] = v ? __ldg(q32 + row + col + 4) : 0u;
+                }
+            }
+            float acc[8][4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+            float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+            while (next_gs < d.base) {
+                const int st = next_gs % NSTAGE;
+                mbar_wait(full + st, (next_gs / NSTAGE) & 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + st);
+                next_gs += NCW;
+            }
+            next_gs = d.base + (warp < d.nst ? warp + ((d.nst - 1 - warp) / NCW + 1) * NCW : warp);
+            const int lm = lane >> 3, lr = lane & 7;  // ldmatrix: matrix / row of this lane
+            for (int i = warp; i < d.nst; i += NCW) {
+                const int gs = d.base + i;
+                const int st = gs % NSTAGE;
+                mbar_wait(full + st, (gs / NSTAGE) & 1);
+                const uint32_t kst = smem_u32(ring + st * STAGE_BYTES);
+                const uint32_t vst = kst + KV_BYTES;
+                // ---- S^T: 4 key tiles x 8 k-steps; A = K rows (keys) via ldmatrix
+                float s[4][4];
+#pragma unroll
+                for (int kt = 0; kt < 4; ++kt) {
+                    s[kt][0] = s[kt][1] = s[kt][2] = s[kt][3] = 0.f;
+                    const int key = kt * 16 + (lm & 1) * 8 + lr;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const int ci = kk * 2 + (lm >> 1);  // 16-byte chunk (dims / 8)
+                        uint32_t a0, a1, a2, a3;
+                        ldsm_x4(kst + kv_off<LG_R>(key, ci >> 3) + (((ci & 7) ^ (key & 7)) << 4), a0, a1,
+                                a2, a3);
+                        mma_bf16_16816(s[kt], a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+                    }
+                }
+                // ---- mask + online softmax over keys, per head (log2 domain)
+                const int kbase = d.k0 + i * KPS;
+                const bool tail = kbase + KPS > d.k1;
+                float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+                for (int kt = 0; kt < 4; ++kt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        float x = s[kt][e] * p.scale_log2;
+                        if (tail && kbase + kt * 16 + kr + (e >> 1) * 8 >= d.k1) x = -INFINITY;
+                        s[kt][e] = x;
+                        mx[e & 1] = fmaxf(mx[e & 1], x);
+                    }
+                float alpha[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    mx[j] = fmaxf(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], 4));
+                    mx[j] = fmaxf(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], 8));
+                    mx[j] = fmaxf(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], 16));
+                    const float mnew = fmaxf(mrow[j], mx[j]);
+                    alpha[j] = fast_exp2(mrow[j] - mnew);
+                    mrow[j] = mnew;
+                }
+                float ls[2] = {0.f, 0.f};
+                uint32_t pb[4][2];
+#pragma unroll
+                for (int kt = 0; kt < 4; ++kt) {
+                    const float p0 = fast_exp2(s[kt][0] - mrow[0]);
+                    const float p1 = fast_exp2(s[kt][1] - mrow[1]);
+                    const float p2 = fast_exp2(s[kt][2] - mrow[0]);
+                    const float p3 = fast_exp2(s[kt][3] - mrow[1]);
+                    ls[0] += p0 + p2;
+                    ls[1] += p1 + p3;
+                    // C (key row, head cols) -> B (key k, head n): 8x8 transposes
+                    pb[kt][0] = movmatrix_t(pack_bf16(p0, p1));
+                    pb[kt][1] = movmatrix_t(pack_bf16(p2, p3));
+                }
+                lrow[0] = lrow[0] * alpha[0] + ls[0];
+                lrow[1] = lrow[1] * alpha[1] + ls[1];
+                if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
+#pragma unroll
+                    for (int dt = 0; dt < 8; ++dt) {
+                        acc[dt][0] *= alpha[0];
+                        acc[dt][1] *= alpha[1];
+                        acc[dt][2] *= alpha[0];
+                        acc[dt][3] *= alpha[1];
+                    }
+                }
+                // ---- O^T += V^T P^T: 8 dv tiles x 4 key steps; A = V^T via ldmatrix.trans
+#pragma unroll
+                for (int kt = 0; kt < 4; ++kt) {
+                    const int key = kt * 16 + (lm >> 1) * 8 + lr;
+#pragma unroll
+                    for (int dt = 0; dt < 8; ++dt) {
+                        const int ch = dt * 2 + (lm & 1);
+                        uint32_t a0, a1, a2, a3;
+                        ldsm_x4_t(vst + kv_off<LG_R>(key, ch >> 3) + (((ch & 7) ^ (key & 7)) << 4), a0, a1,
+                                  a2, a3);
+                        mma_bf16_16816(acc[dt], a0, a1, a2, a3, pb[kt][0], pb[kt][1]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + st);
+            }
+            // ---- per-warp partial -> shared scratch (rows = heads)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                lrow[j] += __shfl_xor_sync(0xffffffffu, lrow[j], 4);
+                lrow[j] += __shfl_xor_sync(0xffffffffu, lrow[j], 8);
+                lrow[j] += __shfl_xor_sync(0xffffffffu, lrow[j], 16);
+            }
+            float* wacc = scr_acc + warp * 16 * HD;
+#pragma unroll
+            for (int dt = 0; dt < 8; ++dt) {
+                const int dv = dt * 16 + kr;
+                wacc[hc * HD + dv] = acc[dt][0];
+                wacc[(hc + 1) * HD + dv] = acc[dt][1];
+                wacc[hc * HD + dv + 8] = acc[dt][2];
+                wacc[(hc + 1) * HD + dv + 8] = acc[dt][3];
+            }
+            if (kr == 0) {
+                scr_ml[(warp * 16 + hc) * 2 + 0] = mrow[0];
+                scr_ml[(warp * 16 + hc) * 2 + 1] = lrow[0];
+                scr_ml[(warp * 16 + hc + 1) * 2 + 0] = mrow[1];
+                scr_ml[(warp * 16 + hc + 1) * 2 + 1] = lrow[1];
+            }
+            named_bar_sync(1, NCW * 32);
+            merge_and_store(d);
         }
     } else {
         // =========================== consumers ===========================
@@ -379,85 +615,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 scr_ml[(warp * 16 + r0 + 8) * 2 + 1] = lrow[1];
             }
             named_bar_sync(1, NCW * 32);
-            // ---- cross-warp merge: thread t handles (head h, 4 columns)
-            const int tid = threadIdx.x;  // 0..127
-            const bool split = d.S > 1;
-            for (int idx = tid; idx < p.G * (HD / 4); idx += NCW * 32) {
-                const int h = idx / (HD / 4), c = (idx % (HD / 4)) * 4;
-                float M = -INFINITY;
-#pragma unroll
-                for (int w = 0; w < NCW; ++w) M = fmaxf(M, scr_ml[(w * 16 + h) * 2]);
-                float L = 0.f;
-                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int w = 0; w < NCW; ++w) {
-                    const float mw = scr_ml[(w * 16 + h) * 2];
-                    const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
-                    L += f * scr_ml[(w * 16 + h) * 2 + 1];
-                    const float4 a = *reinterpret_cast<const float4*>(scr_acc + (w * 16 + h) * HD + c);
-                    o.x += f * a.x;
-                    o.y += f * a.y;
-                    o.z += f * a.z;
-                    o.w += f * a.w;
-                }
-                const int hq = d.g * p.G + h;
-                if (!split) {
-                    const float inv = 1.f / L;
-                    const size_t off = p.out_head_major ? (((size_t)hq * p.B + d.b) * HD + c)
-                                                        : (((size_t)d.b * p.Hq + hq) * HD + c);
-                    uint2 v;
-                    v.x = pack_bf16(o.x * inv, o.y * inv);
-                    v.y = pack_bf16(o.z * inv, o.w * inv);
-                    *reinterpret_cast<uint2*>(p.out + off) = v;
-                } else {
-                    const size_t pi = ((size_t)d.b * p.Hq + hq) * p.S_max + d.s;
-                    *reinterpret_cast<float4*>(p.ws_acc + pi * HD + c) = o;
-                    if (c == 0) {
-                        p.ws_m[pi] = M;
-                        p.ws_l[pi] = L;
-                    }
-                }
-            }
-            if (split) {
-                __threadfence();
-                named_bar_sync(1, NCW * 32);
-                if (tid == 0) {
-                    const int prev = atomicAdd(p.ws_cnt + d.b * p.Hkv + d.g, 1);
-                    *s_last = prev == d.S - 1;
-                }
-                named_bar_sync(1, NCW * 32);
-                if (*s_last) {
-                    __threadfence();
-                    // merge over splits in split-index order (flash-decoding)
-                    for (int idx = tid; idx < p.G * (HD / 4); idx += NCW * 32) {
-                        const int h = idx / (HD / 4), c = (idx % (HD / 4)) * 4;
-                        const int hq = d.g * p.G + h;
-                        const size_t pb = ((size_t)d.b * p.Hq + hq) * p.S_max;
-                        float M = -INFINITY;
-                        for (int sI = 0; sI < d.S; ++sI) M = fmaxf(M, __ldcg(p.ws_m + pb + sI));
-                        float L = 0.f;
-                        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-                        for (int sI = 0; sI < d.S; ++sI) {
-                            const float f = fast_exp2(__ldcg(p.ws_m + pb + sI) - M);
-                            L += f * __ldcg(p.ws_l + pb + sI);
-                            const float4 a = __ldcg(reinterpret_cast<const float4*>(p.ws_acc + (pb + sI) * HD + c));
-                            o.x += f * a.x;
-                            o.y += f * a.y;
-                            o.z += f * a.z;
-                            o.w += f * a.w;
-                        }
-                        const float inv = 1.f / L;
-                        const size_t off = p.out_head_major ? (((size_t)hq * p.B + d.b) * HD + c)
-                                                            : (((size_t)d.b * p.Hq + hq) * HD + c);
-                        uint2 v;
-                        v.x = pack_bf16(o.x * inv, o.y * inv);
-                        v.y = pack_bf16(o.z * inv, o.w * inv);
-                        *reinterpret_cast<uint2*>(p.out + off) = v;
-                    }
-                    if (tid == 0) p.ws_cnt[d.b * p.Hkv + d.g] = 0;  // ready for the next call
-                }
-            }
-            named_bar_sync(1, NCW * 32);  // scratch reuse
+            merge_and_store(d);
         }
     }
     __syncthreads();
@@ -1019,18 +1177,20 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     const int lg_r = __builtin_ctz((unsigned)pool->dbox_rows);
     cudaError_t e = cudaSuccess;
     auto launch = [&](auto kern) {
-        static bool attr_set[3] = {false, false, false};
-        if (!attr_set[lg_r - 4]) {
+        static bool attr_set[6] = {false, false, false, false, false, false};
+        const int ai = (lg_r - 4) * 2 + (prm.G <= 8);
+        if (!attr_set[ai]) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return;
-            attr_set[lg_r - 4] = true;
+            attr_set[ai] = true;
         }
         kern<<<grid, NTHREADS, smem, st>>>(pool->dkmap[layer], pool->dvmap[layer], prm);
         e = cudaGetLastError();
     };
-    if (lg_r == 4) launch(decode_bf16_kernel<4>);
-    else if (lg_r == 5) launch(decode_bf16_kernel<5>);
-    else launch(decode_bf16_kernel<6>);
+    const bool swap = prm.G <= 8;  // heads fit the MMA N = 8: swap-AB consumers
+    if (lg_r == 4) swap ? launch(decode_bf16_kernel<4, true>) : launch(decode_bf16_kernel<4, false>);
+    else if (lg_r == 5) swap ? launch(decode_bf16_kernel<5, true>) : launch(decode_bf16_kernel<5, false>);
+    else swap ? launch(decode_bf16_kernel<6, true>) : launch(decode_bf16_kernel<6, false>);
     if (e != cudaSuccess) return SEMIPD_ERR_CUDA;
     pool->launches += 1;
     return SEMIPD_OK;

@@ -510,7 +510,15 @@ def main():
     # ---- timed region
     launches0 = w.pool.launch_count()
     with ClockSampler(local) as clk:
-        t = time_steps(lambda: w.corun_step(x, y, timed=True), args.steps, dev, barrier)
+        # per-launch CUDA events only in the last timed step: an event pair between every
+        # back-to-back kernel costs ~3 us per launch on each stream
+        k_step = [0]
+
+        def step():
+            k_step[0] += 1
+            w.corun_step(x, y, timed=k_step[0] == args.steps)
+
+        t = time_steps(step, args.steps, dev, barrier)
     launches = w.pool.launch_count() - launches0
     if ws > 1:
         tt = torch.tensor([t], device=dev)

@@ -13,16 +13,15 @@ oracle.  Nothing here computes attention: every step runs in libsemipd's kernels
 """
 from __future__ import annotations
 
-import math
 from collections import deque
 from dataclasses import dataclass, field
 
 import torch
 
-from . import KVPool, blocks_for_tokens
+from . import KVPool
 
 
-@dataclass
+@dataclass(eq=False)  # identity: queues hold distinct requests
 class Request:
     trace_id: int
     input_len: int
@@ -32,6 +31,7 @@ class Request:
     generated: int = 0      # decode steps done
     nblk: int = 0           # blocks held (host mirror of the device table row)
     preempted: int = 0
+    admit_seq: int = -1     # order of the last slot grant (preemption picks the newest)
 
     @property
     def ctx(self) -> int:   # tokens cached before the next decode step (R5)
@@ -63,6 +63,123 @@ class Plan:
     decode: list = field(default_factory=list)    # (Request, ctx)
 
 
+class Scheduler:
+    """Host-side admission and block accounting of the co-run engine (no device work; unit
+    tested on CPU).  Mirrors the device allocator's free count exactly: every grant it plans
+    succeeds on the device (LIFO stack, all-or-nothing per call, R9/R10)."""
+
+    def __init__(self, num_blocks: int, block_size: int, max_reqs: int, *, chunk_budget: int = 2048,
+                 max_decode: int = 512):
+        self.bs = block_size
+        self.chunk_budget, self.max_decode = chunk_budget, max_decode
+        self.num_blocks = num_blocks
+        self.free_blocks = num_blocks
+        self.free_slots = deque(range(max_reqs))
+        self.waiting: deque[Request] = deque()     # arrived, prompt not fully prefilled (FCFS)
+        self.running: list[Request] = []           # prompt done, decoding (admission order)
+        self.finished: list[Request] = []
+        self.rejected: list[Request] = []        # can never fit the pool, even alone
+        self.n_admit = 0
+
+    def blocks(self, tokens: int) -> int:
+        return -(-tokens // self.bs)  # semipd_blocks_for_tokens (S:252-259)
+
+    def add(self, reqs):
+        for r in reqs:
+            q = Request(r.rid, int(r.input_len), int(r.output_len))
+            if self.blocks(q.input_len + q.output_len) > self.num_blocks:
+                self.rejected.append(q)  # admission could only livelock (S:331 waits forever)
+            else:
+                self.waiting.append(q)
+
+    @property
+    def idle(self) -> bool:
+        return not self.waiting and not self.running
+
+    def plan(self):
+        """-> (Plan, allocs [(slot, n_blocks)] in call order, preempted requests)."""
+        plan = Plan()
+        allocs = []
+        # decode first: every running request steps (cap max_decode); a request whose next
+        # slot opens a new block needs one (R8: blocks are taken before layer 0)
+        for r in self.running[:self.max_decode]:
+            need = self.blocks(r.ctx + 1) - r.nblk
+            if need > self.free_blocks:
+                continue  # stalls this iteration (its blocks stay resident)
+            if need > 0:
+                self.free_blocks -= need
+                r.nblk += need
+                allocs.append((r.slot, need))
+            plan.decode.append((r, r.ctx))
+        # prefill: FCFS chunk budget; headroom of one block per running request keeps
+        # decode from starving (a waiting request never takes the last blocks)
+        budget = self.chunk_budget
+        headroom = len(self.running)
+        for r in list(self.waiting):
+            if budget == 0:
+                break
+            chunk = min(r.input_len - r.prefilled, budget)
+            need = self.blocks(r.prefilled + chunk) - r.nblk
+            if need > self.free_blocks - headroom:
+                break  # FCFS: the head waits (S:331)
+            if r.slot < 0:
+                if not self.free_slots:
+                    break
+                r.slot = self.free_slots.popleft()
+                r.admit_seq = self.n_admit
+                self.n_admit += 1
+            if need > 0:
+                self.free_blocks -= need
+                r.nblk += need
+                allocs.append((r.slot, need))
+            plan.prefill.append((r, chunk, r.prefilled))
+            budget -= chunk
+        preempt = []
+        if not plan.decode and not plan.prefill:
+            # nothing can run on a full pool: recompute-preempt the newest block holder
+            # (running, or partially prefilled); the oldest request then always progresses
+            holders = self.running + [r for r in self.waiting if r.nblk > 0]
+            if holders:
+                victim = max(holders, key=lambda r: r.admit_seq)
+                if victim in self.running:
+                    self.running.remove(victim)
+                preempt.append(victim)
+        return plan, allocs, preempt
+
+    def finishing(self, plan: Plan):
+        """Requests whose decode step in `plan` is their last (freed after the iteration)."""
+        return [r for r, _ in plan.decode if r.generated + 1 >= r.output_len]
+
+    def commit(self, plan: Plan, preempt) -> tuple[int, int, list]:
+        """Host state after the iteration ran: -> (prefill pairs, decode keys, finished)."""
+        pairs = 0
+        for r, ch, pf in plan.prefill:
+            pairs += ch * pf + ch * (ch + 1) // 2
+            r.prefilled += ch
+            if r.prefilled == r.input_len:
+                self.waiting.remove(r)
+                self.running.append(r)
+        finished = self.finishing(plan)
+        dkeys = 0
+        for r, ctx in plan.decode:
+            dkeys += ctx + 1
+            r.generated += 1
+        for r in finished:
+            self.running.remove(r)
+        for r in finished + list(preempt):
+            self.free_blocks += r.nblk
+            r.nblk = 0
+            self.free_slots.append(r.slot)
+            r.slot = -1
+        for v in preempt:  # recompute: the request restarts from its prompt
+            v.prefilled, v.generated = 0, 0
+            v.preempted += 1
+            if v not in self.waiting:
+                self.waiting.appendleft(v)
+        self.finished.extend(finished)
+        return pairs, dkeys, finished
+
+
 class CoRunEngine:
     def __init__(self, pool: KVPool, num_q_heads: int, scale: float, *, chunk_budget: int = 2048,
                  max_decode: int = 512, partition=(50.0, 50.0), seed: int = 0,
@@ -74,12 +191,9 @@ class CoRunEngine:
         self.L = c.num_layers
         self.bs = c.block_size
         self.chunk_budget, self.max_decode = chunk_budget, max_decode
-        self.free_blocks = c.num_blocks
-        self.free_slots = deque(range(c.max_reqs))
-        self.waiting: deque[Request] = deque()     # arrived, prompt not fully prefilled (FCFS)
-        self.running: list[Request] = []           # prompt done, decoding (admission order)
+        self.sched = Scheduler(c.num_blocks, c.block_size, c.max_reqs, chunk_budget=chunk_budget,
+                               max_decode=max_decode)
         self.it = 0
-        self.finished: list[Request] = []
         pool.set_partition(*partition)
         g = torch.Generator(device=self.dev)
         g.manual_seed(seed)
@@ -106,62 +220,22 @@ class CoRunEngine:
         self.sCtl, self.sP, self.sD = (torch.cuda.Stream(device=self.dev) for _ in range(3))
         self.ev_prev_p = None
 
-    # ------------------------------------------------------------------ planning (host)
     def add(self, reqs):
-        for r in reqs:
-            self.waiting.append(Request(r.rid, int(r.input_len), int(r.output_len)))
+        self.sched.add(reqs)
 
-    def _plan(self) -> tuple[Plan, list, list]:
-        plan = Plan()
-        allocs = []  # (slot, n_blocks) in call order
-        # decode first: every running request steps (cap max_decode); a request whose next
-        # slot opens a new block needs one (R8: blocks are taken before layer 0)
-        for r in self.running[:self.max_decode]:
-            need = blocks_for_tokens(r.ctx + 1, self.bs) - r.nblk
-            if need > self.free_blocks:
-                continue  # stalls this iteration (its blocks stay resident)
-            if need > 0:
-                self.free_blocks -= need
-                r.nblk += need
-                allocs.append((r.slot, need))
-            plan.decode.append((r, r.ctx))
-        # prefill: FCFS chunk budget; headroom of one block per running request keeps
-        # decode from starving (a waiting request never takes the last blocks)
-        budget = self.chunk_budget
-        headroom = len(self.running)
-        for r in list(self.waiting):
-            if budget == 0:
-                break
-            chunk = min(r.input_len - r.prefilled, budget)
-            need = blocks_for_tokens(r.prefilled + chunk, self.bs) - r.nblk
-            if need > self.free_blocks - headroom:
-                break  # FCFS: the head waits
-            if r.slot < 0:
-                if not self.free_slots:
-                    break
-                r.slot = self.free_slots.popleft()
-            if need > 0:
-                self.free_blocks -= need
-                r.nblk += need
-                allocs.append((r.slot, need))
-            plan.prefill.append((r, chunk, r.prefilled))
-            budget -= chunk
-        preempt = []
-        if not plan.decode and not plan.prefill and self.running:
-            # every running request is blocked on a full pool: recompute-preempt the newest
-            victim = self.running.pop()
-            preempt.append(victim)
-        return plan, allocs, preempt
+    @property
+    def finished(self):
+        return self.sched.finished
 
     # ------------------------------------------------------------------ one iteration
     def step(self, arrivals=()) -> tuple[IterStats, Plan]:
-        self.add(arrivals)
-        plan, allocs, preempt = self._plan()
+        self.sched.add(arrivals)
+        plan, allocs, preempt = self.sched.plan()
         pool, dev = self.pool, self.dev
         n_p, n_d = len(plan.prefill), len(plan.decode)
         # metadata: [cu_seqlens (n_p+1) | req_ids (n_p) | prefix (n_p) | dec rids | dec ctx |
         #            alloc ids | alloc counts | free ids]
-        finished = [r for r, _ in plan.decode if r.generated + 1 >= r.output_len]
+        finished = self.sched.finishing(plan)
         frees = [r.slot for r in finished] + [v.slot for v in preempt]
         meta, off = [], {}
 
@@ -242,41 +316,18 @@ class CoRunEngine:
         bad = torch.nonzero(self.status[:st_i]).flatten().tolist()
         if bad:
             raise RuntimeError(f"iteration {self.it}: device status {self.status[bad].tolist()}")
-        # host state transitions
-        pairs = 0
-        for r, ch, pf in plan.prefill:
-            pairs += ch * pf + ch * (ch + 1) // 2
-            r.prefilled += ch
-            if r.prefilled == r.input_len:
-                self.waiting.remove(r)
-                self.running.append(r)
-        dkeys = 0
-        for r, ctx in plan.decode:
-            dkeys += ctx + 1
-            r.generated += 1
-        for r in finished:
-            self.running.remove(r)
-        for r in finished + preempt:
-            self.free_blocks += r.nblk
-            r.nblk = 0
-            self.free_slots.append(r.slot)
-            r.slot = -1
-        for v in preempt:  # recompute: the request restarts from its prompt
-            v.prefilled, v.generated = 0, 0
-            v.preempted += 1
-            self.waiting.appendleft(v)
-        self.finished.extend(finished)
+        pairs, dkeys, finished = self.sched.commit(plan, preempt)
         el = lambda a, b: ev[a].elapsed_time(ev[b])  # noqa: E731
         s = IterStats(self.it, n_p, T, pairs, n_d, dkeys,
                       el("p0", "p1") if n_p else 0.0, el("d0", "d1") if n_d else 0.0,
-                      el("i0", "i1"), len(allocs), 1 if frees else 0, self.free_blocks,
+                      el("i0", "i1"), len(allocs), 1 if frees else 0, self.sched.free_blocks,
                       len(finished), len(preempt))
         self.it += 1
         return s, plan
 
     @property
     def idle(self) -> bool:
-        return not self.waiting and not self.running
+        return self.sched.idle
 
 
 def mla_flops_per_pair(shape_dk: int, shape_dv: int, Hq: int) -> float:
@@ -284,4 +335,4 @@ def mla_flops_per_pair(shape_dk: int, shape_dv: int, Hq: int) -> float:
     return 2.0 * Hq * (shape_dk + shape_dv)
 
 
-__all__ = ["CoRunEngine", "Request", "IterStats", "Plan", "mla_flops_per_pair"]
+__all__ = ["CoRunEngine", "Scheduler", "Request", "IterStats", "Plan", "mla_flops_per_pair"]

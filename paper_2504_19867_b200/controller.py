@@ -11,7 +11,9 @@ SM partition that `semipd_set_partition` applies at each phase's next launch.
 Readings (R22): Alg. 1's `step` is incremented once per loop
 iteration; observed percentiles decide the fail branches, the fitted model is used only
 inside the while loops; estimates use the normalised shares x' = 100 x / (x + y)
-(lines 11, 16); lambda is fitted by a 0.25 % grid search with OLS at each lambda.
+(lines 11, 16); lambda is fitted by a 0.25 % grid search with OLS at each lambda.  Until a
+side has been observed at two distinct shares (no fit), a failing SLO takes one probing step
+(R24).
 """
 from __future__ import annotations
 
@@ -164,6 +166,12 @@ class SloController:
             return x0, y0
         step, s = 0, self.cfg.step_size
         m = self.model
+        if (ttft_fail and not m.fitted_ttft) or (tpot_fail and not m.fitted_tpot and not ttft_fail):
+            # no model yet (< 2 distinct shares observed, R24): one probing step in
+            # the failing phase's favour, which also gives the fit its second share
+            if ttft_fail:
+                return (x + s, y) if x + s <= 100 else ((x, y - s) if y - s > 0 else (x, y))
+            return (x, y + s) if y + s <= 100 else ((x - s, y) if x - s > 0 else (x, y))
         if ttft_fail and m.fitted_ttft:                         # lines 8-11
             while step < self.cfg.max_step and m.estimate_ttft(100 * x / (x + y)) > self.slo.ttft_slo:
                 if x + s <= 100:                                # increase_x_ratio

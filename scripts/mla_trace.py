@@ -63,6 +63,11 @@ def replay(words, N_B, R, MBR):
     return ref, n_ops
 
 
+def nearest_rank_(vals, p):
+    vals = sorted(vals)
+    return vals[max(1, math.ceil(p * len(vals))) - 1] if vals else None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--requests", type=int, default=2000)
@@ -73,6 +78,11 @@ def main():
     ap.add_argument("--samples", type=int, default=10)
     ap.add_argument("--max-iters", type=int, default=100000)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--controller", action="store_true",
+                    help="N1: adjust (x, y) every --window iterations with Alg. 1 + the Eq. 4 fit")
+    ap.add_argument("--window", type=int, default=100)
+    ap.add_argument("--ttft-slo", type=float, default=0.25, help="seconds (attention-only clock)")
+    ap.add_argument("--tpot-slo", type=float, default=0.0045, help="seconds (attention-only clock)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     shape = synth.CFG5_MLA
@@ -89,6 +99,16 @@ def main():
     last_arrival = trace[-1].arrival_iter
     sample_its = set(int(x) for x in np.linspace(5, max(6, last_arrival), args.samples))
     stats, parity, idx = [], [], 0
+    # latency bookkeeping on a device clock: the sum of measured iteration times
+    now, arrive_t, first_dec_t = 0.0, {}, {}
+    ttft, tpot, win_ttft, win_tpot, splits = {}, {}, [], [], []
+    x_cur, y_cur = args.x, 100.0 - args.x
+    ctl = None
+    if args.controller:
+        from paper_2504_19867_b200.controller import (ControllerConfig, Observation, SloConfig,
+                                                      SloController, nearest_rank)
+        ctl = SloController(SloConfig(args.ttft_slo, args.tpot_slo, 0.9),
+                            ControllerConfig(window_size=args.window))
     t0 = time.perf_counter()
     while (idx < len(trace) or not eng.idle) and eng.it < args.max_iters:
         arr = []
@@ -99,8 +119,34 @@ def main():
         if sample:
             torch.cuda.synchronize()
             k_pre = bits(pool.views(0)[0])  # layer-0 latent pool before this iteration
+        for r in arr:
+            arrive_t[r.rid] = now
         s, plan = eng.step(arr)
         stats.append(s)
+        now += s.t_iter_ms / 1e3
+        for r, ch, pf in plan.prefill:
+            if r.prefilled == r.input_len and r.trace_id not in ttft:
+                ttft[r.trace_id] = now - arrive_t[r.trace_id]
+                win_ttft.append(ttft[r.trace_id])
+        for r, _ in plan.decode:
+            if r.generated == 1:
+                first_dec_t[r.trace_id] = now
+            if r.slot < 0 and r.generated == r.output_len:  # finished this iteration
+                tp = (now - first_dec_t[r.trace_id]) / max(1, r.output_len - 1)
+                tpot[r.trace_id] = tp
+                win_tpot.append(tp)
+        if ctl is not None and s.it > 0 and s.it % args.window == 0:
+            p_tt = nearest_rank(win_ttft, 0.9)
+            p_tp = nearest_rank(win_tpot, 0.9)
+            ctl.update_estimate_model(Observation(100 * x_cur / (x_cur + y_cur),
+                                                  100 * y_cur / (x_cur + y_cur), p_tt, p_tp))
+            nx, ny = ctl.adjust(s.it, x_cur, y_cur, p_tt, p_tp)
+            splits.append({"it": s.it, "x": x_cur, "y": y_cur, "p90_ttft_s": p_tt, "p90_tpot_s": p_tp,
+                           "next": [nx, ny]})
+            if (nx, ny) != (x_cur, y_cur):
+                x_cur, y_cur = nx, ny
+                pool.set_partition(x_cur, y_cur)  # adopted at each phase's next launch (R15)
+            win_ttft, win_tpot = [], []
         if sample and (plan.prefill or plan.decode):
             bt = pool.views(0)[2].cpu().numpy()
             rec = {"it": s.it}
@@ -164,6 +210,14 @@ def main():
         "op_log_ops": n_ops, "op_log_dropped": dropped, "op_log_replay_tables_equal": tables_ok,
         "pool_blocks": args.blocks, "pool_min_free": min_free,
         "pool_high_water_blocks": args.blocks - min_free, "pool_free_end": free_now,
+        "p90_ttft_s": nearest_rank_(list(ttft.values()), 0.9),
+        "p90_tpot_s": nearest_rank_(list(tpot.values()), 0.9),
+        "controller": ({"ttft_slo_s": args.ttft_slo, "tpot_slo_s": args.tpot_slo, "window": args.window,
+                        "trajectory": splits,
+                        "ttft_slo_attainment": sum(v <= args.ttft_slo for v in ttft.values()) / max(1, len(ttft)),
+                        "tpot_slo_attainment": sum(v <= args.tpot_slo for v in tpot.values()) / max(1, len(tpot)),
+                        "model": None if ctl is None else ctl.model.__dict__}
+                       if args.controller else None),
         "parity_samples": parity,
         "parity_all_ok": all(v["ok"] for rec in parity for k, v in rec.items() if k != "it"),
     }

@@ -98,3 +98,15 @@ def test_closed_loop_convergence_on_exact_model():
         xn = 100 * x / (x + y)
         x, y = c.adjust(it, x, y, true.estimate_ttft(xn), true.estimate_tpot(100 * y / (x + y)))
     assert true.estimate_ttft(100 * x / (x + y)) <= 0.12
+
+
+def test_unfitted_model_takes_one_probing_step():
+    """R24: without a fit (one share observed) a failing SLO moves one step toward the
+    failing phase; passing SLOs or both failing leave the partition unchanged."""
+    c = SloController(SloConfig(0.2, 0.1), ControllerConfig(window_size=10, max_step=6, step_size=5))
+    c.update_estimate_model(Observation(50, 50, 0.3, 0.05))
+    assert c.adjust(10, 50, 50, 0.3, 0.05) == (55, 50)      # TTFT fails
+    assert c.adjust(10, 50, 50, 0.1, 0.2) == (50, 55)       # TPOT fails
+    assert c.adjust(10, 100, 50, 0.3, 0.05) == (100, 45)    # TTFT fails at x = 100
+    assert c.adjust(10, 50, 50, 0.1, 0.05) == (50, 50)      # both pass
+    assert c.adjust(10, 50, 50, 0.3, 0.2) == (50, 50)       # both fail

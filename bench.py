@@ -32,7 +32,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -94,9 +93,23 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def _clock_sampler_proc(index: int, period: float, stop, out):
+    """Child process: poll NVML SM clock + clock-event reasons until `stop` is set."""
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(index)
+    rows = []
+    out.put(("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)))
+    while not stop.is_set():
+        rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                     pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+        time.sleep(period)
+    out.put(("rows", rows))
+
+
 class ClockSampler:
-    """SM clocks + throttle reasons polled through NVML every ~10 ms while the timed
-    region runs (nvidia-smi's 100 ms interval is longer than short timed regions)."""
+    """SM clocks + throttle reasons polled through NVML every ~5 ms while the timed region
+    runs, from a child process (a thread would starve behind the launch loop's GIL)."""
 
     REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
                "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
@@ -104,50 +117,42 @@ class ClockSampler:
                "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
                "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-    def __init__(self, index: int, period_s: float = 0.01):
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index, self.period, self.rows, self.max_mhz = index, period_s, [], None
-        self._stop = threading.Event()
         self.err = None
 
     def __enter__(self):
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+            import multiprocessing as mp
+            ctx = mp.get_context("spawn")
+            self.stop, self.q = ctx.Event(), ctx.Queue()
+            self.p = ctx.Process(target=_clock_sampler_proc,
+                                 args=(self.index, self.period, self.stop, self.q), daemon=True)
+            self.p.start()
+            kind, v = self.q.get(timeout=60)  # NVML is up before the timed region starts
+            self.max_mhz = v
         except Exception as e:  # pragma: no cover
             self.err = repr(e)
         return self
 
-    def _run(self):
-        nv = self.nv
-        while not self._stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.rows.append((sm, rs))
-            except Exception as e:  # pragma: no cover
-                self.err = repr(e)
-                return
-            time.sleep(self.period)
-
     def __exit__(self, *a):
-        self._stop.set()
-        if hasattr(self, "t"):
-            self.t.join(timeout=1)
+        try:
+            self.stop.set()
+            kind, rows = self.q.get(timeout=30)
+            self.rows = rows
+            self.p.join(timeout=10)
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
                     "error": self.err}
-        nv = self.nv
+        import pynvml as nv
         reasons = sorted({name for _, rs in self.rows for name, attr in self.REASONS.items()
                           if rs & getattr(nv, attr)})
         return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.rows), "source": "nvml, 10 ms"}
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml, 5 ms, child process"}
 
 
 def dist_info():

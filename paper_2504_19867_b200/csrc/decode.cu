@@ -9,7 +9,7 @@
 //     swizzle, one 4-D box = min(bs,64) rows x all 128 columns of one (block, head)
 //     page) into a 6-deep shared-memory ring (192 KiB: Little's law for HBM latency
 //     on a minority of SMs);
-//   warps 0-2 (consumers): global stage gs goes to warp gs % 3; QK^T and PV on
+//   consumer warps 0-2: global stage gs goes to warp gs % 3; QK^T and PV on
 //     mma.sync m16n8k16 (the G <= 16 query heads of one kv head fill M = 16, so
 //     each K/V byte is read once for all G heads), warp-shuffle online softmax in
 //     the log2 domain, then a cross-warp merge in shared memory and, for split
@@ -29,9 +29,6 @@ using namespace spd;
 constexpr int HD = 128;           // head dim (dk == dv)
 constexpr int KPS = 64;           // keys per stage
 constexpr int NSTAGE = 6;
-constexpr int NCW = 3;            // consumer warps; slot s is always consumed by warp s % NCW
-static_assert(NSTAGE % NCW == 0, "each ring slot must have one fixed consumer warp");
-constexpr int NTHREADS = (NCW + 1) * 32;
 constexpr int KV_BYTES = KPS * HD * 2;         // 16 KiB of K (or V) per stage
 constexpr int STAGE_BYTES = 2 * KV_BYTES;      // K + V
 constexpr int SPLIT_KEYS = 4096;  // maximum keys per split (shape-only decomposition)
@@ -79,17 +76,22 @@ __device__ __forceinline__ uint32_t kv_off(int key, int h) {
 }
 
 template <int LG_R, bool SWAP>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(4 * 32, 1)
     decode_bf16_kernel(const __grid_constant__ CUtensorMap kmap,
                        const __grid_constant__ CUtensorMap vmap, DecodeParams p) {
     constexpr int R = 1 << LG_R;     // rows per TMA box (= min(bs, 64))
     constexpr int NB = KPS / R;      // boxes per stage per tensor
+    // consumer warps and scratch rows (the swap-AB partials have G <= 8 rows); 6 swap-AB
+    // consumer warps measured 2-5 % slower than 3 (more padding stages and merge work)
+    constexpr int CW = 3;
+    constexpr int SR = SWAP ? 8 : 16;
+    static_assert(NSTAGE % CW == 0, "each ring slot must have one fixed consumer warp");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* ring = smem;                                   // NSTAGE x 32 KiB
-    float* scr_acc = reinterpret_cast<float*>(ring + NSTAGE * STAGE_BYTES);  // [NCW][16][128]
-    float* scr_ml = scr_acc + NCW * 16 * HD;                       // [NCW][16][2]
-    uint64_t* full = reinterpret_cast<uint64_t*>(scr_ml + NCW * 16 * 2);
+    float* scr_acc = reinterpret_cast<float*>(ring + NSTAGE * STAGE_BYTES);  // [CW][16][128]
+    float* scr_ml = scr_acc + CW * SR * HD;                       // [CW][16][2]
+    uint64_t* full = reinterpret_cast<uint64_t*>(scr_ml + CW * SR * 2);
     uint64_t* empty = full + NSTAGE;
     uint64_t* ufull = empty + NSTAGE;
     uint64_t* uempty = ufull + 2;
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(ufull + i, 1);
-            mbar_init(uempty + i, NCW);
+            mbar_init(uempty + i, CW);
         }
         fence_mbar_init();
         if (p.trace.buf) {
@@ -123,19 +125,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // ---- cross-warp merge: thread t handles (head h, 4 columns)
         const int tid = threadIdx.x;  // 0..127
         const bool split = d.S > 1;
-        for (int idx = tid; idx < p.G * (HD / 4); idx += NCW * 32) {
+        for (int idx = tid; idx < p.G * (HD / 4); idx += CW * 32) {
             const int h = idx / (HD / 4), c = (idx % (HD / 4)) * 4;
             float M = -INFINITY;
 #pragma unroll
-            for (int w = 0; w < NCW; ++w) M = fmaxf(M, scr_ml[(w * 16 + h) * 2]);
+            for (int w = 0; w < CW; ++w) M = fmaxf(M, scr_ml[(w * SR + h) * 2]);
             float L = 0.f;
             float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int w = 0; w < NCW; ++w) {
-                const float mw = scr_ml[(w * 16 + h) * 2];
+            for (int w = 0; w < CW; ++w) {
+                const float mw = scr_ml[(w * SR + h) * 2];
                 const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
-                L += f * scr_ml[(w * 16 + h) * 2 + 1];
-                const float4 a = *reinterpret_cast<const float4*>(scr_acc + (w * 16 + h) * HD + c);
+                L += f * scr_ml[(w * SR + h) * 2 + 1];
+                const float4 a = *reinterpret_cast<const float4*>(scr_acc + (w * SR + h) * HD + c);
                 o.x += f * a.x;
                 o.y += f * a.y;
                 o.z += f * a.z;
@@ -161,16 +163,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         if (split) {
             __threadfence();
-            named_bar_sync(1, NCW * 32);
+            named_bar_sync(1, CW * 32);
             if (tid == 0) {
                 const int prev = atomicAdd(p.ws_cnt + d.b * p.Hkv + d.g, 1);
                 *s_last = prev == d.S - 1;
             }
-            named_bar_sync(1, NCW * 32);
+            named_bar_sync(1, CW * 32);
             if (*s_last) {
                 __threadfence();
                 // merge over splits in split-index order (flash-decoding)
-                for (int idx = tid; idx < p.G * (HD / 4); idx += NCW * 32) {
+                for (int idx = tid; idx < p.G * (HD / 4); idx += CW * 32) {
                     const int h = idx / (HD / 4), c = (idx % (HD / 4)) * 4;
                     const int hq = d.g * p.G + h;
                     const size_t pb = ((size_t)d.b * p.Hq + hq) * p.S_max;
@@ -198,9 +200,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (tid == 0) p.ws_cnt[d.b * p.Hkv + d.g] = 0;  // ready for the next call
             }
         }
-        named_bar_sync(1, NCW * 32);  // scratch reuse
+        named_bar_sync(1, CW * 32);  // scratch reuse
     };
-    if (warp == NCW) {
+    if (warp == CW) {
         // =========================== producer ===========================
         // Whole warp: lane l holds the raw block id of box (32*batch + l) of the unit,
         // loaded one batch ahead (block-table reads off the TMA issue path); lane 0
@@ -229,10 +231,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (d.s >= d.S) continue;  // warp-uniform
                 split_range(ctx, d.S, d.s, d.k0, d.k1);
                 d.nst = (d.k1 - d.k0 + KPS - 1) / KPS;
-                // align the unit's first stage to a multiple of NCW with data-less padding
+                // align the unit's first stage to a multiple of CW with data-less padding
                 // stages, so the stage -> warp split depends on the unit only (bitwise
                 // identical results for every grid size / schedule)
-                while (gstage % NCW != 0) {
+                while (gstage % CW != 0) {
                     if (lane == 0) {
                         const int st = gstage % NSTAGE;
                         mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
@@ -345,11 +347,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_wait(full + st, (next_gs / NSTAGE) & 1);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty + st);
-                next_gs += NCW;
+                next_gs += CW;
             }
-            next_gs = d.base + (warp < d.nst ? warp + ((d.nst - 1 - warp) / NCW + 1) * NCW : warp);
+            next_gs = d.base + (warp < d.nst ? warp + ((d.nst - 1 - warp) / CW + 1) * CW : warp);
             const int lm = lane >> 3, lr = lane & 7;  // ldmatrix: matrix / row of this lane
-            for (int i = warp; i < d.nst; i += NCW) {
+            for (int i = warp; i < d.nst; i += CW) {
                 const int gs = d.base + i;
                 const int st = gs % NSTAGE;
                 mbar_wait(full + st, (gs / NSTAGE) & 1);
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 lrow[j] += __shfl_xor_sync(0xffffffffu, lrow[j], 8);
                 lrow[j] += __shfl_xor_sync(0xffffffffu, lrow[j], 16);
             }
-            float* wacc = scr_acc + warp * 16 * HD;
+            float* wacc = scr_acc + warp * SR * HD;
 #pragma unroll
             for (int dt = 0; dt < 8; ++dt) {
                 const int dv = dt * 16 + kr;
@@ -451,12 +453,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 wacc[(hc + 1) * HD + dv + 8] = acc[dt][3];
             }
             if (kr == 0) {
-                scr_ml[(warp * 16 + hc) * 2 + 0] = mrow[0];
-                scr_ml[(warp * 16 + hc) * 2 + 1] = lrow[0];
-                scr_ml[(warp * 16 + hc + 1) * 2 + 0] = mrow[1];
-                scr_ml[(warp * 16 + hc + 1) * 2 + 1] = lrow[1];
+                scr_ml[(warp * SR + hc) * 2 + 0] = mrow[0];
+                scr_ml[(warp * SR + hc) * 2 + 1] = lrow[0];
+                scr_ml[(warp * SR + hc + 1) * 2 + 0] = mrow[1];
+                scr_ml[(warp * SR + hc + 1) * 2 + 1] = lrow[1];
             }
-            named_bar_sync(1, NCW * 32);
+            named_bar_sync(1, CW * 32);
             merge_and_store(d);
         }
     } else {
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
             float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
 
-            // global stage gs goes to warp gs % NCW, so every ring slot is consumed by one
+            // global stage gs goes to warp gs % CW, so every ring slot is consumed by one
             // warp in order (each full/empty phase is waited for exactly once); first
             // release the padding stages in front of this unit
             while (next_gs < d.base) {
@@ -502,10 +504,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_wait(full + st, (next_gs / NSTAGE) & 1);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty + st);
-                next_gs += NCW;
+                next_gs += CW;
             }
-            next_gs = d.base + (warp < d.nst ? warp + ((d.nst - 1 - warp) / NCW + 1) * NCW : warp);
-            for (int i = warp; i < d.nst; i += NCW) {
+            next_gs = d.base + (warp < d.nst ? warp + ((d.nst - 1 - warp) / CW + 1) * CW : warp);
+            for (int i = warp; i < d.nst; i += CW) {
                 const int gs = d.base + i;
                 const int st = gs % NSTAGE;
                 mbar_wait(full + st, (gs / NSTAGE) & 1);
@@ -600,7 +602,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 1);
                 lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 2);
             }
-            float* wacc = scr_acc + warp * 16 * HD;
+            float* wacc = scr_acc + warp * SR * HD;
 #pragma unroll
             for (int nd = 0; nd < 16; ++nd) {
                 const int col = nd * 8 + c0;
@@ -609,12 +611,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     make_float2(acc[nd][2], acc[nd][3]);
             }
             if ((lane & 3) == 0) {
-                scr_ml[(warp * 16 + r0) * 2 + 0] = mrow[0];
-                scr_ml[(warp * 16 + r0) * 2 + 1] = lrow[0];
-                scr_ml[(warp * 16 + r0 + 8) * 2 + 0] = mrow[1];
-                scr_ml[(warp * 16 + r0 + 8) * 2 + 1] = lrow[1];
+                scr_ml[(warp * SR + r0) * 2 + 0] = mrow[0];
+                scr_ml[(warp * SR + r0) * 2 + 1] = lrow[0];
+                scr_ml[(warp * SR + r0 + 8) * 2 + 0] = mrow[1];
+                scr_ml[(warp * SR + r0 + 8) * 2 + 1] = lrow[1];
             }
-            named_bar_sync(1, NCW * 32);
+            named_bar_sync(1, CW * 32);
             merge_and_store(d);
         }
     }
@@ -1030,8 +1032,9 @@ size_t decode_pair_smem_bytes() {
            (2 * P_NSTAGE + 4) * 8 + 2 * sizeof(UnitDesc) + 16;
 }
 
-size_t decode_smem_bytes() {
-    return 1024 + NSTAGE * STAGE_BYTES + NCW * 16 * HD * 4 + NCW * 16 * 2 * 4 +
+size_t decode_smem_bytes(bool swap) {
+    const int cw = 3, sr = swap ? 8 : 16;
+    return 1024 + NSTAGE * STAGE_BYTES + cw * sr * HD * 4 + cw * sr * 2 * 4 +
            (2 * NSTAGE + 4) * 8 + 2 * sizeof(UnitDesc) + 16;
 }
 
@@ -1171,7 +1174,9 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
         pool->launches += 1;
         return SEMIPD_OK;
     }
-    const size_t smem = decode_smem_bytes();
+    const bool swap = prm.G <= 8;  // heads fit the MMA N = 8: swap-AB consumers
+    const size_t smem = decode_smem_bytes(swap);
+    const int nthreads = 4 * 32;
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;
     const int lg_r = __builtin_ctz((unsigned)pool->dbox_rows);
@@ -1184,10 +1189,9 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
             if (e != cudaSuccess) return;
             attr_set[ai] = true;
         }
-        kern<<<grid, NTHREADS, smem, st>>>(pool->dkmap[layer], pool->dvmap[layer], prm);
+        kern<<<grid, nthreads, smem, st>>>(pool->dkmap[layer], pool->dvmap[layer], prm);
         e = cudaGetLastError();
     };
-    const bool swap = prm.G <= 8;  // heads fit the MMA N = 8: swap-AB consumers
     if (lg_r == 4) swap ? launch(decode_bf16_kernel<4, true>) : launch(decode_bf16_kernel<4, false>);
     else if (lg_r == 5) swap ? launch(decode_bf16_kernel<5, true>) : launch(decode_bf16_kernel<5, false>);
     else swap ? launch(decode_bf16_kernel<6, true>) : launch(decode_bf16_kernel<6, false>);

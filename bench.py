@@ -61,6 +61,8 @@ def parse():
                     help="KV page size in tokens (64: one 16 KiB TMA box per (block, head) "
                          "page on B200; 16 is supported but TMA-per-box bound)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch every kernel from Python instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extra", action="store_true", help="serial / (100,100) / isolated curves")
     return ap.parse_args()
@@ -491,8 +493,23 @@ def main():
         w.corun_step(50, 50)
     sweep = []
 
+    use_graph = not args.no_graph and ws == 1
+
+    def capture(x):
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            w.corun_step(x, 100 - x)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        return g
+
     def measure(x):
-        t = time_steps(lambda: w.corun_step(x, 100 - x), 2, dev, barrier) / 2
+        if use_graph:
+            g = capture(x)
+            t = time_steps(g.replay, 3, dev, barrier) / 3
+        else:
+            t = time_steps(lambda: w.corun_step(x, 100 - x), 2, dev, barrier) / 2
         if ws > 1:
             tt = torch.tensor([t], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -512,19 +529,30 @@ def main():
     x, y = best["x"], best["y"]
     for _ in range(W):
         w.corun_step(x, y)
+    # the co-run step (both streams, alloc -> 32 layers x 2 kernels -> free) is captured once
+    # into a CUDA graph and replayed: no per-kernel launch gaps from the Python loop
+    graph = capture(x) if use_graph else None
+    if graph is not None:
+        graph.replay()
+        torch.cuda.synchronize(dev)
     # ---- timed region
-    launches0 = w.pool.launch_count()
+    per_step = [0]
     with ClockSampler(local) as clk:
-        # per-launch CUDA events only in the last timed step: an event pair between every
-        # back-to-back kernel costs ~3 us per launch on each stream
+        # the last timed step runs eagerly with per-launch CUDA events (the roofline's kernel
+        # times; an event pair between back-to-back kernels costs ~3 us, so only one step)
         k_step = [0]
 
         def step():
             k_step[0] += 1
-            w.corun_step(x, y, timed=k_step[0] == args.steps)
+            if k_step[0] == args.steps or graph is None:
+                c0 = w.pool.launch_count()
+                w.corun_step(x, y, timed=k_step[0] == args.steps)
+                per_step[0] = w.pool.launch_count() - c0
+            else:
+                graph.replay()
 
         t = time_steps(step, args.steps, dev, barrier)
-    launches = w.pool.launch_count() - launches0
+    launches = per_step[0] * args.steps  # the graph replays the same launches
     if ws > 1:
         tt = torch.tensor([t], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -555,8 +583,20 @@ def main():
                 "avg_launch_ms": pre_ms, "sm_budget": n_p}
     extra = {}
     if args.extra:
-        ts = time_steps(w.serial_step, 2, dev, barrier) / 2
-        tu = time_steps(w.uncontrolled_step, 2, dev, barrier) / 2
+        def graphed(fn):  # the baselines get the same CUDA-graph replay as the co-run step
+            if not use_graph:
+                return fn
+            fn()
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            g.replay()
+            torch.cuda.synchronize(dev)
+            return g.replay
+
+        ts = time_steps(graphed(w.serial_step), 3, dev, barrier) / 3
+        tu = time_steps(graphed(w.uncontrolled_step), 3, dev, barrier) / 3
         extra = {"serial_ms": ts * 1e3, "uncontrolled_100_100_ms": tu * 1e3,
                  "corun_ms": t / args.steps * 1e3,
                  "speedup_vs_serial": ts / (t / args.steps),
@@ -594,7 +634,7 @@ def main():
             "decode_tokens_per_s": DECODE_BATCH * args.steps / t,
             "prefill_tokens_per_s": PREFILL_TOKENS * args.steps / t,
             "sweep": sweep, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
-            "gpu_launches": launches, "extra": extra or None,
+            "gpu_launches": launches, "cuda_graph": graph is not None, "extra": extra or None,
         }
         print(json.dumps(line))
     if ws > 1:

@@ -37,6 +37,9 @@ def main():
     ap.add_argument("--hq", type=int, default=32)
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--bs", type=int, default=16)
+    ap.add_argument("--ctx-uniform", default=None,
+                    help="lo,hi: decode contexts ~ U[lo, hi] (seed 2002) instead of all = --ctx "
+                         "(SURVEY §8(d) item 7, load balance)")
     ap.add_argument("--mla", action="store_true", help="cfg5 absorbed-MLA decode (576/512, 16 heads)")
     ap.add_argument("--mla-prefill", action="store_true", help="cfg5 absorbed-MLA prefill chunk")
     args = ap.parse_args()
@@ -47,12 +50,19 @@ def main():
         return mla_prefill(args, dev)
     L, B, ctx, C, P = args.layers, args.batch, args.ctx, args.chunk, args.prefix
     Hq, Hkv, d, bs = args.hq, args.hkv, 128, args.bs
+    if args.ctx_uniform:
+        import numpy as np
+        lo, hi = (int(v) for v in args.ctx_uniform.split(","))
+        ctx_list = [int(v) for v in np.random.default_rng(2002).integers(lo, hi + 1, size=B)]
+    else:
+        ctx_list = [ctx] * B
+    ctx = max(ctx_list)
     nb_dec = ctx // bs + 1
     nb_pre = -(-(C + P) // bs)
     cfg = PoolConfig(L, B * nb_dec + nb_pre + 8, bs, Hkv, d, d, B + 2, max(nb_dec, nb_pre) + 2)
     pool = KVPool(cfg, dev)
     i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
-    pool.alloc_blocks(i32(list(range(B))), i32([nb_dec] * B))
+    pool.alloc_blocks(i32(list(range(B))), i32([c // bs + 1 for c in ctx_list]))
     pool.alloc_blocks(i32([B]), i32([nb_pre]))
     g = torch.Generator(device=dev)
     g.manual_seed(0)
@@ -65,11 +75,11 @@ def main():
     qd, kd, vd = rnd(B, Hq, d), rnd(B, Hkv, d), rnd(B, Hkv, d)
     od = torch.empty(B, Hq, d, dtype=torch.bfloat16, device=dev)
     ws = pool.new_decode_workspace(B, Hq, ctx)
-    rid, ctxs = i32(list(range(B))), i32([ctx] * B)
+    rid, ctxs = i32(list(range(B))), i32(ctx_list)
     qp, kp, vp = rnd(C, Hq, d), rnd(C, Hkv, d), rnd(C, Hkv, d)
     op = torch.empty(C, Hq, d, dtype=torch.bfloat16, device=dev)
     cu, ridp, pre = i32([0, C]), i32([B]), i32([P])
-    dec_bytes = B * (ctx + 1) * Hkv * 2 * d * 2 + B * Hq * 2 * d * 2
+    dec_bytes = sum(c + 1 for c in ctx_list) * Hkv * 2 * d * 2 + B * Hq * 2 * d * 2
     pairs = C * P + C * (C + 1) / 2
     pre_flops = 2 * Hq * 2 * d * pairs
     kernels = ["decode", "prefill"] if args.kernel == "both" else [args.kernel]
@@ -117,7 +127,7 @@ def mla(args, dev):
     kn = torch.randn(B, 1, 576, device=dev, generator=g).bfloat16()
     out = torch.empty(B, 16, 512, dtype=torch.bfloat16, device=dev)
     ws = pool.new_decode_workspace(B, 16, ctx)
-    rid, ctxs = i32(list(range(B))), i32([ctx] * B)
+    rid, ctxs = i32(list(range(B))), i32(ctx_list)
     byts = B * (ctx + 1) * 576 * 2 + B * 16 * (576 + 512) * 2
     flops = 2 * B * 16 * (ctx + 1) * (576 + 512)
     for bud in [int(x) for x in args.budgets.split(",")]:

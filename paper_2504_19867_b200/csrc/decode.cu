@@ -1038,22 +1038,6 @@ size_t decode_smem_bytes(bool swap) {
            (2 * NSTAGE + 4) * 8 + 2 * sizeof(UnitDesc) + 16;
 }
 
-inline size_t al256(size_t x) { return (x + 255) / 256 * 256; }
-
-struct WsLayout {
-    size_t cnt, sched, m, l, acc, total;
-};
-WsLayout ws_layout(int B, int Hq, int Hkv, int S_max, int dv) {
-    WsLayout w;
-    w.cnt = 0;
-    w.sched = al256((size_t)B * Hkv * 4);
-    w.m = w.sched + 256;
-    w.l = al256(w.m + (size_t)B * Hq * S_max * 4);
-    w.acc = al256(w.l + (size_t)B * Hq * S_max * 4);
-    w.total = al256(w.acc + (size_t)B * Hq * S_max * dv * 4);
-    return w;
-}
-
 bool fast_path_ok(const semipd_pool* p, int Hq) {
     const auto& c = p->cfg;
     const int bs = c.block_size;
@@ -1069,16 +1053,18 @@ extern "C" {
 size_t semipd_decode_workspace_bytes(semipd_pool_t pool, int32_t max_batch, int32_t num_q_heads,
                                      int32_t max_ctx) {
     if (!pool || max_batch < 0 || num_q_heads <= 0 || max_ctx < 0) return 0;
+    // SpdWs: counters for max_batch x Hkv at the front + the largest split-partial set of any
+    // decode kernel / batch <= max_batch at the back
     const int S_max = (max_ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
-    size_t n = ws_layout(max_batch, num_q_heads, pool->cfg.num_kv_heads, S_max,
-                         pool->cfg.head_dim_v).total;
+    size_t part = spd_ws_partial_bytes((size_t)max_batch * num_q_heads, S_max, pool->cfg.head_dim_v);
     if (pool->cfg.kv_shared) {
         const size_t m = spd_mla_ws_bytes(max_batch, max_ctx);
         const size_t m2 = spd_mla_tc_ws_bytes(max_batch, max_ctx);
-        if (m > n) n = m;
-        if (m2 > n) n = m2;
+        if (m > part) part = m;
+        if (m2 > part) part = m2;
     }
-    return n;
+    const int hkv = pool->cfg.num_kv_heads > 0 ? pool->cfg.num_kv_heads : 1;
+    return spd_ws_counter_bytes((size_t)max_batch * hkv) + part;
 }
 
 semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* q,
@@ -1117,9 +1103,10 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
                                     status_dev, st);
     }
     const int S_max = (max_ctx_len + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
-    const WsLayout w = ws_layout(batch, num_q_heads, c.num_kv_heads, S_max, HD);
-    if (!workspace || ws_bytes < w.total) return SEMIPD_ERR_INVALID;
-    unsigned char* ws = static_cast<unsigned char*>(workspace);
+    SpdWs w;
+    if (!spd_ws_carve(workspace, ws_bytes, (size_t)batch * c.num_kv_heads, (size_t)batch * num_q_heads,
+                      S_max, HD, &w))
+        return SEMIPD_ERR_INVALID;
     DecodeParams prm;
     prm.q = static_cast<const __nv_bfloat16*>(q);
     prm.k_new = static_cast<const uint4*>(k_new);
@@ -1130,11 +1117,11 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     prm.k_pool = static_cast<unsigned char*>(pool->k_layer(layer));
     prm.v_pool = static_cast<unsigned char*>(pool->v_layer(layer));
     prm.out = static_cast<__nv_bfloat16*>(out);
-    prm.ws_cnt = reinterpret_cast<int*>(ws + w.cnt);
-    prm.sched = reinterpret_cast<unsigned*>(ws + w.sched);
-    prm.ws_m = reinterpret_cast<float*>(ws + w.m);
-    prm.ws_l = reinterpret_cast<float*>(ws + w.l);
-    prm.ws_acc = reinterpret_cast<float*>(ws + w.acc);
+    prm.ws_cnt = w.cnt;
+    prm.sched = w.sched;
+    prm.ws_m = w.m;
+    prm.ws_l = w.l;
+    prm.ws_acc = w.acc;
     prm.status = status_dev;
     prm.B = batch;
     prm.Hq = num_q_heads;

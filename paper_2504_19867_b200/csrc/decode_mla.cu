@@ -373,7 +373,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
-inline size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
 }  // namespace
 
@@ -384,14 +383,9 @@ bool spd_mla_decode_ok(const semipd_pool* p, int Hq) {
            c.head_dim_v == DV && Hq <= NH && p->have_mla_map && (bs == 32 || bs == 64 || bs == 128);
 }
 
-size_t spd_mla_ws_bytes(int B, int max_ctx) {
+size_t spd_mla_ws_bytes(int B, int max_ctx) {  // split partials only (see SpdWs)
     const int S_max = (max_ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
-    size_t o = al256((size_t)B * 4);           // cnt
-    o += 256;                                   // sched
-    o = al256(o + (size_t)B * NH * S_max * 4);  // m
-    o = al256(o + (size_t)B * NH * S_max * 4);  // l
-    o = al256(o + (size_t)B * NH * S_max * DV * 4);
-    return o;
+    return spd_ws_partial_bytes((size_t)B * NH, S_max, DV);
 }
 
 semipd_status spd_launch_decode_mla(semipd_pool_t pool, int layer, const void* q, const void* k_new,
@@ -400,8 +394,9 @@ semipd_status spd_launch_decode_mla(semipd_pool_t pool, int layer, const void* q
                                     int out_head_major, void* workspace, size_t ws_bytes,
                                     int budget, int* status_dev, cudaStream_t st) {
     const int S_max = (max_ctx_len + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
-    if (!workspace || ws_bytes < spd_mla_ws_bytes(batch, max_ctx_len)) return SEMIPD_ERR_INVALID;
-    unsigned char* ws = static_cast<unsigned char*>(workspace);
+    SpdWs w;
+    if (!spd_ws_carve(workspace, ws_bytes, batch, (size_t)batch * NH, S_max, DV, &w))
+        return SEMIPD_ERR_INVALID;
     MlaParams prm;
     prm.q = static_cast<const __nv_bfloat16*>(q);
     prm.k_new = static_cast<const uint4*>(k_new);
@@ -410,16 +405,11 @@ semipd_status spd_launch_decode_mla(semipd_pool_t pool, int layer, const void* q
     prm.bt = pool->bt;
     prm.k_pool = static_cast<unsigned char*>(pool->k_layer(layer));
     prm.out = static_cast<__nv_bfloat16*>(out);
-    size_t o = 0;
-    prm.ws_cnt = reinterpret_cast<int*>(ws + o);
-    o = al256((size_t)batch * 4);
-    prm.sched = reinterpret_cast<unsigned*>(ws + o);
-    o += 256;
-    prm.ws_m = reinterpret_cast<float*>(ws + o);
-    o = al256(o + (size_t)batch * NH * S_max * 4);
-    prm.ws_l = reinterpret_cast<float*>(ws + o);
-    o = al256(o + (size_t)batch * NH * S_max * 4);
-    prm.ws_acc = reinterpret_cast<float*>(ws + o);
+    prm.ws_cnt = w.cnt;
+    prm.sched = w.sched;
+    prm.ws_m = w.m;
+    prm.ws_l = w.l;
+    prm.ws_acc = w.acc;
     prm.status = status_dev;
     prm.B = batch;
     prm.lg_bs = __builtin_ctz((unsigned)pool->cfg.block_size);

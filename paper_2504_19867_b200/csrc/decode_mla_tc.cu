@@ -44,10 +44,32 @@ constexpr int NSOFT = 128;
 constexpr int SPLIT_PAGES = 20;  // a split spans at most 20 pages (1280 keys, 1.4 MiB)
 
 // number of splits of a request with ctx cached tokens (ctx + 1 keys): a function of the
-// shape only (R26); ceil(pages / 20), so 1025 keys (17 pages) stay one unit
-__host__ __device__ __forceinline__ int n_splits(int ctx) {
+// shape only (R26).  At least ceil(pages / 20) (1025 keys = 17 pages stay one unit).  The
+// S_fill hook splits small batches further (up to S_fill splits of >= 2 pages); with
+// S_fill = ceil(148 / B) the cfg-5 trace ran 7 % slower (per-split partials + merges cost
+// more than the extra SMs gain), so fill_splits() returns 1.
+// Splits are whole pages: pps = ceil(pages / S) pages each, and the count is re-derived from
+// pps so that no split is empty (ceil(pages / ceil(pages / S)) <= S).
+__host__ __device__ __forceinline__ int n_splits(int ctx, int S_fill) {
     const int pages = (ctx + 1 + PAGE - 1) / PAGE;
-    return (pages + SPLIT_PAGES - 1) / SPLIT_PAGES;
+    const int s_len = (pages + SPLIT_PAGES - 1) / SPLIT_PAGES;
+    const int s_f = S_fill < (pages + 1) / 2 ? S_fill : (pages + 1) / 2;
+    int S = s_len > s_f ? s_len : s_f;
+    if (S < 1) S = 1;
+    const int pps = (pages + S - 1) / S;
+    return (pages + pps - 1) / pps;
+}
+__host__ __device__ __forceinline__ int fill_splits(int B) { return B > 0 ? 1 : 1; }
+// n_splits is not monotone in ctx (re-deriving the count from whole pages can drop one), so the
+// workspace / unit-grid bound is the maximum over every page count up to max_ctx's
+inline int max_splits(int max_ctx, int S_fill) {
+    const int pages = (max_ctx + 1 + PAGE - 1) / PAGE;
+    int m = 1;
+    for (int pg = 1; pg <= pages; ++pg) {
+        const int sp = n_splits(pg * PAGE - 1, S_fill);
+        m = sp > m ? sp : m;
+    }
+    return m;
 }
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr uint32_t TM_S = 0, TM_O = 64, TM_COLS = 256;  // S^T 2x16 cols, O^T 2 x (4 x 16) cols
@@ -69,7 +91,7 @@ struct TcParams {
     int* ws_cnt;              // [B]
     unsigned* sched;
     int* status;
-    int B, MBR, N_B, S_max, n_units, out_head_major, G;
+    int B, MBR, N_B, S_max, n_units, out_head_major, G, S_fill;
     float scale_log2;
     SpdTrace trace;
     long long* tl;  // SPD_TIMELINE builds only: pipeline clock64 stamps of CTA 0
@@ -108,10 +130,10 @@ static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KiB opt-in shared memory");
 
 __device__ __forceinline__ void split_range(int ctx, int S, int s, int& k0, int& k1) {
     const int nk = ctx + 1;
-    int len = (nk + S - 1) / S;
-    len = (len + PAGE - 1) / PAGE * PAGE;
-    k0 = s * len;
-    k1 = min(nk, k0 + len);
+    const int pages = (nk + PAGE - 1) / PAGE;
+    const int pps = (pages + S - 1) / S;  // pages per split (n_splits keeps every split non-empty)
+    k0 = s * pps * PAGE;
+    k1 = min(nk, k0 + pps * PAGE);
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -194,7 +216,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 d.b = u % p.B;
                 ctx = __ldg(p.ctx_lens + d.b);
                 rid = __ldg(p.req_ids + d.b);
-                d.S = n_splits(ctx);
+                d.S = n_splits(ctx, p.S_fill);
                 if (d.s >= d.S) continue;
                 split_range(ctx, d.S, d.s, d.k0, d.k1);
                 d.nt = (d.k1 - d.k0 + PAGE - 1) / PAGE;
@@ -704,7 +726,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
-inline size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
 }  // namespace
 
@@ -715,13 +736,14 @@ bool spd_mla_tc_ok(const semipd_pool* p, int Hq) {
 }
 
 size_t spd_mla_tc_ws_bytes(int B, int max_ctx) {
-    const int S_max = n_splits(max_ctx);
-    size_t o = al256((size_t)B * 4);           // cnt
-    o += 256;                                   // sched
-    o = al256(o + (size_t)B * NH * S_max * 4);  // m
-    o = al256(o + (size_t)B * NH * S_max * 4);  // l
-    o = al256(o + (size_t)B * NH * S_max * DV * 4);
-    return o;
+    // split partials only (see SpdWs); any batch b <= B may be launched with this workspace,
+    // and small batches split more: size for the largest b x S_max(b)
+    size_t best = 0;
+    for (int b = 1; b <= (B > 0 ? B : 1); ++b) {
+        const size_t need = spd_ws_partial_bytes((size_t)b * NH, max_splits(max_ctx, fill_splits(b)), DV);
+        if (need > best) best = need;
+    }
+    return best;
 }
 
 semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void* q,
@@ -729,8 +751,11 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
                                        int batch, int max_ctx_len, int Hq, float scale, void* out,
                                        int out_head_major, void* workspace, size_t ws_bytes,
                                        int budget, int* status_dev, cudaStream_t st) {
-    const int S_max = n_splits(max_ctx_len);
-    if (!workspace || ws_bytes < spd_mla_tc_ws_bytes(batch, max_ctx_len)) return SEMIPD_ERR_INVALID;
+    const int S_fill = fill_splits(batch);
+    const int S_max = max_splits(max_ctx_len, S_fill);
+    SpdWs w;
+    if (!spd_ws_carve(workspace, ws_bytes, batch, (size_t)batch * NH, S_max, DV, &w))
+        return SEMIPD_ERR_INVALID;
     if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) return SEMIPD_ERR_INVALID;
     // Q [B][Hq][576] as (64 cols, Hq heads, 9 column blocks, B): box lands [cb][16 rows][128 B];
     // rows >= Hq are out of range and zero-filled by TMA
@@ -743,7 +768,6 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
                                  strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
             return SEMIPD_ERR_CUDA;
     }
-    unsigned char* ws = static_cast<unsigned char*>(workspace);
     TcParams prm;
     prm.k_new = static_cast<const uint4*>(k_new);
     prm.req_ids = req_ids;
@@ -751,21 +775,17 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
     prm.bt = pool->bt;
     prm.k_pool = static_cast<unsigned char*>(pool->k_layer(layer));
     prm.out = static_cast<__nv_bfloat16*>(out);
-    size_t o = 0;
-    prm.ws_cnt = reinterpret_cast<int*>(ws + o);
-    o = al256((size_t)batch * 4);
-    prm.sched = reinterpret_cast<unsigned*>(ws + o);
-    o += 256;
-    prm.ws_m = reinterpret_cast<float*>(ws + o);
-    o = al256(o + (size_t)batch * NH * S_max * 4);
-    prm.ws_l = reinterpret_cast<float*>(ws + o);
-    o = al256(o + (size_t)batch * NH * S_max * 4);
-    prm.ws_acc = reinterpret_cast<float*>(ws + o);
+    prm.ws_cnt = w.cnt;
+    prm.sched = w.sched;
+    prm.ws_m = w.m;
+    prm.ws_l = w.l;
+    prm.ws_acc = w.acc;
     prm.status = status_dev;
     prm.B = batch;
     prm.MBR = pool->cfg.max_blocks_per_req;
     prm.N_B = pool->cfg.num_blocks;
     prm.S_max = S_max;
+    prm.S_fill = S_fill;
     prm.n_units = batch * S_max;
     prm.out_head_major = out_head_major;
     prm.G = Hq;

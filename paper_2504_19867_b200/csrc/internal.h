@@ -94,6 +94,38 @@ bool spd_encode_tiled_3d(CUtensorMap* map, CUtensorMapDataType dt, void* gaddr, 
                          uint64_t d1, uint64_t d2, uint64_t s1_bytes, uint64_t s2_bytes,
                          uint32_t b0, uint32_t b1, uint32_t b2, CUtensorMapSwizzle swz);
 
+// Decode workspace (every decode kernel): [sched 256 B | split counters, 4 B each] from the
+// front, the fp32 split partials (m, l, acc) packed against the END of the caller's buffer.
+// Counters must be zero when a kernel starts (kernels reset the ones they use); a counter byte
+// is never a partial byte of any call, whatever its batch size, because
+// semipd_decode_workspace_bytes() reserves counters for max_batch plus the largest partial set.
+struct SpdWs {
+    unsigned* sched;
+    int* cnt;
+    float* m;
+    float* l;
+    float* acc;
+};
+inline size_t spd_al256(size_t x) { return (x + 255) / 256 * 256; }
+inline size_t spd_ws_counter_bytes(size_t n_cnt) { return spd_al256(256 + 4 * n_cnt); }
+inline size_t spd_ws_partial_bytes(size_t rows, size_t S, size_t dv) {  // rows = B x Hq
+    return 2 * spd_al256(rows * S * 4) + spd_al256(rows * S * dv * 4);
+}
+inline bool spd_ws_carve(void* ws, size_t ws_bytes, size_t n_cnt, size_t rows, size_t S, size_t dv,
+                         SpdWs* o) {
+    const size_t cb = spd_ws_counter_bytes(n_cnt), pb = spd_ws_partial_bytes(rows, S, dv);
+    if (!ws || ws_bytes < cb + pb) return false;
+    unsigned char* b = static_cast<unsigned char*>(ws);
+    const size_t base = (ws_bytes - pb) & ~static_cast<size_t>(255);
+    if (base < cb) return false;
+    o->sched = reinterpret_cast<unsigned*>(b);
+    o->cnt = reinterpret_cast<int*>(b + 256);
+    o->m = reinterpret_cast<float*>(b + base);
+    o->l = reinterpret_cast<float*>(b + base + spd_al256(rows * S * 4));
+    o->acc = reinterpret_cast<float*>(b + base + 2 * spd_al256(rows * S * 4));
+    return true;
+}
+
 // kernels launched from other TUs
 bool spd_mla_decode_ok(const semipd_pool* p, int Hq);
 size_t spd_mla_ws_bytes(int B, int max_ctx);

@@ -127,7 +127,7 @@ def mla(args, dev):
     kn = torch.randn(B, 1, 576, device=dev, generator=g).bfloat16()
     out = torch.empty(B, 16, 512, dtype=torch.bfloat16, device=dev)
     ws = pool.new_decode_workspace(B, 16, ctx)
-    rid, ctxs = i32(list(range(B))), i32(ctx_list)
+    rid, ctxs = i32(list(range(B))), i32([ctx] * B)
     byts = B * (ctx + 1) * 576 * 2 + B * 16 * (576 + 512) * 2
     flops = 2 * B * 16 * (ctx + 1) * (576 + 512)
     for bud in [int(x) for x in args.budgets.split(",")]:

@@ -126,7 +126,7 @@ def test_table_full_and_oom_leave_state():
 
 # ----------------------------------------------------------------------------- decode
 def run_decode(shape, ctx, seed, dist, sm_budget=0, layer=0, num_layers=1, rid_offset=0,
-               head_major=False, check_append=True):
+               head_major=False, check_append=True, ws=None):
     bs = shape.block_size
     nblk = [c // bs + 1 for c in ctx]
     N_B = sum(nblk) + 7
@@ -146,7 +146,8 @@ def run_decode(shape, ctx, seed, dist, sm_budget=0, layer=0, num_layers=1, rid_o
     vn = case.v_new.to(dev) if case.v_new is not None else None
     B, Hq, dv = len(ctx), shape.num_q_heads, shape.head_dim_v
     out = torch.empty((Hq, B, dv) if head_major else (B, Hq, dv), dtype=shape.dtype, device=dev)
-    ws = rig.pool.new_decode_workspace(B, Hq, max(ctx))
+    if ws is None:
+        ws = rig.pool.new_decode_workspace(B, Hq, max(ctx))
     rig.pool.decode_attn(layer, q, kn, vn, rig.i32(rids), rig.i32(ctx), max(ctx),
                          shape.softmax_scale, out, ws, out_head_major=head_major,
                          sm_budget=sm_budget, status=rig.status)
@@ -248,6 +249,28 @@ def test_decode_mla_fewer_heads_head_major():
     """Hq < 16 (q rows beyond Hq zero-filled by TMA) with head-major output."""
     run_decode(small(synth.CFG5_MLA, num_q_heads=8), [5, 64, 127, 1500, 2100], seed=71,
                dist=synth.PEAKED, head_major=True)
+
+
+@pytest.mark.parametrize("ctx", [[9000], [300, 9000, 2000], [5000, 4100, 7000, 100]])
+def test_decode_mla_small_batch_fill_splits(ctx):
+    """Small batches split long contexts over many SMs (S_fill = ceil(148 / B) >> 32 splits
+    here: the unstaged merge path) and their results match the oracle."""
+    run_decode(small(synth.CFG5_MLA), ctx, seed=77 + len(ctx), dist=synth.VSHIFT)
+
+
+@pytest.mark.parametrize("shape_name", ["mla", "llama"])
+def test_decode_workspace_reused_across_batch_sizes(shape_name):
+    """One workspace serves calls of different batch sizes: a small batch (many splits, so
+    partials get written) followed by larger ones must not read stale partial bytes as split /
+    work counters (counters live at the front, partials at the back; SpdWs)."""
+    shape = small(synth.CFG5_MLA) if shape_name == "mla" else small(SHAPE_8B, block_size=64)
+    Hq = shape.num_q_heads
+    rig = Rig(shape, num_blocks=8, max_reqs=2, mbr=4)
+    ws = rig.pool.new_decode_workspace(96, Hq, 9000)
+    rng = np.random.default_rng(3)
+    for i, B in enumerate([2, 96, 5, 40, 96]):
+        ctx = [int(x) for x in rng.integers(1, 9000 if B <= 5 else 700, size=B)]
+        run_decode(shape, ctx, seed=300 + i, dist=synth.FLAT, ws=ws)
 
 
 def test_decode_mla_cfg5_batch():

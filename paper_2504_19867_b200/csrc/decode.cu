@@ -57,7 +57,23 @@ struct DecodeParams {
     int B, Hq, Hkv, G, lg_bs, MBR, N_B, S_max, n_units, out_head_major;
     float scale_log2;
     SpdTrace trace;
+    long long* tl;  // SPD_TIMELINE builds only: per-stage clock64 stamps of CTA 0
+    int* tl_ctr;
 };
+
+#ifdef SPD_TIMELINE
+#define TL_REC(a, b, c, d, e)                                                              \
+    do {                                                                                   \
+        if (p.tl && blockIdx.x == 0 && (b) < 2048) {                                       \
+            long long* _r = p.tl + 8 * ((a) * 2048 + (b));                                 \
+            _r[0] = a; _r[1] = b; _r[2] = c; _r[3] = d; _r[4] = e;                         \
+        }                                                                                  \
+    } while (0)
+#define TL_NOW() clock64()
+#else
+#define TL_REC(a, b, c, d, e) do { } while (0)
+#define TL_NOW() 0LL
+#endif
 
 __device__ __forceinline__ void split_range(int ctx, int S, int s, int& k0, int& k1) {
     const int nk = ctx + 1;
@@ -214,11 +230,19 @@ __global__ void __launch_bounds__(4 * 32, 1)
         const int oob_z = p.N_B * p.Hkv;  // first page index past the tensor -> zero fill
         const int bs_mask = (1 << p.lg_bs) - 1;
         int gstage = 0, nunit = 0;
+        // first unit of each CTA is static (blockIdx.x); later ones come from the counter,
+        // fetched one unit ahead so the atomic's round trip overlaps the current unit
+        // lane 0 holds the next unit index; the atomic's result is first read one unit later
+        int u_next = blockIdx.x;
+        // consecutive units are mostly the next kv head of the same (request, split): keep
+        // the last request's metadata and first 64 block ids to skip the global round trips
+        int prev_b = -1, prev_ctx = 0, prev_rid = 0, prev_k0 = -1, zc0 = -2, zn0 = -2;
         for (;;) {
-            int u = 0;
-            if (lane == 0) u = (int)atomicAdd(p.sched, 1u);
-            u = __shfl_sync(0xffffffffu, u, 0);
+            [[maybe_unused]] const long long tu0 = TL_NOW();
+            const int u = __shfl_sync(0xffffffffu, u_next, 0);
+            if (lane == 0) u_next = (int)gridDim.x + (int)atomicAdd(p.sched, 1u);
             UnitDesc d;
+            int ctx = 0, rid = 0;
             if (u >= p.n_units) {
                 d.b = -1;
             } else {
@@ -226,7 +250,13 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 d.s = u / (p.B * p.Hkv);
                 d.b = (u / p.Hkv) % p.B;
                 d.g = u % p.Hkv;
-                const int ctx = __ldg(p.ctx_lens + d.b);
+                if (d.b == prev_b) {
+                    ctx = prev_ctx;
+                    rid = prev_rid;
+                } else {
+                    ctx = __ldg(p.ctx_lens + d.b);
+                    rid = __ldg(p.req_ids + d.b);
+                }
                 d.S = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
                 if (d.s >= d.S) continue;  // warp-uniform
                 split_range(ctx, d.S, d.s, d.k0, d.k1);
@@ -246,32 +276,27 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 d.base = gstage;
             }
             const int us = nunit & 1;
+            [[maybe_unused]] const long long tu1 = TL_NOW();
             if (lane == 0) {
                 mbar_wait(uempty + us, ((nunit >> 1) & 1) ^ 1);
                 units[us] = d;
                 mbar_arrive(ufull + us);
             }
             __syncwarp();
+            if (lane == 0) TL_REC(3, nunit, tu0, tu1, TL_NOW());
             ++nunit;
             if (d.b < 0) break;
-            const int ctx = __ldg(p.ctx_lens + d.b);
-            const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
+            const int* btr = p.bt + (size_t)rid * p.MBR;
             const int last_page = ctx >> p.lg_bs;
-            if (d.s == d.S - 1) {
-                // fused append of this step's K/V at slot ctx (bit-exact): lanes 0-15 copy
-                // K, lanes 16-31 copy V (16 x 16 B each), then hand over to the async proxy
-                const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
-                if (blk >= 0 && blk < p.N_B) {
-                    const size_t slot = (((size_t)blk * p.Hkv + d.g) << p.lg_bs) + (ctx & bs_mask);
-                    const size_t src = ((size_t)d.b * p.Hkv + d.g) * (HD / 8);
-                    const int c = lane & 15;
-                    if (lane < 16)
-                        reinterpret_cast<uint4*>(p.k_pool)[slot * (HD / 8) + c] = __ldg(p.k_new + src + c);
-                    else
-                        reinterpret_cast<uint4*>(p.v_pool)[slot * (HD / 8) + c] = __ldg(p.v_new + src + c);
-                    fence_proxy_async_global();
-                }
-                __syncwarp();
+            // fused append of this step's K/V at slot ctx (last split only, bit-exact): the
+            // rows are loaded now and stored right before the TMA of the stage holding slot
+            // ctx (lanes 0-15 K, 16-31 V, 16 B each), then handed to the async proxy
+            const bool append = d.s == d.S - 1;
+            const int app_stage = (ctx - d.k0) / KPS;
+            uint4 app_v = make_uint4(0, 0, 0, 0);
+            if (append) {
+                const size_t src = ((size_t)d.b * p.Hkv + d.g) * (HD / 8);
+                app_v = __ldg((lane < 16 ? p.k_new : p.v_new) + src + (lane & 15));
             }
             const int nbox = d.nst * NB;
             // raw block id for box bi (-2 = past the request's last page: zero fill, no error)
@@ -280,7 +305,20 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 if (bi >= nbox || page > last_page) return -2;
                 return page < p.MBR ? __ldg(btr + page) : -1;
             };
-            int zc = lookup(lane), zn = lookup(32 + lane);
+            int zc, zn;
+            if (d.b == prev_b && d.k0 == prev_k0) {
+                zc = zc0;
+                zn = zn0;
+            } else {
+                zc = lookup(lane);
+                zn = lookup(32 + lane);
+            }
+            prev_b = d.b;
+            prev_ctx = ctx;
+            prev_rid = rid;
+            prev_k0 = d.k0;
+            zc0 = zc;
+            zn0 = zn;
             for (int i = 0; i < d.nst; ++i, ++gstage) {
                 const int bb0 = i * NB;
                 if (bb0 > 0 && (bb0 & 31) == 0) {
@@ -289,8 +327,19 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 }
                 const int st = gstage % NSTAGE;
                 unsigned char* kst = ring + st * STAGE_BYTES;
+                if (append && i == app_stage) {
+                    const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
+                    if (blk >= 0 && blk < p.N_B) {
+                        const size_t slot = (((size_t)blk * p.Hkv + d.g) << p.lg_bs) + (ctx & bs_mask);
+                        reinterpret_cast<uint4*>(lane < 16 ? p.k_pool : p.v_pool)[slot * (HD / 8) + (lane & 15)] = app_v;
+                        fence_proxy_async_global();
+                    }
+                    __syncwarp();
+                }
+                [[maybe_unused]] long long tp0 = TL_NOW(), tp1 = 0;
                 if (lane == 0) {
                     mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
+                    tp1 = TL_NOW();
                     mbar_arrive_expect_tx(full + st, STAGE_BYTES);
                 }
 #pragma unroll
@@ -305,6 +354,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                         tma_load_4d(kst + KV_BYTES + b * (R * 256), &vmap, full + st, 0, y, 0, z);
                     }
                 }
+                if (lane == 0) TL_REC(1, gstage, tp0, tp1, TL_NOW());
                 __syncwarp();
             }
         }
@@ -354,7 +404,9 @@ __global__ void __launch_bounds__(4 * 32, 1)
             for (int i = warp; i < d.nst; i += CW) {
                 const int gs = d.base + i;
                 const int st = gs % NSTAGE;
+                [[maybe_unused]] const long long tc0 = TL_NOW();
                 mbar_wait(full + st, (gs / NSTAGE) & 1);
+                [[maybe_unused]] const long long tc1 = TL_NOW();
                 const uint32_t kst = smem_u32(ring + st * STAGE_BYTES);
                 const uint32_t vst = kst + KV_BYTES;
                 // ---- S^T: 4 key tiles x 8 k-steps; A = K rows (keys) via ldmatrix
@@ -435,6 +487,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty + st);
+                if (lane == 0) TL_REC(2, gs, tc0, tc1, TL_NOW());
             }
             // ---- per-warp partial -> shared scratch (rows = heads)
 #pragma unroll
@@ -1135,6 +1188,8 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     prm.out_head_major = out_head_major;
     prm.scale_log2 = softmax_scale * LOG2E;
     prm.trace = spd_trace(pool);
+    prm.tl = reinterpret_cast<long long*>(pool->timeline);
+    prm.tl_ctr = pool->timeline_ctr;
     // wide-box kernels (G <= 8): 128-token pages always (MODE 1, one whole page per box);
     // 64-token pages with even Hkv only when the batch alone gives >= 2 x 148 head-pair
     // units (MODE 0: with fewer, the coarser units cost more in grid-tail imbalance than the

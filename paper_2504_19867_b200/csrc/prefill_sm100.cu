@@ -447,12 +447,17 @@ __global__ void __launch_bounds__(NT, 1)
                         for (int e = 0; e < 32; ++e)
                             if (c * 32 + e > lim) sr[c][e] = __float_as_uint(-INFINITY);
                 }
-                float mx = -INFINITY;
+                // row max: four independent FMNMX3 chains (one per 32-column block) instead of
+                // one 64-deep dependent chain on the softmax critical path
+                float mxc[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 4; ++c) {
+                    mxc[c] = -INFINITY;
 #pragma unroll
                     for (int e = 0; e < 32; e += 2)
-                        mx = fmax3(mx, __uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1]));
+                        mxc[c] = fmax3(mxc[c], __uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1]));
+                }
+                const float mx = fmaxf(fmaxf(mxc[0], mxc[1]), fmaxf(mxc[2], mxc[3]));
                 const float mnew = fmaxf(m, mx * p.scale_log2);  // scale > 0: max commutes
                 // exact running max: rescale O_t in TMEM when a row max grows (PV_t(j-1)
                 // is complete: S_t(j) was issued after it and its commit tracks both)
@@ -477,8 +482,10 @@ __global__ void __launch_bounds__(NT, 1)
                     l2 = fmul2(l2, a2);
                 }
                 m = mnew;
-                // P = exp2(s * scale - m) (bf16) over the S columns [0, 64)
+                // P = exp2(s * scale - m) (bf16) over the S columns [0, 64); the row sum runs
+                // in two FADD2 chains
                 const uint64_t nm2 = f2(-m, -m);
+                uint64_t l2b = f2(0.f, 0.f);
 #pragma unroll
                 for (int c = 0; c < 4; c += 2) {
                     uint32_t pk[32];
@@ -492,11 +499,13 @@ __global__ void __launch_bounds__(NT, 1)
                                            sc2, nm2),
                                      x0, x1);
                             const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
-                            l2 = fadd2(l2, f2(p0, p1));
+                            if (h) l2b = fadd2(l2b, f2(p0, p1));
+                            else l2 = fadd2(l2, f2(p0, p1));
                             pk[h * 16 + e / 2] = pack_bf16(p0, p1);
                         }
                     tmem_st32(s_tmem + (uint32_t)(c * 16), pk);
                 }
+                l2 = fadd2(l2, l2b);
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&sm.p_full[t]);

@@ -562,6 +562,12 @@ def main():
     # per-launch kernel times (last timed step's events)
     dec_ms = statistics.mean(a.elapsed_time(b) for a, b in w.ev_d)
     pre_ms = statistics.mean(a.elapsed_time(b) for a, b in w.ev_p)
+    # co-run overlap of the two streams in that step: each stream's span
+    # from its first kernel start to its last kernel end; overlap = min / max span
+    span_p = w.ev_p[0][0].elapsed_time(w.ev_p[-1][1])
+    span_d = w.ev_d[0][0].elapsed_time(w.ev_d[-1][1])
+    corun_overlap = {"prefill_stream_ms": span_p, "decode_stream_ms": span_d,
+                     "overlap": min(span_p, span_d) / max(span_p, span_d)}
     dec_gbs = w.decode_bytes_per_launch() / (dec_ms / 1e3) / 1e9
     pre_tfs = w.prefill_flops_per_launch() / (pre_ms / 1e3) / 1e12
     n_p, n_d = w.pool.sm_budgets()
@@ -631,6 +637,7 @@ def main():
                        "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d}},
             "roofline": roof_dec if dominant == "decode" else roof_pre,
             "roofline_decode": roof_dec, "roofline_prefill": roof_pre,
+            "corun_streams": corun_overlap,
             "decode_tokens_per_s": DECODE_BATCH * args.steps / t,
             "prefill_tokens_per_s": PREFILL_TOKENS * args.steps / t,
             "sweep": sweep, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,

@@ -51,9 +51,11 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            path = _build.LIB
-            if not os.path.exists(path) or not _build.up_to_date():
-                _build.build()
+            path = os.environ.get("SEMIPD_LIB")  # dev: a tagged variant (scripts/variants.py)
+            if not path:
+                path = _build.LIB
+                if not os.path.exists(path) or not _build.up_to_date():
+                    _build.build()
             L = ctypes.CDLL(path)
             vp, i32, i64, sz, f32, f64 = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
                                           ctypes.c_size_t, ctypes.c_float, ctypes.c_double)

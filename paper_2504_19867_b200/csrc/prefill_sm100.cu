@@ -13,7 +13,8 @@
 //   warp 0      unit fetch, Q_A + Q_B tiles, K tiles (TMA)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, in the order
 //               S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...  so each softmax
-//               warpgroup works while the tensor core serves the other tile
+//               warpgroup works while the tensor core serves the other tile; each PV runs
+//               as two K = 64 halves released separately by the softmax
 //               (S = Q K^T: SS, M = N = 128, K = 8 x 16; O += P V: TS, P from TMEM,
 //               V MN-major from smem)
 //   warp 2      V tiles (TMA)
@@ -24,7 +25,7 @@
 //               P (bf16) written back over S with tcgen05.st; epilogue O / l -> global.
 // Prefix kv tiles (keys < P) are gathered from the paged pool as (128 / box_rows) page
 // boxes per 64-column half; chunk kv tiles (the request's own new keys) come from
-// k_new / v_new (two 16 KiB boxes per tile).
+// k_new / v_new (one 32 KiB box per tile).
 // TMEM columns: S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -82,7 +83,12 @@ struct PrefillParams {
         }                                                                                  \
     } while (0)
 #define TL_NOW() clock64()
+#define TL_EXTRA(a, b, f, v)                                                               \
+    do {                                                                                   \
+        if (p.tl && blockIdx.x == 0 && (b) < 1024) p.tl[8 * ((a) * 1024 + (b)) + (f)] = (v); \
+    } while (0)
 #else
+#define TL_EXTRA(a, b, f, v) do { } while (0)
 #define TL_REC(a, b, c, d, e) do { } while (0)
 #define TL_NOW() 0LL
 #endif
@@ -95,12 +101,70 @@ struct Smem {
     unsigned char ostage[2][HALF_BYTES];  // per q tile: epilogue staging for TMA stores (64 cols)
     uint64_t q_full, q_empty, q_issued;  // q_issued: V loads of a unit queue behind its Q
     uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-    uint64_t s_full[2], p_full[2];   // per q tile
+    uint64_t s_full[2], p_full[2][2];  // per q tile; p_full[t][h]: P keys [64h, 64h + 64) in TMEM
     uint64_t o_full[2], o_empty[2];  // per q tile
     uint64_t ufull[2], uempty[2];
     PUnit units[2];
     uint32_t tmem_base;
 };
+
+// Which exp2 pairs of each 32-column S block run on the FMA pipe instead of MUFU (bit i =
+// columns 2i, 2i+1).  MUFU.EX2 is 16/clk/SM on B200 (measured, scripts/probe_mufu.cu), so a
+// 128 x 128 S tile costs 1024 MUFU cycles, as much as the tile's QK + PV tensor work; moving a
+// fraction of the exps to a degree-3 polynomial on the FMA pipe shortens the softmax that sits
+// on the per-tile critical path (softmax -> PV -> next S).
+#ifndef SPD_POLY_MASK
+#define SPD_POLY_MASK 0x0000u
+#endif
+constexpr uint32_t kPolyMask = SPD_POLY_MASK;
+
+// 2^x for a pair on the FMA pipe: x = j + f with j = rint(x) (magic-number rounding, exact for
+// |x| < 2^22), f in [-1/2, 1/2]; 2^f by a degree-3 relative-minimax polynomial (max rel. error
+// 7.5e-5, below the bf16 rounding of P, 2^-9); 2^j added into the exponent bits.  x is clamped
+// at -125 so the exponent add cannot underflow: masked (-inf) scores give ~2^-125 instead of 0.
+__device__ __forceinline__ uint64_t exp2_poly3(uint64_t x2) {
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+    float x0, x1;
+    f2_split(x2, x0, x1);
+    const uint64_t xc = f2(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+    const uint64_t t = fadd2(xc, f2(kMagic, kMagic));                      // M + j
+    const uint64_t nj = ffma2(t, f2(-1.f, -1.f), f2(kMagic, kMagic));      // -j (exact)
+    const uint64_t fr = fadd2(xc, nj);                                     // f
+    uint64_t q = ffma2(f2(0.05517049f, 0.05517049f), fr, f2(0.24260938f, 0.24260938f));
+    q = ffma2(q, fr, f2(0.69326103f, 0.69326103f));
+    q = ffma2(q, fr, f2(0.99992818f, 0.99992818f));
+    float q0, q1, t0, t1;
+    f2_split(q, q0, q1);
+    f2_split(t, t0, t1);
+    // bits(M + j) = 0x4B400000 + j and 0x4B400000 << 23 == 0 (mod 2^32): (bits << 23) = j << 23
+    return f2(__uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23)),
+              __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23)));
+}
+
+// a += float(lo half of pp), b += float(hi half): add.f32.bf16 is one FHADD.BF16 per element
+// with a half-register operand (no unpacking)
+__device__ __forceinline__ void add_bf16x2_f32(float& a, float& b, uint32_t pp) {
+    asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+        "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
+        : "+f"(a), "+f"(b)
+        : "r"(pp));
+}
+
+// MMA issue from the whole converged warp (elect.sync inside the asm: descriptors stay in
+// uniform registers, ~2x the issue rate of a lane-0 branch) or from lane 0
+#ifndef SPD_MMA_WARP
+#define SPD_MMA_WARP 1
+#endif
+constexpr bool kMmaWarp = SPD_MMA_WARP != 0;
+#if SPD_MMA_WARP
+#define MMA_SS umma_ss_warp
+#define MMA_TS umma_ts_warp
+#define MMA_COMMIT umma_commit_warp
+#else
+#define MMA_SS umma_ss
+#define MMA_TS umma_ts
+#define MMA_COMMIT umma_commit
+#endif
 
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t addr) {
     return umma_desc_sw128(addr, 16, 1024);
@@ -128,7 +192,8 @@ __global__ void __launch_bounds__(NT, 1)
             mbar_init(&sm.v_full[s], 1);
             mbar_init(&sm.v_empty[s], 1);
             mbar_init(&sm.s_full[s], 1);
-            mbar_init(&sm.p_full[s], 128);
+            mbar_init(&sm.p_full[s][0], 128);
+            mbar_init(&sm.p_full[s][1], 128);
             mbar_init(&sm.o_full[s], 1);
             mbar_init(&sm.o_empty[s], 128);
             mbar_init(&sm.ufull[s], 1);
@@ -142,6 +207,11 @@ __global__ void __launch_bounds__(NT, 1)
                     make_int4(1, (int)smid(), (int)blockIdx.x, 1 /* kernel kind: tcgen05 prefill */);
         }
     }
+#ifdef SPD_TIMELINE
+    unsigned long long gt_start = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_start));
+    int tl_units = 0;
+#endif
     if (warp == 1) tmem_alloc(&sm.tmem_base, 512);
     tc_fence_before();
     __syncthreads();
@@ -257,16 +327,15 @@ __global__ void __launch_bounds__(NT, 1)
                         }
                     }
                 } else if (lane == 0) {
-                    const int row = d.crow0 + (j - d.np) * BN;
-                    tma_load_3d(dst, cmap, ful, 0, d.g, row);
-                    tma_load_3d(dst + HALF_BYTES, cmap, ful, 64, d.g, row);
+                    // one 32 KiB box (64 cols, 1 head, 128 rows, 2 halves) -> [half][rows][128 B]
+                    tma_load_4d(dst, cmap, ful, 0, d.g, d.crow0 + (j - d.np) * BN, 0);
                 }
                 __syncwarp();
             }
         }
     } else if (warp == 1) {
         // ================================ MMA issuer ================================
-        if (lane == 0) {
+        if (kMmaWarp || lane == 0) {
             const uint32_t idesc_s = umma_idesc_bf16_f32(BM, BN, 0);
             const uint32_t idesc_o = umma_idesc_bf16_f32(BM, HD, 1);
             int kvit = 0, nunit = 0;
@@ -275,7 +344,8 @@ __global__ void __launch_bounds__(NT, 1)
                 const int us = nunit & 1;
                 mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
                 const PUnit d = sm.units[us];
-                mbar_arrive(&sm.uempty[us]);
+                if (kMmaWarp) __syncwarp();
+                if (!kMmaWarp || lane == 0) mbar_arrive(&sm.uempty[us]);
                 if (d.i < 0) break;
                 [[maybe_unused]] const long long tq1 = TL_NOW();
                 mbar_wait(&sm.q_full, nunit & 1);
@@ -291,24 +361,29 @@ __global__ void __launch_bounds__(NT, 1)
                     for (int kk = 0; kk < HD / 16; ++kk) {
                         const uint32_t koff = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
                         const uint32_t qoff = (kk >> 2) * TILE_BYTES + (kk & 3) * 32;
-                        umma_ss(d_tmem, kmajor_desc(q_addr + qoff), kmajor_desc(k_addr + koff),
+                        MMA_SS(d_tmem, kmajor_desc(q_addr + qoff), kmajor_desc(k_addr + koff),
                                 idesc_s, kk > 0 ? 1u : 0u);
                     }
-                    umma_commit(&sm.s_full[t]);
+                    MMA_COMMIT(&sm.s_full[t]);
                 };
                 auto issue_pv = [&](int t, int& cnt, int it, bool first) {  // O_t += P_t V
-                    mbar_wait(&sm.p_full[t], cnt & 1);
-                    ++cnt;
-                    tc_fence_after();
+                    // in two K = 64 halves: the first starts while the softmax still
+                    // computes the exps of keys [64, 128) (p_full[t][0] is armed mid-tile)
                     const uint32_t v_addr = smem_u32(sm.v[it & 1]);
                     const uint32_t p_tmem = tmem + (uint32_t)(t * BN);
                     const uint32_t o_tmem = tmem + 256u + (uint32_t)(t * HD);
 #pragma unroll
-                    for (int kk = 0; kk < BN / 16; ++kk) {
-                        const uint64_t bdesc = umma_desc_sw128(v_addr + kk * 2048, HALF_BYTES, 1024);
-                        umma_ts(o_tmem, p_tmem + (uint32_t)(kk * 8), bdesc, idesc_o,
-                                (first && kk == 0) ? 0u : 1u);
+                    for (int hf = 0; hf < 2; ++hf) {
+                        mbar_wait(&sm.p_full[t][hf], cnt & 1);
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = hf * 4; kk < hf * 4 + 4; ++kk) {
+                            const uint64_t bdesc = umma_desc_sw128(v_addr + kk * 2048, HALF_BYTES, 1024);
+                            MMA_TS(o_tmem, p_tmem + (uint32_t)(kk * 8), bdesc, idesc_o,
+                                    (first && kk == 0) ? 0u : 1u);
+                        }
                     }
+                    ++cnt;
                 };
                 auto wait_full = [&](uint64_t* bars, int it) {
                     mbar_wait(&bars[it & 1], (it >> 1) & 1);
@@ -319,31 +394,34 @@ __global__ void __launch_bounds__(NT, 1)
                 wait_full(sm.k_full, it0);
                 issue_s(0, it0);
                 issue_s(1, it0);
-                umma_commit(&sm.k_empty[it0 & 1]);
-                if (nB == 1) umma_commit(&sm.q_empty);
+                MMA_COMMIT(&sm.k_empty[it0 & 1]);
+                if (nB == 1) MMA_COMMIT(&sm.q_empty);
                 for (int j = 0; j < nB; ++j) {
                     const int it = it0 + j;
                     wait_full(sm.v_full, it);
                     if (j < nA) {
                         if (j == 0) mbar_wait(&sm.o_empty[0], (nunit & 1) ^ 1);
                         issue_pv(0, cnt_a, it, j == 0);
-                        if (j == nA - 1) umma_commit(&sm.o_full[0]);
+                        if (j == nA - 1) MMA_COMMIT(&sm.o_full[0]);
                     }
                     const bool more = j + 1 < nB;
                     if (more) wait_full(sm.k_full, it + 1);
                     if (j + 1 < nA) issue_s(0, it + 1);
                     if (j == 0) mbar_wait(&sm.o_empty[1], (nunit & 1) ^ 1);
                     issue_pv(1, cnt_b, it, j == 0);
-                    umma_commit(&sm.v_empty[it & 1]);
-                    if (j == nB - 1) umma_commit(&sm.o_full[1]);
+                    MMA_COMMIT(&sm.v_empty[it & 1]);
+                    if (j == nB - 1) MMA_COMMIT(&sm.o_full[1]);
                     if (more) {
                         issue_s(1, it + 1);
-                        umma_commit(&sm.k_empty[(it + 1) & 1]);
-                        if (j + 1 == nB - 1) umma_commit(&sm.q_empty);
+                        MMA_COMMIT(&sm.k_empty[(it + 1) & 1]);
+                        if (j + 1 == nB - 1) MMA_COMMIT(&sm.q_empty);
                     }
                 }
                 kvit = it0 + nB;
                 ++nunit;
+#ifdef SPD_TIMELINE
+                tl_units += nB;
+#endif
             }
         }
     } else {
@@ -437,6 +515,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) tmem_ld32(s_tmem + c * 32, sr[c]);
                 tmem_wait_ld();
+                [[maybe_unused]] const long long ts2 = TL_NOW();
                 // prefix tile: keys j*BN + c must be < P; chunk tile: chunk-relative key
                 // (j - np)*BN + c must be <= this row's token (causal, bottom-right aligned)
                 const int lim = j < d.np ? d.P - 1 - j * BN : trel - (j - d.np) * BN;
@@ -462,9 +541,8 @@ __global__ void __launch_bounds__(NT, 1)
                 // lazy rescale (R21): the reference max m moves only when the row max
                 // exceeds it by > 8 (log2 units), so P <= 2^8 and nearly every tile skips the O
                 // round trip through TMEM (the exact-max rescale ran on most tiles: ~10 % of the
-                // kernel).  The row sum adds the bf16-rounded P the PV MMA consumes, so a
-                // dominant key's rounding cancels in O / l.  O_t(j-1) is complete when it is
-                // rescaled: S_t(j) was issued after PV_t(j-1) and its commit tracks both.
+                // kernel).  O_t(j-1) is complete when it is rescaled: S_t(j) was issued after
+                // PV_t(j-1) and its commit tracks both.
                 const bool move = j == 0 || mtrue > m + 8.f;
                 if (j > 0 && __any_sync(0xffffffffu, move)) {
                     const float alpha = move ? fast_exp2(m - mtrue) : 1.f;
@@ -487,10 +565,12 @@ __global__ void __launch_bounds__(NT, 1)
                     l2 = fmul2(l2, a2);
                 }
                 if (move) m = mtrue;
-                // P = exp2(s * scale - m) (bf16) over the S columns [0, 64); the row sum runs
-                // in two FADD2 chains over the rounded P
+                [[maybe_unused]] const long long ts3 = TL_NOW();
+                // P = exp2(s * scale - m) (bf16) over the S columns [0, 64); the row sum adds
+                // the bf16-rounded P the PV MMA consumes (R21) with mixed-precision FHADD.BF16
+                // (one instruction per element, half-register operand), in four chains
                 const uint64_t nm2 = f2(-m, -m);
-                uint64_t l2b = f2(0.f, 0.f);
+                float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < 4; c += 2) {
                     uint32_t pk[32];
@@ -498,24 +578,36 @@ __global__ void __launch_bounds__(NT, 1)
                     for (int h = 0; h < 2; ++h)
 #pragma unroll
                         for (int e = 0; e < 32; e += 2) {
-                            float x0, x1;
-                            f2_split(ffma2(f2(__uint_as_float(sr[c + h][e]),
-                                              __uint_as_float(sr[c + h][e + 1])),
-                                           sc2, nm2),
-                                     x0, x1);
-                            const uint32_t pp = pack_bf16(fast_exp2(x0), fast_exp2(x1));
-                            const uint64_t pr = f2(__uint_as_float(pp << 16), __uint_as_float(pp & 0xFFFF0000u));
-                            if (h) l2b = fadd2(l2b, pr);
-                            else l2 = fadd2(l2, pr);
+                            const uint64_t x2 = ffma2(f2(__uint_as_float(sr[c + h][e]),
+                                                         __uint_as_float(sr[c + h][e + 1])),
+                                                      sc2, nm2);
+                            float p0, p1;
+                            if ((kPolyMask >> (e >> 1)) & 1u) {
+                                f2_split(exp2_poly3(x2), p0, p1);
+                            } else {
+                                float x0, x1;
+                                f2_split(x2, x0, x1);
+                                p0 = fast_exp2(x0);
+                                p1 = fast_exp2(x1);
+                            }
+                            const uint32_t pp = pack_bf16(p0, p1);
                             pk[h * 16 + e / 2] = pp;
+                            add_bf16x2_f32(ls[2 * h], ls[2 * h + 1], pp);
                         }
                     tmem_st32(s_tmem + (uint32_t)(c * 16), pk);
+                    // release this half of P to the PV MMA (keys [32c, 32c + 64))
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(&sm.p_full[t][c >> 1]);
                 }
-                l2 = fadd2(l2, l2b);
-                tmem_wait_st();
-                tc_fence_before();
-                mbar_arrive(&sm.p_full[t]);
-                if (lane == 0 && q4 == 0) TL_REC(t, tl_tile, ts0, ts1, TL_NOW());
+                l2 = fadd2(l2, f2(ls[0] + ls[2], ls[1] + ls[3]));
+                [[maybe_unused]] const long long ts4 = TL_NOW();
+                if (lane == 0 && q4 == 0) {
+                    TL_REC(t, tl_tile, ts0, ts1, TL_NOW());
+                    TL_EXTRA(t, tl_tile, 5, ts2);
+                    TL_EXTRA(t, tl_tile, 6, ts3);
+                    TL_EXTRA(t, tl_tile, 7, ts4);
+                }
                 ++tl_tile;
             }
             // ---- epilogue: O / l -> bf16 -> global
@@ -597,6 +689,16 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
     tc_fence_after();
     if (warp == 1) tmem_dealloc(tmem, 512);
+#ifdef SPD_TIMELINE
+    // every CTA: [40, cta, globaltimer start, end, kv-tile pair steps run, smid]
+    if (p.tl && warp == 1 && lane == 0 && blockIdx.x < 1024) {
+        unsigned long long gt_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_end));
+        long long* r = p.tl + 8 * (40 * 1024 + blockIdx.x);
+        r[0] = 40; r[1] = blockIdx.x; r[2] = (long long)gt_start; r[3] = (long long)gt_end;
+        r[4] = tl_units; r[5] = smid();
+    }
+#endif
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned done = atomicAdd(p.sched + 1, 1u);
@@ -702,16 +804,20 @@ extern "C" semipd_status semipd_prefill_attn(
                                  strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
             return SEMIPD_ERR_CUDA;
     }
-    // chunk K / V straight from k_new / v_new: (dk, Hkv, T), box 64 cols x 1 head x 128 rows
+    // chunk K / V straight from k_new / v_new as (64 cols, Hkv, T, 2 halves): one 32 KiB box
+    // (64, 1, 128 rows, 2) per kv tile lands as [half][128 rows][128 B] (the TMA unit's cost is
+    // per box, so one box per tile instead of one per 64-column half)
     CUtensorMap kcmap, vcmap;
-    const uint64_t kvrow = (uint64_t)c.num_kv_heads * HD * 2;
-    if (!spd_encode_tiled_3d(&kcmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(k_new), HD,
-                             (uint64_t)c.num_kv_heads, (uint64_t)total_q, HD * 2, kvrow, 64, 1, BN,
-                             CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !spd_encode_tiled_3d(&vcmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(v_new), HD,
-                             (uint64_t)c.num_kv_heads, (uint64_t)total_q, HD * 2, kvrow, 64, 1, BN,
-                             CU_TENSOR_MAP_SWIZZLE_128B))
-        return SEMIPD_ERR_CUDA;
+    {
+        const uint64_t dims[4] = {64, (uint64_t)c.num_kv_heads, (uint64_t)total_q, 2};
+        const uint64_t strides[3] = {HD * 2, (uint64_t)c.num_kv_heads * HD * 2, 128};
+        const uint32_t box[4] = {64, 1, BN, 2};
+        if (!spd_encode_tiled_4d(&kcmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(k_new),
+                                 dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !spd_encode_tiled_4d(&vcmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(v_new),
+                                 dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+            return SEMIPD_ERR_CUDA;
+    }
     // output map for the epilogue's TMA stores: token-major [T][Hq][128] box (64, G, TQ) or
     // head-major [Hq][T][128] box (64, TQ, G)
     CUtensorMap omap;

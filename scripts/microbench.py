@@ -24,6 +24,24 @@ sys.path.insert(0, ROOT)
 from paper_2504_19867_b200 import KVPool, PoolConfig  # noqa: E402
 
 
+def timed_ms(run, iters, L, reps=5):
+    """Median over `reps` of the mean time per launch of `iters` back-to-back launches
+    (rotating over L layers).  Launches are queued without a host sync between them, so the
+    host's per-call work (ctypes marshalling, tensor-map encodes) overlaps the previous kernel
+    instead of sitting between two events; a synchronised per-call loop over-counts short
+    kernels by that host time (~15 us)."""
+    out = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for it in range(iters):
+            run(it % L)
+        e1.record()
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1) / iters)
+    return statistics.median(out), min(out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kernel", default="decode", choices=["decode", "prefill", "both"])
@@ -93,16 +111,8 @@ def main():
             for l in range(min(L, 3)):
                 run(l)
             torch.cuda.synchronize()
-            times = []
-            for it in range(args.iters):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                run(it % L)
-                e1.record()
-                torch.cuda.synchronize()
-                times.append(e0.elapsed_time(e1))
-            ms = statistics.median(times)
-            rec = {"kernel": kern, "budget": bud, "ms": ms, "min_ms": min(times)}
+            ms, ms_min = timed_ms(run, args.iters, L)
+            rec = {"kernel": kern, "budget": bud, "ms": ms, "min_ms": ms_min}
             if kern == "decode":
                 rec["GB_s"] = dec_bytes / (ms / 1e3) / 1e9
             else:
@@ -134,16 +144,8 @@ def mla(args, dev):
         for l in range(min(L, 3)):
             pool.decode_attn(l, q, kn, None, rid, ctxs, ctx, 1 / math.sqrt(192), out, ws, sm_budget=bud)
         torch.cuda.synchronize()
-        times = []
-        for it in range(args.iters):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            pool.decode_attn(it % L, q, kn, None, rid, ctxs, ctx, 1 / math.sqrt(192), out, ws,
-                             sm_budget=bud)
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-        ms = statistics.median(times)
+        ms, _ = timed_ms(lambda l: pool.decode_attn(l, q, kn, None, rid, ctxs, ctx, 1 / math.sqrt(192),
+                                                    out, ws, sm_budget=bud), args.iters, L)
         print(json.dumps({"kernel": "decode_mla", "budget": bud, "B": B, "ctx": ctx, "ms": ms,
                           "GB_s": byts / (ms / 1e3) / 1e9, "TFLOP_s": flops / (ms / 1e3) / 1e12}),
               flush=True)
@@ -171,15 +173,7 @@ def mla_prefill(args, dev):
         for l in range(min(L, 2)):
             run(l)
         torch.cuda.synchronize()
-        times = []
-        for it in range(args.iters):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            run(it % L)
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-        ms = statistics.median(times)
+        ms, _ = timed_ms(run, args.iters, L)
         print(json.dumps({"kernel": "prefill_mla", "budget": bud, "C": C, "P": P, "ms": ms,
                           "TFLOP_s": flops / (ms / 1e3) / 1e12}), flush=True)
 

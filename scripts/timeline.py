@@ -28,20 +28,37 @@ i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)
 pool.alloc_blocks(i32([0]), i32([32]))
 q = torch.randn(C, Hq, d, device=dev).bfloat16(); k = torch.randn(C, Hkv, d, device=dev).bfloat16()
 v = torch.randn(C, Hkv, d, device=dev).bfloat16(); out = torch.empty_like(q)
-buf = torch.zeros(32 * 1024 * 8, dtype=torch.int64, device=dev); ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+buf = torch.zeros(48 * 1024 * 8, dtype=torch.int64, device=dev); ctr = torch.zeros(1, dtype=torch.int32, device=dev)
 for it in range(3):
     ctr.zero_()
     buf.zero_()
     L.semipd_debug_set_timeline(pool.h, ctypes.c_void_p(buf.data_ptr()), ctypes.c_void_p(ctr.data_ptr()))
     pool.prefill_attn(0, q, k, v, i32([0, C]), i32([0]), i32([0]), C, C, 1 / math.sqrt(d), out, sm_budget=budget)
     torch.cuda.synchronize()
-rec = [r for r in buf.view(-1, 8).cpu().tolist() if r[2] != 0]
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ev[0].record()
+pool.prefill_attn(0, q, k, v, i32([0, C]), i32([0]), i32([0]), C, C, 1 / math.sqrt(d), out, sm_budget=budget)
+ev[1].record()
+torch.cuda.synchronize()
+print("kernel_us", ev[0].elapsed_time(ev[1]) * 1e3)
+allr = buf.view(-1, 8).cpu().tolist()
+cta = [r for r in allr if r[0] == 40]
+if cta:
+    g0 = min(r[2] for r in cta)
+    ends = sorted(((r[3] - g0) / 1e3, (r[2] - g0) / 1e3, r[4], r[1]) for r in cta)
+    print("cta_end_us min/med/max", ends[0][0], ends[len(ends) // 2][0], ends[-1][0],
+          "start_us max", max(e[1] for e in ends))
+    print("slowest CTAs (end_us, start_us, pair_steps, cta):", ends[-6:])
+    print("pair steps per CTA: max", max(e[2] for e in ends), "min", min(e[2] for e in ends))
+    json.dump(ends, open(os.path.join(ROOT, "gpurun_out", "tl_cta_%d.json" % budget), "w"))
+rec = [r for r in allr if r[2] != 0 and r[0] != 40]
 n = len(rec)
 t0 = min(r[2] for r in rec)
 for r in rec:
     r[2:4] = [x - t0 if x else 0 for x in r[2:4]]
     if r[0] < 20:
         r[4] = r[4] - t0 if r[4] else 0
+        r[5:8] = [x - t0 if x else 0 for x in r[5:8]]
 rec.sort(key=lambda r: r[2])
 json.dump(rec, open(os.path.join(ROOT, "gpurun_out", os.environ.get("TL_OUT", "timeline.json")), "w"))
 print("records", n)

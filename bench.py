@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--impl", default="semipd", choices=["semipd", "reference"])
     ap.add_argument("--model", default="llama3-8b", choices=list(MODELS))
     ap.add_argument("--split", type=float, default=None, help="prefill SM percent x (y = 100-x)")
-    ap.add_argument("--sweep", default="30,35,40,45,50,60")
+    ap.add_argument("--sweep", default="25,30,35,40,45,50,60")
     ap.add_argument("--block-size", type=int, default=64,
                     help="KV page size in tokens (64: one 16 KiB TMA box per (block, head) "
                          "page on B200; 16 is supported but TMA-per-box bound)")
@@ -239,6 +239,15 @@ class Workload:
         kv = self.B * (self.ctx + 1) * s.num_kv_heads * (s.head_dim_k + s.head_dim_v) * eb
         io = self.B * s.num_q_heads * (s.head_dim_k + s.head_dim_v) * eb  # q in, o out
         return float(kv + io)
+
+    def prefill_bytes_per_launch(self) -> float:
+        # HBM bytes the prefill launch must move at P = 0: q in, o out, k_new / v_new in and
+        # their copy into the pool pages (a3, fused)
+        s = self.shape
+        eb = 2
+        qo = self.C * s.num_q_heads * (s.head_dim_k + s.head_dim_v) * eb
+        kv = self.C * s.num_kv_heads * (s.head_dim_k + s.head_dim_v) * eb
+        return float(qo + 2 * kv)
 
     def prefill_flops_per_launch(self) -> float:
         s = self.shape
@@ -587,6 +596,14 @@ def main():
                 "traffic_unit": "DRAM bytes per launch (ncu)",
                 "algorithmic_flops_per_launch": w.prefill_flops_per_launch(),
                 "avg_launch_ms": pre_ms, "sm_budget": n_p}
+    # whole co-run step against HBM: both phases' algorithmic bytes per step / step time.
+    # Decode streams the KV cache and the prefill moves q / o / chunk K/V, all through the one
+    # shared HBM, so this bounds the step however the SMs are split
+    step_bytes = w.L * (w.decode_bytes_per_launch() + w.prefill_bytes_per_launch())
+    step_gbs = step_bytes / (t / args.steps) / 1e9
+    roof_step = {"bound": "hbm", "achieved": step_gbs, "peak": hbm_peak, "unit": "GB/s",
+                 "frac": step_gbs / hbm_peak, "peak_kind": peak_kind,
+                 "algorithmic_bytes_per_step": step_bytes}
     extra = {}
     if args.extra:
         def graphed(fn):  # the baselines get the same CUDA-graph replay as the co-run step
@@ -636,7 +653,7 @@ def main():
             "config": {**workload_config(shape, ws),
                        "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d}},
             "roofline": roof_dec if dominant == "decode" else roof_pre,
-            "roofline_decode": roof_dec, "roofline_prefill": roof_pre,
+            "roofline_decode": roof_dec, "roofline_prefill": roof_pre, "roofline_step": roof_step,
             "corun_streams": corun_overlap,
             "decode_tokens_per_s": DECODE_BATCH * args.steps / t,
             "prefill_tokens_per_s": PREFILL_TOKENS * args.steps / t,

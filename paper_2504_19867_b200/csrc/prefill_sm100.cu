@@ -45,6 +45,15 @@ constexpr uint32_t TILE_BYTES = BM * HD * 2;    // 32 KiB
 constexpr uint32_t HALF_BYTES = TILE_BYTES / 2; // 16 KiB (64 columns)
 constexpr float LOG2E = 1.4426950408889634f;
 
+// The PV MMA of a tile runs in kPvParts K-slices, each released by the softmax as soon as
+// its P columns are in TMEM (the first slices overlap the softmax's remaining exps)
+#ifndef SPD_PV_PARTS
+#define SPD_PV_PARTS 4
+#endif
+constexpr int kPvParts = SPD_PV_PARTS;
+static_assert(kPvParts == 1 || kPvParts == 2 || kPvParts == 4, "PV parts");
+
+
 struct PUnit {
     // i < 0: no more work.  t0: first chunk row of tile A (tile B starts at t0 + TQ);
     // tv[t]: valid rows (tokens) of tile t; P: cached prefix; np: prefix kv tiles;
@@ -101,7 +110,7 @@ struct Smem {
     unsigned char ostage[2][HALF_BYTES];  // per q tile: epilogue staging for TMA stores (64 cols)
     uint64_t q_full, q_empty, q_issued;  // q_issued: V loads of a unit queue behind its Q
     uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-    uint64_t s_full[2], p_full[2][2];  // per q tile; p_full[t][h]: P keys [64h, 64h + 64) in TMEM
+    uint64_t s_full[2], p_full[2][kPvParts];  // per q tile; p_full[t][h]: P part h in TMEM
     uint64_t o_full[2], o_empty[2];  // per q tile
     uint64_t ufull[2], uempty[2];
     PUnit units[2];
@@ -114,7 +123,7 @@ struct Smem {
 // fraction of the exps to a degree-3 polynomial on the FMA pipe shortens the softmax that sits
 // on the per-tile critical path (softmax -> PV -> next S).
 #ifndef SPD_POLY_MASK
-#define SPD_POLY_MASK 0x0000u
+#define SPD_POLY_MASK 0x1111u
 #endif
 constexpr uint32_t kPolyMask = SPD_POLY_MASK;
 
@@ -149,6 +158,12 @@ __device__ __forceinline__ void add_bf16x2_f32(float& a, float& b, uint32_t pp) 
         : "+f"(a), "+f"(b)
         : "r"(pp));
 }
+
+// Epilogue of full tiles: 1 = coalesced st.global from a swizzled smem staging, 0 = TMA store
+#ifndef SPD_EPI_DIRECT
+#define SPD_EPI_DIRECT 0
+#endif
+constexpr bool kEpiDirect = SPD_EPI_DIRECT != 0;
 
 // MMA issue from the whole converged warp (elect.sync inside the asm: descriptors stay in
 // uniform registers, ~2x the issue rate of a lane-0 branch) or from lane 0
@@ -192,8 +207,7 @@ __global__ void __launch_bounds__(NT, 1)
             mbar_init(&sm.v_full[s], 1);
             mbar_init(&sm.v_empty[s], 1);
             mbar_init(&sm.s_full[s], 1);
-            mbar_init(&sm.p_full[s][0], 128);
-            mbar_init(&sm.p_full[s][1], 128);
+            for (int h = 0; h < kPvParts; ++h) mbar_init(&sm.p_full[s][h], 128);
             mbar_init(&sm.o_full[s], 1);
             mbar_init(&sm.o_empty[s], 128);
             mbar_init(&sm.ufull[s], 1);
@@ -373,11 +387,11 @@ __global__ void __launch_bounds__(NT, 1)
                     const uint32_t p_tmem = tmem + (uint32_t)(t * BN);
                     const uint32_t o_tmem = tmem + 256u + (uint32_t)(t * HD);
 #pragma unroll
-                    for (int hf = 0; hf < 2; ++hf) {
+                    for (int hf = 0; hf < kPvParts; ++hf) {
                         mbar_wait(&sm.p_full[t][hf], cnt & 1);
                         tc_fence_after();
 #pragma unroll
-                        for (int kk = hf * 4; kk < hf * 4 + 4; ++kk) {
+                        for (int kk = hf * 8 / kPvParts; kk < (hf + 1) * 8 / kPvParts; ++kk) {
                             const uint64_t bdesc = umma_desc_sw128(v_addr + kk * 2048, HALF_BYTES, 1024);
                             MMA_TS(o_tmem, p_tmem + (uint32_t)(kk * 8), bdesc, idesc_o,
                                     (first && kk == 0) ? 0u : 1u);
@@ -572,33 +586,32 @@ __global__ void __launch_bounds__(NT, 1)
                 const uint64_t nm2 = f2(-m, -m);
                 float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int c = 0; c < 4; c += 2) {
-                    uint32_t pk[32];
+                for (int c = 0; c < 4; ++c) {  // 32 S columns -> 16 packed P columns
+                    uint32_t pk[16];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int e = 0; e < 32; e += 2) {
-                            const uint64_t x2 = ffma2(f2(__uint_as_float(sr[c + h][e]),
-                                                         __uint_as_float(sr[c + h][e + 1])),
-                                                      sc2, nm2);
-                            float p0, p1;
-                            if ((kPolyMask >> (e >> 1)) & 1u) {
-                                f2_split(exp2_poly3(x2), p0, p1);
-                            } else {
-                                float x0, x1;
-                                f2_split(x2, x0, x1);
-                                p0 = fast_exp2(x0);
-                                p1 = fast_exp2(x1);
-                            }
-                            const uint32_t pp = pack_bf16(p0, p1);
-                            pk[h * 16 + e / 2] = pp;
-                            add_bf16x2_f32(ls[2 * h], ls[2 * h + 1], pp);
+                    for (int e = 0; e < 32; e += 2) {
+                        const uint64_t x2 = ffma2(f2(__uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1])),
+                                                  sc2, nm2);
+                        float p0, p1;
+                        if ((kPolyMask >> (e >> 1)) & 1u) {
+                            f2_split(exp2_poly3(x2), p0, p1);
+                        } else {
+                            float x0, x1;
+                            f2_split(x2, x0, x1);
+                            p0 = fast_exp2(x0);
+                            p1 = fast_exp2(x1);
                         }
-                    tmem_st32(s_tmem + (uint32_t)(c * 16), pk);
-                    // release this half of P to the PV MMA (keys [32c, 32c + 64))
-                    tmem_wait_st();
-                    tc_fence_before();
-                    mbar_arrive(&sm.p_full[t][c >> 1]);
+                        const uint32_t pp = pack_bf16(p0, p1);
+                        pk[e / 2] = pp;
+                        add_bf16x2_f32(ls[2 * (c & 1)], ls[2 * (c & 1) + 1], pp);
+                    }
+                    tmem_st16(s_tmem + (uint32_t)(c * 16), pk);
+                    if ((c + 1) % (4 / kPvParts) == 0) {
+                        // release this part of P to the PV MMA
+                        tmem_wait_st();
+                        tc_fence_before();
+                        mbar_arrive(&sm.p_full[t][(c + 1) / (4 / kPvParts) - 1]);
+                    }
                 }
                 l2 = fadd2(l2, f2(ls[0] + ls[2], ls[1] + ls[3]));
                 [[maybe_unused]] const long long ts4 = TL_NOW();
@@ -621,7 +634,47 @@ __global__ void __launch_bounds__(NT, 1)
             const bool valid = tok < d.tv[t];
             const int hq = d.g * p.G + (r % p.G);
             const int trow = d.qrow0 + t * p.TQ + tok;
-            if (d.tv[t] == p.TQ) {
+            bool o_released = false;
+            if (kEpiDirect && d.tv[t] == p.TQ) {
+                // full tile: O -> registers (O's TMEM is released to the next unit's PV at
+                // once), then per 64-column half: rows -> swizzled smem staging -> coalesced
+                // 16-byte global stores, 8 threads per 128-byte row segment (no TMA store: its
+                // smem read queued behind the next unit's Q / K / V loads in the TMA unit)
+                uint32_t o[4][32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32(o_tmem + c * 32, o[c]);
+                tmem_wait_ld();
+                tc_fence_before();
+                mbar_arrive(&sm.o_empty[t]);
+                o_released = true;
+                unsigned char* stg = sm.ostage[t];
+                unsigned char* outb = reinterpret_cast<unsigned char*>(p.out);
+                const int lgG = __ffs(p.G) - 1;  // G divides 128: a power of two
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    if (hh) named_bar_sync(2 + t, 128);  // half 0 copied out of the staging
+#pragma unroll
+                    for (int c8 = 0; c8 < 8; ++c8) {
+                        const uint32_t* oo = &o[2 * hh + (c8 >> 2)][(c8 & 3) * 8];
+                        uint4 v;
+                        v.x = pack_bf16(__uint_as_float(oo[0]) * inv, __uint_as_float(oo[1]) * inv);
+                        v.y = pack_bf16(__uint_as_float(oo[2]) * inv, __uint_as_float(oo[3]) * inv);
+                        v.z = pack_bf16(__uint_as_float(oo[4]) * inv, __uint_as_float(oo[5]) * inv);
+                        v.w = pack_bf16(__uint_as_float(oo[6]) * inv, __uint_as_float(oo[7]) * inv);
+                        *reinterpret_cast<uint4*>(stg + r * 128 + ((c8 ^ (r & 7)) << 4)) = v;
+                    }
+                    named_bar_sync(2 + t, 128);
+#pragma unroll
+                    for (int it = 0; it < 8; ++it) {
+                        const int row = it * 16 + (r >> 3), c = r & 7;
+                        const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((c ^ (row & 7)) << 4));
+                        const int rt = d.qrow0 + t * p.TQ + (row >> lgG);
+                        const int rh = d.g * p.G + (row & (p.G - 1));
+                        const size_t rowoff = p.out_head_major ? (size_t)rh * p.T + rt : (size_t)rt * p.Hq + rh;
+                        *reinterpret_cast<uint4*>(outb + rowoff * (HD * 2) + hh * 128 + c * 16) = v;
+                    }
+                }
+            } else if (d.tv[t] == p.TQ) {
                 // full tile: rows -> swizzled smem staging -> one TMA store per 64-column half
                 // (per-thread 16-byte stores to 256-byte-strided rows were ~4k cycles and held
                 // up the next unit's Q load in the SM's memory path)
@@ -678,8 +731,10 @@ __global__ void __launch_bounds__(NT, 1)
                     }
                 }
             }
-            tc_fence_before();
-            mbar_arrive(&sm.o_empty[t]);
+            if (!o_released) {
+                tc_fence_before();
+                mbar_arrive(&sm.o_empty[t]);
+            }
             if (lane == 0 && q4 == 0) TL_REC(10 + t, nunit, te0, te1, TL_NOW());
             ++nunit;
         }

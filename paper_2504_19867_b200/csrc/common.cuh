@@ -84,6 +84,36 @@ SPD_DEV void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int x, 
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w)
         : "memory");
 }
+// L2 eviction-priority policies for TMA loads (createpolicy): the decode KV stream is read
+// once per step and should not push out the prefill's reused chunk K/V tiles in the co-run
+SPD_DEV uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+SPD_DEV uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+SPD_DEV uint64_t l2_policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// 0 = evict_normal, 1 = evict_first, 2 = evict_last
+SPD_DEV uint64_t l2_policy(int kind) {
+    return kind == 1 ? l2_policy_evict_first() : kind == 2 ? l2_policy_evict_last() : l2_policy_evict_normal();
+}
+SPD_DEV void tma_load_4d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y, int z,
+                              int w, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w),
+        "l"(policy)
+        : "memory");
+}
 // smem -> global tensor store (bulk async group), and the group completion waits
 SPD_DEV void tma_store_3d(const CUtensorMap* m, const void* src, int x, int y, int z) {
     asm volatile(

@@ -24,6 +24,13 @@
 
 namespace {
 
+// L2 policy of the KV page stream: evict_first keeps the co-running prefill's
+// reused chunk K/V tiles resident in L2 while decode streams the cache through it
+#ifndef SPD_DEC_L2
+#define SPD_DEC_L2 1
+#endif
+constexpr int kDecL2 = SPD_DEC_L2;
+
 using namespace spd;
 
 constexpr int HD = 128;           // head dim (dk == dv)
@@ -116,6 +123,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
 
     const int warp = (int)warp_id();
     const int lane = (int)lane_id();
+    const uint64_t kv_pol = l2_policy(kDecL2);  // KV stream: read once per step
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
             mbar_init(full + i, 1);
@@ -350,8 +358,8 @@ __global__ void __launch_bounds__(4 * 32, 1)
                         if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
                         else if (blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
                         const int y = (d.k0 + i * KPS + b * R) & bs_mask;
-                        tma_load_4d(kst + b * (R * 256), &kmap, full + st, 0, y, 0, z);
-                        tma_load_4d(kst + KV_BYTES + b * (R * 256), &vmap, full + st, 0, y, 0, z);
+                        tma_load_4d_hint(kst + b * (R * 256), &kmap, full + st, 0, y, 0, z, kv_pol);
+                        tma_load_4d_hint(kst + KV_BYTES + b * (R * 256), &vmap, full + st, 0, y, 0, z, kv_pol);
                     }
                 }
                 if (lane == 0) TL_REC(1, gstage, tp0, tp1, TL_NOW());
@@ -722,6 +730,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
 
     const int warp = (int)warp_id();
     const int lane = (int)lane_id();
+    const uint64_t kv_pol = l2_policy(kDecL2);  // KV stream: read once per step
     const int NP = MODE == 0 ? p.Hkv >> 1 : p.Hkv;  // head groups per request
     if (threadIdx.x == 0) {
         for (int i = 0; i < P_NSTAGE; ++i) {
@@ -836,8 +845,8 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                     if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
                     else if (blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
                     const int y = (d.k0 + i * KPS_M) & bs_mask;
-                    tma_load_4d(kst, &kmap2, full + st, 0, y, 0, z);
-                    tma_load_4d(kst + 2 * KV_BYTES, &vmap2, full + st, 0, y, 0, z);
+                    tma_load_4d_hint(kst, &kmap2, full + st, 0, y, 0, z, kv_pol);
+                    tma_load_4d_hint(kst + 2 * KV_BYTES, &vmap2, full + st, 0, y, 0, z, kv_pol);
                 }
                 __syncwarp();
             }

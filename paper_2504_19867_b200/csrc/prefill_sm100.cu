@@ -159,6 +159,20 @@ __device__ __forceinline__ void add_bf16x2_f32(float& a, float& b, uint32_t pp) 
         : "r"(pp));
 }
 
+// independent FMNMX3 chains of the row max (latency-bound: 64 three-input maxes per row)
+#ifndef SPD_MAX_CHAINS
+#define SPD_MAX_CHAINS 4
+#endif
+constexpr int kMaxChains = SPD_MAX_CHAINS;
+
+// L2 policy of the chunk K/V tile loads (each is re-read by all later q-tile pairs of its
+// request and kv head); 0 = evict_normal (evict_last measured no better in the co-run: the
+// decode stream is already evict_first)
+#ifndef SPD_PRE_L2
+#define SPD_PRE_L2 0
+#endif
+constexpr int kPreL2 = SPD_PRE_L2;
+
 // Epilogue of full tiles: 1 = coalesced st.global from a swizzled smem staging, 0 = TMA store
 #ifndef SPD_EPI_DIRECT
 #define SPD_EPI_DIRECT 0
@@ -196,6 +210,7 @@ __global__ void __launch_bounds__(NT, 1)
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = (int)warp_id();
     const int lane = (int)lane_id();
+    const uint64_t kv_pol = l2_policy(kPreL2);  // chunk K/V: re-read by every later q pair
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.q_full, 1);
@@ -342,7 +357,7 @@ __global__ void __launch_bounds__(NT, 1)
                     }
                 } else if (lane == 0) {
                     // one 32 KiB box (64 cols, 1 head, 128 rows, 2 halves) -> [half][rows][128 B]
-                    tma_load_4d(dst, cmap, ful, 0, d.g, d.crow0 + (j - d.np) * BN, 0);
+                    tma_load_4d_hint(dst, cmap, ful, 0, d.g, d.crow0 + (j - d.np) * BN, 0, kv_pol);
                 }
                 __syncwarp();
             }
@@ -540,17 +555,23 @@ __global__ void __launch_bounds__(NT, 1)
                         for (int e = 0; e < 32; ++e)
                             if (c * 32 + e > lim) sr[c][e] = __float_as_uint(-INFINITY);
                 }
-                // row max: four independent FMNMX3 chains (one per 32-column block) instead of
+                // row max: kMaxChains independent FMNMX3 chains over the 128 columns instead of
                 // one 64-deep dependent chain on the softmax critical path
-                float mxc[4];
+                float mxc[kMaxChains];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    mxc[c] = -INFINITY;
+                for (int k = 0; k < kMaxChains; ++k) mxc[k] = -INFINITY;
 #pragma unroll
-                    for (int e = 0; e < 32; e += 2)
-                        mxc[c] = fmax3(mxc[c], __uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1]));
-                }
-                const float mx = fmaxf(fmaxf(mxc[0], mxc[1]), fmaxf(mxc[2], mxc[3]));
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        const int k = (c * 16 + e / 2) % kMaxChains;
+                        mxc[k] = fmax3(mxc[k], __uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1]));
+                    }
+#pragma unroll
+                for (int w = kMaxChains / 2; w >= 1; w /= 2)
+#pragma unroll
+                    for (int k = 0; k < w; ++k) mxc[k] = fmaxf(mxc[k], mxc[k + w]);
+                const float mx = mxc[0];
                 const float mtrue = fmaxf(m, mx * p.scale_log2);  // scale > 0: max commutes
                 // lazy rescale (R21): the reference max m moves only when the row max
                 // exceeds it by > 8 (log2 units), so P <= 2^8 and nearly every tile skips the O

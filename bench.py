@@ -334,8 +334,15 @@ def time_steps(fn, steps, dev, barrier=None):
 
 # ----------------------------------------------------------------------------- e2e
 class E2E:
-    """Same step through the public API with pinned host inputs/outputs (copies
-    inside the timed region, on each phase's stream)."""
+    """Same step through the public API with pinned host inputs/outputs: every step copies
+    its inputs host -> device and its outputs device -> host inside the timed region.
+    The copies run on their own streams, per layer, so the PCIe transfers pipeline with
+    the attention kernels and H2D overlaps D2H (the copy engines are independent):
+      H2D stream: layer l's prefill q / k / v and decode q / k / v, then an event each;
+      stream P / D: wait for layer l's inputs, run the kernel, record an event;
+      D2H stream: wait for layer l's outputs, copy them out.
+    Device buffers are per layer and the step ends with the main stream joining all four
+    streams, so nothing is overwritten while still in use."""
 
     def __init__(self, w: Workload):
         self.w = w
@@ -351,33 +358,49 @@ class E2E:
         self.h2d = sum(t.numel() * t.element_size() for lst in
                        (self.h_qp, self.h_kp, self.h_vp, self.h_qd, self.h_kd, self.h_vd) for t in lst)
         self.d2h = sum(t.numel() * t.element_size() for lst in (self.h_op, self.h_od) for t in lst)
+        self.s_in = torch.cuda.Stream(w.dev)
+        self.s_out = torch.cuda.Stream(w.dev)
+        ev = lambda: [torch.cuda.Event() for _ in range(w.L)]  # noqa: E731
+        self.in_p, self.in_d, self.out_p, self.out_d = ev(), ev(), ev(), ev()
 
     def step(self, x, y):
         w = self.w
         main = torch.cuda.current_stream(w.dev)
         w.pool.set_partition(x, y)
-        w.sP.wait_stream(main)
-        w.sD.wait_stream(main)
-        with torch.cuda.stream(w.sP):
-            w.pool.alloc_blocks(w.rid_pre, w.nblk_pre, None, stream=w.sP)
-            for l in range(w.L):
-                w.qp[l].copy_(self.h_qp[l], non_blocking=True)
-                w.kp[l].copy_(self.h_kp[l], non_blocking=True)
-                w.vp[l].copy_(self.h_vp[l], non_blocking=True)
-                w.pool.prefill_attn(l, w.qp[l], w.kp[l], w.vp[l], w.cu, w.rid_pre, w.prefix, w.C,
-                                    w.C, w.scale, w.op[l], out_head_major=w.tp > 1, stream=w.sP)
-                self.h_op[l].copy_(w.op[l], non_blocking=True)
-            w.pool.free_blocks(w.rid_pre, None, stream=w.sP)
-        with torch.cuda.stream(w.sD):
+        for s in (self.s_in, self.s_out, w.sP, w.sD):
+            s.wait_stream(main)
+        with torch.cuda.stream(self.s_in):
             for l in range(w.L):
                 w.qd[l].copy_(self.h_qd[l], non_blocking=True)
                 w.kd[l].copy_(self.h_kd[l], non_blocking=True)
                 w.vd[l].copy_(self.h_vd[l], non_blocking=True)
+                self.in_d[l].record(self.s_in)
+                w.qp[l].copy_(self.h_qp[l], non_blocking=True)
+                w.kp[l].copy_(self.h_kp[l], non_blocking=True)
+                w.vp[l].copy_(self.h_vp[l], non_blocking=True)
+                self.in_p[l].record(self.s_in)
+        with torch.cuda.stream(w.sP):
+            w.pool.alloc_blocks(w.rid_pre, w.nblk_pre, None, stream=w.sP)
+            for l in range(w.L):
+                w.sP.wait_event(self.in_p[l])
+                w.pool.prefill_attn(l, w.qp[l], w.kp[l], w.vp[l], w.cu, w.rid_pre, w.prefix, w.C,
+                                    w.C, w.scale, w.op[l], out_head_major=w.tp > 1, stream=w.sP)
+                self.out_p[l].record(w.sP)
+            w.pool.free_blocks(w.rid_pre, None, stream=w.sP)
+        with torch.cuda.stream(w.sD):
+            for l in range(w.L):
+                w.sD.wait_event(self.in_d[l])
                 w.pool.decode_attn(l, w.qd[l], w.kd[l], w.vd[l], w.rid_dec, w.ctx_lens, w.ctx,
                                    w.scale, w.od[l], w.ws, out_head_major=w.tp > 1, stream=w.sD)
+                self.out_d[l].record(w.sD)
+        with torch.cuda.stream(self.s_out):
+            for l in range(w.L):
+                self.s_out.wait_event(self.out_d[l])
                 self.h_od[l].copy_(w.od[l], non_blocking=True)
-        main.wait_stream(w.sP)
-        main.wait_stream(w.sD)
+                self.s_out.wait_event(self.out_p[l])
+                self.h_op[l].copy_(w.op[l], non_blocking=True)
+        for s in (self.s_in, self.s_out, w.sP, w.sD):
+            main.wait_stream(s)
 
 
 # ----------------------------------------------------------------------------- oracle arm

@@ -627,19 +627,36 @@ def main():
     roof_step = {"bound": "hbm", "achieved": step_gbs, "peak": hbm_peak, "unit": "GB/s",
                  "frac": step_gbs / hbm_peak, "peak_kind": peak_kind,
                  "algorithmic_bytes_per_step": step_bytes}
+    def graphed(fn):  # the baselines get the same CUDA-graph replay as the co-run step
+        if not use_graph:
+            return fn
+        fn()
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize(dev)
+        return g.replay
+
+    # each phase alone on the whole GPU (148 SMs): the kernels' full-chip roofline fractions,
+    # next to the co-run ones above (32 launches + the phase's alloc / free, graph replay)
+    # (the stream is looked up at call time: under graph capture it is the capture stream)
+    nsm = w.pool.num_sms
+    t_pi = time_steps(graphed(lambda: w.phase_prefill(nsm, stream=torch.cuda.current_stream(dev))),
+                      3, dev, barrier) / 3
+    t_di = time_steps(graphed(lambda: w.phase_decode(nsm, stream=torch.cuda.current_stream(dev))),
+                      3, dev, barrier) / 3
+    pre_iso = w.prefill_flops_per_launch() * w.L / t_pi / 1e12
+    dec_iso = w.decode_bytes_per_launch() * w.L / t_di / 1e9
+    isolated = {"sm_budget": nsm,
+                "prefill": {"achieved": pre_iso, "unit": "TFLOP/s", "peak": bf16_sus,
+                            "frac": pre_iso / bf16_sus, "ms_per_launch": t_pi / w.L * 1e3},
+                "decode": {"achieved": dec_iso, "unit": "GB/s", "peak": hbm_peak,
+                           "frac": dec_iso / hbm_peak, "ms_per_launch": t_di / w.L * 1e3},
+                "note": "per phase, all SMs, 32-layer graph replay incl. the phase's alloc/free"}
     extra = {}
     if args.extra:
-        def graphed(fn):  # the baselines get the same CUDA-graph replay as the co-run step
-            if not use_graph:
-                return fn
-            fn()
-            torch.cuda.synchronize(dev)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                fn()
-            g.replay()
-            torch.cuda.synchronize(dev)
-            return g.replay
 
         ts = time_steps(graphed(w.serial_step), 3, dev, barrier) / 3
         tu = time_steps(graphed(w.uncontrolled_step), 3, dev, barrier) / 3
@@ -677,7 +694,7 @@ def main():
                        "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d}},
             "roofline": roof_dec if dominant == "decode" else roof_pre,
             "roofline_decode": roof_dec, "roofline_prefill": roof_pre, "roofline_step": roof_step,
-            "corun_streams": corun_overlap,
+            "corun_streams": corun_overlap, "isolated_full_chip": isolated,
             "decode_tokens_per_s": DECODE_BATCH * args.steps / t,
             "prefill_tokens_per_s": PREFILL_TOKENS * args.steps / t,
             "sweep": sweep, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,

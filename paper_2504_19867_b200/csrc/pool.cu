@@ -194,7 +194,12 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
     }
     // TMA descriptors: bf16 pools with 64-multiple head dims (the tensor-core paths)
     if (cfg->dtype == SEMIPD_BF16 && cfg->head_dim_k % 64 == 0 && cfg->head_dim_v % 64 == 0) {
-        p->box_rows = cfg->block_size < 32 ? cfg->block_size : 32;
+        // prefill prefix page boxes: min(bs, SPD_PREFIX_BOX_ROWS) rows x 64 columns (the TMA
+        // unit's cost is per box, so the largest box a page allows)
+#ifndef SPD_PREFIX_BOX_ROWS
+#define SPD_PREFIX_BOX_ROWS 128
+#endif
+        p->box_rows = cfg->block_size < SPD_PREFIX_BOX_ROWS ? cfg->block_size : SPD_PREFIX_BOX_ROWS;
         const uint64_t pages = (uint64_t)cfg->num_blocks * cfg->num_kv_heads;
         p->kmap.resize(cfg->num_layers);
         p->vmap.resize(cfg->num_layers);

@@ -1,0 +1,68 @@
+"""Host-side checks of bench.py's roofline numerators (no GPU): the algorithmic bytes / FLOPs
+per launch that `roofline*.achieved` divide by must equal the closed forms of SURVEY §8(a)/(d)
+for the cfg-2 workload:
+  decode  Σ_r (ctx_r + 1)·Hkv·(dk + dv)·eb + B·Hq·(dk + dv)·eb  = 538.2 MB  (§8(d) cfg 2 row: 538.5 MB
+          counts q / o in fp32 partial form; the bench counts the bf16 q in / o out it moves)
+  prefill 2·Hq·(dk + dv)·C(C + 1)/2                              = 34.38 GFLOP (P = 0)
+  bytes   q + o (C·Hq·(dk+dv)·eb) + k_new / v_new in and their pool copy (2·C·Hkv·(dk+dv)·eb)
+"""
+import dataclasses
+import importlib.util
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def _workload(mod, block_size=64):
+    import synth
+    w = mod.Workload.__new__(mod.Workload)  # the formulas only read shapes (no pool, no GPU)
+    w.shape = dataclasses.replace(synth.CFG2_LLAMA8B, block_size=block_size)
+    w.B, w.ctx, w.C = mod.DECODE_BATCH, mod.DECODE_CTX, mod.PREFILL_TOKENS
+    w.L = w.shape.num_layers
+    return w
+
+
+def test_decode_bytes_closed_form():
+    mod = _bench()
+    w = _workload(mod)
+    B, ctx, Hq, Hkv, d = 64, 2048, 32, 8, 128
+    assert (w.B, w.ctx) == (B, ctx)
+    kv = B * (ctx + 1) * Hkv * (d + d) * 2
+    io = B * Hq * (d + d) * 2
+    assert w.decode_bytes_per_launch() == kv + io
+    assert abs(w.decode_bytes_per_launch() / 1e6 - 538.2) < 0.1
+
+
+def test_prefill_flops_closed_form():
+    mod = _bench()
+    w = _workload(mod)
+    C, Hq, d = 2048, 32, 128
+    assert w.C == C
+    # brute-force count of unmasked causal pairs for a small chunk, then the closed form
+    assert sum(t + 1 for t in range(37)) == 37 * 38 // 2
+    flops = 2 * Hq * (d + d) * (C * (C + 1) / 2)
+    assert w.prefill_flops_per_launch() == flops
+    assert abs(flops / 1e9 - 34.38) < 0.01
+
+
+def test_prefill_bytes_and_step_bytes():
+    mod = _bench()
+    w = _workload(mod)
+    C, Hq, Hkv, d = 2048, 32, 8, 128
+    assert w.prefill_bytes_per_launch() == C * Hq * 2 * d * 2 + 2 * C * Hkv * 2 * d * 2
+    step = w.L * (w.decode_bytes_per_launch() + w.prefill_bytes_per_launch())
+    assert abs(step / 1e9 - 18.83) < 0.01  # the roofline_step numerator
+
+
+def test_bytes_independent_of_block_size():
+    mod = _bench()
+    assert _workload(mod, 16).decode_bytes_per_launch() == _workload(mod, 64).decode_bytes_per_launch()

@@ -64,7 +64,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every kernel from Python instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--extra", action="store_true", help="serial / (100,100) / isolated curves")
+    ap.add_argument("--extra", action="store_true", default=True,
+                    help="serial / (100,100) baselines (default on: the paper's spatial-vs-temporal claim)")
+    ap.add_argument("--no-extra", dest="extra", action="store_false")
     return ap.parse_args()
 
 

@@ -702,14 +702,17 @@ __global__ void __launch_bounds__(NT, 1)
                 const int srow = p.out_head_major ? (r % p.G) * p.TQ + tok : r;
                 unsigned char* stg = sm.ostage[t];
                 const bool issuer = q4 == 0 && lane == 0;
+                [[maybe_unused]] long long tea = 0, teb = 0;
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     if (issuer) bulk_wait_group_read0();  // previous store has read the staging
                     named_bar_sync(2 + t, 128);
+                    if (hh) teb = TL_NOW();
                     uint32_t o[2][32];
                     tmem_ld32(o_tmem + hh * 64, o[0]);
                     tmem_ld32(o_tmem + hh * 64 + 32, o[1]);
                     tmem_wait_ld();
+                    if (!hh) tea = TL_NOW();
 #pragma unroll
                     for (int c8 = 0; c8 < 8; ++c8) {
                         const uint32_t* oo = &o[c8 >> 2][(c8 & 3) * 8];
@@ -729,6 +732,11 @@ __global__ void __launch_bounds__(NT, 1)
                             tma_store_3d(&omap, stg, hh * 64, d.g * p.G, d.qrow0 + t * p.TQ);
                         bulk_commit_group();
                     }
+                }
+                if (lane == 0 && q4 == 0) {
+                    TL_EXTRA(10 + t, nunit, 5, tea);
+                    TL_EXTRA(10 + t, nunit, 6, teb);
+                    TL_EXTRA(10 + t, nunit, 7, TL_NOW());
                 }
             } else {
                 __nv_bfloat16* dst = p.out + (p.out_head_major

@@ -58,7 +58,7 @@ for r in rec:
     r[2:4] = [x - t0 if x else 0 for x in r[2:4]]
     if r[0] < 20:
         r[4] = r[4] - t0 if r[4] else 0
-        r[5:8] = [x - t0 if x else 0 for x in r[5:8]]
+        r[5:8] = [x - t0 if x > 0 else 0 for x in r[5:8]]
 rec.sort(key=lambda r: r[2])
 json.dump(rec, open(os.path.join(ROOT, "gpurun_out", os.environ.get("TL_OUT", "timeline.json")), "w"))
 print("records", n)

@@ -97,11 +97,24 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def _clock_sampler_proc(index: int, period: float, stop, out):
+def nvml_id(dev: torch.device):
+    """The NVML handle key of a CUDA device: its PCI bus id (CUDA and NVML indices differ
+    under CUDA_VISIBLE_DEVICES), else the CUDA index."""
+    try:
+        pr = torch.cuda.get_device_properties(dev)
+        return "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+    except Exception:
+        return dev.index or 0
+
+
+def _clock_sampler_proc(index, period: float, stop, out):
     """Child process: poll NVML SM clock + clock-event reasons until `stop` is set."""
     import pynvml
     pynvml.nvmlInit()
-    h = pynvml.nvmlDeviceGetHandleByIndex(index)
+    if isinstance(index, str):
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(index.encode())
+    else:
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
     rows = []
     out.put(("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)))
     while not stop.is_set():
@@ -121,7 +134,7 @@ class ClockSampler:
                "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
                "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-    def __init__(self, index: int, period_s: float = 0.005):
+    def __init__(self, index, period_s: float = 0.005):
         self.index, self.period, self.rows, self.max_mhz = index, period_s, [], None
         self.err = None
 
@@ -224,7 +237,8 @@ class Workload:
         self.gath_p = self.gath_d = None
         if tp > 1:
             from paper_2504_19867_b200 import tp as tpmod
-            groups = tpmod.PhaseGroups.create(backend="nccl")  # one communicator per phase
+            groups = tpmod.PhaseGroups.create(  # one communicator per phase
+                backend=os.environ.get("SPD_BENCH_BACKEND", "nccl"))
             self.pg_p, self.pg_d = groups.prefill, groups.decode
             self.gath_p = torch.empty((self.full.num_q_heads, self.C, d), dtype=s.dtype, device=dev)
             self.gath_d = torch.empty((self.full.num_q_heads, self.B, d), dtype=s.dtype, device=dev)
@@ -510,12 +524,19 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     ws, rank, local = dist_info()
-    dev = torch.device("cuda", local)
+    # dev-only overrides to exercise the N > 1 plumbing on a one-GPU box: every rank on
+    # cuda:0 and the gloo backend (NCCL refuses two ranks on one device). Never set by the driver.
+    one_gpu = os.environ.get("SPD_BENCH_ONE_GPU") == "1"
+    backend = os.environ.get("SPD_BENCH_BACKEND", "nccl")
+    dev = torch.device("cuda", 0 if one_gpu else local)
     torch.cuda.set_device(dev)
     barrier = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         barrier = lambda: dist.barrier()  # noqa: E731
     shape = dataclasses.replace(MODELS[args.model], block_size=args.block_size)
     w = Workload(shape, ws, dev)
@@ -571,7 +592,7 @@ def main():
         torch.cuda.synchronize(dev)
     # ---- timed region
     per_step = [0]
-    with ClockSampler(local) as clk:
+    with ClockSampler(nvml_id(dev)) as clk:
         # the last timed step runs eagerly with per-launch CUDA events (the roofline's kernel
         # times; an event pair between back-to-back kernels costs ~3 us, so only one step)
         k_step = [0]

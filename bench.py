@@ -60,6 +60,11 @@ def parse():
     ap.add_argument("--block-size", type=int, default=64,
                     help="KV page size in tokens (64: one 16 KiB TMA box per (block, head) "
                          "page on B200; 16 is supported but TMA-per-box bound)")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
+                    help="TP head all-gather: NCCL all_gather (CTAs) or copy-engine pushes over "
+                         "IPC-mapped peer memory with stream-memop flags (no SMs)")
+    ap.add_argument("--peer-graph", action="store_true",
+                    help="N > 1 with --gather peer: replay the co-run step as a CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every kernel from Python instead of replaying a CUDA graph")
@@ -183,7 +188,8 @@ def dist_info():
 class Workload:
     """Pool + resident inputs for one rank (head shard under TP)."""
 
-    def __init__(self, shape: synth.AttnShape, tp: int, dev: torch.device, seed: int = 1020):
+    def __init__(self, shape: synth.AttnShape, tp: int, dev: torch.device, seed: int = 1020,
+                 gather: str = "nccl"):
         from paper_2504_19867_b200 import KVPool, PoolConfig
         self.full = shape
         self.shape = synth.shard_heads(shape, tp) if tp > 1 else shape
@@ -234,6 +240,7 @@ class Workload:
         self.sP = torch.cuda.Stream(device=dev)
         self.sD = torch.cuda.Stream(device=dev)
         self.pg_p = self.pg_d = None
+        self.peer_p = self.peer_d = None
         self.gath_p = self.gath_d = None
         if tp > 1:
             from paper_2504_19867_b200 import tp as tpmod
@@ -242,6 +249,9 @@ class Workload:
             self.pg_p, self.pg_d = groups.prefill, groups.decode
             self.gath_p = torch.empty((self.full.num_q_heads, self.C, d), dtype=s.dtype, device=dev)
             self.gath_d = torch.empty((self.full.num_q_heads, self.B, d), dtype=s.dtype, device=dev)
+            if gather == "peer":  # copy engines + stream memops instead of NCCL CTAs
+                self.peer_p = tpmod.PeerGather(self.gath_p.shape, s.dtype, self.pg_p, dev)
+                self.peer_d = tpmod.PeerGather(self.gath_d.shape, s.dtype, self.pg_d, dev)
         # per-launch timing events (decode kernel on stream D, prefill call on stream P)
         self.ev_d = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                      for _ in range(self.L)]
@@ -285,7 +295,10 @@ class Workload:
                     self.ev_p[l][1].record(s)
                 if self.tp > 1:
                     from paper_2504_19867_b200 import tp as tpmod
-                    tpmod.gather_heads(self.op[l], self.gath_p, self.pg_p)
+                    if self.peer_p is not None:
+                        self.peer_p(self.op[l], stream=s)
+                    else:
+                        tpmod.gather_heads(self.op[l], self.gath_p, self.pg_p)
             p.free_blocks(self.rid_pre, None, stream=s)
 
     def phase_decode(self, budget, timed=False, stream=None):
@@ -302,7 +315,10 @@ class Workload:
                     self.ev_d[l][1].record(s)
                 if self.tp > 1:
                     from paper_2504_19867_b200 import tp as tpmod
-                    tpmod.gather_heads(self.od[l], self.gath_d, self.pg_d)
+                    if self.peer_d is not None:
+                        self.peer_d(self.od[l], stream=s)
+                    else:
+                        tpmod.gather_heads(self.od[l], self.gath_d, self.pg_d)
 
     def corun_step(self, x, y, timed=False):
         """One co-run iteration: both workers concurrently at budgets from (x, y)."""
@@ -476,13 +492,15 @@ def oracle_sample_rate(shape: synth.AttnShape, threads: int, budget_s: float = 1
     return tokens / t_step, sample, time.perf_counter()
 
 
-def workload_config(shape: synth.AttnShape, ws: int) -> dict:
+def workload_config(shape: synth.AttnShape, ws: int, gather: str = "nccl") -> dict:
     """The `config` both arms print (the reference arm runs the same workload)."""
     decode_gb = shape.num_layers * (DECODE_BATCH * (DECODE_CTX + 1) * shape.num_kv_heads * 2 * 128 * 2) / 1e9
     return {"workload": f"{shape.name} attention (Hq {shape.num_q_heads}, Hkv {shape.num_kv_heads}, "
                         f"d 128, bs {shape.block_size}, {shape.num_layers} layers): decode B={DECODE_BATCH} "
                         f"ctx={DECODE_CTX} + prefill chunk {PREFILL_TOKENS} (P=0), co-run",
-            "parallelism": f"tp{ws} (KV-head shards, NCCL all-gather)" if ws > 1 else "tp1",
+            "parallelism": (f"tp{ws} (KV-head shards, "
+                            + ("copy-engine peer all-gather)" if gather == "peer" else "NCCL all-gather)")
+                            if ws > 1 else "tp1"),
             "l2": f"no flush: per-step decode working set {decode_gb:.1f} GB >> 126 MB L2"}
 
 
@@ -539,7 +557,7 @@ def main():
             dist.init_process_group(backend)
         barrier = lambda: dist.barrier()  # noqa: E731
     shape = dataclasses.replace(MODELS[args.model], block_size=args.block_size)
-    w = Workload(shape, ws, dev)
+    w = Workload(shape, ws, dev, gather=args.gather)
     hbm_peak, bf16_peak, bf16_sus, peak_kind = peaks()
     W = max(3, args.warmup)
     splits = [float(x) for x in args.sweep.split(",")] if args.split is None else [args.split]
@@ -548,7 +566,10 @@ def main():
         w.corun_step(50, 50)
     sweep = []
 
-    use_graph = not args.no_graph and ws == 1
+    # N > 1 runs eagerly.  The peer gather is graph-safe (tests/test_gpu_peer_gather.py replays
+    # a captured gather), but with two ranks time-slicing one GPU the replayed step was 7x
+    # slower than eager (138 vs 19 ms), so graph replay for N > 1 stays opt-in (--peer-graph)
+    use_graph = not args.no_graph and (ws == 1 or (args.gather == "peer" and args.peer_graph))
 
     def capture(x):
         torch.cuda.synchronize(dev)
@@ -713,7 +734,7 @@ def main():
             "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": W,
             "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {**workload_config(shape, ws),
+            "config": {**workload_config(shape, ws, args.gather),
                        "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d}},
             "roofline": roof_dec if dominant == "decode" else roof_pre,
             "roofline_decode": roof_dec, "roofline_prefill": roof_pre, "roofline_step": roof_step,

@@ -215,6 +215,46 @@ int64_t semipd_launch_count(semipd_pool_t pool);
 semipd_status semipd_set_trace(semipd_pool_t pool, int32_t* buf, int32_t cap,
                                int32_t* counter_dev);
 
+/* ---- Head-output all-gather over peer memory (TP by KV head) ----
+ * P:232 §4.5: the prefill workers (and, separately, the decode workers) of a TP group
+ * exchange only among themselves.  With attention sharded by KV head the one exchange is
+ * the all-gather of head-major shards [Hq/TP, T, dv] into [Hq, T, dv] on every rank.
+ * These calls do it with the copy engines and GPU-front-end stream memory operations, so
+ * the gather occupies no SM of either partition (NCCL's all-gather runs CTAs).
+ *
+ * semipd_ipc_alloc: the ONE call that allocates device memory: `bytes` (> 0) of zeroed
+ *   cudaMalloc memory on the current device, exportable to other processes.  *dev_ptr
+ *   receives it, handle_out (host, SEMIPD_IPC_HANDLE_BYTES bytes) its IPC handle.  Owned by
+ *   the caller; release with semipd_ipc_free.  Errors: INVALID (NULL / 0), CUDA.
+ * semipd_ipc_open: map a peer's handle (host bytes) into this process (peer access enabled
+ *   lazily); *dev_ptr is the peer allocation's base.  Unmap with semipd_ipc_close.  A handle
+ *   cannot be opened in the process that created it (CUDA rule): CUDA.
+ * semipd_peer_gather: on stream s, for rank `rank` of `world` (1..SEMIPD_MAX_PEERS):
+ *   - entry handshake: set peer_flags[k][world + rank] for every k != rank, then wait for
+ *     my_flags[world + k] to be set by every k != rank and reset it (every peer has reached
+ *     this call in its stream order, so its reads of the previous gather are done);
+ *   - copy `bytes` from src (device, this rank's shard) to dsts[k] for every k (host array of
+ *     `world` device pointers: rank k's gathered buffer, already offset to this rank's shard;
+ *     dsts[rank] == src skips the local copy);
+ *   - set peer_flags[k][rank] (host array of `world` device pointers to each rank's flag
+ *     array as mapped in this process; the write is fenced after the copies);
+ *   - wait for my_flags[k] to be set by every k != rank and reset it (my_flags: this rank's
+ *     own 2*world uint32 flag array, zero-initialised, used by one stream at a time).
+ *   Flags only take the values 0 / 1 and every call issues the same operations, so the call
+ *   may be captured into a CUDA graph and replayed.  After the call's stream position the
+ *   gathered buffer holds every rank's shard.  All ranks must make the same sequence of
+ *   calls on a given flag array.  Errors: INVALID (bad rank / world / NULL), UNSUPPORTED (no
+ *   stream memory operations), CUDA. */
+#define SEMIPD_IPC_HANDLE_BYTES 64
+#define SEMIPD_MAX_PEERS 8
+semipd_status semipd_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out);
+semipd_status semipd_ipc_free(void* dev_ptr);
+semipd_status semipd_ipc_open(const void* handle, void** dev_ptr);
+semipd_status semipd_ipc_close(void* dev_ptr);
+semipd_status semipd_peer_gather(const void* src, size_t bytes, void* const* dsts,
+                                 uint32_t* const* peer_flags, uint32_t* my_flags, int32_t world,
+                                 int32_t rank, semipd_stream_t s);
+
 /* Library version string (host, static). */
 const char* semipd_version(void);
 

@@ -81,6 +81,11 @@ def lib():
                 "semipd_launch_count": (i64, [vp]),
                 "semipd_set_trace": (i32, [vp, vp, i32, vp]),
                 "semipd_version": (ctypes.c_char_p, []),
+                "semipd_ipc_alloc": (i32, [sz, P(vp), vp]),
+                "semipd_ipc_free": (i32, [vp]),
+                "semipd_ipc_open": (i32, [vp, P(vp)]),
+                "semipd_ipc_close": (i32, [vp]),
+                "semipd_peer_gather": (i32, [vp, sz, P(vp), P(vp), vp, i32, i32, vp]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)

@@ -1,0 +1,159 @@
+// peer.cu — head-output all-gather over peer memory with no SMs (§8(e)).
+//
+// TP by KV head (§4.5: the prefill workers form one group, the decode workers another)
+// leaves one exchange step: every rank's head-major shard [Hq/TP, T, dv] must reach every
+// other rank's gathered buffer [Hq, T, dv].  NCCL's all-gather does that with CTAs taken from
+// the phase's SM partition.  Here the copy engines do it instead:
+//   1. entry handshake: tell every peer "my previous reads of the gathered buffer are done"
+//      and wait for the same from all of them, so a push cannot overwrite data a peer is
+//      still reading;
+//   2. push the local shard into each peer's gathered buffer (cudaMemcpyAsync on IPC-mapped
+//      pointers: copy-engine DMA over NVLink, no kernel);
+//   3. set slot `rank` of each peer's flag array (cuStreamWriteValue32, which fences the
+//      stream's prior writes first);
+//   4. wait until every peer's slot of the own flag array is set, and reset it
+//      (cuStreamWaitValue32 / cuStreamWriteValue32).
+// Steps 3-4 are stream memory operations executed by the GPU front end: the gather occupies
+// no SM of either partition.  Everything is stream-ordered on the caller's stream.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "internal.h"
+
+namespace {
+
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+PFN_wait32 g_wait = nullptr;
+PFN_write32 g_write = nullptr;
+
+bool load_stream_memops() {
+    static bool tried = false, ok = false;
+    if (tried) return ok;
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    // the _v2 stream memory operations (CUDA >= 11.7) are enabled by default; the v1 ones
+    // need a driver module option, so ask for the CUDA 12.0 ABI explicitly
+    if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        g_wait = reinterpret_cast<PFN_wait32>(p);
+    p = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        g_write = reinterpret_cast<PFN_write32>(p);
+    ok = g_wait && g_write;
+    return ok;
+}
+
+semipd_status fail(const char* what, int code) {
+    std::fprintf(stderr, "semipd_peer_gather: %s failed (%d)\n", what, code);
+    return SEMIPD_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+semipd_status semipd_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out) {
+    if (!dev_ptr || !handle_out || bytes == 0) return SEMIPD_ERR_INVALID;
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return SEMIPD_ERR_CUDA;
+    cudaIpcMemHandle_t h;
+    if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+        cudaFree(p);
+        return SEMIPD_ERR_CUDA;
+    }
+    static_assert(sizeof(h) == SEMIPD_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle_out, &h, sizeof(h));
+    *dev_ptr = p;
+    return SEMIPD_OK;
+}
+
+semipd_status semipd_ipc_free(void* dev_ptr) {
+    if (!dev_ptr) return SEMIPD_ERR_INVALID;
+    return cudaFree(dev_ptr) == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+}
+
+semipd_status semipd_ipc_open(const void* handle, void** dev_ptr) {
+    if (!handle || !dev_ptr) return SEMIPD_ERR_INVALID;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return SEMIPD_ERR_CUDA;
+    }
+    *dev_ptr = p;
+    return SEMIPD_OK;
+}
+
+semipd_status semipd_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return SEMIPD_ERR_INVALID;
+    return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+}
+
+semipd_status semipd_peer_gather(const void* src, size_t bytes, void* const* dsts,
+                                 uint32_t* const* peer_flags, uint32_t* my_flags, int32_t world,
+                                 int32_t rank, semipd_stream_t s) {
+    if (world < 1 || world > SEMIPD_MAX_PEERS || rank < 0 || rank >= world || !dsts ||
+        !peer_flags || !my_flags || (bytes > 0 && !src))
+        return SEMIPD_ERR_INVALID;
+    for (int k = 0; k < world; ++k)
+        if (!dsts[k] || !peer_flags[k]) return SEMIPD_ERR_INVALID;
+    if (!load_stream_memops()) return SEMIPD_ERR_UNSUPPORTED;
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    CUstream cs = reinterpret_cast<CUstream>(st);
+    auto dp = [](const uint32_t* p) { return reinterpret_cast<CUdeviceptr>(p); };
+    // Flags are binary semaphores (values 0 / 1): a waiter resets its own slot after the wait,
+    // so the operations carry no per-call value and a captured CUDA graph replays correctly.
+    // Slots [world, 2 world) = "ready", [0, world) = "landed".  The ready handshake orders a
+    // peer's next "landed" write after this rank's reset of the previous one (and vice versa).
+    for (int k = 0; k < world; ++k)
+        if (k != rank) {
+            const CUresult r = g_write(cs, dp(peer_flags[k] + world + rank), 1u, 0);
+            if (r != CUDA_SUCCESS) return fail("ready write", (int)r);
+        }
+    for (int k = 0; k < world; ++k) {
+        if (k == rank) continue;
+        CUresult r = g_wait(cs, dp(my_flags + world + k), 1u, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) return fail("ready wait", (int)r);
+        r = g_write(cs, dp(my_flags + world + k), 0u, 0);
+        if (r != CUDA_SUCCESS) return fail("ready reset", (int)r);
+    }
+    if (bytes > 0) {
+        // push to the peers in ring order starting after this rank, so the ranks' first copies
+        // target different destinations
+        for (int i = 0; i < world; ++i) {
+            const int k = (rank + 1 + i) % world;
+            if (dsts[k] == src) continue;
+            const cudaError_t e = cudaMemcpyAsync(dsts[k], src, bytes, cudaMemcpyDefault, st);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail("peer copy", (int)e);
+            }
+        }
+    }
+    // default write flags: a memory barrier orders the copies before the flag
+    for (int k = 0; k < world; ++k)
+        if (k != rank) {
+            const CUresult r = g_write(cs, dp(peer_flags[k] + rank), 1u, 0);
+            if (r != CUDA_SUCCESS) return fail("landed write", (int)r);
+        }
+    for (int k = 0; k < world; ++k) {
+        if (k == rank) continue;
+        CUresult r = g_wait(cs, dp(my_flags + k), 1u, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) return fail("landed wait", (int)r);
+        r = g_write(cs, dp(my_flags + k), 0u, 0);
+        if (r != CUDA_SUCCESS) return fail("landed reset", (int)r);
+    }
+    return SEMIPD_OK;
+}
+
+}  // extern "C"

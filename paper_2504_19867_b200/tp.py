@@ -61,3 +61,110 @@ def gather_heads(local_head_major: torch.Tensor, out: torch.Tensor, group) -> to
         parts = list(out.chunk(dist.get_world_size(group), dim=0))
         dist.all_gather(parts, local, group=group)
     return out
+
+
+class _DevBuf:
+    """A raw device allocation exposed to torch through __cuda_array_interface__ (bytes)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 2}
+
+
+class PeerGather:
+    """All-gather of head-major shards [Hq/TP, T, dv] -> [Hq, T, dv] with the copy engines
+    over IPC-mapped peer memory (C ABI ``semipd_peer_gather``).
+
+    Every rank owns one exportable region (``semipd_ipc_alloc``) holding ``n_bufs`` gathered
+    buffers plus a 2·TP uint32 flag array; the regions' IPC handles are exchanged once over
+    ``group`` (any backend) and mapped (``semipd_ipc_open``).  A gather pushes this rank's
+    shard into slot ``rank`` of every peer's buffer, then signals and waits with stream
+    memory operations: no kernel, no SM of the phase partition.  The operations carry no
+    per-call value, so a gather can be captured in a CUDA graph and replayed.  All ranks
+    must issue the same sequence of gathers on one PeerGather, from one stream at a time.  The attention kernel can
+    write its head-major output straight into ``local_view(buf)`` (then the local copy is
+    skipped).  Plumbing only: no attention arithmetic lives here."""
+
+    def __init__(self, full_shape, dtype: torch.dtype, group, device, n_bufs: int = 1):
+        import ctypes
+        import math
+
+        from . import _check, lib
+
+        self._ct = ctypes
+        self._lib = lib()
+        self._check = _check
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > 8 or full_shape[0] % self.world:
+            raise ValueError(f"{full_shape[0]} heads do not shard over {self.world} ranks")
+        self.device = torch.device(device)
+        self.full_shape = tuple(full_shape)
+        self.dtype = dtype
+        esz = torch.tensor([], dtype=dtype).element_size()
+        self.full_bytes = math.prod(full_shape) * esz
+        self.shard_bytes = self.full_bytes // self.world
+        self.buf_stride = -(-self.full_bytes // 256) * 256
+        self.n_bufs = n_bufs
+        self.flag_off = n_bufs * self.buf_stride
+        nbytes = self.flag_off + 2 * self.world * 4
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        with torch.cuda.device(self.device):
+            _check("semipd_ipc_alloc", self._lib.semipd_ipc_alloc(nbytes, ctypes.byref(ptr), handle))
+        self.base = ptr.value
+        self._mem = torch.as_tensor(_DevBuf(self.base, nbytes), device=self.device)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self.peer_base = []
+        self._opened = []
+        for k, h in enumerate(handles):
+            if k == self.rank:
+                self.peer_base.append(self.base)
+                continue
+            p = ctypes.c_void_p()
+            with torch.cuda.device(self.device):
+                _check("semipd_ipc_open", self._lib.semipd_ipc_open(ctypes.create_string_buffer(h, 64),
+                                                                    ctypes.byref(p)))
+            self.peer_base.append(p.value)
+            self._opened.append(p.value)
+        self.calls = 0
+        vp = ctypes.c_void_p
+        self._flags = (vp * self.world)(*[b + self.flag_off for b in self.peer_base])
+
+    def out(self, buf: int = 0) -> torch.Tensor:
+        """The gathered buffer ``buf`` as a [Hq, T, dv] tensor on this rank."""
+        off = buf * self.buf_stride
+        return self._mem[off:off + self.full_bytes].view(self.dtype).view(self.full_shape)
+
+    def local_view(self, buf: int = 0) -> torch.Tensor:
+        """This rank's head slice of ``out(buf)`` (write the shard here to skip the local copy)."""
+        h = self.full_shape[0] // self.world
+        return self.out(buf)[self.rank * h:(self.rank + 1) * h]
+
+    def __call__(self, local: torch.Tensor, buf: int = 0, stream=None) -> torch.Tensor:
+        ct = self._ct
+        if local.dtype != self.dtype or local.numel() * local.element_size() != self.shard_bytes:
+            raise ValueError("shard shape / dtype does not match the gather")
+        local = local.contiguous()
+        off = buf * self.buf_stride + self.rank * self.shard_bytes
+        dsts = (ct.c_void_p * self.world)(*[b + off for b in self.peer_base])
+        self.calls += 1
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self._check("semipd_peer_gather", self._lib.semipd_peer_gather(
+            ct.c_void_p(local.data_ptr()), self.shard_bytes, dsts, self._flags,
+            ct.c_void_p(self.base + self.flag_off), self.world, self.rank,
+            ct.c_void_p(stream.cuda_stream)))
+        return self.out(buf)
+
+    def close(self):
+        """Unmap the peers' regions and free this rank's (after a device sync / barrier)."""
+        for p in self._opened:
+            self._lib.semipd_ipc_close(self._ct.c_void_p(p))
+        self._opened = []
+        if self.base:
+            self._mem = None
+            self._lib.semipd_ipc_free(self._ct.c_void_p(self.base))
+            self.base = 0

@@ -52,3 +52,27 @@ def test_sass_is_blackwell_native():
     sass = subprocess.run([tool, "-sass", spd.lib()._name], capture_output=True, text=True).stdout
     for mnem in ("UTCHMMA", "LDTM", "STTM", "UTMALDG"):
         assert mnem in sass, mnem
+
+
+def test_peer_gather_host_argument_checks():
+    """The peer-gather calls reject bad host arguments before touching a device."""
+    L = spd.lib()
+    vp = ctypes.c_void_p
+    assert L.semipd_ipc_alloc(0, ctypes.byref(vp()), None) == spd.INVALID
+    assert L.semipd_ipc_open(None, None) == spd.INVALID
+    assert L.semipd_ipc_close(None) == spd.INVALID
+    assert L.semipd_ipc_free(None) == spd.INVALID
+    d = (vp * 2)(1, 2)
+    f = (vp * 2)(3, 4)
+    args = dict(src=vp(5), bytes=16, dsts=d, flags=f, mine=vp(6), world=2, rank=0)
+
+    def call(**kw):
+        a = {**args, **kw}
+        return L.semipd_peer_gather(a["src"], a["bytes"], a["dsts"], a["flags"], a["mine"],
+                                    a["world"], a["rank"], None)
+    assert call(world=0) == spd.INVALID
+    assert call(world=9) == spd.INVALID
+    assert call(rank=2) == spd.INVALID
+    assert call(mine=None) == spd.INVALID
+    assert call(dsts=(vp * 2)(1, None)) == spd.INVALID
+    assert call(src=None) == spd.INVALID

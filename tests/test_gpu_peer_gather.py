@@ -1,0 +1,155 @@
+"""Copy-engine peer all-gather of head-major shards (``semipd_peer_gather``; SURVEY §8(e),
+§8(f) N2).  Two processes share the one GPU of the box: IPC handles open across processes
+on the same device exactly as across NVLink peers, and the copies / stream memory
+operations are the same calls.  Checks are bitwise: a gather moves bytes.
+
+- generic: several rounds of seeded shards with the entry handshake; every rank's gathered
+  buffer equals the rank-order concatenation; a shard written in place (local_view) skips
+  the local copy and is gathered too;
+- kernel outputs: each rank's head-major decode / prefill output for its KV-head shard
+  (cfg3 shapes, Hkv 8 -> 4 per rank), gathered, equals the unsharded run bitwise."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _shard(rnd, rank, shape_local):
+    g = torch.Generator().manual_seed(1000 * rnd + rank)
+    return torch.randn(*shape_local, generator=g).to(torch.bfloat16)
+
+
+def _generic_worker(rank, ws, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from paper_2504_19867_b200 import tp
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    try:
+        full = (8, 37, 64)
+        loc = (full[0] // ws,) + full[1:]
+        pg = tp.PeerGather(full, torch.bfloat16, dist.group.WORLD, dev, n_bufs=2)
+        s = torch.cuda.Stream(dev)
+        bad = []
+        for rnd in range(6):
+            buf = rnd % 2
+            with torch.cuda.stream(s):
+                if rnd % 3 == 2:  # in place: the shard is already in the gathered buffer
+                    pg.local_view(buf).copy_(_shard(rnd, rank, loc).to(dev))
+                    out = pg(pg.local_view(buf), buf=buf, stream=s)
+                else:
+                    out = pg(_shard(rnd, rank, loc).to(dev), buf=buf, stream=s)
+                got = out.cpu()
+            s.synchronize()
+            want = torch.cat([_shard(rnd, k, loc) for k in range(ws)])
+            if not torch.equal(got.view(torch.int16), want.view(torch.int16)):
+                bad.append(rnd)
+        # captured once into a CUDA graph, replayed with new shard contents (the flag
+        # operations carry no per-call value, so every replay synchronises afresh)
+        torch.cuda.synchronize()
+        src = torch.empty(loc, dtype=torch.bfloat16, device=dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            pg(src, buf=0, stream=torch.cuda.current_stream())
+        for rnd in range(6, 10):
+            src.copy_(_shard(rnd, rank, loc).to(dev))
+            g.replay()
+            got = pg.out(0).cpu()
+            want = torch.cat([_shard(rnd, k, loc) for k in range(ws)])
+            if not torch.equal(got.view(torch.int16), want.view(torch.int16)):
+                bad.append(rnd)
+        torch.cuda.synchronize()
+        dist.barrier()
+        pg.close()
+        q.put((rank, bad, pg.calls))
+    except Exception as e:  # report instead of leaving the parent waiting
+        q.put((rank, repr(e), -1))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_two(target, timeout):
+    """Start two daemon workers; collect one result each; never leave a worker behind (a
+    worker whose peer died would wait on its stream forever)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, 2, port, q), daemon=True) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        res = [q.get(timeout=timeout) for _ in procs]
+        for p in procs:
+            p.join(timeout=60)
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+    return res, procs
+
+
+def test_peer_gather_generic_two_processes():
+    res, procs = _run_two(_generic_worker, 240)
+    for rank, bad, calls in res:
+        assert bad == [], f"rank {rank}: rounds {bad} gathered wrong bytes"
+        assert calls == 7  # 6 eager calls + the one captured
+    assert all(p.exitcode == 0 for p in procs)
+
+
+def _kernel_worker(rank, ws, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import synth
+    from paper_2504_19867_b200 import tp
+    from test_gpu_tp_emulated import _run
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    try:
+        shape = synth.AttnShape("llama3-70b", 64, 8, 128, 128, 64, torch.bfloat16)
+        ctx, chunk = [300, 2048, 4500], 700
+        cd = synth.decode_case(shape, ctx, seed=3030)
+        cp = synth.prefill_case(shape, [chunk], [0], seed=3031)
+        od, op = _run(shape, ctx, chunk, cd, cp, tp.head_range(8, ws, rank),
+                      tp.head_range(64, ws, rank), dev)
+        groups = tp.PhaseGroups.create(backend="gloo")
+        pgd = tp.PeerGather((64, len(ctx), 128), torch.bfloat16, groups.decode, dev)
+        pgp = tp.PeerGather((64, chunk, 128), torch.bfloat16, groups.prefill, dev)
+        sd, sp = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        with torch.cuda.stream(sd):
+            gd = pgd(od.to(dev), stream=sd)
+        with torch.cuda.stream(sp):
+            gp = pgp(op.to(dev), stream=sp)
+        torch.cuda.synchronize()
+        gd, gp = gd.cpu(), gp.cpu()
+        ok = True
+        if rank == 0:
+            full_d, full_p = _run(shape, ctx, chunk, cd, cp, (0, 8), (0, 64), dev)
+            ok = torch.equal(gd, full_d) and torch.equal(gp, full_p)
+        dist.barrier()
+        pgd.close()
+        pgp.close()
+        q.put((rank, ok))
+    except Exception as e:
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_gather_kernel_outputs_equal_unsharded():
+    res, procs = _run_two(_kernel_worker, 300)
+    for rank, ok in res:
+        assert ok is True, f"rank {rank}: {ok if isinstance(ok, str) else 'gathered kernel outputs differ from the unsharded run'}"
+    assert all(p.exitcode == 0 for p in procs)

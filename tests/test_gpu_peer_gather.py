@@ -153,3 +153,15 @@ def test_peer_gather_kernel_outputs_equal_unsharded():
     for rank, ok in res:
         assert ok is True, f"rank {rank}: {ok if isinstance(ok, str) else 'gathered kernel outputs differ from the unsharded run'}"
     assert all(p.exitcode == 0 for p in procs)
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_peer_gather_emulated_ranks_one_process(tp):
+    """TP ranks emulated as streams of one process (plain device pointers for the peers'
+    buffers and flags): bitwise gather, every flag reset afterwards, repeatable."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "scripts"))
+    from peer_gather_bench import run
+    r = run(tp, (16, 129, 64), iters=3)
+    assert r["shard_bytes"] == 16 // tp * 129 * 64 * 2

@@ -280,6 +280,24 @@ class Workload:
         pairs = self.C * (self.C + 1) / 2
         return 2.0 * s.num_q_heads * (s.head_dim_k + s.head_dim_v) * pairs
 
+    # TP > 1: the head all-gather of layer l's head-major output on the phase stream s
+    # (one communicator per phase); a no-op at TP = 1
+    def gather_p(self, l, s):
+        if self.tp > 1:
+            from paper_2504_19867_b200 import tp as tpmod
+            if self.peer_p is not None:
+                self.peer_p(self.op[l], stream=s)
+            else:
+                tpmod.gather_heads(self.op[l], self.gath_p, self.pg_p)
+
+    def gather_d(self, l, s):
+        if self.tp > 1:
+            from paper_2504_19867_b200 import tp as tpmod
+            if self.peer_d is not None:
+                self.peer_d(self.od[l], stream=s)
+            else:
+                tpmod.gather_heads(self.od[l], self.gath_d, self.pg_d)
+
     def phase_prefill(self, budget, timed=False, stream=None):
         s = stream or self.sP
         p = self.pool
@@ -293,12 +311,7 @@ class Workload:
                                out_head_major=self.tp > 1, sm_budget=budget, stream=s)
                 if timed:
                     self.ev_p[l][1].record(s)
-                if self.tp > 1:
-                    from paper_2504_19867_b200 import tp as tpmod
-                    if self.peer_p is not None:
-                        self.peer_p(self.op[l], stream=s)
-                    else:
-                        tpmod.gather_heads(self.op[l], self.gath_p, self.pg_p)
+                self.gather_p(l, s)
             p.free_blocks(self.rid_pre, None, stream=s)
 
     def phase_decode(self, budget, timed=False, stream=None):
@@ -313,12 +326,7 @@ class Workload:
                               out_head_major=self.tp > 1, sm_budget=budget, stream=s)
                 if timed:
                     self.ev_d[l][1].record(s)
-                if self.tp > 1:
-                    from paper_2504_19867_b200 import tp as tpmod
-                    if self.peer_d is not None:
-                        self.peer_d(self.od[l], stream=s)
-                    else:
-                        tpmod.gather_heads(self.od[l], self.gath_d, self.pg_d)
+                self.gather_d(l, s)
 
     def corun_step(self, x, y, timed=False):
         """One co-run iteration: both workers concurrently at budgets from (x, y)."""
@@ -417,6 +425,7 @@ class E2E:
                 w.sP.wait_event(self.in_p[l])
                 w.pool.prefill_attn(l, w.qp[l], w.kp[l], w.vp[l], w.cu, w.rid_pre, w.prefix, w.C,
                                     w.C, w.scale, w.op[l], out_head_major=w.tp > 1, stream=w.sP)
+                w.gather_p(l, w.sP)  # TP > 1: same exchange step as the device-timed path
                 self.out_p[l].record(w.sP)
             w.pool.free_blocks(w.rid_pre, None, stream=w.sP)
         with torch.cuda.stream(w.sD):
@@ -424,6 +433,7 @@ class E2E:
                 w.sD.wait_event(self.in_d[l])
                 w.pool.decode_attn(l, w.qd[l], w.kd[l], w.vd[l], w.rid_dec, w.ctx_lens, w.ctx,
                                    w.scale, w.od[l], w.ws, out_head_major=w.tp > 1, stream=w.sD)
+                w.gather_d(l, w.sD)
                 self.out_d[l].record(w.sD)
         with torch.cuda.stream(self.s_out):
             for l in range(w.L):

@@ -255,6 +255,28 @@ semipd_status semipd_peer_gather(const void* src, size_t bytes, void* const* dst
                                  uint32_t* const* peer_flags, uint32_t* my_flags, int32_t world,
                                  int32_t rank, semipd_stream_t s);
 
+/* ---- Rotary position embedding of the step's new rows ----
+ * P:355 §6: "To support the Llama3.1 series model, we also modify the RoPE kernel."
+ * Rotates q [num_tokens][num_q_heads][head_dim] and k [num_tokens][num_kv_heads][head_dim]
+ * (device, token-major, contiguous, 16-byte aligned, pool dtype `dtype`) IN PLACE for the
+ * token positions positions[num_tokens] (device int32), before the attention call that
+ * writes k into the pool.  Half-split pairs (i, i + d/2) (reading R27):
+ *   f_i = theta^(-2i/d); if factor > 1, the Llama-3.1 rescaling with wavelength
+ *   w_i = 2 pi / f_i and L0 = original_max_pos: w_i < L0/high_freq_factor -> f_i;
+ *   w_i > L0/low_freq_factor -> f_i / factor; otherwise (1-a) f_i / factor + a f_i with
+ *   a = (L0 / w_i - low_freq_factor) / (high_freq_factor - low_freq_factor);
+ *   phi = pos * f_i;  x_i' = x_i cos phi - x_{i+d/2} sin phi;
+ *   x_{i+d/2}' = x_{i+d/2} cos phi + x_i sin phi.
+ * The frequencies, the angle and its sine / cosine are formed in fp64, the rotation in fp32.
+ * factor <= 1 disables the rescaling (plain RoPE).  q (k) may be NULL when its head count is
+ * 0.  Errors: INVALID (negative sizes, odd head_dim, theta <= 1, bad scaling parameters,
+ * NULL), UNSUPPORTED (head_dim/2 not a multiple of 8 (bf16) / 4 (fp32), head_dim > 256,
+ * misaligned rows), CUDA.  num_tokens == 0 is a no-op. */
+semipd_status semipd_rope(void* q, void* k, const int32_t* positions, int32_t num_tokens,
+                          int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
+                          int32_t dtype, double theta, double factor, double low_freq_factor,
+                          double high_freq_factor, int32_t original_max_pos, semipd_stream_t s);
+
 /* Library version string (host, static). */
 const char* semipd_version(void);
 

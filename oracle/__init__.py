@@ -66,6 +66,10 @@ def lib():
             L.semipd_ref_effective_shares.argtypes = [d, d, ctypes.POINTER(d), ctypes.POINTER(d)]
             L.semipd_ref_effective_shares.restype = None
             L.semipd_ref_blocks_for_tokens.argtypes = [i, i]
+            L.semipd_ref_rope_inv_freq.argtypes = [i, d, d, d, d, d, dp]
+            L.semipd_ref_rope_inv_freq.restype = None
+            L.semipd_ref_rope.argtypes = [i, i, i, vp, i, vp, d, d, d, d, d, dp]
+            L.semipd_ref_rope.restype = None
             _ = ip
             _lib = L
     return _lib
@@ -242,3 +246,24 @@ class Allocator:
 
     def snapshot(self):
         return (self.free_stack.copy(), int(self.top[0]), self.bt.copy(), self.nblk.copy())
+
+
+def rope_inv_freq(d: int, theta: float, factor: float = 0.0, lf: float = 1.0, hf: float = 4.0,
+                  L0: float = 8192.0) -> np.ndarray:
+    """RoPE frequencies f_i, i < d/2 (Llama-3.1 rescaling if factor > 1; DESIGN R27)."""
+    out = np.zeros(d // 2, np.float64)
+    lib().semipd_ref_rope_inv_freq(d, theta, factor, lf, hf, L0, _p(out))
+    return out
+
+
+def rope(x, positions, theta: float, factor: float = 0.0, lf: float = 1.0, hf: float = 4.0,
+         L0: float = 8192.0) -> np.ndarray:
+    """Rotate x [T, H, d] (bf16 bits as uint16, or float32) at positions [T]; returns fp64
+    [T, H, d] (half-split pairs, DESIGN R27)."""
+    x = _c(x)
+    T, H, d = x.shape
+    pos = np.ascontiguousarray(positions, dtype=np.int32)
+    out = np.zeros((T, H, d), np.float64)
+    lib().semipd_ref_rope(T, H, d, _p(x), _dtype_code(x), _p(pos), theta, factor, lf, hf, L0,
+                          _p(out))
+    return out

@@ -441,3 +441,54 @@ int semipd_ref_blocks_for_tokens(int tokens, int bs) {
     if (tokens < 0 || bs <= 0) return -1;
     return (tokens + bs - 1) / bs;
 }
+
+/* ---- Rotary position embedding ----
+ * PAPER P:355 §6: "To support the Llama3.1 series model, we also modify the RoPE kernel."
+ * The paper gives no formula; reading R27 fixes it as RoFormer's rotation with
+ * Llama's half-split pairing (i, i + d/2) and the Llama-3.1 frequency rescaling.
+ *
+ * semipd_ref_rope_inv_freq: the d/2 frequencies, step by step:
+ *   f_i = theta^(-2i/d)                                    (RoFormer)
+ *   if factor > 1 (Llama 3.1), with w_i = 2 pi / f_i:
+ *     w_i < L0 / hf            -> f_i           (high frequencies kept)
+ *     w_i > L0 / lf            -> f_i / factor  (low frequencies stretched)
+ *     otherwise                -> (1 - a) f_i / factor + a f_i,  a = (L0 / w_i - lf) / (hf - lf) */
+void semipd_ref_rope_inv_freq(int d, double theta, double factor, double lf, double hf, double L0,
+                              double* out) {
+    const double pi = 3.14159265358979323846;
+    for (int i = 0; i < d / 2; ++i) {
+        double f = pow(theta, -2.0 * (double)i / (double)d);
+        if (factor > 1.0) {
+            double w = 2.0 * pi / f;
+            if (w < L0 / hf) {
+                /* unchanged */
+            } else if (w > L0 / lf) {
+                f = f / factor;
+            } else {
+                double a = (L0 / w - lf) / (hf - lf);
+                f = (1.0 - a) * f / factor + a * f;
+            }
+        }
+        out[i] = f;
+    }
+}
+
+/* semipd_ref_rope: x [T][H][d] (stored dtype, widened exactly) -> out [T][H][d] fp64:
+ *   phi = pos_t * f_i;  out_i = x_i cos phi - x_{i+d/2} sin phi;
+ *                       out_{i+d/2} = x_{i+d/2} cos phi + x_i sin phi. */
+void semipd_ref_rope(int T, int H, int d, const void* x, int dtype, const int* pos, double theta,
+                     double factor, double lf, double hf, double L0, double* out) {
+    double* f = (double*)malloc(sizeof(double) * (size_t)(d / 2));
+    semipd_ref_rope_inv_freq(d, theta, factor, lf, hf, L0, f);
+    for (int t = 0; t < T; ++t)
+        for (int h = 0; h < H; ++h) {
+            size_t row = ((size_t)t * H + h) * d;
+            for (int i = 0; i < d / 2; ++i) {
+                double phi = (double)pos[t] * f[i];
+                double x0 = ld(x, row + i, dtype), x1 = ld(x, row + d / 2 + i, dtype);
+                out[row + i] = x0 * cos(phi) - x1 * sin(phi);
+                out[row + d / 2 + i] = x1 * cos(phi) + x0 * sin(phi);
+            }
+        }
+    free(f);
+}

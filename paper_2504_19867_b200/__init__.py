@@ -19,7 +19,7 @@ import torch
 from . import _build
 
 __all__ = ["SemipdError", "PoolConfig", "KVPool", "lib", "build", "blocks_for_tokens",
-           "STATUS"]
+           "STATUS", "RopeConfig", "rope_"]
 
 STATUS = {0: "OK", 1: "INVALID", 2: "OOM", 3: "UNKNOWN_REQ", 4: "TABLE_FULL", 5: "BAD_BLOCK",
           6: "CUDA", 7: "UNSUPPORTED"}
@@ -86,6 +86,8 @@ def lib():
                 "semipd_ipc_open": (i32, [vp, P(vp)]),
                 "semipd_ipc_close": (i32, [vp]),
                 "semipd_peer_gather": (i32, [vp, sz, P(vp), P(vp), vp, i32, i32, vp]),
+                "semipd_rope": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, f64, f64, f64, f64,
+                                      i32, vp]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -115,6 +117,36 @@ def blocks_for_tokens(tokens: int, block_size: int) -> int:
 
 
 _TORCH_DT = {BF16: torch.bfloat16, FP32: torch.float32}
+
+
+@dataclass
+class RopeConfig:
+    """RoPE parameters (Llama-3.1 defaults: theta 5e5, factor 8, low / high frequency factors
+    1 / 4, original context 8192; factor <= 1 = plain RoPE)."""
+    theta: float = 500000.0
+    factor: float = 8.0
+    low_freq_factor: float = 1.0
+    high_freq_factor: float = 4.0
+    original_max_pos: int = 8192
+
+
+def rope_(q, k, positions, cfg: RopeConfig | None = None, stream=None):
+    """Rotate q [T, Hq, d] and k [T, Hkv, d] in place at int32 positions [T] (C ABI
+    ``semipd_rope``; runs in the library's kernel)."""
+    cfg = cfg or RopeConfig()
+    t = q if q is not None else k
+    dt = BF16 if t.dtype == torch.bfloat16 else FP32 if t.dtype == torch.float32 else None
+    if dt is None:
+        raise SemipdError("semipd_rope", UNSUPPORTED)
+    for x in (q, k):
+        if x is not None and not x.is_contiguous():
+            raise SemipdError("semipd_rope", INVALID)
+    _check("semipd_rope", lib().semipd_rope(
+        _ptr(q), _ptr(k), _ptr(positions), int(t.shape[0]), 0 if q is None else int(q.shape[1]),
+        0 if k is None else int(k.shape[1]), int(t.shape[2]), dt, float(cfg.theta),
+        float(cfg.factor), float(cfg.low_freq_factor), float(cfg.high_freq_factor),
+        int(cfg.original_max_pos), _stream(stream)))
+    return q, k
 
 
 @dataclass

@@ -1,7 +1,7 @@
 cd /root/repo
 timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "mla" -p no:cacheprovider > gpurun_out/mla_tests.log 2>&1; tail -2 gpurun_out/mla_tests.log
 for rep in 1 2; do
-for t in base rope; do
+for t in base rope; do  # rope = candidate build
   echo "== $t"
   SEMIPD_LIB=$PWD/paper_2504_19867_b200/libsemipd_v_$t.so timeout 300 python scripts/microbench.py --mla --budgets 74,148 --batch 256 --ctx 1000 --layers 4 2>&1 | tail -2
   SEMIPD_LIB=$PWD/paper_2504_19867_b200/libsemipd_v_$t.so timeout 300 python scripts/microbench.py --mla --budgets 148 --batch 64 --ctx 4000 --layers 4 2>&1 | tail -1

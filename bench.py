@@ -60,9 +60,11 @@ def parse():
     ap.add_argument("--block-size", type=int, default=64,
                     help="KV page size in tokens (64: one 16 KiB TMA box per (block, head) "
                          "page on B200; 16 is supported but TMA-per-box bound)")
-    ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
-                    help="TP head all-gather: NCCL all_gather (CTAs) or copy-engine pushes over "
-                         "IPC-mapped peer memory with stream-memop flags (no SMs)")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "peer", "fused"],
+                    help="TP head all-gather: NCCL all_gather (CTAs); peer = copy-engine pushes "
+                         "over IPC-mapped peer memory with stream-memop flags (no SMs); fused = "
+                         "decode stores its output into the peers' buffers from its epilogue "
+                         "(prefill as peer)")
     ap.add_argument("--peer-graph", action="store_true",
                     help="N > 1 with --gather peer: replay the co-run step as a CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
@@ -241,6 +243,7 @@ class Workload:
         self.sD = torch.cuda.Stream(device=dev)
         self.pg_p = self.pg_d = None
         self.peer_p = self.peer_d = None
+        self.fused_d = False
         self.gath_p = self.gath_d = None
         if tp > 1:
             from paper_2504_19867_b200 import tp as tpmod
@@ -249,9 +252,13 @@ class Workload:
             self.pg_p, self.pg_d = groups.prefill, groups.decode
             self.gath_p = torch.empty((self.full.num_q_heads, self.C, d), dtype=s.dtype, device=dev)
             self.gath_d = torch.empty((self.full.num_q_heads, self.B, d), dtype=s.dtype, device=dev)
-            if gather == "peer":  # copy engines + stream memops instead of NCCL CTAs
+            if gather in ("peer", "fused"):  # copy engines + stream memops instead of NCCL CTAs
                 self.peer_p = tpmod.PeerGather(self.gath_p.shape, s.dtype, self.pg_p, dev)
                 self.peer_d = tpmod.PeerGather(self.gath_d.shape, s.dtype, self.pg_d, dev)
+            if gather == "fused":  # decode epilogue stores straight into every rank's buffer
+                self.fused_d = True
+                self.pool.set_decode_peers(self.peer_d.peer_shard_ptrs())
+                self.od = [self.peer_d.local_view() for _ in range(self.L)]
         # per-launch timing events (decode kernel on stream D, prefill call on stream P)
         self.ev_d = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                      for _ in range(self.L)]
@@ -290,8 +297,14 @@ class Workload:
             else:
                 tpmod.gather_heads(self.op[l], self.gath_p, self.pg_p)
 
+    def pre_d(self, l, s):  # fused gather: every peer is done reading before the stores
+        if self.fused_d:
+            self.peer_d.handshake(0, stream=s)
+
     def gather_d(self, l, s):
-        if self.tp > 1:
+        if self.fused_d:  # the kernel already stored; wait until every peer's stores landed
+            self.peer_d.handshake(1, stream=s)
+        elif self.tp > 1:
             from paper_2504_19867_b200 import tp as tpmod
             if self.peer_d is not None:
                 self.peer_d(self.od[l], stream=s)
@@ -319,6 +332,7 @@ class Workload:
         p = self.pool
         with torch.cuda.stream(s):
             for l in range(self.L):
+                self.pre_d(l, s)
                 if timed:
                     self.ev_d[l][0].record(s)
                 p.decode_attn(l, self.qd[l], self.kd[l], self.vd[l], self.rid_dec, self.ctx_lens,
@@ -431,6 +445,7 @@ class E2E:
         with torch.cuda.stream(w.sD):
             for l in range(w.L):
                 w.sD.wait_event(self.in_d[l])
+                w.pre_d(l, w.sD)
                 w.pool.decode_attn(l, w.qd[l], w.kd[l], w.vd[l], w.rid_dec, w.ctx_lens, w.ctx,
                                    w.scale, w.od[l], w.ws, out_head_major=w.tp > 1, stream=w.sD)
                 w.gather_d(l, w.sD)
@@ -509,7 +524,9 @@ def workload_config(shape: synth.AttnShape, ws: int, gather: str = "nccl") -> di
                         f"d 128, bs {shape.block_size}, {shape.num_layers} layers): decode B={DECODE_BATCH} "
                         f"ctx={DECODE_CTX} + prefill chunk {PREFILL_TOKENS} (P=0), co-run",
             "parallelism": (f"tp{ws} (KV-head shards, "
-                            + ("copy-engine peer all-gather)" if gather == "peer" else "NCCL all-gather)")
+                            + {"peer": "copy-engine peer all-gather)",
+                               "fused": "decode-epilogue peer stores + copy-engine prefill gather)"}
+                            .get(gather, "NCCL all-gather)")
                             if ws > 1 else "tp1"),
             "l2": f"no flush: per-step decode working set {decode_gb:.1f} GB >> 126 MB L2"}
 

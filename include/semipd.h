@@ -255,6 +255,24 @@ semipd_status semipd_peer_gather(const void* src, size_t bytes, void* const* dst
                                  uint32_t* const* peer_flags, uint32_t* my_flags, int32_t world,
                                  int32_t rank, semipd_stream_t s);
 
+/* ---- The decode head gather fused into the decode kernel's epilogue ----
+ * semipd_set_decode_peers: later semipd_decode_attn calls on this pool ALSO store every output
+ * vector to peer_out[k] + (the same element offset as in `out`), k < n (host array of device
+ * pointers, n <= SEMIPD_MAX_PEERS - 1; n = 0 clears).  With head-major output
+ * ([Hq/TP, B, dv], out_head_major = 1, required) and peer_out[k] = peer k's gathered buffer
+ * [Hq, B, dv] as mapped in this process, offset to this rank's head slice, the kernel's
+ * epilogue performs this rank's part of the all-gather itself (posted NVLink stores, no
+ * copies).  Bracket each such decode call with semipd_peer_handshake: which = 0 ("ready")
+ * before it, so no peer is still reading the buffer, and which = 1 ("landed") after it, which
+ * fences the kernel's stores and waits until every peer's have landed here.  Only the bf16
+ * split-K decode kernels support peers: other decode paths return UNSUPPORTED, row-major
+ * output INVALID.  Errors: INVALID (NULL pool, n out of range, NULL / unaligned pointer).
+ * semipd_peer_handshake: one of the two handshakes semipd_peer_gather performs (flag arrays
+ * as there; which: 0 = ready, 1 = landed), as one batched stream-memory-operation call. */
+semipd_status semipd_set_decode_peers(semipd_pool_t pool, void* const* peer_out, int32_t n);
+semipd_status semipd_peer_handshake(uint32_t* const* peer_flags, uint32_t* my_flags,
+                                    int32_t world, int32_t rank, int32_t which, semipd_stream_t s);
+
 /* ---- Rotary position embedding of the step's new rows ----
  * P:355 §6: "To support the Llama3.1 series model, we also modify the RoPE kernel."
  * Rotates q [num_tokens][num_q_heads][head_dim] and k [num_tokens][num_kv_heads][head_dim]

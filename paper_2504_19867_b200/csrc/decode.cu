@@ -62,11 +62,24 @@ struct DecodeParams {
     unsigned* sched;             // [2]: next unit, finished CTAs
     int* status;
     int B, Hq, Hkv, G, lg_bs, MBR, N_B, S_max, n_units, out_head_major;
+    // TP head all-gather fused into the epilogue: every output vector is also
+    // stored to each peer's gathered buffer (peer-mapped, already offset to this rank's shard)
+    __nv_bfloat16* peers[SEMIPD_MAX_PEERS - 1];
+    int n_peers;
     float scale_log2;
     SpdTrace trace;
     long long* tl;  // SPD_TIMELINE builds only: per-stage clock64 stamps of CTA 0
     int* tl_ctr;
 };
+
+// one bf16x4 output vector: local buffer, then every peer's gathered buffer (NVLink posted
+// stores; the caller's "landed" handshake after the kernel publishes them)
+__device__ __forceinline__ void store_out(const DecodeParams& p, size_t off, uint2 v) {
+    *reinterpret_cast<uint2*>(p.out + off) = v;
+#pragma unroll
+    for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k)
+        if (k < p.n_peers) *reinterpret_cast<uint2*>(p.peers[k] + off) = v;
+}
 
 #ifdef SPD_TIMELINE
 #define TL_REC(a, b, c, d, e)                                                              \
@@ -175,7 +188,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 uint2 v;
                 v.x = pack_bf16(o.x * inv, o.y * inv);
                 v.y = pack_bf16(o.z * inv, o.w * inv);
-                *reinterpret_cast<uint2*>(p.out + off) = v;
+                store_out(p, off, v);
             } else {
                 const size_t pi = ((size_t)d.b * p.Hq + hq) * p.S_max + d.s;
                 *reinterpret_cast<float4*>(p.ws_acc + pi * HD + c) = o;
@@ -219,7 +232,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                     uint2 v;
                     v.x = pack_bf16(o.x * inv, o.y * inv);
                     v.y = pack_bf16(o.z * inv, o.w * inv);
-                    *reinterpret_cast<uint2*>(p.out + off) = v;
+                    store_out(p, off, v);
                 }
                 if (tid == 0) p.ws_cnt[d.b * p.Hkv + d.g] = 0;  // ready for the next call
             }
@@ -1028,7 +1041,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                     uint2 v;
                     v.x = pack_bf16(o.x * inv, o.y * inv);
                     v.y = pack_bf16(o.z * inv, o.w * inv);
-                    *reinterpret_cast<uint2*>(p.out + off) = v;
+                    store_out(p, off, v);
                 } else {
                     const size_t pi = ((size_t)d.b * p.Hq + hq) * p.S_max + d.s;
                     *reinterpret_cast<float4*>(p.ws_acc + pi * HD + c) = o;
@@ -1069,7 +1082,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                         uint2 v;
                         v.x = pack_bf16(o.x * inv, o.y * inv);
                         v.y = pack_bf16(o.z * inv, o.w * inv);
-                        *reinterpret_cast<uint2*>(p.out + off) = v;
+                        store_out(p, off, v);
                     }
                     if (tid == 0) p.ws_cnt[d.b * p.Hkv + d.g] = 0;
                 }
@@ -1147,6 +1160,10 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     if (!q || !k_new || (!v_new && !c.kv_shared) || !req_ids || !ctx_lens || !out)
         return SEMIPD_ERR_INVALID;
     const int budget = spd_resolve_budget(pool, sm_budget, false);
+    if (pool->dec_n_peers > 0 && (!out_head_major || !fast_path_ok(pool, num_q_heads) ||
+                                  spd_mla_tc_ok(pool, num_q_heads) ||
+                                  spd_mla_decode_ok(pool, num_q_heads)))
+        return pool->dec_n_peers > 0 && !out_head_major ? SEMIPD_ERR_INVALID : SEMIPD_ERR_UNSUPPORTED;
     if (spd_mla_tc_ok(pool, num_q_heads))  // absorbed MLA latent cache, 64-token pages (cfg 5)
         return spd_launch_decode_mla_tc(pool, layer, q, k_new, req_ids, ctx_lens, batch,
                                         max_ctx_len, num_q_heads, softmax_scale, out,
@@ -1195,6 +1212,9 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     prm.S_max = S_max;
     prm.n_units = batch * c.num_kv_heads * S_max;
     prm.out_head_major = out_head_major;
+    prm.n_peers = pool->dec_n_peers;
+    for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k)
+        prm.peers[k] = k < pool->dec_n_peers ? static_cast<__nv_bfloat16*>(pool->dec_peers[k]) : nullptr;
     prm.scale_log2 = softmax_scale * LOG2E;
     prm.trace = spd_trace(pool);
     prm.tl = reinterpret_cast<long long*>(pool->timeline);
@@ -1248,6 +1268,15 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     else swap ? launch(decode_bf16_kernel<6, true>) : launch(decode_bf16_kernel<6, false>);
     if (e != cudaSuccess) return SEMIPD_ERR_CUDA;
     pool->launches += 1;
+    return SEMIPD_OK;
+}
+
+semipd_status semipd_set_decode_peers(semipd_pool_t pool, void* const* peer_out, int32_t n) {
+    if (!pool || n < 0 || n > SEMIPD_MAX_PEERS - 1 || (n > 0 && !peer_out)) return SEMIPD_ERR_INVALID;
+    for (int k = 0; k < n; ++k)
+        if (!peer_out[k] || reinterpret_cast<uintptr_t>(peer_out[k]) % 8) return SEMIPD_ERR_INVALID;
+    for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k) pool->dec_peers[k] = k < n ? peer_out[k] : nullptr;
+    pool->dec_n_peers = n;
     return SEMIPD_OK;
 }
 

@@ -64,6 +64,40 @@ semipd_status fail(const char* what, int code) {
     return SEMIPD_ERR_CUDA;
 }
 
+// One batched stream-memory-operation call per handshake (measured on this B200: one write /
+// wait call costs ~2 us of submission, a batch ~0.6 us per op): set this rank's slot in every
+// peer's flag array (writes fence the stream's prior writes, so copies / kernel stores land
+// first), then wait for and reset each own slot.  base_slot: 0 = "landed", world = "ready".
+semipd_status handshake(CUstream cs, uint32_t* const* peer_flags, uint32_t* my_flags, int world,
+                        int rank, int base_slot) {
+    auto dp = [](const uint32_t* p) { return reinterpret_cast<CUdeviceptr>(p); };
+    CUstreamBatchMemOpParams ops[3 * SEMIPD_MAX_PEERS];
+    std::memset(ops, 0, sizeof(ops));
+    int n = 0;
+    for (int k = 0; k < world; ++k) {
+        if (k == rank) continue;
+        ops[n].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+        ops[n].writeValue.address = dp(peer_flags[k] + base_slot + rank);
+        ops[n].writeValue.value = 1u;
+        ++n;
+    }
+    for (int k = 0; k < world; ++k) {
+        if (k == rank) continue;
+        ops[n].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+        ops[n].waitValue.address = dp(my_flags + base_slot + k);
+        ops[n].waitValue.value = 1u;
+        ops[n].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+        ++n;
+        ops[n].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+        ops[n].writeValue.address = dp(my_flags + base_slot + k);
+        ops[n].writeValue.value = 0u;
+        ++n;
+    }
+    if (n == 0) return SEMIPD_OK;
+    const CUresult r = g_batch(cs, (unsigned)n, ops, 0);
+    return r == CUDA_SUCCESS ? SEMIPD_OK : fail("batched flag operations", (int)r);
+}
+
 }  // namespace
 
 extern "C" {
@@ -117,43 +151,12 @@ semipd_status semipd_peer_gather(const void* src, size_t bytes, void* const* dst
     if (!load_stream_memops()) return SEMIPD_ERR_UNSUPPORTED;
     cudaStream_t st = static_cast<cudaStream_t>(s);
     CUstream cs = reinterpret_cast<CUstream>(st);
-    auto dp = [](const uint32_t* p) { return reinterpret_cast<CUdeviceptr>(p); };
-    // One batched stream-memory-operation call per handshake (measured on this B200: one
-    // write / wait call costs ~2 us of submission, a batch ~0.6 us per op): set the peers'
-    // slots (writes fence the stream's prior writes, so the copies land first), then wait for
-    // and reset each own slot.
-    auto signal_and_wait = [&](int base_slot) -> semipd_status {
-        CUstreamBatchMemOpParams ops[3 * SEMIPD_MAX_PEERS];
-        std::memset(ops, 0, sizeof(ops));
-        int n = 0;
-        for (int k = 0; k < world; ++k) {
-            if (k == rank) continue;
-            ops[n].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
-            ops[n].writeValue.address = dp(peer_flags[k] + base_slot + rank);
-            ops[n].writeValue.value = 1u;
-            ++n;
-        }
-        for (int k = 0; k < world; ++k) {
-            if (k == rank) continue;
-            ops[n].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
-            ops[n].waitValue.address = dp(my_flags + base_slot + k);
-            ops[n].waitValue.value = 1u;
-            ops[n].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
-            ++n;
-            ops[n].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
-            ops[n].writeValue.address = dp(my_flags + base_slot + k);
-            ops[n].writeValue.value = 0u;
-            ++n;
-        }
-        if (n == 0) return SEMIPD_OK;
-        const CUresult r = g_batch(cs, (unsigned)n, ops, 0);
-        return r == CUDA_SUCCESS ? SEMIPD_OK : fail("batched flag operations", (int)r);
-    };
     // Flags are binary semaphores (values 0 / 1): a waiter resets its own slot after the wait,
     // so the operations carry no per-call value and a captured CUDA graph replays correctly.
     // Slots [world, 2 world) = "ready", [0, world) = "landed".  The ready handshake orders a
     // peer's next "landed" write after this rank's reset of the previous one (and vice versa).
-    if (semipd_status e = signal_and_wait(world); e != SEMIPD_OK) return e;
+    if (semipd_status e = handshake(cs, peer_flags, my_flags, world, rank, world); e != SEMIPD_OK)
+        return e;
     if (bytes > 0) {
         // push to the peers in ring order starting after this rank, so the ranks' first copies
         // target different destinations
@@ -167,8 +170,21 @@ semipd_status semipd_peer_gather(const void* src, size_t bytes, void* const* dst
             }
         }
     }
-    if (semipd_status e = signal_and_wait(0); e != SEMIPD_OK) return e;
+    if (semipd_status e = handshake(cs, peer_flags, my_flags, world, rank, 0); e != SEMIPD_OK)
+        return e;
     return SEMIPD_OK;
+}
+
+semipd_status semipd_peer_handshake(uint32_t* const* peer_flags, uint32_t* my_flags,
+                                    int32_t world, int32_t rank, int32_t which, semipd_stream_t s) {
+    if (world < 1 || world > SEMIPD_MAX_PEERS || rank < 0 || rank >= world || !peer_flags ||
+        !my_flags || (which != 0 && which != 1))
+        return SEMIPD_ERR_INVALID;
+    for (int k = 0; k < world; ++k)
+        if (!peer_flags[k]) return SEMIPD_ERR_INVALID;
+    if (!load_stream_memops()) return SEMIPD_ERR_UNSUPPORTED;
+    return handshake(reinterpret_cast<CUstream>(s), peer_flags, my_flags, world, rank,
+                     which == 0 ? world : 0);
 }
 
 }  // extern "C"

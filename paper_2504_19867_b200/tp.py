@@ -143,6 +143,23 @@ class PeerGather:
         h = self.full_shape[0] // self.world
         return self.out(buf)[self.rank * h:(self.rank + 1) * h]
 
+    def peer_shard_ptrs(self, buf: int = 0) -> list[int]:
+        """Device addresses of this rank's head slice in every OTHER rank's gathered buffer
+        ``buf`` (for ``KVPool.set_decode_peers``: the decode epilogue stores there)."""
+        off = buf * self.buf_stride + self.rank * self.shard_bytes
+        return [b + off for k, b in enumerate(self.peer_base) if k != self.rank]
+
+    def handshake(self, which: int, stream=None):
+        """``which`` 0 ("ready": every peer is done reading) before a fused-epilogue decode,
+        1 ("landed": every peer's stores are here) after it (C ABI ``semipd_peer_handshake``)."""
+        ct = self._ct
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.calls += which
+        self._check("semipd_peer_handshake", self._lib.semipd_peer_handshake(
+            self._flags, ct.c_void_p(self.base + self.flag_off), self.world, self.rank, int(which),
+            ct.c_void_p(stream.cuda_stream)))
+
     def __call__(self, local: torch.Tensor, buf: int = 0, stream=None) -> torch.Tensor:
         ct = self._ct
         if local.dtype != self.dtype or local.numel() * local.element_size() != self.shard_bytes:

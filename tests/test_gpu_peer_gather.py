@@ -165,3 +165,97 @@ def test_peer_gather_emulated_ranks_one_process(tp):
     from peer_gather_bench import run
     r = run(tp, (16, 129, 64), iters=3)
     assert r["shard_bytes"] == 16 // tp * 129 * 64 * 2
+
+
+def _decode_pool(shape, ctx, case, heads_kv, dev):
+    """A pool holding kv heads [heads_kv) of the cached contexts (harness bit copies)."""
+    from paper_2504_19867_b200 import KVPool, PoolConfig
+    kl, kh = heads_kv
+    bs = shape.block_size
+    nb = [c // bs + 1 for c in ctx]
+    pool = KVPool(PoolConfig(1, sum(nb) + 2, bs, kh - kl, 128, 128, len(ctx), max(nb)), dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    for b, n in enumerate(nb):
+        pool.alloc_blocks(i32([b]), i32([n]))
+    K, V, BT, _ = pool.views(0)
+    bt = BT.cpu()
+    for b, c in enumerate(ctx):
+        pos = torch.arange(c)
+        blk = bt[b].long()[pos // bs].to(dev)
+        K[blk, :, (pos % bs).to(dev)] = case.k_ctx[b][:, kl:kh].to(dev)
+        V[blk, :, (pos % bs).to(dev)] = case.v_ctx[b][:, kl:kh].to(dev)
+    return pool
+
+
+@pytest.mark.parametrize("tpn", [2, 4, 8])
+def test_decode_epilogue_peer_stores_emulated(tpn):
+    """The TP head gather fused into the decode epilogue (semipd_set_decode_peers +
+    semipd_peer_handshake), TP ranks emulated as streams of one process: rank r's decode kernel
+    stores its head slice into every rank's gathered buffer; after the landed handshake each
+    gathered buffer equals the unsharded decode output bitwise.  Twice, to exercise the flag
+    resets and the ready handshake of the second round."""
+    import ctypes
+
+    import synth
+    from paper_2504_19867_b200 import lib, tp
+    dev = torch.device("cuda", 0)
+    shape = synth.AttnShape("llama3-70b", 64, 8, 128, 128, 64, torch.bfloat16)
+    ctx = [300, 2048, 4500, 64]
+    B = len(ctx)
+    cd = synth.decode_case(shape, ctx, seed=3040)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    sc = shape.softmax_scale
+    # unsharded reference run
+    full_pool = _decode_pool(shape, ctx, cd, (0, 8), dev)
+    ref = torch.empty(64, B, 128, dtype=torch.bfloat16, device=dev)
+    full_pool.decode_attn(0, cd.q.to(dev), cd.k_new.to(dev), cd.v_new.to(dev), i32(list(range(B))),
+                          i32(ctx), max(ctx), sc, ref, full_pool.new_decode_workspace(B, 64, max(ctx)),
+                          out_head_major=True)
+    torch.cuda.synchronize()
+    pools, outs, flags, streams, wss = [], [], [], [], []
+    for r in range(tpn):
+        pools.append(_decode_pool(shape, ctx, cd, tp.head_range(8, tpn, r), dev))
+        outs.append(torch.full((64, B, 128), float("nan"), dtype=torch.bfloat16, device=dev))
+        flags.append(torch.zeros(2 * tpn, dtype=torch.int32, device=dev))
+        streams.append(torch.cuda.Stream(dev))
+        wss.append(pools[r].new_decode_workspace(B, 64 // tpn, max(ctx)))
+    hq = 64 // tpn
+    fl = (ctypes.c_void_p * tpn)(*[f.data_ptr() for f in flags])
+    L = lib()
+    # every device input exists before the first handshake: a host-to-device copy issued on a
+    # rank's stream while it waits for a later rank's flag would block this (single) host thread
+    rid, ctx_d = i32(list(range(B))), i32(ctx)
+    ins = []
+    for r in range(tpn):
+        ql, qh = tp.head_range(64, tpn, r)
+        kl, kh = tp.head_range(8, tpn, r)
+        ins.append((cd.q[:, ql:qh].contiguous().to(dev), cd.k_new[:, kl:kh].contiguous().to(dev),
+                    cd.v_new[:, kl:kh].contiguous().to(dev), ql, qh))
+    torch.cuda.synchronize()
+    for rnd in range(2):
+        for o in outs:
+            o.fill_(float("nan"))
+        torch.cuda.synchronize()
+        for r in range(tpn):
+            shard = hq * B * 128 * 2
+            pools[r].set_decode_peers([outs[k].data_ptr() + r * shard for k in range(tpn) if k != r])
+        for r in range(tpn):
+            qs, ks, vs, ql, qh = ins[r]
+            s = streams[r]
+            cs = ctypes.c_void_p(s.cuda_stream)
+            assert L.semipd_peer_handshake(fl, ctypes.c_void_p(flags[r].data_ptr()), tpn, r, 0, cs) == 0
+            # the rank's own slice goes straight into its gathered buffer
+            pools[r].decode_attn(0, qs, ks, vs, rid, ctx_d, max(ctx), sc, outs[r][ql:qh], wss[r],
+                                 out_head_major=True, stream=s)
+            assert L.semipd_peer_handshake(fl, ctypes.c_void_p(flags[r].data_ptr()), tpn, r, 1, cs) == 0
+        torch.cuda.synchronize()
+        for r in range(tpn):
+            assert torch.equal(outs[r].view(torch.int16), ref.view(torch.int16)), (rnd, r)
+        assert all(int(f.abs().sum()) == 0 for f in flags)
+    # peers need head-major output
+    pools[0].set_decode_peers([outs[1].data_ptr()])
+    with pytest.raises(Exception):
+        pools[0].decode_attn(0, ins[0][0], ins[0][1], ins[0][2], rid, ctx_d, max(ctx), sc,
+                             torch.empty(B, hq, 128, dtype=torch.bfloat16, device=dev), wss[0],
+                             out_head_major=False)
+    pools[0].set_decode_peers([])

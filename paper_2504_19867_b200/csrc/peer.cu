@@ -25,37 +25,22 @@
 
 namespace {
 
-typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*PFN_batch)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 
-PFN_wait32 g_wait = nullptr;
-PFN_write32 g_write = nullptr;
 PFN_batch g_batch = nullptr;
 
 bool load_stream_memops() {
-    static bool tried = false, ok = false;
-    if (tried) return ok;
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
     // the _v2 stream memory operations (CUDA >= 11.7) are enabled by default; the v1 ones
-    // need a driver module option, so ask for the CUDA 12.0 ABI explicitly
-    if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 12000, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-        g_wait = reinterpret_cast<PFN_wait32>(p);
-    p = nullptr;
-    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &p, 12000, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-        g_write = reinterpret_cast<PFN_write32>(p);
-    p = nullptr;
-    if (cudaGetDriverEntryPointByVersion("cuStreamBatchMemOp", &p, 12000, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-        g_batch = reinterpret_cast<PFN_batch>(p);
-    ok = g_batch != nullptr;  // g_wait / g_write: single-op forms, kept for probes
+    // need a driver module option, so ask for the CUDA 12.0 ABI explicitly (thread-safe once)
+    static const bool ok = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuStreamBatchMemOp", &p, 12000, cudaEnableDefault,
+                                             &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_batch = reinterpret_cast<PFN_batch>(p);
+        return g_batch != nullptr;
+    }();
     return ok;
 }
 

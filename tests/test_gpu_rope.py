@@ -79,3 +79,41 @@ def test_rope_edge_cases():
     z = torch.randn(3, 2, 72, device=dev).to(torch.bfloat16)
     with pytest.raises(SemipdError):
         rope_(z, None, torch.zeros(3, dtype=torch.int32, device=dev))
+
+
+def test_rope_then_prefill_matches_oracle_chain():
+    """The adjacent step composed with the path: semipd_rope on the chunk's q / k, then
+    semipd_prefill_attn (which writes the rotated k into the pool) equals the oracle's
+    attention over the oracle's rotated q / k (fp64 rotation, fed as fp32), within the bf16
+    bar.  The pool must hold exactly the kernel's rotated k rows."""
+    from harness import compare
+    from paper_2504_19867_b200 import KVPool, PoolConfig
+    dev = torch.device("cuda", 0)
+    C, Hq, Hkv, d, bs = 300, 32, 8, 128, 64
+    g = torch.Generator().manual_seed(21)
+    q = torch.randn(C, Hq, d, generator=g).to(torch.bfloat16)
+    k = torch.randn(C, Hkv, d, generator=g).to(torch.bfloat16)
+    v = torch.randn(C, Hkv, d, generator=g).to(torch.bfloat16)
+    pos = list(range(C))
+    nb = -(-C // bs)
+    pool = KVPool(PoolConfig(1, nb + 1, bs, Hkv, d, d, 1, nb), dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32([0]), i32([nb]))
+    qd, kd, vd = q.to(dev), k.to(dev), v.to(dev)
+    rope_(qd, kd, i32(pos), LLAMA31)
+    out = torch.empty(C, Hq, d, dtype=torch.bfloat16, device=dev)
+    scale = 1.0 / np.sqrt(d)
+    pool.prefill_attn(0, qd, kd, vd, i32([0, C]), i32([0]), i32([0]), C, C, scale, out)
+    torch.cuda.synchronize()
+    K, _, BT, _ = pool.views(0)
+    bt = BT.cpu().numpy()
+    # the pool holds the kernel's rotated k rows bit for bit (a3 after the rotation)
+    posn = np.arange(C)
+    pooled = K.cpu()[torch.from_numpy(bt[0][posn // bs]).long(), :, torch.from_numpy(posn % bs)]
+    assert torch.equal(pooled.view(torch.int16), kd.cpu().view(torch.int16))
+    qr = oracle.rope(synth.bits(q), pos, **_ocfg(LLAMA31)).astype(np.float32)
+    kr = oracle.rope(synth.bits(k), pos, **_ocfg(LLAMA31)).astype(np.float32)
+    kp = np.zeros((nb + 1, Hkv, bs, d), np.float32)
+    vp = np.zeros_like(kp)
+    ref = oracle.prefill(qr, kr, v.float().numpy(), kp, vp, bt, [0, C], [0], [0], scale)
+    compare(out.float().cpu().double().numpy(), ref, torch.bfloat16, "rope + prefill")

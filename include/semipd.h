@@ -278,21 +278,26 @@ semipd_status semipd_peer_handshake(uint32_t* const* peer_flags, uint32_t* my_fl
  * Rotates q [num_tokens][num_q_heads][head_dim] and k [num_tokens][num_kv_heads][head_dim]
  * (device, token-major, contiguous, 16-byte aligned, pool dtype `dtype`) IN PLACE for the
  * token positions positions[num_tokens] (device int32), before the attention call that
- * writes k into the pool.  Half-split pairs (i, i + d/2) (reading R27):
- *   f_i = theta^(-2i/d); if factor > 1, the Llama-3.1 rescaling with wavelength
+ * writes k into the pool.  Only columns [rot_offset, rot_offset + rot_dim) of each row
+ * rotate (Llama: 0, head_dim; the MLA latent row's decoupled rope part: 512, 64); the other
+ * columns are not touched.  With R = rot_dim (reading R27):
+ *   pairs: (i, i + R/2) if interleaved == 0 (Llama / NeoX), (2i, 2i + 1) otherwise
+ *          (GPT-J / DeepSeek), i < R/2;
+ *   f_i = theta^(-2i/R); if factor > 1, the Llama-3.1 rescaling with wavelength
  *   w_i = 2 pi / f_i and L0 = original_max_pos: w_i < L0/high_freq_factor -> f_i;
  *   w_i > L0/low_freq_factor -> f_i / factor; otherwise (1-a) f_i / factor + a f_i with
  *   a = (L0 / w_i - low_freq_factor) / (high_freq_factor - low_freq_factor);
- *   phi = pos * f_i;  x_i' = x_i cos phi - x_{i+d/2} sin phi;
- *   x_{i+d/2}' = x_{i+d/2} cos phi + x_i sin phi.
+ *   phi = pos * f_i;  (x, y) of pair i -> (x cos phi - y sin phi, y cos phi + x sin phi).
  * The frequencies, the angle and its sine / cosine are formed in fp64, the rotation in fp32.
  * factor <= 1 disables the rescaling (plain RoPE).  q (k) may be NULL when its head count is
- * 0.  Errors: INVALID (negative sizes, odd head_dim, theta <= 1, bad scaling parameters,
- * NULL), UNSUPPORTED (head_dim/2 not a multiple of 8 (bf16) / 4 (fp32), head_dim > 256,
- * misaligned rows), CUDA.  num_tokens == 0 is a no-op. */
+ * 0.  Errors: INVALID (negative sizes, odd / empty rot_dim, range outside the row,
+ * theta <= 1, bad scaling parameters, NULL), UNSUPPORTED (head_dim, rot_offset or the
+ * per-vector span (R/2 half-split, R interleaved) not a multiple of 8 (bf16) / 4 (fp32)
+ * elements, R > 256, misaligned rows), CUDA.  num_tokens == 0 is a no-op. */
 semipd_status semipd_rope(void* q, void* k, const int32_t* positions, int32_t num_tokens,
                           int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
-                          int32_t dtype, double theta, double factor, double low_freq_factor,
+                          int32_t rot_offset, int32_t rot_dim, int32_t interleaved, int32_t dtype,
+                          double theta, double factor, double low_freq_factor,
                           double high_freq_factor, int32_t original_max_pos, semipd_stream_t s);
 
 /* Library version string (host, static). */

@@ -68,7 +68,7 @@ def lib():
             L.semipd_ref_blocks_for_tokens.argtypes = [i, i]
             L.semipd_ref_rope_inv_freq.argtypes = [i, d, d, d, d, d, dp]
             L.semipd_ref_rope_inv_freq.restype = None
-            L.semipd_ref_rope.argtypes = [i, i, i, vp, i, vp, d, d, d, d, d, dp]
+            L.semipd_ref_rope.argtypes = [i, i, i, i, i, i, vp, i, vp, d, d, d, d, d, dp]
             L.semipd_ref_rope.restype = None
             _ = ip
             _lib = L
@@ -257,13 +257,15 @@ def rope_inv_freq(d: int, theta: float, factor: float = 0.0, lf: float = 1.0, hf
 
 
 def rope(x, positions, theta: float, factor: float = 0.0, lf: float = 1.0, hf: float = 4.0,
-         L0: float = 8192.0) -> np.ndarray:
-    """Rotate x [T, H, d] (bf16 bits as uint16, or float32) at positions [T]; returns fp64
-    [T, H, d] (half-split pairs, DESIGN R27)."""
+         L0: float = 8192.0, off: int = 0, rd: int | None = None,
+         interleaved: bool = False) -> np.ndarray:
+    """Rotate columns [off, off + rd) of x [T, H, d] (bf16 bits as uint16, or float32) at
+    positions [T]; returns fp64 [T, H, d] (half-split or interleaved pairs, DESIGN R27)."""
     x = _c(x)
     T, H, d = x.shape
     pos = np.ascontiguousarray(positions, dtype=np.int32)
     out = np.zeros((T, H, d), np.float64)
-    lib().semipd_ref_rope(T, H, d, _p(x), _dtype_code(x), _p(pos), theta, factor, lf, hf, L0,
-                          _p(out))
+    rd = d - off if rd is None else rd
+    lib().semipd_ref_rope(T, H, d, off, rd, int(bool(interleaved)), _p(x), _dtype_code(x), _p(pos),
+                          theta, factor, lf, hf, L0, _p(out))
     return out

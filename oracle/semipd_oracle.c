@@ -473,21 +473,26 @@ void semipd_ref_rope_inv_freq(int d, double theta, double factor, double lf, dou
     }
 }
 
-/* semipd_ref_rope: x [T][H][d] (stored dtype, widened exactly) -> out [T][H][d] fp64:
- *   phi = pos_t * f_i;  out_i = x_i cos phi - x_{i+d/2} sin phi;
- *                       out_{i+d/2} = x_{i+d/2} cos phi + x_i sin phi. */
-void semipd_ref_rope(int T, int H, int d, const void* x, int dtype, const int* pos, double theta,
-                     double factor, double lf, double hf, double L0, double* out) {
-    double* f = (double*)malloc(sizeof(double) * (size_t)(d / 2));
-    semipd_ref_rope_inv_freq(d, theta, factor, lf, hf, L0, f);
+/* semipd_ref_rope: x [T][H][d] (stored dtype, widened exactly) -> out [T][H][d] fp64.
+ * Columns outside [off, off + rd) are copied.  Pair i (i < rd/2) is (off + i, off + rd/2 + i)
+ * (half-split) or (off + 2i, off + 2i + 1) (interleaved); with f = inv_freq(rd):
+ *   phi = pos_t * f_i;  (x, y) -> (x cos phi - y sin phi, y cos phi + x sin phi). */
+void semipd_ref_rope(int T, int H, int d, int off, int rd, int inter, const void* x, int dtype,
+                     const int* pos, double theta, double factor, double lf, double hf, double L0,
+                     double* out) {
+    double* f = (double*)malloc(sizeof(double) * (size_t)(rd / 2));
+    semipd_ref_rope_inv_freq(rd, theta, factor, lf, hf, L0, f);
     for (int t = 0; t < T; ++t)
         for (int h = 0; h < H; ++h) {
             size_t row = ((size_t)t * H + h) * d;
-            for (int i = 0; i < d / 2; ++i) {
+            for (int c = 0; c < d; ++c) out[row + c] = ld(x, row + c, dtype);
+            for (int i = 0; i < rd / 2; ++i) {
+                size_t ix = row + off + (inter ? 2 * i : i);
+                size_t iy = row + off + (inter ? 2 * i + 1 : rd / 2 + i);
                 double phi = (double)pos[t] * f[i];
-                double x0 = ld(x, row + i, dtype), x1 = ld(x, row + d / 2 + i, dtype);
-                out[row + i] = x0 * cos(phi) - x1 * sin(phi);
-                out[row + d / 2 + i] = x1 * cos(phi) + x0 * sin(phi);
+                double x0 = ld(x, ix, dtype), x1 = ld(x, iy, dtype);
+                out[ix] = x0 * cos(phi) - x1 * sin(phi);
+                out[iy] = x1 * cos(phi) + x0 * sin(phi);
             }
         }
     free(f);

@@ -88,8 +88,8 @@ def lib():
                 "semipd_peer_gather": (i32, [vp, sz, P(vp), P(vp), vp, i32, i32, vp]),
                 "semipd_set_decode_peers": (i32, [vp, P(vp), i32]),
                 "semipd_peer_handshake": (i32, [P(vp), vp, i32, i32, i32, vp]),
-                "semipd_rope": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, f64, f64, f64, f64,
-                                      i32, vp]),
+                "semipd_rope": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, f64,
+                                      f64, f64, f64, i32, vp]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -132,9 +132,11 @@ class RopeConfig:
     original_max_pos: int = 8192
 
 
-def rope_(q, k, positions, cfg: RopeConfig | None = None, stream=None):
-    """Rotate q [T, Hq, d] and k [T, Hkv, d] in place at int32 positions [T] (C ABI
-    ``semipd_rope``; runs in the library's kernel)."""
+def rope_(q, k, positions, cfg: RopeConfig | None = None, stream=None, rot_offset: int = 0,
+          rot_dim: int | None = None, interleaved: bool = False):
+    """Rotate columns [rot_offset, rot_offset + rot_dim) of q [T, Hq, d] and k [T, Hkv, d] in
+    place at int32 positions [T]; half-split pairs, or adjacent pairs if ``interleaved``
+    (C ABI ``semipd_rope``; runs in the library's kernel)."""
     cfg = cfg or RopeConfig()
     t = q if q is not None else k
     dt = BF16 if t.dtype == torch.bfloat16 else FP32 if t.dtype == torch.float32 else None
@@ -145,7 +147,9 @@ def rope_(q, k, positions, cfg: RopeConfig | None = None, stream=None):
             raise SemipdError("semipd_rope", INVALID)
     _check("semipd_rope", lib().semipd_rope(
         _ptr(q), _ptr(k), _ptr(positions), int(t.shape[0]), 0 if q is None else int(q.shape[1]),
-        0 if k is None else int(k.shape[1]), int(t.shape[2]), dt, float(cfg.theta),
+        0 if k is None else int(k.shape[1]), int(t.shape[2]), int(rot_offset),
+        int(t.shape[2] - rot_offset if rot_dim is None else rot_dim), int(bool(interleaved)), dt,
+        float(cfg.theta),
         float(cfg.factor), float(cfg.low_freq_factor), float(cfg.high_freq_factor),
         int(cfg.original_max_pos), _stream(stream)))
     return q, k

@@ -3,8 +3,10 @@
 // the step's new q / k rows before the attention call that writes k into the pool (a3 / a5),
 // so the pool holds rotated keys, as in Llama.
 //
-// Definition (reading R27): half-split pairs (i, i + d/2), i < d/2,
-//   f_i   = theta^(-2i/d), rescaled by the Llama-3.1 rule when factor > 1:
+// Definition (reading R27) over the rotated columns [off, off + rd) of each row (the
+// whole head for Llama; the 64 decoupled-rope columns of a 576-d MLA row): half-split pairs
+// (i, i + rd/2), i < rd/2 (Llama), or interleaved pairs (2i, 2i + 1) (GPT-J / DeepSeek layout),
+//   f_i   = theta^(-2i/rd), rescaled by the Llama-3.1 rule when factor > 1:
 //           wavelength w_i = 2 pi / f_i; w_i < L0/hf: f_i;  w_i > L0/lf: f_i / factor;
 //           else (1 - a) f_i / factor + a f_i with a = (L0 / w_i - lf) / (hf - lf)
 //   phi   = pos * f_i
@@ -31,7 +33,7 @@ struct RopeParams {
     unsigned char* q;
     unsigned char* k;
     const int* pos;
-    int Hq, Hkv, d;
+    int Hq, Hkv, d, off, rd;  // row length, rotated columns [off, off + rd)
     double inv_freq[MAX_HALF];  // f_i in fp64, formed once per call on the host
 };
 
@@ -47,27 +49,33 @@ double rope_inv_freq(int i, int d, double theta, double factor, double lf, doubl
     return (1.0 - a) * f / factor + a * f;
 }
 
-template <typename T>
+template <typename T, bool INTER>
 __global__ void __launch_bounds__(512) rope_kernel(const __grid_constant__ RopeParams p) {
     constexpr int VEC = 16 / sizeof(T);  // elements per 16-byte vector
-    extern __shared__ float cs[];         // [d/2] cos, [d/2] sin
+    extern __shared__ float cs[];         // [rd/2] cos, [rd/2] sin
     const int t = blockIdx.x;
-    const int half = p.d >> 1;
-    const int vph = half / VEC;  // vectors per half head
+    const int half = p.rd >> 1;
+    // half-split: a vector of x_i and the matching vector of x_{i+rd/2};
+    // interleaved: one vector of VEC/2 adjacent pairs (x_2i, x_2i+1)
+    const int vph = (INTER ? p.rd : half) / VEC;  // vectors per head
     const int nvec = (p.Hq + p.Hkv) * vph;
-    // this thread's first pair of vectors is loaded before the angles are formed, so the HBM
+    auto row_of = [&](int v, int& i0) {
+        const int h = v / vph;
+        i0 = (v % vph) * VEC;
+        T* row = h < p.Hq ? reinterpret_cast<T*>(p.q) + ((size_t)t * p.Hq + h) * p.d
+                          : reinterpret_cast<T*>(p.k) + ((size_t)t * p.Hkv + (h - p.Hq)) * p.d;
+        return row + p.off;
+    };
+    // this thread's first vectors are loaded before the angles are formed, so the HBM
     // latency overlaps the fp64 sincos
     const int v0 = threadIdx.x;
     T* row0 = nullptr;
     uint4 a0 = make_uint4(0, 0, 0, 0), b0 = a0;
     int i00 = 0;
     if (v0 < nvec) {
-        const int h = v0 / vph;
-        i00 = (v0 % vph) * VEC;
-        row0 = h < p.Hq ? reinterpret_cast<T*>(p.q) + ((size_t)t * p.Hq + h) * p.d
-                        : reinterpret_cast<T*>(p.k) + ((size_t)t * p.Hkv + (h - p.Hq)) * p.d;
+        row0 = row_of(v0, i00);
         a0 = __ldcs(reinterpret_cast<const uint4*>(row0 + i00));
-        b0 = __ldcs(reinterpret_cast<const uint4*>(row0 + half + i00));
+        if (!INTER) b0 = __ldcs(reinterpret_cast<const uint4*>(row0 + half + i00));
     }
     const double pos = (double)__ldg(p.pos + t);
     for (int i = threadIdx.x; i < half; i += blockDim.x) {
@@ -77,6 +85,17 @@ __global__ void __launch_bounds__(512) rope_kernel(const __grid_constant__ RopeP
         cs[half + i] = (float)s;
     }
     __syncthreads();
+    auto rot = [](T& e0, T& e1, float c, float s) {
+        if constexpr (sizeof(T) == 2) {
+            const float x0 = __bfloat162float(e0), x1 = __bfloat162float(e1);
+            e0 = __float2bfloat16_rn(fmaf(x0, c, -x1 * s));
+            e1 = __float2bfloat16_rn(fmaf(x1, c, x0 * s));
+        } else {
+            const float x0 = e0, x1 = e1;
+            e0 = fmaf(x0, c, -x1 * s);
+            e1 = fmaf(x1, c, x0 * s);
+        }
+    };
     for (int v = v0; v < nvec; v += blockDim.x) {
         T* row;
         int i0;
@@ -84,33 +103,25 @@ __global__ void __launch_bounds__(512) rope_kernel(const __grid_constant__ RopeP
         if (v == v0) {
             row = row0, i0 = i00, a = a0, b = b0;
         } else {
-            const int h = v / vph;
-            i0 = (v % vph) * VEC;
-            row = h < p.Hq ? reinterpret_cast<T*>(p.q) + ((size_t)t * p.Hq + h) * p.d
-                           : reinterpret_cast<T*>(p.k) + ((size_t)t * p.Hkv + (h - p.Hq)) * p.d;
+            row = row_of(v, i0);
             a = __ldcs(reinterpret_cast<const uint4*>(row + i0));
-            b = __ldcs(reinterpret_cast<const uint4*>(row + half + i0));
+            if (!INTER) b = __ldcs(reinterpret_cast<const uint4*>(row + half + i0));
         }
         T* xa = reinterpret_cast<T*>(&a);
-        T* xb = reinterpret_cast<T*>(&b);
+        if constexpr (INTER) {
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-            const float c = cs[i0 + j], s = cs[half + i0 + j];
-            float x0, x1;
-            if constexpr (sizeof(T) == 2) {
-                x0 = __bfloat162float(xa[j]);
-                x1 = __bfloat162float(xb[j]);
-                xa[j] = __float2bfloat16_rn(fmaf(x0, c, -x1 * s));
-                xb[j] = __float2bfloat16_rn(fmaf(x1, c, x0 * s));
-            } else {
-                x0 = xa[j];
-                x1 = xb[j];
-                xa[j] = fmaf(x0, c, -x1 * s);
-                xb[j] = fmaf(x1, c, x0 * s);
+            for (int j = 0; j < VEC / 2; ++j) {
+                const int fi = (i0 >> 1) + j;
+                rot(xa[2 * j], xa[2 * j + 1], cs[fi], cs[half + fi]);
             }
+            __stcs(reinterpret_cast<uint4*>(row + i0), a);
+        } else {
+            T* xb = reinterpret_cast<T*>(&b);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) rot(xa[j], xb[j], cs[i0 + j], cs[half + i0 + j]);
+            __stcs(reinterpret_cast<uint4*>(row + i0), a);
+            __stcs(reinterpret_cast<uint4*>(row + half + i0), b);
         }
-        __stcs(reinterpret_cast<uint4*>(row + i0), a);
-        __stcs(reinterpret_cast<uint4*>(row + half + i0), b);
     }
 }
 
@@ -118,11 +129,13 @@ __global__ void __launch_bounds__(512) rope_kernel(const __grid_constant__ RopeP
 
 extern "C" semipd_status semipd_rope(void* q, void* k, const int32_t* positions,
                                      int32_t num_tokens, int32_t num_q_heads, int32_t num_kv_heads,
-                                     int32_t head_dim, int32_t dtype, double theta, double factor,
+                                     int32_t head_dim, int32_t rot_offset, int32_t rot_dim,
+                                     int32_t interleaved, int32_t dtype, double theta, double factor,
                                      double low_freq_factor, double high_freq_factor,
                                      int32_t original_max_pos, semipd_stream_t s) {
-    if (num_tokens < 0 || num_q_heads < 0 || num_kv_heads < 0 || head_dim <= 0 || head_dim % 2 ||
-        !(theta > 1.0) || (dtype != SEMIPD_BF16 && dtype != SEMIPD_FP32))
+    if (num_tokens < 0 || num_q_heads < 0 || num_kv_heads < 0 || head_dim <= 0 || rot_offset < 0 ||
+        rot_dim <= 0 || rot_dim % 2 || rot_offset + rot_dim > head_dim || !(theta > 1.0) ||
+        (dtype != SEMIPD_BF16 && dtype != SEMIPD_FP32))
         return SEMIPD_ERR_INVALID;
     if (factor > 1.0 && (!(high_freq_factor > low_freq_factor) || !(low_freq_factor > 0.0) ||
                          original_max_pos <= 0))
@@ -130,8 +143,9 @@ extern "C" semipd_status semipd_rope(void* q, void* k, const int32_t* positions,
     if (num_tokens == 0 || num_q_heads + num_kv_heads == 0) return SEMIPD_OK;
     if ((num_q_heads > 0 && !q) || (num_kv_heads > 0 && !k) || !positions) return SEMIPD_ERR_INVALID;
     const int vec = dtype == SEMIPD_BF16 ? 8 : 4;
-    const int half = head_dim / 2;
-    if (half % vec || half > MAX_HALF) return SEMIPD_ERR_UNSUPPORTED;
+    const int half = rot_dim / 2;
+    if ((interleaved ? rot_dim : half) % vec || rot_offset % vec || head_dim % vec || half > MAX_HALF)
+        return SEMIPD_ERR_UNSUPPORTED;
     if ((q && reinterpret_cast<uintptr_t>(q) % 16) || (k && reinterpret_cast<uintptr_t>(k) % 16))
         return SEMIPD_ERR_UNSUPPORTED;
     RopeParams p;
@@ -141,18 +155,22 @@ extern "C" semipd_status semipd_rope(void* q, void* k, const int32_t* positions,
     p.Hq = num_q_heads;
     p.Hkv = num_kv_heads;
     p.d = head_dim;
+    p.off = rot_offset;
+    p.rd = rot_dim;
     for (int i = 0; i < half; ++i)
-        p.inv_freq[i] = rope_inv_freq(i, head_dim, theta, factor, low_freq_factor, high_freq_factor,
+        p.inv_freq[i] = rope_inv_freq(i, rot_dim, theta, factor, low_freq_factor, high_freq_factor,
                                       (double)original_max_pos);
-    const int nvec = (num_q_heads + num_kv_heads) * (half / vec);
+    const int nvec = (num_q_heads + num_kv_heads) * ((interleaved ? rot_dim : half) / vec);
     int threads = ((nvec + 31) / 32) * 32;
     if (threads > 512) threads = 512;
     if (threads < 64) threads = 64;
-    const size_t smem = (size_t)head_dim * sizeof(float);
+    const size_t smem = (size_t)rot_dim * sizeof(float);
     cudaStream_t st = static_cast<cudaStream_t>(s);
     if (dtype == SEMIPD_BF16)
-        rope_kernel<__nv_bfloat16><<<num_tokens, threads, smem, st>>>(p);
+        interleaved ? rope_kernel<__nv_bfloat16, true><<<num_tokens, threads, smem, st>>>(p)
+                    : rope_kernel<__nv_bfloat16, false><<<num_tokens, threads, smem, st>>>(p);
     else
-        rope_kernel<float><<<num_tokens, threads, smem, st>>>(p);
+        interleaved ? rope_kernel<float, true><<<num_tokens, threads, smem, st>>>(p)
+                    : rope_kernel<float, false><<<num_tokens, threads, smem, st>>>(p);
     return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }

@@ -117,3 +117,27 @@ def test_rope_then_prefill_matches_oracle_chain():
     vp = np.zeros_like(kp)
     ref = oracle.prefill(qr, kr, v.float().numpy(), kp, vp, bt, [0, C], [0], [0], scale)
     compare(out.float().cpu().double().numpy(), ref, torch.bfloat16, "rope + prefill")
+
+
+@pytest.mark.parametrize("inter", [True, False], ids=["interleaved", "half_split"])
+def test_rope_mla_latent_rows_sub_range(inter):
+    """DeepSeek-V2-Lite MLA rows (cfg 5): q [T, 16, 576] and the latent k [T, 1, 576]; only
+    the 64 decoupled-rope columns at 512 rotate (interleaved pairs, as DeepSeek lays them out);
+    the 512 latent columns stay bit-identical."""
+    dev = torch.device("cuda", 0)
+    T = 129
+    g = torch.Generator().manual_seed(15)
+    q = torch.randn(T, 16, 576, generator=g).to(torch.bfloat16)
+    k = torch.randn(T, 1, 576, generator=g).to(torch.bfloat16)
+    pos = list(range(1000, 1000 + T))
+    qd, kd = q.to(dev), k.to(dev)
+    cfg = RopeConfig(theta=10000.0, factor=0.0)
+    rope_(qd, kd, torch.tensor(pos, dtype=torch.int32, device=dev), cfg, rot_offset=512,
+          rot_dim=64, interleaved=inter)
+    torch.cuda.synchronize()
+    for got, x in ((qd.cpu(), q), (kd.cpu(), k)):
+        assert torch.equal(got[..., :512].view(torch.int16), x[..., :512].view(torch.int16))
+        ref = oracle.rope(synth.bits(x), pos, **_ocfg(cfg), off=512, rd=64, interleaved=inter)
+        diff = np.abs(got.double().numpy() - ref)
+        assert diff.max() <= 2e-2
+        assert np.linalg.norm(got.double().numpy() - ref) / np.linalg.norm(ref) <= 1e-2

@@ -96,3 +96,27 @@ def test_llama31_rescaling_shape():
     assert np.max(np.abs(A @ coef - r[mid])) < 1e-12
     np.testing.assert_allclose(coef[0] * (4.0 / 8192.0) + coef[1], 1.0, rtol=1e-9)
     np.testing.assert_allclose(coef[0] * (1.0 / 8192.0) + coef[1], 1.0 / 8.0, rtol=1e-9)
+
+
+def test_interleaved_equals_complex_multiplication_on_adjacent_pairs():
+    T, H, d = 4, 2, 64
+    x = _x(T, H, d, 6)
+    pos = np.array([0, 3, 900, 77777])
+    out = oracle.rope(x, pos, theta=10000.0, interleaved=True)
+    f = oracle.rope_inv_freq(d, 10000.0)
+    z = x[..., 0::2].astype(np.float64) + 1j * x[..., 1::2].astype(np.float64)
+    zr = z * np.exp(1j * pos[:, None, None] * f[None, None, :])
+    np.testing.assert_allclose(out[..., 0::2], zr.real, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(out[..., 1::2], zr.imag, rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("inter", [False, True])
+def test_sub_range_rotates_only_its_columns(inter):
+    """An MLA latent row: only the 64 rope columns at 512 rotate, exactly as a stand-alone
+    64-wide rotation of those columns; the 512 latent columns pass through bit for bit."""
+    x = _x(3, 2, 576, 7)
+    pos = [5, 600, 40000]
+    out = oracle.rope(x, pos, theta=10000.0, off=512, rd=64, interleaved=inter)
+    assert np.array_equal(out[..., :512], x[..., :512].astype(np.float64))
+    alone = oracle.rope(np.ascontiguousarray(x[..., 512:]), pos, theta=10000.0, interleaved=inter)
+    np.testing.assert_array_equal(out[..., 512:], alone)

@@ -63,8 +63,8 @@ def parse():
     ap.add_argument("--gather", default="nccl", choices=["nccl", "peer", "fused"],
                     help="TP head all-gather: NCCL all_gather (CTAs); peer = copy-engine pushes "
                          "over IPC-mapped peer memory with stream-memop flags (no SMs); fused = "
-                         "decode stores its output into the peers' buffers from its epilogue "
-                         "(prefill as peer)")
+                         "both kernels store their output into the peers' buffers from the "
+                         "epilogue")
     ap.add_argument("--peer-graph", action="store_true",
                     help="N > 1 with --gather peer: replay the co-run step as a CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
@@ -243,7 +243,7 @@ class Workload:
         self.sD = torch.cuda.Stream(device=dev)
         self.pg_p = self.pg_d = None
         self.peer_p = self.peer_d = None
-        self.fused_d = False
+        self.fused_d = self.fused_p = False
         self.gath_p = self.gath_d = None
         if tp > 1:
             from paper_2504_19867_b200 import tp as tpmod
@@ -255,10 +255,12 @@ class Workload:
             if gather in ("peer", "fused"):  # copy engines + stream memops instead of NCCL CTAs
                 self.peer_p = tpmod.PeerGather(self.gath_p.shape, s.dtype, self.pg_p, dev)
                 self.peer_d = tpmod.PeerGather(self.gath_d.shape, s.dtype, self.pg_d, dev)
-            if gather == "fused":  # decode epilogue stores straight into every rank's buffer
-                self.fused_d = True
+            if gather == "fused":  # both epilogues store straight into every rank's buffer
+                self.fused_d = self.fused_p = True
                 self.pool.set_decode_peers(self.peer_d.peer_shard_ptrs())
                 self.od = [self.peer_d.local_view() for _ in range(self.L)]
+                self.pool.set_prefill_peers(self.peer_p.peer_shard_ptrs())
+                self.op = [self.peer_p.local_view() for _ in range(self.L)]
         # per-launch timing events (decode kernel on stream D, prefill call on stream P)
         self.ev_d = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                      for _ in range(self.L)]
@@ -289,8 +291,14 @@ class Workload:
 
     # TP > 1: the head all-gather of layer l's head-major output on the phase stream s
     # (one communicator per phase); a no-op at TP = 1
+    def pre_p(self, l, s):  # fused gather: every peer is done reading before the stores
+        if self.fused_p:
+            self.peer_p.handshake(0, stream=s)
+
     def gather_p(self, l, s):
-        if self.tp > 1:
+        if self.fused_p:  # the kernel already stored; wait until every peer's stores landed
+            self.peer_p.handshake(1, stream=s)
+        elif self.tp > 1:
             from paper_2504_19867_b200 import tp as tpmod
             if self.peer_p is not None:
                 self.peer_p(self.op[l], stream=s)
@@ -317,6 +325,7 @@ class Workload:
         with torch.cuda.stream(s):
             p.alloc_blocks(self.rid_pre, self.nblk_pre, None, stream=s)
             for l in range(self.L):
+                self.pre_p(l, s)
                 if timed:
                     self.ev_p[l][0].record(s)
                 p.prefill_attn(l, self.qp[l], self.kp[l], self.vp[l], self.cu, self.rid_pre,
@@ -437,6 +446,7 @@ class E2E:
             w.pool.alloc_blocks(w.rid_pre, w.nblk_pre, None, stream=w.sP)
             for l in range(w.L):
                 w.sP.wait_event(self.in_p[l])
+                w.pre_p(l, w.sP)
                 w.pool.prefill_attn(l, w.qp[l], w.kp[l], w.vp[l], w.cu, w.rid_pre, w.prefix, w.C,
                                     w.C, w.scale, w.op[l], out_head_major=w.tp > 1, stream=w.sP)
                 w.gather_p(l, w.sP)  # TP > 1: same exchange step as the device-timed path
@@ -525,7 +535,7 @@ def workload_config(shape: synth.AttnShape, ws: int, gather: str = "nccl") -> di
                         f"ctx={DECODE_CTX} + prefill chunk {PREFILL_TOKENS} (P=0), co-run",
             "parallelism": (f"tp{ws} (KV-head shards, "
                             + {"peer": "copy-engine peer all-gather)",
-                               "fused": "decode-epilogue peer stores + copy-engine prefill gather)"}
+                               "fused": "peer stores from the decode / prefill epilogues)"}
                             .get(gather, "NCCL all-gather)")
                             if ws > 1 else "tp1"),
             "l2": f"no flush: per-step decode working set {decode_gb:.1f} GB >> 126 MB L2"}

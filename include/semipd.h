@@ -270,6 +270,10 @@ semipd_status semipd_peer_gather(const void* src, size_t bytes, void* const* dst
  * semipd_peer_handshake: one of the two handshakes semipd_peer_gather performs (flag arrays
  * as there; which: 0 = ready, 1 = landed), as one batched stream-memory-operation call. */
 semipd_status semipd_set_decode_peers(semipd_pool_t pool, void* const* peer_out, int32_t n);
+/* The same for semipd_prefill_attn (tcgen05 GQA path only; 16-byte aligned pointers): full
+ * output tiles then take the direct 16-byte-store epilogue instead of the TMA store, and
+ * every output vector also goes to each peer. */
+semipd_status semipd_set_prefill_peers(semipd_pool_t pool, void* const* peer_out, int32_t n);
 semipd_status semipd_peer_handshake(uint32_t* const* peer_flags, uint32_t* my_flags,
                                     int32_t world, int32_t rank, int32_t which, semipd_stream_t s);
 

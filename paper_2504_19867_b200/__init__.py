@@ -87,6 +87,7 @@ def lib():
                 "semipd_ipc_close": (i32, [vp]),
                 "semipd_peer_gather": (i32, [vp, sz, P(vp), P(vp), vp, i32, i32, vp]),
                 "semipd_set_decode_peers": (i32, [vp, P(vp), i32]),
+                "semipd_set_prefill_peers": (i32, [vp, P(vp), i32]),
                 "semipd_peer_handshake": (i32, [P(vp), vp, i32, i32, i32, vp]),
                 "semipd_rope": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, f64,
                                       f64, f64, f64, i32, vp]),
@@ -281,6 +282,12 @@ class KVPool:
         ``tp.PeerGather.peer_shard_ptrs`` gives them).  [] clears."""
         arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[int(x) for x in peer_ptrs])
         _check("semipd_set_decode_peers", lib().semipd_set_decode_peers(self.h, arr, len(peer_ptrs)))
+
+    def set_prefill_peers(self, peer_ptrs):
+        """Fuse the TP head all-gather into the prefill epilogue (C ABI
+        ``semipd_set_prefill_peers``); [] clears."""
+        arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[int(x) for x in peer_ptrs])
+        _check("semipd_set_prefill_peers", lib().semipd_set_prefill_peers(self.h, arr, len(peer_ptrs)))
 
     def launch_count(self) -> int:
         return int(lib().semipd_launch_count(self.h))

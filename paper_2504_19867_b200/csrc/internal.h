@@ -51,6 +51,8 @@ struct semipd_pool {
     // decode epilogue peer stores (semipd_set_decode_peers; TP gather fused into the kernel)
     void* dec_peers[SEMIPD_MAX_PEERS - 1] = {};
     int dec_n_peers = 0;
+    void* pre_peers[SEMIPD_MAX_PEERS - 1] = {};  // semipd_set_prefill_peers
+    int pre_n_peers = 0;
     // MLA latent pool (kv_shared): 4-D (64 cols, rows, dk/64 blocks, pages), box 32 rows x all
     // column blocks (one 36 KiB TMA per 32-key stage at dk = 576)
     std::vector<CUtensorMap> mla_kmap;

@@ -72,6 +72,11 @@ struct PrefillParams {
     int* status;
     unsigned* sched;
     int n, T, Hq, Hkv, G, TQ, pairs_max, n_units, lg_bs, box_rows, MBR, N_B, out_head_major;
+    // TP head all-gather fused into the epilogue: full tiles take the direct
+    // 16-byte-store epilogue and every output vector also goes to each peer's gathered buffer
+    // (peer-mapped, offset to this rank's head slice)
+    __nv_bfloat16* peers[SEMIPD_MAX_PEERS - 1];
+    int n_peers;
     const uint4* k_new;     // chunk K / V rows [T][Hkv][128] (fused pool write, warp 3)
     const uint4* v_new;
     unsigned char* k_pool;  // this layer's K / V pages
@@ -179,6 +184,7 @@ constexpr int kPreL2 = SPD_PRE_L2;
 #endif
 constexpr bool kEpiDirect = SPD_EPI_DIRECT != 0;
 
+
 // MMA issue from the whole converged warp (elect.sync inside the asm: descriptors stay in
 // uniform registers, ~2x the issue rate of a lane-0 branch) or from lane 0
 #ifndef SPD_MMA_WARP
@@ -199,6 +205,10 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t addr) {
     return umma_desc_sw128(addr, 16, 1024);
 }
 
+// PEERS: the epilogue also stores every output vector to the peers' gathered buffers (the
+// fused TP gather).  A separate instantiation, because compiling the peer stores into the
+// one kernel cost the plain path 1-3 % (measured A/B, scripts/gpu_prefill_ab.sh)
+template <bool PEERS>
 __global__ void __launch_bounds__(NT, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap,
                       const __grid_constant__ CUtensorMap kmap,
@@ -725,7 +735,25 @@ __global__ void __launch_bounds__(NT, 1)
                     }
                     fence_proxy_async_smem();
                     named_bar_sync(2 + t, 128);
-                    if (issuer) {
+                    if (PEERS && p.n_peers > 0) {
+                        // fused TP gather (head-major only): the 128 threads copy the staged
+                        // half out with 16-byte stores, to the local output and to every peer
+                        // (the next half's barrier keeps the staging until all have read it)
+                        unsigned char* outb = reinterpret_cast<unsigned char*>(p.out);
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            const int row = it * 16 + (r >> 3), c = r & 7;
+                            const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((c ^ (row & 7)) << 4));
+                            const int rt = d.qrow0 + t * p.TQ + row % p.TQ;
+                            const int rh = d.g * p.G + row / p.TQ;
+                            const size_t bo = ((size_t)rh * p.T + rt) * (HD * 2) + hh * 128 + c * 16;
+                            *reinterpret_cast<uint4*>(outb + bo) = v;
+#pragma unroll
+                            for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k)
+                                if (k < p.n_peers)
+                                    *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(p.peers[k]) + bo) = v;
+                        }
+                    } else if (issuer) {
                         if (p.out_head_major)
                             tma_store_3d(&omap, stg, hh * 64, d.qrow0 + t * p.TQ, d.g * p.G);
                         else
@@ -756,6 +784,12 @@ __global__ void __launch_bounds__(NT, 1)
                             v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
                             v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
                             *reinterpret_cast<uint4*>(dst + c * 32 + e) = v;
+                            if (PEERS) {
+#pragma unroll
+                                for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k)
+                                    if (k < p.n_peers)
+                                        *reinterpret_cast<uint4*>(p.peers[k] + (dst - p.out) + c * 32 + e) = v;
+                            }
                         }
                     }
                 }
@@ -826,6 +860,10 @@ extern "C" semipd_status semipd_prefill_attn(
         !out)
         return SEMIPD_ERR_INVALID;
     const int budget = spd_resolve_budget(pool, sm_budget, true);
+    if (pool->pre_n_peers > 0 && !out_head_major) return SEMIPD_ERR_INVALID;
+    if (pool->pre_n_peers > 0 &&
+        (!fast_path_ok(pool, num_q_heads) || spd_mla_prefill_ok(pool, num_q_heads)))
+        return SEMIPD_ERR_UNSUPPORTED;
     if (!fast_path_ok(pool, num_q_heads) || spd_mla_prefill_ok(pool, num_q_heads)) {
         // K/V write into the pool, stream-ordered before attention reads it (these
         // paths read the chunk's own keys from the pool); the tcgen05 path fuses it
@@ -850,6 +888,9 @@ extern "C" semipd_status semipd_prefill_attn(
     prm.prefix = prefix_lens;
     prm.bt = pool->bt;
     prm.out = static_cast<__nv_bfloat16*>(out);
+    prm.n_peers = pool->pre_n_peers;
+    for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k)
+        prm.peers[k] = k < pool->pre_n_peers ? static_cast<__nv_bfloat16*>(pool->pre_peers[k]) : nullptr;
     prm.status = status_dev;
     prm.sched = &pool->st->sched[0];
     prm.n = n;
@@ -919,15 +960,31 @@ extern "C" semipd_status semipd_prefill_attn(
     const size_t smem = sizeof(Smem) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(prefill_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess ||
+            cudaFuncSetAttribute(prefill_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess)
             return SEMIPD_ERR_CUDA;
         attr_set = true;
     }
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;
-    prefill_tc_kernel<<<grid, NT, smem, st>>>(qmap, pool->kmap[layer], pool->vmap[layer], kcmap,
-                                              vcmap, omap, prm);
+    if (prm.n_peers > 0)
+        prefill_tc_kernel<true><<<grid, NT, smem, st>>>(qmap, pool->kmap[layer], pool->vmap[layer],
+                                                        kcmap, vcmap, omap, prm);
+    else
+        prefill_tc_kernel<false><<<grid, NT, smem, st>>>(qmap, pool->kmap[layer], pool->vmap[layer],
+                                                         kcmap, vcmap, omap, prm);
     pool->launches += 1;
     return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+}
+
+extern "C" semipd_status semipd_set_prefill_peers(semipd_pool_t pool, void* const* peer_out,
+                                                  int32_t n) {
+    if (!pool || n < 0 || n > SEMIPD_MAX_PEERS - 1 || (n > 0 && !peer_out)) return SEMIPD_ERR_INVALID;
+    for (int k = 0; k < n; ++k)
+        if (!peer_out[k] || reinterpret_cast<uintptr_t>(peer_out[k]) % 16) return SEMIPD_ERR_INVALID;
+    for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k) pool->pre_peers[k] = k < n ? peer_out[k] : nullptr;
+    pool->pre_n_peers = n;
+    return SEMIPD_OK;
 }

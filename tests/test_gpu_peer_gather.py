@@ -259,3 +259,68 @@ def test_decode_epilogue_peer_stores_emulated(tpn):
                              torch.empty(B, hq, 128, dtype=torch.bfloat16, device=dev), wss[0],
                              out_head_major=False)
     pools[0].set_decode_peers([])
+
+
+@pytest.mark.parametrize("tpn", [2, 8])
+def test_prefill_epilogue_peer_stores_emulated(tpn):
+    """The TP head gather fused into the tcgen05 prefill epilogue (semipd_set_prefill_peers):
+    ranks emulated as streams of one process, a 700-token chunk (full and ragged q tiles) over
+    a 300-token paged prefix; every rank's gathered buffer equals the unsharded prefill bitwise,
+    and the unsharded run is unchanged by the peer-store code path being present."""
+    import ctypes
+
+    import synth
+    from paper_2504_19867_b200 import KVPool, PoolConfig, lib, tp
+    dev = torch.device("cuda", 0)
+    shape = synth.AttnShape("llama3-70b", 64, 8, 128, 128, 64, torch.bfloat16)
+    C, P, bs = 700, 300, 64
+    pc = synth.prefill_case(shape, [C], [P], seed=3050)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    sc = shape.softmax_scale
+    nb = -(-(C + P) // bs)
+
+    def make(heads):
+        kl, kh = heads
+        pool = KVPool(PoolConfig(1, nb + 1, bs, kh - kl, 128, 128, 1, nb), dev)
+        pool.alloc_blocks(i32([0]), i32([nb]))
+        K, V, BT, _ = pool.views(0)
+        pos = torch.arange(P)
+        blk = BT.cpu()[0].long()[pos // bs].to(dev)
+        K[blk, :, (pos % bs).to(dev)] = pc.k_prefix[0][:, kl:kh].to(dev)
+        V[blk, :, (pos % bs).to(dev)] = pc.v_prefix[0][:, kl:kh].to(dev)
+        return pool
+
+    cu, rid, pre = i32([0, C]), i32([0]), i32([P])
+    full = make((0, 8))
+    ref = torch.empty(64, C, 128, dtype=torch.bfloat16, device=dev)
+    full.prefill_attn(0, pc.q.to(dev), pc.k_new.to(dev), pc.v_new.to(dev), cu, rid, pre, C, C, sc,
+                      ref, out_head_major=True)
+    hq = 64 // tpn
+    pools, outs, flags, streams, ins = [], [], [], [], []
+    for r in range(tpn):
+        ql, qh = tp.head_range(64, tpn, r)
+        kl, kh = tp.head_range(8, tpn, r)
+        pools.append(make((kl, kh)))
+        outs.append(torch.full((64, C, 128), float("nan"), dtype=torch.bfloat16, device=dev))
+        flags.append(torch.zeros(2 * tpn, dtype=torch.int32, device=dev))
+        streams.append(torch.cuda.Stream(dev))
+        ins.append((pc.q[:, ql:qh].contiguous().to(dev), pc.k_new[:, kl:kh].contiguous().to(dev),
+                    pc.v_new[:, kl:kh].contiguous().to(dev), ql, qh))
+    shard = hq * C * 128 * 2
+    for r in range(tpn):
+        pools[r].set_prefill_peers([outs[k].data_ptr() + r * shard for k in range(tpn) if k != r])
+    fl = (ctypes.c_void_p * tpn)(*[f.data_ptr() for f in flags])
+    L = lib()
+    torch.cuda.synchronize()
+    for r in range(tpn):
+        qs, ks, vs, ql, qh = ins[r]
+        s = streams[r]
+        cs = ctypes.c_void_p(s.cuda_stream)
+        assert L.semipd_peer_handshake(fl, ctypes.c_void_p(flags[r].data_ptr()), tpn, r, 0, cs) == 0
+        pools[r].prefill_attn(0, qs, ks, vs, cu, rid, pre, C, C, sc, outs[r][ql:qh],
+                              out_head_major=True, stream=s)
+        assert L.semipd_peer_handshake(fl, ctypes.c_void_p(flags[r].data_ptr()), tpn, r, 1, cs) == 0
+    torch.cuda.synchronize()
+    for r in range(tpn):
+        assert torch.equal(outs[r].view(torch.int16), ref.view(torch.int16)), r
+    assert all(int(f.abs().sum()) == 0 for f in flags)

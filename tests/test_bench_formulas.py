@@ -66,3 +66,13 @@ def test_prefill_bytes_and_step_bytes():
 def test_bytes_independent_of_block_size():
     mod = _bench()
     assert _workload(mod, 16).decode_bytes_per_launch() == _workload(mod, 64).decode_bytes_per_launch()
+
+
+def test_parallelism_label_names_the_gather():
+    import dataclasses
+    import bench
+    shape = dataclasses.replace(bench.MODELS["llama3-8b"], block_size=64)
+    assert bench.workload_config(shape, 1)["parallelism"] == "tp1"
+    assert "NCCL" in bench.workload_config(shape, 4)["parallelism"]
+    assert "copy-engine" in bench.workload_config(shape, 4, "peer")["parallelism"]
+    assert "epilogues" in bench.workload_config(shape, 8, "fused")["parallelism"]

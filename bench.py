@@ -1,26 +1,39 @@
 #!/usr/bin/env python
 """bench.py — co-run prefill + decode attention on one unified paged KV pool.
 
-Workload (BASELINE.json configs[1], "Llama-3-8B attention shapes bf16"): 32 layers,
-32 q / 8 kv heads, d = 128, block 16; per step (one co-run iteration, SURVEY §8(a)
-rows a1-a9):
-  stream P (prefill worker): alloc 128 blocks for the prefill request, then for each
-    layer semipd_prefill_attn on one 2048-token chunk (P = 0; K/V write + causal GQA
-    attention), then free the request's blocks;
-  stream D (decode worker), concurrently: for each layer semipd_decode_attn on 64
-    requests at ctx 2048 (K/V append + split-K paged attention).
-The two persistent grids are capped to the (x, y) SM partition.  A short
-sweep over x picks the best split during warm-up; the K timed steps run at it.
+Headline workload (BASELINE.json configs[1], "Llama-3-8B attention shapes bf16"): 32 layers,
+32 q / 8 kv heads, d = 128, 64-token pages (R7; the 16-token setting is reported
+as the `block16` field); per step (one co-run iteration):
+  stream P (prefill worker): alloc the prefill request's blocks, then for each layer
+    semipd_prefill_attn on one 2048-token chunk (P = 0; K/V write + causal GQA attention),
+    then free the request's blocks;
+  stream D (decode worker), concurrently: for each layer semipd_decode_attn on 64 requests
+    at ctx 2048 (K/V append + split-K paged attention).
+The two persistent grids are capped to the (x, y) SM partition.  The sweep
+x = 10 .. 90 (+ refinement around the best) picks the split; the K timed steps run there.
 
-metric: attention-stack tokens/s = (2048 prefill + 64 decode tokens) x steps / time
-(each token through all 32 layers).  value = device time (CUDA events, max over
-ranks), inputs resident in HBM; e2e = the same through the public API with pinned
-host inputs copied in and outputs copied out every step.
+metric: attention-stack tokens/s = (2048 prefill + 64 decode tokens) x steps / time (each
+token through all 32 layers).  value = device time (CUDA events around K CUDA-graph
+replays, max over ranks), inputs resident in HBM; e2e = the same through the public API with
+pinned host inputs copied in and outputs copied out every step.
 
-Multi-GPU (torchrun, N ranks): tensor parallel by KV head (Hq/N, Hkv/N per rank,
-own pool shard), NCCL all-gather of head-major outputs per layer on a per-phase
-process group, strong scaling.  --impl reference times the fp64 oracle
-(oracle/, the reference arm of this tier) on the host cores.
+Kernel times come from the library's device-side launch spans (semipd_set_spans: first CTA
+entry -> last CTA exit, %globaltimer) accumulated over the same timed replays, so the
+roofline fractions describe the timed steps themselves.
+
+Secondary fields (N = 1): block16 (same workload, 16-token pages), cfg3 (Llama-3-70B shapes,
+TP 1), cfg4 (long-context mix), cfg5 (DeepSeek-V2-Lite MLA latent), each with per-phase
+roofline fractions at its best split.
+
+Multi-GPU (torchrun, N ranks): tensor parallel by KV head (Hq/N, Hkv/N per rank, own pool
+shard), the head-major outputs all-gathered per layer on a per-phase process group
+whose NCCL communicator is capped to --nccl-max-ctas CTAs; strong scaling; the step is
+captured into a CUDA graph (collectives included) when NCCL allows it, else it runs eagerly
+and the line says so.  --tp-mode pipelined runs each gather on a per-phase comm stream
+overlapping the next layer (attention grid = budget - NCCL CTAs).  The DP-replica reference
+(every rank runs the TP-1 workload, no collective) is reported as `dp_replicas`.
+--impl reference times the fp64 oracle (oracle/, the reference arm of this tier) on the host
+cores.
 """
 from __future__ import annotations
 
@@ -30,7 +43,6 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -46,9 +58,10 @@ MODELS = {"llama3-8b": synth.CFG2_LLAMA8B, "llama3-70b": synth.CFG3_LLAMA70B}
 PREFILL_TOKENS = 2048
 DECODE_BATCH = 64
 DECODE_CTX = 2048
+METRIC = "co-run prefill+decode attention tokens/s (32-layer stack)"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -56,25 +69,32 @@ def parse():
     ap.add_argument("--impl", default="semipd", choices=["semipd", "reference"])
     ap.add_argument("--model", default="llama3-8b", choices=list(MODELS))
     ap.add_argument("--split", type=float, default=None, help="prefill SM percent x (y = 100-x)")
-    ap.add_argument("--sweep", default="25,30,35,40,45,50,60")
+    ap.add_argument("--sweep", default="10,20,30,40,50,60,70,80,90")
     ap.add_argument("--block-size", type=int, default=64,
                     help="KV page size in tokens (64: one 16 KiB TMA box per (block, head) "
-                         "page on B200; 16 is supported but TMA-per-box bound)")
+                         "page on B200; 16 is reported as the block16 field)")
     ap.add_argument("--gather", default="nccl", choices=["nccl", "peer", "fused"],
                     help="TP head all-gather: NCCL all_gather (CTAs); peer = copy-engine pushes "
                          "over IPC-mapped peer memory with stream-memop flags (no SMs); fused = "
                          "both kernels store their output into the peers' buffers from the "
                          "epilogue")
-    ap.add_argument("--peer-graph", action="store_true",
-                    help="N > 1 with --gather peer: replay the co-run step as a CUDA graph")
+    ap.add_argument("--tp-mode", default="dependent", choices=["dependent", "pipelined"],
+                    help="dependent: layer l's gather on the phase stream before layer l+1; "
+                         "pipelined: on a per-phase comm stream overlapping layer l+1 (NCCL)")
+    ap.add_argument("--nccl-max-ctas", type=int, default=4,
+                    help="ncclConfig_t.maxCTAs of each phase communicator (counted inside the "
+                         "phase budget in pipelined mode)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every kernel from Python instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the block16 / cfg3 / cfg4 / cfg5 fields")
+    ap.add_argument("--no-dp", action="store_true", help="N > 1: skip the DP-replica reference")
     ap.add_argument("--extra", action="store_true", default=True,
                     help="serial / (100,100) baselines (default on: the paper's spatial-vs-temporal claim)")
     ap.add_argument("--no-extra", dest="extra", action="store_false")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -83,25 +103,29 @@ def ncu_traffic(kernel: str):
     (profiles/r*_ncu_traffic.json, written from an `ncu --set full` run of the same shapes)."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
-    if not files:
-        return None
-    try:
-        with open(files[-1]) as f:
-            d = json.load(f)[kernel]
-        return int(d["dram_read_bytes"]) + int(d["dram_write_bytes"])
-    except Exception:
-        return None
+    for path in reversed(files):
+        try:
+            with open(path) as f:
+                d = json.load(f)[kernel]
+            return int(d["dram_read_bytes"]) + int(d["dram_write_bytes"])
+        except Exception:
+            continue
+    return None
 
 
 def peaks():
+    """HBM GB/s and dense bf16 TFLOP/s (burst and sustained) from MEASURED_PEAKS.json, else
+    the profiling guide's fallback."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(
-            d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+        return {"hbm": float(d["hbm_gbs"]), "burst": float(d["bf16_tflops"]),
+                "sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "kind": "measured (MEASURED_PEAKS.json)"}
     except Exception:
-        return 6650.0, 1590.0, 1400.0, "fallback"
+        return {"hbm": 6650.0, "burst": 1590.0, "sustained": 1400.0,
+                "kind": "fallback (B200_PROFILING.md)"}
 
 
 def nvml_id(dev: torch.device):
@@ -186,179 +210,249 @@ def dist_info():
     return ws, rank, local
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------- algorithmic work
+def decode_bytes(shape: synth.AttnShape, ctx_lens) -> float:
+    """Algorithmic HBM bytes of one decode launch: every visible
+    key's K and V once (V aliases K for the MLA latent: the 576-d row once), q in, o out."""
+    eb = 2
+    row = shape.head_dim_k if shape.kv_shared else shape.head_dim_k + shape.head_dim_v
+    kv = sum(c + 1 for c in ctx_lens) * shape.num_kv_heads * row * eb
+    io = len(ctx_lens) * shape.num_q_heads * (shape.head_dim_k + shape.head_dim_v) * eb
+    return float(kv + io)
+
+
+def prefill_flops(shape: synth.AttnShape, C: int, P: int) -> float:
+    """2 Hq (dk + dv) per unmasked (q, k) pair; pairs = C P + C (C + 1) / 2."""
+    pairs = C * P + C * (C + 1) / 2
+    return 2.0 * shape.num_q_heads * (shape.head_dim_k + shape.head_dim_v) * pairs
+
+
+def prefill_bytes(shape: synth.AttnShape, C: int) -> float:
+    """HBM bytes a prefill launch must move at P = 0: q in, o out, k_new / v_new in and
+    their copy into the pool pages (a3, fused)."""
+    eb = 2
+    qo = C * shape.num_q_heads * (shape.head_dim_k + shape.head_dim_v) * eb
+    kvrow = shape.head_dim_k if shape.kv_shared else shape.head_dim_k + shape.head_dim_v
+    return float(qo + 2 * C * shape.num_kv_heads * kvrow * eb)
+
+
 # ----------------------------------------------------------------------------- workload
 class Workload:
-    """Pool + resident inputs for one rank (head shard under TP)."""
+    """Pool + resident inputs for one rank (head shard under TP): `L` layers of one prefill
+    chunk of C tokens at prefix P (one request) and a decode step of B requests."""
 
     def __init__(self, shape: synth.AttnShape, tp: int, dev: torch.device, seed: int = 1020,
-                 gather: str = "nccl"):
+                 gather: str = "nccl", B: int = DECODE_BATCH, ctx=DECODE_CTX,
+                 C: int = PREFILL_TOKENS, P: int = 0, layers: int | None = None,
+                 tp_mode: str = "dependent", nccl_max_ctas: int = 4, groups=None,
+                 max_prefix: int | None = None):
         from paper_2504_19867_b200 import KVPool, PoolConfig
         self.full = shape
         self.shape = synth.shard_heads(shape, tp) if tp > 1 else shape
-        self.tp, self.dev = tp, dev
+        self.tp, self.dev, self.gather_mode, self.tp_mode = tp, dev, gather, tp_mode
+        self.nccl_ctas = nccl_max_ctas
         s = self.shape
-        self.L = s.num_layers
-        self.B, self.ctx, self.C = DECODE_BATCH, DECODE_CTX, PREFILL_TOKENS
+        self.L = layers or s.num_layers
+        self.B, self.C = B, C
+        self.ctx_list = list(ctx) if isinstance(ctx, (list, tuple)) else [int(ctx)] * B
+        self.ctx = max(self.ctx_list)
         bs = s.block_size
-        self.nb_dec = self.ctx // bs + 1                 # slot ctx needs block ctx // bs
-        self.nb_pre = -(-self.C // bs)
-        n_blocks = self.B * self.nb_dec + self.nb_pre + 64
+        nb_dec = [c // bs + 1 for c in self.ctx_list]   # slot ctx needs block ctx // bs
+        nb_pre_max = -(-(C + max(P, max_prefix or 0)) // bs)
+        n_blocks = sum(nb_dec) + nb_pre_max + 64
         self.cfg = PoolConfig(num_layers=self.L, num_blocks=n_blocks, block_size=bs,
                               num_kv_heads=s.num_kv_heads, head_dim_k=s.head_dim_k,
-                              head_dim_v=s.head_dim_v, max_reqs=self.B + 2,
-                              max_blocks_per_req=self.nb_dec + 8, dtype=s.dtype)
+                              head_dim_v=s.head_dim_v, max_reqs=B + 2,
+                              max_blocks_per_req=max(max(nb_dec), nb_pre_max) + 8, dtype=s.dtype,
+                              kv_shared=s.kv_shared)
         self.pool = KVPool(self.cfg, dev)
         i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
-        self.rid_dec = i32(list(range(self.B)))
-        self.ctx_lens = i32([self.ctx] * self.B)
-        self.pool.alloc_blocks(self.rid_dec, i32([self.nb_dec] * self.B))
-        self.rid_pre = i32([self.B])
-        self.nblk_pre = i32([self.nb_pre])
-        self.cu = i32([0, self.C])
-        self.prefix = i32([0])
+        self.i32 = i32
+        self.rid_dec = i32(list(range(B)))
+        self.ctx_lens = i32(self.ctx_list)
+        self.pool.alloc_blocks(self.rid_dec, i32(nb_dec))
+        self.rid_pre = i32([B])
+        self.cu = i32([0, C])
+        self.set_prefix(P)
         g = torch.Generator(device=dev)
         g.manual_seed(seed)
-        # cached context: random bf16 in every layer's pool (distinct memory per layer,
-        # so the per-step decode working set (L x 537 MB) is far larger than L2)
+        # cached context: random bf16 in every layer's pool (distinct memory per layer, so the
+        # per-step decode working set is far larger than L2)
         for l in range(self.L):
             K, V, _, _ = self.pool.views(l)
             K.normal_(generator=g)
-            V.normal_(generator=g)
-        Hq, Hkv, d = s.num_q_heads, s.num_kv_heads, s.head_dim_k
+            if V is not None:
+                V.normal_(generator=g)
+        Hq, Hkv, dk, dv = s.num_q_heads, s.num_kv_heads, s.head_dim_k, s.head_dim_v
         mk = lambda *shp: torch.randn(*shp, generator=g, device=dev, dtype=torch.float32).to(s.dtype)  # noqa: E731
-        self.qp = [mk(self.C, Hq, d) for _ in range(self.L)]
-        self.kp = [mk(self.C, Hkv, d) for _ in range(self.L)]
-        self.vp = [mk(self.C, Hkv, d) for _ in range(self.L)]
-        self.qd = [mk(self.B, Hq, d) for _ in range(self.L)]
-        self.kd = [mk(self.B, Hkv, d) for _ in range(self.L)]
-        self.vd = [mk(self.B, Hkv, d) for _ in range(self.L)]
+        self.qp = [mk(C, Hq, dk) for _ in range(self.L)]
+        self.kp = [mk(C, Hkv, dk) for _ in range(self.L)]
+        self.vp = [None if s.kv_shared else mk(C, Hkv, dv) for _ in range(self.L)]
+        self.qd = [mk(B, Hq, dk) for _ in range(self.L)]
+        self.kd = [mk(B, Hkv, dk) for _ in range(self.L)]
+        self.vd = [None if s.kv_shared else mk(B, Hkv, dv) for _ in range(self.L)]
         hm = tp > 1
-        self.op = [torch.empty((Hq, self.C, d) if hm else (self.C, Hq, d), dtype=s.dtype,
-                               device=dev) for _ in range(self.L)]
-        self.od = [torch.empty((Hq, self.B, d) if hm else (self.B, Hq, d), dtype=s.dtype,
-                               device=dev) for _ in range(self.L)]
-        self.ws = self.pool.new_decode_workspace(self.B, Hq, self.ctx)
+        self.op = [torch.empty((Hq, C, dv) if hm else (C, Hq, dv), dtype=s.dtype, device=dev)
+                   for _ in range(self.L)]
+        self.od = [torch.empty((Hq, B, dv) if hm else (B, Hq, dv), dtype=s.dtype, device=dev)
+                   for _ in range(self.L)]
+        self.ws = self.pool.new_decode_workspace(B, Hq, self.ctx)
         self.scale = s.softmax_scale
         self.sP = torch.cuda.Stream(device=dev)
         self.sD = torch.cuda.Stream(device=dev)
         self.pg_p = self.pg_d = None
         self.peer_p = self.peer_d = None
-        self.fused_d = self.fused_p = False
+        self.fused = False
         self.gath_p = self.gath_d = None
+        self.cP = self.cD = None
         if tp > 1:
             from paper_2504_19867_b200 import tp as tpmod
-            groups = tpmod.PhaseGroups.create(  # one communicator per phase (P:232)
-                backend=os.environ.get("SPD_BENCH_BACKEND", "nccl"))
             self.pg_p, self.pg_d = groups.prefill, groups.decode
-            self.gath_p = torch.empty((self.full.num_q_heads, self.C, d), dtype=s.dtype, device=dev)
-            self.gath_d = torch.empty((self.full.num_q_heads, self.B, d), dtype=s.dtype, device=dev)
+            n_g = self.L if tp_mode == "pipelined" else 1
+            self.gath_p = [torch.empty((self.full.num_q_heads, C, dv), dtype=s.dtype, device=dev)
+                           for _ in range(n_g)]
+            self.gath_d = [torch.empty((self.full.num_q_heads, B, dv), dtype=s.dtype, device=dev)
+                           for _ in range(n_g)]
+            if tp_mode == "pipelined":
+                self.cP = torch.cuda.Stream(device=dev)
+                self.cD = torch.cuda.Stream(device=dev)
+                self.ev_kp = [torch.cuda.Event() for _ in range(self.L)]
+                self.ev_kd = [torch.cuda.Event() for _ in range(self.L)]
             if gather in ("peer", "fused"):  # copy engines + stream memops instead of NCCL CTAs
-                self.peer_p = tpmod.PeerGather(self.gath_p.shape, s.dtype, self.pg_p, dev)
-                self.peer_d = tpmod.PeerGather(self.gath_d.shape, s.dtype, self.pg_d, dev)
-            if gather == "fused":  # both epilogues store straight into every rank's buffer
-                self.fused_d = self.fused_p = True
-                self.pool.set_decode_peers(self.peer_d.peer_shard_ptrs())
-                self.od = [self.peer_d.local_view() for _ in range(self.L)]
-                self.pool.set_prefill_peers(self.peer_p.peer_shard_ptrs())
-                self.op = [self.peer_p.local_view() for _ in range(self.L)]
-        # per-launch timing events (decode kernel on stream D, prefill call on stream P)
-        self.ev_d = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                     for _ in range(self.L)]
-        self.ev_p = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                     for _ in range(self.L)]
+                nb = 2 if gather == "fused" else 1
+                self.peer_p = tpmod.PeerGather((self.full.num_q_heads, C, dv), s.dtype, self.pg_p,
+                                               dev, n_bufs=nb)
+                self.peer_d = tpmod.PeerGather((self.full.num_q_heads, B, dv), s.dtype, self.pg_d,
+                                               dev, n_bufs=nb)
+            if gather == "fused":
+                # both epilogues store straight into every rank's gathered buffer; layers
+                # alternate between two buffers, so a layer's output stays readable (e2e D2H)
+                # while the next layer is written (E2E waits before reusing a buffer)
+                self.fused = True
+                self.od = [self.peer_d.local_view(l % 2) for l in range(self.L)]
+                self.op = [self.peer_p.local_view(l % 2) for l in range(self.L)]
+        # device-side launch spans: prefill launches first (slots 0..L-1), then decode
+        self.spans = torch.zeros(2 * self.L + 8, 8, dtype=torch.int64, device=dev)
 
-    # algorithmic work (SURVEY §8(a)/(d)): count unmasked pairs and K/V bytes once
+    def set_prefix(self, P: int):
+        """The prefill request's prefix length (its chunk's blocks are allocated per step)."""
+        self.P = P
+        self.prefix = self.i32([P])
+        self.nb_pre = -(-(self.C + P) // self.shape.block_size)
+        self.nblk_pre = self.i32([self.nb_pre])
+
+    # ---- algorithmic work of one launch
     def decode_bytes_per_launch(self) -> float:
-        s = self.shape
-        eb = 2
-        kv = self.B * (self.ctx + 1) * s.num_kv_heads * (s.head_dim_k + s.head_dim_v) * eb
-        io = self.B * s.num_q_heads * (s.head_dim_k + s.head_dim_v) * eb  # q in, o out
-        return float(kv + io)
-
-    def prefill_bytes_per_launch(self) -> float:
-        # HBM bytes the prefill launch must move at P = 0: q in, o out, k_new / v_new in and
-        # their copy into the pool pages (a3, fused)
-        s = self.shape
-        eb = 2
-        qo = self.C * s.num_q_heads * (s.head_dim_k + s.head_dim_v) * eb
-        kv = self.C * s.num_kv_heads * (s.head_dim_k + s.head_dim_v) * eb
-        return float(qo + 2 * kv)
+        return decode_bytes(self.shape, self.ctx_list)
 
     def prefill_flops_per_launch(self) -> float:
-        s = self.shape
-        pairs = self.C * (self.C + 1) / 2
-        return 2.0 * s.num_q_heads * (s.head_dim_k + s.head_dim_v) * pairs
+        return prefill_flops(self.shape, self.C, self.P)
 
-    # TP > 1: the head all-gather of layer l's head-major output on the phase stream s
-    # (one communicator per phase, P:232); a no-op at TP = 1
-    def pre_p(self, l, s):  # fused gather: every peer is done reading before the stores
-        if self.fused_p:
-            self.peer_p.handshake(0, stream=s)
+    def prefill_bytes_per_launch(self) -> float:
+        return prefill_bytes(self.shape, self.C)
 
-    def gather_p(self, l, s):
-        if self.fused_p:  # the kernel already stored; wait until every peer's stores landed
-            self.peer_p.handshake(1, stream=s)
-        elif self.tp > 1:
-            from paper_2504_19867_b200 import tp as tpmod
-            if self.peer_p is not None:
-                self.peer_p(self.op[l], stream=s)
-            else:
-                tpmod.gather_heads(self.op[l], self.gath_p, self.pg_p)
+    # ---- launch spans
+    def arm_spans(self):
+        self.pool.set_spans(self.spans)
 
-    def pre_d(self, l, s):  # fused gather: every peer is done reading before the stores
-        if self.fused_d:
-            self.peer_d.handshake(0, stream=s)
+    def kernel_stats(self, order=("prefill", "decode")):
+        """Mean launch duration (ms) per phase over everything folded into the spans since
+        the last zero, and the last launch sequence's per-stream spans."""
+        sp = self.spans.cpu().numpy().astype(np.float64)
+        out = {}
+        for i, ph in enumerate(order):
+            r = sp[i * self.L:(i + 1) * self.L]
+            n = r[:, 3].sum()
+            out[ph] = {"ms": float(r[:, 2].sum() / n / 1e6) if n else None,
+                       "launches": int(n),
+                       "stream_ms": float((r[-1, 6] - r[0, 5]) / 1e6) if n else None}
+        return out
 
-    def gather_d(self, l, s):
-        if self.fused_d:  # the kernel already stored; wait until every peer's stores landed
-            self.peer_d.handshake(1, stream=s)
-        elif self.tp > 1:
-            from paper_2504_19867_b200 import tp as tpmod
-            if self.peer_d is not None:
-                self.peer_d(self.od[l], stream=s)
-            else:
-                tpmod.gather_heads(self.od[l], self.gath_d, self.pg_d)
+    # ---- TP exchange of layer l on phase stream s
+    def _gather(self, phase, l, s):
+        from paper_2504_19867_b200 import tp as tpmod
+        peer = self.peer_p if phase == "p" else self.peer_d
+        outs = self.op if phase == "p" else self.od
+        if self.fused:  # the kernel already stored; wait until every peer's stores landed
+            peer.handshake(1, stream=s)
+            return
+        if peer is not None:
+            peer(outs[l], stream=s)
+            return
+        gath = self.gath_p if phase == "p" else self.gath_d
+        pg = self.pg_p if phase == "p" else self.pg_d
+        if self.tp_mode == "pipelined":
+            cs, ev = (self.cP, self.ev_kp) if phase == "p" else (self.cD, self.ev_kd)
+            ev[l].record(s)
+            cs.wait_event(ev[l])
+            with torch.cuda.stream(cs):
+                tpmod.gather_heads(outs[l], gath[l], pg)
+        else:
+            with torch.cuda.stream(s):
+                tpmod.gather_heads(outs[l], gath[0], pg)
 
-    def phase_prefill(self, budget, timed=False, stream=None):
+    def _budget(self, budget, phase):
+        """Pipelined TP: the NCCL CTAs of the overlapping gather come out of the phase budget."""
+        if self.tp > 1 and self.tp_mode == "pipelined" and self.gather_mode == "nccl":
+            n = budget if budget > 0 else self.pool.sm_budgets()[0 if phase == "p" else 1]
+            return max(1, n - self.nccl_ctas)
+        return budget
+
+    def phase_prefill(self, budget=0, stream=None):
         s = stream or self.sP
         p = self.pool
+        b = self._budget(budget, "p")
         with torch.cuda.stream(s):
             p.alloc_blocks(self.rid_pre, self.nblk_pre, None, stream=s)
             for l in range(self.L):
-                self.pre_p(l, s)
-                if timed:
-                    self.ev_p[l][0].record(s)
+                if self.fused:
+                    p.set_prefill_peers(self.peer_p.peer_shard_ptrs(l % 2), self.C)
+                    self.peer_p.handshake(0, stream=s)  # every peer is done reading
                 p.prefill_attn(l, self.qp[l], self.kp[l], self.vp[l], self.cu, self.rid_pre,
                                self.prefix, self.C, self.C, self.scale, self.op[l],
-                               out_head_major=self.tp > 1, sm_budget=budget, stream=s)
-                if timed:
-                    self.ev_p[l][1].record(s)
-                self.gather_p(l, s)
+                               out_head_major=self.tp > 1, sm_budget=b, stream=s)
+                if self.tp > 1:
+                    self._gather("p", l, s)
             p.free_blocks(self.rid_pre, None, stream=s)
+            if self.cP is not None:
+                s.wait_stream(self.cP)
 
-    def phase_decode(self, budget, timed=False, stream=None):
+    def phase_decode(self, budget=0, stream=None):
         s = stream or self.sD
         p = self.pool
+        b = self._budget(budget, "d")
         with torch.cuda.stream(s):
             for l in range(self.L):
-                self.pre_d(l, s)
-                if timed:
-                    self.ev_d[l][0].record(s)
+                if self.fused:
+                    p.set_decode_peers(self.peer_d.peer_shard_ptrs(l % 2), self.B)
+                    self.peer_d.handshake(0, stream=s)
                 p.decode_attn(l, self.qd[l], self.kd[l], self.vd[l], self.rid_dec, self.ctx_lens,
                               self.ctx, self.scale, self.od[l], self.ws,
-                              out_head_major=self.tp > 1, sm_budget=budget, stream=s)
-                if timed:
-                    self.ev_d[l][1].record(s)
-                self.gather_d(l, s)
+                              out_head_major=self.tp > 1, sm_budget=b, stream=s)
+                if self.tp > 1:
+                    self._gather("d", l, s)
+            if self.cD is not None:
+                s.wait_stream(self.cD)
 
-    def corun_step(self, x, y, timed=False):
+    def corun_step(self, x, y):
         """One co-run iteration: both workers concurrently at budgets from (x, y)."""
         main = torch.cuda.current_stream(self.dev)
         self.pool.set_partition(x, y)
         self.sP.wait_stream(main)
         self.sD.wait_stream(main)
-        self.phase_prefill(0, timed)
-        self.phase_decode(0, timed)
+        self.phase_prefill(0)
+        self.phase_decode(0)
         main.wait_stream(self.sP)
         main.wait_stream(self.sD)
 
@@ -379,6 +473,9 @@ class Workload:
         main.wait_stream(self.sP)
         main.wait_stream(self.sD)
 
+    def tokens_per_step(self) -> int:
+        return self.C + self.B
+
 
 def time_steps(fn, steps, dev, barrier=None):
     torch.cuda.synchronize(dev)
@@ -395,6 +492,109 @@ def time_steps(fn, steps, dev, barrier=None):
     return e0.elapsed_time(e1) / 1e3  # seconds
 
 
+def max_over_ranks(t: float, ws: int, dev) -> float:
+    if ws > 1:
+        tt = torch.tensor([t], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    return t
+
+
+class Runner:
+    """Graph capture + timing of one workload's steps with the launch spans armed."""
+
+    def __init__(self, w: Workload, dev, barrier=None, use_graph=True, ws=1):
+        self.w, self.dev, self.barrier, self.use_graph, self.ws = w, dev, barrier, use_graph, ws
+        self.graph_error = None
+
+    def capture(self, fn):
+        """Capture fn into a CUDA graph (spans armed first, so slot i = launch i of fn);
+        returns a replay callable, or an eager callable that re-arms the spans each step if
+        capture is off or fails."""
+        w = self.w
+        if self.use_graph:
+            try:
+                w.arm_spans()
+                fn()
+                torch.cuda.synchronize(self.dev)
+                w.arm_spans()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    fn()
+                g.replay()
+                torch.cuda.synchronize(self.dev)
+                return g.replay
+            except Exception as e:  # NCCL without graph support etc.: eager, said in the line
+                self.graph_error = repr(e)[:200]
+                self.use_graph = False
+                torch.cuda.synchronize(self.dev)
+
+        def eager():
+            w.arm_spans()
+            fn()
+        eager()
+        torch.cuda.synchronize(self.dev)
+        return eager
+
+    def time(self, step, reps):
+        """Seconds per step over `reps` calls (max over ranks) + the spans' kernel stats."""
+        self.w.spans.zero_()
+        t = time_steps(step, reps, self.dev, self.barrier) / reps
+        return max_over_ranks(t, self.ws, self.dev), self.w.kernel_stats()
+
+
+def phase_record(w: Workload, n_p: int, n_d: int, t_step: float, ks: dict, pk: dict) -> dict:
+    """Per-split record: both phases' rates and roofline fractions
+    from the spans of the timed replays.  tokens_per_s is for the workload's L-layer stack."""
+    N = w.pool.num_sms
+    dec_ms, pre_ms = ks["decode"]["ms"], ks["prefill"]["ms"]
+    rec = {"n_p": n_p, "n_d": n_d, "ms": t_step * 1e3,
+           "tokens_per_s": w.tokens_per_step() / t_step}
+    if dec_ms:
+        gbs = w.decode_bytes_per_launch() / (dec_ms / 1e3) / 1e9
+        rec.update(decode_ms=dec_ms, decode_gbs=gbs, decode_frac=gbs / pk["hbm"])
+    if pre_ms:
+        tfs = w.prefill_flops_per_launch() / (pre_ms / 1e3) / 1e12
+        share = n_p / N
+        rec.update(prefill_ms=pre_ms, prefill_tflops=tfs, prefill_frac=tfs / pk["burst"],
+                   prefill_frac_share_burst=tfs / (pk["burst"] * share),
+                   prefill_frac_share_sustained=tfs / (pk["sustained"] * share))
+    if dec_ms and pre_ms:
+        rec["target_score"] = min(rec["decode_frac"] / 0.70, rec["prefill_frac_share_burst"] / 0.50)
+        sp, sd = ks["prefill"]["stream_ms"], ks["decode"]["stream_ms"]
+        rec["overlap"] = min(sp, sd) / max(sp, sd)
+    return rec
+
+
+def sweep_splits(w: Workload, run: Runner, xs, pk, reps=3, refine=True):
+    """Co-run at every x in xs (y = 100 - x), graph-replayed; refine +-2.5 / 5 around the
+    best tokens/s.  Returns the records."""
+    out = []
+
+    def measure(x):
+        step = run.capture(lambda: w.corun_step(x, 100 - x))
+        t, ks = run.time(step, reps)
+        n_p, n_d = w.pool.sm_budgets()
+        out.append({"x": x, "y": 100 - x, **phase_record(w, n_p, n_d, t, ks, pk)})
+
+    for x in xs:
+        measure(x)
+    if refine and len(xs) > 1:
+        x0 = max(out, key=lambda r: r["tokens_per_s"])["x"]
+        for x in (x0 - 5, x0 - 2.5, x0 + 2.5, x0 + 5):
+            if 0 < x < 100 and all(abs(r["x"] - x) > 1e-6 for r in out):
+                measure(x)
+    out.sort(key=lambda r: r["x"])
+    return out
+
+
+def best_of(recs):
+    best = max(recs, key=lambda r: r["tokens_per_s"])
+    tgt = max((r for r in recs if "target_score" in r), key=lambda r: r["target_score"],
+              default=None)
+    return best, tgt
+
+
 # ----------------------------------------------------------------------------- e2e
 class E2E:
     """Same step through the public API with pinned host inputs/outputs: every step copies
@@ -403,13 +603,14 @@ class E2E:
     the attention kernels and H2D overlaps D2H (the copy engines are independent):
       H2D stream: layer l's prefill q / k / v and decode q / k / v, then an event each;
       stream P / D: wait for layer l's inputs, run the kernel, record an event;
-      D2H stream: wait for layer l's outputs, copy them out.
-    Device buffers are per layer and the step ends with the main stream joining all four
-    streams, so nothing is overwritten while still in use."""
+      D2H stream: wait for layer l's outputs, copy them out, record an event.
+    Device buffers are per layer (fused TP gather: two alternating buffers, and a phase
+    waits for the D2H of layer l - 2 before writing its buffer again) and the step ends with
+    the main stream joining all four streams, so nothing is overwritten while in use."""
 
     def __init__(self, w: Workload):
         self.w = w
-        pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+        pin = lambda t: None if t is None else t.cpu().pin_memory()  # noqa: E731
         self.h_qp = [pin(t) for t in w.qp]
         self.h_kp = [pin(t) for t in w.kp]
         self.h_vp = [pin(t) for t in w.vp]
@@ -419,12 +620,14 @@ class E2E:
         self.h_op = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in w.op]
         self.h_od = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in w.od]
         self.h2d = sum(t.numel() * t.element_size() for lst in
-                       (self.h_qp, self.h_kp, self.h_vp, self.h_qd, self.h_kd, self.h_vd) for t in lst)
+                       (self.h_qp, self.h_kp, self.h_vp, self.h_qd, self.h_kd, self.h_vd)
+                       for t in lst if t is not None)
         self.d2h = sum(t.numel() * t.element_size() for lst in (self.h_op, self.h_od) for t in lst)
         self.s_in = torch.cuda.Stream(w.dev)
         self.s_out = torch.cuda.Stream(w.dev)
         ev = lambda: [torch.cuda.Event() for _ in range(w.L)]  # noqa: E731
         self.in_p, self.in_d, self.out_p, self.out_d = ev(), ev(), ev(), ev()
+        self.done_p, self.done_d = ev(), ev()
 
     def step(self, x, y):
         w = self.w
@@ -432,40 +635,62 @@ class E2E:
         w.pool.set_partition(x, y)
         for s in (self.s_in, self.s_out, w.sP, w.sD):
             s.wait_stream(main)
+
+        def cp(d, h):
+            if h is not None:
+                d.copy_(h, non_blocking=True)
+
         with torch.cuda.stream(self.s_in):
             for l in range(w.L):
-                w.qd[l].copy_(self.h_qd[l], non_blocking=True)
-                w.kd[l].copy_(self.h_kd[l], non_blocking=True)
-                w.vd[l].copy_(self.h_vd[l], non_blocking=True)
+                cp(w.qd[l], self.h_qd[l])
+                cp(w.kd[l], self.h_kd[l])
+                cp(w.vd[l], self.h_vd[l])
                 self.in_d[l].record(self.s_in)
-                w.qp[l].copy_(self.h_qp[l], non_blocking=True)
-                w.kp[l].copy_(self.h_kp[l], non_blocking=True)
-                w.vp[l].copy_(self.h_vp[l], non_blocking=True)
+                cp(w.qp[l], self.h_qp[l])
+                cp(w.kp[l], self.h_kp[l])
+                cp(w.vp[l], self.h_vp[l])
                 self.in_p[l].record(self.s_in)
+        tp = w.tp > 1
         with torch.cuda.stream(w.sP):
             w.pool.alloc_blocks(w.rid_pre, w.nblk_pre, None, stream=w.sP)
             for l in range(w.L):
                 w.sP.wait_event(self.in_p[l])
-                w.pre_p(l, w.sP)
+                if w.fused:
+                    if l >= 2:
+                        w.sP.wait_event(self.done_p[l - 2])  # buffer l % 2 read out
+                    w.pool.set_prefill_peers(w.peer_p.peer_shard_ptrs(l % 2), w.C)
+                    w.peer_p.handshake(0, stream=w.sP)
                 w.pool.prefill_attn(l, w.qp[l], w.kp[l], w.vp[l], w.cu, w.rid_pre, w.prefix, w.C,
-                                    w.C, w.scale, w.op[l], out_head_major=w.tp > 1, stream=w.sP)
-                w.gather_p(l, w.sP)  # TP > 1: same exchange step as the device-timed path
+                                    w.C, w.scale, w.op[l], out_head_major=tp, stream=w.sP)
+                if tp:
+                    w._gather("p", l, w.sP)  # same exchange step as the device-timed path
                 self.out_p[l].record(w.sP)
             w.pool.free_blocks(w.rid_pre, None, stream=w.sP)
+            if w.cP is not None:
+                w.sP.wait_stream(w.cP)
         with torch.cuda.stream(w.sD):
             for l in range(w.L):
                 w.sD.wait_event(self.in_d[l])
-                w.pre_d(l, w.sD)
+                if w.fused:
+                    if l >= 2:
+                        w.sD.wait_event(self.done_d[l - 2])
+                    w.pool.set_decode_peers(w.peer_d.peer_shard_ptrs(l % 2), w.B)
+                    w.peer_d.handshake(0, stream=w.sD)
                 w.pool.decode_attn(l, w.qd[l], w.kd[l], w.vd[l], w.rid_dec, w.ctx_lens, w.ctx,
-                                   w.scale, w.od[l], w.ws, out_head_major=w.tp > 1, stream=w.sD)
-                w.gather_d(l, w.sD)
+                                   w.scale, w.od[l], w.ws, out_head_major=tp, stream=w.sD)
+                if tp:
+                    w._gather("d", l, w.sD)
                 self.out_d[l].record(w.sD)
+            if w.cD is not None:
+                w.sD.wait_stream(w.cD)
         with torch.cuda.stream(self.s_out):
             for l in range(w.L):
                 self.s_out.wait_event(self.out_d[l])
                 self.h_od[l].copy_(w.od[l], non_blocking=True)
+                self.done_d[l].record(self.s_out)
                 self.s_out.wait_event(self.out_p[l])
                 self.h_op[l].copy_(w.op[l], non_blocking=True)
+                self.done_p[l].record(self.s_out)
         for s in (self.s_in, self.s_out, w.sP, w.sD):
             main.wait_stream(s)
 
@@ -527,7 +752,21 @@ def oracle_sample_rate(shape: synth.AttnShape, threads: int, budget_s: float = 1
     return tokens / t_step, sample, time.perf_counter()
 
 
-def workload_config(shape: synth.AttnShape, ws: int, gather: str = "nccl") -> dict:
+def cpu_baseline(shape, budget_nproc: float = 12.0, budget_1: float = 8.0) -> dict:
+    """The oracle at nproc threads (the reported value) and at 1 thread, with the CPU model."""
+    import oracle
+    threads = os.cpu_count() or 1
+    v, sample, _ = oracle_sample_rate(shape, threads, budget_nproc)
+    v1, sample1, _ = oracle_sample_rate(shape, 1, budget_1)
+    oracle.set_threads(threads)
+    return {"value": v, "unit": "tokens/s", "cores": threads, "kind": "oracle", "sample": sample,
+            "nproc": threads, "cpu_model": cpu_model(),
+            "one_thread": {"value": v1, "unit": "tokens/s", "sample": sample1},
+            "parallel_speedup": v / v1 if v1 else None}
+
+
+def workload_config(shape: synth.AttnShape, ws: int, gather: str = "nccl",
+                    tp_mode: str = "dependent") -> dict:
     """The `config` both arms print (the reference arm runs the same workload)."""
     decode_gb = shape.num_layers * (DECODE_BATCH * (DECODE_CTX + 1) * shape.num_kv_heads * 2 * 128 * 2) / 1e9
     return {"workload": f"{shape.name} attention (Hq {shape.num_q_heads}, Hkv {shape.num_kv_heads}, "
@@ -536,7 +775,7 @@ def workload_config(shape: synth.AttnShape, ws: int, gather: str = "nccl") -> di
             "parallelism": (f"tp{ws} (KV-head shards, "
                             + {"peer": "copy-engine peer all-gather)",
                                "fused": "peer stores from the decode / prefill epilogues)"}
-                            .get(gather, "NCCL all-gather)")
+                            .get(gather, f"NCCL all-gather, {tp_mode})")
                             if ws > 1 else "tp1"),
             "l2": f"no flush: per-step decode working set {decode_gb:.1f} GB >> 126 MB L2"}
 
@@ -558,13 +797,14 @@ def run_reference(args):
     elapsed = time.perf_counter() - t_start
     value = statistics.median(vals)
     line = {
-        "impl": "reference", "metric": "co-run prefill+decode attention tokens/s (32-layer stack)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * (PREFILL_TOKENS + DECODE_BATCH) / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(shape, 1),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model(),
+                         "step_time": "extrapolated from the sample (per-row / per-layer rates)"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "wall_s": elapsed,
@@ -573,9 +813,83 @@ def run_reference(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- secondary fields
+def _sweep_field(w: Workload, dev, pk, xs, **info):
+    run = Runner(w, dev)
+    recs = sweep_splits(w, run, xs, pk, reps=3, refine=False)
+    best, tgt = best_of(recs)
+    return {**info, "layers": w.L, "best": best, "best_target": tgt, "sweep": recs}
+
+
+def secondary_block16(args, dev, pk):
+    """The headline workload with 16-token pages (SURVEY S7's reading)."""
+    shape = dataclasses.replace(MODELS[args.model], block_size=16)
+    return _sweep_field(Workload(shape, 1, dev, seed=1016), dev, pk, [30, 40, 50],
+                        block_size=16)
+
+
+def secondary_cfg3(args, dev, pk):
+    """BASELINE configs[2] shapes on one GPU (TP 1): Llama-3-70B attention (Hq 64, Hkv 8,
+    G = 8), 80 layers, same per-step workload."""
+    shape = dataclasses.replace(synth.CFG3_LLAMA70B, block_size=args.block_size)
+    return _sweep_field(Workload(shape, 1, dev, seed=1030), dev, pk, [40, 45, 50, 55, 60],
+                        model="llama3-70b (TP 1)")
+
+
+def secondary_cfg4(args, dev, pk, layers: int = 8):
+    """BASELINE configs[3]: 16 decode requests at ctx 32768 + 8192-token chunks of a 32k
+    prompt at P = 0, 8192, 16384, 24576, under the partition schedule (30,70) -> (50,50) ->
+    (70,30).  `layers` distinct layers (working set 17 GB >> L2); rates are per launch;
+    tokens_per_s is for the `layers`-layer stack.  Also the partition-switch cost (eager: the
+    first step after set_partition vs the next two) with zero KV bytes moved."""
+    shape = dataclasses.replace(synth.CFG2_LLAMA8B, block_size=64)
+    w = Workload(shape, 1, dev, seed=1040, B=16, ctx=32768, C=8192, P=0, layers=layers,
+                 max_prefix=24576)
+    out = {"layers": layers, "decode": "B=16 ctx 32768 (S=9 splits)",
+           "prefill": "C=8192 at P = 0 / 8192 / 16384 / 24576", "splits": []}
+    for x, y in [(30, 70), (50, 50), (70, 30)]:
+        per_p = []
+        for P in (0, 8192, 16384, 24576):
+            w.set_prefix(P)
+            run = Runner(w, dev)
+            step = run.capture(lambda: w.corun_step(x, y))
+            t, ks = run.time(step, 2)
+            n_p, n_d = w.pool.sm_budgets()
+            per_p.append({"P": P, **phase_record(w, n_p, n_d, t, ks, pk)})
+        out["splits"].append({
+            "x": x, "y": y, "n_p": per_p[0]["n_p"], "n_d": per_p[0]["n_d"], "per_prefix": per_p,
+            "decode_frac_mean": statistics.mean(r["decode_frac"] for r in per_p),
+            "prefill_frac_share_burst_mean": statistics.mean(r["prefill_frac_share_burst"]
+                                                             for r in per_p),
+            "tokens_per_s_cycle": 4 * w.tokens_per_step() / sum(r["ms"] for r in per_p) * 1e3})
+    w.set_prefix(0)
+    ptr0 = w.pool.mem.data_ptr()
+    sw = []
+    for x, y in [(30, 70), (50, 50), (70, 30), (30, 70)]:
+        ts = [time_steps(lambda: w.corun_step(x, y), 1, dev) * 1e3 for _ in range(3)]
+        sw.append({"x": x, "first_ms": ts[0], "steady_ms": statistics.mean(ts[1:]),
+                   "switch_cost_ms": ts[0] - statistics.mean(ts[1:])})
+    out["switch"] = sw
+    out["kv_moved_bytes"] = 0 if w.pool.mem.data_ptr() == ptr0 else None
+    out["best_target"] = max(out["splits"], key=lambda r: min(
+        r["decode_frac_mean"] / 0.7, r["prefill_frac_share_burst_mean"] / 0.5))
+    return out
+
+
+def secondary_cfg5(args, dev, pk):
+    """BASELINE configs[4] kernels at trace-like scale: DeepSeek-V2-Lite absorbed MLA (16 q
+    heads over the 576-d latent, V = K[:, :512], 64-token pages, 27 layers); decode B = 256
+    at lognormal contexts (mean ~350, seed 5005) co-running with a 2048-token prefill chunk."""
+    rng = np.random.default_rng(5005)
+    ctx = [int(c) for c in np.clip(rng.lognormal(math.log(350.0) - 0.125, 0.5, 256), 64, 4096)]
+    w = Workload(synth.CFG5_MLA, 1, dev, seed=1050, B=256, ctx=ctx, C=2048)
+    return _sweep_field(w, dev, pk, [30, 40, 50, 60, 70], model="deepseek-v2-lite-mla",
+                        decode_ctx_mean=statistics.mean(ctx))
+
+
 # ----------------------------------------------------------------------------- main
-def main():
-    args = parse()
+def main(argv=None):
+    args = parse(argv)
     if args.impl == "reference":
         return run_reference(args)
     ws, rank, local = dist_info()
@@ -586,201 +900,175 @@ def main():
     dev = torch.device("cuda", 0 if one_gpu else local)
     torch.cuda.set_device(dev)
     barrier = None
+    groups = None
     if ws > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")       # communicator rank counts in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
         barrier = lambda: dist.barrier()  # noqa: E731
+        from paper_2504_19867_b200 import tp as tpmod
+        groups = tpmod.PhaseGroups.create(backend=backend, max_ctas=args.nccl_max_ctas)
     shape = dataclasses.replace(MODELS[args.model], block_size=args.block_size)
-    w = Workload(shape, ws, dev, gather=args.gather)
-    hbm_peak, bf16_peak, bf16_sus, peak_kind = peaks()
+    w = Workload(shape, ws, dev, gather=args.gather, tp_mode=args.tp_mode,
+                 nccl_max_ctas=args.nccl_max_ctas, groups=groups)
+    pk = peaks()
     W = max(3, args.warmup)
-    splits = [float(x) for x in args.sweep.split(",")] if args.split is None else [args.split]
-    # warm-up + split sweep (1 timed step per split, not part of the reported number)
+    run = Runner(w, dev, barrier, not args.no_graph, ws)
     for _ in range(2):
         w.corun_step(50, 50)
-    sweep = []
-
-    # N > 1 runs eagerly.  The peer gather is graph-safe (tests/test_gpu_peer_gather.py replays
-    # a captured gather), but with two ranks time-slicing one GPU the replayed step was 7x
-    # slower than eager (138 vs 19 ms), so graph replay for N > 1 stays opt-in (--peer-graph)
-    use_graph = not args.no_graph and (ws == 1 or (args.gather == "peer" and args.peer_graph))
-
-    def capture(x):
-        torch.cuda.synchronize(dev)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            w.corun_step(x, 100 - x)
-        g.replay()
-        torch.cuda.synchronize(dev)
-        return g
-
-    def measure(x):
-        if use_graph:
-            g = capture(x)
-            t = time_steps(g.replay, 3, dev, barrier) / 3
-        else:
-            t = time_steps(lambda: w.corun_step(x, 100 - x), 2, dev, barrier) / 2
-        if ws > 1:
-            tt = torch.tensor([t], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            t = float(tt.item())
-        sweep.append({"x": x, "y": 100 - x, "n_p": w.pool.sm_budgets()[0],
-                      "n_d": w.pool.sm_budgets()[1],
-                      "tokens_per_s": (PREFILL_TOKENS + DECODE_BATCH) / t, "ms": t * 1e3})
-
-    for x in splits:
-        measure(x)
-    if args.split is None:  # refine around the best coarse split (+-2.5 % = ~4 SMs)
-        x0 = max(sweep, key=lambda r: r["tokens_per_s"])["x"]
-        for x in (x0 - 2.5, x0 + 2.5):
-            if 0 < x < 100 and all(abs(r["x"] - x) > 1e-6 for r in sweep):
-                measure(x)
-    best = max(sweep, key=lambda r: r["tokens_per_s"])
+    # ---- split sweep (graph-replayed, per-split roofline record; not part of the value)
+    xs = [float(x) for x in args.sweep.split(",")] if args.split is None else [args.split]
+    sweep = sweep_splits(w, run, xs, pk, reps=3, refine=args.split is None)
+    best, tgt = best_of(sweep)
     x, y = best["x"], best["y"]
+    # library launches of one step (an eager step; graph replays launch the same kernels)
+    c0 = w.pool.launch_count()
+    w.corun_step(x, y)
+    torch.cuda.synchronize(dev)
+    per_step = w.pool.launch_count() - c0
+    # ---- the timed region: K replays of the captured co-run step at the best split
+    step = run.capture(lambda: w.corun_step(x, y))
     for _ in range(W):
-        w.corun_step(x, y)
-    # the co-run step (both streams, alloc -> 32 layers x 2 kernels -> free) is captured once
-    # into a CUDA graph and replayed: no per-kernel launch gaps from the Python loop
-    graph = capture(x) if use_graph else None
-    if graph is not None:
-        graph.replay()
-        torch.cuda.synchronize(dev)
-    # ---- timed region
-    per_step = [0]
+        step()
+    w.spans.zero_()
     with ClockSampler(nvml_id(dev)) as clk:
-        # the last timed step runs eagerly with per-launch CUDA events (the roofline's kernel
-        # times; an event pair between back-to-back kernels costs ~3 us, so only one step)
-        k_step = [0]
-
-        def step():
-            k_step[0] += 1
-            if k_step[0] == args.steps or graph is None:
-                c0 = w.pool.launch_count()
-                w.corun_step(x, y, timed=k_step[0] == args.steps)
-                per_step[0] = w.pool.launch_count() - c0
-            else:
-                graph.replay()
-
         t = time_steps(step, args.steps, dev, barrier)
-    launches = per_step[0] * args.steps  # the graph replays the same launches
-    if ws > 1:
-        tt = torch.tensor([t], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t = float(tt.item())
-    tokens = (PREFILL_TOKENS + DECODE_BATCH) * args.steps
-    value = tokens / t
-    # per-launch kernel times (last timed step's events)
-    dec_ms = statistics.mean(a.elapsed_time(b) for a, b in w.ev_d)
-    pre_ms = statistics.mean(a.elapsed_time(b) for a, b in w.ev_p)
-    # co-run overlap of the two streams in that step: each stream's span
-    # from its first kernel start to its last kernel end; overlap = min / max span
-    span_p = w.ev_p[0][0].elapsed_time(w.ev_p[-1][1])
-    span_d = w.ev_d[0][0].elapsed_time(w.ev_d[-1][1])
-    corun_overlap = {"prefill_stream_ms": span_p, "decode_stream_ms": span_d,
-                     "overlap": min(span_p, span_d) / max(span_p, span_d)}
-    dec_gbs = w.decode_bytes_per_launch() / (dec_ms / 1e3) / 1e9
-    pre_tfs = w.prefill_flops_per_launch() / (pre_ms / 1e3) / 1e12
+    t = max_over_ranks(t, ws, dev)
+    ks = w.kernel_stats()
+    launches = per_step * args.steps
+    value = w.tokens_per_step() * args.steps / t
+    ms_step = t / args.steps * 1e3
     n_p, n_d = w.pool.sm_budgets()
-    dec_total, pre_total = dec_ms * w.L, pre_ms * w.L
-    dominant = "decode" if dec_total >= pre_total else "prefill"
-    roof_dec = {"kernel": "decode_bf16_kernel (split-K paged decode)", "bound": "hbm",
-                "achieved": dec_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": dec_gbs / hbm_peak,
-                "peak_kind": peak_kind, "traffic": ncu_traffic("decode_bf16_kernel"),
-                "traffic_unit": "DRAM bytes per launch (ncu)",
+    if args.tp_mode == "pipelined" and ws > 1 and args.gather == "nccl":
+        n_p, n_d = w._budget(0, "p"), w._budget(0, "d")
+    rec = phase_record(w, n_p, n_d, t / args.steps, ks, pk)
+    dec_ms, pre_ms = ks["decode"]["ms"], ks["prefill"]["ms"]
+    roof_dec = {"kernel": "decode_bf16_kernel / decode_pair_kernel (split-K paged decode)",
+                "bound": "hbm", "achieved": rec["decode_gbs"], "peak": pk["hbm"], "unit": "GB/s",
+                "frac": rec["decode_frac"], "peak_kind": pk["kind"],
+                "traffic": ncu_traffic("decode_bf16_kernel"),
+                "traffic_unit": "DRAM bytes per launch (ncu --set full)",
                 "algorithmic_bytes_per_launch": w.decode_bytes_per_launch(),
-                "avg_launch_ms": dec_ms, "sm_budget": n_d}
-    share = n_p / w.pool.num_sms
-    roof_pre = {"kernel": "prefill_tc_kernel tcgen05 causal GQA (K/V pool write fused)", "bound": "tensor",
-                "achieved": pre_tfs, "peak": bf16_sus, "unit": "TFLOP/s",
-                "frac": pre_tfs / bf16_sus, "frac_share_scaled": pre_tfs / (bf16_sus * share),
-                "peak_kind": f"{peak_kind} sustained", "traffic": ncu_traffic("prefill_tc_kernel"),
-                "traffic_unit": "DRAM bytes per launch (ncu)",
+                "avg_launch_ms": dec_ms, "launches_timed": ks["decode"]["launches"],
+                "timing": "device launch spans (first CTA entry -> last CTA exit) over the K "
+                          "timed graph replays", "sm_budget": n_d}
+    roof_pre = {"kernel": "prefill_tc_kernel tcgen05 causal GQA (K/V pool write fused)",
+                "bound": "tensor", "achieved": rec["prefill_tflops"],
+                "peak": pk["burst"] * n_p / w.pool.num_sms, "unit": "TFLOP/s",
+                "frac": rec["prefill_frac_share_burst"],
+                "frac_whole_gpu_burst": rec["prefill_frac"],
+                "frac_share_scaled_burst": rec["prefill_frac_share_burst"],
+                "frac_share_scaled_sustained": rec["prefill_frac_share_sustained"],
+                "peak_kind": f"{pk['kind']} burst x n_p/148 (the kernel runs at full clocks on "
+                             f"its partition; sustained {pk['sustained']} is a power-limited "
+                             f"full-chip rate)",
+                "traffic": ncu_traffic("prefill_tc_kernel"),
+                "traffic_unit": "DRAM bytes per launch (ncu --set full)",
                 "algorithmic_flops_per_launch": w.prefill_flops_per_launch(),
-                "avg_launch_ms": pre_ms, "sm_budget": n_p}
-    # whole co-run step against HBM: both phases' algorithmic bytes per step / step time.
-    # Decode streams the KV cache and the prefill moves q / o / chunk K/V, all through the one
-    # shared HBM, so this bounds the step however the SMs are split
+                "avg_launch_ms": pre_ms, "launches_timed": ks["prefill"]["launches"],
+                "sm_budget": n_p}
+    dominant = "decode" if dec_ms >= pre_ms else "prefill"
+    consistency = {"decode_kernels_ms_per_step": dec_ms * w.L,
+                   "prefill_kernels_ms_per_step": pre_ms * w.L, "ms_per_step": ms_step,
+                   "ok": max(dec_ms, pre_ms) * w.L <= ms_step * 1.001}
     step_bytes = w.L * (w.decode_bytes_per_launch() + w.prefill_bytes_per_launch())
     step_gbs = step_bytes / (t / args.steps) / 1e9
-    roof_step = {"bound": "hbm", "achieved": step_gbs, "peak": hbm_peak, "unit": "GB/s",
-                 "frac": step_gbs / hbm_peak, "peak_kind": peak_kind,
+    roof_step = {"bound": "hbm", "achieved": step_gbs, "peak": pk["hbm"], "unit": "GB/s",
+                 "frac": step_gbs / pk["hbm"], "peak_kind": pk["kind"],
                  "algorithmic_bytes_per_step": step_bytes}
-    def graphed(fn):  # the baselines get the same CUDA-graph replay as the co-run step
-        if not use_graph:
-            return fn
-        fn()
-        torch.cuda.synchronize(dev)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            fn()
-        g.replay()
-        torch.cuda.synchronize(dev)
-        return g.replay
-
-    # each phase alone on the whole GPU (148 SMs): the kernels' full-chip roofline fractions,
-    # next to the co-run ones above (32 launches + the phase's alloc / free, graph replay)
-    # (the stream is looked up at call time: under graph capture it is the capture stream)
+    corun_streams = {"prefill_stream_ms": ks["prefill"]["stream_ms"],
+                     "decode_stream_ms": ks["decode"]["stream_ms"],
+                     "overlap": rec.get("overlap"),
+                     "note": "first-kernel start to last-kernel end per stream, last replay"}
+    # ---- each phase alone on all SMs (graph replay) and the time-sliced / (100,100) baselines
     nsm = w.pool.num_sms
-    t_pi = time_steps(graphed(lambda: w.phase_prefill(nsm, stream=torch.cuda.current_stream(dev))),
-                      3, dev, barrier) / 3
-    t_di = time_steps(graphed(lambda: w.phase_decode(nsm, stream=torch.cuda.current_stream(dev))),
-                      3, dev, barrier) / 3
-    pre_iso = w.prefill_flops_per_launch() * w.L / t_pi / 1e12
-    dec_iso = w.decode_bytes_per_launch() * w.L / t_di / 1e9
-    isolated = {"sm_budget": nsm,
-                "prefill": {"achieved": pre_iso, "unit": "TFLOP/s", "peak": bf16_sus,
-                            "frac": pre_iso / bf16_sus, "ms_per_launch": t_pi / w.L * 1e3},
-                "decode": {"achieved": dec_iso, "unit": "GB/s", "peak": hbm_peak,
-                           "frac": dec_iso / hbm_peak, "ms_per_launch": t_di / w.L * 1e3},
-                "note": "per phase, all SMs, 32-layer graph replay incl. the phase's alloc/free"}
+    iso = {"sm_budget": nsm}
+    for ph, fn in (("prefill", lambda: w.phase_prefill(nsm, stream=torch.cuda.current_stream(dev))),
+                   ("decode", lambda: w.phase_decode(nsm, stream=torch.cuda.current_stream(dev)))):
+        ti, kk = run.time(run.capture(fn), 3)
+        kk = w.kernel_stats(order=(ph,))[ph]
+        if ph == "prefill":
+            a = w.prefill_flops_per_launch() / (kk["ms"] / 1e3) / 1e12
+            iso[ph] = {"achieved": a, "unit": "TFLOP/s", "peak": pk["burst"], "frac": a / pk["burst"],
+                       "frac_sustained": a / pk["sustained"], "ms_per_launch": kk["ms"],
+                       "ms_per_phase_step": ti * 1e3}
+        else:
+            a = w.decode_bytes_per_launch() / (kk["ms"] / 1e3) / 1e9
+            iso[ph] = {"achieved": a, "unit": "GB/s", "peak": pk["hbm"], "frac": a / pk["hbm"],
+                       "ms_per_launch": kk["ms"], "ms_per_phase_step": ti * 1e3}
     extra = {}
     if args.extra:
-
-        ts = time_steps(graphed(w.serial_step), 3, dev, barrier) / 3
-        tu = time_steps(graphed(w.uncontrolled_step), 3, dev, barrier) / 3
-        extra = {"serial_ms": ts * 1e3, "uncontrolled_100_100_ms": tu * 1e3,
-                 "corun_ms": t / args.steps * 1e3,
+        ts = run.time(run.capture(w.serial_step), 3)[0]
+        tu = run.time(run.capture(w.uncontrolled_step), 3)[0]
+        extra = {"serial_ms": ts * 1e3, "uncontrolled_100_100_ms": tu * 1e3, "corun_ms": ms_step,
                  "speedup_vs_serial": ts / (t / args.steps),
                  "speedup_vs_100_100": tu / (t / args.steps)}
+    w.pool.set_spans(None)
     e2e = None
     if not args.no_e2e:
         ee = E2E(w)
         for _ in range(2):
             ee.step(x, y)
-        te = time_steps(lambda: ee.step(x, y), max(2, min(args.steps, 5)), dev, barrier)
-        te /= max(2, min(args.steps, 5))
-        if ws > 1:
-            tt = torch.tensor([te], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            te = float(tt.item())
-        e2e = {"value": (PREFILL_TOKENS + DECODE_BATCH) / te, "unit": "tokens/s",
+        ne = max(2, min(args.steps, 5))
+        te = max_over_ranks(time_steps(lambda: ee.step(x, y), ne, dev, barrier) / ne, ws, dev)
+        e2e = {"value": w.tokens_per_step() / te, "unit": "tokens/s",
                "h2d_bytes_per_step": ee.h2d, "d2h_bytes_per_step": ee.d2h,
-               "ms_per_step": te * 1e3}
+               "ms_per_step": te * 1e3,
+               "pcie_gbs_effective": (ee.h2d + ee.d2h) / te / 1e9}
+        del ee
+    dp = None
+    if ws > 1 and not args.no_dp:
+        # DP-replica reference (SURVEY §8(e) "Replicas"): every rank runs the TP-1 workload
+        # on its own GPU, no collective; ideal weak scaling
+        full = Workload(shape, 1, dev, seed=1020 + rank)
+        rr = Runner(full, dev, barrier, not args.no_graph, ws)
+        td = rr.time(rr.capture(lambda: full.corun_step(x, y)), 5)[0]
+        dp = {"value": ws * full.tokens_per_step() / td, "unit": "tokens/s",
+              "ms_per_step": td * 1e3, "scaling": "weak", "replicas": ws,
+              "split": {"x": x, "y": y}, "cuda_graph": rr.use_graph}
+        del rr, full
+    graph_used, graph_error = run.use_graph, run.graph_error
+    secondary = {}
+    if ws == 1 and not args.no_secondary:
+        del run, step
+        for name, fn in (("block16", secondary_block16), ("cfg3_llama70b", secondary_cfg3),
+                         ("cfg4_longctx", secondary_cfg4), ("cfg5_mla", secondary_cfg5)):
+            try:
+                secondary[name] = fn(args, dev, pk)
+            except Exception as e:  # a secondary field never voids the headline
+                secondary[name] = {"error": repr(e)[:300]}
+            torch.cuda.synchronize(dev)
+            torch.cuda.empty_cache()
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        v, sample, _ = oracle_sample_rate(shape, threads)
-        cpu = {"value": v, "unit": "tokens/s", "cores": threads, "kind": "oracle",
-               "sample": sample}
+        cpu = cpu_baseline(shape)
     if rank == 0:
         line = {
-            "metric": "co-run prefill+decode attention tokens/s (32-layer stack)",
+            "metric": METRIC,
             "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": W,
-            "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {**workload_config(shape, ws, args.gather),
+            "config": {**workload_config(shape, ws, args.gather, args.tp_mode),
                        "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d}},
             "roofline": roof_dec if dominant == "decode" else roof_pre,
             "roofline_decode": roof_dec, "roofline_prefill": roof_pre, "roofline_step": roof_step,
-            "corun_streams": corun_overlap, "isolated_full_chip": isolated,
-            "decode_tokens_per_s": DECODE_BATCH * args.steps / t,
-            "prefill_tokens_per_s": PREFILL_TOKENS * args.steps / t,
+            "kernel_time_check": consistency,
+            "corun_streams": corun_streams, "isolated_full_chip": iso,
+            "decode_tokens_per_s": w.B * args.steps / t,
+            "prefill_tokens_per_s": w.C * args.steps / t,
+            "best_target_split": tgt,
+            "target_met": bool(tgt and tgt["target_score"] >= 1.0),
             "sweep": sweep, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
-            "gpu_launches": launches, "cuda_graph": graph is not None, "extra": extra or None,
+            "gpu_launches": launches, "cuda_graph": graph_used, "graph_error": graph_error,
+            "dp_replicas": dp, "extra": extra or None, **secondary,
         }
+        if ws > 1:
+            line["tp"] = {"mode": args.tp_mode, "gather": args.gather,
+                          "nccl_max_ctas": args.nccl_max_ctas}
         print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()

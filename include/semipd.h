@@ -215,6 +215,19 @@ int64_t semipd_launch_count(semipd_pool_t pool);
 semipd_status semipd_set_trace(semipd_pool_t pool, int32_t* buf, int32_t cap,
                                int32_t* counter_dev);
 
+/* Device-side launch timing (measurement hook; SURVEY §8(d) "Timing").  buf: device array of
+ * cap x 8 uint64, zero-filled by the caller, owned by the caller.  From this call on, the
+ * i-th attention kernel launched through this pool (the tcgen05 / split-K / MLA kernels of
+ * either phase; the generic CUDA-core path records nothing) uses record i % cap, and every CTA stamps %globaltimer at entry and after its last barrier; the CTA
+ * that finishes last folds the launch into the record:
+ *   [2] += end - start (ns, start = first CTA entry, end = last CTA exit), [3] += 1,
+ *   [5] / [6] = that launch's start / end; [0], [1], [4] are running state (zero between
+ *   launches).
+ * A launch captured into a CUDA graph keeps its record, so [2] / [3] average it over the
+ * replays.  The host cursor restarts at 0 with every call.  buf = NULL disables (default).
+ * Errors: INVALID (NULL pool, cap <= 0 with a buffer). */
+semipd_status semipd_set_spans(semipd_pool_t pool, uint64_t* buf, int32_t cap);
+
 /* ---- Head-output all-gather over peer memory (TP by KV head) ----
  * P:232 §4.5: the prefill workers (and, separately, the decode workers) of a TP group
  * exchange only among themselves.  With attention sharded by KV head the one exchange is
@@ -266,14 +279,21 @@ semipd_status semipd_peer_gather(const void* src, size_t bytes, void* const* dst
  * before it, so no peer is still reading the buffer, and which = 1 ("landed") after it, which
  * fences the kernel's stores and waits until every peer's have landed here.  Only the bf16
  * split-K decode kernels support peers: other decode paths return UNSUPPORTED, row-major
- * output INVALID.  Errors: INVALID (NULL pool, n out of range, NULL / unaligned pointer).
+ * output INVALID.  `tokens` (> 0 when n > 0) is the token count B the gathered buffers were
+ * sized for ([Hq, tokens, dv]): the peer offsets depend on it, so a later decode call whose
+ * batch differs returns INVALID (and launches nothing) instead of storing at wrong offsets or
+ * past a peer's buffer.  Errors: INVALID (NULL pool, n out of range, NULL / unaligned pointer,
+ * tokens <= 0 with n > 0).
  * semipd_peer_handshake: one of the two handshakes semipd_peer_gather performs (flag arrays
  * as there; which: 0 = ready, 1 = landed), as one batched stream-memory-operation call. */
-semipd_status semipd_set_decode_peers(semipd_pool_t pool, void* const* peer_out, int32_t n);
+semipd_status semipd_set_decode_peers(semipd_pool_t pool, void* const* peer_out, int32_t n,
+                                      int32_t tokens);
 /* The same for semipd_prefill_attn (tcgen05 GQA path only; 16-byte aligned pointers): full
  * output tiles then take the direct 16-byte-store epilogue instead of the TMA store, and
- * every output vector also goes to each peer. */
-semipd_status semipd_set_prefill_peers(semipd_pool_t pool, void* const* peer_out, int32_t n);
+ * every output vector also goes to each peer.  `tokens` = the total_q the gathered buffers
+ * were sized for; a prefill call with another total_q returns INVALID. */
+semipd_status semipd_set_prefill_peers(semipd_pool_t pool, void* const* peer_out, int32_t n,
+                                       int32_t tokens);
 semipd_status semipd_peer_handshake(uint32_t* const* peer_flags, uint32_t* my_flags,
                                     int32_t world, int32_t rank, int32_t which, semipd_stream_t s);
 

@@ -80,14 +80,15 @@ def lib():
                 "semipd_decode_workspace_bytes": (sz, [vp, i32, i32, i32]),
                 "semipd_launch_count": (i64, [vp]),
                 "semipd_set_trace": (i32, [vp, vp, i32, vp]),
+                "semipd_set_spans": (i32, [vp, vp, i32]),
                 "semipd_version": (ctypes.c_char_p, []),
                 "semipd_ipc_alloc": (i32, [sz, P(vp), vp]),
                 "semipd_ipc_free": (i32, [vp]),
                 "semipd_ipc_open": (i32, [vp, P(vp)]),
                 "semipd_ipc_close": (i32, [vp]),
                 "semipd_peer_gather": (i32, [vp, sz, P(vp), P(vp), vp, i32, i32, vp]),
-                "semipd_set_decode_peers": (i32, [vp, P(vp), i32]),
-                "semipd_set_prefill_peers": (i32, [vp, P(vp), i32]),
+                "semipd_set_decode_peers": (i32, [vp, P(vp), i32, i32]),
+                "semipd_set_prefill_peers": (i32, [vp, P(vp), i32, i32]),
                 "semipd_peer_handshake": (i32, [P(vp), vp, i32, i32, i32, vp]),
                 "semipd_rope": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, f64,
                                       f64, f64, f64, i32, vp]),
@@ -144,8 +145,15 @@ def rope_(q, k, positions, cfg: RopeConfig | None = None, stream=None, rot_offse
     if dt is None:
         raise SemipdError("semipd_rope", UNSUPPORTED)
     for x in (q, k):
-        if x is not None and not x.is_contiguous():
+        if x is not None and (not x.is_contiguous() or x.dim() != 3 or x.dtype != t.dtype or
+                              x.device != t.device or x.shape[0] != t.shape[0] or
+                              x.shape[2] != t.shape[2]):
             raise SemipdError("semipd_rope", INVALID)
+    # positions: int32, one per token, on the rows' device (torch.arange defaults to int64,
+    # which the kernel would misread)
+    if (positions is None or positions.dtype != torch.int32 or positions.device != t.device or
+            positions.numel() < t.shape[0] or not positions.is_contiguous()):
+        raise SemipdError("semipd_rope", INVALID)
     _check("semipd_rope", lib().semipd_rope(
         _ptr(q), _ptr(k), _ptr(positions), int(t.shape[0]), 0 if q is None else int(q.shape[1]),
         0 if k is None else int(k.shape[1]), int(t.shape[2]), int(rot_offset),
@@ -276,18 +284,22 @@ class KVPool:
                                                                      ctypes.byref(b)))
         return a.value, b.value
 
-    def set_decode_peers(self, peer_ptrs):
+    def set_decode_peers(self, peer_ptrs, tokens: int = 0):
         """Fuse the TP head all-gather into the decode epilogue: later decode calls also store
         each output vector at these device addresses (C ABI ``semipd_set_decode_peers``;
-        ``tp.PeerGather.peer_shard_ptrs`` gives them).  [] clears."""
+        ``tp.PeerGather.peer_shard_ptrs`` gives them).  ``tokens`` = the batch the gathered
+        buffers hold; a decode call with another batch is refused.  [] clears."""
         arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[int(x) for x in peer_ptrs])
-        _check("semipd_set_decode_peers", lib().semipd_set_decode_peers(self.h, arr, len(peer_ptrs)))
+        _check("semipd_set_decode_peers", lib().semipd_set_decode_peers(
+            self.h, arr, len(peer_ptrs), int(tokens)))
 
-    def set_prefill_peers(self, peer_ptrs):
+    def set_prefill_peers(self, peer_ptrs, tokens: int = 0):
         """Fuse the TP head all-gather into the prefill epilogue (C ABI
-        ``semipd_set_prefill_peers``); [] clears."""
+        ``semipd_set_prefill_peers``); ``tokens`` = the total_q the gathered buffers hold.
+        [] clears."""
         arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[int(x) for x in peer_ptrs])
-        _check("semipd_set_prefill_peers", lib().semipd_set_prefill_peers(self.h, arr, len(peer_ptrs)))
+        _check("semipd_set_prefill_peers", lib().semipd_set_prefill_peers(
+            self.h, arr, len(peer_ptrs), int(tokens)))
 
     def launch_count(self) -> int:
         return int(lib().semipd_launch_count(self.h))
@@ -295,6 +307,14 @@ class KVPool:
     def set_trace(self, buf: torch.Tensor | None, counter: torch.Tensor | None = None):
         cap = 0 if buf is None else buf.numel() // 4
         _check("semipd_set_trace", lib().semipd_set_trace(self.h, _ptr(buf), cap, _ptr(counter)))
+
+    def set_spans(self, buf: torch.Tensor | None):
+        """Device-side launch timing (C ABI ``semipd_set_spans``): ``buf`` is a zeroed int64
+        tensor [cap, 8] on the pool's device; the i-th attention launch from now on folds its
+        first-CTA-entry -> last-CTA-exit time into row i % cap (col 2: total ns, col 3:
+        launches, cols 5 / 6: the last launch's start / end).  None disables."""
+        cap = 0 if buf is None else buf.shape[0]
+        _check("semipd_set_spans", lib().semipd_set_spans(self.h, _ptr(buf), cap))
 
     # ---------------------------------------------------------------- attention
     def prefill_attn(self, layer: int, q, k_new, v_new, cu_seqlens, req_ids, prefix_lens,

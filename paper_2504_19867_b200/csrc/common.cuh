@@ -21,6 +21,41 @@ SPD_DEV uint32_t smid() {
     return r;
 }
 
+SPD_DEV unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ------------------------------------------------------------------ launch spans
+// Device-side launch timing (semipd_set_spans): every CTA's thread 0 calls span_begin at
+// entry and span_end after the CTA's final __syncthreads.  Record (8 x u64, zero-initialised):
+//   [0] ~min(start)  [1] max(end)  [2] sum of durations (ns)  [3] launches
+//   [4] CTAs done in the running launch  [5] last start  [6] last end
+// The CTA that finishes last folds the launch into [2] / [3], keeps [5] / [6] and resets
+// [0], [1], [4], so a launch captured in a CUDA graph accumulates over its replays.
+SPD_DEV void span_begin(unsigned long long* rec) {
+    if (rec) atomicMax(rec + 0, ~globaltimer_ns());
+}
+SPD_DEV void span_end(unsigned long long* rec) {
+    if (!rec) return;
+    atomicMax(rec + 1, globaltimer_ns());
+    __threadfence();
+    if (atomicAdd(rec + 4, 1ull) == gridDim.x - 1) {
+        __threadfence();
+        volatile unsigned long long* v = rec;
+        const unsigned long long t0 = ~v[0], t1 = v[1];
+        rec[2] += t1 - t0;
+        rec[3] += 1;
+        rec[5] = t0;
+        rec[6] = t1;
+        rec[0] = 0;
+        rec[1] = 0;
+        rec[4] = 0;
+        __threadfence();
+    }
+}
+
 // ------------------------------------------------------------------ mbarrier
 SPD_DEV void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)

@@ -61,6 +61,7 @@ struct DecodeParams {
     int* ws_cnt;                 // [B][Hkv]
     unsigned* sched;             // [2]: next unit, finished CTAs
     int* status;
+    unsigned long long* span;  // semipd_set_spans record of this launch (or null)
     int B, Hq, Hkv, G, lg_bs, MBR, N_B, S_max, n_units, out_head_major;
     // TP head all-gather fused into the epilogue: every output vector is also
     // stored to each peer's gathered buffer (peer-mapped, already offset to this rank's shard)
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
             mbar_init(uempty + i, CW);
         }
         fence_mbar_init();
+        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -696,6 +698,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        span_end(p.span);
         __threadfence();
         const unsigned done = atomicAdd(p.sched + 1, 1u);
         if (done == gridDim.x - 1) {  // last CTA: reset the work counter for the next launch
@@ -755,6 +758,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             mbar_init(uempty + i, 2 * P_NCW);
         }
         fence_mbar_init();
+        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -1092,6 +1096,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        span_end(p.span);
         __threadfence();
         const unsigned done = atomicAdd(p.sched + 1, 1u);
         if (done == gridDim.x - 1) {
@@ -1164,6 +1169,9 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
                                   spd_mla_tc_ok(pool, num_q_heads) ||
                                   spd_mla_decode_ok(pool, num_q_heads)))
         return pool->dec_n_peers > 0 && !out_head_major ? SEMIPD_ERR_INVALID : SEMIPD_ERR_UNSUPPORTED;
+    // the peer offsets were fixed for the gathered buffers' batch: any other batch would store
+    // at wrong head / token positions or past a peer's buffer
+    if (pool->dec_n_peers > 0 && batch != pool->dec_peer_tokens) return SEMIPD_ERR_INVALID;
     if (spd_mla_tc_ok(pool, num_q_heads))  // absorbed MLA latent cache, 64-token pages (cfg 5)
         return spd_launch_decode_mla_tc(pool, layer, q, k_new, req_ids, ctx_lens, batch,
                                         max_ctx_len, num_q_heads, softmax_scale, out,
@@ -1202,6 +1210,7 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     prm.ws_l = w.l;
     prm.ws_acc = w.acc;
     prm.status = status_dev;
+    prm.span = spd_next_span(pool);
     prm.B = batch;
     prm.Hq = num_q_heads;
     prm.Hkv = c.num_kv_heads;
@@ -1271,12 +1280,15 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     return SEMIPD_OK;
 }
 
-semipd_status semipd_set_decode_peers(semipd_pool_t pool, void* const* peer_out, int32_t n) {
-    if (!pool || n < 0 || n > SEMIPD_MAX_PEERS - 1 || (n > 0 && !peer_out)) return SEMIPD_ERR_INVALID;
+semipd_status semipd_set_decode_peers(semipd_pool_t pool, void* const* peer_out, int32_t n,
+                                      int32_t tokens) {
+    if (!pool || n < 0 || n > SEMIPD_MAX_PEERS - 1 || (n > 0 && (!peer_out || tokens <= 0)))
+        return SEMIPD_ERR_INVALID;
     for (int k = 0; k < n; ++k)
         if (!peer_out[k] || reinterpret_cast<uintptr_t>(peer_out[k]) % 8) return SEMIPD_ERR_INVALID;
     for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k) pool->dec_peers[k] = k < n ? peer_out[k] : nullptr;
     pool->dec_n_peers = n;
+    pool->dec_peer_tokens = n > 0 ? tokens : 0;
     return SEMIPD_OK;
 }
 

@@ -54,6 +54,7 @@ struct MlaParams {
     int* ws_cnt;              // [B]
     unsigned* sched;
     int* status;
+    unsigned long long* span;  // semipd_set_spans record of this launch (or null)
     int B, lg_bs, MBR, N_B, S_max, n_units, out_head_major, G;
     float scale_log2;
     SpdTrace trace;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(uempty + i, NCW);
         }
         fence_mbar_init();
+        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        span_end(p.span);
         __threadfence();
         const unsigned done = atomicAdd(p.sched + 1, 1u);
         if (done == gridDim.x - 1) {
@@ -411,6 +414,7 @@ semipd_status spd_launch_decode_mla(semipd_pool_t pool, int layer, const void* q
     prm.ws_l = w.l;
     prm.ws_acc = w.acc;
     prm.status = status_dev;
+    prm.span = spd_next_span(pool);
     prm.B = batch;
     prm.lg_bs = __builtin_ctz((unsigned)pool->cfg.block_size);
     prm.MBR = pool->cfg.max_blocks_per_req;

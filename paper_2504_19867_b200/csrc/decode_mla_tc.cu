@@ -91,6 +91,7 @@ struct TcParams {
     int* ws_cnt;              // [B]
     unsigned* sched;
     int* status;
+    unsigned long long* span;  // semipd_set_spans record of this launch (or null)
     int B, MBR, N_B, S_max, n_units, out_head_major, G, S_fill;
     float scale_log2;
     SpdTrace trace;
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_init(&bar.q_full, 1);
         mbar_init(&bar.q_empty, 1);
         fence_mbar_init();
+        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -716,6 +718,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_dealloc(tmem, TM_COLS);
     }
     if (threadIdx.x == 0) {
+        span_end(p.span);
         __threadfence();
         const unsigned done = atomicAdd(p.sched + 1, 1u);
         if (done == gridDim.x - 1) {
@@ -781,6 +784,7 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
     prm.ws_l = w.l;
     prm.ws_acc = w.acc;
     prm.status = status_dev;
+    prm.span = spd_next_span(pool);
     prm.B = batch;
     prm.MBR = pool->cfg.max_blocks_per_req;
     prm.N_B = pool->cfg.num_blocks;

@@ -51,8 +51,10 @@ struct semipd_pool {
     // decode epilogue peer stores (semipd_set_decode_peers; TP gather fused into the kernel)
     void* dec_peers[SEMIPD_MAX_PEERS - 1] = {};
     int dec_n_peers = 0;
+    int dec_peer_tokens = 0;  // batch the decode peers' gathered buffers were sized for
     void* pre_peers[SEMIPD_MAX_PEERS - 1] = {};  // semipd_set_prefill_peers
     int pre_n_peers = 0;
+    int pre_peer_tokens = 0;  // total_q the prefill peers' gathered buffers were sized for
     // MLA latent pool (kv_shared): 4-D (64 cols, rows, dk/64 blocks, pages), box 32 rows x all
     // column blocks (one 36 KiB TMA per 32-key stage at dk = 576)
     std::vector<CUtensorMap> mla_kmap;
@@ -66,6 +68,9 @@ struct semipd_pool {
     int* trace_buf = nullptr;
     int trace_cap = 0;
     int* trace_ctr = nullptr;
+    unsigned long long* span_buf = nullptr;  // semipd_set_spans: 8 x u64 per launch slot
+    int span_cap = 0;
+    int span_next = 0;
     void* timeline = nullptr;      // debug builds (SPD_TIMELINE): prefill clock64 stamps
     int* timeline_ctr = nullptr;
 
@@ -83,6 +88,14 @@ struct SpdTrace {
 };
 
 inline SpdTrace spd_trace(const semipd_pool* p) { return SpdTrace{p->trace_buf, p->trace_cap, p->trace_ctr}; }
+
+// launch-span slot of the next attention launch (semipd_set_spans), or nullptr when off
+inline unsigned long long* spd_next_span(semipd_pool* p) {
+    if (!p->span_buf || p->span_cap <= 0) return nullptr;
+    unsigned long long* r = p->span_buf + 8 * (size_t)(p->span_next % p->span_cap);
+    p->span_next += 1;
+    return r;
+}
 
 // budget resolution (host): >0 cap, 0 partition, -1 non-persistent
 inline int spd_resolve_budget(const semipd_pool* p, int requested, bool prefill) {

@@ -92,7 +92,10 @@ semipd_status semipd_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out) {
     void* p = nullptr;
     if (cudaMalloc(&p, bytes) != cudaSuccess) return SEMIPD_ERR_CUDA;
     cudaIpcMemHandle_t h;
-    if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+    // cudaMemset is asynchronous to the host: finish the zeroing before the handle leaves
+    // this call, or a late memset could erase a peer's first ready / landed flag
+    if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+        cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
         cudaFree(p);
         return SEMIPD_ERR_CUDA;
     }

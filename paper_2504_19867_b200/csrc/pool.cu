@@ -379,6 +379,14 @@ semipd_status semipd_set_trace(semipd_pool_t pool, int32_t* buf, int32_t cap, in
     return SEMIPD_OK;
 }
 
+semipd_status semipd_set_spans(semipd_pool_t pool, uint64_t* buf, int32_t cap) {
+    if (!pool || (buf && cap <= 0)) return SEMIPD_ERR_INVALID;
+    pool->span_buf = reinterpret_cast<unsigned long long*>(buf);
+    pool->span_cap = buf ? cap : 0;
+    pool->span_next = 0;
+    return SEMIPD_OK;
+}
+
 }  // extern "C"
 
 #ifdef SPD_TIMELINE

@@ -57,6 +57,7 @@ struct PmParams {
     const int* bt;
     __nv_bfloat16* out;  // [T][Hq][512] or [Hq][T][512]
     int* status;
+    unsigned long long* span;  // semipd_set_spans record of this launch (or null)
     unsigned* sched;
     int n, T, Hq, maxqb, n_units, MBR, N_B, out_head_major;
     float scale_log2;
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_init(&bar.q_full, 1);
         mbar_init(&bar.q_empty, 1);
         fence_mbar_init();
+        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -413,6 +415,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_dealloc(tmem, TM_COLS);
     }
     if (threadIdx.x == 0) {
+        span_end(p.span);
         __threadfence();
         const unsigned done = atomicAdd(p.sched + 1, 1u);
         if (done == gridDim.x - 1) {
@@ -456,6 +459,7 @@ semipd_status spd_launch_prefill_mla(semipd_pool_t pool, int layer, const void* 
     prm.bt = pool->bt;
     prm.out = static_cast<__nv_bfloat16*>(out);
     prm.status = status_dev;
+    prm.span = spd_next_span(pool);
     prm.sched = &pool->st->sched[0];
     prm.n = n;
     prm.T = total_q;

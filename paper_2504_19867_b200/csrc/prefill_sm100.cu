@@ -70,6 +70,7 @@ struct PrefillParams {
     const int* bt;
     __nv_bfloat16* out;
     int* status;
+    unsigned long long* span;  // semipd_set_spans record of this launch (or null)
     unsigned* sched;
     int n, T, Hq, Hkv, G, TQ, pairs_max, n_units, lg_bs, box_rows, MBR, N_B, out_head_major;
     // TP head all-gather fused into the epilogue: full tiles take the direct
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(NT, 1)
             mbar_init(&sm.uempty[s], 1 + 8 + 1);  // MMA warp + 8 softmax warps + V producer
         }
         fence_mbar_init();
+        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -666,7 +668,7 @@ __global__ void __launch_bounds__(NT, 1)
             const int hq = d.g * p.G + (r % p.G);
             const int trow = d.qrow0 + t * p.TQ + tok;
             bool o_released = false;
-            if (kEpiDirect && d.tv[t] == p.TQ) {
+            if (!PEERS && kEpiDirect && d.tv[t] == p.TQ) {
                 // full tile: O -> registers (O's TMEM is released to the next unit's PV at
                 // once), then per 64-column half: rows -> swizzled smem staging -> coalesced
                 // 16-byte global stores, 8 threads per 128-byte row segment (no TMA store: its
@@ -818,6 +820,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
 #endif
     if (threadIdx.x == 0) {
+        span_end(p.span);
         __threadfence();
         const unsigned done = atomicAdd(p.sched + 1, 1u);
         if (done == gridDim.x - 1) {
@@ -860,7 +863,8 @@ extern "C" semipd_status semipd_prefill_attn(
         !out)
         return SEMIPD_ERR_INVALID;
     const int budget = spd_resolve_budget(pool, sm_budget, true);
-    if (pool->pre_n_peers > 0 && !out_head_major) return SEMIPD_ERR_INVALID;
+    if (pool->pre_n_peers > 0 && (!out_head_major || total_q != pool->pre_peer_tokens))
+        return SEMIPD_ERR_INVALID;
     if (pool->pre_n_peers > 0 &&
         (!fast_path_ok(pool, num_q_heads) || spd_mla_prefill_ok(pool, num_q_heads)))
         return SEMIPD_ERR_UNSUPPORTED;
@@ -892,6 +896,7 @@ extern "C" semipd_status semipd_prefill_attn(
     for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k)
         prm.peers[k] = k < pool->pre_n_peers ? static_cast<__nv_bfloat16*>(pool->pre_peers[k]) : nullptr;
     prm.status = status_dev;
+    prm.span = spd_next_span(pool);
     prm.sched = &pool->st->sched[0];
     prm.n = n;
     prm.T = total_q;
@@ -980,11 +985,13 @@ extern "C" semipd_status semipd_prefill_attn(
 }
 
 extern "C" semipd_status semipd_set_prefill_peers(semipd_pool_t pool, void* const* peer_out,
-                                                  int32_t n) {
-    if (!pool || n < 0 || n > SEMIPD_MAX_PEERS - 1 || (n > 0 && !peer_out)) return SEMIPD_ERR_INVALID;
+                                                  int32_t n, int32_t tokens) {
+    if (!pool || n < 0 || n > SEMIPD_MAX_PEERS - 1 || (n > 0 && (!peer_out || tokens <= 0)))
+        return SEMIPD_ERR_INVALID;
     for (int k = 0; k < n; ++k)
         if (!peer_out[k] || reinterpret_cast<uintptr_t>(peer_out[k]) % 16) return SEMIPD_ERR_INVALID;
     for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k) pool->pre_peers[k] = k < n ? peer_out[k] : nullptr;
     pool->pre_n_peers = n;
+    pool->pre_peer_tokens = n > 0 ? tokens : 0;
     return SEMIPD_OK;
 }

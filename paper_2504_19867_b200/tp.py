@@ -43,12 +43,27 @@ class PhaseGroups:
     rank: int
 
     @staticmethod
-    def create(backend: str | None = None) -> "PhaseGroups":
+    def create(backend: str | None = None, max_ctas: int | None = None) -> "PhaseGroups":
+        """Two groups over all ranks.  With NCCL and ``max_ctas``, each communicator is
+        capped to that many CTAs (ncclConfig_t.maxCTAs), so its collectives take a bounded
+        number of SMs out of the phase partition."""
         ws, rank = dist.get_world_size(), dist.get_rank()
         ranks = list(range(ws))
-        pg_p = dist.new_group(ranks, backend=backend)
-        pg_d = dist.new_group(ranks, backend=backend)
+        opts = nccl_options(max_ctas) if backend in (None, "nccl") and max_ctas else None
+        pg_p = dist.new_group(ranks, backend=backend, pg_options=opts)
+        pg_d = dist.new_group(ranks, backend=backend, pg_options=opts)
         return PhaseGroups(pg_p, pg_d, ws, rank)
+
+
+def nccl_options(max_ctas: int):
+    """ProcessGroupNCCL options whose communicator runs at most ``max_ctas`` CTAs per
+    collective (and at least 1)."""
+    if max_ctas < 1:
+        raise ValueError("max_ctas must be >= 1")
+    opts = dist.ProcessGroupNCCL.Options()
+    opts.config.max_ctas = int(max_ctas)
+    opts.config.min_ctas = 1
+    return opts
 
 
 def gather_heads(local_head_major: torch.Tensor, out: torch.Tensor, group) -> torch.Tensor:

@@ -72,7 +72,7 @@ for tpn in (2, 4, 8):
     for mode in ("none", "copy", "fused"):
         for r in range(tpn):
             pools[r].set_decode_peers([outs[k].data_ptr() + r * shard for k in range(tpn) if k != r]
-                                      if mode == "fused" else [])
+                                      if mode == "fused" else [], B)
         round_(mode)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -143,7 +143,7 @@ for tpn in (2, 4, 8):
     for mode in ("none", "copy", "fused"):
         for r in range(tpn):
             pools[r].set_prefill_peers([outs[k].data_ptr() + r * shard for k in range(tpn) if k != r]
-                                       if mode == "fused" else [])
+                                       if mode == "fused" else [], Cp)
         round_p(mode)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()

@@ -26,7 +26,8 @@ def _workload(mod, block_size=64):
     import synth
     w = mod.Workload.__new__(mod.Workload)  # the formulas only read shapes (no pool, no GPU)
     w.shape = dataclasses.replace(synth.CFG2_LLAMA8B, block_size=block_size)
-    w.B, w.ctx, w.C = mod.DECODE_BATCH, mod.DECODE_CTX, mod.PREFILL_TOKENS
+    w.B, w.ctx, w.C, w.P = mod.DECODE_BATCH, mod.DECODE_CTX, mod.PREFILL_TOKENS, 0
+    w.ctx_list = [w.ctx] * w.B
     w.L = w.shape.num_layers
     return w
 
@@ -76,3 +77,41 @@ def test_parallelism_label_names_the_gather():
     assert "NCCL" in bench.workload_config(shape, 4)["parallelism"]
     assert "copy-engine" in bench.workload_config(shape, 4, "peer")["parallelism"]
     assert "epilogues" in bench.workload_config(shape, 8, "fused")["parallelism"]
+
+
+def test_mla_and_prefix_work_formulas():
+    """cfg 5: the latent row (576 x bf16) is read once per key (V aliases K); cfg 4: the
+    prefix adds C*P pairs (SURVEY §8(a) FLOP table: 549.8 GFLOP at P = 0, 3.85 TFLOP at
+    P = 24576 for C = 8192)."""
+    import synth
+    mod = _bench()
+    mla = synth.CFG5_MLA
+    assert mod.decode_bytes(mla, [100, 200]) == (101 + 201) * 576 * 2 + 2 * 16 * (576 + 512) * 2
+    s8 = synth.CFG2_LLAMA8B
+    assert abs(mod.prefill_flops(s8, 8192, 0) / 1e9 - 549.8) < 0.1
+    assert abs(mod.prefill_flops(s8, 8192, 24576) / 1e12 - 3.85) < 0.01
+
+
+def test_phase_record_fractions():
+    """The per-split record divides the algorithmic work by the span-timed launch: decode vs
+    the HBM peak, prefill vs the burst peak scaled by the partition's SM share."""
+    mod = _bench()
+    w = _workload(mod)
+    w.pool = type("P", (), {"num_sms": 148})()
+    pk = {"hbm": 6500.0, "burst": 1600.0, "sustained": 1400.0}
+    ks = {"decode": {"ms": 0.1, "stream_ms": 3.2}, "prefill": {"ms": 0.05, "stream_ms": 1.6}}
+    r = mod.phase_record(w, 74, 74, 3.2e-3, ks, pk)
+    assert abs(r["decode_gbs"] - w.decode_bytes_per_launch() / 1e-4 / 1e9) < 1e-6
+    assert abs(r["decode_frac"] - r["decode_gbs"] / 6500.0) < 1e-12
+    tf = w.prefill_flops_per_launch() / 5e-5 / 1e12
+    assert abs(r["prefill_frac_share_burst"] - tf / 800.0) < 1e-9
+    assert abs(r["prefill_frac_share_sustained"] - tf / 700.0) < 1e-9
+    assert abs(r["overlap"] - 0.5) < 1e-12
+    assert r["target_score"] == min(r["decode_frac"] / 0.7, r["prefill_frac_share_burst"] / 0.5)
+    assert abs(r["tokens_per_s"] - (2048 + 64) / 3.2e-3) < 1e-6
+
+
+def test_nccl_options_cap_ctas():
+    from paper_2504_19867_b200 import tp
+    o = tp.nccl_options(4)
+    assert o.config.max_ctas == 4 and o.config.min_ctas == 1

@@ -11,10 +11,15 @@ operations are the same calls.  Checks are bitwise: a gather moves bytes.
 import os
 import socket
 
+import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
+
+import oracle
+from harness import compare, np_bits
+from paper_2504_19867_b200 import INVALID, SemipdError
 
 pytestmark = pytest.mark.gpu
 
@@ -238,7 +243,7 @@ def test_decode_epilogue_peer_stores_emulated(tpn):
         torch.cuda.synchronize()
         for r in range(tpn):
             shard = hq * B * 128 * 2
-            pools[r].set_decode_peers([outs[k].data_ptr() + r * shard for k in range(tpn) if k != r])
+            pools[r].set_decode_peers([outs[k].data_ptr() + r * shard for k in range(tpn) if k != r], B)
         for r in range(tpn):
             qs, ks, vs, ql, qh = ins[r]
             s = streams[r]
@@ -252,12 +257,28 @@ def test_decode_epilogue_peer_stores_emulated(tpn):
         for r in range(tpn):
             assert torch.equal(outs[r].view(torch.int16), ref.view(torch.int16)), (rnd, r)
         assert all(int(f.abs().sum()) == 0 for f in flags)
+    # the gathered buffers against the fp64 oracle (the plain definition over each request's
+    # contiguous keys: cached context + the appended row), not only against the unsharded run
+    ref64 = np.concatenate([oracle.attention_contig(
+        np_bits(cd.q[b:b + 1]), np_bits(torch.cat([cd.k_ctx[b], cd.k_new[b:b + 1]])),
+        np_bits(torch.cat([cd.v_ctx[b], cd.v_new[b:b + 1]])), -1, sc) for b in range(B)])
+    for r in range(tpn):
+        compare(outs[r].float().cpu().double().numpy().transpose(1, 0, 2), ref64, torch.bfloat16,
+                f"fused decode gather tp{tpn} rank {r}")
     # peers need head-major output
-    pools[0].set_decode_peers([outs[1].data_ptr()])
+    pools[0].set_decode_peers([outs[1].data_ptr()], B)
     with pytest.raises(Exception):
         pools[0].decode_attn(0, ins[0][0], ins[0][1], ins[0][2], rid, ctx_d, max(ctx), sc,
                              torch.empty(B, hq, 128, dtype=torch.bfloat16, device=dev), wss[0],
                              out_head_major=False)
+    # the peer offsets were fixed for batch B: another batch is refused, nothing launches
+    with pytest.raises(SemipdError) as ei:
+        pools[0].decode_attn(0, ins[0][0][:B - 1].contiguous(), ins[0][1][:B - 1].contiguous(),
+                             ins[0][2][:B - 1].contiguous(), rid[:B - 1], ctx_d[:B - 1], max(ctx),
+                             sc, outs[0][ins[0][3]:ins[0][4], :B - 1], wss[0], out_head_major=True)
+    assert ei.value.status == INVALID
+    with pytest.raises(SemipdError):  # tokens must be given with peers
+        pools[0].set_decode_peers([outs[1].data_ptr()], 0)
     pools[0].set_decode_peers([])
 
 
@@ -308,7 +329,7 @@ def test_prefill_epilogue_peer_stores_emulated(tpn):
                     pc.v_new[:, kl:kh].contiguous().to(dev), ql, qh))
     shard = hq * C * 128 * 2
     for r in range(tpn):
-        pools[r].set_prefill_peers([outs[k].data_ptr() + r * shard for k in range(tpn) if k != r])
+        pools[r].set_prefill_peers([outs[k].data_ptr() + r * shard for k in range(tpn) if k != r], C)
     fl = (ctypes.c_void_p * tpn)(*[f.data_ptr() for f in flags])
     L = lib()
     torch.cuda.synchronize()
@@ -324,3 +345,17 @@ def test_prefill_epilogue_peer_stores_emulated(tpn):
     for r in range(tpn):
         assert torch.equal(outs[r].view(torch.int16), ref.view(torch.int16)), r
     assert all(int(f.abs().sum()) == 0 for f in flags)
+    # every rank's gathered buffer against the fp64 oracle (bottom-right causal over the
+    # paged prefix + the chunk, all 64 heads), not only against the unsharded kernel
+    ref64 = oracle.attention_contig(np_bits(pc.q), np_bits(torch.cat([pc.k_prefix[0], pc.k_new])),
+                                    np_bits(torch.cat([pc.v_prefix[0], pc.v_new])), P, sc)
+    for r in range(tpn):
+        compare(outs[r].float().cpu().double().numpy().transpose(1, 0, 2), ref64, torch.bfloat16,
+                f"fused prefill gather tp{tpn} rank {r}")
+    # another total_q than the gathered buffers hold is refused
+    with pytest.raises(SemipdError) as ei:
+        qs, ks, vs, ql, qh = ins[0]
+        pools[0].prefill_attn(0, qs[:C - 1].contiguous(), ks[:C - 1].contiguous(),
+                              vs[:C - 1].contiguous(), i32([0, C - 1]), rid, pre, C - 1, C - 1, sc,
+                              outs[0][ql:qh, :C - 1], out_head_major=True)
+    assert ei.value.status == INVALID

@@ -324,6 +324,24 @@ semipd_status semipd_rope(void* q, void* k, const int32_t* positions, int32_t nu
                           double theta, double factor, double low_freq_factor,
                           double high_freq_factor, int32_t original_max_pos, semipd_stream_t s);
 
+/* ---- RoPE fused with the K/V write of the attention calls ----
+ * semipd_set_rope: from now on, every semipd_prefill_attn / semipd_decode_attn on this pool
+ * first rotates the step's new rows exactly as semipd_rope would (same definition, same fp64
+ * angles, same fp32 rotation: bit-identical rows) at the positions the call's layout implies
+ *   prefill: row t of request r (chunk-relative) sits at prefix_lens[r] + t   (R4)
+ *   decode:  request b's new row sits at ctx_lens[b]                           (R5)
+ * and in the SAME pass writes the rotated k rows (and v) into the pool slots of those
+ * positions, replacing both the separate semipd_rope pass and the attention kernels' own
+ * K/V write / append (one pass over q / k / v instead of two; R28).  q and k_new
+ * are rotated IN PLACE (the attention then reads the rotated rows).  cfg = NULL turns it off.
+ * cfg fields as semipd_rope's arguments; head_dim = the pool's head_dim_k.  Errors: INVALID /
+ * UNSUPPORTED as semipd_rope, plus INVALID for a NULL pool. */
+typedef struct {
+    double theta, factor, low_freq_factor, high_freq_factor;
+    int32_t original_max_pos, rot_offset, rot_dim, interleaved;
+} semipd_rope_config;
+semipd_status semipd_set_rope(semipd_pool_t pool, const semipd_rope_config* cfg);
+
 /* Library version string (host, static). */
 const char* semipd_version(void);
 

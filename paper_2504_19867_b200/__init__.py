@@ -42,6 +42,13 @@ class _Cfg(ctypes.Structure):
         "kv_shared", "max_reqs", "max_blocks_per_req", "dtype", "device", "oplog_words")]
 
 
+class _RopeCfg(ctypes.Structure):
+    _fields_ = [("theta", ctypes.c_double), ("factor", ctypes.c_double),
+                ("low_freq_factor", ctypes.c_double), ("high_freq_factor", ctypes.c_double),
+                ("original_max_pos", ctypes.c_int32), ("rot_offset", ctypes.c_int32),
+                ("rot_dim", ctypes.c_int32), ("interleaved", ctypes.c_int32)]
+
+
 def build(force: bool = False) -> str:
     return _build.build(force=force)
 
@@ -81,6 +88,7 @@ def lib():
                 "semipd_launch_count": (i64, [vp]),
                 "semipd_set_trace": (i32, [vp, vp, i32, vp]),
                 "semipd_set_spans": (i32, [vp, vp, i32]),
+                "semipd_set_rope": (i32, [vp, P(_RopeCfg)]),
                 "semipd_version": (ctypes.c_char_p, []),
                 "semipd_ipc_alloc": (i32, [sz, P(vp), vp]),
                 "semipd_ipc_free": (i32, [vp]),
@@ -315,6 +323,21 @@ class KVPool:
         launches, cols 5 / 6: the last launch's start / end).  None disables."""
         cap = 0 if buf is None else buf.shape[0]
         _check("semipd_set_spans", lib().semipd_set_spans(self.h, _ptr(buf), cap))
+
+    def set_rope(self, cfg: "RopeConfig | None", rot_offset: int = 0, rot_dim: int | None = None,
+                 interleaved: bool = False):
+        """Fuse RoPE into the attention calls' K/V write (C ABI ``semipd_set_rope``): from now
+        on prefill_attn / decode_attn rotate q and k_new IN PLACE at the positions the call
+        implies (prefix + t / ctx) and write the rotated rows into the pool in the same pass.
+        None turns it off."""
+        if cfg is None:
+            _check("semipd_set_rope", lib().semipd_set_rope(self.h, None))
+            return
+        rd = self.cfg.head_dim_k - rot_offset if rot_dim is None else rot_dim
+        c = _RopeCfg(float(cfg.theta), float(cfg.factor), float(cfg.low_freq_factor),
+                     float(cfg.high_freq_factor), int(cfg.original_max_pos), int(rot_offset),
+                     int(rd), int(bool(interleaved)))
+        _check("semipd_set_rope", lib().semipd_set_rope(self.h, ctypes.byref(c)))
 
     # ---------------------------------------------------------------- attention
     def prefill_attn(self, layer: int, q, k_new, v_new, cu_seqlens, req_ids, prefix_lens,

@@ -62,6 +62,7 @@ struct DecodeParams {
     unsigned* sched;             // [2]: next unit, finished CTAs
     int* status;
     unsigned long long* span;  // semipd_set_spans record of this launch (or null)
+    int skip_append;           // 1: the step's K/V rows are already in the pool (RoPE pre-pass)
     int B, Hq, Hkv, G, lg_bs, MBR, N_B, S_max, n_units, out_head_major;
     // TP head all-gather fused into the epilogue: every output vector is also
     // stored to each peer's gathered buffer (peer-mapped, already offset to this rank's shard)
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
             // fused append of this step's K/V at slot ctx (last split only, bit-exact): the
             // rows are loaded now and stored right before the TMA of the stage holding slot
             // ctx (lanes 0-15 K, 16-31 V, 16 B each), then handed to the async proxy
-            const bool append = d.s == d.S - 1;
+            const bool append = d.s == d.S - 1 && !p.skip_append;
             const int app_stage = (ctx - d.k0) / KPS;
             uint4 app_v = make_uint4(0, 0, 0, 0);
             if (append) {
@@ -822,7 +823,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             const int ctx = __ldg(p.ctx_lens + d.b);
             const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
             const int last_page = ctx >> p.lg_bs;
-            if (d.s == d.S - 1) {
+            if (d.s == d.S - 1 && !p.skip_append) {
                 // fused append of the unit's heads' K and V rows at slot ctx (16 B per lane per
                 // copy; MODE 0: lanes 16-31 take the second head, MODE 1: they take V)
                 const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
@@ -1172,6 +1173,14 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     // the peer offsets were fixed for the gathered buffers' batch: any other batch would store
     // at wrong head / token positions or past a peer's buffer
     if (pool->dec_n_peers > 0 && batch != pool->dec_peer_tokens) return SEMIPD_ERR_INVALID;
+    if (pool->rope_on) {
+        // RoPE of q / k_new (in place) at position ctx, fused with the append of the rotated
+        // rows (R28): the attention kernels below skip their own append
+        semipd_status r = spd_launch_rope_write(pool, layer, const_cast<void*>(q),
+                                                const_cast<void*>(k_new), v_new, nullptr, req_ids,
+                                                ctx_lens, batch, batch, num_q_heads, status_dev, st);
+        if (r != SEMIPD_OK) return r;
+    }
     if (spd_mla_tc_ok(pool, num_q_heads))  // absorbed MLA latent cache, 64-token pages (cfg 5)
         return spd_launch_decode_mla_tc(pool, layer, q, k_new, req_ids, ctx_lens, batch,
                                         max_ctx_len, num_q_heads, softmax_scale, out,
@@ -1182,9 +1191,11 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
                                      ws_bytes, budget, status_dev, st);
     if (!fast_path_ok(pool, num_q_heads)) {
         // generic CUDA-core path: append, then attention (same stream)
-        semipd_status r = spd_launch_kv_write(pool, layer, k_new, v_new, nullptr, req_ids,
-                                              ctx_lens, batch, batch, 1, status_dev, st);
-        if (r != SEMIPD_OK) return r;
+        if (!pool->rope_on) {
+            semipd_status r = spd_launch_kv_write(pool, layer, k_new, v_new, nullptr, req_ids,
+                                                  ctx_lens, batch, batch, 1, status_dev, st);
+            if (r != SEMIPD_OK) return r;
+        }
         return spd_launch_simt_attn(pool, layer, q, nullptr, req_ids, ctx_lens, batch, batch, 1,
                                     num_q_heads, softmax_scale, out, out_head_major, budget,
                                     status_dev, st);
@@ -1211,6 +1222,7 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     prm.ws_acc = w.acc;
     prm.status = status_dev;
     prm.span = spd_next_span(pool);
+    prm.skip_append = pool->rope_on ? 1 : 0;
     prm.B = batch;
     prm.Hq = num_q_heads;
     prm.Hkv = c.num_kv_heads;

@@ -55,6 +55,7 @@ struct MlaParams {
     unsigned* sched;
     int* status;
     unsigned long long* span;  // semipd_set_spans record of this launch (or null)
+    int skip_append;           // 1: the step's latent row is already in the pool (RoPE pre-pass)
     int B, lg_bs, MBR, N_B, S_max, n_units, out_head_major, G;
     float scale_log2;
     SpdTrace trace;
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int ctx = __ldg(p.ctx_lens + d.b);
             const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
             const int last_page = ctx >> p.lg_bs;
-            if (d.s == d.S - 1) {
+            if (d.s == d.S - 1 && !p.skip_append) {
                 // fused append of the step's latent row (576 bf16 = 72 x 16 B) at slot ctx
                 const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
                 if (blk >= 0 && blk < p.N_B) {
@@ -415,6 +416,7 @@ semipd_status spd_launch_decode_mla(semipd_pool_t pool, int layer, const void* q
     prm.ws_acc = w.acc;
     prm.status = status_dev;
     prm.span = spd_next_span(pool);
+    prm.skip_append = pool->rope_on ? 1 : 0;
     prm.B = batch;
     prm.lg_bs = __builtin_ctz((unsigned)pool->cfg.block_size);
     prm.MBR = pool->cfg.max_blocks_per_req;

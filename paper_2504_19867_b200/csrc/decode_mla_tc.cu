@@ -92,6 +92,7 @@ struct TcParams {
     unsigned* sched;
     int* status;
     unsigned long long* span;  // semipd_set_spans record of this launch (or null)
+    int skip_append;           // 1: the step's latent row is already in the pool (RoPE pre-pass)
     int B, MBR, N_B, S_max, n_units, out_head_major, G, S_fill;
     float scale_log2;
     SpdTrace trace;
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int last_page = ctx / PAGE;
             // fused append (last split only): the step's latent row (576 bf16 = 72 x 16 B) goes
             // to slot ctx right before the TMA of the page holding it
-            const bool append = d.s == d.S - 1;
+            const bool append = d.s == d.S - 1 && !p.skip_append;
             uint4 kn[3];
             if (append) {
 #pragma unroll
@@ -785,6 +786,7 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
     prm.ws_acc = w.acc;
     prm.status = status_dev;
     prm.span = spd_next_span(pool);
+    prm.skip_append = pool->rope_on ? 1 : 0;
     prm.B = batch;
     prm.MBR = pool->cfg.max_blocks_per_req;
     prm.N_B = pool->cfg.num_blocks;

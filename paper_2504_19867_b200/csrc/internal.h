@@ -68,6 +68,10 @@ struct semipd_pool {
     int* trace_buf = nullptr;
     int trace_cap = 0;
     int* trace_ctr = nullptr;
+    // semipd_set_rope: RoPE of the step's new q / k rows fused with the K/V write
+    bool rope_on = false;
+    semipd_rope_config rope{};
+    double rope_inv_freq[128] = {};
     unsigned long long* span_buf = nullptr;  // semipd_set_spans: 8 x u64 per launch slot
     int span_cap = 0;
     int span_next = 0;
@@ -165,6 +169,12 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
                                        int batch, int max_ctx_len, int Hq, float scale, void* out,
                                        int out_head_major, void* workspace, size_t ws_bytes,
                                        int budget, int* status_dev, cudaStream_t st);
+// RoPE of q / k_new in place at the rows' positions (prefill: prefix + chunk index; decode:
+// ctx) fused with the K/V write of the rotated rows into the pool (rope.cu)
+semipd_status spd_launch_rope_write(semipd_pool_t p, int layer, void* q, void* k_new,
+                                    const void* v_new, const int* cu_seqlens, const int* req_ids,
+                                    const int* base_pos, int n, int T, int Hq, int* status_dev,
+                                    cudaStream_t s);
 semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new, const void* v_new,
                                   const int* cu_seqlens, const int* req_ids, const int* pos0,
                                   int n, int total_rows, int mode, int* status_dev,

@@ -73,6 +73,7 @@ struct PrefillParams {
     unsigned long long* span;  // semipd_set_spans record of this launch (or null)
     unsigned* sched;
     int n, T, Hq, Hkv, G, TQ, pairs_max, n_units, lg_bs, box_rows, MBR, N_B, out_head_major;
+    int write_kv;  // 0: the chunk's K/V rows are already in the pool (RoPE pre-pass wrote them)
     // TP head all-gather fused into the epilogue: full tiles take the direct
     // 16-byte-store epilogue and every output vector also goes to each peer's gathered buffer
     // (peer-mapped, offset to this rank's head slice)
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(NT, 1)
         // k_new / v_new and prefix pages written by earlier calls, so nothing in this launch
         // reads what this warp writes (the next kernel on the stream does).
         const int r0 = (int)((long long)p.T * blockIdx.x / gridDim.x);
-        const int r1 = (int)((long long)p.T * (blockIdx.x + 1) / gridDim.x);
+        const int r1 = p.write_kv ? (int)((long long)p.T * (blockIdx.x + 1) / gridDim.x) : r0;
         if (r0 < r1) {
             int i = 0, hi = p.n - 1;  // last request with cu[i] <= r0
             while (i < hi) {
@@ -868,7 +869,16 @@ extern "C" semipd_status semipd_prefill_attn(
     if (pool->pre_n_peers > 0 &&
         (!fast_path_ok(pool, num_q_heads) || spd_mla_prefill_ok(pool, num_q_heads)))
         return SEMIPD_ERR_UNSUPPORTED;
-    if (!fast_path_ok(pool, num_q_heads) || spd_mla_prefill_ok(pool, num_q_heads)) {
+    const bool rope = pool->rope_on;
+    if (rope) {
+        // RoPE of q / k_new (in place) at positions prefix + t, fused with the K/V write of the
+        // rotated rows (R28): the attention kernels below skip their own write
+        semipd_status r = spd_launch_rope_write(pool, layer, const_cast<void*>(q),
+                                                const_cast<void*>(k_new), v_new, cu_seqlens_q,
+                                                req_ids, prefix_lens, n, total_q, num_q_heads,
+                                                status_dev, st);
+        if (r != SEMIPD_OK) return r;
+    } else if (!fast_path_ok(pool, num_q_heads) || spd_mla_prefill_ok(pool, num_q_heads)) {
         // K/V write into the pool, stream-ordered before attention reads it (these
         // paths read the chunk's own keys from the pool); the tcgen05 path fuses it
         semipd_status r = spd_launch_kv_write(pool, layer, k_new, v_new, cu_seqlens_q, req_ids,
@@ -900,6 +910,7 @@ extern "C" semipd_status semipd_prefill_attn(
     prm.sched = &pool->st->sched[0];
     prm.n = n;
     prm.T = total_q;
+    prm.write_kv = rope ? 0 : 1;
     prm.Hq = num_q_heads;
     prm.Hkv = c.num_kv_heads;
     prm.G = G;

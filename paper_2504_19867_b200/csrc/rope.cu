@@ -49,6 +49,21 @@ double rope_inv_freq(int i, int d, double theta, double factor, double lf, doubl
     return (1.0 - a) * f / factor + a * f;
 }
 
+// the rotation of one pair in fp32 (shared by rope_kernel and rope_write_kernel, so both
+// produce bit-identical rows)
+template <typename T>
+__device__ __forceinline__ void rot_pair(T& e0, T& e1, float c, float s) {
+    if constexpr (sizeof(T) == 2) {
+        const float x0 = __bfloat162float(e0), x1 = __bfloat162float(e1);
+        e0 = __float2bfloat16_rn(fmaf(x0, c, -x1 * s));
+        e1 = __float2bfloat16_rn(fmaf(x1, c, x0 * s));
+    } else {
+        const float x0 = e0, x1 = e1;
+        e0 = fmaf(x0, c, -x1 * s);
+        e1 = fmaf(x1, c, x0 * s);
+    }
+}
+
 template <typename T, bool INTER>
 __global__ void __launch_bounds__(512) rope_kernel(const __grid_constant__ RopeParams p) {
     constexpr int VEC = 16 / sizeof(T);  // elements per 16-byte vector
@@ -85,17 +100,7 @@ __global__ void __launch_bounds__(512) rope_kernel(const __grid_constant__ RopeP
         cs[half + i] = (float)s;
     }
     __syncthreads();
-    auto rot = [](T& e0, T& e1, float c, float s) {
-        if constexpr (sizeof(T) == 2) {
-            const float x0 = __bfloat162float(e0), x1 = __bfloat162float(e1);
-            e0 = __float2bfloat16_rn(fmaf(x0, c, -x1 * s));
-            e1 = __float2bfloat16_rn(fmaf(x1, c, x0 * s));
-        } else {
-            const float x0 = e0, x1 = e1;
-            e0 = fmaf(x0, c, -x1 * s);
-            e1 = fmaf(x1, c, x0 * s);
-        }
-    };
+    auto rot = [](T& e0, T& e1, float c, float s) { rot_pair<T>(e0, e1, c, s); };
     for (int v = v0; v < nvec; v += blockDim.x) {
         T* row;
         int i0;
@@ -125,7 +130,197 @@ __global__ void __launch_bounds__(512) rope_kernel(const __grid_constant__ RopeP
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// RoPE fused with the K/V write (semipd_set_rope; R28).  One CTA per new row t:
+//   position  prefill: prefix[r] + (t - cu[r]) for the request r holding t (R4);
+//             decode (cu == NULL): ctx[t] (R5)
+//   q rows    rotated in place (the attention reads them next)
+//   k rows    rotated in place (the prefill attention reads the chunk's keys from k_new) and
+//             stored, with the unrotated columns, into the pool slot of that position
+//   v rows    copied into the pool slot (absent for the MLA latent: V aliases K)
+// The angles and the rotation are rope_kernel's (fp64 sincos, rot_pair), so a fused call and
+// semipd_rope followed by an unfused call leave bit-identical rows and pool pages.
+struct RopeWriteParams {
+    unsigned char* q;
+    unsigned char* k;
+    const unsigned char* v;
+    unsigned char* kpool;  // this layer's pages [N_B][Hkv][bs][dk]
+    unsigned char* vpool;  // [N_B][Hkv][bs][dv] or null (kv_shared)
+    const int* cu;         // prefill [n + 1]; null = decode
+    const int* req_ids;
+    const int* base;       // prefix_lens (prefill) / ctx_lens (decode)
+    const int* bt;
+    int* status;
+    int n, Hq, Hkv, dk, dv, off, rd, lg_bs, MBR, N_B;
+    double inv_freq[MAX_HALF];
+};
+
+template <typename T, bool INTER>
+__global__ void __launch_bounds__(256) rope_write_kernel(const __grid_constant__ RopeWriteParams p) {
+    constexpr int VEC = 16 / sizeof(T);
+    extern __shared__ float cs[];  // [rd/2] cos, [rd/2] sin
+    const int t = blockIdx.x;
+    int r = t, pos;
+    if (p.cu) {
+        int hi = p.n - 1;  // the last request r with cu[r] <= t
+        r = 0;
+        while (r < hi) {
+            const int mid = (r + hi + 1) >> 1;
+            if (__ldg(p.cu + mid) <= t) r = mid; else hi = mid - 1;
+        }
+        pos = __ldg(p.base + r) + t - __ldg(p.cu + r);
+    } else {
+        pos = __ldg(p.base + t);
+    }
+    const int page = pos >> p.lg_bs;
+    const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + r) * p.MBR + page) : -1;
+    const bool ok = blk >= 0 && blk < p.N_B;
+    if (!ok && threadIdx.x == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+    const int half = p.rd >> 1;
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        double s, c;
+        sincos((double)pos * p.inv_freq[i], &s, &c);
+        cs[i] = (float)c;
+        cs[half + i] = (float)s;
+    }
+    __syncthreads();
+    const int nrot = (INTER ? p.rd : half) / VEC;  // rotation items per head row
+    const int nkp = (p.dk - p.rd) / VEC;           // unrotated k vectors per head row
+    const int nv = p.vpool ? p.dv / VEC : 0;
+    const int n_q = p.Hq * nrot, n_kr = p.Hkv * nrot, n_kp = p.Hkv * nkp, n_v = p.Hkv * nv;
+    const int total = n_q + n_kr + n_kp + n_v;
+    const size_t bs_mask = ((size_t)1 << p.lg_bs) - 1;
+    auto slot = [&](int h) { return (((size_t)blk * p.Hkv + h) << p.lg_bs) + ((size_t)pos & bs_mask); };
+    for (int it = threadIdx.x; it < total; it += blockDim.x) {
+        if (it < n_q + n_kr) {
+            const bool is_q = it < n_q;
+            const int j = is_q ? it : it - n_q;
+            const int h = j / nrot, i0 = (j % nrot) * VEC;
+            T* row = is_q ? reinterpret_cast<T*>(p.q) + ((size_t)t * p.Hq + h) * p.dk
+                          : reinterpret_cast<T*>(p.k) + ((size_t)t * p.Hkv + h) * p.dk;
+            row += p.off;
+            uint4 a = *reinterpret_cast<const uint4*>(row + i0);
+            T* xa = reinterpret_cast<T*>(&a);
+            uint4 b = a;
+            if constexpr (INTER) {
+#pragma unroll
+                for (int e = 0; e < VEC / 2; ++e) {
+                    const int fi = (i0 >> 1) + e;
+                    rot_pair<T>(xa[2 * e], xa[2 * e + 1], cs[fi], cs[half + fi]);
+                }
+            } else {
+                b = *reinterpret_cast<const uint4*>(row + half + i0);
+                T* xb = reinterpret_cast<T*>(&b);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) rot_pair<T>(xa[e], xb[e], cs[i0 + e], cs[half + i0 + e]);
+            }
+            *reinterpret_cast<uint4*>(row + i0) = a;
+            if (!INTER) *reinterpret_cast<uint4*>(row + half + i0) = b;
+            if (!is_q && ok) {
+                T* dst = reinterpret_cast<T*>(p.kpool) + slot(h) * p.dk + p.off;
+                *reinterpret_cast<uint4*>(dst + i0) = a;
+                if (!INTER) *reinterpret_cast<uint4*>(dst + half + i0) = b;
+            }
+        } else if (it < n_q + n_kr + n_kp) {
+            if (!ok) continue;
+            const int j = it - n_q - n_kr;
+            const int h = j / nkp, c0 = (j % nkp) * VEC;
+            const int c = c0 < p.off ? c0 : c0 + p.rd;  // columns outside [off, off + rd)
+            const T* src = reinterpret_cast<const T*>(p.k) + ((size_t)t * p.Hkv + h) * p.dk + c;
+            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.kpool) + slot(h) * p.dk + c) =
+                *reinterpret_cast<const uint4*>(src);
+        } else {
+            if (!ok) continue;
+            const int j = it - n_q - n_kr - n_kp;
+            const int h = j / nv, c = (j % nv) * VEC;
+            const T* src = reinterpret_cast<const T*>(p.v) + ((size_t)t * p.Hkv + h) * p.dv + c;
+            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.vpool) + slot(h) * p.dv + c) =
+                __ldg(reinterpret_cast<const uint4*>(src));
+        }
+    }
+}
+
+// the semipd_rope argument checks (shared with semipd_set_rope)
+semipd_status rope_check(int head_dim, int rot_offset, int rot_dim, int dtype, double theta,
+                         double factor, double lf, double hf, int L0) {
+    if (head_dim <= 0 || rot_offset < 0 || rot_dim <= 0 || rot_dim % 2 ||
+        rot_offset + rot_dim > head_dim || !(theta > 1.0) ||
+        (dtype != SEMIPD_BF16 && dtype != SEMIPD_FP32))
+        return SEMIPD_ERR_INVALID;
+    if (factor > 1.0 && (!(hf > lf) || !(lf > 0.0) || L0 <= 0)) return SEMIPD_ERR_INVALID;
+    return SEMIPD_OK;
+}
+
 }  // namespace
+
+semipd_status spd_launch_rope_write(semipd_pool_t pool, int layer, void* q, void* k_new,
+                                    const void* v_new, const int* cu_seqlens, const int* req_ids,
+                                    const int* base_pos, int n, int T, int Hq, int* status_dev,
+                                    cudaStream_t st) {
+    const auto& c = pool->cfg;
+    const auto& rc = pool->rope;
+    if (T <= 0) return SEMIPD_OK;
+    const uintptr_t mis = reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k_new) |
+                          reinterpret_cast<uintptr_t>(v_new);
+    if (mis % 16) return SEMIPD_ERR_UNSUPPORTED;
+    RopeWriteParams p;
+    p.q = static_cast<unsigned char*>(q);
+    p.k = static_cast<unsigned char*>(k_new);
+    p.v = static_cast<const unsigned char*>(v_new);
+    p.kpool = static_cast<unsigned char*>(pool->k_layer(layer));
+    p.vpool = c.kv_shared ? nullptr : static_cast<unsigned char*>(pool->v_layer(layer));
+    p.cu = cu_seqlens;
+    p.req_ids = req_ids;
+    p.base = base_pos;
+    p.bt = pool->bt;
+    p.status = status_dev;
+    p.n = n;
+    p.Hq = Hq;
+    p.Hkv = c.num_kv_heads;
+    p.dk = c.head_dim_k;
+    p.dv = c.head_dim_v;
+    p.off = rc.rot_offset;
+    p.rd = rc.rot_dim;
+    p.lg_bs = __builtin_ctz((unsigned)c.block_size);
+    p.MBR = c.max_blocks_per_req;
+    p.N_B = c.num_blocks;
+    for (int i = 0; i < MAX_HALF; ++i) p.inv_freq[i] = pool->rope_inv_freq[i];
+    const size_t smem = (size_t)rc.rot_dim * sizeof(float);
+    if (c.dtype == SEMIPD_BF16)
+        rc.interleaved ? rope_write_kernel<__nv_bfloat16, true><<<T, 256, smem, st>>>(p)
+                       : rope_write_kernel<__nv_bfloat16, false><<<T, 256, smem, st>>>(p);
+    else
+        rc.interleaved ? rope_write_kernel<float, true><<<T, 256, smem, st>>>(p)
+                       : rope_write_kernel<float, false><<<T, 256, smem, st>>>(p);
+    pool->launches += 1;
+    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+}
+
+extern "C" semipd_status semipd_set_rope(semipd_pool_t pool, const semipd_rope_config* cfg) {
+    if (!pool) return SEMIPD_ERR_INVALID;
+    if (!cfg) {
+        pool->rope_on = false;
+        return SEMIPD_OK;
+    }
+    const auto& c = pool->cfg;
+    const semipd_status e = rope_check(c.head_dim_k, cfg->rot_offset, cfg->rot_dim, c.dtype,
+                                       cfg->theta, cfg->factor, cfg->low_freq_factor,
+                                       cfg->high_freq_factor, cfg->original_max_pos);
+    if (e != SEMIPD_OK) return e;
+    const int vec = c.dtype == SEMIPD_BF16 ? 8 : 4;
+    const int half = cfg->rot_dim / 2;
+    if ((cfg->interleaved ? cfg->rot_dim : half) % vec || cfg->rot_offset % vec ||
+        c.head_dim_k % vec || c.head_dim_v % vec || half > MAX_HALF)
+        return SEMIPD_ERR_UNSUPPORTED;
+    pool->rope = *cfg;
+    for (int i = 0; i < MAX_HALF; ++i)
+        pool->rope_inv_freq[i] = i < half ? rope_inv_freq(i, cfg->rot_dim, cfg->theta, cfg->factor,
+                                                           cfg->low_freq_factor, cfg->high_freq_factor,
+                                                           (double)cfg->original_max_pos)
+                                          : 0.0;
+    pool->rope_on = true;
+    return SEMIPD_OK;
+}
 
 extern "C" semipd_status semipd_rope(void* q, void* k, const int32_t* positions,
                                      int32_t num_tokens, int32_t num_q_heads, int32_t num_kv_heads,
@@ -133,13 +328,10 @@ extern "C" semipd_status semipd_rope(void* q, void* k, const int32_t* positions,
                                      int32_t interleaved, int32_t dtype, double theta, double factor,
                                      double low_freq_factor, double high_freq_factor,
                                      int32_t original_max_pos, semipd_stream_t s) {
-    if (num_tokens < 0 || num_q_heads < 0 || num_kv_heads < 0 || head_dim <= 0 || rot_offset < 0 ||
-        rot_dim <= 0 || rot_dim % 2 || rot_offset + rot_dim > head_dim || !(theta > 1.0) ||
-        (dtype != SEMIPD_BF16 && dtype != SEMIPD_FP32))
-        return SEMIPD_ERR_INVALID;
-    if (factor > 1.0 && (!(high_freq_factor > low_freq_factor) || !(low_freq_factor > 0.0) ||
-                         original_max_pos <= 0))
-        return SEMIPD_ERR_INVALID;
+    if (num_tokens < 0 || num_q_heads < 0 || num_kv_heads < 0) return SEMIPD_ERR_INVALID;
+    const semipd_status e = rope_check(head_dim, rot_offset, rot_dim, dtype, theta, factor,
+                                       low_freq_factor, high_freq_factor, original_max_pos);
+    if (e != SEMIPD_OK) return e;
     if (num_tokens == 0 || num_q_heads + num_kv_heads == 0) return SEMIPD_OK;
     if ((num_q_heads > 0 && !q) || (num_kv_heads > 0 && !k) || !positions) return SEMIPD_ERR_INVALID;
     const int vec = dtype == SEMIPD_BF16 ? 8 : 4;

@@ -35,8 +35,24 @@ constexpr int NCB = DK / 64;                            // 9 column blocks of 12
 constexpr int CB_LO = 4;                                // boxes: cb [0,4) and [4,9)
 constexpr uint32_t LO_BYTES = CB_LO * PAGE * 128;       // 32 KiB
 constexpr uint32_t HI_BYTES = (NCB - CB_LO) * PAGE * 128;  // 40 KiB
+// SPD_MLA_DQ = 1: two Q buffers (the next unit's Q lands while the current unit still runs
+// QK, so the unit boundary no longer waits a Q TMA round trip) and a 4-slot ring of exactly
+// sized halves (even slots 32 KiB = LO boxes, odd slots 40 KiB = HI boxes: 2 pages in flight);
+// 0: one Q buffer and 5 uniform 40 KiB slots (2.5 pages in flight).  Measured (same box,
+// microbench, 2 reps): DQ = 1 is 1-6 % SLOWER at every shape (B 256 ctx 350 at 44 / 104 /
+// 148 SMs, B 256 ctx 1000, B 64 ctx 4000): the unit boundary is not held by the Q load, and
+// the shallower ring costs more than the second Q buffer gains.  Default 0.
+#ifndef SPD_MLA_DQ
+#define SPD_MLA_DQ 0
+#endif
 constexpr uint32_t SLOT_BYTES = HI_BYTES;
-constexpr int NSLOT = 5;
+constexpr int NSLOT = SPD_MLA_DQ ? 4 : 5;
+constexpr int NQBUF = SPD_MLA_DQ ? 2 : 1;
+constexpr uint32_t RING_BYTES = SPD_MLA_DQ ? 2 * (LO_BYTES + HI_BYTES) : NSLOT * SLOT_BYTES;
+__host__ __device__ constexpr uint32_t slot_off(int s) {
+    return SPD_MLA_DQ ? (uint32_t)(s >> 1) * (LO_BYTES + HI_BYTES) + (uint32_t)(s & 1) * LO_BYTES
+                      : (uint32_t)s * SLOT_BYTES;
+}
 constexpr uint32_t Q_BYTES = NCB * NH * 128;            // 18 KiB
 constexpr uint32_t P_BYTES = NH * 128;                  // 2 KiB per buffer (2 buffers)
 constexpr int NTHREADS = 192;
@@ -116,12 +132,12 @@ struct TcParams {
 #endif
 
 struct Bars {
-    uint64_t full[NSLOT], empty[NSLOT], s_full[2], s_empty[2], p_full[2], o_done[2], q_full, q_empty,
-        ufull[2], uempty[2];
+    uint64_t full[NSLOT], empty[NSLOT], s_full[2], s_empty[2], p_full[2], o_done[2], q_full[NQBUF],
+        q_empty[NQBUF], ufull[2], uempty[2];
 };
 
-constexpr uint32_t OFF_Q = NSLOT * SLOT_BYTES;
-constexpr uint32_t OFF_P = OFF_Q + Q_BYTES;
+constexpr uint32_t OFF_Q = RING_BYTES;
+constexpr uint32_t OFF_P = OFF_Q + NQBUF * Q_BYTES;
 constexpr uint32_t OFF_RED = OFF_P + 2 * P_BYTES;            // [2][64] maxima, [64] sums
 constexpr uint32_t OFF_BARS = OFF_RED + 3 * 64 * 4;
 constexpr uint32_t OFF_UNITS = OFF_BARS + sizeof(Bars);
@@ -170,8 +186,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(bar.p_full + i, 4);
             mbar_init(bar.o_done + i, 1);
         }
-        mbar_init(&bar.q_full, 1);
-        mbar_init(&bar.q_empty, 1);
+        for (int i = 0; i < NQBUF; ++i) {
+            mbar_init(bar.q_full + i, 1);
+            mbar_init(bar.q_empty + i, 1);
+        }
         fence_mbar_init();
         span_begin(p.span);
         if (p.trace.buf) {
@@ -271,18 +289,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mbar_wait(bar.empty + s0, ((gh / NSLOT) & 1) ^ 1);
                     [[maybe_unused]] const long long tp1 = TL_NOW();
                     mbar_arrive_expect_tx(bar.full + s0, LO_BYTES);
-                    tma_load_4d(ring + s0 * SLOT_BYTES, &map_lo, bar.full + s0, 0, 0, 0, z);
+                    tma_load_4d(ring + slot_off(s0), &map_lo, bar.full + s0, 0, 0, 0, z);
+                    if (i == 0) {
+                        // Q of this unit: its buffer frees when the last QK of the unit that
+                        // used it before completes (issued before this tile: no deadlock)
+                        const int qb = nq % NQBUF;
+                        mbar_wait(bar.q_empty + qb, ((nq / NQBUF) & 1) ^ 1);
+                        mbar_arrive_expect_tx(bar.q_full + qb, Q_BYTES);
+                        tma_load_4d(qs + qb * Q_BYTES, &qmap, bar.q_full + qb, 0, 0, 0, d.b);
+                    }
                     mbar_wait(bar.empty + s1, (((gh + 1) / NSLOT) & 1) ^ 1);
                     mbar_arrive_expect_tx(bar.full + s1, HI_BYTES);
-                    tma_load_4d(ring + s1 * SLOT_BYTES, &map_hi, bar.full + s1, 0, 0, CB_LO, z);
+                    tma_load_4d(ring + slot_off(s1), &map_hi, bar.full + s1, 0, 0, CB_LO, z);
                     TL_REC(1, gh / 2, tp0, tp1, TL_NOW());
-                    if (i == 0) {
-                        // Q of this unit: its buffer frees when the previous unit's last QK
-                        // completes (that tile was issued before this one: no deadlock)
-                        mbar_wait(&bar.q_empty, (nq & 1) ^ 1);
-                        mbar_arrive_expect_tx(&bar.q_full, Q_BYTES);
-                        tma_load_4d(qs, &qmap, &bar.q_full, 0, 0, 0, d.b);
-                    }
                 }
                 __syncwarp();
             }
@@ -322,7 +341,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int h0 = gh + 2 * npv;
                     const int s0 = h0 % NSLOT, s1 = (h0 + 1) % NSLOT;
                     tc_fence_after();
-                    const uint32_t lo = ring_a + s0 * SLOT_BYTES, hi = ring_a + s1 * SLOT_BYTES;
+                    const uint32_t lo = ring_a + slot_off(s0), hi = ring_a + slot_off(s1);
 #pragma unroll
                     for (int m = 0; m < DV / 128; ++m) {
                         // dv block m = column blocks 2m, 2m+1 (both in the same half-page)
@@ -347,33 +366,36 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // landed, [4,9) when the second has
                     const int t = gt + nqk, sb = t & 1, h0 = gh + 2 * nqk;
                     const int s0 = h0 % NSLOT, s1 = (h0 + 1) % NSLOT;
-                    if (!q_ok) q_ok = probe(&bar.q_full, nq & 1);
+                    const int qb = nq % NQBUF;
+                    if (!q_ok) q_ok = probe(bar.q_full + qb, (nq / NQBUF) & 1);
                     if (q_ok && !qk_lo && probe(bar.s_empty + sb, ((t >> 1) & 1) ^ 1) &&
                         probe(bar.full + s0, (h0 / NSLOT) & 1)) {
                         tc_fence_after();
-                        const uint64_t dlo = umma_desc_sw128(ring_a + s0 * SLOT_BYTES, 16, 1024);
+                        const uint64_t dlo = umma_desc_sw128(ring_a + slot_off(s0), 16, 1024);
+                        const uint64_t dq = dq0 + (uint64_t)(qb * (Q_BYTES / 16));
 #pragma unroll
                         for (int k = 0; k < CB_LO * 4; ++k) {
                             const int cb = k >> 2;
                             // descriptor start address is in 16-byte units
                             umma_ss_warp(tmem + TM_S + sb * NH, dlo + (uint64_t)(cb * (PAGE * 128 / 16) + (k & 3) * 2),
-                                         dq0 + (uint64_t)(cb * (NH * 128 / 16) + (k & 3) * 2), ID_QK, k > 0);
+                                         dq + (uint64_t)(cb * (NH * 128 / 16) + (k & 3) * 2), ID_QK, k > 0);
                         }
                         qk_lo = true;
                         continue;
                     }
                     if (qk_lo && probe(bar.full + s1, ((h0 + 1) / NSLOT) & 1)) {
                         tc_fence_after();
-                        const uint64_t dhi = umma_desc_sw128(ring_a + s1 * SLOT_BYTES, 16, 1024);
+                        const uint64_t dhi = umma_desc_sw128(ring_a + slot_off(s1), 16, 1024);
+                        const uint64_t dq = dq0 + (uint64_t)(qb * (Q_BYTES / 16));
 #pragma unroll
                         for (int k = CB_LO * 4; k < DK / 16; ++k) {
                             const int cb = k >> 2;
                             umma_ss_warp(tmem + TM_S + sb * NH, dhi + (uint64_t)((cb - CB_LO) * (PAGE * 128 / 16) + (k & 3) * 2),
-                                         dq0 + (uint64_t)(cb * (NH * 128 / 16) + (k & 3) * 2), ID_QK, 1u);
+                                         dq + (uint64_t)(cb * (NH * 128 / 16) + (k & 3) * 2), ID_QK, 1u);
                         }
                         umma_commit_warp(bar.s_full + sb);
                         if (lane == 0) TL_REC(2, t, TL_NOW(), 0, 0);
-                        if (nqk == d.nt - 1) umma_commit_warp(&bar.q_empty);
+                        if (nqk == d.nt - 1) umma_commit_warp(bar.q_empty + qb);
                         qk_lo = false;
                         ++nqk;
                         continue;

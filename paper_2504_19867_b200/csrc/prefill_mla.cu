@@ -36,7 +36,25 @@ constexpr int CB_LO = 4;
 constexpr uint32_t LO_BYTES = CB_LO * PAGE * 128;       // 32 KiB
 constexpr uint32_t HI_BYTES = (NCB - CB_LO) * PAGE * 128;  // 40 KiB
 constexpr uint32_t SLOT_BYTES = HI_BYTES;
-constexpr int NSLOT = 3;
+// SPD_MLAP_SWAP = 1: PV as O^T[128 dv x 64 rows] += V^T . P^T per 128-dv block (M = 128: the
+//   full tensor rate; 4 accumulators over all 128 TMEM lanes) instead of O_lo / O_hi at
+//   M = 64 (half rate); P^T is the K-major P tile the softmax writes anyway.
+// SPD_MLAP_RING4 = 1: a 4-slot ring of exactly sized halves (even slots 32 KiB LO boxes, odd
+//   slots 40 KiB HI boxes: 2 pages in flight instead of 1.5) and one P buffer.
+#ifndef SPD_MLAP_SWAP
+#define SPD_MLAP_SWAP 1
+#endif
+#ifndef SPD_MLAP_RING4
+#define SPD_MLAP_RING4 1
+#endif
+constexpr bool SWAP = SPD_MLAP_SWAP != 0;
+constexpr int NSLOT = SPD_MLAP_RING4 ? 4 : 3;
+constexpr int NPBUF = SPD_MLAP_RING4 ? 1 : 2;
+constexpr uint32_t RING_BYTES = SPD_MLAP_RING4 ? 2 * (LO_BYTES + HI_BYTES) : NSLOT * SLOT_BYTES;
+__host__ __device__ constexpr uint32_t slot_off(int s) {
+    return SPD_MLAP_RING4 ? (uint32_t)(s >> 1) * (LO_BYTES + HI_BYTES) + (uint32_t)(s & 1) * LO_BYTES
+                          : (uint32_t)s * SLOT_BYTES;
+}
 constexpr int TQ = 4;                                   // tokens per unit
 constexpr int BM = TQ * NH;                             // 64 rows
 constexpr uint32_t Q_BYTES = NCB * BM * 128;            // 72 KiB
@@ -69,9 +87,10 @@ struct Bars {
         q_empty, ufull[2], uempty[2];
 };
 
-constexpr uint32_t OFF_Q = NSLOT * SLOT_BYTES;
+constexpr uint32_t OFF_Q = RING_BYTES;
 constexpr uint32_t OFF_P = OFF_Q + Q_BYTES;
-constexpr uint32_t OFF_BARS = OFF_P + 2 * P_BYTES;
+constexpr uint32_t OFF_RED = OFF_P + NPBUF * P_BYTES;   // swap: [2][64] alphas, [64] 1/l, flags
+constexpr uint32_t OFF_BARS = OFF_RED + (SWAP ? (3 * 64 + 8) * 4 : 0);
 constexpr uint32_t OFF_UNITS = OFF_BARS + sizeof(Bars);
 constexpr uint32_t OFF_MISC = OFF_UNITS + 2 * sizeof(PUnit);
 constexpr uint32_t SMEM_BYTES = 1024 + OFF_MISC + 16;
@@ -177,7 +196,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int s0 = gh % NSLOT, s1 = (gh + 1) % NSLOT;
                     mbar_wait(bar.empty + s0, ((gh / NSLOT) & 1) ^ 1);
                     mbar_arrive_expect_tx(bar.full + s0, LO_BYTES);
-                    tma_load_4d(ring + s0 * SLOT_BYTES, &map_lo, bar.full + s0, 0, 0, 0, z);
+                    tma_load_4d(ring + slot_off(s0), &map_lo, bar.full + s0, 0, 0, 0, z);
                     if (j == 0) {
                         // this unit's Q (64 rows): free once the previous unit's last QK is done
                         mbar_wait(&bar.q_empty, (nq & 1) ^ 1);
@@ -186,7 +205,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     mbar_wait(bar.empty + s1, (((gh + 1) / NSLOT) & 1) ^ 1);
                     mbar_arrive_expect_tx(bar.full + s1, HI_BYTES);
-                    tma_load_4d(ring + s1 * SLOT_BYTES, &map_hi, bar.full + s1, 0, 0, CB_LO, z);
+                    tma_load_4d(ring + slot_off(s1), &map_hi, bar.full + s1, 0, 0, CB_LO, z);
                 }
                 __syncwarp();
             }
@@ -195,7 +214,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else if (warp == 1) {
         // =========================== MMA issuer (warp-collective) ===========================
         constexpr uint32_t ID_QK = umma_idesc_bf16_f32_ab(BM, PAGE, 0, 0);
-        constexpr uint32_t ID_PV = umma_idesc_bf16_f32_ab(BM, 256, 0, 1);
+        constexpr uint32_t ID_PV = SWAP ? umma_idesc_bf16_f32_ab(128, BM, 1, 0)
+                                        : umma_idesc_bf16_f32_ab(BM, 256, 0, 1);
         const uint32_t ring_a = smem_u32(ring);
         const uint64_t dq0 = umma_desc_sw128(smem_u32(qs), 16, 1024);
         const uint64_t dp0 = umma_desc_sw128(smem_u32(ps), 16, 1024);
@@ -221,19 +241,37 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int h0 = gh + 2 * npv;
                     const int s0 = h0 % NSLOT, s1 = (h0 + 1) % NSLOT;
                     tc_fence_after();
-                    // V^T blocks: dv [0,256) = column blocks 0-3 (first box), [256,512) = 4-7
-                    const uint64_t dvlo = umma_desc_sw128(ring_a + s0 * SLOT_BYTES, PAGE * 128, 1024);
-                    const uint64_t dvhi = umma_desc_sw128(ring_a + s1 * SLOT_BYTES, PAGE * 128, 1024);
-                    const uint64_t dpa = dp0 + (uint64_t)(pb * (P_BYTES / 16));
+                    const uint64_t dpa = dp0 + (uint64_t)((pb % NPBUF) * (P_BYTES / 16));
+                    if constexpr (SWAP) {
+                        // O^T[dv block m] += V^T[128 dv x 64 keys] . P^T: V^T MN-major straight
+                        // from the page boxes (LBO 8 KiB between 64-column blocks, SBO 1 KiB
+                        // between 8-key groups); blocks 0, 1 in the first box, 2, 3 in the second
+                        const uint32_t lo = ring_a + slot_off(s0), hi = ring_a + slot_off(s1);
 #pragma unroll
-                    for (int ks = 0; ks < PAGE / 16; ++ks)
-                        umma_ss_warp(tmem + TM_O, dpa + (uint64_t)(ks * 2), dvlo + (uint64_t)(ks * 128),
-                                     ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
-                    umma_commit_warp(bar.empty + s0);
+                        for (int m = 0; m < DV / 128; ++m) {
+                            const uint32_t a0 = m < 2 ? lo + m * (2 * PAGE * 128)
+                                                      : hi + (2 * m - CB_LO) * (PAGE * 128);
+                            const uint64_t da = umma_desc_sw128(a0, PAGE * 128, 1024);
 #pragma unroll
-                    for (int ks = 0; ks < PAGE / 16; ++ks)
-                        umma_ss_warp(tmem + TM_O + (16u << 16), dpa + (uint64_t)(ks * 2),
-                                     dvhi + (uint64_t)(ks * 128), ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
+                            for (int ks = 0; ks < PAGE / 16; ++ks)
+                                umma_ss_warp(tmem + TM_O + m * BM, da + (uint64_t)(ks * 128),
+                                             dpa + (uint64_t)(ks * 2), ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
+                            if (m == 1) umma_commit_warp(bar.empty + s0);
+                        }
+                    } else {
+                        // V^T blocks: dv [0,256) = column blocks 0-3 (first box), [256,512) = 4-7
+                        const uint64_t dvlo = umma_desc_sw128(ring_a + slot_off(s0), PAGE * 128, 1024);
+                        const uint64_t dvhi = umma_desc_sw128(ring_a + slot_off(s1), PAGE * 128, 1024);
+#pragma unroll
+                        for (int ks = 0; ks < PAGE / 16; ++ks)
+                            umma_ss_warp(tmem + TM_O, dpa + (uint64_t)(ks * 2), dvlo + (uint64_t)(ks * 128),
+                                         ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
+                        umma_commit_warp(bar.empty + s0);
+#pragma unroll
+                        for (int ks = 0; ks < PAGE / 16; ++ks)
+                            umma_ss_warp(tmem + TM_O + (16u << 16), dpa + (uint64_t)(ks * 2),
+                                         dvhi + (uint64_t)(ks * 128), ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
+                    }
                     umma_commit_warp(bar.o_done + pb);
                     umma_commit_warp(bar.empty + s1);
                     ++npv;
@@ -246,7 +284,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (q_ok && !qk_lo && probe(bar.s_empty + sb, ((t >> 1) & 1) ^ 1) &&
                         probe(bar.full + s0, (h0 / NSLOT) & 1)) {
                         tc_fence_after();
-                        const uint64_t dk = umma_desc_sw128(ring_a + s0 * SLOT_BYTES, 16, 1024);
+                        const uint64_t dk = umma_desc_sw128(ring_a + slot_off(s0), 16, 1024);
 #pragma unroll
                         for (int k = 0; k < CB_LO * 4; ++k) {
                             const int cb = k >> 2;
@@ -260,7 +298,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     if (qk_lo && probe(bar.full + s1, ((h0 + 1) / NSLOT) & 1)) {
                         tc_fence_after();
-                        const uint64_t dk = umma_desc_sw128(ring_a + s1 * SLOT_BYTES, 16, 1024);
+                        const uint64_t dk = umma_desc_sw128(ring_a + slot_off(s1), 16, 1024);
 #pragma unroll
                         for (int k = CB_LO * 4; k < DK / 16; ++k) {
                             const int cb = k >> 2;
@@ -288,6 +326,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
         const bool lo = lane < 16;
         const int h = lane & 15;  // head of this lane's row
+        const int row = qd * 16 + h;
+        float* red = reinterpret_cast<float*>(base + OFF_RED);  // swap: [2][64] alpha, [64] 1/l
+        int* rflag = reinterpret_cast<int*>(red + 3 * BM);       // swap: [2][4] rescale flags
         int gt = 0, nunit = 0;
         for (;;) {
             const int us = nunit & 1;
@@ -326,35 +367,64 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const float alpha = (move && j > 0) ? fast_exp2(mref - mnew) : 1.f;
                 mref = mnew;
                 lsum *= alpha;
-                const bool any_rescale = __any_sync(0xffffffffu, move && j > 0);
-                // P buffer t&1 is free once PV(t-2) completed; O may be rescaled only after
-                // PV(t-1) completed
+                bool any_rescale = __any_sync(0xffffffffu, move && j > 0);
+                if constexpr (SWAP) {
+                    // O^T holds every row in a column across all 128 lanes: the four warps
+                    // agree on this tile's rescale set through smem (double-buffered by tile)
+                    float* alph = red + sb * BM;
+                    if (lo) alph[row] = alpha;
+                    if (lane == 0) rflag[sb * 4 + qd] = any_rescale ? 1 : 0;
+                    named_bar_sync(1, 128);
+                    any_rescale = (rflag[sb * 4 + 0] | rflag[sb * 4 + 1] | rflag[sb * 4 + 2] |
+                                   rflag[sb * 4 + 3]) != 0;
+                }
+                // the P buffer is free once the PV that last read it completed (NPBUF = 2:
+                // PV(t-2), NPBUF = 1: PV(t-1)); O may be rescaled only after PV(t-1) completed
                 if (any_rescale && j > 0) {
                     mbar_wait(bar.o_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
-                } else if (t >= 2) {
-                    mbar_wait(bar.o_done + sb, ((t >> 1) & 1) ^ 1);
+                } else if (t >= NPBUF) {
+                    mbar_wait(bar.o_done + ((t - NPBUF) & 1), ((t - NPBUF) >> 1) & 1);
                 }
                 tc_fence_after();
                 if (any_rescale && j > 0) {
-                    // lanes 0-15: O_lo of row (qd, h); lanes 16-31: O_hi of the same row
-                    const float a = __shfl_sync(0xffffffffu, alpha, h);
-                    const uint32_t ob = tmem + lane_base + TM_O;
+                    if constexpr (SWAP) {
+                        // column r of every O^T block scales by alpha[r]
+                        const float* alph = red + sb * BM;
 #pragma unroll 1
-                    for (int cc = 0; cc < 256; cc += 32) {
-                        uint32_t o[32];
-                        tmem_ld32(ob + cc, o);
-                        tmem_wait_ld();
+                        for (int m = 0; m < DV / 128; ++m) {
+#pragma unroll 1
+                            for (int cc = 0; cc < BM; cc += 32) {
+                                const uint32_t oa = tmem + lane_base + TM_O + m * BM + cc;
+                                uint32_t o[32];
+                                tmem_ld32(oa, o);
+                                tmem_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * a);
-                        tmem_st32(ob + cc, o);
+                                for (int e = 0; e < 32; ++e)
+                                    o[e] = __float_as_uint(__uint_as_float(o[e]) * alph[cc + e]);
+                                tmem_st32(oa, o);
+                            }
+                        }
+                    } else {
+                        // lanes 0-15: O_lo of row (qd, h); lanes 16-31: O_hi of the same row
+                        const float a = __shfl_sync(0xffffffffu, alpha, h);
+                        const uint32_t ob = tmem + lane_base + TM_O;
+#pragma unroll 1
+                        for (int cc = 0; cc < 256; cc += 32) {
+                            uint32_t o[32];
+                            tmem_ld32(ob + cc, o);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * a);
+                            tmem_st32(ob + cc, o);
+                        }
                     }
                     tmem_wait_st();
                 }
-                // P row (64 keys, bf16) -> P buffer sb, K-major 128-B swizzle; lsum from the
-                // rounded values
+                // P row (64 keys, bf16) -> P buffer, K-major 128-B swizzle (the A operand of
+                // P.V, or the B operand P^T of the swapped V^T.P^T); lsum from the rounded values
                 if (lo) {
-                    unsigned char* prow = ps + sb * P_BYTES + (qd * 16 + h) * 128;
-                    const int sw = (qd * 16 + h) & 7;
+                    unsigned char* prow = ps + (sb % NPBUF) * P_BYTES + row * 128;
+                    const int sw = row & 7;
 #pragma unroll
                     for (int c8 = 0; c8 < 8; ++c8) {
                         uint32_t w[4];
@@ -378,30 +448,65 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (lane == 0) mbar_arrive(bar.p_full + sb);
             }
             gt += d.nt;
-            // ---- epilogue: O / l -> bf16 (lanes 0-15: dv [0,256), lanes 16-31: [256,512))
+            // ---- epilogue: O / l -> bf16
             mbar_wait(bar.o_done + ((gt - 1) & 1), ((gt - 1) >> 1) & 1);
             tc_fence_after();
-            const float rl = __frcp_rn(__shfl_sync(0xffffffffu, lsum, h));
-            const bool store = qd < d.ntok && h < p.Hq;
-            const size_t tok = (size_t)d.row0 + qd;
-            __nv_bfloat16* orow = p.out + (p.out_head_major ? ((size_t)h * p.T + tok) * DV
-                                                            : (tok * p.Hq + h) * DV) +
-                                  (lo ? 0 : 256);
-            const uint32_t ob = tmem + lane_base + TM_O;
+            if constexpr (SWAP) {
+                // thread = dv index (block m, quadrant qd, lane) of all 64 rows: lane pairs
+                // exchange so each lane stores bf16x2 of every other row
+                float* rl = red + 2 * BM;
+                if (lo) rl[row] = __frcp_rn(lsum);
+                named_bar_sync(1, 128);
+                const bool odd = lane & 1;
 #pragma unroll 1
-            for (int cc = 0; cc < 256; cc += 32) {
-                uint32_t o[32];
-                tmem_ld32(ob + cc, o);
-                tmem_wait_ld();
-                if (store) {
+                for (int m = 0; m < DV / 128; ++m) {
+                    const int dve = m * 128 + qd * 32 + (lane & ~1);
+#pragma unroll 1
+                    for (int cc = 0; cc < BM; cc += 32) {
+                        uint32_t o[32];
+                        tmem_ld32(tmem + lane_base + TM_O + m * BM + cc, o);
+                        tmem_wait_ld();
 #pragma unroll
-                    for (int e8 = 0; e8 < 4; ++e8) {
-                        uint4 v;
-                        v.x = pack_bf16(__uint_as_float(o[e8 * 8 + 0]) * rl, __uint_as_float(o[e8 * 8 + 1]) * rl);
-                        v.y = pack_bf16(__uint_as_float(o[e8 * 8 + 2]) * rl, __uint_as_float(o[e8 * 8 + 3]) * rl);
-                        v.z = pack_bf16(__uint_as_float(o[e8 * 8 + 4]) * rl, __uint_as_float(o[e8 * 8 + 5]) * rl);
-                        v.w = pack_bf16(__uint_as_float(o[e8 * 8 + 6]) * rl, __uint_as_float(o[e8 * 8 + 7]) * rl);
-                        *reinterpret_cast<uint4*>(orow + cc + e8 * 8) = v;
+                        for (int e = 0; e < 32; ++e) {
+                            const int r = cc + e;
+                            const float v = __uint_as_float(o[e]) * rl[r];
+                            const float other = __shfl_xor_sync(0xffffffffu, v, 1);
+                            const int tk = r >> 4, hh = r & 15;
+                            if (((r & 1) != 0) == odd && tk < d.ntok && hh < p.Hq) {
+                                const size_t tok = (size_t)d.row0 + tk;
+                                __nv_bfloat16* op = p.out + (p.out_head_major ? ((size_t)hh * p.T + tok) * DV
+                                                                              : (tok * p.Hq + hh) * DV) + dve;
+                                *reinterpret_cast<uint32_t*>(op) = odd ? pack_bf16(other, v) : pack_bf16(v, other);
+                            }
+                        }
+                    }
+                }
+                // rl / alpha / flags are rewritten by the next unit
+                named_bar_sync(1, 128);
+            } else {
+                // lanes 0-15: dv [0,256), lanes 16-31: [256,512)
+                const float rl = __frcp_rn(__shfl_sync(0xffffffffu, lsum, h));
+                const bool store = qd < d.ntok && h < p.Hq;
+                const size_t tok = (size_t)d.row0 + qd;
+                __nv_bfloat16* orow = p.out + (p.out_head_major ? ((size_t)h * p.T + tok) * DV
+                                                                : (tok * p.Hq + h) * DV) +
+                                      (lo ? 0 : 256);
+                const uint32_t ob = tmem + lane_base + TM_O;
+#pragma unroll 1
+                for (int cc = 0; cc < 256; cc += 32) {
+                    uint32_t o[32];
+                    tmem_ld32(ob + cc, o);
+                    tmem_wait_ld();
+                    if (store) {
+#pragma unroll
+                        for (int e8 = 0; e8 < 4; ++e8) {
+                            uint4 v;
+                            v.x = pack_bf16(__uint_as_float(o[e8 * 8 + 0]) * rl, __uint_as_float(o[e8 * 8 + 1]) * rl);
+                            v.y = pack_bf16(__uint_as_float(o[e8 * 8 + 2]) * rl, __uint_as_float(o[e8 * 8 + 3]) * rl);
+                            v.z = pack_bf16(__uint_as_float(o[e8 * 8 + 4]) * rl, __uint_as_float(o[e8 * 8 + 5]) * rl);
+                            v.w = pack_bf16(__uint_as_float(o[e8 * 8 + 6]) * rl, __uint_as_float(o[e8 * 8 + 7]) * rl);
+                            *reinterpret_cast<uint4*>(orow + cc + e8 * 8) = v;
+                        }
                     }
                 }
             }

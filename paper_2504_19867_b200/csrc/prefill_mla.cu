@@ -41,8 +41,13 @@ constexpr uint32_t SLOT_BYTES = HI_BYTES;
 //   M = 64 (half rate); P^T is the K-major P tile the softmax writes anyway.
 // SPD_MLAP_RING4 = 1: a 4-slot ring of exactly sized halves (even slots 32 KiB LO boxes, odd
 //   slots 40 KiB HI boxes: 2 pages in flight instead of 1.5) and one P buffer.
+// Measured (same box, microbench C = 2048, TFLOP/s at 104 / 148 SMs; profiles/r2_mla_prefill_ab.log):
+//   SWAP 0 RING4 0: 235 / 309    SWAP 1 RING4 0: 196 / 255
+//   SWAP 0 RING4 1: 301 / 389    SWAP 1 RING4 1: 235 / 302
+// The ring depth is what limits the pipeline (+28 %); the swapped PV's per-tile four-warp
+// agreement on the rescale set and its 16 MMAs per page cost more than its full-rate MMAs gain.
 #ifndef SPD_MLAP_SWAP
-#define SPD_MLAP_SWAP 1
+#define SPD_MLAP_SWAP 0
 #endif
 #ifndef SPD_MLAP_RING4
 #define SPD_MLAP_RING4 1

@@ -56,6 +56,20 @@ SPD_DEV void span_end(unsigned long long* rec) {
     }
 }
 
+// ------------------------------------------------------------------ cp.async (LDGSTS)
+// 16-byte global -> shared copy through L2 (.cg) with an L2 policy; src_bytes = 0 zero-fills
+SPD_DEV void cp_async16_hint(uint32_t dst, const void* src, uint32_t src_bytes, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst),
+                 "l"(src), "r"(src_bytes), "l"(pol)
+                 : "memory");
+}
+// arrive on `bar` once every cp.async this thread issued so far has landed (no pending-count
+// increment: the barrier's expected count includes this arrival)
+SPD_DEV void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
 // ------------------------------------------------------------------ mbarrier
 SPD_DEV void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)

@@ -34,6 +34,14 @@ constexpr int kDecL2 = SPD_DEC_L2;
 using namespace spd;
 
 constexpr int HD = 128;           // head dim (dk == dv)
+// SPD_DEC_CPASYNC = 1: 16-token pages streamed by the producer warp with 16-byte cp.async
+// (LDGSTS) instead of one TMA box per 4 KiB (page, head).  Parity-green, but measured 9-10 %
+// SLOWER at every SM budget (cfg-2 decode, bs 16: 3.58 vs 3.95 TB/s at 104 SMs, 4.46 vs 4.92 at
+// 148; profiles/r2_decode_bs16_cpasync_ab.log): the 4 KiB TMA box is not what limits 16-token
+// pages, so the default stays 0 (TMA).
+#ifndef SPD_DEC_CPASYNC
+#define SPD_DEC_CPASYNC 0
+#endif
 constexpr int KPS = 64;           // keys per stage
 constexpr int NSTAGE = 6;
 constexpr int KV_BYTES = KPS * HD * 2;         // 16 KiB of K (or V) per stage
@@ -119,6 +127,10 @@ __global__ void __launch_bounds__(4 * 32, 1)
                        const __grid_constant__ CUtensorMap vmap, DecodeParams p) {
     constexpr int R = 1 << LG_R;     // rows per TMA box (= min(bs, 64))
     constexpr int NB = KPS / R;      // boxes per stage per tensor
+    // 16-token pages: a 4 KiB (page, head) box costs the SM's TMA unit about as much as a
+    // 16 KiB one, so the producer warp streams them with 16-byte cp.async (LDGSTS) instead,
+    // into the same 128-B-swizzled stage layout, 32 lanes arriving on the stage barrier
+    constexpr bool CPA = LG_R == 4 && SPD_DEC_CPASYNC;
     // consumer warps and scratch rows (the swap-AB partials have G <= 8 rows); 6 swap-AB
     // consumer warps measured 2-5 % slower than 3 (more padding stages and merge work)
     constexpr int CW = 3;
@@ -141,7 +153,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
     const uint64_t kv_pol = l2_policy(kDecL2);  // KV stream: read once per step
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
-            mbar_init(full + i, 1);
+            mbar_init(full + i, CPA ? 32 : 1);
             mbar_init(empty + i, 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -289,11 +301,10 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 // stages, so the stage -> warp split depends on the unit only (bitwise
                 // identical results for every grid size / schedule)
                 while (gstage % CW != 0) {
-                    if (lane == 0) {
-                        const int st = gstage % NSTAGE;
-                        mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
-                        mbar_arrive(full + st);
-                    }
+                    const int st = gstage % NSTAGE;
+                    if (lane == 0) mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
+                    __syncwarp();
+                    if (CPA || lane == 0) mbar_arrive(full + st);
                     ++gstage;
                 }
                 __syncwarp();
@@ -364,8 +375,34 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 if (lane == 0) {
                     mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
                     tp1 = TL_NOW();
-                    mbar_arrive_expect_tx(full + st, STAGE_BYTES);
+                    if (!CPA) mbar_arrive_expect_tx(full + st, STAGE_BYTES);
                 }
+                if constexpr (CPA) {
+                    // every lane copies 8 of the 256 16-byte chunks of each 4 KiB K and V page
+                    // (consecutive lanes: consecutive 16 B of a row), swizzled as the TMA box
+                    // would land: [half][16 rows][128 B], chunk cc of row r at cc ^ (r & 7)
+                    __syncwarp();
+                    const uint32_t kst_a = smem_u32(kst);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        const int blk = __shfl_sync(0xffffffffu, zc, (bb0 & 31) + b);
+                        const bool ok = blk >= 0 && blk < p.N_B;
+                        if (lane == 0 && !ok && blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                        const size_t pg = ok ? ((size_t)blk * p.Hkv + d.g) * (R * 256) : 0;
+                        const uint32_t nbytes = ok ? 16u : 0u;  // 0: zero fill
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int idx = lane + 32 * e;      // chunk of the page, 0..255
+                            const int r = idx >> 4, c = idx & 15;
+                            const uint32_t so = (uint32_t)(b * (R * 256) + (c >> 3) * (R * 128) + r * 128 +
+                                                           (((c & 7) ^ (r & 7)) << 4));
+                            const size_t go = pg + (size_t)(r * 256 + c * 16);
+                            cp_async16_hint(kst_a + so, p.k_pool + go, nbytes, kv_pol);
+                            cp_async16_hint(kst_a + KV_BYTES + so, p.v_pool + go, nbytes, kv_pol);
+                        }
+                    }
+                    cp_async_mbar_arrive_noinc(full + st);
+                } else {
 #pragma unroll
                 for (int b = 0; b < NB; ++b) {
                     const int blk = __shfl_sync(0xffffffffu, zc, (bb0 & 31) + b);
@@ -377,6 +414,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                         tma_load_4d_hint(kst + b * (R * 256), &kmap, full + st, 0, y, 0, z, kv_pol);
                         tma_load_4d_hint(kst + KV_BYTES + b * (R * 256), &vmap, full + st, 0, y, 0, z, kv_pol);
                     }
+                }
                 }
                 if (lane == 0) TL_REC(1, gstage, tp0, tp1, TL_NOW());
                 __syncwarp();

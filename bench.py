@@ -210,6 +210,23 @@ def dist_info():
     return ws, rank, local
 
 
+def gpu_local_cpus(dev: torch.device):
+    """The host CPUs NVML reports as local to `dev` (its NUMA node), or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        idx = nvml_id(dev)
+        h = (pynvml.nvmlDeviceGetHandleByPciBusId(idx.encode()) if isinstance(idx, str)
+             else pynvml.nvmlDeviceGetHandleByIndex(idx))
+        n = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (n + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1}
+        cpus &= set(range(n))
+        return cpus or None
+    except Exception:
+        return None
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -865,6 +882,9 @@ def secondary_cfg4(args, dev, pk, layers: int = 8):
     w.set_prefix(0)
     ptr0 = w.pool.mem.data_ptr()
     sw = []
+    for _ in range(2):  # eager warm-up at the last split, so the first switch is not a cold step
+        w.corun_step(70, 30)
+    torch.cuda.synchronize(dev)
     for x, y in [(30, 70), (50, 50), (70, 30), (30, 70)]:
         ts = [time_steps(lambda: w.corun_step(x, y), 1, dev) * 1e3 for _ in range(3)]
         sw.append({"x": x, "first_ms": ts[0], "steady_ms": statistics.mean(ts[1:]),
@@ -1010,6 +1030,15 @@ def main(argv=None):
     w.pool.set_spans(None)
     e2e = None
     if not args.no_e2e:
+        # pinned host buffers on the GPU's own NUMA node (first touch by a local CPU) and the
+        # launching thread there too: a remote node would cap the host <-> device copies
+        local = gpu_local_cpus(dev)
+        saved = os.sched_getaffinity(0)
+        if local:
+            try:
+                os.sched_setaffinity(0, local)
+            except OSError:
+                local = None
         ee = E2E(w)
         for _ in range(2):
             ee.step(x, y)
@@ -1018,8 +1047,13 @@ def main(argv=None):
         e2e = {"value": w.tokens_per_step() / te, "unit": "tokens/s",
                "h2d_bytes_per_step": ee.h2d, "d2h_bytes_per_step": ee.d2h,
                "ms_per_step": te * 1e3,
-               "pcie_gbs_effective": (ee.h2d + ee.d2h) / te / 1e9}
+               "pcie_gbs_effective": (ee.h2d + ee.d2h) / te / 1e9,
+               "host_cpus_gpu_local": len(local) if local else None}
         del ee
+        try:
+            os.sched_setaffinity(0, saved)
+        except OSError:
+            pass
     dp = None
     if ws > 1 and not args.no_dp:
         # DP-replica reference (SURVEY §8(e) "Replicas"): every rank runs the TP-1 workload

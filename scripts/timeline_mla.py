@@ -24,7 +24,7 @@ spd._build.LIB = lib_tl
 spd._build.up_to_date = lambda: True
 L = spd.lib()
 budget = int(sys.argv[1]) if len(sys.argv) > 1 else 148
-B, ctx = 256, 1000
+B, ctx = int(os.environ.get("TL_B", "256")), int(os.environ.get("TL_CTX", "1000"))
 dev = torch.device("cuda", 0)
 nb = ctx // 64 + 1
 pool = spd.KVPool(spd.PoolConfig(1, B * nb + 4, 64, 1, 576, 512, B + 1, nb + 1, kv_shared=True), dev)

@@ -139,7 +139,7 @@ struct Bars {
 constexpr uint32_t OFF_Q = RING_BYTES;
 constexpr uint32_t OFF_P = OFF_Q + NQBUF * Q_BYTES;
 constexpr uint32_t OFF_RED = OFF_P + 2 * P_BYTES;            // [2][64] maxima, [64] sums
-constexpr uint32_t OFF_BARS = OFF_RED + 3 * 64 * 4;
+constexpr uint32_t OFF_BARS = OFF_RED + 4 * 64 * 4;
 constexpr uint32_t OFF_UNITS = OFF_BARS + sizeof(Bars);
 constexpr uint32_t OFF_MISC = OFF_UNITS + 2 * sizeof(TUnit);
 constexpr uint32_t SMEM_BYTES = 1024 + OFF_MISC + 16;
@@ -569,15 +569,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (two) mbar_wait(bar.o_done + (bl ^ 1), ((gt - 2) >> 1) & 1);
             tc_fence_after();
             named_bar_sync(1, NSOFT);
-            float L[NH], f2[NH], rl[NH];
-#pragma unroll
-            for (int h = 0; h < NH; ++h) {
-                L[h] = red_l[h] + red_l[NH + h] + red_l[2 * NH + h] + red_l[3 * NH + h];
-                f2[h] = two ? fast_exp2(mold2[h] - mrun[h]) : 0.f;
-                rl[h] = __frcp_rn(L[h]);
-            }
-            [[maybe_unused]] const long long te1 = TL_NOW();
             const bool split = d.S > 1;
+            // per-head factors, formed once by 16 threads into smem (registers stay free for
+            // the O^T tiles): fac[h] multiplies the last tile's buffer, fac[16 + h] the other
+            // one (its contents are relative to mold2); unsplit units fold in 1 / L
+            float* fac = red + 3 * 64;  // [3][16]: factor, other-buffer factor, L
+            if (tid < NH) {
+                float mr = mrun[0], mo = mold2[0];
+#pragma unroll
+                for (int h = 1; h < NH; ++h) {
+                    mr = tid == h ? mrun[h] : mr;
+                    mo = tid == h ? mold2[h] : mo;
+                }
+                const float Lh = red_l[tid] + red_l[NH + tid] + red_l[2 * NH + tid] + red_l[3 * NH + tid];
+                const float f2 = two ? fast_exp2(mo - mr) : 0.f;
+                const float r = split ? 1.f : __fdividef(1.f, Lh);
+                fac[tid] = r;
+                fac[NH + tid] = f2 * r;
+                fac[2 * NH + tid] = Lh;
+            }
+            named_bar_sync(1, NSOFT);
+            [[maybe_unused]] const long long te1 = TL_NOW();
             // per-unit bases: head h of this unit's output / partial row sits at base + h * hs
             __nv_bfloat16* obase = p.out + (p.out_head_major ? (size_t)d.b * DV : (size_t)d.b * p.G * DV);
             const size_t ohs = p.out_head_major ? (size_t)p.B * DV : (size_t)DV;
@@ -590,20 +602,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int m = 0; m < DV / 128; ++m) {
                 uint32_t o[NH], o2[NH];
                 tmem_ld16(tmem + lane_base + TM_O + bl * 64 + m * NH, o);
-                tmem_ld16(tmem + lane_base + TM_O + (bl ^ 1) * 64 + m * NH, o2);
+                if (two) tmem_ld16(tmem + lane_base + TM_O + (bl ^ 1) * 64 + m * NH, o2);
                 tmem_wait_ld();
                 const int dv = m * 128 + qd * 32 + lane;
-                float v[NH];
-#pragma unroll
-                for (int h = 0; h < NH; ++h)
-                    v[h] = two ? fmaf(__uint_as_float(o2[h]), f2[h], __uint_as_float(o[h]))
-                               : __uint_as_float(o[h]);
+                auto val = [&](int h) {
+                    const float x = __uint_as_float(o[h]) * fac[h];
+                    return two ? fmaf(__uint_as_float(o2[h]), fac[NH + h], x) : x;
+                };
                 if (!split) {
                     __nv_bfloat16* op = obase + (dv & ~1) + (odd ? 8 * ohs : 0);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         // even lanes store head j, odd lanes head j + 8
-                        const float a0 = v[j] * rl[j], a1 = v[j + 8] * rl[j + 8];
+                        const float a0 = val(j), a1 = val(j + 8);
                         const float send = odd ? a0 : a1;
                         const float got = __shfl_xor_sync(0xffffffffu, send, 1);
                         const int h = odd ? j + 8 : j;
@@ -615,21 +626,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     float* wp = wbase + dv;
 #pragma unroll
                     for (int h = 0; h < NH; ++h)
-                        if (h < p.G) wp[h * whs] = v[h];
+                        if (h < p.G) wp[h * whs] = val(h);
                 }
             }
             tc_fence_before();
             if (split) {
                 if (tid < p.G) {
                     const size_t pi = ((size_t)d.b * NH + tid) * p.S_max + d.s;
-                    float mv = mrun[0], lv = L[0];
+                    float mv = mrun[0];
 #pragma unroll
-                    for (int h = 1; h < NH; ++h) {
-                        mv = tid == h ? mrun[h] : mv;
-                        lv = tid == h ? L[h] : lv;
-                    }
+                    for (int h = 1; h < NH; ++h) mv = tid == h ? mrun[h] : mv;
                     p.ws_m[pi] = mv;
-                    p.ws_l[pi] = lv;
+                    p.ws_l[pi] = fac[2 * NH + tid];
                 }
                 __threadfence();
                 named_bar_sync(1, NSOFT);

@@ -48,13 +48,28 @@ int main() {
     printf("multicast granularity %zu\n", gran);
     mp.size = gran;
     CUmemGenericAllocationHandle mc;
-    CK(cuMulticastCreate(&mc, &mp));
+    {
+        const int nd[4] = {1, 1, 1, 2};
+        const CUmemAllocationHandleType ht[4] = {CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_NONE,
+                                                 CU_MEM_HANDLE_TYPE_FABRIC, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR};
+        CUresult ok = CUDA_ERROR_UNKNOWN;
+        for (int t = 0; t < 4; ++t) {
+            CUmulticastObjectProp q = mp;
+            q.numDevices = nd[t];
+            q.handleTypes = ht[t];
+            CUresult r = cuMulticastCreate(&mc, &q);
+            printf("cuMulticastCreate numDevices %d handleTypes %d -> %d\n", nd[t], (int)ht[t], (int)r);
+            if (r == CUDA_SUCCESS && nd[t] == 1) { ok = r; mp = q; break; }
+            if (r == CUDA_SUCCESS) cuMemRelease(mc);
+        }
+        if (ok != CUDA_SUCCESS) return 1;
+    }
     CK(cuMulticastAddDevice(mc, dev));
     CUmemAllocationProp ap = {};
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = 0;
-    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    ap.requestedHandleTypes = (CUmemAllocationHandleType)mp.handleTypes;
     size_t mgran = 0;
     CK(cuMemGetAllocationGranularity(&mgran, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
     const size_t sz = ((gran + mgran - 1) / mgran) * mgran;

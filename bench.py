@@ -84,6 +84,10 @@ def parse(argv=None):
     ap.add_argument("--nccl-max-ctas", type=int, default=4,
                     help="ncclConfig_t.maxCTAs of each phase communicator (counted inside the "
                          "phase budget in pipelined mode)")
+    ap.add_argument("--tails", default="0:0,0:4,0:8,0:12,4:0,8:0",
+                    help="tail_p:tail_d schedules swept with every split (R30: the last layers of "
+                         "the worker that finishes second run on all SMs once the other is done); "
+                         "0:0 = the pure split")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every kernel from Python instead of replaying a CUDA graph")
@@ -359,8 +363,10 @@ class Workload:
                 self.fused = True
                 self.od = [self.peer_d.local_view(l % 2) for l in range(self.L)]
                 self.op = [self.peer_p.local_view(l % 2) for l in range(self.L)]
-        # device-side launch spans: prefill launches first (slots 0..L-1), then decode
+        # device-side launch spans: slots in enqueue order (corun_step sets span_order)
         self.spans = torch.zeros(2 * self.L + 8, 8, dtype=torch.int64, device=dev)
+        self.span_order = ("prefill", "decode")
+        self.ev_p_done, self.ev_d_done = torch.cuda.Event(), torch.cuda.Event()
 
     def set_prefix(self, P: int):
         """The prefill request's prefix length (its chunk's blocks are allocated per step)."""
@@ -383,9 +389,10 @@ class Workload:
     def arm_spans(self):
         self.pool.set_spans(self.spans)
 
-    def kernel_stats(self, order=("prefill", "decode")):
+    def kernel_stats(self, order=None):
         """Mean launch duration (ms) per phase over everything folded into the spans since
         the last zero, and the last launch sequence's per-stream spans."""
+        order = order or self.span_order
         sp = self.spans.cpu().numpy().astype(np.float64)
         out = {}
         for i, ph in enumerate(order):
@@ -426,13 +433,19 @@ class Workload:
             return max(1, n - self.nccl_ctas)
         return budget
 
-    def phase_prefill(self, budget=0, stream=None):
+    def phase_prefill(self, budget=0, stream=None, tail=0):
+        """The prefill worker's iteration.  tail > 0: the last `tail` layers wait until the
+        decode worker has issued all of its launches and then run on every SM (the freed
+        decode SMs are adopted at the next launch, R30)."""
         s = stream or self.sP
         p = self.pool
         b = self._budget(budget, "p")
         with torch.cuda.stream(s):
             p.alloc_blocks(self.rid_pre, self.nblk_pre, None, stream=s)
             for l in range(self.L):
+                if tail and l == self.L - tail:
+                    s.wait_event(self.ev_d_done)
+                    b = p.num_sms
                 if self.fused:
                     p.set_prefill_peers(self.peer_p.peer_shard_ptrs(l % 2), self.C)
                     self.peer_p.handshake(0, stream=s)  # every peer is done reading
@@ -444,13 +457,19 @@ class Workload:
             p.free_blocks(self.rid_pre, None, stream=s)
             if self.cP is not None:
                 s.wait_stream(self.cP)
+            self.ev_p_done.record(s)
 
-    def phase_decode(self, budget=0, stream=None):
+    def phase_decode(self, budget=0, stream=None, tail=0):
+        """The decode worker's iteration; tail as for phase_prefill (waits for the prefill
+        worker's last launch, then runs its last `tail` layers on every SM)."""
         s = stream or self.sD
         p = self.pool
         b = self._budget(budget, "d")
         with torch.cuda.stream(s):
             for l in range(self.L):
+                if tail and l == self.L - tail:
+                    s.wait_event(self.ev_p_done)
+                    b = p.num_sms
                 if self.fused:
                     p.set_decode_peers(self.peer_d.peer_shard_ptrs(l % 2), self.B)
                     self.peer_d.handshake(0, stream=s)
@@ -461,15 +480,26 @@ class Workload:
                     self._gather("d", l, s)
             if self.cD is not None:
                 s.wait_stream(self.cD)
+            self.ev_d_done.record(s)
 
-    def corun_step(self, x, y):
-        """One co-run iteration: both workers concurrently at budgets from (x, y)."""
+    def corun_step(self, x, y, tail_p=0, tail_d=0):
+        """One co-run iteration: both workers concurrently at budgets from (x, y).  With
+        tail_d (tail_p) > 0 the decode (prefill) worker's last layers run on all SMs once the
+        other worker is done (R30); at most one of the two is non-zero.  The worker that
+        waits is enqueued second, so its event wait sees this iteration's record."""
+        assert not (tail_p and tail_d)
         main = torch.cuda.current_stream(self.dev)
         self.pool.set_partition(x, y)
         self.sP.wait_stream(main)
         self.sD.wait_stream(main)
-        self.phase_prefill(0)
-        self.phase_decode(0)
+        if tail_p:
+            self.span_order = ("decode", "prefill")
+            self.phase_decode(0)
+            self.phase_prefill(0, tail=tail_p)
+        else:
+            self.span_order = ("prefill", "decode")
+            self.phase_prefill(0)
+            self.phase_decode(0, tail=tail_d)
         main.wait_stream(self.sP)
         main.wait_stream(self.sD)
 
@@ -583,25 +613,29 @@ def phase_record(w: Workload, n_p: int, n_d: int, t_step: float, ks: dict, pk: d
     return rec
 
 
-def sweep_splits(w: Workload, run: Runner, xs, pk, reps=3, refine=True):
-    """Co-run at every x in xs (y = 100 - x), graph-replayed; refine +-2.5 / 5 around the
-    best tokens/s.  Returns the records."""
+def sweep_splits(w: Workload, run: Runner, xs, pk, reps=3, refine=True, tails=((0, 0),)):
+    """Co-run at every x in xs (y = 100 - x) and every (tail_p, tail_d) schedule in `tails`,
+    graph-replayed; refine +-2.5 / 5 around the best tokens/s with its tail.  Returns the
+    records (pure splits have tail_p = tail_d = 0)."""
     out = []
 
-    def measure(x):
-        step = run.capture(lambda: w.corun_step(x, 100 - x))
+    def measure(x, tp=0, td=0):
+        step = run.capture(lambda: w.corun_step(x, 100 - x, tp, td))
         t, ks = run.time(step, reps)
         n_p, n_d = w.pool.sm_budgets()
-        out.append({"x": x, "y": 100 - x, **phase_record(w, n_p, n_d, t, ks, pk)})
+        out.append({"x": x, "y": 100 - x, "tail_p": tp, "tail_d": td,
+                    **phase_record(w, n_p, n_d, t, ks, pk)})
 
     for x in xs:
-        measure(x)
+        for tp, td in tails:
+            measure(x, tp, td)
     if refine and len(xs) > 1:
-        x0 = max(out, key=lambda r: r["tokens_per_s"])["x"]
-        for x in (x0 - 5, x0 - 2.5, x0 + 2.5, x0 + 5):
-            if 0 < x < 100 and all(abs(r["x"] - x) > 1e-6 for r in out):
-                measure(x)
-    out.sort(key=lambda r: r["x"])
+        b = max(out, key=lambda r: r["tokens_per_s"])
+        for x in (b["x"] - 5, b["x"] - 2.5, b["x"] + 2.5, b["x"] + 5):
+            if 0 < x < 100 and all(abs(r["x"] - x) > 1e-6 or (r["tail_p"], r["tail_d"]) !=
+                                   (b["tail_p"], b["tail_d"]) for r in out):
+                measure(x, b["tail_p"], b["tail_d"])
+    out.sort(key=lambda r: (r["x"], r["tail_p"], r["tail_d"]))
     return out
 
 
@@ -646,8 +680,9 @@ class E2E:
         self.in_p, self.in_d, self.out_p, self.out_d = ev(), ev(), ev(), ev()
         self.done_p, self.done_d = ev(), ev()
 
-    def step(self, x, y):
+    def step(self, x, y, tail_p=0, tail_d=0):
         w = self.w
+        assert not (tail_p and tail_d)
         main = torch.cuda.current_stream(w.dev)
         w.pool.set_partition(x, y)
         for s in (self.s_in, self.s_out, w.sP, w.sD):
@@ -668,38 +703,64 @@ class E2E:
                 cp(w.vp[l], self.h_vp[l])
                 self.in_p[l].record(self.s_in)
         tp = w.tp > 1
-        with torch.cuda.stream(w.sP):
-            w.pool.alloc_blocks(w.rid_pre, w.nblk_pre, None, stream=w.sP)
-            for l in range(w.L):
-                w.sP.wait_event(self.in_p[l])
-                if w.fused:
-                    if l >= 2:
-                        w.sP.wait_event(self.done_p[l - 2])  # buffer l % 2 read out
-                    w.pool.set_prefill_peers(w.peer_p.peer_shard_ptrs(l % 2), w.C)
-                    w.peer_p.handshake(0, stream=w.sP)
-                w.pool.prefill_attn(l, w.qp[l], w.kp[l], w.vp[l], w.cu, w.rid_pre, w.prefix, w.C,
-                                    w.C, w.scale, w.op[l], out_head_major=tp, stream=w.sP)
-                if tp:
-                    w._gather("p", l, w.sP)  # same exchange step as the device-timed path
-                self.out_p[l].record(w.sP)
-            w.pool.free_blocks(w.rid_pre, None, stream=w.sP)
-            if w.cP is not None:
-                w.sP.wait_stream(w.cP)
-        with torch.cuda.stream(w.sD):
-            for l in range(w.L):
-                w.sD.wait_event(self.in_d[l])
-                if w.fused:
-                    if l >= 2:
-                        w.sD.wait_event(self.done_d[l - 2])
-                    w.pool.set_decode_peers(w.peer_d.peer_shard_ptrs(l % 2), w.B)
-                    w.peer_d.handshake(0, stream=w.sD)
-                w.pool.decode_attn(l, w.qd[l], w.kd[l], w.vd[l], w.rid_dec, w.ctx_lens, w.ctx,
-                                   w.scale, w.od[l], w.ws, out_head_major=tp, stream=w.sD)
-                if tp:
-                    w._gather("d", l, w.sD)
-                self.out_d[l].record(w.sD)
-            if w.cD is not None:
-                w.sD.wait_stream(w.cD)
+        nsm = w.pool.num_sms
+
+        def prefill_phase():
+            with torch.cuda.stream(w.sP):
+                w.pool.alloc_blocks(w.rid_pre, w.nblk_pre, None, stream=w.sP)
+                for l in range(w.L):
+                    w.sP.wait_event(self.in_p[l])
+                    b = 0
+                    if tail_p and l >= w.L - tail_p:
+                        if l == w.L - tail_p:
+                            w.sP.wait_event(w.ev_d_done)
+                        b = nsm
+                    if w.fused:
+                        if l >= 2:
+                            w.sP.wait_event(self.done_p[l - 2])  # buffer l % 2 read out
+                        w.pool.set_prefill_peers(w.peer_p.peer_shard_ptrs(l % 2), w.C)
+                        w.peer_p.handshake(0, stream=w.sP)
+                    w.pool.prefill_attn(l, w.qp[l], w.kp[l], w.vp[l], w.cu, w.rid_pre, w.prefix,
+                                        w.C, w.C, w.scale, w.op[l], out_head_major=tp,
+                                        sm_budget=b, stream=w.sP)
+                    if tp:
+                        w._gather("p", l, w.sP)  # same exchange step as the device-timed path
+                    self.out_p[l].record(w.sP)
+                w.pool.free_blocks(w.rid_pre, None, stream=w.sP)
+                if w.cP is not None:
+                    w.sP.wait_stream(w.cP)
+                w.ev_p_done.record(w.sP)
+
+        def decode_phase():
+            with torch.cuda.stream(w.sD):
+                for l in range(w.L):
+                    w.sD.wait_event(self.in_d[l])
+                    b = 0
+                    if tail_d and l >= w.L - tail_d:
+                        if l == w.L - tail_d:
+                            w.sD.wait_event(w.ev_p_done)
+                        b = nsm
+                    if w.fused:
+                        if l >= 2:
+                            w.sD.wait_event(self.done_d[l - 2])
+                        w.pool.set_decode_peers(w.peer_d.peer_shard_ptrs(l % 2), w.B)
+                        w.peer_d.handshake(0, stream=w.sD)
+                    w.pool.decode_attn(l, w.qd[l], w.kd[l], w.vd[l], w.rid_dec, w.ctx_lens, w.ctx,
+                                       w.scale, w.od[l], w.ws, out_head_major=tp, sm_budget=b,
+                                       stream=w.sD)
+                    if tp:
+                        w._gather("d", l, w.sD)
+                    self.out_d[l].record(w.sD)
+                if w.cD is not None:
+                    w.sD.wait_stream(w.cD)
+                w.ev_d_done.record(w.sD)
+
+        if tail_p:
+            decode_phase()
+            prefill_phase()
+        else:
+            prefill_phase()
+            decode_phase()
         with torch.cuda.stream(self.s_out):
             for l in range(w.L):
                 self.s_out.wait_event(self.out_d[l])
@@ -942,16 +1003,19 @@ def main(argv=None):
         w.corun_step(50, 50)
     # ---- split sweep (graph-replayed, per-split roofline record; not part of the value)
     xs = [float(x) for x in args.sweep.split(",")] if args.split is None else [args.split]
-    sweep = sweep_splits(w, run, xs, pk, reps=3, refine=args.split is None)
+    tails = tuple(tuple(int(v) for v in t.split(":")) for t in args.tails.split(","))
+    sweep = sweep_splits(w, run, xs, pk, reps=3, refine=args.split is None, tails=tails)
     best, tgt = best_of(sweep)
-    x, y = best["x"], best["y"]
+    pure = [r for r in sweep if r["tail_p"] == 0 and r["tail_d"] == 0]
+    best_pure = max(pure, key=lambda r: r["tokens_per_s"]) if pure else None
+    x, y, tp, td = best["x"], best["y"], best["tail_p"], best["tail_d"]
     # library launches of one step (an eager step; graph replays launch the same kernels)
     c0 = w.pool.launch_count()
-    w.corun_step(x, y)
+    w.corun_step(x, y, tp, td)
     torch.cuda.synchronize(dev)
     per_step = w.pool.launch_count() - c0
-    # ---- the timed region: K replays of the captured co-run step at the best split
-    step = run.capture(lambda: w.corun_step(x, y))
+    # ---- the timed region: K replays of the captured co-run step at the best schedule
+    step = run.capture(lambda: w.corun_step(x, y, tp, td))
     for _ in range(W):
         step()
     w.spans.zero_()
@@ -1041,9 +1105,9 @@ def main(argv=None):
                 local = None
         ee = E2E(w)
         for _ in range(2):
-            ee.step(x, y)
+            ee.step(x, y, tp, td)
         ne = max(2, min(args.steps, 5))
-        te = max_over_ranks(time_steps(lambda: ee.step(x, y), ne, dev, barrier) / ne, ws, dev)
+        te = max_over_ranks(time_steps(lambda: ee.step(x, y, tp, td), ne, dev, barrier) / ne, ws, dev)
         e2e = {"value": w.tokens_per_step() / te, "unit": "tokens/s",
                "h2d_bytes_per_step": ee.h2d, "d2h_bytes_per_step": ee.d2h,
                "ms_per_step": te * 1e3,
@@ -1060,9 +1124,9 @@ def main(argv=None):
         # on its own GPU, no collective; ideal weak scaling
         full = Workload(shape, 1, dev, seed=1020 + rank)
         rr = Runner(full, dev, barrier, not args.no_graph, ws)
-        td = rr.time(rr.capture(lambda: full.corun_step(x, y)), 5)[0]
-        dp = {"value": ws * full.tokens_per_step() / td, "unit": "tokens/s",
-              "ms_per_step": td * 1e3, "scaling": "weak", "replicas": ws,
+        t_dp = rr.time(rr.capture(lambda: full.corun_step(x, y, tp, td)), 5)[0]
+        dp = {"value": ws * full.tokens_per_step() / t_dp, "unit": "tokens/s",
+              "ms_per_step": t_dp * 1e3, "scaling": "weak", "replicas": ws,
               "split": {"x": x, "y": y}, "cuda_graph": rr.use_graph}
         del rr, full
     graph_used, graph_error = run.use_graph, run.graph_error
@@ -1087,7 +1151,13 @@ def main(argv=None):
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {**workload_config(shape, ws, args.gather, args.tp_mode),
-                       "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d}},
+                       "split": {"x": x, "y": y, "n_prefill_sms": n_p, "n_decode_sms": n_d,
+                                 "tail_p": tp, "tail_d": td,
+                                 "schedule": "pure split" if not (tp or td) else
+                                 f"split, then the last {tp or td} {'prefill' if tp else 'decode'} "
+                                 f"layers on all {w.pool.num_sms} SMs once the other worker is "
+                                 f"done (R30)"}},
+            "best_pure_split": best_pure,
             "roofline": roof_dec if dominant == "decode" else roof_pre,
             "roofline_decode": roof_dec, "roofline_prefill": roof_pre, "roofline_step": roof_step,
             "kernel_time_check": consistency,

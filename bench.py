@@ -84,7 +84,7 @@ def parse(argv=None):
     ap.add_argument("--nccl-max-ctas", type=int, default=4,
                     help="ncclConfig_t.maxCTAs of each phase communicator (counted inside the "
                          "phase budget in pipelined mode)")
-    ap.add_argument("--tails", default="0:0,0:4,0:8,0:12,4:0,8:0",
+    ap.add_argument("--tails", default="0:0",
                     help="tail_p:tail_d schedules swept with every split (R30: the last layers of "
                          "the worker that finishes second run on all SMs once the other is done); "
                          "0:0 = the pure split")

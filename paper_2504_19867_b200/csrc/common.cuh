@@ -163,6 +163,13 @@ SPD_DEV void tma_load_4d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, in
         "l"(policy)
         : "memory");
 }
+// L2 prefetch of one 4-D box (no shared memory, no barrier: fire and forget)
+SPD_DEV void tma_prefetch_l2_4d(const CUtensorMap* m, int x, int y, int z, int w) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(x), "r"(y), "r"(z), "r"(w)
+                 : "memory");
+}
 // smem -> global tensor store (bulk async group), and the group completion waits
 SPD_DEV void tma_store_3d(const CUtensorMap* m, const void* src, int x, int y, int z) {
     asm volatile(

@@ -39,6 +39,15 @@ constexpr int HD = 128;           // head dim (dk == dv)
 // SLOWER at every SM budget (cfg-2 decode, bs 16: 3.58 vs 3.95 TB/s at 104 SMs, 4.46 vs 4.92 at
 // 148; profiles/r2_decode_bs16_cpasync_ab.log): the 4 KiB TMA box is not what limits 16-token
 // pages, so the default stays 0 (TMA).
+// SPD_DEC_PF = D > 0: the producer also prefetches the boxes D stages ahead of the one it loads
+// into L2 (cp.async.bulk.prefetch.tensor: no smem, no barrier), so the ring's own loads hit
+// L2 and a slot is held for less than the HBM round trip.  Measured (profiles/r2_l2_prefetch_ab.log):
+// D = 2 / 4 are 13-37 % SLOWER (bs 16: 3.96 -> 2.47 TB/s at 104 SMs; bs 64: 6.02 -> 5.20 at 89):
+// a prefetch costs the SM's TMA engine as much as a load, and that engine is what bounds
+// small pages.  Default 0.
+#ifndef SPD_DEC_PF
+#define SPD_DEC_PF 0
+#endif
 #ifndef SPD_DEC_CPASYNC
 #define SPD_DEC_CPASYNC 0
 #endif
@@ -413,6 +422,21 @@ __global__ void __launch_bounds__(4 * 32, 1)
                         const int y = (d.k0 + i * KPS + b * R) & bs_mask;
                         tma_load_4d_hint(kst + b * (R * 256), &kmap, full + st, 0, y, 0, z, kv_pol);
                         tma_load_4d_hint(kst + KV_BYTES + b * (R * 256), &vmap, full + st, 0, y, 0, z, kv_pol);
+                    }
+                }
+                if constexpr (SPD_DEC_PF > 0) {
+                    // boxes SPD_DEC_PF stages ahead: in this 32-box batch (zc) or the next (zn)
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        const int pbi = bb0 + SPD_DEC_PF * NB + b;
+                        const int src = pbi - (bb0 & ~31);
+                        const int v = __shfl_sync(0xffffffffu, src < 32 ? zc : zn, src & 31);
+                        if (lane == 0 && pbi < nbox && src < 64 && v >= 0 && v < p.N_B) {
+                            const int y = (d.k0 + i * KPS + SPD_DEC_PF * KPS + b * R) & bs_mask;
+                            const int z = v * p.Hkv + d.g;
+                            tma_prefetch_l2_4d(&kmap, 0, y, 0, z);
+                            tma_prefetch_l2_4d(&vmap, 0, y, 0, z);
+                        }
                     }
                 }
                 }

@@ -42,6 +42,13 @@ constexpr uint32_t HI_BYTES = (NCB - CB_LO) * PAGE * 128;  // 40 KiB
 // microbench, 2 reps): DQ = 1 is 1-6 % SLOWER at every shape (B 256 ctx 350 at 44 / 104 /
 // 148 SMs, B 256 ctx 1000, B 64 ctx 4000): the unit boundary is not held by the Q load, and
 // the shallower ring costs more than the second Q buffer gains.  Default 0.
+// SPD_MLA_PF = D > 0: the producer prefetches page i + D (both boxes) into L2 after loading
+// page i, so a ring slot is held for an L2 hit instead of the HBM round trip.  Measured 1-12 %
+// SLOWER (B 256 ctx 350: 3.17 -> 2.81 TB/s at 148 SMs; profiles/r2_l2_prefetch_ab.log).
+// Default 0.
+#ifndef SPD_MLA_PF
+#define SPD_MLA_PF 0
+#endif
 #ifndef SPD_MLA_DQ
 #define SPD_MLA_DQ 0
 #endif
@@ -302,6 +309,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mbar_arrive_expect_tx(bar.full + s1, HI_BYTES);
                     tma_load_4d(ring + slot_off(s1), &map_hi, bar.full + s1, 0, 0, CB_LO, z);
                     TL_REC(1, gh / 2, tp0, tp1, TL_NOW());
+                }
+                if constexpr (SPD_MLA_PF > 0) {
+                    // page i + D of this unit, if its block id is in the current 32-page batch
+                    const int ip = i + SPD_MLA_PF;
+                    const int bp = __shfl_sync(0xffffffffu, blk_l, ip & 31);
+                    if (lane == 0 && ip < d.nt && (ip >> 5) == (i >> 5) && bp >= 0 && bp < p.N_B) {
+                        tma_prefetch_l2_4d(&map_lo, 0, 0, 0, bp);
+                        tma_prefetch_l2_4d(&map_hi, 0, 0, CB_LO, bp);
+                    }
                 }
                 __syncwarp();
             }

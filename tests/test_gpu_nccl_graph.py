@@ -52,9 +52,10 @@ def _main(port, q):
         gd = torch.full((32, B, 128), float("nan"), dtype=torch.bfloat16, device=dev)
         ws = pool.new_decode_workspace(B, 32, max(ctx))
         s = torch.cuda.Stream(dev)
+        ids, ctx_d = i32(range(B)), i32(ctx)
 
         def step():
-            pool.decode_attn(0, qd, kd, vd, i32(range(B)), i32(ctx), max(ctx),
+            pool.decode_attn(0, qd, kd, vd, ids, ctx_d, max(ctx),
                              shape.softmax_scale, od, ws, out_head_major=True,
                              stream=torch.cuda.current_stream(dev))
             tp.gather_heads(od, gd, groups.decode)

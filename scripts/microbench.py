@@ -60,6 +60,8 @@ def main():
                          "(SURVEY §8(d) item 7, load balance)")
     ap.add_argument("--mla", action="store_true", help="cfg5 absorbed-MLA decode (576/512, 16 heads)")
     ap.add_argument("--mla-prefill", action="store_true", help="cfg5 absorbed-MLA prefill chunk")
+    ap.add_argument("--ctx-lognormal", action="store_true",
+                    help="--mla: contexts lognormal around --ctx (sigma 0.5, seed 5005), as bench.py cfg5")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     if args.mla:
@@ -123,11 +125,19 @@ def main():
 def mla(args, dev):
     """MLA decode: B requests at ctx, latent 576 (V = first 512), 16 heads, bs 64."""
     L, B, ctx, bs = args.layers, args.batch, args.ctx, 64
-    nb = ctx // bs + 1
-    cfg = PoolConfig(L, B * nb + 4, bs, 1, 576, 512, B + 1, nb + 1, kv_shared=True)
+    if args.ctx_lognormal:  # the bench's cfg-5 mix: lognormal around --ctx (sigma 0.5, seed 5005)
+        import numpy as np
+        rng = np.random.default_rng(5005)
+        ctx_list = [int(c) for c in np.clip(rng.lognormal(math.log(ctx) - 0.125, 0.5, B), 64, 4096)]
+    else:
+        ctx_list = [ctx] * B
+    ctx = max(ctx_list)
+    nbs = [c // bs + 1 for c in ctx_list]
+    nb = max(nbs)
+    cfg = PoolConfig(L, sum(nbs) + 4, bs, 1, 576, 512, B + 1, nb + 1, kv_shared=True)
     pool = KVPool(cfg, dev)
     i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
-    pool.alloc_blocks(i32(list(range(B))), i32([nb] * B))
+    pool.alloc_blocks(i32(list(range(B))), i32(nbs))
     g = torch.Generator(device=dev)
     g.manual_seed(0)
     for l in range(L):
@@ -137,9 +147,9 @@ def mla(args, dev):
     kn = torch.randn(B, 1, 576, device=dev, generator=g).bfloat16()
     out = torch.empty(B, 16, 512, dtype=torch.bfloat16, device=dev)
     ws = pool.new_decode_workspace(B, 16, ctx)
-    rid, ctxs = i32(list(range(B))), i32([ctx] * B)
-    byts = B * (ctx + 1) * 576 * 2 + B * 16 * (576 + 512) * 2
-    flops = 2 * B * 16 * (ctx + 1) * (576 + 512)
+    rid, ctxs = i32(list(range(B))), i32(ctx_list)
+    byts = sum(c + 1 for c in ctx_list) * 576 * 2 + B * 16 * (576 + 512) * 2
+    flops = 2 * sum(c + 1 for c in ctx_list) * 16 * (576 + 512)
     for bud in [int(x) for x in args.budgets.split(",")]:
         for l in range(min(L, 3)):
             pool.decode_attn(l, q, kn, None, rid, ctxs, ctx, 1 / math.sqrt(192), out, ws, sm_budget=bud)

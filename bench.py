@@ -1011,6 +1011,7 @@ def secondary_cfg5(args, dev, pk):
     at lognormal contexts (mean ~350, seed 5005) co-running with a 2048-token prefill chunk."""
     rng = np.random.default_rng(5005)
     ctx = [int(c) for c in np.clip(rng.lognormal(math.log(350.0) - 0.125, 0.5, 256), 64, 4096)]
+    ctx.sort(reverse=True)  # the engine's decode batch order: longest first (LPT, engine.py)
     w = Workload(synth.CFG5_MLA, 1, dev, seed=1050, B=256, ctx=ctx, C=2048)
     return _sweep_field(w, dev, pk, [30, 40, 50, 60, 70], model="deepseek-v2-lite-mla",
                         decode_ctx_mean=statistics.mean(ctx))

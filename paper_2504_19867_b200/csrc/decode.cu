@@ -1207,9 +1207,7 @@ size_t semipd_decode_workspace_bytes(semipd_pool_t pool, int32_t max_batch, int3
         if (m2 > part) part = m2;
     }
     const int hkv = pool->cfg.num_kv_heads > 0 ? pool->cfg.num_kv_heads : 1;
-    // MLA latent pools also keep a [B] request order next to the counters (decode_mla_tc.cu)
-    const size_t n_cnt = (size_t)max_batch * (pool->cfg.kv_shared ? 2 : hkv);
-    return spd_ws_counter_bytes(n_cnt) + part;
+    return spd_ws_counter_bytes((size_t)max_batch * hkv) + part;
 }
 
 semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* q,

@@ -49,12 +49,6 @@ constexpr uint32_t HI_BYTES = (NCB - CB_LO) * PAGE * 128;  // 40 KiB
 #ifndef SPD_MLA_PF
 #define SPD_MLA_PF 0
 #endif
-// SPD_MLA_LPT = 1: a one-CTA pre-pass orders the requests by context length (longest first,
-// ties by index) into the workspace and the persistent grid takes units in that order, so the
-// dynamic counter hands out the longest units first (LPT) at every split level
-#ifndef SPD_MLA_LPT
-#define SPD_MLA_LPT 1
-#endif
 #ifndef SPD_MLA_DQ
 #define SPD_MLA_DQ 0
 #endif
@@ -118,7 +112,6 @@ struct TcParams {
     float* ws_l;
     float* ws_acc;            // [B][16][S_max][512]
     int* ws_cnt;              // [B]
-    const int* order;         // [B] requests longest first (SPD_MLA_LPT), or null
     unsigned* sched;
     int* status;
     unsigned long long* span;  // semipd_set_spans record of this launch (or null)
@@ -248,7 +241,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // longest-first: units of the highest split index (full-length splits of the
                 // longest requests) are handed out first
                 d.s = p.S_max - 1 - u / p.B;
-                d.b = p.order ? __ldg(p.order + u % p.B) : u % p.B;
+                d.b = u % p.B;
                 ctx = __ldg(p.ctx_lens + d.b);
                 rid = __ldg(p.req_ids + d.b);
                 d.S = n_splits(ctx, p.S_fill);
@@ -784,27 +777,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 
-// order[r] = the request with the r-th longest context (ties: lower index first): a rank per
-// request by counting, contexts staged in smem
-constexpr int LPT_SMEM = 4096;
-__global__ void __launch_bounds__(1024) mla_lpt_order_kernel(const int* __restrict__ ctx, int B,
-                                                              int* __restrict__ order) {
-    __shared__ int c[LPT_SMEM];
-    const bool staged = B <= LPT_SMEM;
-    if (staged)
-        for (int j = threadIdx.x; j < B; j += blockDim.x) c[j] = __ldg(ctx + j);
-    __syncthreads();
-    for (int b = threadIdx.x; b < B; b += blockDim.x) {
-        const int kb = staged ? c[b] : __ldg(ctx + b);
-        int r = 0;
-        for (int j = 0; j < B; ++j) {
-            const int kj = staged ? c[j] : __ldg(ctx + j);
-            r += (kj > kb) || (kj == kb && j < b);
-        }
-        order[r] = b;
-    }
-}
-
 }  // namespace
 
 bool spd_mla_tc_ok(const semipd_pool* p, int Hq) {
@@ -832,9 +804,7 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
     const int S_fill = fill_splits(batch);
     const int S_max = max_splits(max_ctx_len, S_fill);
     SpdWs w;
-    // counters [B] + (SPD_MLA_LPT) the request order [B] in the counter region
-    if (!spd_ws_carve(workspace, ws_bytes, SPD_MLA_LPT ? 2 * (size_t)batch : batch, (size_t)batch * NH,
-                      S_max, DV, &w))
+    if (!spd_ws_carve(workspace, ws_bytes, batch, (size_t)batch * NH, S_max, DV, &w))
         return SEMIPD_ERR_INVALID;
     if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) return SEMIPD_ERR_INVALID;
     // Q [B][Hq][576] as (64 cols, Hq heads, 9 column blocks, B): box lands [cb][16 rows][128 B];
@@ -856,14 +826,6 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
     prm.k_pool = static_cast<unsigned char*>(pool->k_layer(layer));
     prm.out = static_cast<__nv_bfloat16*>(out);
     prm.ws_cnt = w.cnt;
-    prm.order = nullptr;
-    if (SPD_MLA_LPT && batch > 1) {
-        int* order = w.cnt + batch;
-        mla_lpt_order_kernel<<<1, 1024, 0, st>>>(ctx_lens, batch, order);
-        if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
-        pool->launches += 1;
-        prm.order = order;
-    }
     prm.sched = w.sched;
     prm.ws_m = w.m;
     prm.ws_l = w.l;

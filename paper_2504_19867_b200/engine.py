@@ -111,6 +111,10 @@ class Scheduler:
                 r.nblk += need
                 allocs.append((r.slot, need))
             plan.decode.append((r, r.ctx))
+        # the decode batch goes to the device longest context first: the persistent decode
+        # grids take units in batch order, so this is LPT scheduling of the requests (the
+        # outputs are per row; the order changes no result, R26)
+        plan.decode.sort(key=lambda rc: -rc[1])
         # prefill: FCFS chunk budget; headroom of one block per running request keeps
         # decode from starving (a waiting request never takes the last blocks)
         budget = self.chunk_budget

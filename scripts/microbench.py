@@ -60,6 +60,7 @@ def main():
                          "(SURVEY §8(d) item 7, load balance)")
     ap.add_argument("--mla", action="store_true", help="cfg5 absorbed-MLA decode (576/512, 16 heads)")
     ap.add_argument("--mla-prefill", action="store_true", help="cfg5 absorbed-MLA prefill chunk")
+    ap.add_argument("--lpt", action="store_true", help="--ctx-lognormal: batch longest first")
     ap.add_argument("--ctx-lognormal", action="store_true",
                     help="--mla: contexts lognormal around --ctx (sigma 0.5, seed 5005), as bench.py cfg5")
     args = ap.parse_args()
@@ -129,6 +130,8 @@ def mla(args, dev):
         import numpy as np
         rng = np.random.default_rng(5005)
         ctx_list = [int(c) for c in np.clip(rng.lognormal(math.log(ctx) - 0.125, 0.5, B), 64, 4096)]
+        if args.lpt:
+            ctx_list.sort(reverse=True)
     else:
         ctx_list = [ctx] * B
     ctx = max(ctx_list)

@@ -950,7 +950,7 @@ def _sweep_field(w: Workload, dev, pk, xs, **info):
 def secondary_block16(args, dev, pk):
     """The headline workload with 16-token pages (SURVEY S7's reading)."""
     shape = dataclasses.replace(MODELS[args.model], block_size=16)
-    return _sweep_field(Workload(shape, 1, dev, seed=1016), dev, pk, [30, 40, 50],
+    return _sweep_field(Workload(shape, 1, dev, seed=1016), dev, pk, [20, 25, 30, 40, 50],
                         block_size=16)
 
 
@@ -958,7 +958,7 @@ def secondary_cfg3(args, dev, pk):
     """BASELINE configs[2] shapes on one GPU (TP 1): Llama-3-70B attention (Hq 64, Hkv 8,
     G = 8), 80 layers, same per-step workload."""
     shape = dataclasses.replace(synth.CFG3_LLAMA70B, block_size=args.block_size)
-    return _sweep_field(Workload(shape, 1, dev, seed=1030), dev, pk, [40, 45, 50, 55, 60],
+    return _sweep_field(Workload(shape, 1, dev, seed=1030), dev, pk, [30, 35, 40, 45, 50, 55, 60],
                         model="llama3-70b (TP 1)")
 
 
@@ -1013,7 +1013,7 @@ def secondary_cfg5(args, dev, pk):
     ctx = [int(c) for c in np.clip(rng.lognormal(math.log(350.0) - 0.125, 0.5, 256), 64, 4096)]
     ctx.sort(reverse=True)  # the engine's decode batch order: longest first (LPT, engine.py)
     w = Workload(synth.CFG5_MLA, 1, dev, seed=1050, B=256, ctx=ctx, C=2048)
-    return _sweep_field(w, dev, pk, [30, 40, 50, 60, 70], model="deepseek-v2-lite-mla",
+    return _sweep_field(w, dev, pk, [15, 20, 25, 30, 40, 50, 60, 70], model="deepseek-v2-lite-mla",
                         decode_ctx_mean=statistics.mean(ctx))
 
 

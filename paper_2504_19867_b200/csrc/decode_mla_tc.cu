@@ -95,7 +95,18 @@ inline int max_splits(int max_ctx, int S_fill) {
     return m;
 }
 constexpr float LOG2E = 1.4426950408889634f;
-constexpr uint32_t TM_S = 0, TM_O = 64, TM_COLS = 256;  // S^T 2x16 cols, O^T 2 x (4 x 16) cols
+// SPD_MLA_DEFER = 1: an unsplit unit's O^T read-out is deferred into the next unit: its four
+// 128-dv blocks are stored after the next unit's first four P writes (one block per tile), so
+// the softmax warps go straight on to the next unit's first tile instead of idling through the
+// epilogue.  O^T then has one double buffer per unit parity (TMEM 512 columns).  Measured
+// (profiles/r2_mla_decode_defer_ab.log, parity 36/36): +1-2 % on the lognormal cfg-5 batch,
+// +4 % at B 64 / ctx 4000, within noise at ctx 1000.
+#ifndef SPD_MLA_DEFER
+#define SPD_MLA_DEFER 1
+#endif
+constexpr uint32_t TM_S = 0, TM_O = 64;              // S^T 2 x 16 cols; O^T 2 x (4 x 16) per set
+constexpr uint32_t TM_OSET = SPD_MLA_DEFER ? 128 : 0;  // column offset of the odd units' O^T set
+constexpr uint32_t TM_COLS = SPD_MLA_DEFER ? 512 : 256;
 
 struct TUnit {
     int b, s, S, k0, k1, nt;  // b < 0: done
@@ -146,7 +157,7 @@ struct Bars {
 constexpr uint32_t OFF_Q = RING_BYTES;
 constexpr uint32_t OFF_P = OFF_Q + NQBUF * Q_BYTES;
 constexpr uint32_t OFF_RED = OFF_P + 2 * P_BYTES;            // [2][64] maxima, [64] sums
-constexpr uint32_t OFF_BARS = OFF_RED + 4 * 64 * 4;
+constexpr uint32_t OFF_BARS = OFF_RED + 5 * 64 * 4;
 constexpr uint32_t OFF_UNITS = OFF_BARS + sizeof(Bars);
 constexpr uint32_t OFF_MISC = OFF_UNITS + 2 * sizeof(TUnit);
 constexpr uint32_t SMEM_BYTES = 1024 + OFF_MISC + 16;
@@ -366,7 +377,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const uint64_t da = umma_desc_sw128(a0, PAGE * 128, 1024);
 #pragma unroll
                         for (int ks = 0; ks < PAGE / 16; ++ks)
-                            umma_ss_warp(tmem + TM_O + ob * 64 + m * NH, da + (uint64_t)(ks * 128),
+                            umma_ss_warp(tmem + TM_O + ((nunit - 1) & 1) * TM_OSET + ob * 64 + m * NH,
+                                         da + (uint64_t)(ks * 128),
                                          dp0 + (uint64_t)(ob * (P_BYTES / 16) + ks * 2), ID_PV,
                                          (npv > 1 || ks > 0) ? 1u : 0u);
                         if (m == 1) umma_commit_warp(bar.empty + s0);  // blocks 0,1 read the first box
@@ -430,6 +442,49 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int tid = threadIdx.x - 64;              // 0..127
         const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
         float* red_l = red + 128;
+        const bool odd = lane & 1;
+        const size_t ohs = p.out_head_major ? (size_t)p.B * DV : (size_t)DV;
+        const size_t whs = (size_t)p.S_max * DV;
+        // one 128-dv block of a unit's O^T read-out: combine the two buffers of set upx with the
+        // per-head factors facp (smem), then store bf16 output (unsplit) or fp32 partials (split).
+        // Lane pairs (dv, dv + 1) exchange so each lane stores bf16x2 for 8 of the 16 heads
+        // (even lane: heads 0-7, odd lane: heads 8-15)
+        auto store_block = [&](int m, int b, int s_idx, int upx, int bl, bool two, bool split,
+                               const float* facp) {
+            uint32_t o[NH], o2[NH];
+            const uint32_t ob0 = tmem + lane_base + TM_O + upx * TM_OSET;
+            tmem_ld16(ob0 + bl * 64 + m * NH, o);
+            if (two) tmem_ld16(ob0 + (bl ^ 1) * 64 + m * NH, o2);
+            tmem_wait_ld();
+            const int dv = m * 128 + qd * 32 + lane;
+            auto val = [&](int h) {
+                const float x = __uint_as_float(o[h]) * facp[h];
+                return two ? fmaf(__uint_as_float(o2[h]), facp[NH + h], x) : x;
+            };
+            if (!split) {
+                __nv_bfloat16* op = p.out + (p.out_head_major ? (size_t)b * DV : (size_t)b * p.G * DV) +
+                                    (dv & ~1) + (odd ? 8 * ohs : 0);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    // even lanes store head j, odd lanes head j + 8
+                    const float a0 = val(j), a1 = val(j + 8);
+                    const float send = odd ? a0 : a1;
+                    const float got = __shfl_xor_sync(0xffffffffu, send, 1);
+                    const int h = odd ? j + 8 : j;
+                    if (h < p.G)
+                        *reinterpret_cast<uint32_t*>(op + j * ohs) =
+                            odd ? pack_bf16(got, a1) : pack_bf16(a0, got);
+                }
+            } else {
+                float* wp = p.ws_acc + ((size_t)b * NH * p.S_max + s_idx) * DV + dv;
+#pragma unroll
+                for (int h = 0; h < NH; ++h)
+                    if (h < p.G) wp[h * whs] = val(h);
+            }
+        };
+        // the deferred read-out of the previous unsplit unit (SPD_MLA_DEFER)
+        bool pend = false, pend_ready = false, pend_two = false;
+        int pend_b = 0, pend_up = 0, pend_bl = 0, pend_chunk = 0;
         int gt = 0, nunit = 0;
         for (;;) {
             const int us = nunit & 1;
@@ -437,6 +492,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const TUnit d = units[us];
             __syncwarp();
             if (lane == 0) mbar_arrive(bar.uempty + us);
+            const int up = nunit & 1;  // this unit's O^T set
             ++nunit;
             if (d.b < 0) break;
             // O^T is double-buffered: PV(t) accumulates into buffer t & 1 with P(t) from P
@@ -523,7 +579,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 [[maybe_unused]] const long long ts3 = TL_NOW();
                 tc_fence_after();
                 if (grow && i >= 2) {
-                    const uint32_t ta = tmem + lane_base + TM_O + ob * 64;
+                    const uint32_t ta = tmem + lane_base + TM_O + up * TM_OSET + ob * 64;
                     uint32_t o[4][NH];
 #pragma unroll
                     for (int m = 0; m < DV / 128; ++m) tmem_ld16(ta + m * NH, o[m]);
@@ -556,12 +612,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar.p_full + ob);
+                if (pend) {
+                    if (!pend_ready) {
+                        // the previous unit's last PV (tile gt - 1): its barrier cannot have
+                        // moved on, the next PV of that parity needs a P not yet written; the
+                        // one before (gt - 2) was waited for above
+                        mbar_wait(bar.o_done + ((gt - 1) & 1), ((gt - 1) >> 1) & 1);
+                        tc_fence_after();
+                        pend_ready = true;
+                    }
+                    store_block(pend_chunk, pend_b, 0, pend_up, pend_bl, pend_two, false,
+                                red + 192 + pend_up * 48);
+                    if (++pend_chunk == DV / 128) pend = false;
+                    tc_fence_before();
+                }
                 if (lane == 0 && qd == 2) {
                     TL_REC(4, t, ts0, ts1, ts2);
                     TL_REC(5, t, ts3, TL_NOW(), 0);
                 }
             }
             gt += d.nt;
+            // the previous unit's blocks this (short) unit had no tiles left for
+            if (pend) {
+                while (pend_chunk < DV / 128)
+                    store_block(pend_chunk++, pend_b, 0, pend_up, pend_bl, pend_two, false,
+                                red + 192 + pend_up * 48);
+                pend = false;
+                tc_fence_before();
+            }
             // ---- unit epilogue: l totals, O^T from TMEM (combining the two buffers)
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
@@ -581,15 +659,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             [[maybe_unused]] const long long te0 = TL_NOW();
             const int bl = (gt - 1) & 1;  // buffer of the last tile (relative to mrun)
             const bool two = d.nt >= 2;   // the other buffer holds tiles <= nt-2 (mold2)
-            mbar_wait(bar.o_done + bl, ((gt - 1) >> 1) & 1);
-            if (two) mbar_wait(bar.o_done + (bl ^ 1), ((gt - 2) >> 1) & 1);
-            tc_fence_after();
-            named_bar_sync(1, NSOFT);
             const bool split = d.S > 1;
+            const bool defer = SPD_MLA_DEFER && !split;
+            if (!defer) {
+                mbar_wait(bar.o_done + bl, ((gt - 1) >> 1) & 1);
+                if (two) mbar_wait(bar.o_done + (bl ^ 1), ((gt - 2) >> 1) & 1);
+                tc_fence_after();
+            }
+            named_bar_sync(1, NSOFT);
             // per-head factors, formed once by 16 threads into smem (registers stay free for
             // the O^T tiles): fac[h] multiplies the last tile's buffer, fac[16 + h] the other
-            // one (its contents are relative to mold2); unsplit units fold in 1 / L
-            float* fac = red + 3 * 64;  // [3][16]: factor, other-buffer factor, L
+            // one (its contents are relative to mold2); unsplit units fold in 1 / L.  One slot
+            // per O^T set, so a deferred unit's factors survive the next unit's
+            float* fac = red + 192 + up * 48;  // [3][16]: factor, other-buffer factor, L
             if (tid < NH) {
                 float mr = mrun[0], mo = mold2[0];
 #pragma unroll
@@ -606,44 +688,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             named_bar_sync(1, NSOFT);
             [[maybe_unused]] const long long te1 = TL_NOW();
-            // per-unit bases: head h of this unit's output / partial row sits at base + h * hs
-            __nv_bfloat16* obase = p.out + (p.out_head_major ? (size_t)d.b * DV : (size_t)d.b * p.G * DV);
-            const size_t ohs = p.out_head_major ? (size_t)p.B * DV : (size_t)DV;
-            float* wbase = p.ws_acc + ((size_t)d.b * NH * p.S_max + d.s) * DV;
-            const size_t whs = (size_t)p.S_max * DV;
-            // lane pairs (dv, dv + 1) exchange so each lane stores bf16x2 for 8 of the 16
-            // heads (even lane: heads 0-7, odd lane: heads 8-15)
-            const bool odd = lane & 1;
-#pragma unroll
-            for (int m = 0; m < DV / 128; ++m) {
-                uint32_t o[NH], o2[NH];
-                tmem_ld16(tmem + lane_base + TM_O + bl * 64 + m * NH, o);
-                if (two) tmem_ld16(tmem + lane_base + TM_O + (bl ^ 1) * 64 + m * NH, o2);
-                tmem_wait_ld();
-                const int dv = m * 128 + qd * 32 + lane;
-                auto val = [&](int h) {
-                    const float x = __uint_as_float(o[h]) * fac[h];
-                    return two ? fmaf(__uint_as_float(o2[h]), fac[NH + h], x) : x;
-                };
-                if (!split) {
-                    __nv_bfloat16* op = obase + (dv & ~1) + (odd ? 8 * ohs : 0);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        // even lanes store head j, odd lanes head j + 8
-                        const float a0 = val(j), a1 = val(j + 8);
-                        const float send = odd ? a0 : a1;
-                        const float got = __shfl_xor_sync(0xffffffffu, send, 1);
-                        const int h = odd ? j + 8 : j;
-                        if (h < p.G)
-                            *reinterpret_cast<uint32_t*>(op + j * ohs) =
-                                odd ? pack_bf16(got, a1) : pack_bf16(a0, got);
-                    }
-                } else {
-                    float* wp = wbase + dv;
-#pragma unroll
-                    for (int h = 0; h < NH; ++h)
-                        if (h < p.G) wp[h * whs] = val(h);
-                }
+            if (defer) {
+                pend = true;
+                pend_ready = false;
+                pend_b = d.b;
+                pend_up = up;
+                pend_bl = bl;
+                pend_two = two;
+                pend_chunk = 0;
+            } else {
+#pragma unroll 1
+                for (int m = 0; m < DV / 128; ++m) store_block(m, d.b, d.s, up, bl, two, split, fac);
             }
             tc_fence_before();
             if (split) {
@@ -748,6 +803,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             named_bar_sync(1, NSOFT);
             if (lane == 0 && qd == 2) TL_REC(6, nunit, te0, te1, te2);
             if (lane == 0 && qd == 2) TL_REC(7, nunit, TL_NOW(), 0, 0);
+        }
+        if (pend) {  // the last unit's read-out: no next unit to carry it
+            if (!pend_ready) {
+                mbar_wait(bar.o_done + ((gt - 1) & 1), ((gt - 1) >> 1) & 1);
+                if (pend_two) mbar_wait(bar.o_done + ((gt - 2) & 1), ((gt - 2) >> 1) & 1);
+                tc_fence_after();
+            }
+            while (pend_chunk < DV / 128)
+                store_block(pend_chunk++, pend_b, 0, pend_up, pend_bl, pend_two, false,
+                            red + 192 + pend_up * 48);
         }
     }
     tc_fence_before();

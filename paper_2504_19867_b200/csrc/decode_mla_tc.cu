@@ -49,6 +49,13 @@ constexpr uint32_t HI_BYTES = (NCB - CB_LO) * PAGE * 128;  // 40 KiB
 #ifndef SPD_MLA_PF
 #define SPD_MLA_PF 0
 #endif
+// SPD_MLA_LOOKAHEAD = 1: while streaming a unit, the producer already resolves the next one
+// (its context, request id and first 32 block ids, in two steps so no load stalls the page
+// loop), so the next unit's first page goes out as soon as a ring slot frees.  Parity-green
+// but neutral (+-0.5 %, profiles/r2_mla_decode_lookahead_ab.log), as in round 1: default 0.
+#ifndef SPD_MLA_LOOKAHEAD
+#define SPD_MLA_LOOKAHEAD 0
+#endif
 #ifndef SPD_MLA_DQ
 #define SPD_MLA_DQ 0
 #endif
@@ -240,12 +247,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // first unit of each CTA is static (blockIdx.x); later ones come from the counter,
         // fetched one unit ahead so the atomic's round trip overlaps the current unit
         int u_next = blockIdx.x;
+        // lookahead state: the unit la_u's context / request id (step 1) and its first 32 block
+        // ids (step 2, la_ok)
+        int la_u = -1, la_ctx = 0, la_rid = 0, la_blk = -1;
+        bool la_ok = false;
         for (;;) {
             const int u = u_next;
             if (lane == 0) u_next = (int)gridDim.x + (int)atomicAdd(p.sched, 1u);
             u_next = __shfl_sync(0xffffffffu, u_next, 0);
             TUnit d;
             int ctx = 0, rid = 0;
+            const bool have_la = SPD_MLA_LOOKAHEAD && u == la_u;
             if (u >= p.n_units) {
                 d.b = -1;
             } else {
@@ -253,8 +265,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // longest requests) are handed out first
                 d.s = p.S_max - 1 - u / p.B;
                 d.b = u % p.B;
-                ctx = __ldg(p.ctx_lens + d.b);
-                rid = __ldg(p.req_ids + d.b);
+                ctx = have_la ? la_ctx : __ldg(p.ctx_lens + d.b);
+                rid = have_la ? la_rid : __ldg(p.req_ids + d.b);
                 d.S = n_splits(ctx, p.S_fill);
                 if (d.s >= d.S) continue;
                 split_range(ctx, d.S, d.s, d.k0, d.k1);
@@ -284,10 +296,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             const int page0 = d.k0 / PAGE;
             int blk_l = -1;
+            const bool use_la_blk = have_la && la_ok;
+            la_u = -1;
+            la_ok = false;
             for (int i = 0; i < d.nt; ++i, gh += 2) {
                 if ((i & 31) == 0) {
-                    const int pg = page0 + i + lane;
-                    blk_l = (pg <= last_page && pg < p.MBR) ? __ldg(btr + pg) : -1;
+                    if (i == 0 && use_la_blk) {
+                        blk_l = la_blk;
+                    } else {
+                        const int pg = page0 + i + lane;
+                        blk_l = (pg <= last_page && pg < p.MBR) ? __ldg(btr + pg) : -1;
+                    }
                 }
                 const int blk = __shfl_sync(0xffffffffu, blk_l, i & 31);
                 if (append && page0 + i == last_page && blk >= 0 && blk < p.N_B) {
@@ -328,6 +347,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (lane == 0 && ip < d.nt && (ip >> 5) == (i >> 5) && bp >= 0 && bp < p.N_B) {
                         tma_prefetch_l2_4d(&map_lo, 0, 0, 0, bp);
                         tma_prefetch_l2_4d(&map_hi, 0, 0, CB_LO, bp);
+                    }
+                }
+                // after this page's TMA issue, so no lookahead load delays it
+                if (SPD_MLA_LOOKAHEAD && i == 0 && u_next < p.n_units) {
+                    // step 1: the next unit's context and request id (consumed at step 2)
+                    la_u = u_next;
+                    const int b2 = u_next % p.B;
+                    la_ctx = __ldg(p.ctx_lens + b2);
+                    la_rid = __ldg(p.req_ids + b2);
+                }
+                if (SPD_MLA_LOOKAHEAD && i == (d.nt > 1 ? 1 : 0) && la_u >= 0) {
+                    // step 2 (a page later): its split range and first 32 block ids
+                    const int s2 = p.S_max - 1 - la_u / p.B;
+                    const int S2 = n_splits(la_ctx, p.S_fill);
+                    if (s2 < S2) {
+                        int k0b, k1b;
+                        split_range(la_ctx, S2, s2, k0b, k1b);
+                        const int pg = k0b / PAGE + lane;
+                        la_blk = (pg <= la_ctx / PAGE && pg < p.MBR) ? __ldg(p.bt + (size_t)la_rid * p.MBR + pg) : -1;
+                        la_ok = true;
                     }
                 }
                 __syncwarp();

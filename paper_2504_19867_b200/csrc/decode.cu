@@ -48,6 +48,11 @@ constexpr int HD = 128;           // head dim (dk == dv)
 #ifndef SPD_DEC_PF
 #define SPD_DEC_PF 0
 #endif
+// SPD_DEC_PAIR16 = 1: 16-token pages with an even Hkv run the head-pair wide-box kernel
+// (MODE 2): one 8 KiB TMA box per (block, head pair) and tensor
+#ifndef SPD_DEC_PAIR16
+#define SPD_DEC_PAIR16 1
+#endif
 #ifndef SPD_DEC_CPASYNC
 #define SPD_DEC_CPASYNC 0
 #endif
@@ -128,6 +133,17 @@ template <int LG_R>
 __device__ __forceinline__ uint32_t kv_off(int key, int h) {
     return ((uint32_t)(key >> LG_R) << (LG_R + 8)) + ((uint32_t)h << (LG_R + 7)) +
            ((uint32_t)(key & ((1 << LG_R) - 1)) << 7);
+}
+
+// offset of (key, 64-column half h) in a wide-box stage: MODE 0 / 1 as kv_off; MODE 2
+// (16-token pages, one 8 KiB box = both heads' 16 rows): [box][head][half][16 rows][128 B],
+// the head's own 4 KiB already added to the base
+template <int MODE, int LG_R>
+__device__ __forceinline__ uint32_t pair_off(int key, int h) {
+    if constexpr (MODE == 2)
+        return ((uint32_t)(key >> 4) << 13) + ((uint32_t)h << 11) + ((uint32_t)(key & 15) << 7);
+    else
+        return kv_off<LG_R>(key, h);
 }
 
 template <int LG_R, bool SWAP>
@@ -792,9 +808,11 @@ template <int MODE>
 __global__ void __launch_bounds__(P_NTHREADS, 1)
     decode_pair_kernel(const __grid_constant__ CUtensorMap kmap2,
                        const __grid_constant__ CUtensorMap vmap2, DecodeParams p) {
-    constexpr int LG_R = MODE == 0 ? 6 : 7;   // rows per box (and per page in the stage)
-    constexpr int KPS_M = MODE == 0 ? 64 : 128;  // keys per stage
-    constexpr int NHU = MODE == 0 ? 2 : 1;       // kv heads per unit
+    constexpr int LG_R = MODE == 0 ? 6 : MODE == 1 ? 7 : 4;  // rows per box (= per page)
+    constexpr int KPS_M = MODE == 1 ? 128 : 64;               // keys per stage
+    constexpr int NHU = MODE == 1 ? 1 : 2;                    // kv heads per unit
+    constexpr int NBX = KPS_M >> LG_R;                        // boxes per stage per tensor
+    constexpr bool PAIR = MODE != 1;                          // two heads per unit
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* ring = smem;                                                     // 3 x 64 KiB
@@ -810,7 +828,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
     const int warp = (int)warp_id();
     const int lane = (int)lane_id();
     const uint64_t kv_pol = l2_policy(kDecL2);  // KV stream: read once per step
-    const int NP = MODE == 0 ? p.Hkv >> 1 : p.Hkv;  // head groups per request
+    const int NP = PAIR ? p.Hkv >> 1 : p.Hkv;  // head groups per request
     if (threadIdx.x == 0) {
         for (int i = 0; i < P_NSTAGE; ++i) {
             mbar_init(full + i, 1);
@@ -891,7 +909,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                 const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
                 if (blk >= 0 && blk < p.N_B) {
                     const int c = lane & 15, e = lane >> 4;
-                    if (MODE == 0) {
+                    if (PAIR) {
                         const size_t slot = (((size_t)blk * p.Hkv + d.g + e) << p.lg_bs) + (ctx & bs_mask);
                         const size_t src = ((size_t)d.b * p.Hkv + d.g + e) * (HD / 8);
                         reinterpret_cast<uint4*>(p.k_pool)[slot * (HD / 8) + c] = __ldg(p.k_new + src + c);
@@ -907,26 +925,34 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                 }
                 __syncwarp();
             }
-            auto lookup = [&](int i) -> int {  // raw block id of stage i (-2: past the request)
-                const int page = (d.k0 + i * KPS_M) >> p.lg_bs;
-                if (i >= d.nst || page > last_page) return -2;
+            // raw block id of box bi (NBX boxes per stage; -2: past the request)
+            const int nbox = d.nst * NBX;
+            auto lookup = [&](int bi) -> int {
+                const int page = (d.k0 + bi * (KPS_M / NBX)) >> p.lg_bs;
+                if (bi >= nbox || page > last_page) return -2;
                 return page < p.MBR ? __ldg(btr + page) : -1;
             };
             int zc = lookup(lane);
             for (int i = 0; i < d.nst; ++i, ++gstage) {
-                if (i > 0 && (i & 31) == 0) zc = lookup(i + lane);
-                const int blk = __shfl_sync(0xffffffffu, zc, i & 31);
                 const int st = gstage % P_NSTAGE;
                 if (lane == 0) {
-                    unsigned char* kst = ring + st * P_STAGE;
                     mbar_wait(empty + st, ((gstage / P_NSTAGE) & 1) ^ 1);
                     mbar_arrive_expect_tx(full + st, P_STAGE);
-                    int z = oob_z;
-                    if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
-                    else if (blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
-                    const int y = (d.k0 + i * KPS_M) & bs_mask;
-                    tma_load_4d_hint(kst, &kmap2, full + st, 0, y, 0, z, kv_pol);
-                    tma_load_4d_hint(kst + 2 * KV_BYTES, &vmap2, full + st, 0, y, 0, z, kv_pol);
+                }
+#pragma unroll
+                for (int b = 0; b < NBX; ++b) {
+                    const int bi = i * NBX + b;
+                    if (bi > 0 && (bi & 31) == 0) zc = lookup(bi + lane);
+                    const int blk = __shfl_sync(0xffffffffu, zc, bi & 31);
+                    if (lane == 0) {
+                        unsigned char* kst = ring + st * P_STAGE + b * (KV_BYTES * 2 / NBX);
+                        int z = oob_z;
+                        if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
+                        else if (blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                        const int y = (d.k0 + bi * (KPS_M / NBX)) & bs_mask;
+                        tma_load_4d_hint(kst, &kmap2, full + st, 0, y, 0, z, kv_pol);
+                        tma_load_4d_hint(kst + 2 * KV_BYTES, &vmap2, full + st, 0, y, 0, z, kv_pol);
+                    }
                 }
                 __syncwarp();
             }
@@ -946,7 +972,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             if (lane == 0) mbar_arrive(uempty + us);
             ++nunit;
             if (d.b < 0) break;
-            const int g = d.g + (MODE == 0 ? e : 0);
+            const int g = d.g + (PAIR ? e : 0);
             uint32_t qa[8][4];
             {
                 const uint32_t* q32 = reinterpret_cast<const uint32_t*>(p.q);
@@ -979,9 +1005,11 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                 mbar_wait(full + st, (gs / P_NSTAGE) & 1);
                 // MODE 0: [K g0 | K g0+1 | V g0 | V g0+1], 64-row pages; MODE 1: [K | V], one
                 // 128-row page each ([half][128 rows][128 B]); this warp's keys start at koff
-                const uint32_t kst = smem_u32(ring + st * P_STAGE) + (MODE == 0 ? e * KV_BYTES : 0);
+                // MODE 2: [box b][head e][half][16 rows][128 B] (8 KiB per box), K then V
+                const uint32_t kst = smem_u32(ring + st * P_STAGE) +
+                                     (MODE == 0 ? e * KV_BYTES : MODE == 2 ? e * 4096 : 0);
                 const uint32_t vst = kst + 2 * KV_BYTES;
-                const int koff = MODE == 0 ? 0 : 64 * e;
+                const int koff = MODE == 1 ? 64 * e : 0;
                 float s[8][4];
 #pragma unroll
                 for (int nt = 0; nt < 8; ++nt) {
@@ -990,7 +1018,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
 #pragma unroll
                     for (int kk = 0; kk < 8; kk += 2) {
                         const int ci = 2 * kk + (lane >> 3);
-                        const uint32_t addr = kst + kv_off<LG_R>(key, ci >> 3) + (((ci & 7) ^ (key & 7)) << 4);
+                        const uint32_t addr = kst + pair_off<MODE, LG_R>(key, ci >> 3) + (((ci & 7) ^ (key & 7)) << 4);
                         uint32_t b0, b1, b2, b3;
                         ldsm_x4(addr, b0, b1, b2, b3);
                         mma_bf16_16816(s[nt], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
@@ -1045,7 +1073,7 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
 #pragma unroll
                     for (int nd = 0; nd < 16; nd += 2) {
                         const int ch = nd + (lane >> 4);
-                        const uint32_t addr = vst + kv_off<LG_R>(key, ch >> 3) + (((ch & 7) ^ (key & 7)) << 4);
+                        const uint32_t addr = vst + pair_off<MODE, LG_R>(key, ch >> 3) + (((ch & 7) ^ (key & 7)) << 4);
                         uint32_t b0, b1, b2, b3;
                         ldsm_x4_t(addr, b0, b1, b2, b3);
                         float t0[4] = {acc[nd][0], acc[nd][1], 0.f, 0.f};
@@ -1085,12 +1113,12 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
                 float M = -INFINITY;
 #pragma unroll
                 for (int w = 0; w < WPH; ++w)
-                    M = fmaxf(M, scr_ml[(((MODE == 0 ? w * 2 + ee : w)) * P_GMAX + h) * 2]);
+                    M = fmaxf(M, scr_ml[(((PAIR ? w * 2 + ee : w)) * P_GMAX + h) * 2]);
                 float L = 0.f;
                 float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int w = 0; w < WPH; ++w) {
-                    const int wj = MODE == 0 ? w * 2 + ee : w;
+                    const int wj = PAIR ? w * 2 + ee : w;
                     const float mw = scr_ml[(wj * P_GMAX + h) * 2];
                     const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
                     L += f * scr_ml[(wj * P_GMAX + h) * 2 + 1];
@@ -1309,17 +1337,23 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     // budget (R26).
     const bool mode1 = pool->have_wide_maps && c.block_size == 128 && prm.G <= P_GMAX;
     const bool mode0 = pool->have_wide_maps && c.block_size == 64 && prm.G <= P_GMAX &&
-                       c.num_kv_heads % 2 == 0 && batch * (c.num_kv_heads / 2) >= 2 * 148;
-    if ((mode0 || mode1) && !pool->force_single) {
-        prm.n_units = batch * (mode0 ? c.num_kv_heads / 2 : c.num_kv_heads) * S_max;
+                       c.num_kv_heads % 2 == 0 &&
+                       (batch * (c.num_kv_heads / 2) >= 2 * 148 || pool->force_pair);
+    // 16-token pages, even Hkv (SPD_DEC_PAIR16): one 8 KiB box carries both heads of a
+    // (block, head-pair), half the TMA operations of the one-head kernel's 4 KiB boxes
+    const bool mode2 = SPD_DEC_PAIR16 && pool->have_wide_maps && c.block_size == 16 &&
+                       prm.G <= P_GMAX && c.num_kv_heads % 2 == 0;
+    if ((mode0 || mode1 || mode2) && !pool->force_single) {
+        prm.n_units = batch * (mode1 ? c.num_kv_heads : c.num_kv_heads / 2) * S_max;
         const size_t smem = decode_pair_smem_bytes();
-        static bool attr_pair[2] = {false, false};
-        auto kern = mode0 ? decode_pair_kernel<0> : decode_pair_kernel<1>;
-        if (!attr_pair[mode1]) {
+        static bool attr_pair[3] = {false, false, false};
+        const int mi = mode0 ? 0 : mode1 ? 1 : 2;
+        auto kern = mode0 ? decode_pair_kernel<0> : mode1 ? decode_pair_kernel<1> : decode_pair_kernel<2>;
+        if (!attr_pair[mi]) {
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
                 cudaSuccess)
                 return SEMIPD_ERR_CUDA;
-            attr_pair[mode1] = true;
+            attr_pair[mi] = true;
         }
         int grid = budget > 0 ? budget : prm.n_units;
         if (grid > prm.n_units) grid = prm.n_units;

@@ -48,6 +48,7 @@ struct semipd_pool {
     std::vector<CUtensorMap> dkmap2, dvmap2;
     bool have_wide_maps = false;
     bool force_single = false;  // debug/bench: keep the one-head decode kernel
+    bool force_pair = false;    // debug/bench: head-pair boxes at 64-token pages for any batch
     // decode epilogue peer stores (semipd_set_decode_peers; TP gather fused into the kernel)
     void* dec_peers[SEMIPD_MAX_PEERS - 1] = {};
     int dec_n_peers = 0;

@@ -237,7 +237,8 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
         p->have_dmaps = dok;
         const bool wide64 = cfg->block_size == 64 && cfg->num_kv_heads % 2 == 0;
         const bool wide128 = cfg->block_size == 128;
-        if (dok && (wide64 || wide128) && cfg->head_dim_k == 128 && cfg->head_dim_v == 128 &&
+        const bool wide16 = cfg->block_size == 16 && cfg->num_kv_heads % 2 == 0;
+        if (dok && (wide64 || wide128 || wide16) && cfg->head_dim_k == 128 && cfg->head_dim_v == 128 &&
             !cfg->kv_shared) {
             p->dkmap2.resize(cfg->num_layers);
             p->dvmap2.resize(cfg->num_layers);
@@ -246,7 +247,10 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
                 const uint64_t r = 256;
                 const uint64_t dd[4] = {64, (uint64_t)cfg->block_size, 2, pages};
                 const uint64_t ds[3] = {r, 128, r * cfg->block_size};
-                const uint32_t db[4] = {64, wide64 ? 64u : 128u, 2, wide64 ? 2u : 1u};
+                // (64 cols, rows, 2 halves, pages): 64-token pages -> 64 rows x 2 adjacent
+                // head pages; 128 -> one whole page; 16 -> 16 rows x 2 adjacent head pages
+                const uint32_t db[4] = {64, wide64 ? 64u : wide16 ? 16u : 128u, 2,
+                                        (wide64 || wide16) ? 2u : 1u};
                 pok = spd_encode_tiled_4d(&p->dkmap2[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                                           p->k_layer(l), dd, ds, db, CU_TENSOR_MAP_SWIZZLE_128B) &&
                       spd_encode_tiled_4d(&p->dvmap2[l], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
@@ -254,6 +258,7 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
             }
             p->have_wide_maps = pok;
             p->force_single = getenv("SEMIPD_DECODE_SINGLE") != nullptr;  // A/B debugging only
+            p->force_pair = getenv("SEMIPD_DECODE_PAIR64") != nullptr;    // A/B debugging only
         }
         if (cfg->kv_shared && cfg->block_size % 32 == 0 && pow2) {
             p->mla_kmap.resize(cfg->num_layers);

@@ -210,7 +210,9 @@ int64_t semipd_launch_count(semipd_pool_t pool);
 /* Optional CTA trace for co-run evidence: when buf (device int32, capacity
  * `cap` records of 4 words) is non-NULL every attention CTA appends
  * {phase (1 prefill, 2 decode), %smid, blockIdx.x, kernel kind (0 CUDA-core generic,
- * 1 tcgen05 prefill, 2 split-K decode)}; *counter_dev (device int32)
+ * 1 tcgen05 prefill, 2 split-K decode, 3 MLA mma.sync decode, 4 MLA tcgen05 decode,
+ * 5 MLA tcgen05 prefill, 6 / 7 / 8 wide-box split-K decode: head pairs at 64-token pages /
+ * whole 128-token pages / head pairs at 16-token pages)}; *counter_dev (device int32)
  * is the append cursor.  Pass buf = NULL to disable. */
 semipd_status semipd_set_trace(semipd_pool_t pool, int32_t* buf, int32_t cap,
                                int32_t* counter_dev);

@@ -571,7 +571,7 @@ def test_prefill_then_decode_handoff():
 
 
 # ----------------------------------------------------------------------------- co-run
-@pytest.mark.parametrize("bs,dec_kind", [(16, 2), (64, 2), (128, 7)])
+@pytest.mark.parametrize("bs,dec_kind", [(16, 8), (64, 2), (128, 7)])
 def test_corun_bitwise_identical_and_disjoint_sms(bs, dec_kind):
     """Prefill (stream P) and decode (stream D) co-run on one pool with budgets
     (74, 74): outputs are bitwise identical to isolated runs and the two grids

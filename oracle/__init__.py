@@ -70,6 +70,18 @@ def lib():
             L.semipd_ref_rope_inv_freq.restype = None
             L.semipd_ref_rope.argtypes = [i, i, i, i, i, i, vp, i, vp, d, d, d, d, d, dp]
             L.semipd_ref_rope.restype = None
+            f = ctypes.c_float
+            L.semipd_ref_e4m3_value.argtypes = [i]
+            L.semipd_ref_e4m3_value.restype = d
+            L.semipd_ref_e4m3_encode.argtypes = [f]
+            L.semipd_ref_e4m3_quantize.argtypes = [i, vp, f, vp]
+            L.semipd_ref_e4m3_quantize.restype = None
+            L.semipd_ref_e4m3_values.argtypes = [i, vp, dp]
+            L.semipd_ref_e4m3_values.restype = None
+            L.semipd_ref_decode_fp8.argtypes = [i, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, i,
+                                                vp, i, f, f, d, dp]
+            L.semipd_ref_prefill_fp8.argtypes = [i, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp,
+                                                 i, vp, i, f, f, d, dp, vp]
             _ = ip
             _lib = L
     return _lib
@@ -268,4 +280,84 @@ def rope(x, positions, theta: float, factor: float = 0.0, lf: float = 1.0, hf: f
     rd = d - off if rd is None else rd
     lib().semipd_ref_rope(T, H, d, off, rd, int(bool(interleaved)), _p(x), _dtype_code(x), _p(pos),
                           theta, factor, lf, hf, L0, _p(out))
+    return out
+
+
+# ---- FP8 (E4M3) KV pages (semipd_oracle.c, reading R31) ----
+
+def e4m3_value(code: int) -> float:
+    """Exact value of one E4M3 code (NaN codes -> nan)."""
+    return lib().semipd_ref_e4m3_value(int(code))
+
+
+def e4m3_encode(x: float) -> int:
+    """Round-to-nearest-even, satfinite E4M3 code of one fp32 value."""
+    return lib().semipd_ref_e4m3_encode(float(x))
+
+
+def e4m3_quantize(x_bf16: np.ndarray, scale: float) -> np.ndarray:
+    """Codes (uint8) of bf16 elements (uint16 bits) under the write rule E4M3(fl32(x / s))."""
+    x = _c(x_bf16)
+    assert x.dtype == np.uint16
+    out = np.zeros(x.shape, np.uint8)
+    lib().semipd_ref_e4m3_quantize(x.size, _p(x), float(scale), _p(out))
+    return out
+
+
+def e4m3_values(codes: np.ndarray) -> np.ndarray:
+    """fp64 values of E4M3 codes (uint8)."""
+    c = _c(codes, np.uint8)
+    out = np.zeros(c.shape, np.float64)
+    lib().semipd_ref_e4m3_values(c.size, _p(c), _p(out))
+    return out
+
+
+def decode_fp8(q, k_new, v_new, k_pool, v_pool, block_tables, req_ids, ctx_lens, scale: float,
+               k_scale: float, v_scale: float):
+    """One decode step on an E4M3 pool (uint8 codes [N_B, Hkv, bs, d]); pools MODIFIED in
+    place (quantised append at slot ctx).  q / k_new / v_new are bf16 bits (uint16).
+    Returns fp64 out [B, Hq, dv]."""
+    q, k_new, v_new = _c(q), _c(k_new), _c(v_new)
+    assert q.dtype == k_new.dtype == v_new.dtype == np.uint16
+    assert k_pool.dtype == v_pool.dtype == np.uint8
+    assert k_pool.flags.c_contiguous and v_pool.flags.c_contiguous
+    B, Hq, dk = q.shape
+    N_B, Hkv, bs, _ = k_pool.shape
+    dv = v_new.shape[2]
+    bt = _c(block_tables, np.int32)
+    rid = _c(req_ids, np.int32)
+    cl = _c(ctx_lens, np.int32)
+    out = np.zeros((B, Hq, dv), np.float64)
+    st = lib().semipd_ref_decode_fp8(B, _p(rid), _p(cl), Hq, Hkv, dk, dv, bs, _p(q), _p(k_new),
+                                     _p(v_new), _p(k_pool), _p(v_pool), N_B, _p(bt), bt.shape[1],
+                                     float(k_scale), float(v_scale), float(scale), _p(out))
+    if st != OK:
+        raise ValueError(f"oracle decode_fp8 status {st}")
+    return out
+
+
+def prefill_fp8(q, k_new, v_new, k_pool, v_pool, block_tables, cu_seqlens, req_ids, prefix_lens,
+                scale: float, k_scale: float, v_scale: float, rows_mask=None):
+    """Chunked causal GQA prefill on an E4M3 pool; pools MODIFIED in place (quantised chunk
+    write).  Prefix keys are read back from the pool, the chunk's own keys are its bf16 rows.
+    Returns fp64 out [T, Hq, dv] (rows outside rows_mask are zero)."""
+    q, k_new, v_new = _c(q), _c(k_new), _c(v_new)
+    assert q.dtype == k_new.dtype == v_new.dtype == np.uint16
+    assert k_pool.dtype == v_pool.dtype == np.uint8
+    assert k_pool.flags.c_contiguous and v_pool.flags.c_contiguous
+    T, Hq, dk = q.shape
+    N_B, Hkv, bs, _ = k_pool.shape
+    dv = v_new.shape[2]
+    bt = _c(block_tables, np.int32)
+    cu = _c(cu_seqlens, np.int32)
+    rid = _c(req_ids, np.int32)
+    pl = _c(prefix_lens, np.int32)
+    out = np.zeros((T, Hq, dv), np.float64)
+    mask = None if rows_mask is None else _c(rows_mask, np.uint8)
+    st = lib().semipd_ref_prefill_fp8(len(rid), _p(cu), _p(rid), _p(pl), Hq, Hkv, dk, dv, bs,
+                                      _p(q), _p(k_new), _p(v_new), _p(k_pool), _p(v_pool), N_B,
+                                      _p(bt), bt.shape[1], float(k_scale), float(v_scale),
+                                      float(scale), _p(out), None if mask is None else _p(mask))
+    if st != OK:
+        raise ValueError(f"oracle prefill_fp8 status {st}")
     return out

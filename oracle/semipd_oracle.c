@@ -497,3 +497,235 @@ void semipd_ref_rope(int T, int H, int d, int off, int rd, int inter, const void
         }
     free(f);
 }
+
+/* ---- FP8 (E4M3) KV pages (§7.1 "deployed ... with FP8 precision") ----
+ * The paper names FP8 for DeepSeek-V3 and nothing more; reading R31 fixes the form:
+ *   - a page element is one OCP FP8 E4M3 code (the "fn" variant GPUs implement): sign bit,
+ *     4 exponent bits with bias 7, 3 mantissa bits; exponent 15 with mantissa 7 is NaN; no
+ *     infinities; largest finite 448 = 1.75 * 2^8; subnormals m * 2^-9, m = 1..7.
+ *   - write:  code = E4M3( fl32(x / s) ), x the bf16 input element, s > 0 the layer's fp32
+ *     tensor scale (k_scale for K, v_scale for V), fl32 one IEEE single-precision division,
+ *     E4M3 round-to-nearest-even onto the finite codes with saturation to +-448 ("satfinite").
+ *   - read:   value = s * e4m3_value(code)  (exact in fp64).
+ *   - attention reads every cached key / value through "read"; a prefill chunk's own keys and
+ *     values (the rows it writes this step) enter at input precision (bf16), as the step's
+ *     K / V projections are in hand before they are cached.  Decode attends the
+ *     appended row as stored (it is read back from the pool, "the KV cache ... is
+ *     updated" before attention).
+ * ------------------------------------------------------------------------------------------ */
+
+/* value of an E4M3 code, straight from the bit fields (NaN codes -> NaN) */
+double semipd_ref_e4m3_value(int code) {
+    int s = (code >> 7) & 1, e = (code >> 3) & 15, m = code & 7;
+    double v;
+    if (e == 15 && m == 7) return NAN;
+    if (e == 0) v = (double)m * ldexp(1.0, -9);            /* subnormal: (m/8) * 2^(1-7) */
+    else v = (1.0 + (double)m / 8.0) * ldexp(1.0, e - 7);  /* normal */
+    return s ? -v : v;
+}
+
+/* round-to-nearest-even onto the 127 finite non-negative codes by exhaustive search (ties go
+ * to the even code, i.e. the even mantissa); |x| beyond 448 lands on 448 (satfinite) */
+int semipd_ref_e4m3_encode(float x) {
+    if (isnan(x)) return 0x7F;
+    int sign = signbit(x) ? 0x80 : 0;
+    double a = fabs((double)x);
+    int best = 0;
+    double bd = INFINITY;
+    for (int c = 0; c <= 0x7E; ++c) {
+        double d = fabs(semipd_ref_e4m3_value(c) - a);
+        if (d < bd || (d == bd && (c & 1) == 0)) {
+            bd = d;
+            best = c;
+        }
+    }
+    return sign | best;
+}
+
+/* the write rule: bf16 element (bits) divided by s in fp32, then encoded */
+static unsigned char quant_e4m3(uint16_t bf16_bits, float s) {
+    uint32_t u = ((uint32_t)bf16_bits) << 16;
+    float x;
+    memcpy(&x, &u, 4);
+    volatile float q = x / s; /* one IEEE fp32 division, not contracted or widened */
+    return (unsigned char)semipd_ref_e4m3_encode(q);
+}
+
+/* bulk helpers for the tests: codes of n bf16 elements at scale s / values of n codes */
+void semipd_ref_e4m3_quantize(int n, const uint16_t* x, float s, unsigned char* codes) {
+    for (int i = 0; i < n; ++i) codes[i] = quant_e4m3(x[i], s);
+}
+void semipd_ref_e4m3_values(int n, const unsigned char* codes, double* out) {
+    for (int i = 0; i < n; ++i) out[i] = semipd_ref_e4m3_value(codes[i]);
+}
+
+/* The attention definition over materialised fp64 rows (same formula as attend_row). */
+static void attend_f64(const double* q, const double* k, const double* v, int n, int dk, int dv,
+                       double scale, double* z, double* o) {
+    double M = -INFINITY;
+    for (int j = 0; j < n; ++j) {
+        double dot = 0.0;
+        for (int c = 0; c < dk; ++c) dot += q[c] * k[(size_t)j * dk + c];
+        z[j] = scale * dot;
+        if (z[j] > M) M = z[j];
+    }
+    double denom = 0.0;
+    for (int c = 0; c < dv; ++c) o[c] = 0.0;
+    for (int j = 0; j < n; ++j) {
+        double w = exp(z[j] - M);
+        denom += w;
+        for (int c = 0; c < dv; ++c) o[c] += w * v[(size_t)j * dv + c];
+    }
+    for (int c = 0; c < dv; ++c) o[c] /= denom;
+}
+
+/* Decode step on an E4M3 pool (bf16 q / k_new / v_new; pools of codes [N_B][Hkv][bs][d]).
+ * Step 1: quantise k_new / v_new into slot ctx.  Step 2: attention over keys 0 .. ctx, every
+ * key and value read back from the pool (value = scale * e4m3_value(code)). */
+int semipd_ref_decode_fp8(int B, const int* req_ids, const int* ctx_lens, int Hq, int Hkv, int dk,
+                          int dv, int bs, const uint16_t* q, const uint16_t* k_new,
+                          const uint16_t* v_new, unsigned char* Kpool, unsigned char* Vpool,
+                          int N_B, const int* block_tables, int MBR, float k_scale, float v_scale,
+                          double scale, double* out) {
+    if (B < 0 || Hq <= 0 || Hkv <= 0 || Hq % Hkv || bs <= 0 || !(k_scale > 0) || !(v_scale > 0))
+        return ORC_INVALID;
+    int G = Hq / Hkv;
+    int maxkeys = 1;
+    for (int b = 0; b < B; ++b) {
+        const int* bt = block_tables + (size_t)req_ids[b] * MBR;
+        int pos = ctx_lens[b];
+        if (pos < 0 || pos / bs >= MBR) return ORC_BAD_BLOCK;
+        for (int p = 0; p <= pos / bs; ++p)
+            if (bt[p] < 0 || bt[p] >= N_B) return ORC_BAD_BLOCK;
+        int blk = bt[pos / bs];
+        for (int g = 0; g < Hkv; ++g) {
+            for (int c = 0; c < dk; ++c)
+                Kpool[k_elem(blk, g, pos % bs, Hkv, bs, dk) + c] =
+                    quant_e4m3(k_new[((size_t)b * Hkv + g) * dk + c], k_scale);
+            for (int c = 0; c < dv; ++c)
+                Vpool[k_elem(blk, g, pos % bs, Hkv, bs, dv) + c] =
+                    quant_e4m3(v_new[((size_t)b * Hkv + g) * dv + c], v_scale);
+        }
+        if (pos + 1 > maxkeys) maxkeys = pos + 1;
+    }
+#pragma omp parallel
+    {
+        double* qd = (double*)malloc(sizeof(double) * (size_t)dk);
+        double* kd = (double*)malloc(sizeof(double) * (size_t)maxkeys * dk);
+        double* vd = (double*)malloc(sizeof(double) * (size_t)maxkeys * dv);
+        double* z = (double*)malloc(sizeof(double) * (size_t)maxkeys);
+#pragma omp for schedule(dynamic, 1) collapse(2)
+        for (int b = 0; b < B; ++b)
+            for (int h = 0; h < Hq; ++h) {
+                int g = h / G;
+                const int* bt = block_tables + (size_t)req_ids[b] * MBR;
+                int n = ctx_lens[b] + 1;
+                for (int c = 0; c < dk; ++c) qd[c] = ld(q, ((size_t)b * Hq + h) * dk + c, ORC_BF16);
+                for (int j = 0; j < n; ++j) {
+                    int blk = bt[j / bs];
+                    for (int c = 0; c < dk; ++c)
+                        kd[(size_t)j * dk + c] =
+                            (double)k_scale * semipd_ref_e4m3_value(Kpool[k_elem(blk, g, j % bs, Hkv, bs, dk) + c]);
+                    for (int c = 0; c < dv; ++c)
+                        vd[(size_t)j * dv + c] =
+                            (double)v_scale * semipd_ref_e4m3_value(Vpool[k_elem(blk, g, j % bs, Hkv, bs, dv) + c]);
+                }
+                attend_f64(qd, kd, vd, n, dk, dv, scale, z, out + ((size_t)b * Hq + h) * dv);
+            }
+        free(qd);
+        free(kd);
+        free(vd);
+        free(z);
+    }
+    return ORC_OK;
+}
+
+/* Chunked causal GQA prefill on an E4M3 pool.  Step 1: quantise the chunk rows into slots
+ * P_i + t.  Step 2: row t of request i attends keys j in [0, P_i + t]: j < P_i read back from
+ * the pool (cached by earlier chunks), j >= P_i the chunk's own bf16 rows k_new / v_new
+ * [cu_i + j - P_i].  rows_mask as in semipd_ref_prefill. */
+int semipd_ref_prefill_fp8(int n_req, const int* cu_seqlens, const int* req_ids,
+                           const int* prefix_lens, int Hq, int Hkv, int dk, int dv, int bs,
+                           const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
+                           unsigned char* Kpool, unsigned char* Vpool, int N_B,
+                           const int* block_tables, int MBR, float k_scale, float v_scale,
+                           double scale, double* out, const unsigned char* rows_mask) {
+    if (n_req < 0 || Hq <= 0 || Hkv <= 0 || Hq % Hkv || bs <= 0 || !(k_scale > 0) ||
+        !(v_scale > 0))
+        return ORC_INVALID;
+    int G = Hq / Hkv;
+    for (int i = 0; i < n_req; ++i) {
+        const int* bt = block_tables + (size_t)req_ids[i] * MBR;
+        int nk = prefix_lens[i] + cu_seqlens[i + 1] - cu_seqlens[i];
+        for (int p = 0; p * bs < nk; ++p)
+            if (p >= MBR || bt[p] < 0 || bt[p] >= N_B) return ORC_BAD_BLOCK;
+    }
+    /* step 1: quantised K/V write */
+    for (int i = 0; i < n_req; ++i) {
+        const int* bt = block_tables + (size_t)req_ids[i] * MBR;
+        for (int t = cu_seqlens[i]; t < cu_seqlens[i + 1]; ++t) {
+            int pos = prefix_lens[i] + (t - cu_seqlens[i]);
+            int blk = bt[pos / bs];
+            for (int g = 0; g < Hkv; ++g) {
+                for (int c = 0; c < dk; ++c)
+                    Kpool[k_elem(blk, g, pos % bs, Hkv, bs, dk) + c] =
+                        quant_e4m3(k_new[((size_t)t * Hkv + g) * dk + c], k_scale);
+                for (int c = 0; c < dv; ++c)
+                    Vpool[k_elem(blk, g, pos % bs, Hkv, bs, dv) + c] =
+                        quant_e4m3(v_new[((size_t)t * Hkv + g) * dv + c], v_scale);
+            }
+        }
+    }
+    /* step 2 */
+    int T = n_req > 0 ? cu_seqlens[n_req] : 0;
+    int maxkeys = 1;
+    for (int i = 0; i < n_req; ++i) {
+        int nk = prefix_lens[i] + cu_seqlens[i + 1] - cu_seqlens[i];
+        if (nk > maxkeys) maxkeys = nk;
+    }
+    int* row_req = (int*)malloc(sizeof(int) * (size_t)(T > 0 ? T : 1));
+    for (int i = 0; i < n_req; ++i)
+        for (int t = cu_seqlens[i]; t < cu_seqlens[i + 1]; ++t) row_req[t] = i;
+#pragma omp parallel
+    {
+        double* qd = (double*)malloc(sizeof(double) * (size_t)dk);
+        double* kd = (double*)malloc(sizeof(double) * (size_t)maxkeys * dk);
+        double* vd = (double*)malloc(sizeof(double) * (size_t)maxkeys * dv);
+        double* z = (double*)malloc(sizeof(double) * (size_t)maxkeys);
+#pragma omp for schedule(dynamic, 1) collapse(2)
+        for (int t = 0; t < T; ++t)
+            for (int h = 0; h < Hq; ++h) {
+                if (rows_mask && !rows_mask[t]) continue;
+                int i = row_req[t];
+                int g = h / G;
+                const int* bt = block_tables + (size_t)req_ids[i] * MBR;
+                int P = prefix_lens[i];
+                int n = P + (t - cu_seqlens[i]) + 1;
+                for (int c = 0; c < dk; ++c) qd[c] = ld(q, ((size_t)t * Hq + h) * dk + c, ORC_BF16);
+                for (int j = 0; j < n; ++j) {
+                    if (j < P) {
+                        int blk = bt[j / bs];
+                        for (int c = 0; c < dk; ++c)
+                            kd[(size_t)j * dk + c] = (double)k_scale *
+                                semipd_ref_e4m3_value(Kpool[k_elem(blk, g, j % bs, Hkv, bs, dk) + c]);
+                        for (int c = 0; c < dv; ++c)
+                            vd[(size_t)j * dv + c] = (double)v_scale *
+                                semipd_ref_e4m3_value(Vpool[k_elem(blk, g, j % bs, Hkv, bs, dv) + c]);
+                    } else {
+                        size_t r = (size_t)cu_seqlens[i] + (size_t)(j - P);
+                        for (int c = 0; c < dk; ++c)
+                            kd[(size_t)j * dk + c] = ld(k_new, (r * Hkv + g) * dk + c, ORC_BF16);
+                        for (int c = 0; c < dv; ++c)
+                            vd[(size_t)j * dv + c] = ld(v_new, (r * Hkv + g) * dv + c, ORC_BF16);
+                    }
+                }
+                attend_f64(qd, kd, vd, n, dk, dv, scale, z, out + ((size_t)t * Hq + h) * dv);
+            }
+        free(qd);
+        free(kd);
+        free(vd);
+        free(z);
+    }
+    free(row_req);
+    return ORC_OK;
+}

@@ -243,12 +243,13 @@ def cpu_model() -> str:
 
 
 # ----------------------------------------------------------------------------- algorithmic work
-def decode_bytes(shape: synth.AttnShape, ctx_lens) -> float:
+def decode_bytes(shape: synth.AttnShape, ctx_lens, kv_bytes: int = 2) -> float:
     """Algorithmic HBM bytes of one decode launch: every visible
-    key's K and V once (V aliases K for the MLA latent: the 576-d row once), q in, o out."""
+    key's K and V once (V aliases K for the MLA latent: the 576-d row once), q in, o out.
+    kv_bytes = 1 for an FP8 (E4M3) pool (reading R31); q / o stay bf16."""
     eb = 2
     row = shape.head_dim_k if shape.kv_shared else shape.head_dim_k + shape.head_dim_v
-    kv = sum(c + 1 for c in ctx_lens) * shape.num_kv_heads * row * eb
+    kv = sum(c + 1 for c in ctx_lens) * shape.num_kv_heads * row * kv_bytes
     io = len(ctx_lens) * shape.num_q_heads * (shape.head_dim_k + shape.head_dim_v) * eb
     return float(kv + io)
 
@@ -277,7 +278,7 @@ class Workload:
                  gather: str = "nccl", B: int = DECODE_BATCH, ctx=DECODE_CTX,
                  C: int = PREFILL_TOKENS, P: int = 0, layers: int | None = None,
                  tp_mode: str = "dependent", nccl_max_ctas: int = 4, groups=None,
-                 max_prefix: int | None = None):
+                 max_prefix: int | None = None, kv_fp8: bool = False):
         from paper_2504_19867_b200 import KVPool, PoolConfig
         self.full = shape
         self.shape = synth.shard_heads(shape, tp) if tp > 1 else shape
@@ -295,9 +296,14 @@ class Workload:
         self.cfg = PoolConfig(num_layers=self.L, num_blocks=n_blocks, block_size=bs,
                               num_kv_heads=s.num_kv_heads, head_dim_k=s.head_dim_k,
                               head_dim_v=s.head_dim_v, max_reqs=B + 2,
-                              max_blocks_per_req=max(max(nb_dec), nb_pre_max) + 8, dtype=s.dtype,
+                              max_blocks_per_req=max(max(nb_dec), nb_pre_max) + 8,
+                              dtype=torch.float8_e4m3fn if kv_fp8 else s.dtype,
                               kv_shared=s.kv_shared)
         self.pool = KVPool(self.cfg, dev)
+        self.kv_fp8 = kv_fp8
+        if kv_fp8:  # E4M3 pages (reading R31): per-tensor scales, prefix staging scratch
+            self.pool.set_kv_scales(0.05, 0.02)
+            self.pool.attach_fp8_prefill_scratch(1)
         i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
         self.i32 = i32
         self.rid_dec = i32(list(range(B)))
@@ -312,9 +318,14 @@ class Workload:
         # per-step decode working set is far larger than L2)
         for l in range(self.L):
             K, V, _, _ = self.pool.views(l)
-            K.normal_(generator=g)
-            if V is not None:
-                V.normal_(generator=g)
+            if kv_fp8:  # random finite E4M3 codes (|value| < 2^7 before the scale)
+                for T in (K, V):
+                    T.copy_(torch.randint(0, 0x70, T.shape, generator=g, device=dev, dtype=torch.int32)
+                            .to(torch.uint8))
+            else:
+                K.normal_(generator=g)
+                if V is not None:
+                    V.normal_(generator=g)
         Hq, Hkv, dk, dv = s.num_q_heads, s.num_kv_heads, s.head_dim_k, s.head_dim_v
         mk = lambda *shp: torch.randn(*shp, generator=g, device=dev, dtype=torch.float32).to(s.dtype)  # noqa: E731
         self.qp = [mk(C, Hq, dk) for _ in range(self.L)]
@@ -377,7 +388,7 @@ class Workload:
 
     # ---- algorithmic work of one launch
     def decode_bytes_per_launch(self) -> float:
-        return decode_bytes(self.shape, self.ctx_list)
+        return decode_bytes(self.shape, self.ctx_list, 1 if self.kv_fp8 else 2)
 
     def prefill_flops_per_launch(self) -> float:
         return prefill_flops(self.shape, self.C, self.P)
@@ -1005,6 +1016,15 @@ def secondary_cfg4(args, dev, pk, layers: int = 8):
     return out
 
 
+def secondary_fp8(args, dev, pk):
+    """The headline workload over an FP8 (E4M3) pool (reading R31): decode
+    reads 1-byte codes (half the bytes: the decode fraction is against the FP8 byte count),
+    prefill attends its chunk at bf16 with P = 0 (the quantised K/V write is a separate pass)."""
+    shape = dataclasses.replace(MODELS[args.model], block_size=64)
+    return _sweep_field(Workload(shape, 1, dev, seed=1080, kv_fp8=True), dev, pk,
+                        [30, 35, 40, 45, 50, 55, 60], kv_dtype="e4m3 (scales 0.05 / 0.02)")
+
+
 def secondary_cfg5(args, dev, pk):
     """BASELINE configs[4] kernels at trace-like scale: DeepSeek-V2-Lite absorbed MLA (16 q
     heads over the 576-d latent, V = K[:, :512], 64-token pages, 27 layers); decode B = 256
@@ -1188,7 +1208,8 @@ def main(argv=None):
     if ws == 1 and not args.no_secondary:
         del run, step
         for name, fn in (("block16", secondary_block16), ("cfg3_llama70b", secondary_cfg3),
-                         ("cfg4_longctx", secondary_cfg4), ("cfg5_mla", secondary_cfg5)):
+                         ("cfg4_longctx", secondary_cfg4), ("cfg5_mla", secondary_cfg5),
+                         ("fp8_kv", secondary_fp8)):
             try:
                 secondary[name] = fn(args, dev, pk)
             except Exception as e:  # a secondary field never voids the headline

@@ -28,7 +28,7 @@
  *     table full, bad block) are written to *status_dev (int32, may be NULL) on
  *     the stream; the call itself returns SEMIPD_OK once launched.
  *   - n == 0 / batch == 0 / empty chunk is a no-op returning SEMIPD_OK.
- *   - Element dtype of every activation tensor equals the pool dtype.
+ *   - Element dtype of every activation tensor equals the pool dtype (bf16 for FP8 pools).
  *   - One in-flight prefill call and one in-flight decode call per pool (one
  *     prefill worker stream and one decode worker stream); allocator calls
  *     may come from any number of streams / host threads (linearizable).
@@ -57,7 +57,13 @@ typedef enum {
     SEMIPD_ERR_UNSUPPORTED = 7  /* valid but unsupported shape / dtype combination */
 } semipd_status;
 
-typedef enum { SEMIPD_BF16 = 0, SEMIPD_FP32 = 1 } semipd_dtype;
+/* Pool element dtype.  SEMIPD_FP8_E4M3 ("FP8 precision", DESIGN.md
+ * reading R31): pages hold OCP E4M3 codes (1 byte); a bf16 element x is written as
+ * E4M3_rne_satfinite(fl32(x / s)) and read as s * value(code), s the layer's tensor scale
+ * (semipd_set_kv_scales).  Activations (q, k_new, v_new, out) of an FP8 pool are bf16.
+ * Supported geometry: head_dim_k == head_dim_v == 128, block_size 64, even num_kv_heads, not
+ * kv_shared (create returns UNSUPPORTED otherwise). */
+typedef enum { SEMIPD_BF16 = 0, SEMIPD_FP32 = 1, SEMIPD_FP8_E4M3 = 2 } semipd_dtype;
 
 /* Pool geometry.  One block id spans all layers (reading R8).
  * Layout in the caller's memory (device), every region 1 KiB aligned:
@@ -169,7 +175,11 @@ int32_t semipd_num_sms(semipd_pool_t pool);
  *   "(100,100) uncontrolled" baseline).
  * bf16 with dk = dv = 128 and (Hq/Hkv) | 128 runs the tcgen05/TMEM/TMA kernel;
  * other shapes run the generic CUDA-core kernel.  Output is bitwise identical
- * for every sm_budget (the work decomposition depends on shapes only). */
+ * for every sm_budget (the work decomposition depends on shapes only).
+ * FP8 pools (reading R31): step 1 quantises the rows; in step 2 keys j < P_i are the pool's
+ * dequantised values (staged through the FP8 prefill scratch) and keys j >= P_i the chunk's
+ * own bf16 rows; the tcgen05 kernel runs as for bf16.  Needs the scratch
+ * (semipd_set_fp8_prefill_scratch) and no fused RoPE / peer epilogue (else UNSUPPORTED). */
 semipd_status semipd_prefill_attn(semipd_pool_t pool, int32_t layer, const void* q,
                                   const void* k_new, const void* v_new,
                                   const int32_t* cu_seqlens_q, const int32_t* req_ids,
@@ -190,7 +200,11 @@ semipd_status semipd_prefill_attn(semipd_pool_t pool, int32_t layer, const void*
  *   max_ctx_len (host) >= every ctx_lens[b];
  *   workspace: device scratch of >= semipd_decode_workspace_bytes(...) bytes,
  *   ZERO-FILLED before its first use (the kernels leave their counters at zero);
- *   sm_budget as in semipd_prefill_attn (0 = partition's decode budget). */
+ *   sm_budget as in semipd_prefill_attn (0 = partition's decode budget).
+ * FP8 pools (reading R31): the appended row is quantised and every key / value (the appended
+ * one included) is read back dequantised; num_q_heads / Hkv <= 8; no fused RoPE / peer
+ * epilogue (else UNSUPPORTED).  Kernel: head-pair E4M3 boxes converted to f16 in registers,
+ * f16 mma.sync with fp32 accumulation (kernel kind 9). */
 semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* q,
                                  const void* k_new, const void* v_new, const int32_t* req_ids,
                                  const int32_t* ctx_lens, int32_t batch, int32_t max_ctx_len,
@@ -212,7 +226,8 @@ int64_t semipd_launch_count(semipd_pool_t pool);
  * {phase (1 prefill, 2 decode), %smid, blockIdx.x, kernel kind (0 CUDA-core generic,
  * 1 tcgen05 prefill, 2 split-K decode, 3 MLA mma.sync decode, 4 MLA tcgen05 decode,
  * 5 MLA tcgen05 prefill, 6 / 7 / 8 wide-box split-K decode: head pairs at 64-token pages /
- * whole 128-token pages / head pairs at 16-token pages)}; *counter_dev (device int32)
+ * whole 128-token pages / head pairs at 16-token pages, 9 FP8 E4M3 head-pair decode)};
+ * *counter_dev (device int32)
  * is the append cursor.  Pass buf = NULL to disable. */
 semipd_status semipd_set_trace(semipd_pool_t pool, int32_t* buf, int32_t cap,
                                int32_t* counter_dev);
@@ -343,6 +358,27 @@ typedef struct {
     int32_t original_max_pos, rot_offset, rot_dim, interleaved;
 } semipd_rope_config;
 semipd_status semipd_set_rope(semipd_pool_t pool, const semipd_rope_config* cfg);
+
+/* ---- FP8 (E4M3) pools (reading R31) ----
+ * semipd_set_kv_scales: per-layer tensor scales (host float[num_layers] each, every value
+ * finite and > 0; NULL leaves that tensor's scales unchanged).  Default 1.0.  Later K/V writes
+ * quantise with them and later attention calls dequantise with them; changing a layer's scale
+ * does not rewrite pages already stored.  INVALID on a bad value or a non-FP8 pool. */
+semipd_status semipd_set_kv_scales(semipd_pool_t pool, const float* k_scales,
+                                   const float* v_scales);
+
+/* Prefill on an FP8 pool reads the cached prefix through a bf16 staging copy: before the
+ * tcgen05 attention a dequantisation pass writes s * value(code) of every prefix page of the
+ * call into caller-owned scratch (request i of the call gets pages [i * MBR, (i + 1) * MBR)).
+ * semipd_fp8_prefill_scratch_bytes: bytes for calls of up to max_reqs_per_call requests (host;
+ * 0 if the pool is not FP8 or the argument < 1).
+ * semipd_set_fp8_prefill_scratch: hand the scratch (device, >= that many bytes, 1 KiB aligned,
+ * owned by the caller and alive while prefill calls run; NULL detaches).  It initialises the
+ * scratch's tables synchronously.  An FP8 prefill call with more requests than the scratch was
+ * sized for, or with no scratch, returns INVALID. */
+size_t semipd_fp8_prefill_scratch_bytes(semipd_pool_t pool, int32_t max_reqs_per_call);
+semipd_status semipd_set_fp8_prefill_scratch(semipd_pool_t pool, void* mem, size_t bytes,
+                                             int32_t max_reqs_per_call);
 
 /* Library version string (host, static). */
 const char* semipd_version(void);

@@ -24,7 +24,7 @@ __all__ = ["SemipdError", "PoolConfig", "KVPool", "lib", "build", "blocks_for_to
 STATUS = {0: "OK", 1: "INVALID", 2: "OOM", 3: "UNKNOWN_REQ", 4: "TABLE_FULL", 5: "BAD_BLOCK",
           6: "CUDA", 7: "UNSUPPORTED"}
 OK, INVALID, OOM, UNKNOWN_REQ, TABLE_FULL, BAD_BLOCK, CUDA_ERR, UNSUPPORTED = range(8)
-BF16, FP32 = 0, 1
+BF16, FP32, FP8_E4M3 = 0, 1, 2
 
 _lib = None
 _lock = threading.Lock()
@@ -90,6 +90,9 @@ def lib():
                 "semipd_set_spans": (i32, [vp, vp, i32]),
                 "semipd_set_rope": (i32, [vp, P(_RopeCfg)]),
                 "semipd_version": (ctypes.c_char_p, []),
+                "semipd_set_kv_scales": (i32, [vp, P(f32), P(f32)]),
+                "semipd_fp8_prefill_scratch_bytes": (sz, [vp, i32]),
+                "semipd_set_fp8_prefill_scratch": (i32, [vp, vp, sz, i32]),
                 "semipd_ipc_alloc": (i32, [sz, P(vp), vp]),
                 "semipd_ipc_free": (i32, [vp]),
                 "semipd_ipc_open": (i32, [vp, P(vp)]),
@@ -182,15 +185,17 @@ class PoolConfig:
     head_dim_v: int
     max_reqs: int
     max_blocks_per_req: int
-    dtype: torch.dtype = torch.bfloat16
+    dtype: torch.dtype = torch.bfloat16  # bfloat16, float32, or float8_e4m3fn (E4M3 pages)
     kv_shared: bool = False
     oplog_words: int = 1 << 16
+
+    def code(self) -> int:
+        return {torch.bfloat16: BF16, torch.float32: FP32, torch.float8_e4m3fn: FP8_E4M3}[self.dtype]
 
     def c(self, device: int) -> _Cfg:
         return _Cfg(self.num_layers, self.num_blocks, self.block_size, self.num_kv_heads,
                     self.head_dim_k, self.head_dim_v, int(self.kv_shared), self.max_reqs,
-                    self.max_blocks_per_req, BF16 if self.dtype == torch.bfloat16 else FP32,
-                    device, self.oplog_words)
+                    self.max_blocks_per_req, self.code(), device, self.oplog_words)
 
 
 class KVPool:
@@ -236,12 +241,13 @@ class KVPool:
 
     def views(self, layer: int):
         """(K [N_B,Hkv,bs,dk], V [N_B,Hkv,bs,dv] or None if kv_shared, block_tables
-        [R,MBR], nblk [R]) as torch views of the pool memory (tests/harness)."""
+        [R,MBR], nblk [R]) as torch views of the pool memory (tests/harness).  FP8 pools: K / V
+        are uint8 views of the E4M3 codes."""
         k, v, bt, nb = (ctypes.c_void_p() for _ in range(4))
         _check("semipd_kv_pool_views", lib().semipd_kv_pool_views(
             self.h, layer, ctypes.byref(k), ctypes.byref(v), ctypes.byref(bt), ctypes.byref(nb)))
         c = self.cfg
-        dt = c.dtype
+        dt = torch.uint8 if c.dtype == torch.float8_e4m3fn else c.dtype  # FP8: the raw codes
         K = self._view(k.value, c.num_blocks * c.num_kv_heads * c.block_size * c.head_dim_k, dt,
                        (c.num_blocks, c.num_kv_heads, c.block_size, c.head_dim_k))
         V = None
@@ -308,6 +314,36 @@ class KVPool:
         arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[int(x) for x in peer_ptrs])
         _check("semipd_set_prefill_peers", lib().semipd_set_prefill_peers(
             self.h, arr, len(peer_ptrs), int(tokens)))
+
+    # ---------------------------------------------------------------- FP8 pools (R31)
+    def set_kv_scales(self, k_scales=None, v_scales=None):
+        """Per-layer fp32 tensor scales of an FP8 pool (C ABI ``semipd_set_kv_scales``);
+        a float applies to every layer, None leaves that tensor's scales unchanged."""
+        L = self.cfg.num_layers
+
+        def arr(x):
+            if x is None:
+                return None
+            xs = [float(x)] * L if isinstance(x, (int, float)) else [float(v) for v in x]
+            if len(xs) != L:
+                raise ValueError(f"need {L} scales, got {len(xs)}")
+            return (ctypes.c_float * L)(*xs)
+        _check("semipd_set_kv_scales", lib().semipd_set_kv_scales(self.h, arr(k_scales), arr(v_scales)))
+
+    def attach_fp8_prefill_scratch(self, max_reqs_per_call: int):
+        """Allocate (torch, on the pool's device) and attach the bf16 staging scratch an FP8
+        pool's prefill reads its prefix through (C ABI ``semipd_set_fp8_prefill_scratch``)."""
+        L = lib()
+        nb = int(L.semipd_fp8_prefill_scratch_bytes(self.h, int(max_reqs_per_call)))
+        if nb == 0:
+            raise SemipdError("semipd_fp8_prefill_scratch_bytes", INVALID)
+        mem = torch.empty(nb + 1024, dtype=torch.uint8, device=self.device)
+        off = (-mem.data_ptr()) % 1024
+        with torch.cuda.device(self.device):
+            _check("semipd_set_fp8_prefill_scratch", L.semipd_set_fp8_prefill_scratch(
+                self.h, ctypes.c_void_p(mem.data_ptr() + off), nb, int(max_reqs_per_call)))
+        self._f8_scratch = mem  # keep alive while attached
+        return mem
 
     def launch_count(self) -> int:
         return int(lib().semipd_launch_count(self.h))

@@ -1263,6 +1263,12 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     // the peer offsets were fixed for the gathered buffers' batch: any other batch would store
     // at wrong head / token positions or past a peer's buffer
     if (pool->dec_n_peers > 0 && batch != pool->dec_peer_tokens) return SEMIPD_ERR_INVALID;
+    if (c.dtype == SEMIPD_FP8_E4M3) {  // E4M3 pages (reading R31): quantised append + decode
+        if (pool->rope_on || pool->dec_n_peers > 0) return SEMIPD_ERR_UNSUPPORTED;
+        return spd_launch_decode_fp8(pool, layer, q, k_new, v_new, req_ids, ctx_lens, batch,
+                                     max_ctx_len, num_q_heads, softmax_scale, out, out_head_major,
+                                     workspace, ws_bytes, budget, status_dev, st);
+    }
     if (pool->rope_on) {
         // RoPE of q / k_new (in place) at position ctx, fused with the append of the rotated
         // rows (R28): the attention kernels below skip their own append

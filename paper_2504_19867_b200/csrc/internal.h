@@ -76,6 +76,15 @@ struct semipd_pool {
     unsigned long long* span_buf = nullptr;  // semipd_set_spans: 8 x u64 per launch slot
     int span_cap = 0;
     int span_next = 0;
+    // FP8 E4M3 pools (reading R31): per-layer tensor scales, decode head-pair maps (128 code
+    // bytes x 64 rows x 2 pages per box), and the prefill staging scratch with its bf16 maps
+    std::vector<float> k_scale, v_scale;
+    std::vector<CUtensorMap> f8kmap, f8vmap;
+    bool have_f8_maps = false;
+    unsigned char* f8s = nullptr;
+    int f8s_cap = 0;
+    CUtensorMap f8s_kmap{}, f8s_vmap{};
+    bool have_f8s_maps = false;
     void* timeline = nullptr;      // debug builds (SPD_TIMELINE): prefill clock64 stamps
     int* timeline_ctr = nullptr;
 
@@ -180,6 +189,21 @@ semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new,
                                   const int* cu_seqlens, const int* req_ids, const int* pos0,
                                   int n, int total_rows, int mode, int* status_dev,
                                   cudaStream_t s);
+// FP8 E4M3 pools (fp8.cu)
+bool spd_fp8_geometry_ok(const semipd_pool_config* c);
+bool spd_fp8_init_maps(semipd_pool* p);
+semipd_status spd_launch_kv_write_fp8(semipd_pool_t p, int layer, const void* k_new, const void* v_new,
+                                      const int* cu_seqlens, const int* req_ids, const int* pos0,
+                                      int n, int total_rows, int* status_dev, cudaStream_t s);
+semipd_status spd_launch_dequant_prefix(semipd_pool_t p, int layer, const int* req_ids,
+                                        const int* prefix_lens, int n, int budget, int* status_dev,
+                                        cudaStream_t s);
+void spd_fp8_prefill_view(const semipd_pool* p, const int** ids, const int** bt, int* n_blocks);
+semipd_status spd_launch_decode_fp8(semipd_pool_t pool, int layer, const void* q, const void* k_new,
+                                    const void* v_new, const int* req_ids, const int* ctx_lens,
+                                    int batch, int max_ctx_len, int Hq, float scale, void* out,
+                                    int out_head_major, void* workspace, size_t ws_bytes, int budget,
+                                    int* status_dev, cudaStream_t st);
 semipd_status spd_launch_simt_attn(semipd_pool_t p, int layer, const void* q, const int* cu_seqlens,
                                    const int* req_ids, const int* pos0, int n, int total_rows,
                                    int mode, int Hq, float scale, void* out, int out_head_major,

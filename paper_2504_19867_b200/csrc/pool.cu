@@ -21,6 +21,8 @@ struct Layout {
     size_t k_layer, v_layer, layer_stride, total;
 };
 
+size_t elem_bytes(int dtype) { return dtype == SEMIPD_BF16 ? 2 : dtype == SEMIPD_FP32 ? 4 : 1; }
+
 bool valid_cfg(const semipd_pool_config* c) {
     if (!c) return false;
     if (c->num_layers < 1 || c->num_blocks < 1 || c->block_size < 1 || c->num_kv_heads < 1)
@@ -29,15 +31,15 @@ bool valid_cfg(const semipd_pool_config* c) {
         return false;
     if (c->kv_shared && c->head_dim_v > c->head_dim_k) return false;
     if (c->max_reqs < 1 || c->max_blocks_per_req < 1 || c->oplog_words < 0) return false;
-    if (c->dtype != SEMIPD_BF16 && c->dtype != SEMIPD_FP32) return false;
-    const size_t eb = c->dtype == SEMIPD_BF16 ? 2 : 4;
+    if (c->dtype != SEMIPD_BF16 && c->dtype != SEMIPD_FP32 && c->dtype != SEMIPD_FP8_E4M3) return false;
+    const size_t eb = elem_bytes(c->dtype);
     if ((c->head_dim_k * eb) % 16 || (c->head_dim_v * eb) % 16) return false;  // 16-B rows
     return true;
 }
 
 Layout layout_of(const semipd_pool_config* c) {
     Layout L{};
-    const size_t eb = c->dtype == SEMIPD_BF16 ? 2 : 4;
+    const size_t eb = elem_bytes(c->dtype);
     size_t o = 0;
     L.off_state = o;
     o = align_up(o + sizeof(SpdDevState), kAlign);
@@ -144,6 +146,7 @@ int32_t semipd_blocks_for_tokens(int32_t tokens, int32_t block_size) {
 semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, size_t bytes,
                                     semipd_stream_t s, semipd_pool_t* out) {
     if (!valid_cfg(cfg) || !mem || !out) return SEMIPD_ERR_INVALID;
+    if (cfg->dtype == SEMIPD_FP8_E4M3 && !spd_fp8_geometry_ok(cfg)) return SEMIPD_ERR_UNSUPPORTED;
     if (reinterpret_cast<uintptr_t>(mem) % kAlign) return SEMIPD_ERR_INVALID;
     const Layout L = layout_of(cfg);
     if (bytes < L.total) return SEMIPD_ERR_INVALID;
@@ -170,7 +173,7 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
     p->k_layer_bytes = L.k_layer;
     p->v_layer_bytes = L.v_layer;
     p->layer_stride = L.layer_stride;
-    p->esize = cfg->dtype == SEMIPD_BF16 ? 2 : 4;
+    p->esize = elem_bytes(cfg->dtype);
     p->n_prefill = (p->num_sms + 1) / 2;
     p->n_decode = p->num_sms - p->n_prefill.load();
     // zero everything (K/V zero-filled: masked keys always read finite values)
@@ -188,6 +191,11 @@ semipd_status semipd_kv_pool_create(const semipd_pool_config* cfg, void* mem, si
                                            cfg->max_reqs, nbt);
     p->launches += 1;
     if (cudaGetLastError() != cudaSuccess) {
+        delete p;
+        cudaSetDevice(prev);
+        return SEMIPD_ERR_CUDA;
+    }
+    if (cfg->dtype == SEMIPD_FP8_E4M3 && !spd_fp8_init_maps(p)) {
         delete p;
         cudaSetDevice(prev);
         return SEMIPD_ERR_CUDA;

@@ -84,6 +84,7 @@ struct PrefillParams {
     unsigned char* k_pool;  // this layer's K / V pages
     unsigned char* v_pool;
     float scale_log2;
+    float scale_log2_pre;  // prefix tiles: FP8 pools stage value(code) of K, so k_scale enters here
     SpdTrace trace;
     long long* tl;  // SPD_TIMELINE builds only: phase clock64 stamps of CTA 0
     int* tl_ctr;
@@ -533,7 +534,6 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
         const uint32_t s_tmem = tmem + lane_base + (uint32_t)(t * BN);
         const uint32_t o_tmem = tmem + lane_base + 256u + (uint32_t)(t * HD);
-        const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
         [[maybe_unused]] int tl_tile = 0;  // SPD_TIMELINE record index
         int cnt = 0, nunit = 0;
         for (;;) {
@@ -585,7 +585,8 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
                     for (int k = 0; k < w; ++k) mxc[k] = fmaxf(mxc[k], mxc[k + w]);
                 const float mx = mxc[0];
-                const float mtrue = fmaxf(m, mx * p.scale_log2);  // scale > 0: max commutes
+                const float tsc = j < d.np ? p.scale_log2_pre : p.scale_log2;
+                const float mtrue = fmaxf(m, mx * tsc);  // scale > 0: max commutes
                 // lazy rescale (R21): the reference max m moves only when the row max
                 // exceeds it by > 8 (log2 units), so P <= 2^8 and nearly every tile skips the O
                 // round trip through TMEM (the exact-max rescale ran on most tiles: ~10 % of the
@@ -618,6 +619,7 @@ __global__ void __launch_bounds__(NT, 1)
                 // the bf16-rounded P the PV MMA consumes (R21) with mixed-precision FHADD.BF16
                 // (one instruction per element, half-register operand), in four chains
                 const uint64_t nm2 = f2(-m, -m);
+                const uint64_t sc2 = f2(tsc, tsc);
                 float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {  // 32 S columns -> 16 packed P columns
@@ -834,6 +836,9 @@ __global__ void __launch_bounds__(NT, 1)
 
 bool fast_path_ok(const semipd_pool* pl, int Hq) {
     const auto& c = pl->cfg;
+    if (c.dtype == SEMIPD_FP8_E4M3)  // E4M3 pages: the same kernel over bf16 staging pages (R31)
+        return !c.kv_shared && c.head_dim_k == HD && c.head_dim_v == HD && Hq % c.num_kv_heads == 0 &&
+               Hq / c.num_kv_heads <= 16 && BM % (Hq / c.num_kv_heads) == 0 && c.block_size == 64;
     if (c.dtype != SEMIPD_BF16 || c.kv_shared || c.head_dim_k != HD || c.head_dim_v != HD ||
         !pl->have_maps || Hq % c.num_kv_heads || (c.block_size & (c.block_size - 1)))
         return false;
@@ -870,7 +875,19 @@ extern "C" semipd_status semipd_prefill_attn(
         (!fast_path_ok(pool, num_q_heads) || spd_mla_prefill_ok(pool, num_q_heads)))
         return SEMIPD_ERR_UNSUPPORTED;
     const bool rope = pool->rope_on;
-    if (rope) {
+    const bool fp8 = c.dtype == SEMIPD_FP8_E4M3;
+    if (fp8) {
+        // E4M3 pages (reading R31): quantised K/V write of the chunk, then the call's prefix pages
+        // dequantised into the bf16 staging scratch, which the tcgen05 kernel reads as it reads a
+        // bf16 pool; the chunk's own keys come from k_new / v_new (bf16) as always
+        if (rope || pool->pre_n_peers > 0 || !fast_path_ok(pool, num_q_heads)) return SEMIPD_ERR_UNSUPPORTED;
+        if (!pool->have_f8s_maps || n > pool->f8s_cap) return SEMIPD_ERR_INVALID;
+        semipd_status r = spd_launch_kv_write_fp8(pool, layer, k_new, v_new, cu_seqlens_q, req_ids,
+                                                  prefix_lens, n, total_q, status_dev, st);
+        if (r == SEMIPD_OK)
+            r = spd_launch_dequant_prefix(pool, layer, req_ids, prefix_lens, n, budget, status_dev, st);
+        if (r != SEMIPD_OK) return r;
+    } else if (rope) {
         // RoPE of q / k_new (in place) at positions prefix + t, fused with the K/V write of the
         // rotated rows (R28): the attention kernels below skip their own write
         semipd_status r = spd_launch_rope_write(pool, layer, const_cast<void*>(q),
@@ -910,7 +927,7 @@ extern "C" semipd_status semipd_prefill_attn(
     prm.sched = &pool->st->sched[0];
     prm.n = n;
     prm.T = total_q;
-    prm.write_kv = rope ? 0 : 1;
+    prm.write_kv = rope || fp8 ? 0 : 1;
     prm.Hq = num_q_heads;
     prm.Hkv = c.num_kv_heads;
     prm.G = G;
@@ -926,6 +943,13 @@ extern "C" semipd_status semipd_prefill_attn(
     prm.N_B = c.num_blocks;
     prm.out_head_major = out_head_major;
     prm.scale_log2 = softmax_scale * LOG2E;
+    prm.scale_log2_pre = fp8 ? prm.scale_log2 * pool->k_scale[layer] : prm.scale_log2;
+    const CUtensorMap* pkmap = fp8 ? &pool->f8s_kmap : &pool->kmap[layer];
+    const CUtensorMap* pvmap = fp8 ? &pool->f8s_vmap : &pool->vmap[layer];
+    if (fp8) {  // prefix pages from the staging scratch: request i of the call -> row i
+        spd_fp8_prefill_view(pool, &prm.req_ids, &prm.bt, &prm.N_B);
+        prm.box_rows = 64;
+    }
     prm.k_new = static_cast<const uint4*>(k_new);
     prm.v_new = static_cast<const uint4*>(v_new);
     prm.k_pool = static_cast<unsigned char*>(pool->k_layer(layer));
@@ -986,11 +1010,9 @@ extern "C" semipd_status semipd_prefill_attn(
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;
     if (prm.n_peers > 0)
-        prefill_tc_kernel<true><<<grid, NT, smem, st>>>(qmap, pool->kmap[layer], pool->vmap[layer],
-                                                        kcmap, vcmap, omap, prm);
+        prefill_tc_kernel<true><<<grid, NT, smem, st>>>(qmap, *pkmap, *pvmap, kcmap, vcmap, omap, prm);
     else
-        prefill_tc_kernel<false><<<grid, NT, smem, st>>>(qmap, pool->kmap[layer], pool->vmap[layer],
-                                                         kcmap, vcmap, omap, prm);
+        prefill_tc_kernel<false><<<grid, NT, smem, st>>>(qmap, *pkmap, *pvmap, kcmap, vcmap, omap, prm);
     pool->launches += 1;
     return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }

@@ -303,6 +303,7 @@ extern "C" semipd_status semipd_set_rope(semipd_pool_t pool, const semipd_rope_c
         return SEMIPD_OK;
     }
     const auto& c = pool->cfg;
+    if (c.dtype == SEMIPD_FP8_E4M3) return SEMIPD_ERR_UNSUPPORTED;  // no fused quantised RoPE write
     const semipd_status e = rope_check(c.head_dim_k, cfg->rot_offset, cfg->rot_dim, c.dtype,
                                        cfg->theta, cfg->factor, cfg->low_freq_factor,
                                        cfg->high_freq_factor, cfg->original_max_pos);

@@ -198,6 +198,11 @@ semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new,
                                   int n, int total_rows, int mode, int* status_dev,
                                   cudaStream_t s) {
     if (total_rows <= 0) return SEMIPD_OK;
+    if (p->cfg.dtype == SEMIPD_FP8_E4M3) {  // quantised write (reading R31), prefill rows only
+        if (mode != 0) return SEMIPD_ERR_UNSUPPORTED;
+        return spd_launch_kv_write_fp8(p, layer, k_new, v_new, cu_seqlens, req_ids, pos0, n,
+                                       total_rows, status_dev, s);
+    }
     RowMap m{mode == 0 ? cu_seqlens : nullptr, req_ids, pos0, n};
     const auto& c = p->cfg;
     const int k_vec = (int)(c.head_dim_k * p->esize / 16);

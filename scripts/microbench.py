@@ -61,6 +61,8 @@ def main():
     ap.add_argument("--mla", action="store_true", help="cfg5 absorbed-MLA decode (576/512, 16 heads)")
     ap.add_argument("--mla-prefill", action="store_true", help="cfg5 absorbed-MLA prefill chunk")
     ap.add_argument("--lpt", action="store_true", help="--ctx-lognormal: batch longest first")
+    ap.add_argument("--fp8", action="store_true",
+                    help="E4M3 pool (reading R31; bs must be 64): decode reads 1-byte codes")
     ap.add_argument("--ctx-lognormal", action="store_true",
                     help="--mla: contexts lognormal around --ctx (sigma 0.5, seed 5005), as bench.py cfg5")
     args = ap.parse_args()
@@ -80,8 +82,12 @@ def main():
     ctx = max(ctx_list)
     nb_dec = ctx // bs + 1
     nb_pre = -(-(C + P) // bs)
-    cfg = PoolConfig(L, B * nb_dec + nb_pre + 8, bs, Hkv, d, d, B + 2, max(nb_dec, nb_pre) + 2)
+    cfg = PoolConfig(L, B * nb_dec + nb_pre + 8, bs, Hkv, d, d, B + 2, max(nb_dec, nb_pre) + 2,
+                     dtype=torch.float8_e4m3fn if args.fp8 else torch.bfloat16)
     pool = KVPool(cfg, dev)
+    if args.fp8:
+        pool.set_kv_scales(0.05, 0.02)
+        pool.attach_fp8_prefill_scratch(1)
     i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
     pool.alloc_blocks(i32(list(range(B))), i32([c // bs + 1 for c in ctx_list]))
     pool.alloc_blocks(i32([B]), i32([nb_pre]))
@@ -89,8 +95,13 @@ def main():
     g.manual_seed(0)
     for l in range(L):
         K, V, _, _ = pool.views(l)
-        K.normal_(generator=g)
-        V.normal_(generator=g)
+        if args.fp8:  # random finite E4M3 codes of magnitude < 2^7
+            K.copy_(torch.randint(0, 0x70, K.shape, device=dev, generator=g, dtype=torch.int32).to(torch.uint8) |
+                    (torch.randint(0, 2, K.shape, device=dev, generator=g, dtype=torch.int32) * 128).to(torch.uint8))
+            V.copy_(torch.randint(0, 0x70, V.shape, device=dev, generator=g, dtype=torch.int32).to(torch.uint8))
+        else:
+            K.normal_(generator=g)
+            V.normal_(generator=g)
     rnd = lambda *s: torch.randn(*s, device=dev, generator=g).bfloat16()  # noqa: E731
     sc = 1 / math.sqrt(d)
     qd, kd, vd = rnd(B, Hq, d), rnd(B, Hkv, d), rnd(B, Hkv, d)
@@ -100,7 +111,8 @@ def main():
     qp, kp, vp = rnd(C, Hq, d), rnd(C, Hkv, d), rnd(C, Hkv, d)
     op = torch.empty(C, Hq, d, dtype=torch.bfloat16, device=dev)
     cu, ridp, pre = i32([0, C]), i32([B]), i32([P])
-    dec_bytes = sum(c + 1 for c in ctx_list) * Hkv * 2 * d * 2 + B * Hq * 2 * d * 2
+    kv_elem = 1 if args.fp8 else 2
+    dec_bytes = sum(c + 1 for c in ctx_list) * Hkv * 2 * d * kv_elem + B * Hq * 2 * d * 2
     pairs = C * P + C * (C + 1) / 2
     pre_flops = 2 * Hq * 2 * d * pairs
     kernels = ["decode", "prefill"] if args.kernel == "both" else [args.kernel]

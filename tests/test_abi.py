@@ -76,3 +76,20 @@ def test_peer_gather_host_argument_checks():
     assert call(mine=None) == spd.INVALID
     assert call(dsts=(vp * 2)(1, None)) == spd.INVALID
     assert call(src=None) == spd.INVALID
+
+
+def test_fp8_pool_host_logic():
+    """FP8 (E4M3) pools (reading R31): one byte per K / V element in the layout, and the FP8
+    calls reject bad host arguments before touching a device."""
+    import torch
+    L = spd.lib()
+    c8 = spd.PoolConfig(2, 100, 64, 8, 128, 128, 4, 8, dtype=torch.float8_e4m3fn).c(0)
+    cb = spd.PoolConfig(2, 100, 64, 8, 128, 128, 4, 8).c(0)
+    n8, nb = L.semipd_kv_pool_bytes(ctypes.byref(c8)), L.semipd_kv_pool_bytes(ctypes.byref(cb))
+    kv8 = 2 * 100 * 8 * 64 * 128 * 2
+    assert kv8 < n8 < kv8 + 2 * 1024 * 1024
+    assert nb - n8 == kv8  # exactly half the bf16 pool's K / V bytes
+    one = (ctypes.c_float * 2)(1.0, 1.0)
+    assert L.semipd_set_kv_scales(None, one, one) == spd.INVALID
+    assert L.semipd_fp8_prefill_scratch_bytes(None, 1) == 0
+    assert L.semipd_set_fp8_prefill_scratch(None, None, 0, 1) == spd.INVALID

@@ -388,7 +388,7 @@ class Workload:
 
     # ---- algorithmic work of one launch
     def decode_bytes_per_launch(self) -> float:
-        return decode_bytes(self.shape, self.ctx_list, 1 if self.kv_fp8 else 2)
+        return decode_bytes(self.shape, self.ctx_list, 1 if getattr(self, "kv_fp8", False) else 2)
 
     def prefill_flops_per_launch(self) -> float:
         return prefill_flops(self.shape, self.C, self.P)

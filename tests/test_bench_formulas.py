@@ -41,6 +41,10 @@ def test_decode_bytes_closed_form():
     io = B * Hq * (d + d) * 2
     assert w.decode_bytes_per_launch() == kv + io
     assert abs(w.decode_bytes_per_launch() / 1e6 - 538.2) < 0.1
+    # FP8 (E4M3) pool, reading R31: one byte per cached K / V element, q / o still bf16
+    w.kv_fp8 = True
+    assert w.decode_bytes_per_launch() == kv // 2 + io
+    assert abs(w.decode_bytes_per_launch() / 1e6 - 270.1) < 0.1
 
 
 def test_prefill_flops_closed_form():

@@ -44,7 +44,7 @@ def test_decode_bytes_closed_form():
     # FP8 (E4M3) pool, reading R31: one byte per cached K / V element, q / o still bf16
     w.kv_fp8 = True
     assert w.decode_bytes_per_launch() == kv // 2 + io
-    assert abs(w.decode_bytes_per_launch() / 1e6 - 270.1) < 0.1
+    assert abs(w.decode_bytes_per_launch() / 1e6 - 269.6) < 0.1
 
 
 def test_prefill_flops_closed_form():

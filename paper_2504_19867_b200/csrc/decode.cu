@@ -1226,7 +1226,8 @@ size_t semipd_decode_workspace_bytes(semipd_pool_t pool, int32_t max_batch, int3
     if (!pool || max_batch < 0 || num_q_heads <= 0 || max_ctx < 0) return 0;
     // SpdWs: counters for max_batch x Hkv at the front + the largest split-partial set of any
     // decode kernel / batch <= max_batch at the back
-    const int S_max = (max_ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+    int S_max = (max_ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+    if (pool->cfg.dtype == SEMIPD_FP8_E4M3) S_max *= spd_fp8_pieces();  // FP8: split pieces
     size_t part = spd_ws_partial_bytes((size_t)max_batch * num_q_heads, S_max, pool->cfg.head_dim_v);
     if (pool->cfg.kv_shared) {
         const size_t m = spd_mla_ws_bytes(max_batch, max_ctx);

@@ -47,6 +47,16 @@ constexpr int NST = 6;                   // ring depth (192 KiB)
 constexpr int GMAX = 8;                  // q heads per kv head (swap-AB: MMA N = 8)
 constexpr int NTHREADS = (2 * NCW + 1) * 32;
 constexpr int SPLIT_KEYS = 4096;         // same split rule as the bf16 decode kernels
+// SPD_F8_PIECES = 4: each split of >= 8 stages is cut further into pieces of 1/2, 1/4, 1/8, 1/8
+// of its stages, handed out largest first (guided self-scheduling), aimed at the wave
+// quantisation of 256 equal units (0.057 ms at 89 SMs = 2.88 -> 3 waves, 0.070 ms at 81 SMs =
+// 3.16 -> 4 waves).  Parity-green but measured much SLOWER (0.091 ms at 89 SMs, 0.068 at 148;
+// profiles/r2_fp8_pieces_ab.log): every unit ends in a 6-warp merge and a partial round trip,
+// about 4 us per unit, far more than the tail it removes.  Default 1 (whole splits).
+#ifndef SPD_F8_PIECES
+#define SPD_F8_PIECES 1
+#endif
+constexpr int NPIECE = SPD_F8_PIECES;
 constexpr float LOG2E = 1.4426950408889634f;
 static_assert(NST % NCW == 0, "each ring slot must have one fixed consumer pair");
 // Code -> f16 conversion per operand: 0 = cvt.rn.f16x2.e4m3x2 (F2FP, 2 per 4 codes), 1 = integer
@@ -260,9 +270,9 @@ struct DecParams {
     unsigned char* k_pool;       // layer base (codes)
     unsigned char* v_pool;
     __nv_bfloat16* out;
-    float* ws_m;                 // [B][Hq][S_max]
+    float* ws_m;                 // [B][Hq][S_max * NPIECE]
     float* ws_l;
-    float* ws_acc;               // [B][Hq][S_max][128]
+    float* ws_acc;               // [B][Hq][S_max * NPIECE][128]
     int* ws_cnt;                 // [B][Hkv]
     unsigned* sched;             // [2]
     int* status;
@@ -330,17 +340,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (u >= p.n_units) {
                 d.b = -1;
             } else {
-                d.s = u / (p.B * NP);
+                // unit order: piece (largest first), split, request, head pair
+                const int piece = u / (p.S_max * p.B * NP);
+                const int s0 = (u / (p.B * NP)) % p.S_max;
                 d.b = (u / NP) % p.B;
                 d.g = 2 * (u % NP);
                 ctx = __ldg(p.ctx_lens + d.b);
-                d.S = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
-                if (d.s >= d.S) continue;  // warp-uniform
+                const int S0 = (ctx + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+                if (s0 >= S0) continue;  // warp-uniform
                 const int nk = ctx + 1;
-                int len = (nk + d.S - 1) / d.S;
+                int len = (nk + S0 - 1) / S0;
                 len = (len + KPS - 1) / KPS * KPS;
-                d.k0 = d.s * len;
-                d.k1 = min(nk, d.k0 + len);
+                const int np = len / KPS >= 8 ? NPIECE : 1;  // same for every split of the request
+                if (piece >= np) continue;
+                const int k0s = s0 * len, k1s = min(nk, k0s + len);
+                const int ns = (k1s - k0s + KPS - 1) / KPS;
+                int a = 0, e = ns;  // this piece's stages [a, e) of the split
+                if (np > 1) {
+                    const int c1 = ns / 2, c2 = c1 + (ns - c1) / 2, c3 = c2 + (ns - c2) / 2;
+                    a = piece == 0 ? 0 : piece == 1 ? c1 : piece == 2 ? c2 : c3;
+                    e = piece == 0 ? c1 : piece == 1 ? c2 : piece == 2 ? c3 : ns;
+                }
+                d.S = S0 * np;
+                d.s = s0 * np + piece;
+                d.k0 = k0s + a * KPS;
+                d.k1 = min(k1s, k0s + e * KPS);
+                if (d.k1 < d.k0) d.k1 = d.k0;  // empty piece: a (-inf, 0, 0) partial
                 d.nst = (d.k1 - d.k0 + KPS - 1) / KPS;
                 // align the unit's first stage to the pair rotation (R26: the stage -> warp
                 // assignment depends on the unit only)
@@ -366,8 +391,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (d.b < 0) break;
             const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
             const int last_page = ctx / BS;
-            if (d.s == d.S - 1) {
-                // fused quantised append of both heads' K and V rows at slot ctx: lane
+            if (d.k0 <= ctx && ctx < d.k1) {
+                // fused quantised append of both heads' K and V rows at slot ctx, by the
+                // unit whose key range holds slot ctx (no other unit reads that slot): lane
                 // = (tensor, head e, 16-element chunk c)
                 const int blk = last_page < p.MBR ? __ldg(btr + last_page) : -1;
                 if (blk >= 0 && blk < p.N_B) {
@@ -615,7 +641,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     v.y = pack_bf16(o.z * inv, o.w * inv);
                     *reinterpret_cast<uint2*>(p.out + off) = v;
                 } else {
-                    const size_t pi = ((size_t)d.b * p.Hq + hq) * p.S_max + d.s;
+                    const size_t pi = ((size_t)d.b * p.Hq + hq) * (p.S_max * NPIECE) + d.s;
                     *reinterpret_cast<float4*>(p.ws_acc + pi * HD + c) = o;
                     if (c == 0) {
                         p.ws_m[pi] = M;
@@ -635,7 +661,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const int ee = idx / (p.G * (HD / 4));
                         const int h = (idx / (HD / 4)) % p.G, c = (idx % (HD / 4)) * 4;
                         const int hq = (d.g + ee) * p.G + h;
-                        const size_t pb0 = ((size_t)d.b * p.Hq + hq) * p.S_max;
+                        const size_t pb0 = ((size_t)d.b * p.Hq + hq) * (p.S_max * NPIECE);
                         float M = -INFINITY;
                         for (int sI = 0; sI < d.S; ++sI) M = fmaxf(M, __ldcg(p.ws_m + pb0 + sI));
                         float L = 0.f;
@@ -700,6 +726,8 @@ ScratchLayout scratch_layout(const semipd_pool* p, int cap) {
 }
 
 }  // namespace
+
+int spd_fp8_pieces() { return NPIECE; }
 
 bool spd_fp8_geometry_ok(const semipd_pool_config* c) {
     return c->head_dim_k == HD && c->head_dim_v == HD && c->block_size == BS &&
@@ -800,9 +828,10 @@ semipd_status spd_launch_decode_fp8(semipd_pool_t pool, int layer, const void* q
     const auto& c = pool->cfg;
     const int G = Hq / c.num_kv_heads;
     if (G > GMAX || !pool->have_f8_maps) return SEMIPD_ERR_UNSUPPORTED;
-    const int S_max = (max_ctx_len + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
+    const int S0_max = (max_ctx_len + 1 + SPLIT_KEYS - 1) / SPLIT_KEYS;
     SpdWs w;
-    if (!spd_ws_carve(workspace, ws_bytes, (size_t)batch * c.num_kv_heads, (size_t)batch * Hq, S_max, HD, &w))
+    if (!spd_ws_carve(workspace, ws_bytes, (size_t)batch * c.num_kv_heads, (size_t)batch * Hq,
+                      (size_t)S0_max * NPIECE, HD, &w))
         return SEMIPD_ERR_INVALID;
     DecParams prm;
     prm.q = static_cast<const __nv_bfloat16*>(q);
@@ -827,8 +856,8 @@ semipd_status spd_launch_decode_fp8(semipd_pool_t pool, int layer, const void* q
     prm.G = G;
     prm.MBR = c.max_blocks_per_req;
     prm.N_B = c.num_blocks;
-    prm.S_max = S_max;
-    prm.n_units = batch * (c.num_kv_heads / 2) * S_max;
+    prm.S_max = S0_max;  // unit enumeration; partial rows are indexed [B][Hq][S_max * NPIECE]
+    prm.n_units = NPIECE * S0_max * batch * (c.num_kv_heads / 2);
     prm.out_head_major = out_head_major;
     prm.scale_log2 = scale * pool->k_scale[layer] * LOG2E * (SPD_F8_KALU ? 256.f : 1.f);
     prm.ks = pool->k_scale[layer];

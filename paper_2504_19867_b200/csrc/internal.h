@@ -191,6 +191,7 @@ semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new,
                                   cudaStream_t s);
 // FP8 E4M3 pools (fp8.cu)
 bool spd_fp8_geometry_ok(const semipd_pool_config* c);
+int spd_fp8_pieces();  // split partials per 4096-key split of the FP8 decode kernel
 bool spd_fp8_init_maps(semipd_pool* p);
 semipd_status spd_launch_kv_write_fp8(semipd_pool_t p, int layer, const void* k_new, const void* v_new,
                                       const int* cu_seqlens, const int* req_ids, const int* pos0,

@@ -80,6 +80,10 @@ def lib():
             L.semipd_ref_e4m3_values.restype = None
             L.semipd_ref_decode_fp8.argtypes = [i, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, i,
                                                 vp, i, f, f, d, dp]
+            L.semipd_ref_round_bf16.argtypes = [d]
+            L.semipd_ref_round_bf16.restype = d
+            L.semipd_ref_prefill_mla_expanded.argtypes = [i, vp, vp, vp, i, i, i, i, i, i, vp, vp, vp,
+                                                          i, vp, i, vp, vp, d, dp, vp]
             L.semipd_ref_prefill_fp8.argtypes = [i, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp,
                                                  i, vp, i, f, f, d, dp, vp]
             _ = ip
@@ -360,4 +364,42 @@ def prefill_fp8(q, k_new, v_new, k_pool, v_pool, block_tables, cu_seqlens, req_i
                                       float(scale), _p(out), None if mask is None else _p(mask))
     if st != OK:
         raise ValueError(f"oracle prefill_fp8 status {st}")
+    return out
+
+
+# ---- Expanded-form MLA prefill (semipd_oracle.c, reading R32) ----
+
+def round_bf16(x: float) -> float:
+    """One round-to-nearest-even of a double onto bf16."""
+    return lib().semipd_ref_round_bf16(float(x))
+
+
+def prefill_mla_expanded(q, kv_new, pool, block_tables, cu_seqlens, req_ids, prefix_lens,
+                         w_uk, w_uv, scale: float, dn: int = 128, dr: int = 64, rows_mask=None):
+    """Expanded-form MLA prefill.  q [T, H, dn + dr] (q_nope | q_pe), kv_new [T, dc + dr] latent
+    rows of the chunk, pool [N_B, 1, bs, dc + dr] latent pages (MODIFIED: the chunk rows are
+    written), w_uk [H, dn, dc], w_uv [H, dv, dc]; all bf16 bits (uint16).  Returns fp64
+    out [T, H, dv] (rows outside rows_mask are zero)."""
+    q, kv_new, w_uk, w_uv = _c(q), _c(kv_new), _c(w_uk), _c(w_uv)
+    assert q.dtype == kv_new.dtype == w_uk.dtype == w_uv.dtype == pool.dtype == np.uint16
+    assert pool.flags.c_contiguous
+    T, H, dq = q.shape
+    assert dq == dn + dr
+    N_B, hk, bs, dl = pool.shape
+    assert hk == 1
+    dc = dl - dr
+    dv = w_uv.shape[1]
+    assert w_uk.shape == (H, dn, dc) and w_uv.shape == (H, dv, dc)
+    bt = _c(block_tables, np.int32)
+    cu = _c(cu_seqlens, np.int32)
+    rid = _c(req_ids, np.int32)
+    pl = _c(prefix_lens, np.int32)
+    out = np.zeros((T, H, dv), np.float64)
+    mask = None if rows_mask is None else _c(rows_mask, np.uint8)
+    st = lib().semipd_ref_prefill_mla_expanded(
+        len(rid), _p(cu), _p(rid), _p(pl), H, dn, dr, dv, dc, bs, _p(q), _p(kv_new), _p(pool), N_B,
+        _p(bt), bt.shape[1], _p(w_uk), _p(w_uv), float(scale), _p(out),
+        None if mask is None else _p(mask))
+    if st != OK:
+        raise ValueError(f"oracle prefill_mla_expanded status {st}")
     return out

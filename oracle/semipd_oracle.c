@@ -729,3 +729,108 @@ int semipd_ref_prefill_fp8(int n_req, const int* cu_seqlens, const int* req_ids,
     free(row_req);
     return ORC_OK;
 }
+
+/* ---- Expanded-form MLA prefill (reading R32) ----
+ * DeepSeek MLA caches per token one latent row [c (dc = 512) | k_pe (dr = 64)] (the pool's
+ * kv_shared rows, dk = 576).  The absorbed form (semipd_ref_prefill with kv_shared) attends
+ * over the latent directly; the expanded form first projects every key's latent to per-head
+ * keys and values with the up-projections W_UK, W_UV (h < H, rows d < dn / dv, columns c < dc):
+ *   k_nope[j][h][d] = bf16( sum_c W_UK[h][d][c] * c_j[c] )   (fp64 sum, one RNE to bf16)
+ *   v     [j][h][d] = bf16( sum_c W_UV[h][d][c] * c_j[c] )
+ *   K[j][h] = [k_nope[j][h] | k_pe_j]  (dn + dr dims),  V[j][h] = v[j][h]  (dv dims)
+ * and runs plain causal MHA per head with q [T][H][dn + dr] (q_nope | q_pe):
+ *   o[t][h] = sum_{j <= P_i + t} softmax_j(scale * q[t][h] . K[j][h]) V[j][h].
+ * The bf16 rounding of the projected K / V is R32's reading (they are activations, the
+ * projection GEMM's output dtype).  Step 1 copies the chunk's latent rows into the
+ * pool first, so every key's latent is read from the pool through the block table. */
+/* one round-to-nearest-even of a double onto bf16 (8 significant bits, fp32's exponent range,
+ * subnormal spacing 2^-133), straight from the definition */
+static double round_bf16(double x) {
+    if (x == 0.0 || !isfinite(x)) return x;
+    int e;
+    frexp(x, &e); /* |x| = m * 2^e, m in [0.5, 1) */
+    double ulp = ldexp(1.0, e - 8 > -133 ? e - 8 : -133);
+    return rint(x / ulp) * ulp;
+}
+double semipd_ref_round_bf16(double x) { return round_bf16(x); }
+
+int semipd_ref_prefill_mla_expanded(int n_req, const int* cu_seqlens, const int* req_ids,
+                                    const int* prefix_lens, int H, int dn, int dr, int dv, int dc,
+                                    int bs, const uint16_t* q, const uint16_t* kv_new,
+                                    uint16_t* pool, int N_B, const int* block_tables, int MBR,
+                                    const uint16_t* w_uk, const uint16_t* w_uv, double scale,
+                                    double* out, const unsigned char* rows_mask) {
+    const int dl = dc + dr; /* latent row width */
+    if (n_req < 0 || H <= 0 || dn <= 0 || dr < 0 || dv <= 0 || dc <= 0 || bs <= 0) return ORC_INVALID;
+    for (int i = 0; i < n_req; ++i) {
+        const int* bt = block_tables + (size_t)req_ids[i] * MBR;
+        int nk = prefix_lens[i] + cu_seqlens[i + 1] - cu_seqlens[i];
+        for (int p = 0; p * bs < nk; ++p)
+            if (p >= MBR || bt[p] < 0 || bt[p] >= N_B) return ORC_BAD_BLOCK;
+    }
+    /* step 1: latent rows of the chunk into the pool (element copies) */
+    for (int i = 0; i < n_req; ++i) {
+        const int* bt = block_tables + (size_t)req_ids[i] * MBR;
+        for (int t = cu_seqlens[i]; t < cu_seqlens[i + 1]; ++t) {
+            int pos = prefix_lens[i] + (t - cu_seqlens[i]);
+            size_t dst = ((size_t)bt[pos / bs] * bs + pos % bs) * dl;
+            for (int c = 0; c < dl; ++c) pool[dst + c] = kv_new[(size_t)t * dl + c];
+        }
+    }
+    int T = n_req > 0 ? cu_seqlens[n_req] : 0;
+    for (int i = 0; i < n_req; ++i) {
+        const int* bt = block_tables + (size_t)req_ids[i] * MBR;
+        int P = prefix_lens[i], C = cu_seqlens[i + 1] - cu_seqlens[i], nk = P + C;
+        /* step 2: expanded keys / values of this request (bf16-rounded projections) */
+        double* K = (double*)malloc(sizeof(double) * (size_t)nk * H * (dn + dr));
+        double* V = (double*)malloc(sizeof(double) * (size_t)nk * H * dv);
+#pragma omp parallel for schedule(dynamic, 4)
+        for (int j = 0; j < nk; ++j) {
+            const uint16_t* lat = pool + ((size_t)bt[j / bs] * bs + j % bs) * dl;
+            for (int h = 0; h < H; ++h) {
+                for (int d = 0; d < dn; ++d) {
+                    double acc = 0.0;
+                    for (int c = 0; c < dc; ++c)
+                        acc += ld(w_uk, ((size_t)h * dn + d) * dc + c, ORC_BF16) * ld(lat, c, ORC_BF16);
+                    K[((size_t)j * H + h) * (dn + dr) + d] = round_bf16(acc);
+                }
+                for (int d = 0; d < dr; ++d)
+                    K[((size_t)j * H + h) * (dn + dr) + dn + d] = ld(lat, dc + d, ORC_BF16);
+                for (int d = 0; d < dv; ++d) {
+                    double acc = 0.0;
+                    for (int c = 0; c < dc; ++c)
+                        acc += ld(w_uv, ((size_t)h * dv + d) * dc + c, ORC_BF16) * ld(lat, c, ORC_BF16);
+                    V[((size_t)j * H + h) * dv + d] = round_bf16(acc);
+                }
+            }
+        }
+        /* step 3: causal MHA per head */
+#pragma omp parallel
+        {
+            double* qd = (double*)malloc(sizeof(double) * (size_t)(dn + dr));
+            double* kh = (double*)malloc(sizeof(double) * (size_t)nk * (dn + dr));
+            double* vh = (double*)malloc(sizeof(double) * (size_t)nk * dv);
+            double* z = (double*)malloc(sizeof(double) * (size_t)nk);
+#pragma omp for schedule(dynamic, 1) collapse(2)
+            for (int t = cu_seqlens[i]; t < cu_seqlens[i + 1]; ++t)
+                for (int h = 0; h < H; ++h) {
+                    if (rows_mask && !rows_mask[t]) continue;
+                    int n = P + (t - cu_seqlens[i]) + 1;
+                    for (int c = 0; c < dn + dr; ++c) qd[c] = ld(q, ((size_t)t * H + h) * (dn + dr) + c, ORC_BF16);
+                    for (int j = 0; j < n; ++j) {
+                        for (int c = 0; c < dn + dr; ++c) kh[(size_t)j * (dn + dr) + c] = K[((size_t)j * H + h) * (dn + dr) + c];
+                        for (int c = 0; c < dv; ++c) vh[(size_t)j * dv + c] = V[((size_t)j * H + h) * dv + c];
+                    }
+                    attend_f64(qd, kh, vh, n, dn + dr, dv, scale, z, out + ((size_t)t * H + h) * dv);
+                }
+            free(qd);
+            free(kh);
+            free(vh);
+            free(z);
+        }
+        free(K);
+        free(V);
+    }
+    (void)T;
+    return ORC_OK;
+}

@@ -260,6 +260,14 @@ def prefill_flops(shape: synth.AttnShape, C: int, P: int) -> float:
     return 2.0 * shape.num_q_heads * (shape.head_dim_k + shape.head_dim_v) * pairs
 
 
+def mla_expanded_flops(H: int, C: int, P: int) -> float:
+    """Expanded-form MLA prefill (reading R32): the up-projection of every key's latent
+    (2 x 512 x 2 H 128 per key, P + C keys) plus causal MHA at dqk 192 / dv 128:
+    2 H (192 + 128) per unmasked (q, k) pair."""
+    pairs = C * P + C * (C + 1) / 2
+    return 2.0 * (P + C) * 512 * 2 * H * 128 + 2.0 * H * (192 + 128) * pairs
+
+
 def prefill_bytes(shape: synth.AttnShape, C: int) -> float:
     """HBM bytes a prefill launch must move at P = 0: q in, o out, k_new / v_new in and
     their copy into the pool pages (a3, fused)."""
@@ -278,7 +286,7 @@ class Workload:
                  gather: str = "nccl", B: int = DECODE_BATCH, ctx=DECODE_CTX,
                  C: int = PREFILL_TOKENS, P: int = 0, layers: int | None = None,
                  tp_mode: str = "dependent", nccl_max_ctas: int = 4, groups=None,
-                 max_prefix: int | None = None, kv_fp8: bool = False):
+                 max_prefix: int | None = None, kv_fp8: bool = False, mla_expanded: bool = False):
         from paper_2504_19867_b200 import KVPool, PoolConfig
         self.full = shape
         self.shape = synth.shard_heads(shape, tp) if tp > 1 else shape
@@ -301,6 +309,11 @@ class Workload:
                               kv_shared=s.kv_shared)
         self.pool = KVPool(self.cfg, dev)
         self.kv_fp8 = kv_fp8
+        # expanded-form MLA prefill (reading R32): q [C, H, 192], the chunk's
+        # latent rows [C, 576], per-layer up-projections W_UK / W_UV [H, 128, 512]; the call
+        # runs 2 spanned kernels per layer (up-projection GEMM, attention)
+        self.mla_exp = mla_expanded
+        assert not mla_expanded or s.kv_shared
         if kv_fp8:  # E4M3 pages (reading R31): per-tensor scales, prefix staging scratch
             self.pool.set_kv_scales(0.05, 0.02)
             self.pool.attach_fp8_prefill_scratch(1)
@@ -328,14 +341,19 @@ class Workload:
                     V.normal_(generator=g)
         Hq, Hkv, dk, dv = s.num_q_heads, s.num_kv_heads, s.head_dim_k, s.head_dim_v
         mk = lambda *shp: torch.randn(*shp, generator=g, device=dev, dtype=torch.float32).to(s.dtype)  # noqa: E731
-        self.qp = [mk(C, Hq, dk) for _ in range(self.L)]
+        self.qp = [mk(C, Hq, 192 if mla_expanded else dk) for _ in range(self.L)]
         self.kp = [mk(C, Hkv, dk) for _ in range(self.L)]
+        if mla_expanded:
+            self.w_uk = [(mk(Hq, 128, dk - 64).float() / math.sqrt(dk - 64)).to(s.dtype) for _ in range(self.L)]
+            self.w_uv = [(mk(Hq, 128, dk - 64).float() / math.sqrt(dk - 64)).to(s.dtype) for _ in range(self.L)]
+            self.ws_exp = self.pool.new_mla_expanded_workspace(1, C + max(P, max_prefix or 0), Hq)
         self.vp = [None if s.kv_shared else mk(C, Hkv, dv) for _ in range(self.L)]
         self.qd = [mk(B, Hq, dk) for _ in range(self.L)]
         self.kd = [mk(B, Hkv, dk) for _ in range(self.L)]
         self.vd = [None if s.kv_shared else mk(B, Hkv, dv) for _ in range(self.L)]
         hm = tp > 1
-        self.op = [torch.empty((Hq, C, dv) if hm else (C, Hq, dv), dtype=s.dtype, device=dev)
+        dvp = 128 if mla_expanded else dv
+        self.op = [torch.empty((Hq, C, dvp) if hm else (C, Hq, dvp), dtype=s.dtype, device=dev)
                    for _ in range(self.L)]
         self.od = [torch.empty((Hq, B, dv) if hm else (B, Hq, dv), dtype=s.dtype, device=dev)
                    for _ in range(self.L)]
@@ -375,7 +393,8 @@ class Workload:
                 self.od = [self.peer_d.local_view(l % 2) for l in range(self.L)]
                 self.op = [self.peer_p.local_view(l % 2) for l in range(self.L)]
         # device-side launch spans: slots in enqueue order (corun_step sets span_order)
-        self.spans = torch.zeros(2 * self.L + 8, 8, dtype=torch.int64, device=dev)
+        self.spans = torch.zeros(3 * self.L + 8, 8, dtype=torch.int64, device=dev)
+        self.span_k = {"prefill": 2 if mla_expanded else 1, "decode": 1}  # spans per layer
         self.span_order = ("prefill", "decode")
         self.ev_p_done, self.ev_d_done = torch.cuda.Event(), torch.cuda.Event()
 
@@ -391,6 +410,8 @@ class Workload:
         return decode_bytes(self.shape, self.ctx_list, 1 if getattr(self, "kv_fp8", False) else 2)
 
     def prefill_flops_per_launch(self) -> float:
+        if getattr(self, "mla_exp", False):
+            return mla_expanded_flops(self.shape.num_q_heads, self.C, self.P)
         return prefill_flops(self.shape, self.C, self.P)
 
     def prefill_bytes_per_launch(self) -> float:
@@ -406,12 +427,18 @@ class Workload:
         order = order or self.span_order
         sp = self.spans.cpu().numpy().astype(np.float64)
         out = {}
-        for i, ph in enumerate(order):
-            r = sp[i * self.L:(i + 1) * self.L]
+        off = 0
+        for ph in order:
+            k = getattr(self, "span_k", {}).get(ph, 1)
+            r = sp[off:off + k * self.L]
+            off += k * self.L
             n = r[:, 3].sum()
-            out[ph] = {"ms": float(r[:, 2].sum() / n / 1e6) if n else None,
+            # ms: the phase's kernel time per layer (k spanned kernels per layer summed)
+            out[ph] = {"ms": float(r[:, 2].sum() / (n / k) / 1e6) if n else None,
                        "launches": int(n),
                        "stream_ms": float((r[-1, 6] - r[0, 5]) / 1e6) if n else None}
+            if k > 1 and n:
+                out[ph]["parts_ms"] = [float(r[j::k, 2].sum() / r[j::k, 3].sum() / 1e6) for j in range(k)]
         return out
 
     # ---- TP exchange of layer l on phase stream s
@@ -460,9 +487,15 @@ class Workload:
                 if self.fused:
                     p.set_prefill_peers(self.peer_p.peer_shard_ptrs(l % 2), self.C)
                     self.peer_p.handshake(0, stream=s)  # every peer is done reading
-                p.prefill_attn(l, self.qp[l], self.kp[l], self.vp[l], self.cu, self.rid_pre,
-                               self.prefix, self.C, self.C, self.scale, self.op[l],
-                               out_head_major=self.tp > 1, sm_budget=b, stream=s)
+                if self.mla_exp:
+                    p.prefill_mla_expanded(l, self.qp[l], self.kp[l], self.w_uk[l], self.w_uv[l],
+                                           self.cu, self.rid_pre, self.prefix, self.C, self.C,
+                                           self.C + self.P, 1 / math.sqrt(192), self.op[l],
+                                           self.ws_exp, sm_budget=b, stream=s)
+                else:
+                    p.prefill_attn(l, self.qp[l], self.kp[l], self.vp[l], self.cu, self.rid_pre,
+                                   self.prefix, self.C, self.C, self.scale, self.op[l],
+                                   out_head_major=self.tp > 1, sm_budget=b, stream=s)
                 if self.tp > 1:
                     self._gather("p", l, s)
             p.free_blocks(self.rid_pre, None, stream=s)
@@ -1037,6 +1070,19 @@ def secondary_cfg5(args, dev, pk):
                         decode_ctx_mean=statistics.mean(ctx))
 
 
+def secondary_cfg5_expanded(args, dev, pk):
+    """cfg5_mla with the expanded-form MLA prefill (reading R32): the same
+    decode batch (absorbed decode over the latent) co-running with the 2048-token chunk's
+    prefill as up-projection GEMM + causal MHA at dqk 192 / dv 128 (2 kernels per layer); the
+    prefill rate and fraction are against the expanded form's own flops (mla_expanded_flops)."""
+    rng = np.random.default_rng(5005)
+    ctx = [int(c) for c in np.clip(rng.lognormal(math.log(350.0) - 0.125, 0.5, 256), 64, 4096)]
+    ctx.sort(reverse=True)
+    w = Workload(synth.CFG5_MLA, 1, dev, seed=1050, B=256, ctx=ctx, C=2048, mla_expanded=True)
+    return _sweep_field(w, dev, pk, [10, 15, 20, 25, 30, 40, 50], model="deepseek-v2-lite-mla",
+                        prefill_form="expanded (R32)", decode_ctx_mean=statistics.mean(ctx))
+
+
 # ----------------------------------------------------------------------------- main
 def main(argv=None):
     args = parse(argv)
@@ -1209,6 +1255,7 @@ def main(argv=None):
         del run, step
         for name, fn in (("block16", secondary_block16), ("cfg3_llama70b", secondary_cfg3),
                          ("cfg4_longctx", secondary_cfg4), ("cfg5_mla", secondary_cfg5),
+                         ("cfg5_mla_expanded", secondary_cfg5_expanded),
                          ("fp8_kv", secondary_fp8)):
             try:
                 secondary[name] = fn(args, dev, pk)

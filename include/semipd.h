@@ -380,6 +380,44 @@ size_t semipd_fp8_prefill_scratch_bytes(semipd_pool_t pool, int32_t max_reqs_per
 semipd_status semipd_set_fp8_prefill_scratch(semipd_pool_t pool, void* mem, size_t bytes,
                                              int32_t max_reqs_per_call);
 
+/* ---- Expanded-form MLA prefill (reading R32) ----
+ * P:362-365 / P:395 run DeepSeek (MLA) models; the cache is the latent pool (kv_shared, one
+ * 576-wide row per key: c_j = columns 0..511, k_pe_j = columns 512..575).  For request i
+ * (block-table row req_ids[i], chunk rows cu_seqlens_q[i] .. cu_seqlens_q[i+1]-1, P_i =
+ * prefix_lens[i] keys cached):
+ *   1. writes kv_new rows into the pool slots P_i + t (bit copies);
+ *   2. expands every key j < P_i + C_i of the request with the up-projections:
+ *        k_nope[j][h] = bf16(W_UK[h] c_j) (128), v[j][h] = bf16(W_UV[h] c_j) (128)
+ *      (fp32 accumulation on the tensor cores, one round-to-nearest-even to bf16);
+ *   3. O[t,h,:] = sum_{j <= P_i + t} softmax_j(softmax_scale * q[t,h] . [k_nope[j][h] | k_pe_j])
+ *      v[j][h] (causal, bottom-right aligned).
+ *   q [T][H][192] bf16 (q_nope 128 | q_pe 64), kv_new [T][576] bf16, w_uk [H][128][512] and
+ *   w_uv [H][128][512] bf16 (row-major, 16-byte aligned), out [T][H][128] bf16;
+ *   cu_seqlens_q device int32[n+1], req_ids / prefix_lens device int32[n] (n <= 1024);
+ *   total_q (host) = cu_seqlens_q[n]; max_chunk_len (host) >= every C_i;
+ *   max_total_keys (host) >= sum_i (P_i + C_i) (a smaller sum than the device data sets
+ *   *status_dev = INVALID and nothing is written);
+ *   workspace: device scratch, 256-byte aligned, >= semipd_prefill_mla_expanded_workspace_bytes
+ *   (pool, n, max_total_keys, H) bytes, owned by the caller (holds the expanded K / V; no
+ *   zero-fill needed);
+ *   sm_budget as in semipd_prefill_attn (caps each of the three persistent grids).
+ * Pool: bf16, kv_shared, one KV head, head_dim_k 576, block_size in {16, 32, 64, 128}; H even,
+ * <= 128 (else UNSUPPORTED / INVALID).  A block-table entry outside [0, N_B) sets BAD_BLOCK and
+ * that key's latent is read as zeros.  No fused RoPE / peer epilogue (UNSUPPORTED).
+ * Kernels: a prep pass (copies), a tcgen05 up-projection GEMM over TMA-gathered pool pages, a
+ * tcgen05 causal attention kernel with dqk 192 / dv 128 (trace kernel kind 10); three launches,
+ * the last two with launch spans. */
+size_t semipd_prefill_mla_expanded_workspace_bytes(semipd_pool_t pool, int32_t max_reqs,
+                                                   int32_t max_total_keys, int32_t num_heads);
+semipd_status semipd_prefill_mla_expanded(semipd_pool_t pool, int32_t layer, const void* q,
+                                          const void* kv_new, const void* w_uk, const void* w_uv,
+                                          const int32_t* cu_seqlens_q, const int32_t* req_ids,
+                                          const int32_t* prefix_lens, int32_t n, int32_t total_q,
+                                          int32_t max_chunk_len, int32_t max_total_keys,
+                                          int32_t num_heads, float softmax_scale, void* out,
+                                          void* workspace, size_t ws_bytes, int32_t sm_budget,
+                                          int32_t* status_dev, semipd_stream_t s);
+
 /* Library version string (host, static). */
 const char* semipd_version(void);
 

@@ -103,6 +103,9 @@ def lib():
                 "semipd_peer_handshake": (i32, [P(vp), vp, i32, i32, i32, vp]),
                 "semipd_rope": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, f64,
                                       f64, f64, f64, i32, vp]),
+                "semipd_prefill_mla_expanded_workspace_bytes": (sz, [vp, i32, i32, i32]),
+                "semipd_prefill_mla_expanded": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32,
+                                                      i32, i32, i32, f32, vp, vp, sz, i32, vp, vp]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -385,6 +388,29 @@ class KVPool:
             _ptr(prefix_lens), n, int(total_q), int(max_chunk_len), int(q.shape[1]),
             float(scale), _ptr(out), int(bool(out_head_major)), int(sm_budget), _ptr(status),
             _stream(stream)))
+        return out
+
+    def mla_expanded_workspace_bytes(self, max_reqs: int, max_total_keys: int, num_heads: int) -> int:
+        return int(lib().semipd_prefill_mla_expanded_workspace_bytes(
+            self.h, int(max_reqs), int(max_total_keys), int(num_heads)))
+
+    def new_mla_expanded_workspace(self, max_reqs: int, max_total_keys: int, num_heads: int):
+        nb = self.mla_expanded_workspace_bytes(max_reqs, max_total_keys, num_heads)
+        if nb == 0:
+            raise SemipdError("semipd_prefill_mla_expanded_workspace_bytes", UNSUPPORTED)
+        return torch.empty(nb, dtype=torch.uint8, device=self.device)
+
+    def prefill_mla_expanded(self, layer: int, q, kv_new, w_uk, w_uv, cu_seqlens, req_ids,
+                             prefix_lens, total_q: int, max_chunk_len: int, max_total_keys: int,
+                             scale: float, out, workspace, sm_budget: int = 0, status=None,
+                             stream=None):
+        """Expanded-form MLA prefill (include/semipd.h, reading R32)."""
+        _check("semipd_prefill_mla_expanded", lib().semipd_prefill_mla_expanded(
+            self.h, layer, _ptr(q), _ptr(kv_new), _ptr(w_uk), _ptr(w_uv), _ptr(cu_seqlens),
+            _ptr(req_ids), _ptr(prefix_lens), int(req_ids.numel()), int(total_q),
+            int(max_chunk_len), int(max_total_keys), int(q.shape[1]), float(scale), _ptr(out),
+            _ptr(workspace), 0 if workspace is None else workspace.numel(), int(sm_budget),
+            _ptr(status), _stream(stream)))
         return out
 
     def decode_workspace_bytes(self, max_batch: int, num_q_heads: int, max_ctx: int) -> int:

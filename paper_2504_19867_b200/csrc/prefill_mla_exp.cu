@@ -1,0 +1,874 @@
+// prefill_mla_exp.cu — expanded-form MLA chunked prefill (R32).
+//
+// The absorbed form (prefill_mla.cu) attends over the 576-wide latent directly: 2 x (576 + 512)
+// flops per (query, key, head).  The expanded form first projects every key's cached latent
+// c_j (512) to per-head keys and values with the model's up-projections,
+//   k_nope[j][h] = bf16(W_UK[h] c_j) (128),  v[j][h] = bf16(W_UV[h] c_j) (128),
+// keys [k_nope | k_pe_j] (192, the rope part k_pe_j = latent columns 512..575 is shared by all
+// heads), then runs causal MHA per head: 2 x (192 + 128) flops per (query, key, head) plus
+// 2 x 512 x 2 x 128 per (key, head) for the projection — 3.4x fewer flops than the absorbed
+// form for a chunk without prefix.  The latent pool stays the cache (the chunk's latent
+// rows are written first; P:229 paged access); the expanded K / V are per-call activations.
+//
+// Three launches on the caller's stream:
+//   1. mla_exp_prep_kernel (CUDA cores, HBM-bound): the chunk's latent rows -> pool pages
+//      (bit copies), every key's k_pe -> a contiguous [rows][64] buffer, the call's row
+//      offsets (each request's keys padded to 128-row tiles) -> the workspace header.
+//   2. mla_exp_gemm_kernel (tcgen05): [keys x 512] x [512 x 2 H 128] up-projection.  A = latent
+//      rows gathered from the paged pool by TMA (one box per page per 64-column k-stage), B =
+//      W_UK / W_UV rows (K-major), D = 128 x 256 fp32 tiles in TMEM (two buffers: the epilogue
+//      of tile n overlaps the mainloop of tile n + 1), epilogue -> bf16 RNE -> K_exp / V_exp
+//      [rows][H][128].  Rows past a request's keys are written as zeros (finite P V inputs).
+//   3. mla_exp_attn_kernel (tcgen05): the GQA prefill kernel's structure (prefill_sm100.cu) at
+//      G = 1 with dqk = 192: unit = (request, pair of 128-row q tiles, head), S = Q K^T over
+//      12 K16 steps, O += P V; Q pair in one 96 KiB TMA box, K (3 x 64-column slots: two
+//      k_nope halves + k_pe) and V (2 slots) through one ring of eight 16 KiB slots, so the
+//      96 KiB Q pair and 1.6 kv tiles fit in 224 KiB.  Softmax as in the GQA kernel (exact
+//      causal limit, lazy rescale R21, bf16 P summed as consumed).  Epilogue: 16-byte stores
+//      of each thread's 256-byte output row.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+
+using namespace spd;
+
+constexpr int XDN = 128;            // k_nope / q_nope per head
+constexpr int XDR = 64;             // rope part
+constexpr int XDC = 512;            // latent (W_UK / W_UV input) width
+constexpr int XDV = 128;            // v per head
+constexpr int XDL = XDC + XDR;      // 576: latent pool row
+constexpr int XBM = 128;            // q rows per tile, keys per kv tile, key rows per GEMM tile
+constexpr int XMAXN = 1024;         // requests per call
+constexpr float XLOG2E = 1.4426950408889634f;
+
+// ------------------------------------------------------------------ workspace
+// [hdr: int mtoff[n + 1] (128-row tile offset of each request's keys)] [K_exp rows x H x 128]
+// [V_exp rows x H x 128] [Kpe rows x 64], rows = max_total_keys + 128 n (per-request padding)
+size_t x_hdr_bytes(int n) { return spd_al256(sizeof(int) * (size_t)(n + 1)); }
+size_t x_rows(int n, int max_keys) { return (size_t)max_keys + (size_t)XBM * (size_t)n; }
+size_t x_ws_bytes(int n, int max_keys, int H) {
+    const size_t r = x_rows(n, max_keys);
+    return x_hdr_bytes(n) + spd_al256(r * H * XDN * 2) + spd_al256(r * H * XDV * 2) + spd_al256(r * XDR * 2);
+}
+
+// s_off[i] = sum_{i' < i} ceil((P_i' + C_i') / 128) (exclusive scan over the block; every
+// thread takes a contiguous range of requests)
+__device__ void x_scan(const int* cu, const int* prefix, int n, int* s_off, int* s_warp) {
+    const int T = blockDim.x, tid = threadIdx.x;
+    const int per = (n + T - 1) / T;
+    const int a = min(n, tid * per), b = min(n, a + per);
+    int sum = 0;
+    for (int i = a; i < b; ++i) sum += (__ldg(prefix + i) + __ldg(cu + i + 1) - __ldg(cu + i) + XBM - 1) / XBM;
+    const int lane = tid & 31, w = tid >> 5;
+    int inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) s_warp[w] = inc;
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int k = 0; k < T / 32; ++k) {
+            const int v = s_warp[k];
+            s_warp[k] = acc;
+            acc += v;
+        }
+    }
+    __syncthreads();
+    int run = s_warp[w] + inc - sum;  // exclusive prefix of this thread's range
+    if (tid == 0) s_off[0] = 0;
+    for (int i = a; i < b; ++i) {
+        run += (__ldg(prefix + i) + __ldg(cu + i + 1) - __ldg(cu + i) + XBM - 1) / XBM;
+        s_off[i + 1] = run;
+    }
+    __syncthreads();
+}
+
+// largest i in [0, n) with off[i] <= x (off non-decreasing, off[0] = 0)
+template <typename F>
+__device__ __forceinline__ int x_find(F off, int n, int x) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off(mid) <= x) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// ------------------------------------------------------------------ 1. prep
+struct XPrep {
+    const int* cu;
+    const int* req_ids;
+    const int* prefix;
+    const int* bt;
+    const uint4* kv_new;     // [T][576] bf16
+    unsigned char* pool;     // this layer's latent pages [N_B][bs][576]
+    uint4* kpe;              // [rows][64] bf16
+    int* hdr;
+    int* status;
+    int n, lg_bs, MBR, N_B;
+    long long rows_cap;  // workspace rows (max_total_keys + 128 n)
+};
+
+__global__ void __launch_bounds__(256) mla_exp_prep_kernel(XPrep p) {
+    __shared__ int s_off[XMAXN + 1];
+    __shared__ int s_warp[8];
+    x_scan(p.cu, p.prefix, p.n, s_off, s_warp);
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i <= p.n; i += blockDim.x) p.hdr[i] = s_off[i];
+    const int R = s_off[p.n] * XBM;
+    if (R > p.rows_cap) {  // the caller's max_total_keys was too small: write nothing
+        if (threadIdx.x == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_INVALID);
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const int bs_mask = (1 << p.lg_bs) - 1;
+    constexpr int RU = XDL * 2 / 16;  // 72 uint4 per latent row
+    for (int g = blockIdx.x * 8 + (threadIdx.x >> 5); g < R; g += gridDim.x * 8) {
+        const int i = x_find([&](int k) { return s_off[k]; }, p.n, g / XBM);
+        const int j = g - s_off[i] * XBM;
+        const int P = __ldg(p.prefix + i), c0 = __ldg(p.cu + i), nk = P + __ldg(p.cu + i + 1) - c0;
+        uint4* kd = p.kpe + (size_t)g * (XDR * 2 / 16);
+        const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+        if (j >= nk) {
+            if (lane < 8) kd[lane] = zero;
+            continue;
+        }
+        const int page = j >> p.lg_bs;
+        const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
+        if (blk < 0 || blk >= p.N_B) {
+            if (lane == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+            if (lane < 8) kd[lane] = zero;
+            continue;
+        }
+        uint4* prow = reinterpret_cast<uint4*>(p.pool + ((size_t)blk * (bs_mask + 1) + (j & bs_mask)) * (XDL * 2));
+        if (j >= P) {  // the chunk's own row: latent -> pool, k_pe -> Kpe
+            const uint4* src = p.kv_new + (size_t)(c0 + j - P) * RU;
+            for (int c = lane; c < RU; c += 32) {
+                const uint4 v = __ldg(src + c);
+                prow[c] = v;
+                if (c >= RU - 8) kd[c - (RU - 8)] = v;
+            }
+        } else if (lane < 8) {
+            kd[lane] = prow[RU - 8 + lane];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ 2. up-projection GEMM
+constexpr int GST = 4;                        // k-stages in flight
+constexpr uint32_t GA = XBM * 128;            // A stage: 128 rows x 64 cols (16 KiB)
+constexpr uint32_t GB = 256 * 128;            // B stage: 256 rows x 64 cols (32 KiB)
+constexpr int GNT = 192;
+
+struct GSmem {
+    unsigned char a[GST][GA];
+    unsigned char b[GST][GB];
+    uint64_t full[GST], empty[GST], accf[2], acce[2];
+    uint32_t tmem_base;
+};
+
+struct XGemm {
+    const int* cu;
+    const int* req_ids;
+    const int* prefix;
+    const int* bt;
+    const int* hdr;
+    __nv_bfloat16* kexp;
+    __nv_bfloat16* vexp;
+    int* status;
+    unsigned long long* span;
+    int n, H, lg_bs, box_rows, MBR, N_B;
+    long long rows_cap;
+};
+
+__device__ __forceinline__ uint64_t xk_desc(uint32_t addr) { return umma_desc_sw128(addr, 16, 1024); }
+
+__global__ void __launch_bounds__(GNT, 1)
+    mla_exp_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap ukmap,
+                        const __grid_constant__ CUtensorMap uvmap, XGemm p) {
+    if ((long long)__ldg(p.hdr + p.n) * XBM > p.rows_cap) return;  // INVALID (set by the prep kernel)
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    GSmem& sm = *reinterpret_cast<GSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int warp = (int)warp_id(), lane = (int)lane_id();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < GST; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.accf[s], 1);
+            mbar_init(&sm.acce[s], 128);
+        }
+        fence_mbar_init();
+        span_begin(p.span);
+    }
+    if (warp == 1) tmem_alloc(&sm.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+    const int MT = __ldg(p.hdr + p.n);
+    const int NTN = p.H;  // n tiles of 256 columns: H / 2 head pairs of K_nope, then of V
+    const int total = MT * NTN;
+    auto off = [&](int k) { return __ldg(p.hdr + k); };
+
+    if (warp == 0) {
+        // ================================ TMA producer ================================
+        if (lane == 0) {
+            tma_prefetch_desc(&amap);
+            tma_prefetch_desc(&ukmap);
+            tma_prefetch_desc(&uvmap);
+        }
+        const int nbox = XBM / p.box_rows;
+        const int bs_mask = (1 << p.lg_bs) - 1;
+        int sc = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+            const int mt = tile / NTN, nt = tile % NTN;
+            const int i = x_find(off, p.n, mt);
+            const int kbase = (mt - off(i)) * XBM;
+            const int nk = __ldg(p.prefix + i) + __ldg(p.cu + i + 1) - __ldg(p.cu + i);
+            int z = p.N_B;  // out of bounds: zero fill (keys past the request)
+            if (lane < nbox) {
+                const int j0 = kbase + lane * p.box_rows;
+                if (j0 < nk) {
+                    const int page = j0 >> p.lg_bs;
+                    const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
+                    if (blk >= 0 && blk < p.N_B) z = blk;
+                    else if (p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                }
+            }
+            const CUtensorMap* bm = nt < NTN / 2 ? &ukmap : &uvmap;
+            const int brow = (nt % (NTN / 2)) * 256;
+            for (int ks = 0; ks < XDC / 64; ++ks, ++sc) {
+                const int s = sc % GST;
+                if (lane == 0) {
+                    mbar_wait(&sm.empty[s], ((sc / GST) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&sm.full[s], GA + GB);
+                }
+                __syncwarp();
+                for (int b = 0; b < nbox; ++b) {
+                    const int zb = __shfl_sync(0xffffffffu, z, b);
+                    if (lane == 0)
+                        tma_load_3d(sm.a[s] + b * p.box_rows * 128, &amap, &sm.full[s], ks * 64,
+                                    (kbase + b * p.box_rows) & bs_mask, zb);
+                }
+                if (lane == 0) tma_load_3d(sm.b[s], bm, &sm.full[s], ks * 64, brow, 0);
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1) {
+        // ================================ MMA issuer ================================
+        const uint32_t idesc = umma_idesc_bf16_f32(XBM, 256, 0);
+        int sc = 0, lt = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++lt) {
+            const int ab = lt & 1;
+            mbar_wait(&sm.acce[ab], ((lt >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(ab * 256);
+            for (int ks = 0; ks < XDC / 64; ++ks, ++sc) {
+                const int s = sc % GST;
+                mbar_wait(&sm.full[s], (sc / GST) & 1);
+                tc_fence_after();
+                const uint32_t a0 = smem_u32(sm.a[s]), b0 = smem_u32(sm.b[s]);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    umma_ss_warp(d, xk_desc(a0 + kk * 32), xk_desc(b0 + kk * 32), idesc, (ks | kk) ? 1u : 0u);
+                umma_commit_warp(&sm.empty[s]);
+            }
+            umma_commit_warp(&sm.accf[ab]);
+        }
+    } else {
+        // ============ epilogue (warps 2-5): fp32 TMEM -> bf16 (RNE) -> K_exp / V_exp ============
+        const int q4 = warp & 3;
+        const int r = q4 * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+        int lt = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++lt) {
+            const int ab = lt & 1;
+            const int mt = tile / NTN, nt = tile % NTN;
+            const int i = x_find(off, p.n, mt);
+            const int kbase = (mt - off(i)) * XBM;
+            const int nk = __ldg(p.prefix + i) + __ldg(p.cu + i + 1) - __ldg(p.cu + i);
+            const bool valid = kbase + r < nk;
+            const size_t row = (size_t)mt * XBM + r;
+            __nv_bfloat16* base = nt < NTN / 2 ? p.kexp : p.vexp;
+            const int h0 = (nt % (NTN / 2)) * 2;
+            mbar_wait(&sm.accf[ab], (lt >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 2
+            for (int c = 0; c < 8; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tmem + lane_base + (uint32_t)(ab * 256 + c * 32), v);
+                tmem_wait_ld();
+                uint4* dst = reinterpret_cast<uint4*>(base + (row * p.H + h0 + (c >> 2)) * XDN + (c & 3) * 32);
+#pragma unroll
+                for (int e = 0; e < 32; e += 8) {
+                    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+                    if (valid) {
+                        o.x = pack_bf16(__uint_as_float(v[e + 0]), __uint_as_float(v[e + 1]));
+                        o.y = pack_bf16(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                        o.z = pack_bf16(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5]));
+                        o.w = pack_bf16(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7]));
+                    }
+                    dst[e / 8] = o;
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&sm.acce[ab]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+    if (threadIdx.x == 0) span_end(p.span);
+}
+
+// ------------------------------------------------------------------ 3. attention
+constexpr int ANT = 384;
+constexpr int NSLOT = 8;
+constexpr uint32_t SLOT = XBM * 128;          // 16 KiB: 128 rows x 64 columns
+constexpr uint32_t QCH = 2 * SLOT;            // one 64-column chunk of the Q pair (tiles A, B)
+constexpr int kXPvParts = 4;
+
+struct XUnit {
+    int i, h, t0, P, qrow0, krow0;
+    int tv[2], nkv[2];
+};
+
+struct ASmem {
+    unsigned char q[3][QCH];                  // [chunk][tile A rows | tile B rows][128 B]
+    unsigned char ring[NSLOT][SLOT];
+    uint64_t q_full, q_empty;
+    uint64_t full[NSLOT], empty[NSLOT];
+    uint64_t s_full[2], p_full[2][kXPvParts];
+    uint64_t o_full[2], o_empty[2];
+    uint64_t ufull[2], uempty[2];
+    XUnit units[2];
+    uint32_t tmem_base;
+};
+
+struct XAttn {
+    const int* cu;
+    const int* prefix;
+    const int* hdr;
+    __nv_bfloat16* out;
+    int* status;
+    unsigned long long* span;
+    unsigned* sched;
+    int n, T, H, pairs_max, n_units;
+    float scale_log2;
+    SpdTrace trace;
+};
+
+__global__ void __launch_bounds__(ANT, 1)
+    mla_exp_attn_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kxmap,
+                        const __grid_constant__ CUtensorMap vxmap, const __grid_constant__ CUtensorMap pemap,
+                        XAttn p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    ASmem& sm = *reinterpret_cast<ASmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int warp = (int)warp_id(), lane = (int)lane_id();
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.q_full, 1);
+        mbar_init(&sm.q_empty, 1);
+        for (int s = 0; s < NSLOT; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.s_full[s], 1);
+            for (int h = 0; h < kXPvParts; ++h) mbar_init(&sm.p_full[s][h], 128);
+            mbar_init(&sm.o_full[s], 1);
+            mbar_init(&sm.o_empty[s], 128);
+            mbar_init(&sm.ufull[s], 1);
+            mbar_init(&sm.uempty[s], 1 + 8);  // MMA warp + 8 softmax warps
+        }
+        fence_mbar_init();
+        span_begin(p.span);
+        if (p.trace.buf) {
+            int slot = atomicAdd(p.trace.ctr, 1);
+            if (slot < p.trace.cap)
+                reinterpret_cast<int4*>(p.trace.buf)[slot] =
+                    make_int4(1, (int)smid(), (int)blockIdx.x, 10 /* kernel kind: expanded MLA prefill */);
+        }
+    }
+    if (warp == 1) tmem_alloc(&sm.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp < 4) {
+        setmaxnreg_dec<72>();
+        if (warp == 0) {
+            // ====================== producer: units, Q pair, K / V slots ======================
+            if (lane == 0) {
+                tma_prefetch_desc(&qmap);
+                tma_prefetch_desc(&kxmap);
+                tma_prefetch_desc(&vxmap);
+                tma_prefetch_desc(&pemap);
+            }
+            int sc = 0, nunit = 0;
+            for (;;) {
+                const int us = nunit & 1;
+                XUnit d;
+                d.i = -1;
+                int u = 0;
+                if (lane == 0) u = (int)atomicAdd(p.sched, 1u);
+                u = __shfl_sync(0xffffffffu, u, 0);
+                if (u < p.n_units) {
+                    const int per_pair = p.n * p.H;
+                    const int pair = p.pairs_max - 1 - u / per_pair;  // LPT: last pairs first
+                    d.i = (u / p.H) % p.n;
+                    d.h = u % p.H;
+                    const int c0 = __ldg(p.cu + d.i), C = __ldg(p.cu + d.i + 1) - c0;
+                    d.t0 = pair * 2 * XBM;
+                    if (d.t0 >= C) continue;  // pair past this request's chunk (warp-uniform)
+                    d.tv[0] = min(XBM, C - d.t0);
+                    d.tv[1] = max(0, min(XBM, C - d.t0 - XBM));
+                    d.P = __ldg(p.prefix + d.i);
+                    d.nkv[0] = (d.P + d.t0 + d.tv[0] - 1) / XBM + 1;
+                    d.nkv[1] = d.tv[1] > 0 ? (d.P + d.t0 + XBM + d.tv[1] - 1) / XBM + 1 : d.nkv[0];
+                    d.qrow0 = c0 + d.t0;
+                    d.krow0 = __ldg(p.hdr + d.i) * XBM;
+                }
+                if (lane == 0) {
+                    mbar_wait(&sm.uempty[us], ((nunit >> 1) & 1) ^ 1);
+                    sm.units[us] = d;
+                    mbar_arrive(&sm.ufull[us]);
+                }
+                __syncwarp();
+                if (d.i < 0) break;
+                if (lane == 0) {
+                    mbar_wait(&sm.q_empty, (nunit & 1) ^ 1);
+                    // (64 cols, head h, 256 tokens, 3 chunks) -> [chunk][A rows | B rows][128 B]
+                    mbar_arrive_expect_tx(&sm.q_full, 3 * QCH);
+                    tma_load_4d(sm.q[0], &qmap, &sm.q_full, 0, d.h, d.qrow0, 0);
+                }
+                ++nunit;
+                for (int j = 0; j < d.nkv[1]; ++j) {
+                    const int krow = d.krow0 + j * XBM;
+                    // kv tile j = K slots (k_nope cols 0-63, 64-127, k_pe) then V slots (0-63, 64-127)
+#pragma unroll 1
+                    for (int c = 0; c < 5; ++c, ++sc) {
+                        if (lane == 0) {
+                            const int s = sc % NSLOT;
+                            mbar_wait(&sm.empty[s], ((sc / NSLOT) & 1) ^ 1);
+                            mbar_arrive_expect_tx(&sm.full[s], SLOT);
+                            if (c < 2)
+                                tma_load_3d(sm.ring[s], &kxmap, &sm.full[s], c * 64, d.h, krow);
+                            else if (c == 2)
+                                tma_load_3d(sm.ring[s], &pemap, &sm.full[s], 0, krow, 0);
+                            else
+                                tma_load_3d(sm.ring[s], &vxmap, &sm.full[s], (c - 3) * 64, d.h, krow);
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+        } else if (warp == 1) {
+            // ================================ MMA issuer ================================
+            const uint32_t idesc_s = umma_idesc_bf16_f32(XBM, XBM, 0);
+            const uint32_t idesc_o = umma_idesc_bf16_f32(XBM, XDV, 1);
+            const uint32_t idesc_o64 = umma_idesc_bf16_f32(XBM, 64, 1);
+            int sc = 0, nunit = 0, cnt_a = 0, cnt_b = 0;
+            auto wait_slot = [&](int c) { mbar_wait(&sm.full[c % NSLOT], (c / NSLOT) & 1); };
+            auto release = [&](int c0, int k) {
+                for (int e = 0; e < k; ++e) umma_commit_warp(&sm.empty[(c0 + e) % NSLOT]);
+            };
+            for (;;) {
+                const int us = nunit & 1;
+                mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
+                const XUnit d = sm.units[us];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.uempty[us]);
+                if (d.i < 0) break;
+                mbar_wait(&sm.q_full, nunit & 1);
+                tc_fence_after();
+                const int nA = d.nkv[0], nB = d.nkv[1];
+                const uint32_t q_base = smem_u32(sm.q[0]);
+                auto issue_s = [&](int t, int kc) {  // S_t = Q_t [k_nope | k_pe]^T, 12 x K16
+#pragma unroll
+                    for (int kk = 0; kk < 12; ++kk) {
+                        const int ch = kk >> 2;
+                        const uint32_t a = q_base + ch * QCH + t * SLOT + (kk & 3) * 32;
+                        const uint32_t b = smem_u32(sm.ring[(kc + ch) % NSLOT]) + (kk & 3) * 32;
+                        umma_ss_warp(tmem + (uint32_t)(t * XBM), xk_desc(a), xk_desc(b), idesc_s, kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit_warp(&sm.s_full[t]);
+                };
+                auto issue_pv = [&](int t, int& cnt, int vc, bool first) {  // O_t += P_t V
+                    const int s0 = vc % NSLOT, s1 = (vc + 1) % NSLOT;
+                    const uint32_t v0 = smem_u32(sm.ring[s0]), v1 = smem_u32(sm.ring[s1]);
+                    const uint32_t p_tmem = tmem + (uint32_t)(t * XBM);
+                    const uint32_t o_tmem = tmem + 256u + (uint32_t)(t * XDV);
+#pragma unroll
+                    for (int hf = 0; hf < kXPvParts; ++hf) {
+                        mbar_wait(&sm.p_full[t][hf], cnt & 1);
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = hf * 8 / kXPvParts; kk < (hf + 1) * 8 / kXPvParts; ++kk) {
+                            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+                            if (s1 == s0 + 1) {  // adjacent slots: one N = 128 MMA (LBO = slot pitch)
+                                umma_ts_warp(o_tmem, p_tmem + (uint32_t)(kk * 8),
+                                             umma_desc_sw128(v0 + kk * 2048, SLOT, 1024), idesc_o, acc);
+                            } else {  // ring wrap: the two 64-column halves as N = 64 MMAs
+                                umma_ts_warp(o_tmem, p_tmem + (uint32_t)(kk * 8),
+                                             umma_desc_sw128(v0 + kk * 2048, SLOT, 1024), idesc_o64, acc);
+                                umma_ts_warp(o_tmem + 64u, p_tmem + (uint32_t)(kk * 8),
+                                             umma_desc_sw128(v1 + kk * 2048, SLOT, 1024), idesc_o64, acc);
+                            }
+                        }
+                    }
+                    ++cnt;
+                };
+                const int c0 = sc;
+                for (int e = 0; e < 3; ++e) wait_slot(c0 + e);
+                tc_fence_after();
+                issue_s(0, c0);
+                issue_s(1, c0);
+                release(c0, 3);
+                if (nB == 1) umma_commit_warp(&sm.q_empty);
+                for (int j = 0; j < nB; ++j) {
+                    const int vc = c0 + 5 * j + 3;
+                    wait_slot(vc);
+                    wait_slot(vc + 1);
+                    tc_fence_after();
+                    if (j < nA) {
+                        if (j == 0) mbar_wait(&sm.o_empty[0], (nunit & 1) ^ 1);
+                        issue_pv(0, cnt_a, vc, j == 0);
+                        if (j == nA - 1) umma_commit_warp(&sm.o_full[0]);
+                    }
+                    const bool more = j + 1 < nB;
+                    const int kn = c0 + 5 * (j + 1);
+                    if (more) {
+                        for (int e = 0; e < 3; ++e) wait_slot(kn + e);
+                        tc_fence_after();
+                    }
+                    if (j + 1 < nA) issue_s(0, kn);
+                    if (j == 0) mbar_wait(&sm.o_empty[1], (nunit & 1) ^ 1);
+                    issue_pv(1, cnt_b, vc, j == 0);
+                    release(vc, 2);
+                    if (j == nB - 1) umma_commit_warp(&sm.o_full[1]);
+                    if (more) {
+                        issue_s(1, kn);
+                        release(kn, 3);
+                        if (j + 1 == nB - 1) umma_commit_warp(&sm.q_empty);
+                    }
+                }
+                sc = c0 + 5 * nB;
+                ++nunit;
+            }
+        }
+        // warps 2, 3: no role
+    } else {
+        // ============================ softmax warpgroups ============================
+        setmaxnreg_inc<216>();
+        const int t = (warp - 4) >> 2;  // q tile A (0) or B (1)
+        const int q4 = warp & 3;
+        const int r = q4 * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+        const uint32_t s_tmem = tmem + lane_base + (uint32_t)(t * XBM);
+        const uint32_t o_tmem = tmem + lane_base + 256u + (uint32_t)(t * XDV);
+        const float tsc = p.scale_log2;
+        int cnt = 0, nunit = 0;
+        for (;;) {
+            const int us = nunit & 1;
+            mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
+            const XUnit d = sm.units[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.uempty[us]);
+            if (d.i < 0) break;
+            const int trel = d.t0 + t * XBM + r;  // chunk-relative token of this row
+            const int nkv = d.nkv[t];
+            float m = -INFINITY;
+            uint64_t l2 = f2(0.f, 0.f);
+            for (int j = 0; j < nkv; ++j, ++cnt) {
+                mbar_wait(&sm.s_full[t], cnt & 1);
+                tc_fence_after();
+                uint32_t sr[4][32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32(s_tmem + c * 32, sr[c]);
+                tmem_wait_ld();
+                // causal, bottom-right aligned: key j * 128 + c <= P + trel
+                const int lim = d.P + trel - j * XBM;
+                if (lim < XBM - 1) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (c * 32 + e > lim) sr[c][e] = __float_as_uint(-INFINITY);
+                }
+                float mxc[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        const int k = (c * 16 + e / 2) % 4;
+                        mxc[k] = fmax3(mxc[k], __uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1]));
+                    }
+                const float mx = fmaxf(fmaxf(mxc[0], mxc[1]), fmaxf(mxc[2], mxc[3]));
+                const float mtrue = fmaxf(m, mx * tsc);
+                // lazy rescale (R21): the reference max moves only when exceeded by > 8 (log2)
+                const bool move = j == 0 || mtrue > m + 8.f;
+                if (j > 0 && __any_sync(0xffffffffu, move)) {
+                    const float alpha = move ? fast_exp2(m - mtrue) : 1.f;
+                    const uint64_t a2 = f2(alpha, alpha);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(o_tmem + c * 32, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 32; e += 2) {
+                            float lo, hi;
+                            f2_split(fmul2(f2(__uint_as_float(o[e]), __uint_as_float(o[e + 1])), a2), lo, hi);
+                            o[e] = __float_as_uint(lo);
+                            o[e + 1] = __float_as_uint(hi);
+                        }
+                        tmem_st32(o_tmem + c * 32, o);
+                    }
+                    l2 = fmul2(l2, a2);
+                }
+                if (move) m = mtrue;
+                const uint64_t nm2 = f2(-m, -m);
+                const uint64_t sc2 = f2(tsc, tsc);
+                float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        const uint64_t x2 = ffma2(f2(__uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1])), sc2, nm2);
+                        float p0, p1;
+                        if ((0x1111u >> (e >> 1)) & 1u) {
+                            f2_split(exp2_poly3(x2), p0, p1);
+                        } else {
+                            float x0, x1;
+                            f2_split(x2, x0, x1);
+                            p0 = fast_exp2(x0);
+                            p1 = fast_exp2(x1);
+                        }
+                        const uint32_t pp = pack_bf16(p0, p1);
+                        pk[e / 2] = pp;
+                        add_bf16x2_f32(ls[2 * (c & 1)], ls[2 * (c & 1) + 1], pp);
+                    }
+                    tmem_st16(s_tmem + (uint32_t)(c * 16), pk);
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(&sm.p_full[t][c]);
+                }
+                l2 = fadd2(l2, f2(ls[0] + ls[2], ls[1] + ls[3]));
+            }
+            // ---- epilogue: O / l -> bf16 -> out [T][H][128] (each thread its 256-byte row)
+            mbar_wait(&sm.o_full[t], nunit & 1);
+            tc_fence_after();
+            float la, lb;
+            f2_split(l2, la, lb);
+            const float inv = 1.f / (la + lb);
+            const bool valid = r < d.tv[t];
+            uint4* dst = reinterpret_cast<uint4*>(p.out + ((size_t)(d.qrow0 + t * XBM + r) * p.H + d.h) * XDV);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t o[32];
+                tmem_ld32(o_tmem + c * 32, o);
+                tmem_wait_ld();
+                if (valid) {
+#pragma unroll
+                    for (int e = 0; e < 32; e += 8) {
+                        uint4 v;
+                        v.x = pack_bf16(__uint_as_float(o[e + 0]) * inv, __uint_as_float(o[e + 1]) * inv);
+                        v.y = pack_bf16(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+                        v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+                        v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+                        dst[c * 4 + e / 8] = v;
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&sm.o_empty[t]);
+            ++nunit;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+    if (threadIdx.x == 0) {
+        span_end(p.span);
+        __threadfence();
+        const unsigned done = atomicAdd(p.sched + 1, 1u);
+        if (done == gridDim.x - 1) {
+            p.sched[0] = 0u;
+            p.sched[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+bool x_pool_ok(const semipd_pool* pl) {
+    const auto& c = pl->cfg;
+    const int bs = c.block_size;
+    return c.dtype == SEMIPD_BF16 && c.kv_shared && c.num_kv_heads == 1 && c.head_dim_k == XDL &&
+           pl->have_maps && (bs == 16 || bs == 32 || bs == 64 || bs == 128) && pl->box_rows == bs;
+}
+
+}  // namespace
+
+extern "C" size_t semipd_prefill_mla_expanded_workspace_bytes(semipd_pool_t pool, int32_t max_reqs,
+                                                              int32_t max_total_keys, int32_t num_heads) {
+    if (!pool || !x_pool_ok(pool) || max_reqs <= 0 || max_reqs > XMAXN || max_total_keys < 0 ||
+        num_heads <= 0 || num_heads % 2 || num_heads > 128)
+        return 0;
+    return x_ws_bytes(max_reqs, max_total_keys, num_heads);
+}
+
+extern "C" semipd_status semipd_prefill_mla_expanded(
+    semipd_pool_t pool, int32_t layer, const void* q, const void* kv_new, const void* w_uk,
+    const void* w_uv, const int32_t* cu_seqlens_q, const int32_t* req_ids, const int32_t* prefix_lens,
+    int32_t n, int32_t total_q, int32_t max_chunk_len, int32_t max_total_keys, int32_t num_heads,
+    float softmax_scale, void* out, void* workspace, size_t ws_bytes, int32_t sm_budget,
+    int32_t* status_dev, semipd_stream_t s) {
+    if (!pool || layer < 0 || layer >= pool->cfg.num_layers || n < 0 || n > XMAXN || total_q < 0 ||
+        max_chunk_len < 0 || max_total_keys < 0)
+        return SEMIPD_ERR_INVALID;
+    if (num_heads <= 0 || num_heads % 2 || num_heads > 128) return SEMIPD_ERR_INVALID;
+    if (sm_budget < -1 || sm_budget > pool->num_sms) return SEMIPD_ERR_INVALID;
+    if (!x_pool_ok(pool)) return SEMIPD_ERR_UNSUPPORTED;
+    if (pool->rope_on || pool->pre_n_peers > 0) return SEMIPD_ERR_UNSUPPORTED;
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    if (status_dev && cudaMemsetAsync(status_dev, 0, sizeof(int), st) != cudaSuccess) return SEMIPD_ERR_CUDA;
+    if (n == 0 || total_q == 0) return SEMIPD_OK;
+    if (!q || !kv_new || !w_uk || !w_uv || !cu_seqlens_q || !req_ids || !prefix_lens || !out || !workspace)
+        return SEMIPD_ERR_INVALID;
+    if (reinterpret_cast<uintptr_t>(workspace) % 256 || ws_bytes < x_ws_bytes(n, max_total_keys, num_heads))
+        return SEMIPD_ERR_INVALID;
+    const auto& c = pool->cfg;
+    const int H = num_heads;
+    int budget = spd_resolve_budget(pool, sm_budget, true);
+    const size_t rows = x_rows(n, max_total_keys);
+    unsigned char* wb = static_cast<unsigned char*>(workspace);
+    int* hdr = reinterpret_cast<int*>(wb);
+    __nv_bfloat16* kexp = reinterpret_cast<__nv_bfloat16*>(wb + x_hdr_bytes(n));
+    __nv_bfloat16* vexp = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<unsigned char*>(kexp) +
+                                                           spd_al256(rows * H * XDN * 2));
+    __nv_bfloat16* kpe = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<unsigned char*>(vexp) +
+                                                          spd_al256(rows * H * XDV * 2));
+    const int lg_bs = __builtin_ctz((unsigned)c.block_size);
+
+    // 1. prep: chunk latent rows -> pool, k_pe -> Kpe, row offsets -> hdr
+    XPrep pp;
+    pp.cu = cu_seqlens_q;
+    pp.req_ids = req_ids;
+    pp.prefix = prefix_lens;
+    pp.bt = pool->bt;
+    pp.kv_new = static_cast<const uint4*>(kv_new);
+    pp.pool = static_cast<unsigned char*>(pool->k_layer(layer));
+    pp.kpe = reinterpret_cast<uint4*>(kpe);
+    pp.hdr = hdr;
+    pp.status = status_dev;
+    pp.n = n;
+    pp.lg_bs = lg_bs;
+    pp.MBR = c.max_blocks_per_req;
+    pp.N_B = c.num_blocks;
+    pp.rows_cap = (long long)rows;
+    const int max_mt = (int)((rows + XBM - 1) / XBM);
+    int gprep = budget > 0 ? budget : pool->num_sms;
+    const int prep_need = (int)((rows + 7) / 8);
+    if (gprep > prep_need) gprep = prep_need;
+    mla_exp_prep_kernel<<<gprep, 256, 0, st>>>(pp);
+    pool->launches += 1;
+    if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
+
+    // 2. up-projection GEMM
+    CUtensorMap ukmap, uvmap;
+    if (!spd_encode_tiled_3d(&ukmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(w_uk), XDC,
+                             (uint64_t)H * XDN, 1, XDC * 2, (uint64_t)H * XDN * XDC * 2, 64, 256, 1,
+                             CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !spd_encode_tiled_3d(&uvmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(w_uv), XDC,
+                             (uint64_t)H * XDV, 1, XDC * 2, (uint64_t)H * XDV * XDC * 2, 64, 256, 1,
+                             CU_TENSOR_MAP_SWIZZLE_128B))
+        return SEMIPD_ERR_CUDA;
+    XGemm gp;
+    gp.cu = cu_seqlens_q;
+    gp.req_ids = req_ids;
+    gp.prefix = prefix_lens;
+    gp.bt = pool->bt;
+    gp.hdr = hdr;
+    gp.kexp = kexp;
+    gp.vexp = vexp;
+    gp.status = status_dev;
+    gp.span = spd_next_span(pool);
+    gp.n = n;
+    gp.H = H;
+    gp.lg_bs = lg_bs;
+    gp.box_rows = pool->box_rows;
+    gp.MBR = c.max_blocks_per_req;
+    gp.N_B = c.num_blocks;
+    gp.rows_cap = (long long)rows;
+    const size_t gsm = sizeof(GSmem) + 1024;
+    const size_t asm_ = sizeof(ASmem) + 1024;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(mla_exp_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(mla_exp_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_) !=
+                cudaSuccess)
+            return SEMIPD_ERR_CUDA;
+        attr_set = true;
+    }
+    const long long gtiles = (long long)max_mt * H;
+    int ggrid = budget > 0 ? budget : (int)(gtiles < (1 << 30) ? gtiles : (1 << 30));
+    if (ggrid > gtiles) ggrid = (int)gtiles;
+    mla_exp_gemm_kernel<<<ggrid, GNT, gsm, st>>>(pool->kmap[layer], ukmap, uvmap, gp);
+    pool->launches += 1;
+    if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
+
+    // 3. attention
+    XAttn ap;
+    ap.cu = cu_seqlens_q;
+    ap.prefix = prefix_lens;
+    ap.hdr = hdr;
+    ap.out = static_cast<__nv_bfloat16*>(out);
+    ap.status = status_dev;
+    ap.span = spd_next_span(pool);
+    ap.sched = &pool->st->sched[0];
+    ap.n = n;
+    ap.T = total_q;
+    ap.H = H;
+    ap.pairs_max = (max_chunk_len + 2 * XBM - 1) / (2 * XBM);
+    if (ap.pairs_max < 1) return SEMIPD_OK;
+    const long long units = (long long)n * ap.pairs_max * H;
+    if (units > (1LL << 30)) return SEMIPD_ERR_UNSUPPORTED;
+    ap.n_units = (int)units;
+    ap.scale_log2 = softmax_scale * XLOG2E;
+    ap.trace = spd_trace(pool);
+    CUtensorMap qmap, kxmap, vxmap, pemap;
+    {
+        const uint64_t dims[4] = {64, (uint64_t)H, (uint64_t)total_q, 3};
+        const uint64_t strides[3] = {(XDN + XDR) * 2, (uint64_t)H * (XDN + XDR) * 2, 128};
+        const uint32_t box[4] = {64, 1, 2 * XBM, 3};
+        if (!spd_encode_tiled_4d(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(q), dims, strides, box,
+                                 CU_TENSOR_MAP_SWIZZLE_128B))
+            return SEMIPD_ERR_CUDA;
+    }
+    if (!spd_encode_tiled_3d(&kxmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kexp, XDN, (uint64_t)H, rows, XDN * 2,
+                             (uint64_t)H * XDN * 2, 64, 1, XBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !spd_encode_tiled_3d(&vxmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, vexp, XDV, (uint64_t)H, rows, XDV * 2,
+                             (uint64_t)H * XDV * 2, 64, 1, XBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !spd_encode_tiled_3d(&pemap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kpe, XDR, rows, 1, XDR * 2,
+                             rows * XDR * 2, 64, XBM, 1, CU_TENSOR_MAP_SWIZZLE_128B))
+        return SEMIPD_ERR_CUDA;
+    int grid = budget > 0 ? budget : ap.n_units;
+    if (grid > ap.n_units) grid = ap.n_units;
+    mla_exp_attn_kernel<<<grid, ANT, asm_, st>>>(qmap, kxmap, vxmap, pemap, ap);
+    pool->launches += 1;
+    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+}

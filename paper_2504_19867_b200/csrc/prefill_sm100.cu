@@ -135,38 +135,6 @@ struct Smem {
 #endif
 constexpr uint32_t kPolyMask = SPD_POLY_MASK;
 
-// 2^x for a pair on the FMA pipe: x = j + f with j = rint(x) (magic-number rounding, exact for
-// |x| < 2^22), f in [-1/2, 1/2]; 2^f by a degree-3 relative-minimax polynomial (max rel. error
-// 7.5e-5, below the bf16 rounding of P, 2^-9); 2^j added into the exponent bits.  x is clamped
-// at -125 so the exponent add cannot underflow: masked (-inf) scores give ~2^-125 instead of 0.
-__device__ __forceinline__ uint64_t exp2_poly3(uint64_t x2) {
-    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-    float x0, x1;
-    f2_split(x2, x0, x1);
-    const uint64_t xc = f2(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
-    const uint64_t t = fadd2(xc, f2(kMagic, kMagic));                      // M + j
-    const uint64_t nj = ffma2(t, f2(-1.f, -1.f), f2(kMagic, kMagic));      // -j (exact)
-    const uint64_t fr = fadd2(xc, nj);                                     // f
-    uint64_t q = ffma2(f2(0.05517049f, 0.05517049f), fr, f2(0.24260938f, 0.24260938f));
-    q = ffma2(q, fr, f2(0.69326103f, 0.69326103f));
-    q = ffma2(q, fr, f2(0.99992818f, 0.99992818f));
-    float q0, q1, t0, t1;
-    f2_split(q, q0, q1);
-    f2_split(t, t0, t1);
-    // bits(M + j) = 0x4B400000 + j and 0x4B400000 << 23 == 0 (mod 2^32): (bits << 23) = j << 23
-    return f2(__uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23)),
-              __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23)));
-}
-
-// a += float(lo half of pp), b += float(hi half): add.f32.bf16 is one FHADD.BF16 per element
-// with a half-register operand (no unpacking)
-__device__ __forceinline__ void add_bf16x2_f32(float& a, float& b, uint32_t pp) {
-    asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
-        "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
-        : "+f"(a), "+f"(b)
-        : "r"(pp));
-}
-
 // independent FMNMX3 chains of the row max (latency-bound: 64 three-input maxes per row)
 #ifndef SPD_MAX_CHAINS
 #define SPD_MAX_CHAINS 4

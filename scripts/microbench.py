@@ -60,6 +60,8 @@ def main():
                          "(SURVEY §8(d) item 7, load balance)")
     ap.add_argument("--mla", action="store_true", help="cfg5 absorbed-MLA decode (576/512, 16 heads)")
     ap.add_argument("--mla-prefill", action="store_true", help="cfg5 absorbed-MLA prefill chunk")
+    ap.add_argument("--mla-exp", action="store_true",
+                    help="cfg5 expanded-form MLA prefill chunk (R32): prep + up-projection GEMM + attention")
     ap.add_argument("--lpt", action="store_true", help="--ctx-lognormal: batch longest first")
     ap.add_argument("--fp8", action="store_true",
                     help="E4M3 pool (reading R31; bs must be 64): decode reads 1-byte codes")
@@ -71,6 +73,8 @@ def main():
         return mla(args, dev)
     if args.mla_prefill:
         return mla_prefill(args, dev)
+    if args.mla_exp:
+        return mla_exp(args, dev)
     L, B, ctx, C, P = args.layers, args.batch, args.ctx, args.chunk, args.prefix
     Hq, Hkv, d, bs = args.hq, args.hkv, 128, args.bs
     if args.ctx_uniform:
@@ -201,6 +205,57 @@ def mla_prefill(args, dev):
         ms, _ = timed_ms(run, args.iters, L)
         print(json.dumps({"kernel": "prefill_mla", "budget": bud, "C": C, "P": P, "ms": ms,
                           "TFLOP_s": flops / (ms / 1e3) / 1e12}), flush=True)
+
+
+def mla_exp(args, dev):
+    """Expanded-form MLA prefill (R32): one chunk of C tokens after a prefix P, 16 heads, bs 64.
+    Reports the call's time, the GEMM / attention kernels' span-timed shares, TFLOP/s of each
+    against its own algorithmic flops, and the absorbed-equivalent rate (the absorbed form's flops
+    for the same tokens / this call's time) for comparison with --mla-prefill."""
+    L, C, P, H = args.layers, args.chunk, args.prefix, 16
+    nb = -(-(C + P) // 64)
+    pool = KVPool(PoolConfig(L, nb + 4, 64, 1, 576, 512, 2, nb + 1, kv_shared=True), dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32([0]), i32([nb]))
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    for l in range(L):
+        K, _, _, _ = pool.views(l)
+        K.normal_(generator=g)
+    q = torch.randn(C, H, 192, device=dev, generator=g).bfloat16()
+    kv = torch.randn(C, 576, device=dev, generator=g).bfloat16()
+    w_uk = [(torch.randn(H, 128, 512, device=dev, generator=g) / 22.6).bfloat16() for _ in range(L)]
+    w_uv = [(torch.randn(H, 128, 512, device=dev, generator=g) / 22.6).bfloat16() for _ in range(L)]
+    out = torch.empty(C, H, 128, dtype=torch.bfloat16, device=dev)
+    ws = pool.new_mla_expanded_workspace(1, C + P, H)
+    pairs = C * P + C * (C + 1) / 2
+    f_attn = 2 * H * (192 + 128) * pairs
+    f_gemm = 2 * (C + P) * 512 * 2 * H * 128
+    f_abs = 2 * H * (576 + 512) * pairs
+    spans = torch.zeros(2, 8, dtype=torch.int64, device=dev)
+    for bud in [int(x) for x in args.budgets.split(",")]:
+        run = lambda l: pool.prefill_mla_expanded(l, q, kv, w_uk[l], w_uv[l], i32([0, C]), i32([0]),  # noqa: E731
+                                                  i32([P]), C, C, C + P, 1 / math.sqrt(192), out, ws,
+                                                  sm_budget=bud)
+        for l in range(min(L, 2)):
+            run(l)
+        torch.cuda.synchronize()
+        ms, _ = timed_ms(run, args.iters, L)
+        spans.zero_()
+        pool.set_spans(spans)
+        for it in range(args.iters):
+            run(it % L)
+        torch.cuda.synchronize()
+        pool.set_spans(None)
+        sp = spans.cpu()
+        gms = float(sp[0, 2]) / max(1, int(sp[0, 3])) / 1e6
+        ams = float(sp[1, 2]) / max(1, int(sp[1, 3])) / 1e6
+        print(json.dumps({"kernel": "prefill_mla_expanded", "budget": bud, "C": C, "P": P, "ms": ms,
+                          "gemm_ms": gms, "attn_ms": ams,
+                          "gemm_TFLOP_s": f_gemm / (gms / 1e3) / 1e12 if gms > 0 else None,
+                          "attn_TFLOP_s": f_attn / (ams / 1e3) / 1e12 if ams > 0 else None,
+                          "TFLOP_s": (f_gemm + f_attn) / (ms / 1e3) / 1e12,
+                          "absorbed_equiv_TFLOP_s": f_abs / (ms / 1e3) / 1e12}), flush=True)
 
 
 if __name__ == "__main__":

@@ -243,3 +243,44 @@ def mla_trace(n_req: int = 2000, lam: float = 3.0, seed: int = 5) -> list[TraceR
             rid += 1
         it += 1
     return reqs
+
+
+@dataclass
+class MlaExpandedCase:
+    """Inputs of an expanded-form MLA prefill call (R32): per
+    request the whole latent history lat[i] [P_i + C_i, 576] (rows < P_i are cached, rows >= P_i
+    are the call's kv_new), q [T, H, 192], up-projections w_uk / w_uv [H, 128, 512]."""
+    q: torch.Tensor
+    kv_new: torch.Tensor
+    lat: list
+    w_uk: torch.Tensor
+    w_uv: torch.Tensor
+    cu: list
+    scale: float
+
+
+def mla_expanded_case(chunk_lens, prefix_lens, seed: int, num_heads: int = 16, dist: int = FLAT,
+                      dn: int = 128, dr: int = 64, dc: int = 512, dv: int = 128) -> MlaExpandedCase:
+    """DeepSeek-V2-Lite shapes (16 heads, q_nope 128 | q_pe 64, latent 512 + rope 64, v 128).
+    Latent rows ~ N(0, 1) (VSHIFT: N(1, 1), so V has a non-zero mean), q ~ N(0, 1) (PEAKED:
+    N(0, 16)), W ~ N(0, 1/dc) so projected K / V are ~unit scale.  NEEDLE: 1 % of each
+    request's keys are exact copies of its last key's latent row (repeated keys, a
+    degenerate case of the softmax)."""
+    g = gen(seed)
+    lat = []
+    for p, c in zip(prefix_lens, chunk_lens):
+        x = randn((p + c, dc + dr), g, torch.bfloat16, mean=1.0 if dist == VSHIFT else 0.0)
+        if dist == NEEDLE and p + c > 1:
+            cnt = max(1, (p + c) // 100)
+            pos = torch.randperm(p + c - 1, generator=g)[:cnt]
+            x[pos] = x[-1].clone()
+        lat.append(x)
+    T = int(sum(chunk_lens))
+    q = randn((T, num_heads, dn + dr), g, torch.bfloat16, std=4.0 if dist == PEAKED else 1.0)
+    w_uk = randn((num_heads, dn, dc), g, torch.bfloat16, std=1.0 / math.sqrt(dc))
+    w_uv = randn((num_heads, dv, dc), g, torch.bfloat16, std=1.0 / math.sqrt(dc))
+    kv_new = torch.cat([x[p:] for x, p in zip(lat, prefix_lens)]) if T else torch.zeros(0, dc + dr, dtype=torch.bfloat16)
+    cu = [0]
+    for c in chunk_lens:
+        cu.append(cu[-1] + int(c))
+    return MlaExpandedCase(q, kv_new, lat, w_uk, w_uv, cu, 1.0 / math.sqrt(dn + dr))

@@ -40,6 +40,9 @@ def test_host_only_calls():
     assert L.semipd_set_partition(None, 50.0, 50.0) == spd.INVALID
     assert L.semipd_alloc_blocks(None, None, None, 1, None, None) == spd.INVALID
     assert L.semipd_kv_pool_create(ctypes.byref(cfg), None, 0, None, None) == spd.INVALID
+    assert L.semipd_prefill_mla_expanded_workspace_bytes(None, 1, 100, 16) == 0
+    assert L.semipd_prefill_mla_expanded(None, 0, None, None, None, None, None, None, None, 1, 1,
+                                         1, 1, 16, 0.1, None, None, 0, 0, None, None) == spd.INVALID
 
 
 def test_sass_is_blackwell_native():

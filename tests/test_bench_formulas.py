@@ -119,3 +119,14 @@ def test_nccl_options_cap_ctas():
     from paper_2504_19867_b200 import tp
     o = tp.nccl_options(4)
     assert o.config.max_ctas == 4 and o.config.min_ctas == 1
+
+
+def test_mla_expanded_flops_closed_form():
+    """Expanded-form MLA prefill (R32): projection 2 x 512 x (2 H 128) per key plus 2 H (192 + 128)
+    per unmasked pair; C = 2048, P = 0, H = 16 by hand."""
+    mod = _bench()
+    pairs = 2048 * 2049 // 2
+    assert mod.mla_expanded_flops(16, 2048, 0) == 2 * 2048 * 512 * 4096 + 2 * 16 * 320 * pairs
+    assert mod.mla_expanded_flops(16, 2048, 0) == 30_075_256_832
+    # a prefix adds P keys to the projection and C x P pairs
+    assert mod.mla_expanded_flops(16, 10, 100) == 2 * 110 * 512 * 4096 + 2 * 16 * 320 * (1000 + 55)

@@ -1079,7 +1079,7 @@ def secondary_cfg5_expanded(args, dev, pk):
     ctx = [int(c) for c in np.clip(rng.lognormal(math.log(350.0) - 0.125, 0.5, 256), 64, 4096)]
     ctx.sort(reverse=True)
     w = Workload(synth.CFG5_MLA, 1, dev, seed=1050, B=256, ctx=ctx, C=2048, mla_expanded=True)
-    return _sweep_field(w, dev, pk, [10, 15, 20, 25, 30, 40, 50], model="deepseek-v2-lite-mla",
+    return _sweep_field(w, dev, pk, [15, 25, 40, 50, 60, 70, 80, 90], model="deepseek-v2-lite-mla",
                         prefill_form="expanded (R32)", decode_ctx_mean=statistics.mean(ctx))
 
 

@@ -117,46 +117,85 @@ struct XPrep {
 };
 
 __global__ void __launch_bounds__(256) mla_exp_prep_kernel(XPrep p) {
+    // per-request metadata in smem (every CTA scans; n <= 1024 requests is a few hundred cycles)
     __shared__ int s_off[XMAXN + 1];
+    __shared__ int s_cu[XMAXN + 1];
     __shared__ int s_warp[8];
     x_scan(p.cu, p.prefix, p.n, s_off, s_warp);
-    if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i <= p.n; i += blockDim.x) p.hdr[i] = s_off[i];
+    for (int i = threadIdx.x; i <= p.n; i += blockDim.x) {
+        s_cu[i] = __ldg(p.cu + i);
+        if (blockIdx.x == 0) p.hdr[i] = s_off[i];
+    }
+    __syncthreads();
     const int R = s_off[p.n] * XBM;
     if (R > p.rows_cap) {  // the caller's max_total_keys was too small: write nothing
         if (threadIdx.x == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_INVALID);
         return;
     }
-    const int lane = threadIdx.x & 31;
+    const int T = s_cu[p.n];
     const int bs_mask = (1 << p.lg_bs) - 1;
     constexpr int RU = XDL * 2 / 16;  // 72 uint4 per latent row
-    for (int g = blockIdx.x * 8 + (threadIdx.x >> 5); g < R; g += gridDim.x * 8) {
-        const int i = x_find([&](int k) { return s_off[k]; }, p.n, g / XBM);
-        const int j = g - s_off[i] * XBM;
-        const int P = __ldg(p.prefix + i), c0 = __ldg(p.cu + i), nk = P + __ldg(p.cu + i + 1) - c0;
-        uint4* kd = p.kpe + (size_t)g * (XDR * 2 / 16);
-        const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
-        if (j >= nk) {
-            if (lane < 8) kd[lane] = zero;
-            continue;
-        }
-        const int page = j >> p.lg_bs;
-        const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
-        if (blk < 0 || blk >= p.N_B) {
-            if (lane == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
-            if (lane < 8) kd[lane] = zero;
-            continue;
-        }
-        uint4* prow = reinterpret_cast<uint4*>(p.pool + ((size_t)blk * (bs_mask + 1) + (j & bs_mask)) * (XDL * 2));
-        if (j >= P) {  // the chunk's own row: latent -> pool, k_pe -> Kpe
-            const uint4* src = p.kv_new + (size_t)(c0 + j - P) * RU;
-            for (int c = lane; c < RU; c += 32) {
-                const uint4 v = __ldg(src + c);
-                prow[c] = v;
-                if (c >= RU - 8) kd[c - (RU - 8)] = v;
+    constexpr int PU = XDR * 2 / 16;  // 8 uint4 of k_pe
+    const int nthr = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+    // 1. the chunk's latent rows -> pool pages: one 16-byte element per thread and step,
+    //    four independent elements in flight per thread
+    const int nA = T * RU;
+    for (int e0 = tid; e0 < nA; e0 += 4 * nthr) {
+        uint4 v[4];
+        uint4* dst[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * nthr;
+            dst[u] = nullptr;
+            if (e < nA) {
+                const int t = e / RU, c = e - t * RU;
+                const int i = x_find([&](int k) { return s_cu[k]; }, p.n, t);
+                const int j = __ldg(p.prefix + i) + t - s_cu[i];
+                const int page = j >> p.lg_bs;
+                const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
+                if (blk >= 0 && blk < p.N_B)
+                    dst[u] = reinterpret_cast<uint4*>(p.pool + ((size_t)blk * (bs_mask + 1) + (j & bs_mask)) * (XDL * 2)) + c;
+                else if (c == 0 && p.status)
+                    atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                v[u] = __ldg(p.kv_new + (size_t)t * RU + c);
             }
-        } else if (lane < 8) {
-            kd[lane] = prow[RU - 8 + lane];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (dst[u]) *dst[u] = v[u];
+    }
+    // 2. every key's k_pe -> Kpe [rows][64] (chunk keys from kv_new, prefix keys from the pool,
+    //    padding rows zero)
+    const int nB = R * PU;
+    for (int e0 = tid; e0 < nB; e0 += 4 * nthr) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * nthr;
+            v[u] = zero;
+            if (e < nB) {
+                const int g = e / PU, c = e - g * PU;
+                const int i = x_find([&](int k) { return s_off[k]; }, p.n, g / XBM);
+                const int j = g - s_off[i] * XBM;
+                const int P = __ldg(p.prefix + i), nk = P + s_cu[i + 1] - s_cu[i];
+                if (j >= P && j < nk) {
+                    v[u] = __ldg(p.kv_new + (size_t)(s_cu[i] + j - P) * RU + (RU - PU) + c);
+                } else if (j < P) {
+                    const int page = j >> p.lg_bs;
+                    const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
+                    if (blk >= 0 && blk < p.N_B)
+                        v[u] = reinterpret_cast<const uint4*>(p.pool + ((size_t)blk * (bs_mask + 1) + (j & bs_mask)) * (XDL * 2))[RU - PU + c];
+                    else if (c == 0 && p.status)
+                        atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * nthr;
+            if (e < nB) p.kpe[e] = v[u];
         }
     }
 }
@@ -479,9 +518,9 @@ __global__ void __launch_bounds__(ANT, 1)
             const uint32_t idesc_o = umma_idesc_bf16_f32(XBM, XDV, 1);
             const uint32_t idesc_o64 = umma_idesc_bf16_f32(XBM, 64, 1);
             int sc = 0, nunit = 0, cnt_a = 0, cnt_b = 0;
-            auto wait_slot = [&](int c) { mbar_wait(&sm.full[c % NSLOT], (c / NSLOT) & 1); };
+            auto wait_slot = [&](int c) { mbar_wait(&sm.full[c & (NSLOT - 1)], (c / NSLOT) & 1); };
             auto release = [&](int c0, int k) {
-                for (int e = 0; e < k; ++e) umma_commit_warp(&sm.empty[(c0 + e) % NSLOT]);
+                for (int e = 0; e < k; ++e) umma_commit_warp(&sm.empty[(c0 + e) & (NSLOT - 1)]);
             };
             for (;;) {
                 const int us = nunit & 1;
@@ -494,19 +533,27 @@ __global__ void __launch_bounds__(ANT, 1)
                 tc_fence_after();
                 const int nA = d.nkv[0], nB = d.nkv[1];
                 const uint32_t q_base = smem_u32(sm.q[0]);
+                const uint32_t ring_a = smem_u32(sm.ring[0]);
                 auto issue_s = [&](int t, int kc) {  // S_t = Q_t [k_nope | k_pe]^T, 12 x K16
+                    // descriptors formed once per call; the K16 steps add constant offsets
+                    // (16-byte units) to the start-address field
+                    const uint64_t qd = xk_desc(q_base + t * SLOT);
+                    uint64_t kd[3];
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) kd[ch] = xk_desc(ring_a + ((kc + ch) & (NSLOT - 1)) * SLOT);
 #pragma unroll
                     for (int kk = 0; kk < 12; ++kk) {
                         const int ch = kk >> 2;
-                        const uint32_t a = q_base + ch * QCH + t * SLOT + (kk & 3) * 32;
-                        const uint32_t b = smem_u32(sm.ring[(kc + ch) % NSLOT]) + (kk & 3) * 32;
-                        umma_ss_warp(tmem + (uint32_t)(t * XBM), xk_desc(a), xk_desc(b), idesc_s, kk > 0 ? 1u : 0u);
+                        umma_ss_warp(tmem + (uint32_t)(t * XBM), qd + (uint64_t)((ch * QCH + (kk & 3) * 32) >> 4),
+                                     kd[ch] + (uint64_t)(((kk & 3) * 32) >> 4), idesc_s, kk > 0 ? 1u : 0u);
                     }
                     umma_commit_warp(&sm.s_full[t]);
                 };
                 auto issue_pv = [&](int t, int& cnt, int vc, bool first) {  // O_t += P_t V
-                    const int s0 = vc % NSLOT, s1 = (vc + 1) % NSLOT;
-                    const uint32_t v0 = smem_u32(sm.ring[s0]), v1 = smem_u32(sm.ring[s1]);
+                    const int s0 = vc & (NSLOT - 1), s1 = (vc + 1) & (NSLOT - 1);
+                    const uint64_t vd0 = umma_desc_sw128(ring_a + s0 * SLOT, SLOT, 1024);
+                    const uint64_t vd1 = umma_desc_sw128(ring_a + s1 * SLOT, SLOT, 1024);
+                    const bool adj = s1 == s0 + 1;
                     const uint32_t p_tmem = tmem + (uint32_t)(t * XBM);
                     const uint32_t o_tmem = tmem + 256u + (uint32_t)(t * XDV);
 #pragma unroll
@@ -516,14 +563,12 @@ __global__ void __launch_bounds__(ANT, 1)
 #pragma unroll
                         for (int kk = hf * 8 / kXPvParts; kk < (hf + 1) * 8 / kXPvParts; ++kk) {
                             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-                            if (s1 == s0 + 1) {  // adjacent slots: one N = 128 MMA (LBO = slot pitch)
-                                umma_ts_warp(o_tmem, p_tmem + (uint32_t)(kk * 8),
-                                             umma_desc_sw128(v0 + kk * 2048, SLOT, 1024), idesc_o, acc);
+                            const uint64_t ko = (uint64_t)(kk * (2048 >> 4));
+                            if (adj) {  // adjacent slots: one N = 128 MMA (LBO = slot pitch)
+                                umma_ts_warp(o_tmem, p_tmem + (uint32_t)(kk * 8), vd0 + ko, idesc_o, acc);
                             } else {  // ring wrap: the two 64-column halves as N = 64 MMAs
-                                umma_ts_warp(o_tmem, p_tmem + (uint32_t)(kk * 8),
-                                             umma_desc_sw128(v0 + kk * 2048, SLOT, 1024), idesc_o64, acc);
-                                umma_ts_warp(o_tmem + 64u, p_tmem + (uint32_t)(kk * 8),
-                                             umma_desc_sw128(v1 + kk * 2048, SLOT, 1024), idesc_o64, acc);
+                                umma_ts_warp(o_tmem, p_tmem + (uint32_t)(kk * 8), vd0 + ko, idesc_o64, acc);
+                                umma_ts_warp(o_tmem + 64u, p_tmem + (uint32_t)(kk * 8), vd1 + ko, idesc_o64, acc);
                             }
                         }
                     }
@@ -781,7 +826,9 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     pp.rows_cap = (long long)rows;
     const int max_mt = (int)((rows + XBM - 1) / XBM);
     int gprep = budget > 0 ? budget : pool->num_sms;
-    const int prep_need = (int)((rows + 7) / 8);
+    const size_t prep_elems = (size_t)total_q * (XDL * 2 / 16) > rows * (XDR * 2 / 16)
+                                  ? (size_t)total_q * (XDL * 2 / 16) : rows * (XDR * 2 / 16);
+    const int prep_need = (int)((prep_elems + 1023) / 1024);
     if (gprep > prep_need) gprep = prep_need;
     mla_exp_prep_kernel<<<gprep, 256, 0, st>>>(pp);
     pool->launches += 1;

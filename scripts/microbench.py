@@ -233,14 +233,34 @@ def mla_exp(args, dev):
     f_gemm = 2 * (C + P) * 512 * 2 * H * 128
     f_abs = 2 * H * (576 + 512) * pairs
     spans = torch.zeros(2, 8, dtype=torch.int64, device=dev)
+    cu_t, rid_t, pre_t = i32([0, C]), i32([0]), i32([P])
     for bud in [int(x) for x in args.budgets.split(",")]:
-        run = lambda l: pool.prefill_mla_expanded(l, q, kv, w_uk[l], w_uv[l], i32([0, C]), i32([0]),  # noqa: E731
-                                                  i32([P]), C, C, C + P, 1 / math.sqrt(192), out, ws,
+        run = lambda l: pool.prefill_mla_expanded(l, q, kv, w_uk[l], w_uv[l], cu_t, rid_t,  # noqa: E731
+                                                  pre_t, C, C, C + P, 1 / math.sqrt(192), out, ws,
                                                   sm_budget=bud)
         for l in range(min(L, 2)):
             run(l)
         torch.cuda.synchronize()
         ms, _ = timed_ms(run, args.iters, L)
+        # the same calls captured into a CUDA graph (no host work between launches: the bench's
+        # co-run step is graph-replayed too)
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(torch.cuda.current_stream(dev))
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            for it in range(L):
+                pool.prefill_mla_expanded(it, q, kv, w_uk[it], w_uv[it], cu_t, rid_t,
+                                          pre_t, C, C, C + P, 1 / math.sqrt(192), out, ws,
+                                          sm_budget=bud, stream=gs)
+        graph.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms_graph = e0.elapsed_time(e1) / (5 * L)
         spans.zero_()
         pool.set_spans(spans)
         for it in range(args.iters):
@@ -251,6 +271,7 @@ def mla_exp(args, dev):
         gms = float(sp[0, 2]) / max(1, int(sp[0, 3])) / 1e6
         ams = float(sp[1, 2]) / max(1, int(sp[1, 3])) / 1e6
         print(json.dumps({"kernel": "prefill_mla_expanded", "budget": bud, "C": C, "P": P, "ms": ms,
+                          "ms_graph": ms_graph, "TFLOP_s_graph": (f_gemm + f_attn) / (ms_graph / 1e3) / 1e12,
                           "gemm_ms": gms, "attn_ms": ams,
                           "gemm_TFLOP_s": f_gemm / (gms / 1e3) / 1e12 if gms > 0 else None,
                           "attn_TFLOP_s": f_attn / (ams / 1e3) / 1e12 if ams > 0 else None,

@@ -45,24 +45,72 @@ constexpr int XBM = 128;            // q rows per tile, keys per kv tile, key ro
 constexpr int XMAXN = 1024;         // requests per call
 constexpr float XLOG2E = 1.4426950408889634f;
 
-// ------------------------------------------------------------------ workspace
-// [hdr: int mtoff[n + 1] (128-row tile offset of each request's keys)] [K_exp rows x H x 128]
-// [V_exp rows x H x 128] [Kpe rows x 64], rows = max_total_keys + 128 n (per-request padding)
-size_t x_hdr_bytes(int n) { return spd_al256(sizeof(int) * (size_t)(n + 1)); }
-size_t x_rows(int n, int max_keys) { return (size_t)max_keys + (size_t)XBM * (size_t)n; }
-size_t x_ws_bytes(int n, int max_keys, int H) {
-    const size_t r = x_rows(n, max_keys);
-    return x_hdr_bytes(n) + spd_al256(r * H * XDN * 2) + spd_al256(r * H * XDV * 2) + spd_al256(r * XDR * 2);
+// ------------------------------------------------------------------ kv split of long units
+// SPD_X_SPLIT_MIN = k (a compile switch, OFF by default): a unit (request, pair of q tiles, head)
+// whose tile B needs >= k kv tiles runs as two parts over kv tiles [0, h) and [h, nB), h = nB / 2,
+// on two CTAs; the part that finishes first stores its unnormalised O rows with (m, l), the
+// second merges them with its own in TMEM (x_split_epilogue; weights and sum formed without
+// contraction, so bitwise independent of which part came first).  The rule depends on shapes
+// only (R26).  Parity-green (tests/test_gpu_mla_expanded.py, 30/30 at k = 10), but measured
+// slower (profiles/r2_mla_expanded_split_ab.log, C = 2048): splitting alone shortens the
+// critical path (-18 % at 148 SMs, P = 0, with the merge stubbed out), but the merge handshake
+// (partial store, release / acquire flag, partial load) stalls both parts' pipelines: +17 % at
+// 148 SMs and +52 % at 44 SMs with it.
+#ifndef SPD_X_SPLIT_MIN
+#define SPD_X_SPLIT_MIN 1000000
+#endif
+constexpr int XSPLIT_MIN = SPD_X_SPLIT_MIN;
+constexpr bool kXSplit = XSPLIT_MIN < 1000000;
+#ifndef SPD_X_RESCALE16
+#define SPD_X_RESCALE16 1
+#endif
+constexpr int XPROW = XDV + 4;  // floats per stored partial row: O[128], m, l, pad
+__host__ __device__ __forceinline__ int x_pair_nkv(int P, int C, int pair) {  // kv tiles of tile B
+    const int last = min(C, (pair + 1) * 2 * XBM);  // chunk rows of the pair's end
+    return (P + last - 1) / XBM + 1;
+}
+__host__ __device__ __forceinline__ int x_split_pairs(int P, int C) {  // pairs that split
+    const int pairs = (C + 2 * XBM - 1) / (2 * XBM);
+    int k = 0;
+    for (int pr = 0; pr < pairs; ++pr) k += x_pair_nkv(P, C, pr) >= XSPLIT_MIN;
+    return k;
+}
+__host__ __device__ __forceinline__ int x_first_split_pair(int P, int C) {
+    const int pairs = (C + 2 * XBM - 1) / (2 * XBM);
+    int pr = 0;
+    while (pr < pairs && x_pair_nkv(P, C, pr) < XSPLIT_MIN) ++pr;
+    return pr;
 }
 
-// s_off[i] = sum_{i' < i} ceil((P_i' + C_i') / 128) (exclusive scan over the block; every
-// thread takes a contiguous range of requests)
-__device__ void x_scan(const int* cu, const int* prefix, int n, int* s_off, int* s_warp) {
+// ------------------------------------------------------------------ workspace
+// [hdr: int mtoff[n + 1] (128-row tile offset of each request's keys), int sbase[n + 1] (split
+// pair offset)] [K_exp rows x H x 128] [V_exp rows x H x 128] [Kpe rows x 64]
+// [split counters: slots x 2 tiles x (role counter, flag) int] [partials: slots x 2 tiles x 128 rows
+// x XPROW fp32 (the first part's rows)],
+// rows = max_total_keys + 128 n (per-request padding), slots = (max_total_keys / 256 + n) x H
+// (a split pair has >= 1 chunk row per 256, so the call has at most total_q / 256 + n of them)
+size_t x_hdr_bytes(int n) { return spd_al256(sizeof(int) * 2 * (size_t)(n + 1)); }
+size_t x_rows(int n, int max_keys) { return (size_t)max_keys + (size_t)XBM * (size_t)n; }
+size_t x_slots(int n, int max_keys, int H) {
+    return kXSplit ? ((size_t)max_keys / (2 * XBM) + (size_t)n) * (size_t)H : 0;
+}
+size_t x_cnt_bytes(size_t slots) { return spd_al256(slots * 2 * 2 * sizeof(int)); }
+size_t x_part_bytes(size_t slots) { return spd_al256(slots * 2 * XBM * XPROW * sizeof(float)); }
+size_t x_ws_bytes(int n, int max_keys, int H) {
+    const size_t r = x_rows(n, max_keys), sl = x_slots(n, max_keys, H);
+    return x_hdr_bytes(n) + spd_al256(r * H * XDN * 2) + spd_al256(r * H * XDV * 2) + spd_al256(r * XDR * 2) +
+           x_cnt_bytes(sl) + x_part_bytes(sl);
+}
+
+// s_off[i] = sum_{i' < i} val(i') (exclusive scan over the block; every thread takes a
+// contiguous range of requests)
+template <typename V>
+__device__ void x_scan(V val, int n, int* s_off, int* s_warp) {
     const int T = blockDim.x, tid = threadIdx.x;
     const int per = (n + T - 1) / T;
     const int a = min(n, tid * per), b = min(n, a + per);
     int sum = 0;
-    for (int i = a; i < b; ++i) sum += (__ldg(prefix + i) + __ldg(cu + i + 1) - __ldg(cu + i) + XBM - 1) / XBM;
+    for (int i = a; i < b; ++i) sum += val(i);
     const int lane = tid & 31, w = tid >> 5;
     int inc = sum;
 #pragma unroll
@@ -84,7 +132,7 @@ __device__ void x_scan(const int* cu, const int* prefix, int n, int* s_off, int*
     int run = s_warp[w] + inc - sum;  // exclusive prefix of this thread's range
     if (tid == 0) s_off[0] = 0;
     for (int i = a; i < b; ++i) {
-        run += (__ldg(prefix + i) + __ldg(cu + i + 1) - __ldg(cu + i) + XBM - 1) / XBM;
+        run += val(i);
         s_off[i + 1] = run;
     }
     __syncthreads();
@@ -112,8 +160,10 @@ struct XPrep {
     uint4* kpe;              // [rows][64] bf16
     int* hdr;
     int* status;
-    int n, lg_bs, MBR, N_B;
+    int n, lg_bs, MBR, N_B, H;
     long long rows_cap;  // workspace rows (max_total_keys + 128 n)
+    long long slots_cap; // split slots of the workspace
+    int* cnt;            // split counters / flags [slots][2][2]
 };
 
 __global__ void __launch_bounds__(256) mla_exp_prep_kernel(XPrep p) {
@@ -121,14 +171,24 @@ __global__ void __launch_bounds__(256) mla_exp_prep_kernel(XPrep p) {
     __shared__ int s_off[XMAXN + 1];
     __shared__ int s_cu[XMAXN + 1];
     __shared__ int s_warp[8];
-    x_scan(p.cu, p.prefix, p.n, s_off, s_warp);
+    const int* cu = p.cu;
+    const int* prefix = p.prefix;
+    // split-pair offsets first (s_off is reused for the tile offsets below)
+    x_scan([&](int i) { return x_split_pairs(__ldg(prefix + i), __ldg(cu + i + 1) - __ldg(cu + i)); },
+           p.n, s_off, s_warp);
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i <= p.n; i += blockDim.x) p.hdr[p.n + 1 + i] = s_off[i];
+    const long long n_slots = (long long)s_off[p.n] * p.H;
+    __syncthreads();
+    x_scan([&](int i) { return (__ldg(prefix + i) + __ldg(cu + i + 1) - __ldg(cu + i) + XBM - 1) / XBM; },
+           p.n, s_off, s_warp);
     for (int i = threadIdx.x; i <= p.n; i += blockDim.x) {
         s_cu[i] = __ldg(p.cu + i);
         if (blockIdx.x == 0) p.hdr[i] = s_off[i];
     }
     __syncthreads();
     const int R = s_off[p.n] * XBM;
-    if (R > p.rows_cap) {  // the caller's max_total_keys was too small: write nothing
+    if (R > p.rows_cap || n_slots > p.slots_cap) {  // max_total_keys was too small: write nothing
         if (threadIdx.x == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_INVALID);
         return;
     }
@@ -139,6 +199,7 @@ __global__ void __launch_bounds__(256) mla_exp_prep_kernel(XPrep p) {
     const int nthr = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+    for (long long k = tid; k < 4 * n_slots; k += nthr) p.cnt[k] = 0;  // this call's split counters / flags
     // 1. the chunk's latent rows -> pool pages: one 16-byte element per thread and step,
     //    four independent elements in flight per thread
     const int nA = T * RU;
@@ -379,7 +440,10 @@ constexpr int kXPvParts = 4;
 
 struct XUnit {
     int i, h, t0, P, qrow0, krow0;
-    int tv[2], nkv[2];
+    int tv[2], nkv[2];  // nkv[t]: one past the last kv tile of tile t in this part
+    int kv0;            // first kv tile of this part
+    int slot;           // split slot (-1: unsplit unit)
+    int part;
 };
 
 struct ASmem {
@@ -391,6 +455,7 @@ struct ASmem {
     uint64_t o_full[2], o_empty[2];
     uint64_t ufull[2], uempty[2];
     XUnit units[2];
+    int role[2];  // per softmax warpgroup: the split counter's old value
     uint32_t tmem_base;
 };
 
@@ -402,10 +467,92 @@ struct XAttn {
     int* status;
     unsigned long long* span;
     unsigned* sched;
+    float* part;  // split partials [slots][2 tiles][128 rows][XPROW]
+    int* cnt;     // split counters [slots][2 tiles][role counter, flag]
     int n, T, H, pairs_max, n_units;
     float scale_log2;
     SpdTrace trace;
 };
+
+// Epilogue of one split part.  The warpgroup's thread 0 takes a role from the slot's counter:
+// the part that arrives first stores its unnormalised O rows (relative to 2^m) with (m, l) to
+// rows[r] and raises the slot's flag (release); the second waits for the flag (acquire), reads
+// those rows and merges them with its own O (still in TMEM).  Both weights and the sum are
+// formed without contraction, so the result does not depend on which part came first.  TMEM's
+// O is released (o_empty) as soon as this warpgroup has read it.
+__device__ __forceinline__ void x_split_epilogue(float* rows, int* ctr, int* role, uint64_t* o_empty,
+                                                 uint32_t o_tmem, int r, int t, float m, float l, bool valid,
+                                                 uint4* dst) {
+    if (r == 0) *role = atomicAdd(ctr, 1);
+    named_bar_sync(2 + t, 128);
+    const int rl = *role;
+    float4* row = reinterpret_cast<float4*>(rows + (size_t)r * XPROW);
+    if (rl == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(o_tmem + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+                row[c * 8 + e / 4] = make_float4(__uint_as_float(o[e]), __uint_as_float(o[e + 1]),
+                                                 __uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
+        }
+        tc_fence_before();
+        mbar_arrive(o_empty);
+        row[XDV / 4] = make_float4(m, l, 0.f, 0.f);
+        named_bar_sync(2 + t, 128);
+        if (r == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ctr + 1), "r"(1) : "memory");
+        }
+        return;
+    }
+    if (r == 0) {
+        int f = 0;
+        do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(ctr + 1) : "memory");
+            if (!f) __nanosleep(64);
+        } while (!f);
+    }
+    named_bar_sync(2 + t, 128);
+    const float4 ml = __ldcg(row + XDV / 4);
+    const float mm = fmaxf(ml.x, m);
+    const float fo = fast_exp2(ml.x - mm), fm = fast_exp2(m - mm);
+    const float inv = 1.f / __fadd_rn(__fmul_rn(ml.y, fo), __fmul_rn(l, fm));
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        float4 ot[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ot[k] = __ldcg(row + c * 8 + k);
+        uint32_t o[32];
+        tmem_ld32(o_tmem + c * 32, o);
+        tmem_wait_ld();
+        if (c == 3) {
+            tc_fence_before();
+            mbar_arrive(o_empty);
+        }
+        auto mg = [&](float mine, float other) {
+            return __fmul_rn(__fadd_rn(__fmul_rn(mine, fm), __fmul_rn(other, fo)), inv);
+        };
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) {
+                const float* a = reinterpret_cast<const float*>(&ot[k]);
+                uint4 v;
+                v.x = pack_bf16(mg(__uint_as_float(o[4 * k + 0]), a[0]), mg(__uint_as_float(o[4 * k + 1]), a[1]));
+                v.y = pack_bf16(mg(__uint_as_float(o[4 * k + 2]), a[2]), mg(__uint_as_float(o[4 * k + 3]), a[3]));
+                v.z = pack_bf16(mg(__uint_as_float(o[4 * k + 4]), a[4]), mg(__uint_as_float(o[4 * k + 5]), a[5]));
+                v.w = pack_bf16(mg(__uint_as_float(o[4 * k + 6]), a[6]), mg(__uint_as_float(o[4 * k + 7]), a[7]));
+                dst[c * 4 + k / 2] = v;
+            }
+        }
+    }
+    if (r == 0) {  // ready for the next call
+        ctr[0] = 0;
+        ctr[1] = 0;
+    }
+}
 
 __global__ void __launch_bounds__(ANT, 1)
     mla_exp_attn_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kxmap,
@@ -463,8 +610,11 @@ __global__ void __launch_bounds__(ANT, 1)
                 if (lane == 0) u = (int)atomicAdd(p.sched, 1u);
                 u = __shfl_sync(0xffffffffu, u, 0);
                 if (u < p.n_units) {
+                    // u -> (slot v = (pair, part), request, head); LPT: last pairs first
                     const int per_pair = p.n * p.H;
-                    const int pair = p.pairs_max - 1 - u / per_pair;  // LPT: last pairs first
+                    const int v = u / per_pair;
+                    const int pair = p.pairs_max - 1 - (kXSplit ? v >> 1 : v);
+                    const int part = kXSplit ? v & 1 : 0;
                     d.i = (u / p.H) % p.n;
                     d.h = u % p.H;
                     const int c0 = __ldg(p.cu + d.i), C = __ldg(p.cu + d.i + 1) - c0;
@@ -473,8 +623,24 @@ __global__ void __launch_bounds__(ANT, 1)
                     d.tv[0] = min(XBM, C - d.t0);
                     d.tv[1] = max(0, min(XBM, C - d.t0 - XBM));
                     d.P = __ldg(p.prefix + d.i);
-                    d.nkv[0] = (d.P + d.t0 + d.tv[0] - 1) / XBM + 1;
-                    d.nkv[1] = d.tv[1] > 0 ? (d.P + d.t0 + XBM + d.tv[1] - 1) / XBM + 1 : d.nkv[0];
+                    const int nA = (d.P + d.t0 + d.tv[0] - 1) / XBM + 1;
+                    const int nB = d.tv[1] > 0 ? (d.P + d.t0 + XBM + d.tv[1] - 1) / XBM + 1 : nA;
+                    const bool split = x_pair_nkv(d.P, C, pair) >= XSPLIT_MIN;
+                    if (!split && part) continue;
+                    d.part = part;
+                    if (split) {  // nB >= 10 and nA >= nB - 1: both tiles keep >= 1 kv tile per part
+                        const int hk = nB / 2;
+                        d.kv0 = part ? hk : 0;
+                        d.nkv[0] = part ? nA : hk;
+                        d.nkv[1] = part ? nB : hk;
+                        const int sb = __ldg(p.hdr + p.n + 1 + d.i) + pair - x_first_split_pair(d.P, C);
+                        d.slot = sb * p.H + d.h;
+                    } else {
+                        d.kv0 = 0;
+                        d.nkv[0] = nA;
+                        d.nkv[1] = nB;
+                        d.slot = -1;
+                    }
                     d.qrow0 = c0 + d.t0;
                     d.krow0 = __ldg(p.hdr + d.i) * XBM;
                 }
@@ -492,7 +658,7 @@ __global__ void __launch_bounds__(ANT, 1)
                     tma_load_4d(sm.q[0], &qmap, &sm.q_full, 0, d.h, d.qrow0, 0);
                 }
                 ++nunit;
-                for (int j = 0; j < d.nkv[1]; ++j) {
+                for (int j = d.kv0; j < d.nkv[1]; ++j) {
                     const int krow = d.krow0 + j * XBM;
                     // kv tile j = K slots (k_nope cols 0-63, 64-127, k_pe) then V slots (0-63, 64-127)
 #pragma unroll 1
@@ -574,32 +740,32 @@ __global__ void __launch_bounds__(ANT, 1)
                     }
                     ++cnt;
                 };
-                const int c0 = sc;
+                const int c0 = sc, j0 = d.kv0;
                 for (int e = 0; e < 3; ++e) wait_slot(c0 + e);
                 tc_fence_after();
                 issue_s(0, c0);
                 issue_s(1, c0);
                 release(c0, 3);
-                if (nB == 1) umma_commit_warp(&sm.q_empty);
-                for (int j = 0; j < nB; ++j) {
-                    const int vc = c0 + 5 * j + 3;
+                if (nB - j0 == 1) umma_commit_warp(&sm.q_empty);
+                for (int j = j0; j < nB; ++j) {
+                    const int vc = c0 + 5 * (j - j0) + 3;
                     wait_slot(vc);
                     wait_slot(vc + 1);
                     tc_fence_after();
                     if (j < nA) {
-                        if (j == 0) mbar_wait(&sm.o_empty[0], (nunit & 1) ^ 1);
-                        issue_pv(0, cnt_a, vc, j == 0);
+                        if (j == j0) mbar_wait(&sm.o_empty[0], (nunit & 1) ^ 1);
+                        issue_pv(0, cnt_a, vc, j == j0);
                         if (j == nA - 1) umma_commit_warp(&sm.o_full[0]);
                     }
                     const bool more = j + 1 < nB;
-                    const int kn = c0 + 5 * (j + 1);
+                    const int kn = c0 + 5 * (j + 1 - j0);
                     if (more) {
                         for (int e = 0; e < 3; ++e) wait_slot(kn + e);
                         tc_fence_after();
                     }
                     if (j + 1 < nA) issue_s(0, kn);
-                    if (j == 0) mbar_wait(&sm.o_empty[1], (nunit & 1) ^ 1);
-                    issue_pv(1, cnt_b, vc, j == 0);
+                    if (j == j0) mbar_wait(&sm.o_empty[1], (nunit & 1) ^ 1);
+                    issue_pv(1, cnt_b, vc, j == j0);
                     release(vc, 2);
                     if (j == nB - 1) umma_commit_warp(&sm.o_full[1]);
                     if (more) {
@@ -608,7 +774,7 @@ __global__ void __launch_bounds__(ANT, 1)
                         if (j + 1 == nB - 1) umma_commit_warp(&sm.q_empty);
                     }
                 }
-                sc = c0 + 5 * nB;
+                sc = c0 + 5 * (nB - j0);
                 ++nunit;
             }
         }
@@ -627,15 +793,20 @@ __global__ void __launch_bounds__(ANT, 1)
         for (;;) {
             const int us = nunit & 1;
             mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
-            const XUnit d = sm.units[us];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.uempty[us]);
-            if (d.i < 0) break;
-            const int trel = d.t0 + t * XBM + r;  // chunk-relative token of this row
-            const int nkv = d.nkv[t];
+            // the loop's fields now; the epilogue's are re-read from smem after the loop (fewer
+            // registers live across it) and the unit slot is released after that read
+            const XUnit& du = sm.units[us];
+            if (du.i < 0) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.uempty[us]);
+                break;
+            }
+            const int kv0 = du.kv0, dP = du.P;
+            const int trel = du.t0 + t * XBM + r;  // chunk-relative token of this row
+            const int nkv = du.nkv[t];
             float m = -INFINITY;
             uint64_t l2 = f2(0.f, 0.f);
-            for (int j = 0; j < nkv; ++j, ++cnt) {
+            for (int j = kv0; j < nkv; ++j, ++cnt) {
                 mbar_wait(&sm.s_full[t], cnt & 1);
                 tc_fence_after();
                 uint32_t sr[4][32];
@@ -643,7 +814,7 @@ __global__ void __launch_bounds__(ANT, 1)
                 for (int c = 0; c < 4; ++c) tmem_ld32(s_tmem + c * 32, sr[c]);
                 tmem_wait_ld();
                 // causal, bottom-right aligned: key j * 128 + c <= P + trel
-                const int lim = d.P + trel - j * XBM;
+                const int lim = dP + trel - j * XBM;
                 if (lim < XBM - 1) {
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
@@ -662,10 +833,26 @@ __global__ void __launch_bounds__(ANT, 1)
                 const float mx = fmaxf(fmaxf(mxc[0], mxc[1]), fmaxf(mxc[2], mxc[3]));
                 const float mtrue = fmaxf(m, mx * tsc);
                 // lazy rescale (R21): the reference max moves only when exceeded by > 8 (log2)
-                const bool move = j == 0 || mtrue > m + 8.f;
-                if (j > 0 && __any_sync(0xffffffffu, move)) {
+                const bool move = j == kv0 || mtrue > m + 8.f;
+                if (j > kv0 && __any_sync(0xffffffffu, move)) {
                     const float alpha = move ? fast_exp2(m - mtrue) : 1.f;
                     const uint64_t a2 = f2(alpha, alpha);
+#if SPD_X_RESCALE16
+#pragma unroll 1
+                    for (int c = 0; c < 8; ++c) {  // 16 columns at a time (registers: S is live)
+                        uint32_t o[16];
+                        tmem_ld16(o_tmem + c * 16, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 16; e += 2) {
+                            float lo, hi;
+                            f2_split(fmul2(f2(__uint_as_float(o[e]), __uint_as_float(o[e + 1])), a2), lo, hi);
+                            o[e] = __float_as_uint(lo);
+                            o[e + 1] = __float_as_uint(hi);
+                        }
+                        tmem_st16(o_tmem + c * 16, o);
+                    }
+#else
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         uint32_t o[32];
@@ -680,6 +867,7 @@ __global__ void __launch_bounds__(ANT, 1)
                         }
                         tmem_st32(o_tmem + c * 32, o);
                     }
+#endif
                     l2 = fmul2(l2, a2);
                 }
                 if (move) m = mtrue;
@@ -715,30 +903,45 @@ __global__ void __launch_bounds__(ANT, 1)
             // ---- epilogue: O / l -> bf16 -> out [T][H][128] (each thread its 256-byte row)
             mbar_wait(&sm.o_full[t], nunit & 1);
             tc_fence_after();
+            XUnit d;
+            d.tv[t] = du.tv[t];
+            d.qrow0 = du.qrow0;
+            d.h = du.h;
+            d.slot = du.slot;
+            d.part = du.part;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.uempty[us]);
             float la, lb;
             f2_split(l2, la, lb);
-            const float inv = 1.f / (la + lb);
             const bool valid = r < d.tv[t];
             uint4* dst = reinterpret_cast<uint4*>(p.out + ((size_t)(d.qrow0 + t * XBM + r) * p.H + d.h) * XDV);
+            if (d.slot < 0) {
+                const float inv = 1.f / (la + lb);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t o[32];
-                tmem_ld32(o_tmem + c * 32, o);
-                tmem_wait_ld();
-                if (valid) {
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32(o_tmem + c * 32, o);
+                    tmem_wait_ld();
+                    if (valid) {
 #pragma unroll
-                    for (int e = 0; e < 32; e += 8) {
-                        uint4 v;
-                        v.x = pack_bf16(__uint_as_float(o[e + 0]) * inv, __uint_as_float(o[e + 1]) * inv);
-                        v.y = pack_bf16(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
-                        v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
-                        v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
-                        dst[c * 4 + e / 8] = v;
+                        for (int e = 0; e < 32; e += 8) {
+                            uint4 v;
+                            v.x = pack_bf16(__uint_as_float(o[e + 0]) * inv, __uint_as_float(o[e + 1]) * inv);
+                            v.y = pack_bf16(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+                            v.z = pack_bf16(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+                            v.w = pack_bf16(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+                            dst[c * 4 + e / 8] = v;
+                        }
                     }
                 }
+            } else {
+                x_split_epilogue(p.part + (size_t)(d.slot * 2 + t) * XBM * XPROW, p.cnt + (d.slot * 2 + t) * 2,
+                                 &sm.role[t], &sm.o_empty[t], o_tmem, r, t, m, la + lb, valid, dst);
             }
-            tc_fence_before();
-            mbar_arrive(&sm.o_empty[t]);
+            if (d.slot < 0) {
+                tc_fence_before();
+                mbar_arrive(&sm.o_empty[t]);
+            }
             ++nunit;
         }
     }
@@ -806,6 +1009,9 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
                                                            spd_al256(rows * H * XDN * 2));
     __nv_bfloat16* kpe = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<unsigned char*>(vexp) +
                                                           spd_al256(rows * H * XDV * 2));
+    const size_t slots = x_slots(n, max_total_keys, H);
+    int* cnt = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(kpe) + spd_al256(rows * XDR * 2));
+    float* part = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(cnt) + x_cnt_bytes(slots));
     const int lg_bs = __builtin_ctz((unsigned)c.block_size);
 
     // 1. prep: chunk latent rows -> pool, k_pe -> Kpe, row offsets -> hdr
@@ -824,6 +1030,9 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     pp.MBR = c.max_blocks_per_req;
     pp.N_B = c.num_blocks;
     pp.rows_cap = (long long)rows;
+    pp.slots_cap = (long long)slots;
+    pp.cnt = cnt;
+    pp.H = H;
     const int max_mt = (int)((rows + XBM - 1) / XBM);
     int gprep = budget > 0 ? budget : pool->num_sms;
     const size_t prep_elems = (size_t)total_q * (XDL * 2 / 16) > rows * (XDR * 2 / 16)
@@ -892,10 +1101,12 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     ap.H = H;
     ap.pairs_max = (max_chunk_len + 2 * XBM - 1) / (2 * XBM);
     if (ap.pairs_max < 1) return SEMIPD_OK;
-    const long long units = (long long)n * ap.pairs_max * H;
+    const long long units = (long long)n * ap.pairs_max * H * (kXSplit ? 2 : 1);  // x 2: split parts
     if (units > (1LL << 30)) return SEMIPD_ERR_UNSUPPORTED;
     ap.n_units = (int)units;
     ap.scale_log2 = softmax_scale * XLOG2E;
+    ap.part = part;
+    ap.cnt = cnt;
     ap.trace = spd_trace(pool);
     CUtensorMap qmap, kxmap, vxmap, pemap;
     {

@@ -187,7 +187,7 @@ class Scheduler:
 class CoRunEngine:
     def __init__(self, pool: KVPool, num_q_heads: int, scale: float, *, chunk_budget: int = 2048,
                  max_decode: int = 512, partition=(50.0, 50.0), seed: int = 0,
-                 max_ctx: int = 8192 + 2048):
+                 max_ctx: int = 8192 + 2048, mla_expanded: bool = False):
         c = pool.cfg
         self.pool, self.c = pool, c
         self.dev = pool.device
@@ -204,14 +204,24 @@ class CoRunEngine:
         dk, dv = c.head_dim_k, c.head_dim_v
         bf = torch.bfloat16
         rnd = lambda *s: torch.randn(*s, device=self.dev, generator=g).to(bf)  # noqa: E731
-        self.q_pre = rnd(chunk_budget, num_q_heads, dk)
+        # expanded-form MLA prefill (include/semipd.h semipd_prefill_mla_expanded, reading R32):
+        # q [T, H, 192], the chunk's latent rows [T, 576], per-layer up-projections W_UK / W_UV
+        # [H, 128, 512] (random, scaled to unit-size outputs); out [T, H, 128]
+        self.mla_exp = mla_expanded
+        if mla_expanded:
+            assert c.kv_shared and dk == 576
+            self.w_uk = [(rnd(num_q_heads, 128, 512).float() / 512 ** 0.5).to(bf) for _ in range(self.L)]
+            self.w_uv = [(rnd(num_q_heads, 128, 512).float() / 512 ** 0.5).to(bf) for _ in range(self.L)]
+            self.ws_exp, self.ws_exp_cap = None, (0, 0)
+        self.q_pre = rnd(chunk_budget, num_q_heads, 192 if mla_expanded else dk)
         self.k_pre = rnd(chunk_budget, c.num_kv_heads, dk)
         self.v_pre = None if c.kv_shared else rnd(chunk_budget, c.num_kv_heads, dv)
         self.q_dec = rnd(max_decode, num_q_heads, dk)
         self.k_dec = rnd(max_decode, c.num_kv_heads, dk)
         self.v_dec = None if c.kv_shared else rnd(max_decode, c.num_kv_heads, dv)
         # layer 0 writes its own outputs (kept for parity sampling); other layers share one
-        self.o_pre = [torch.empty(chunk_budget, num_q_heads, dv, dtype=bf, device=self.dev)
+        dv_pre = 128 if mla_expanded else dv
+        self.o_pre = [torch.empty(chunk_budget, num_q_heads, dv_pre, dtype=bf, device=self.dev)
                       for _ in range(2)]
         self.o_dec = [torch.empty(max_decode, num_q_heads, dv, dtype=bf, device=self.dev)
                       for _ in range(2)]
@@ -280,7 +290,24 @@ class CoRunEngine:
         ev_alloc.record(self.sCtl)
         T = cu[-1]
         max_chunk = max((ch for _, ch, _ in plan.prefill), default=0)
-        if n_p:
+        if n_p and self.mla_exp:
+            keys = sum(ch + pf for _, ch, pf in plan.prefill)
+            if self.ws_exp is None or n_p > self.ws_exp_cap[0] or keys > self.ws_exp_cap[1]:
+                cap = (max(n_p, 2 * self.ws_exp_cap[0], 8), max(keys, 2 * self.ws_exp_cap[1], 4096))
+                torch.cuda.synchronize(self.dev)  # earlier iterations may still read the old one
+                self.ws_exp = pool.new_mla_expanded_workspace(cap[0], cap[1], self.Hq)
+                self.ws_exp_cap = cap
+            self.sP.wait_event(ev_alloc)
+            ev["p0"].record(self.sP)
+            for l in range(self.L):
+                pool.prefill_mla_expanded(l, self.q_pre[:T], self.k_pre[:T, 0], self.w_uk[l],
+                                          self.w_uv[l], view("cu", n_p + 1), view("prid", n_p),
+                                          view("pre", n_p), T, max_chunk, keys, 1 / 192 ** 0.5,
+                                          self.o_pre[min(l, 1)][:T], self.ws_exp,
+                                          status=self.status[st_i + l:st_i + l + 1], stream=self.sP)
+            st_i += self.L
+            ev["p1"].record(self.sP)
+        elif n_p:
             self.sP.wait_event(ev_alloc)
             ev["p0"].record(self.sP)
             for l in range(self.L):

@@ -1,0 +1,8 @@
+cd /root/repo
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/s3s_build.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_mla_expanded.py -q -x > gpurun_out/s3s_test.log 2>&1; echo "pytest rc $?"
+tail -3 gpurun_out/s3s_test.log
+timeout 300 python scripts/microbench.py --mla-exp --budgets 44,74,104,148 --layers 4 > gpurun_out/s3s_micro.jsonl 2>&1; echo "micro rc $?"
+timeout 300 python scripts/microbench.py --mla-exp --budgets 74,148 --layers 4 --prefix 4096 >> gpurun_out/s3s_micro.jsonl 2>&1
+cat gpurun_out/s3s_micro.jsonl
+timeout 900 python scripts/bench_field.py cfg5_mla_expanded > gpurun_out/s3s_field.jsonl 2> gpurun_out/s3s_field.err; echo "field rc $?"

@@ -78,6 +78,8 @@ def main():
     ap.add_argument("--samples", type=int, default=10)
     ap.add_argument("--max-iters", type=int, default=100000)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--expanded", action="store_true",
+                    help="expanded-form MLA prefill (semipd_prefill_mla_expanded, reading R32)")
     ap.add_argument("--controller", action="store_true",
                     help="N1: adjust (x, y) every --window iterations with Alg. 1 + the Eq. 4 fit")
     ap.add_argument("--window", type=int, default=100)
@@ -94,7 +96,9 @@ def main():
     g.manual_seed(5)
     for l in range(L):
         pool.views(l)[0].normal_(generator=g)
-    eng = CoRunEngine(pool, Hq, shape.softmax_scale, partition=(args.x, 100.0 - args.x), seed=5)
+    eng = CoRunEngine(pool, Hq, shape.softmax_scale, partition=(args.x, 100.0 - args.x), seed=5,
+                      mla_expanded=args.expanded)
+    pre_keys = 0  # sum over iterations of the prefill calls' keys (P + C), for the expanded flops
     trace = synth.mla_trace(args.requests, args.lam, seed=5)
     last_arrival = trace[-1].arrival_iter
     sample_its = set(int(x) for x in np.linspace(5, max(6, last_arrival), args.samples))
@@ -123,6 +127,7 @@ def main():
             arrive_t[r.rid] = now
         s, plan = eng.step(arr)
         stats.append(s)
+        pre_keys += sum(ch + pf for _, ch, pf in plan.prefill)
         now += s.t_iter_ms / 1e3
         for r, ch, pf in plan.prefill:
             if r.prefilled == r.input_len and r.trace_id not in ttft:
@@ -159,10 +164,17 @@ def main():
                 mask = np.zeros(T, np.uint8)
                 mask[::64] = 1
                 mask[-1] = 1
-                ref = oracle.prefill(bits(eng.q_pre[:T]), bits(eng.k_pre[:T]), None, kp, None, bt, cu,
-                                     [r.slot if r.slot >= 0 else -1 for r, _, _ in plan.prefill],
-                                     [pf for _, _, pf in plan.prefill], shape.softmax_scale,
-                                     kv_shared=True, rows_mask=mask, dv=dv)
+                rids = [r.slot if r.slot >= 0 else -1 for r, _, _ in plan.prefill]
+                pfx = [pf for _, _, pf in plan.prefill]
+                if args.expanded:
+                    ref = oracle.prefill_mla_expanded(
+                        bits(eng.q_pre[:T]), bits(eng.k_pre[:T, 0]), kp.reshape(kp.shape[0], 1, bs, dk),
+                        bt, cu, rids, pfx, bits(eng.w_uk[0]), bits(eng.w_uv[0]), 1 / math.sqrt(192),
+                        rows_mask=mask)
+                else:
+                    ref = oracle.prefill(bits(eng.q_pre[:T]), bits(eng.k_pre[:T]), None, kp, None, bt, cu,
+                                         rids, pfx, shape.softmax_scale, kv_shared=True, rows_mask=mask,
+                                         dv=dv)
                 got = eng.o_pre[0][:T].float().cpu().double().numpy()
                 sel = mask.astype(bool)
                 rec["prefill"] = check(got[sel], ref[sel], f"it {s.it} prefill rows")
@@ -188,7 +200,11 @@ def main():
     t_iter = sum(x.t_iter_ms for x in stats) / 1e3
     pre_tok = sum(x.prefill_tokens for x in stats)
     dec_tok = sum(x.decode_reqs for x in stats)
-    pre_fl = sum(x.prefill_pairs for x in stats) * fl_pair * L
+    if args.expanded:  # causal MHA at dqk 192 / dv 128 + the up-projection of every key
+        pre_fl = (sum(x.prefill_pairs for x in stats) * 2.0 * Hq * (192 + 128) +
+                  pre_keys * 2.0 * 512 * 2 * Hq * 128) * L
+    else:
+        pre_fl = sum(x.prefill_pairs for x in stats) * fl_pair * L
     dec_bytes = sum(x.decode_keys for x in stats) * dk * 2 * L
     t_pre = sum(x.t_prefill_ms for x in stats) / 1e3
     t_dec = sum(x.t_decode_ms for x in stats) / 1e3
@@ -197,6 +213,7 @@ def main():
                   f"{args.blocks}-block pool), Poisson({args.lam})/iteration trace of {args.requests} "
                   f"requests (seed 5), 2048-token chunked prefill, decode cap 512, split "
                   f"({args.x:g},{100 - args.x:g})",
+        "prefill_form": "expanded (R32)" if args.expanded else "absorbed",
         "iterations": len(stats), "finished": len(eng.finished),
         "preemptions": sum(x.preempted for x in stats),
         "prefill_tokens": pre_tok, "decode_tokens": dec_tok,

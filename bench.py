@@ -311,7 +311,7 @@ class Workload:
         self.kv_fp8 = kv_fp8
         # expanded-form MLA prefill (reading R32): q [C, H, 192], the chunk's
         # latent rows [C, 576], per-layer up-projections W_UK / W_UV [H, 128, 512]; the call
-        # runs 2 spanned kernels per layer (up-projection GEMM, attention)
+        # runs 3 spanned kernels per layer (prep, up-projection GEMM, attention)
         self.mla_exp = mla_expanded
         assert not mla_expanded or s.kv_shared
         if kv_fp8:  # E4M3 pages (reading R31): per-tensor scales, prefix staging scratch
@@ -393,8 +393,8 @@ class Workload:
                 self.od = [self.peer_d.local_view(l % 2) for l in range(self.L)]
                 self.op = [self.peer_p.local_view(l % 2) for l in range(self.L)]
         # device-side launch spans: slots in enqueue order (corun_step sets span_order)
-        self.spans = torch.zeros(3 * self.L + 8, 8, dtype=torch.int64, device=dev)
-        self.span_k = {"prefill": 2 if mla_expanded else 1, "decode": 1}  # spans per layer
+        self.spans = torch.zeros(4 * self.L + 8, 8, dtype=torch.int64, device=dev)
+        self.span_k = {"prefill": 3 if mla_expanded else 1, "decode": 1}  # spans per layer
         self.span_order = ("prefill", "decode")
         self.ev_p_done, self.ev_d_done = torch.cuda.Event(), torch.cuda.Event()
 
@@ -1073,7 +1073,7 @@ def secondary_cfg5(args, dev, pk):
 def secondary_cfg5_expanded(args, dev, pk):
     """cfg5_mla with the expanded-form MLA prefill (reading R32): the same
     decode batch (absorbed decode over the latent) co-running with the 2048-token chunk's
-    prefill as up-projection GEMM + causal MHA at dqk 192 / dv 128 (2 kernels per layer); the
+    prefill as prep + up-projection GEMM + causal MHA at dqk 192 / dv 128 (3 kernels per layer); the
     prefill rate and fraction are against the expanded form's own flops (mla_expanded_flops)."""
     rng = np.random.default_rng(5005)
     ctx = [int(c) for c in np.clip(rng.lognormal(math.log(350.0) - 0.125, 0.5, 256), 64, 4096)]

@@ -406,7 +406,7 @@ semipd_status semipd_set_fp8_prefill_scratch(semipd_pool_t pool, void* mem, size
  * that key's latent is read as zeros.  No fused RoPE / peer epilogue (UNSUPPORTED).
  * Kernels: a prep pass (copies), a tcgen05 up-projection GEMM over TMA-gathered pool pages, a
  * tcgen05 causal attention kernel with dqk 192 / dv 128 (trace kernel kind 10); three launches,
- * the last two with launch spans. */
+ * each with a launch span (semipd_set_spans) in that order. */
 size_t semipd_prefill_mla_expanded_workspace_bytes(semipd_pool_t pool, int32_t max_reqs,
                                                    int32_t max_total_keys, int32_t num_heads);
 semipd_status semipd_prefill_mla_expanded(semipd_pool_t pool, int32_t layer, const void* q,

@@ -164,13 +164,15 @@ struct XPrep {
     long long rows_cap;  // workspace rows (max_total_keys + 128 n)
     long long slots_cap; // split slots of the workspace
     int* cnt;            // split counters / flags [slots][2][2]
+    unsigned long long* span;
 };
 
-__global__ void __launch_bounds__(256) mla_exp_prep_kernel(XPrep p) {
+__global__ void __launch_bounds__(1024) mla_exp_prep_kernel(XPrep p) {
     // per-request metadata in smem (every CTA scans; n <= 1024 requests is a few hundred cycles)
     __shared__ int s_off[XMAXN + 1];
     __shared__ int s_cu[XMAXN + 1];
-    __shared__ int s_warp[8];
+    __shared__ int s_warp[32];
+    if (threadIdx.x == 0) span_begin(p.span);
     const int* cu = p.cu;
     const int* prefix = p.prefix;
     // split-pair offsets first (s_off is reused for the tile offsets below)
@@ -189,76 +191,77 @@ __global__ void __launch_bounds__(256) mla_exp_prep_kernel(XPrep p) {
     __syncthreads();
     const int R = s_off[p.n] * XBM;
     if (R > p.rows_cap || n_slots > p.slots_cap) {  // max_total_keys was too small: write nothing
-        if (threadIdx.x == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_INVALID);
+        if (threadIdx.x == 0) {
+            if (p.status) atomicMax(p.status, SEMIPD_ERR_INVALID);
+            span_end(p.span);
+        }
         return;
     }
-    const int T = s_cu[p.n];
     const int bs_mask = (1 << p.lg_bs) - 1;
     constexpr int RU = XDL * 2 / 16;  // 72 uint4 per latent row
     constexpr int PU = XDR * 2 / 16;  // 8 uint4 of k_pe
-    const int nthr = gridDim.x * blockDim.x;
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (blockDim.x >> 5);
     const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
-    for (long long k = tid; k < 4 * n_slots; k += nthr) p.cnt[k] = 0;  // this call's split counters / flags
-    // 1. the chunk's latent rows -> pool pages: one 16-byte element per thread and step,
-    //    four independent elements in flight per thread
-    const int nA = T * RU;
-    for (int e0 = tid; e0 < nA; e0 += 4 * nthr) {
-        uint4 v[4];
-        uint4* dst[4];
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < 4 * n_slots;
+         k += (long long)gridDim.x * blockDim.x)
+        p.cnt[k] = 0;  // this call's split counters / flags
+    // one warp per padded key row, two rows in flight per warp: the chunk's latent rows go to the
+    // pool and every key's k_pe to Kpe (chunk keys from kv_new, prefix keys from the pool,
+    // padding rows zero)
+    for (int g0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g0 < R; g0 += 2 * nw) {
+        uint4 v[2][3];
+        uint4* prow[2];
+        uint4* kd[2];
+        int kind[2];  // 0: padding / bad block, 1: chunk row, 2: prefix row
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = e0 + u * nthr;
-            dst[u] = nullptr;
-            if (e < nA) {
-                const int t = e / RU, c = e - t * RU;
-                const int i = x_find([&](int k) { return s_cu[k]; }, p.n, t);
-                const int j = __ldg(p.prefix + i) + t - s_cu[i];
-                const int page = j >> p.lg_bs;
-                const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
-                if (blk >= 0 && blk < p.N_B)
-                    dst[u] = reinterpret_cast<uint4*>(p.pool + ((size_t)blk * (bs_mask + 1) + (j & bs_mask)) * (XDL * 2)) + c;
-                else if (c == 0 && p.status)
-                    atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
-                v[u] = __ldg(p.kv_new + (size_t)t * RU + c);
+        for (int u = 0; u < 2; ++u) {
+            const int g = g0 + u * nw;
+            kind[u] = 0;
+            prow[u] = nullptr;
+            kd[u] = p.kpe + (size_t)g * PU;
+            if (g >= R) { kd[u] = nullptr; continue; }
+            const int i = x_find([&](int q) { return s_off[q]; }, p.n, g / XBM);
+            const int j = g - s_off[i] * XBM;
+            const int P = __ldg(p.prefix + i), c0 = s_cu[i], nk = P + s_cu[i + 1] - c0;
+            if (j >= nk) continue;
+            const int page = j >> p.lg_bs;
+            const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
+            if (blk < 0 || blk >= p.N_B) {
+                if (lane == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                continue;
+            }
+            prow[u] = reinterpret_cast<uint4*>(p.pool + ((size_t)blk * (bs_mask + 1) + (j & bs_mask)) * (XDL * 2));
+            if (j >= P) {
+                kind[u] = 1;
+                const uint4* src = p.kv_new + (size_t)(c0 + j - P) * RU;
+#pragma unroll
+                for (int r3 = 0; r3 < 3; ++r3)
+                    if (lane + 32 * r3 < RU) v[u][r3] = __ldg(src + lane + 32 * r3);
+            } else {
+                kind[u] = 2;
+                if (lane < PU) v[u][0] = prow[u][RU - PU + lane];
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (dst[u]) *dst[u] = v[u];
-    }
-    // 2. every key's k_pe -> Kpe [rows][64] (chunk keys from kv_new, prefix keys from the pool,
-    //    padding rows zero)
-    const int nB = R * PU;
-    for (int e0 = tid; e0 < nB; e0 += 4 * nthr) {
-        uint4 v[4];
+        for (int u = 0; u < 2; ++u) {
+            if (!kd[u]) continue;
+            if (kind[u] == 1) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = e0 + u * nthr;
-            v[u] = zero;
-            if (e < nB) {
-                const int g = e / PU, c = e - g * PU;
-                const int i = x_find([&](int k) { return s_off[k]; }, p.n, g / XBM);
-                const int j = g - s_off[i] * XBM;
-                const int P = __ldg(p.prefix + i), nk = P + s_cu[i + 1] - s_cu[i];
-                if (j >= P && j < nk) {
-                    v[u] = __ldg(p.kv_new + (size_t)(s_cu[i] + j - P) * RU + (RU - PU) + c);
-                } else if (j < P) {
-                    const int page = j >> p.lg_bs;
-                    const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
-                    if (blk >= 0 && blk < p.N_B)
-                        v[u] = reinterpret_cast<const uint4*>(p.pool + ((size_t)blk * (bs_mask + 1) + (j & bs_mask)) * (XDL * 2))[RU - PU + c];
-                    else if (c == 0 && p.status)
-                        atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                for (int r3 = 0; r3 < 3; ++r3) {
+                    const int c = lane + 32 * r3;
+                    if (c < RU) {
+                        prow[u][c] = v[u][r3];
+                        if (c >= RU - PU) kd[u][c - (RU - PU)] = v[u][r3];
+                    }
                 }
+            } else if (lane < PU) {
+                kd[u][lane] = kind[u] == 2 ? v[u][0] : zero;
             }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = e0 + u * nthr;
-            if (e < nB) p.kpe[e] = v[u];
-        }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) span_end(p.span);
 }
 
 // ------------------------------------------------------------------ 2. up-projection GEMM
@@ -1033,13 +1036,12 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     pp.slots_cap = (long long)slots;
     pp.cnt = cnt;
     pp.H = H;
+    pp.span = spd_next_span(pool);
     const int max_mt = (int)((rows + XBM - 1) / XBM);
     int gprep = budget > 0 ? budget : pool->num_sms;
-    const size_t prep_elems = (size_t)total_q * (XDL * 2 / 16) > rows * (XDR * 2 / 16)
-                                  ? (size_t)total_q * (XDL * 2 / 16) : rows * (XDR * 2 / 16);
-    const int prep_need = (int)((prep_elems + 1023) / 1024);
+    const int prep_need = (int)((rows + 63) / 64);  // 32 warps x 2 rows per CTA and step
     if (gprep > prep_need) gprep = prep_need;
-    mla_exp_prep_kernel<<<gprep, 256, 0, st>>>(pp);
+    mla_exp_prep_kernel<<<gprep, 1024, 0, st>>>(pp);
     pool->launches += 1;
     if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
 

@@ -232,7 +232,7 @@ def mla_exp(args, dev):
     f_attn = 2 * H * (192 + 128) * pairs
     f_gemm = 2 * (C + P) * 512 * 2 * H * 128
     f_abs = 2 * H * (576 + 512) * pairs
-    spans = torch.zeros(2, 8, dtype=torch.int64, device=dev)
+    spans = torch.zeros(3, 8, dtype=torch.int64, device=dev)  # prep, GEMM, attention
     cu_t, rid_t, pre_t = i32([0, C]), i32([0]), i32([P])
     for bud in [int(x) for x in args.budgets.split(",")]:
         run = lambda l: pool.prefill_mla_expanded(l, q, kv, w_uk[l], w_uv[l], cu_t, rid_t,  # noqa: E731
@@ -268,11 +268,12 @@ def mla_exp(args, dev):
         torch.cuda.synchronize()
         pool.set_spans(None)
         sp = spans.cpu()
-        gms = float(sp[0, 2]) / max(1, int(sp[0, 3])) / 1e6
-        ams = float(sp[1, 2]) / max(1, int(sp[1, 3])) / 1e6
+        pms = float(sp[0, 2]) / max(1, int(sp[0, 3])) / 1e6
+        gms = float(sp[1, 2]) / max(1, int(sp[1, 3])) / 1e6
+        ams = float(sp[2, 2]) / max(1, int(sp[2, 3])) / 1e6
         print(json.dumps({"kernel": "prefill_mla_expanded", "budget": bud, "C": C, "P": P, "ms": ms,
                           "ms_graph": ms_graph, "TFLOP_s_graph": (f_gemm + f_attn) / (ms_graph / 1e3) / 1e12,
-                          "gemm_ms": gms, "attn_ms": ams,
+                          "prep_ms": pms, "gemm_ms": gms, "attn_ms": ams,
                           "gemm_TFLOP_s": f_gemm / (gms / 1e3) / 1e12 if gms > 0 else None,
                           "attn_TFLOP_s": f_attn / (ams / 1e3) / 1e12 if ams > 0 else None,
                           "TFLOP_s": (f_gemm + f_attn) / (ms / 1e3) / 1e12,

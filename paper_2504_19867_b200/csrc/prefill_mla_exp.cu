@@ -84,7 +84,7 @@ __host__ __device__ __forceinline__ int x_first_split_pair(int P, int C) {
 
 // ------------------------------------------------------------------ workspace
 // [hdr: int mtoff[n + 1] (128-row tile offset of each request's keys), int sbase[n + 1] (split
-// pair offset)] [K_exp rows x H x 128] [V_exp rows x H x 128] [Kpe rows x 64]
+// pair offset)] [K_exp rows x H x 128] [V_exp rows x H x 128] [Kpe rows x 64] [Lat rows x 512]
 // [split counters: slots x 2 tiles x (role counter, flag) int] [partials: slots x 2 tiles x 128 rows
 // x XPROW fp32 (the first part's rows)],
 // rows = max_total_keys + 128 n (per-request padding), slots = (max_total_keys / 256 + n) x H
@@ -99,7 +99,7 @@ size_t x_part_bytes(size_t slots) { return spd_al256(slots * 2 * XBM * XPROW * s
 size_t x_ws_bytes(int n, int max_keys, int H) {
     const size_t r = x_rows(n, max_keys), sl = x_slots(n, max_keys, H);
     return x_hdr_bytes(n) + spd_al256(r * H * XDN * 2) + spd_al256(r * H * XDV * 2) + spd_al256(r * XDR * 2) +
-           x_cnt_bytes(sl) + x_part_bytes(sl);
+           spd_al256(r * XDC * 2) + x_cnt_bytes(sl) + x_part_bytes(sl);
 }
 
 // s_off[i] = sum_{i' < i} val(i') (exclusive scan over the block; every thread takes a
@@ -158,6 +158,7 @@ struct XPrep {
     const uint4* kv_new;     // [T][576] bf16
     unsigned char* pool;     // this layer's latent pages [N_B][bs][576]
     uint4* kpe;              // [rows][64] bf16
+    uint4* lat;              // [rows][512] bf16: every key's latent c_j, contiguous (GEMM A)
     int* hdr;
     int* status;
     int n, lg_bs, MBR, N_B, H;
@@ -207,20 +208,19 @@ __global__ void __launch_bounds__(1024) mla_exp_prep_kernel(XPrep p) {
          k += (long long)gridDim.x * blockDim.x)
         p.cnt[k] = 0;  // this call's split counters / flags
     // one warp per padded key row, two rows in flight per warp: the chunk's latent rows go to the
-    // pool and every key's k_pe to Kpe (chunk keys from kv_new, prefix keys from the pool,
-    // padding rows zero)
+    // pool; every key's latent to Lat (the GEMM's contiguous A) and its k_pe to Kpe
+    // (chunk keys from kv_new, prefix keys from the pool, padding / bad-block rows zero)
+    constexpr int LU = XDC * 2 / 16;  // 64 uint4 of c_j
     for (int g0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g0 < R; g0 += 2 * nw) {
         uint4 v[2][3];
         uint4* prow[2];
-        uint4* kd[2];
-        int kind[2];  // 0: padding / bad block, 1: chunk row, 2: prefix row
+        int kind[2];  // -1: beyond R, 0: padding / bad block, 1: chunk row, 2: prefix row
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int g = g0 + u * nw;
-            kind[u] = 0;
+            kind[u] = g < R ? 0 : -1;
             prow[u] = nullptr;
-            kd[u] = p.kpe + (size_t)g * PU;
-            if (g >= R) { kd[u] = nullptr; continue; }
+            if (g >= R) continue;
             const int i = x_find([&](int q) { return s_off[q]; }, p.n, g / XBM);
             const int j = g - s_off[i] * XBM;
             const int P = __ldg(p.prefix + i), c0 = s_cu[i], nk = P + s_cu[i + 1] - c0;
@@ -232,31 +232,27 @@ __global__ void __launch_bounds__(1024) mla_exp_prep_kernel(XPrep p) {
                 continue;
             }
             prow[u] = reinterpret_cast<uint4*>(p.pool + ((size_t)blk * (bs_mask + 1) + (j & bs_mask)) * (XDL * 2));
-            if (j >= P) {
-                kind[u] = 1;
-                const uint4* src = p.kv_new + (size_t)(c0 + j - P) * RU;
+            const uint4* src = j >= P ? p.kv_new + (size_t)(c0 + j - P) * RU : prow[u];
+            kind[u] = j >= P ? 1 : 2;
 #pragma unroll
-                for (int r3 = 0; r3 < 3; ++r3)
-                    if (lane + 32 * r3 < RU) v[u][r3] = __ldg(src + lane + 32 * r3);
-            } else {
-                kind[u] = 2;
-                if (lane < PU) v[u][0] = prow[u][RU - PU + lane];
-            }
+            for (int r3 = 0; r3 < 3; ++r3)
+                if (lane + 32 * r3 < RU) v[u][r3] = j >= P ? __ldg(src + lane + 32 * r3) : src[lane + 32 * r3];
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            if (!kd[u]) continue;
-            if (kind[u] == 1) {
+            if (kind[u] < 0) continue;
+            const size_t g = (size_t)g0 + u * nw;
+            uint4* ld = p.lat + g * LU;
+            uint4* kd = p.kpe + g * PU;
 #pragma unroll
-                for (int r3 = 0; r3 < 3; ++r3) {
-                    const int c = lane + 32 * r3;
-                    if (c < RU) {
-                        prow[u][c] = v[u][r3];
-                        if (c >= RU - PU) kd[u][c - (RU - PU)] = v[u][r3];
-                    }
+            for (int r3 = 0; r3 < 3; ++r3) {
+                const int c = lane + 32 * r3;
+                if (c < RU) {
+                    const uint4 x = kind[u] > 0 ? v[u][r3] : zero;
+                    if (kind[u] == 1) prow[u][c] = x;
+                    if (c < LU) ld[c] = x;
+                    else kd[c - LU] = x;
                 }
-            } else if (lane < PU) {
-                kd[u][lane] = kind[u] == 2 ? v[u][0] : zero;
             }
         }
     }
@@ -265,9 +261,10 @@ __global__ void __launch_bounds__(1024) mla_exp_prep_kernel(XPrep p) {
 }
 
 // ------------------------------------------------------------------ 2. up-projection GEMM
-constexpr int GST = 4;                        // k-stages in flight
-constexpr uint32_t GA = XBM * 128;            // A stage: 128 rows x 64 cols (16 KiB)
-constexpr uint32_t GB = 256 * 128;            // B stage: 256 rows x 64 cols (32 KiB)
+constexpr int GCB = 2;                        // 64-column blocks per stage
+constexpr int GST = 2;                        // stages in flight
+constexpr uint32_t GA = XBM * 128 * GCB;      // A stage: 128 rows x 128 cols (32 KiB, one box)
+constexpr uint32_t GB = 256 * 128 * GCB;      // B stage: 256 rows x 128 cols (64 KiB, one box)
 constexpr int GNT = 192;
 
 struct GSmem {
@@ -329,40 +326,20 @@ __global__ void __launch_bounds__(GNT, 1)
             tma_prefetch_desc(&ukmap);
             tma_prefetch_desc(&uvmap);
         }
-        const int nbox = XBM / p.box_rows;
-        const int bs_mask = (1 << p.lg_bs) - 1;
         int sc = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
             const int mt = tile / NTN, nt = tile % NTN;
-            const int i = x_find(off, p.n, mt);
-            const int kbase = (mt - off(i)) * XBM;
-            const int nk = __ldg(p.prefix + i) + __ldg(p.cu + i + 1) - __ldg(p.cu + i);
-            int z = p.N_B;  // out of bounds: zero fill (keys past the request)
-            if (lane < nbox) {
-                const int j0 = kbase + lane * p.box_rows;
-                if (j0 < nk) {
-                    const int page = j0 >> p.lg_bs;
-                    const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
-                    if (blk >= 0 && blk < p.N_B) z = blk;
-                    else if (p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
-                }
-            }
             const CUtensorMap* bm = nt < NTN / 2 ? &ukmap : &uvmap;
             const int brow = (nt % (NTN / 2)) * 256;
-            for (int ks = 0; ks < XDC / 64; ++ks, ++sc) {
+            for (int ks = 0; ks < XDC / (64 * GCB); ++ks, ++sc) {
                 const int s = sc % GST;
                 if (lane == 0) {
                     mbar_wait(&sm.empty[s], ((sc / GST) & 1) ^ 1);
                     mbar_arrive_expect_tx(&sm.full[s], GA + GB);
+                    // (64 cols, rows, column blocks) boxes land as [block][rows][128 B]
+                    tma_load_3d(sm.a[s], &amap, &sm.full[s], 0, mt * XBM, ks * GCB);
+                    tma_load_3d(sm.b[s], bm, &sm.full[s], 0, brow, ks * GCB);
                 }
-                __syncwarp();
-                for (int b = 0; b < nbox; ++b) {
-                    const int zb = __shfl_sync(0xffffffffu, z, b);
-                    if (lane == 0)
-                        tma_load_3d(sm.a[s] + b * p.box_rows * 128, &amap, &sm.full[s], ks * 64,
-                                    (kbase + b * p.box_rows) & bs_mask, zb);
-                }
-                if (lane == 0) tma_load_3d(sm.b[s], bm, &sm.full[s], ks * 64, brow, 0);
                 __syncwarp();
             }
         }
@@ -375,14 +352,18 @@ __global__ void __launch_bounds__(GNT, 1)
             mbar_wait(&sm.acce[ab], ((lt >> 1) & 1) ^ 1);
             tc_fence_after();
             const uint32_t d = tmem + (uint32_t)(ab * 256);
-            for (int ks = 0; ks < XDC / 64; ++ks, ++sc) {
+            for (int ks = 0; ks < XDC / (64 * GCB); ++ks, ++sc) {
                 const int s = sc % GST;
                 mbar_wait(&sm.full[s], (sc / GST) & 1);
                 tc_fence_after();
-                const uint32_t a0 = smem_u32(sm.a[s]), b0 = smem_u32(sm.b[s]);
+                const uint64_t da = xk_desc(smem_u32(sm.a[s])), db = xk_desc(smem_u32(sm.b[s]));
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    umma_ss_warp(d, xk_desc(a0 + kk * 32), xk_desc(b0 + kk * 32), idesc, (ks | kk) ? 1u : 0u);
+                for (int kk = 0; kk < 4 * GCB; ++kk) {
+                    const int cb = kk >> 2;
+                    umma_ss_warp(d, da + (uint64_t)((cb * XBM * 128 + (kk & 3) * 32) >> 4),
+                                 db + (uint64_t)((cb * 256 * 128 + (kk & 3) * 32) >> 4), idesc,
+                                 (ks | kk) ? 1u : 0u);
+                }
                 umma_commit_warp(&sm.empty[s]);
             }
             umma_commit_warp(&sm.accf[ab]);
@@ -1013,7 +994,9 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     __nv_bfloat16* kpe = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<unsigned char*>(vexp) +
                                                           spd_al256(rows * H * XDV * 2));
     const size_t slots = x_slots(n, max_total_keys, H);
-    int* cnt = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(kpe) + spd_al256(rows * XDR * 2));
+    __nv_bfloat16* lat = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<unsigned char*>(kpe) +
+                                                          spd_al256(rows * XDR * 2));
+    int* cnt = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(lat) + spd_al256(rows * XDC * 2));
     float* part = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(cnt) + x_cnt_bytes(slots));
     const int lg_bs = __builtin_ctz((unsigned)c.block_size);
 
@@ -1026,6 +1009,7 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     pp.kv_new = static_cast<const uint4*>(kv_new);
     pp.pool = static_cast<unsigned char*>(pool->k_layer(layer));
     pp.kpe = reinterpret_cast<uint4*>(kpe);
+    pp.lat = reinterpret_cast<uint4*>(lat);
     pp.hdr = hdr;
     pp.status = status_dev;
     pp.n = n;
@@ -1046,14 +1030,23 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
 
     // 2. up-projection GEMM
-    CUtensorMap ukmap, uvmap;
-    if (!spd_encode_tiled_3d(&ukmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(w_uk), XDC,
-                             (uint64_t)H * XDN, 1, XDC * 2, (uint64_t)H * XDN * XDC * 2, 64, 256, 1,
-                             CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !spd_encode_tiled_3d(&uvmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(w_uv), XDC,
-                             (uint64_t)H * XDV, 1, XDC * 2, (uint64_t)H * XDV * XDC * 2, 64, 256, 1,
-                             CU_TENSOR_MAP_SWIZZLE_128B))
-        return SEMIPD_ERR_CUDA;
+    // (64 cols, rows, 8 column blocks) views: one box = 128-column stage of 128 latent rows
+    // (A, 32 KiB) / 256 weight rows (B, 64 KiB), landing as [block][rows][128 B]
+    CUtensorMap amap, ukmap, uvmap;
+    {
+        const uint32_t abox[3] = {64, XBM, GCB}, bbox[3] = {64, 256, GCB};
+        const uint64_t adims[3] = {64, rows, XDC / 64}, astr[2] = {XDC * 2, 128};
+        const uint64_t bdims[3] = {64, (uint64_t)H * XDN, XDC / 64}, bstr[2] = {XDC * 2, 128};
+        if (!spd_encode_tiled_3d(&amap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, lat, adims[0], adims[1], adims[2],
+                                 astr[0], astr[1], abox[0], abox[1], abox[2], CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !spd_encode_tiled_3d(&ukmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(w_uk), bdims[0],
+                                 bdims[1], bdims[2], bstr[0], bstr[1], bbox[0], bbox[1], bbox[2],
+                                 CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !spd_encode_tiled_3d(&uvmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(w_uv), bdims[0],
+                                 bdims[1], bdims[2], bstr[0], bstr[1], bbox[0], bbox[1], bbox[2],
+                                 CU_TENSOR_MAP_SWIZZLE_128B))
+            return SEMIPD_ERR_CUDA;
+    }
     XGemm gp;
     gp.cu = cu_seqlens_q;
     gp.req_ids = req_ids;
@@ -1085,7 +1078,7 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     const long long gtiles = (long long)max_mt * H;
     int ggrid = budget > 0 ? budget : (int)(gtiles < (1 << 30) ? gtiles : (1 << 30));
     if (ggrid > gtiles) ggrid = (int)gtiles;
-    mla_exp_gemm_kernel<<<ggrid, GNT, gsm, st>>>(pool->kmap[layer], ukmap, uvmap, gp);
+    mla_exp_gemm_kernel<<<ggrid, GNT, gsm, st>>>(amap, ukmap, uvmap, gp);
     pool->launches += 1;
     if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
 

@@ -28,7 +28,7 @@ __global__ void rate(int M, int N, int reps, long long* out, int mode) {
     __shared__ uint32_t tbase;
     __shared__ __align__(8) uint64_t bar;
     for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(base)[i] = 0x3f803f80u;
-    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+    if (threadIdx.x == 0) { mbar_init(&bar, mode == 3 ? 2 : 1); fence_mbar_init(); }
     if (threadIdx.x < 32) tmem_alloc(&tbase, 256);
     fence_proxy_async_smem();
     tc_fence_before();
@@ -77,6 +77,28 @@ __global__ void rate(int M, int N, int reps, long long* out, int mode) {
         if (threadIdx.x == 0) umma_commit(&bar);
         mbar_wait(&bar, 0);
     }
+    if (mode == 3 && threadIdx.x < 64) {
+        // two issuing warps, each 36 x reps MMAs into its own accumulator columns: does the
+        // aggregate MMA rate grow with a second issuer?
+        const uint32_t id = idesc(M, N, 0, 0);
+        const uint32_t a0 = smem_u32(base), b0 = smem_u32(base + 96 * 1024);
+        const uint64_t da = umma_desc_sw128(a0, 16, 1024), db = umma_desc_sw128(b0, 16, 1024);
+        const uint32_t dt = tbase + (threadIdx.x >> 5) * 64;
+        __syncwarp();
+        long long t0 = clock64();
+        for (int r = 0; r < reps; ++r) {
+#pragma unroll
+            for (int k = 0; k < 36; ++k) {
+                umma_ss_elect(dt, da + (uint64_t)((k >> 2) * 512 + (k & 3) * 2),
+                              db + (uint64_t)((k >> 2) * 128 + (k & 3) * 2), id, k > 0);
+            }
+        }
+        long long t1 = clock64();
+        if ((threadIdx.x & 31) == 0) umma_commit(&bar);
+        mbar_wait(&bar, 0);
+        long long t2 = clock64();
+        if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t2 - t0; }
+    }
     if (mode == 0 && threadIdx.x == 0) {
         const uint32_t id = idesc(M, N, 0, 0);
         const uint32_t a0 = smem_u32(base), b0 = smem_u32(base + 96 * 1024);
@@ -114,12 +136,13 @@ int main() {
                cudaGetErrorString(cudaGetLastError()));
     }
     for (auto& s : shapes) {
-        for (int mode : {0, 1}) for (int reps : {1, 20}) {
+        for (int mode : {0, 1, 3}) for (int reps : {1, 20}) {
             rate<<<1, 128, 170 * 1024>>>(s[0], s[1], reps, d, mode);
             long long h[2];
             cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+            const int nmma = 36 * reps * (mode == 3 ? 2 : 1);  // mode 3: per-MMA over both warps
             printf("mode=%d M=%d N=%d reps=%d: issue %.1f cyc/mma, complete %.1f cyc/mma (%s)\n", mode, s[0], s[1], reps,
-                   (double)h[0] / (36 * reps), (double)h[1] / (36 * reps),
+                   (double)h[0] / nmma, (double)h[1] / nmma,
                    cudaGetErrorString(cudaGetLastError()));
         }
     }

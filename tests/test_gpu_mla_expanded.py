@@ -18,20 +18,20 @@ pytestmark = pytest.mark.gpu
 H = 16
 
 
-def _shape(bs):
+def _shape(bs, nh=H):
     s = synth.CFG5_MLA
-    return synth.AttnShape(s.name, H, 1, 576, 512, bs, torch.bfloat16, num_layers=1, kv_shared=True,
+    return synth.AttnShape(s.name, nh, 1, 576, 512, bs, torch.bfloat16, num_layers=1, kv_shared=True,
                            scale=s.scale)
 
 
 def run_exp(chunks, prefixes, seed, dist=synth.FLAT, bs=64, sm_budget=0, rows_mask=None,
-            bad_entry=None, max_total_keys=None, check=True):
-    case = synth.mla_expanded_case(chunks, prefixes, seed, H, dist)
+            bad_entry=None, max_total_keys=None, check=True, nh=H):
+    case = synth.mla_expanded_case(chunks, prefixes, seed, nh, dist)
     n = len(chunks)
     nk = [p + c for p, c in zip(prefixes, chunks)]
     need = [-(-k // bs) for k in nk]
     mbr = max(need) + 1
-    rig = Rig(_shape(bs), num_blocks=sum(need) + 3, max_reqs=n, mbr=mbr)
+    rig = Rig(_shape(bs, nh), num_blocks=sum(need) + 3, max_reqs=n, mbr=mbr)
     for i in range(n):
         rig.alloc([i], [need[i]])
     K, _, BT, _ = rig.pool.views(0)
@@ -47,9 +47,9 @@ def run_exp(chunks, prefixes, seed, dist=synth.FLAT, bs=64, sm_budget=0, rows_ma
     dev = rig.dev
     T = case.cu[-1]
     mtk = sum(nk) if max_total_keys is None else max_total_keys
-    ws = rig.pool.new_mla_expanded_workspace(n, mtk, H)
+    ws = rig.pool.new_mla_expanded_workspace(n, mtk, nh)
     ws.fill_(0xFF)  # NaN patterns: the kernels must not read workspace rows they did not write
-    out = torch.full((T, H, 128), float("nan"), dtype=torch.bfloat16, device=dev)
+    out = torch.full((T, nh, 128), float("nan"), dtype=torch.bfloat16, device=dev)
     rig.pool.prefill_mla_expanded(0, case.q.to(dev), case.kv_new.to(dev), case.w_uk.to(dev),
                                   case.w_uv.to(dev), rig.i32(case.cu), rig.i32(range(n)),
                                   rig.i32(prefixes), T, max(chunks), mtk, case.scale, out, ws,
@@ -76,6 +76,13 @@ def run_exp(chunks, prefixes, seed, dist=synth.FLAT, bs=64, sm_budget=0, rows_ma
 @pytest.mark.parametrize("dist", synth.DISTS)
 def test_mla_expanded_parity(chunks, prefixes, dist):
     run_exp(chunks, prefixes, seed=700 + dist, dist=dist)
+
+
+@pytest.mark.parametrize("nh", [2, 8, 32])
+def test_mla_expanded_head_counts(nh):
+    """Other head counts (a TP shard of the 16 heads, a wider model): the GEMM's n-tiles are
+    head pairs, the attention's units per head."""
+    run_exp([200, 57], [30, 140], seed=750 + nh, nh=nh, dist=synth.PEAKED)
 
 
 @pytest.mark.parametrize("bs", [16, 32, 128])

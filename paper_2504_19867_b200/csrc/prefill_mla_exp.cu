@@ -684,41 +684,50 @@ __global__ void __launch_bounds__(ANT, 1)
                 const int nA = d.nkv[0], nB = d.nkv[1];
                 const uint32_t q_base = smem_u32(sm.q[0]);
                 const uint32_t ring_a = smem_u32(sm.ring[0]);
+                // smem descriptors as (low, high) words: low = start >> 4 | LBO >> 4 << 16 (the K16
+                // steps add 16-byte offsets to it), high = SBO 1 KiB, version 1, 128-byte swizzle
+                constexpr uint32_t DHI = (1024u >> 4) | (1u << 14) | (2u << 29);
+                auto dlo = [](uint32_t addr, uint32_t lbo) { return (addr >> 4) | ((lbo >> 4) << 16); };
                 auto issue_s = [&](int t, int kc) {  // S_t = Q_t [k_nope | k_pe]^T, 12 x K16
-                    // descriptors formed once per call; the K16 steps add constant offsets
-                    // (16-byte units) to the start-address field
-                    const uint64_t qd = xk_desc(q_base + t * SLOT);
-                    uint64_t kd[3];
+                    const uint32_t qd = dlo(q_base + t * SLOT, 16);
+                    uint32_t kd[3];
 #pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) kd[ch] = xk_desc(ring_a + ((kc + ch) & (NSLOT - 1)) * SLOT);
+                    for (int ch = 0; ch < 3; ++ch) kd[ch] = dlo(ring_a + ((kc + ch) & (NSLOT - 1)) * SLOT, 16);
 #pragma unroll
                     for (int kk = 0; kk < 12; ++kk) {
                         const int ch = kk >> 2;
-                        umma_ss_warp(tmem + (uint32_t)(t * XBM), qd + (uint64_t)((ch * QCH + (kk & 3) * 32) >> 4),
-                                     kd[ch] + (uint64_t)(((kk & 3) * 32) >> 4), idesc_s, kk > 0 ? 1u : 0u);
+                        umma_ss_warp2(tmem + (uint32_t)(t * XBM), qd + ((ch * QCH + (kk & 3) * 32) >> 4), DHI,
+                                      kd[ch] + (((kk & 3) * 32) >> 4), DHI, idesc_s, kk > 0 ? 1u : 0u);
                     }
                     umma_commit_warp(&sm.s_full[t]);
                 };
                 auto issue_pv = [&](int t, int& cnt, int vc, bool first) {  // O_t += P_t V
                     const int s0 = vc & (NSLOT - 1), s1 = (vc + 1) & (NSLOT - 1);
-                    const uint64_t vd0 = umma_desc_sw128(ring_a + s0 * SLOT, SLOT, 1024);
-                    const uint64_t vd1 = umma_desc_sw128(ring_a + s1 * SLOT, SLOT, 1024);
-                    const bool adj = s1 == s0 + 1;
+                    const uint32_t vd0 = dlo(ring_a + s0 * SLOT, SLOT), vd1 = dlo(ring_a + s1 * SLOT, SLOT);
                     const uint32_t p_tmem = tmem + (uint32_t)(t * XBM);
                     const uint32_t o_tmem = tmem + 256u + (uint32_t)(t * XDV);
+                    if (s1 == s0 + 1) {  // adjacent slots: one N = 128 MMA per K16 (LBO = slot pitch)
 #pragma unroll
-                    for (int hf = 0; hf < kXPvParts; ++hf) {
-                        mbar_wait(&sm.p_full[t][hf], cnt & 1);
-                        tc_fence_after();
+                        for (int hf = 0; hf < kXPvParts; ++hf) {
+                            mbar_wait(&sm.p_full[t][hf], cnt & 1);
+                            tc_fence_after();
 #pragma unroll
-                        for (int kk = hf * 8 / kXPvParts; kk < (hf + 1) * 8 / kXPvParts; ++kk) {
-                            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-                            const uint64_t ko = (uint64_t)(kk * (2048 >> 4));
-                            if (adj) {  // adjacent slots: one N = 128 MMA (LBO = slot pitch)
-                                umma_ts_warp(o_tmem, p_tmem + (uint32_t)(kk * 8), vd0 + ko, idesc_o, acc);
-                            } else {  // ring wrap: the two 64-column halves as N = 64 MMAs
-                                umma_ts_warp(o_tmem, p_tmem + (uint32_t)(kk * 8), vd0 + ko, idesc_o64, acc);
-                                umma_ts_warp(o_tmem + 64u, p_tmem + (uint32_t)(kk * 8), vd1 + ko, idesc_o64, acc);
+                            for (int kk = hf * 8 / kXPvParts; kk < (hf + 1) * 8 / kXPvParts; ++kk)
+                                umma_ts_warp2(o_tmem, p_tmem + (uint32_t)(kk * 8), vd0 + kk * (2048 >> 4), DHI,
+                                              idesc_o, (first && kk == 0) ? 0u : 1u);
+                        }
+                    } else {  // ring wrap: the two 64-column halves as N = 64 MMAs
+#pragma unroll
+                        for (int hf = 0; hf < kXPvParts; ++hf) {
+                            mbar_wait(&sm.p_full[t][hf], cnt & 1);
+                            tc_fence_after();
+#pragma unroll
+                            for (int kk = hf * 8 / kXPvParts; kk < (hf + 1) * 8 / kXPvParts; ++kk) {
+                                const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+                                umma_ts_warp2(o_tmem, p_tmem + (uint32_t)(kk * 8), vd0 + kk * (2048 >> 4), DHI,
+                                              idesc_o64, acc);
+                                umma_ts_warp2(o_tmem + 64u, p_tmem + (uint32_t)(kk * 8), vd1 + kk * (2048 >> 4), DHI,
+                                              idesc_o64, acc);
                             }
                         }
                     }

@@ -246,6 +246,12 @@ SPD_DEV void umma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uin
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
         : "memory");
 }
+// The two 32-bit words of umma_desc_sw128(addr, lbo, 1024): low = start >> 4 | LBO >> 4 << 16,
+// high = SBO (1 KiB) >> 4 | version 1 | 128-byte swizzle.
+constexpr uint32_t DESC_HI_SBO1K = (1024u >> 4) | (1u << 14) | (2u << 29);
+SPD_DEV uint32_t desc_lo(uint32_t smem_addr, uint32_t lbo_bytes) {
+    return ((smem_addr >> 4) & 0x3FFFu) | (((lbo_bytes >> 4) & 0x3FFFu) << 16);
+}
 // Same, with each smem descriptor passed as two 32-bit words (low: start address and LBO
 // fields, high: SBO / version / layout): callers add 16-byte offsets to the low word with 32-bit
 // arithmetic and keep the constant high word in one register (no 64-bit adds per MMA).

@@ -381,8 +381,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         constexpr uint32_t ID_QK = umma_idesc_bf16_f32_ab(64, NH, 0, 0);
         constexpr uint32_t ID_PV = umma_idesc_bf16_f32_ab(128, NH, 1, 0);
         const uint32_t ring_a = smem_u32(ring), q_a = smem_u32(qs), p_a = smem_u32(ps);
-        const uint64_t dq0 = umma_desc_sw128(q_a, 16, 1024);
-        const uint64_t dp0 = umma_desc_sw128(p_a, 16, 1024);
+        // smem descriptors as (low, high) words: the K16 / block offsets are 32-bit adds to the
+        // low word on the uniform datapath (umma_ss_warp2)
+        const uint32_t dq0 = desc_lo(q_a, 16);
+        const uint32_t dp0 = desc_lo(p_a, 16);
+        constexpr uint32_t DH = DESC_HI_SBO1K;
         auto probe = [&](const uint64_t* b, uint32_t par) {
             bool r = false;
             if (lane == 0) r = mbar_test_wait(b, par);
@@ -413,13 +416,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         // dv block m = column blocks 2m, 2m+1 (both in the same half-page)
                         const uint32_t a0 = m < 2 ? lo + m * (2 * PAGE * 128)
                                                   : hi + (2 * m - CB_LO) * (PAGE * 128);
-                        const uint64_t da = umma_desc_sw128(a0, PAGE * 128, 1024);
+                        const uint32_t da = desc_lo(a0, PAGE * 128);
 #pragma unroll
                         for (int ks = 0; ks < PAGE / 16; ++ks)
-                            umma_ss_warp(tmem + TM_O + ((nunit - 1) & 1) * TM_OSET + ob * 64 + m * NH,
-                                         da + (uint64_t)(ks * 128),
-                                         dp0 + (uint64_t)(ob * (P_BYTES / 16) + ks * 2), ID_PV,
-                                         (npv > 1 || ks > 0) ? 1u : 0u);
+                            umma_ss_warp2(tmem + TM_O + ((nunit - 1) & 1) * TM_OSET + ob * 64 + m * NH,
+                                          da + (uint32_t)(ks * 128), DH,
+                                          dp0 + (uint32_t)(ob * (P_BYTES / 16) + ks * 2), DH, ID_PV,
+                                          (npv > 1 || ks > 0) ? 1u : 0u);
                         if (m == 1) umma_commit_warp(bar.empty + s0);  // blocks 0,1 read the first box
                     }
                     umma_commit_warp(bar.o_done + ob);
@@ -438,27 +441,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (q_ok && !qk_lo && probe(bar.s_empty + sb, ((t >> 1) & 1) ^ 1) &&
                         probe(bar.full + s0, (h0 / NSLOT) & 1)) {
                         tc_fence_after();
-                        const uint64_t dlo = umma_desc_sw128(ring_a + slot_off(s0), 16, 1024);
-                        const uint64_t dq = dq0 + (uint64_t)(qb * (Q_BYTES / 16));
+                        const uint32_t dlo = desc_lo(ring_a + slot_off(s0), 16);
+                        const uint32_t dq = dq0 + (uint32_t)(qb * (Q_BYTES / 16));
 #pragma unroll
                         for (int k = 0; k < CB_LO * 4; ++k) {
                             const int cb = k >> 2;
                             // descriptor start address is in 16-byte units
-                            umma_ss_warp(tmem + TM_S + sb * NH, dlo + (uint64_t)(cb * (PAGE * 128 / 16) + (k & 3) * 2),
-                                         dq + (uint64_t)(cb * (NH * 128 / 16) + (k & 3) * 2), ID_QK, k > 0);
+                            umma_ss_warp2(tmem + TM_S + sb * NH, dlo + (uint32_t)(cb * (PAGE * 128 / 16) + (k & 3) * 2), DH,
+                                          dq + (uint32_t)(cb * (NH * 128 / 16) + (k & 3) * 2), DH, ID_QK, k > 0);
                         }
                         qk_lo = true;
                         continue;
                     }
                     if (qk_lo && probe(bar.full + s1, ((h0 + 1) / NSLOT) & 1)) {
                         tc_fence_after();
-                        const uint64_t dhi = umma_desc_sw128(ring_a + slot_off(s1), 16, 1024);
-                        const uint64_t dq = dq0 + (uint64_t)(qb * (Q_BYTES / 16));
+                        const uint32_t dhi = desc_lo(ring_a + slot_off(s1), 16);
+                        const uint32_t dq = dq0 + (uint32_t)(qb * (Q_BYTES / 16));
 #pragma unroll
                         for (int k = CB_LO * 4; k < DK / 16; ++k) {
                             const int cb = k >> 2;
-                            umma_ss_warp(tmem + TM_S + sb * NH, dhi + (uint64_t)((cb - CB_LO) * (PAGE * 128 / 16) + (k & 3) * 2),
-                                         dq + (uint64_t)(cb * (NH * 128 / 16) + (k & 3) * 2), ID_QK, 1u);
+                            umma_ss_warp2(tmem + TM_S + sb * NH, dhi + (uint32_t)((cb - CB_LO) * (PAGE * 128 / 16) + (k & 3) * 2), DH,
+                                          dq + (uint32_t)(cb * (NH * 128 / 16) + (k & 3) * 2), DH, ID_QK, 1u);
                         }
                         umma_commit_warp(bar.s_full + sb);
                         if (lane == 0) TL_REC(2, t, TL_NOW(), 0, 0);

@@ -222,8 +222,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         constexpr uint32_t ID_PV = SWAP ? umma_idesc_bf16_f32_ab(128, BM, 1, 0)
                                         : umma_idesc_bf16_f32_ab(BM, 256, 0, 1);
         const uint32_t ring_a = smem_u32(ring);
-        const uint64_t dq0 = umma_desc_sw128(smem_u32(qs), 16, 1024);
-        const uint64_t dp0 = umma_desc_sw128(smem_u32(ps), 16, 1024);
+        const uint32_t dq0 = desc_lo(smem_u32(qs), 16);  // (low, high) descriptor words (umma_ss_warp2)
+        constexpr uint32_t DH = DESC_HI_SBO1K;
+        const uint32_t dp0 = desc_lo(smem_u32(ps), 16);
         auto probe = [&](const uint64_t* b, uint32_t par) {
             bool r = false;
             if (lane == 0) r = mbar_test_wait(b, par);
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int h0 = gh + 2 * npv;
                     const int s0 = h0 % NSLOT, s1 = (h0 + 1) % NSLOT;
                     tc_fence_after();
-                    const uint64_t dpa = dp0 + (uint64_t)((pb % NPBUF) * (P_BYTES / 16));
+                    const uint32_t dpa = dp0 + (uint32_t)((pb % NPBUF) * (P_BYTES / 16));
                     if constexpr (SWAP) {
                         // O^T[dv block m] += V^T[128 dv x 64 keys] . P^T: V^T MN-major straight
                         // from the page boxes (LBO 8 KiB between 64-column blocks, SBO 1 KiB
@@ -256,26 +257,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         for (int m = 0; m < DV / 128; ++m) {
                             const uint32_t a0 = m < 2 ? lo + m * (2 * PAGE * 128)
                                                       : hi + (2 * m - CB_LO) * (PAGE * 128);
-                            const uint64_t da = umma_desc_sw128(a0, PAGE * 128, 1024);
+                            const uint32_t da = desc_lo(a0, PAGE * 128);
 #pragma unroll
                             for (int ks = 0; ks < PAGE / 16; ++ks)
-                                umma_ss_warp(tmem + TM_O + m * BM, da + (uint64_t)(ks * 128),
-                                             dpa + (uint64_t)(ks * 2), ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
+                                umma_ss_warp2(tmem + TM_O + m * BM, da + (uint32_t)(ks * 128), DH,
+                                             dpa + (uint32_t)(ks * 2), DH, ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
                             if (m == 1) umma_commit_warp(bar.empty + s0);
                         }
                     } else {
                         // V^T blocks: dv [0,256) = column blocks 0-3 (first box), [256,512) = 4-7
-                        const uint64_t dvlo = umma_desc_sw128(ring_a + slot_off(s0), PAGE * 128, 1024);
-                        const uint64_t dvhi = umma_desc_sw128(ring_a + slot_off(s1), PAGE * 128, 1024);
+                        const uint32_t dvlo = desc_lo(ring_a + slot_off(s0), PAGE * 128);
+                        const uint32_t dvhi = desc_lo(ring_a + slot_off(s1), PAGE * 128);
 #pragma unroll
                         for (int ks = 0; ks < PAGE / 16; ++ks)
-                            umma_ss_warp(tmem + TM_O, dpa + (uint64_t)(ks * 2), dvlo + (uint64_t)(ks * 128),
+                            umma_ss_warp2(tmem + TM_O, dpa + (uint32_t)(ks * 2), DH, dvlo + (uint32_t)(ks * 128), DH,
                                          ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
                         umma_commit_warp(bar.empty + s0);
 #pragma unroll
                         for (int ks = 0; ks < PAGE / 16; ++ks)
-                            umma_ss_warp(tmem + TM_O + (16u << 16), dpa + (uint64_t)(ks * 2),
-                                         dvhi + (uint64_t)(ks * 128), ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
+                            umma_ss_warp2(tmem + TM_O + (16u << 16), dpa + (uint32_t)(ks * 2), DH,
+                                         dvhi + (uint32_t)(ks * 128), DH, ID_PV, (npv > 0 || ks > 0) ? 1u : 0u);
                     }
                     umma_commit_warp(bar.o_done + pb);
                     umma_commit_warp(bar.empty + s1);
@@ -289,13 +290,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (q_ok && !qk_lo && probe(bar.s_empty + sb, ((t >> 1) & 1) ^ 1) &&
                         probe(bar.full + s0, (h0 / NSLOT) & 1)) {
                         tc_fence_after();
-                        const uint64_t dk = umma_desc_sw128(ring_a + slot_off(s0), 16, 1024);
+                        const uint32_t dk = desc_lo(ring_a + slot_off(s0), 16);
 #pragma unroll
                         for (int k = 0; k < CB_LO * 4; ++k) {
                             const int cb = k >> 2;
-                            umma_ss_warp(tmem + TM_S + sb * PAGE,
-                                         dq0 + (uint64_t)(cb * (BM * 128 / 16) + (k & 3) * 2),
-                                         dk + (uint64_t)(cb * (PAGE * 128 / 16) + (k & 3) * 2), ID_QK,
+                            umma_ss_warp2(tmem + TM_S + sb * PAGE,
+                                         dq0 + (uint32_t)(cb * (BM * 128 / 16) + (k & 3) * 2), DH,
+                                         dk + (uint32_t)(cb * (PAGE * 128 / 16) + (k & 3) * 2), DH, ID_QK,
                                          k > 0);
                         }
                         qk_lo = true;
@@ -303,13 +304,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     if (qk_lo && probe(bar.full + s1, ((h0 + 1) / NSLOT) & 1)) {
                         tc_fence_after();
-                        const uint64_t dk = umma_desc_sw128(ring_a + slot_off(s1), 16, 1024);
+                        const uint32_t dk = desc_lo(ring_a + slot_off(s1), 16);
 #pragma unroll
                         for (int k = CB_LO * 4; k < DK / 16; ++k) {
                             const int cb = k >> 2;
-                            umma_ss_warp(tmem + TM_S + sb * PAGE,
-                                         dq0 + (uint64_t)(cb * (BM * 128 / 16) + (k & 3) * 2),
-                                         dk + (uint64_t)((cb - CB_LO) * (PAGE * 128 / 16) + (k & 3) * 2),
+                            umma_ss_warp2(tmem + TM_S + sb * PAGE,
+                                         dq0 + (uint32_t)(cb * (BM * 128 / 16) + (k & 3) * 2), DH,
+                                         dk + (uint32_t)((cb - CB_LO) * (PAGE * 128 / 16) + (k & 3) * 2), DH,
                                          ID_QK, 1u);
                         }
                         umma_commit_warp(bar.s_full + sb);

@@ -368,6 +368,18 @@ __global__ void __launch_bounds__(NT, 1)
                     const uint32_t q_addr = smem_u32(sm.q[0]) + (uint32_t)t * HALF_BYTES;
                     const uint32_t k_addr = smem_u32(sm.k[it & 1]);
                     const uint32_t d_tmem = tmem + (uint32_t)(t * BN);
+#if SPD_MMA_WARP
+                    // descriptors as (low, high) words: the K16 offsets are 32-bit adds to the low
+                    // word on the uniform datapath (umma_ss_warp2)
+                    const uint32_t qd = desc_lo(q_addr, 16), kd = desc_lo(k_addr, 16);
+#pragma unroll
+                    for (int kk = 0; kk < HD / 16; ++kk) {
+                        const uint32_t koff = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
+                        const uint32_t qoff = (kk >> 2) * TILE_BYTES + (kk & 3) * 32;
+                        umma_ss_warp2(d_tmem, qd + (qoff >> 4), DESC_HI_SBO1K, kd + (koff >> 4), DESC_HI_SBO1K,
+                                      idesc_s, kk > 0 ? 1u : 0u);
+                    }
+#else
 #pragma unroll
                     for (int kk = 0; kk < HD / 16; ++kk) {
                         const uint32_t koff = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
@@ -375,6 +387,7 @@ __global__ void __launch_bounds__(NT, 1)
                         MMA_SS(d_tmem, kmajor_desc(q_addr + qoff), kmajor_desc(k_addr + koff),
                                 idesc_s, kk > 0 ? 1u : 0u);
                     }
+#endif
                     MMA_COMMIT(&sm.s_full[t]);
                 };
                 auto issue_pv = [&](int t, int& cnt, int it, bool first) {  // O_t += P_t V
@@ -389,9 +402,14 @@ __global__ void __launch_bounds__(NT, 1)
                         tc_fence_after();
 #pragma unroll
                         for (int kk = hf * 8 / kPvParts; kk < (hf + 1) * 8 / kPvParts; ++kk) {
+#if SPD_MMA_WARP
+                            umma_ts_warp2(o_tmem, p_tmem + (uint32_t)(kk * 8), desc_lo(v_addr, HALF_BYTES) + kk * (2048 >> 4),
+                                          DESC_HI_SBO1K, idesc_o, (first && kk == 0) ? 0u : 1u);
+#else
                             const uint64_t bdesc = umma_desc_sw128(v_addr + kk * 2048, HALF_BYTES, 1024);
                             MMA_TS(o_tmem, p_tmem + (uint32_t)(kk * 8), bdesc, idesc_o,
                                     (first && kk == 0) ? 0u : 1u);
+#endif
                         }
                     }
                     ++cnt;

@@ -169,27 +169,35 @@ struct XPrep {
 };
 
 __global__ void __launch_bounds__(1024) mla_exp_prep_kernel(XPrep p) {
-    // per-request metadata in smem (every CTA scans; n <= 1024 requests is a few hundred cycles)
+    // per-request metadata in smem (every CTA loads and scans it; n <= 1024 requests): chunk
+    // offsets, prefixes and block-table rows first (coalesced), then the tile-offset scan
     __shared__ int s_off[XMAXN + 1];
     __shared__ int s_cu[XMAXN + 1];
+    __shared__ int s_P[XMAXN];
+    __shared__ int s_rid[XMAXN];
     __shared__ int s_warp[32];
     if (threadIdx.x == 0) span_begin(p.span);
-    const int* cu = p.cu;
-    const int* prefix = p.prefix;
-    // split-pair offsets first (s_off is reused for the tile offsets below)
-    x_scan([&](int i) { return x_split_pairs(__ldg(prefix + i), __ldg(cu + i + 1) - __ldg(cu + i)); },
-           p.n, s_off, s_warp);
-    if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i <= p.n; i += blockDim.x) p.hdr[p.n + 1 + i] = s_off[i];
-    const long long n_slots = (long long)s_off[p.n] * p.H;
-    __syncthreads();
-    x_scan([&](int i) { return (__ldg(prefix + i) + __ldg(cu + i + 1) - __ldg(cu + i) + XBM - 1) / XBM; },
-           p.n, s_off, s_warp);
     for (int i = threadIdx.x; i <= p.n; i += blockDim.x) {
         s_cu[i] = __ldg(p.cu + i);
-        if (blockIdx.x == 0) p.hdr[i] = s_off[i];
+        if (i < p.n) {
+            s_P[i] = __ldg(p.prefix + i);
+            s_rid[i] = __ldg(p.req_ids + i);
+        }
     }
     __syncthreads();
+    long long n_slots = 0;
+    if constexpr (kXSplit) {  // split-pair offsets first (s_off is reused for the tile offsets)
+        x_scan([&](int i) { return x_split_pairs(s_P[i], s_cu[i + 1] - s_cu[i]); }, p.n, s_off, s_warp);
+        if (blockIdx.x == 0)
+            for (int i = threadIdx.x; i <= p.n; i += blockDim.x) p.hdr[p.n + 1 + i] = s_off[i];
+        n_slots = (long long)s_off[p.n] * p.H;
+        __syncthreads();
+    } else if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i <= p.n; i += blockDim.x) p.hdr[p.n + 1 + i] = 0;
+    }
+    x_scan([&](int i) { return (s_P[i] + s_cu[i + 1] - s_cu[i] + XBM - 1) / XBM; }, p.n, s_off, s_warp);
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i <= p.n; i += blockDim.x) p.hdr[i] = s_off[i];
     const int R = s_off[p.n] * XBM;
     if (R > p.rows_cap || n_slots > p.slots_cap) {  // max_total_keys was too small: write nothing
         if (threadIdx.x == 0) {
@@ -223,10 +231,10 @@ __global__ void __launch_bounds__(1024) mla_exp_prep_kernel(XPrep p) {
             if (g >= R) continue;
             const int i = x_find([&](int q) { return s_off[q]; }, p.n, g / XBM);
             const int j = g - s_off[i] * XBM;
-            const int P = __ldg(p.prefix + i), c0 = s_cu[i], nk = P + s_cu[i + 1] - c0;
+            const int P = s_P[i], c0 = s_cu[i], nk = P + s_cu[i + 1] - c0;
             if (j >= nk) continue;
             const int page = j >> p.lg_bs;
-            const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + i) * p.MBR + page) : -1;
+            const int blk = page < p.MBR ? __ldg(p.bt + (size_t)s_rid[i] * p.MBR + page) : -1;
             if (blk < 0 || blk >= p.N_B) {
                 if (lane == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
                 continue;

@@ -423,6 +423,209 @@ __global__ void __launch_bounds__(GNT, 1)
     if (threadIdx.x == 0) span_end(p.span);
 }
 
+// ------------------------------------------------------------------ 2'. up-projection GEMM, A in TMEM
+// The same product with the latent tile held in TMEM (the MMA's A operand, K packed two bf16 per
+// column: cols [0, 256)) and only W streamed through shared memory, so each SM ingests 128 B of
+// operands per 128 x 128 x 16 MMA (64 cycles) instead of the SS form's 48 KiB per 512 cycles.
+// Work item = (128-key m-tile, XG consecutive 128-column n-tiles = XG heads of K or V); the
+// epilogue warps stage the item's A rows (global -> registers -> tcgen05.st) and then drain the
+// double-buffered 128-column accumulators (cols [256, 512)); while an item's n-tiles run they
+// already hold the first half of the next item's rows in registers.
+// SPD_X_GEMM_TA = 1 selects this kernel.  Parity-green (33/33) but measured SLOWER than the SS
+// GEMM at every budget (C = 2048, P = 0: 241 / 365 / 655 vs 283 / 414 / 740 TFLOP/s at 44 / 74 /
+// 148 SMs; profiles/r2_mla_expanded_gemm_ta_ab.log): the A staging between items (a global load
+// round trip and 8 TMEM stores per thread, the MMA idle meanwhile) and the N = 128 tiles cost more
+// than the halved operand traffic gains.  Default 0.
+#ifndef SPD_X_GEMM_TA
+#define SPD_X_GEMM_TA 0
+#endif
+constexpr bool kXGemmTA = SPD_X_GEMM_TA != 0;
+constexpr int XG = 4;                         // n-tiles (heads) per work item
+constexpr int TCB = 2;                        // 64-column blocks per B stage
+constexpr int TST = 6;                        // B stages in flight
+constexpr uint32_t TB = 128 * 128 * TCB;      // B stage: 128 rows x 128 cols (32 KiB, one box)
+
+struct TSmem {
+    unsigned char b[TST][TB];
+    uint64_t full[TST], empty[TST], dfull[2], dempty[2], a_full, a_free;
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(GNT, 1)
+    mla_exp_gemm_ta_kernel(const __grid_constant__ CUtensorMap ukmap, const __grid_constant__ CUtensorMap uvmap,
+                           const uint4* __restrict__ lat, XGemm p) {
+    if ((long long)__ldg(p.hdr + p.n) * XBM > p.rows_cap) return;  // INVALID (set by the prep kernel)
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    TSmem& sm = *reinterpret_cast<TSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int warp = (int)warp_id(), lane = (int)lane_id();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TST; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.dfull[s], 1);
+            mbar_init(&sm.dempty[s], 128);
+        }
+        mbar_init(&sm.a_full, 128);
+        mbar_init(&sm.a_free, 1);
+        fence_mbar_init();
+        span_begin(p.span);
+    }
+    if (warp == 1) tmem_alloc(&sm.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+    const int MT = __ldg(p.hdr + p.n);
+    const int NG = 2 * p.H / XG;  // items per m-tile
+    const int total = MT * NG;
+    constexpr int KS = XDC / (64 * TCB);  // B stages per n-tile
+
+    if (warp == 0) {
+        // ================================ TMA producer (W rows) ================================
+        if (lane == 0) {
+            tma_prefetch_desc(&ukmap);
+            tma_prefetch_desc(&uvmap);
+        }
+        int sc = 0;
+        for (int it = blockIdx.x; it < total; it += gridDim.x) {
+            const int g = it % NG;
+            for (int j = 0; j < XG; ++j) {
+                const int nt = g * XG + j;  // < H: K head nt; else V head nt - H
+                const CUtensorMap* bm = nt < p.H ? &ukmap : &uvmap;
+                const int brow = (nt < p.H ? nt : nt - p.H) * XDN;
+                for (int ks = 0; ks < KS; ++ks, ++sc) {
+                    const int s = sc % TST;
+                    if (lane == 0) {
+                        mbar_wait(&sm.empty[s], ((sc / TST) & 1) ^ 1);
+                        mbar_arrive_expect_tx(&sm.full[s], TB);
+                        tma_load_3d(sm.b[s], bm, &sm.full[s], 0, brow, ks * TCB);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================================ MMA issuer (A from TMEM) ================================
+        const uint32_t idesc = umma_idesc_bf16_f32(XBM, XDN, 0);
+        int sc = 0, dt = 0, li = 0;
+        for (int it = blockIdx.x; it < total; it += gridDim.x, ++li) {
+            mbar_wait(&sm.a_full, li & 1);
+            tc_fence_after();
+            for (int j = 0; j < XG; ++j, ++dt) {
+                const int db = dt & 1;
+                mbar_wait(&sm.dempty[db], ((dt >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + 256u + (uint32_t)(db * XDN);
+                for (int ks = 0; ks < KS; ++ks, ++sc) {
+                    const int s = sc % TST;
+                    mbar_wait(&sm.full[s], (sc / TST) & 1);
+                    tc_fence_after();
+                    const uint32_t bl = desc_lo(smem_u32(sm.b[s]), 16);
+#pragma unroll
+                    for (int kk = 0; kk < 4 * TCB; ++kk)
+                        umma_ts_warp2(d, tmem + (uint32_t)(ks * 64 + kk * 8),
+                                      bl + (uint32_t)(((kk >> 2) * 128 * 128 + (kk & 3) * 32) >> 4), DESC_HI_SBO1K,
+                                      idesc, (ks | kk) ? 1u : 0u);
+                    umma_commit_warp(&sm.empty[s]);
+                }
+                umma_commit_warp(&sm.dfull[db]);
+            }
+            umma_commit_warp(&sm.a_free);  // every MMA of the item done: A may be replaced
+        }
+    } else {
+        // ===== warps 2-5: stage A rows into TMEM, drain the accumulators (fp32 -> bf16 RNE) =====
+        const int q4 = warp & 3;
+        const int r = q4 * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+        constexpr int LU = XDC * 2 / 16;  // 64 uint4 per latent row
+        uint4 nxt[LU / 2];                // first half of the next item's row
+        auto load_half = [&](int it, int h, uint4 (&v)[LU / 2]) {
+            const uint4* src = lat + ((size_t)(it / NG) * XBM + r) * LU + h * (LU / 2);
+#pragma unroll
+            for (int c = 0; c < LU / 2; ++c) v[c] = __ldg(src + c);
+        };
+        auto store_half = [&](int h, const uint4 (&v)[LU / 2]) {  // 32 uint4 = 128 columns
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t w[32];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    w[4 * e + 0] = v[c * 8 + e].x;
+                    w[4 * e + 1] = v[c * 8 + e].y;
+                    w[4 * e + 2] = v[c * 8 + e].z;
+                    w[4 * e + 3] = v[c * 8 + e].w;
+                }
+                tmem_st32(tmem + lane_base + (uint32_t)(h * 128 + c * 32), w);
+            }
+        };
+        // A of item `it` into TMEM: the prefetched first half + the second half loaded now
+        auto stage = [&](int it) {
+            uint4 h1[LU / 2];
+            load_half(it, 1, h1);
+            store_half(0, nxt);
+            store_half(1, h1);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&sm.a_full);
+            if (it + (int)gridDim.x < total) load_half(it + gridDim.x, 0, nxt);
+        };
+        int dt = 0;
+        if (blockIdx.x < total) {
+            load_half(blockIdx.x, 0, nxt);
+            stage(blockIdx.x);
+        }
+        for (int it = blockIdx.x; it < total; it += gridDim.x) {
+            const int mt = it / NG, g = it % NG;
+            const int i = x_find([&](int k) { return __ldg(p.hdr + k); }, p.n, mt);
+            const int kbase = (mt - __ldg(p.hdr + i)) * XBM;
+            const int nk = __ldg(p.prefix + i) + __ldg(p.cu + i + 1) - __ldg(p.cu + i);
+            const bool valid = kbase + r < nk;
+            const size_t row = (size_t)mt * XBM + r;
+            for (int j = 0; j < XG; ++j, ++dt) {
+                const int db = dt & 1;
+                const int nt = g * XG + j;
+                __nv_bfloat16* base = nt < p.H ? p.kexp : p.vexp;
+                const int h = nt < p.H ? nt : nt - p.H;
+                mbar_wait(&sm.dfull[db], (dt >> 1) & 1);
+                tc_fence_after();
+                if (j == XG - 1 && it + (int)gridDim.x < total) {
+                    // the item's last accumulator is complete, so are all its MMAs: the next
+                    // item's A goes in first (the MMA warp restarts on the other accumulator)
+                    mbar_wait(&sm.a_free, ((dt / XG) & 1));
+                    stage(it + gridDim.x);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(base + (row * p.H + h) * XDN);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + lane_base + (uint32_t)(256 + db * XDN + c * 32), v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; e += 8) {
+                        uint4 o = make_uint4(0u, 0u, 0u, 0u);
+                        if (valid) {
+                            o.x = pack_bf16(__uint_as_float(v[e + 0]), __uint_as_float(v[e + 1]));
+                            o.y = pack_bf16(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                            o.z = pack_bf16(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5]));
+                            o.w = pack_bf16(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7]));
+                        }
+                        dst[c * 4 + e / 8] = o;
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&sm.dempty[db]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+    if (threadIdx.x == 0) span_end(p.span);
+}
+
 // ------------------------------------------------------------------ 3. attention
 constexpr int ANT = 384;
 constexpr int NSLOT = 8;
@@ -1082,20 +1285,41 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     gp.N_B = c.num_blocks;
     gp.rows_cap = (long long)rows;
     const size_t gsm = sizeof(GSmem) + 1024;
+    const size_t tsm = sizeof(TSmem) + 1024;
     const size_t asm_ = sizeof(ASmem) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(mla_exp_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(mla_exp_gemm_ta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
                 cudaSuccess ||
             cudaFuncSetAttribute(mla_exp_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_) !=
                 cudaSuccess)
             return SEMIPD_ERR_CUDA;
         attr_set = true;
     }
-    const long long gtiles = (long long)max_mt * H;
-    int ggrid = budget > 0 ? budget : (int)(gtiles < (1 << 30) ? gtiles : (1 << 30));
-    if (ggrid > gtiles) ggrid = (int)gtiles;
-    mla_exp_gemm_kernel<<<ggrid, GNT, gsm, st>>>(amap, ukmap, uvmap, gp);
+    if (kXGemmTA) {
+        // W views for the A-in-TMEM GEMM: one box = 128 rows (one head) x 128 columns
+        CUtensorMap tuk, tuv;
+        const uint32_t tbox[3] = {64, XDN, TCB};
+        const uint64_t bdims[3] = {64, (uint64_t)H * XDN, XDC / 64}, bstr[2] = {XDC * 2, 128};
+        if (!spd_encode_tiled_3d(&tuk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(w_uk), bdims[0],
+                                 bdims[1], bdims[2], bstr[0], bstr[1], tbox[0], tbox[1], tbox[2],
+                                 CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !spd_encode_tiled_3d(&tuv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<void*>(w_uv), bdims[0],
+                                 bdims[1], bdims[2], bstr[0], bstr[1], tbox[0], tbox[1], tbox[2],
+                                 CU_TENSOR_MAP_SWIZZLE_128B))
+            return SEMIPD_ERR_CUDA;
+        const long long items = (long long)max_mt * (2 * H / XG);
+        int tgrid = budget > 0 ? budget : (int)(items < (1 << 30) ? items : (1 << 30));
+        if (tgrid > items) tgrid = (int)items;
+        mla_exp_gemm_ta_kernel<<<tgrid, GNT, tsm, st>>>(tuk, tuv, reinterpret_cast<const uint4*>(lat), gp);
+    } else {
+        const long long gtiles = (long long)max_mt * H;
+        int ggrid = budget > 0 ? budget : (int)(gtiles < (1 << 30) ? gtiles : (1 << 30));
+        if (ggrid > gtiles) ggrid = (int)gtiles;
+        mla_exp_gemm_kernel<<<ggrid, GNT, gsm, st>>>(amap, ukmap, uvmap, gp);
+    }
     pool->launches += 1;
     if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
 

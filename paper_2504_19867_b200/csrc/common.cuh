@@ -505,6 +505,15 @@ SPD_DEV void add_bf16x2_f32(float& a, float& b, uint32_t pp) {
         : "r"(pp));
 }
 
+// Programmatic dependent launch (the attention kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, internal.h spd_launch_pdl): a kernel may
+// start while the previous kernel on its stream drains; pdl_wait() blocks until that kernel has
+// completed and its memory is visible, so it comes before any dependent global access.
+// pdl_trigger() lets the next kernel's CTAs be scheduled once every CTA of this grid has issued
+// it (or exited).
+SPD_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SPD_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // named barrier among `nthreads` threads (id 1..15; 0 is __syncthreads)
 SPD_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

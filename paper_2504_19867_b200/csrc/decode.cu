@@ -186,7 +186,6 @@ __global__ void __launch_bounds__(4 * 32, 1)
             mbar_init(uempty + i, CW);
         }
         fence_mbar_init();
-        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -195,6 +194,8 @@ __global__ void __launch_bounds__(4 * 32, 1)
         }
     }
     __syncthreads();
+    pdl_wait();  // PDL: the previous kernel on this stream is complete (workspace, pool)
+    if (threadIdx.x == 0) span_begin(p.span);
 
     // cross-warp merge of the consumer warps' partials (scratch rows = q heads of the group),
     // then the output (or the split partial and, by the last split, the split-order merge)
@@ -345,7 +346,10 @@ __global__ void __launch_bounds__(4 * 32, 1)
             __syncwarp();
             if (lane == 0) TL_REC(3, nunit, tu0, tu1, TL_NOW());
             ++nunit;
-            if (d.b < 0) break;
+            if (d.b < 0) {  // no more units: the next kernel on the stream may be scheduled
+                pdl_trigger();
+                break;
+            }
             const int* btr = p.bt + (size_t)rid * p.MBR;
             const int last_page = ctx >> p.lg_bs;
             // fused append of this step's K/V at slot ctx (last split only, bit-exact): the
@@ -839,7 +843,6 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             mbar_init(uempty + i, 2 * P_NCW);
         }
         fence_mbar_init();
-        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -848,6 +851,8 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
         }
     }
     __syncthreads();
+    pdl_wait();  // PDL: the previous kernel on this stream is complete (workspace, pool)
+    if (threadIdx.x == 0) span_begin(p.span);
 
     if (warp == 2 * P_NCW) {
         // =========================== producer ===========================
@@ -899,7 +904,10 @@ __global__ void __launch_bounds__(P_NTHREADS, 1)
             }
             __syncwarp();
             ++nunit;
-            if (d.b < 0) break;
+            if (d.b < 0) {  // no more units: the next kernel on the stream may be scheduled
+                pdl_trigger();
+                break;
+            }
             const int ctx = __ldg(p.ctx_lens + d.b);
             const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
             const int last_page = ctx >> p.lg_bs;
@@ -1364,8 +1372,10 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
         }
         int grid = budget > 0 ? budget : prm.n_units;
         if (grid > prm.n_units) grid = prm.n_units;
-        kern<<<grid, P_NTHREADS, smem, st>>>(pool->dkmap2[layer], pool->dvmap2[layer], prm);
-        if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
+        if (spd_launch_pdl(kern, dim3(grid), dim3(P_NTHREADS), smem, st, pool->dkmap2[layer], pool->dvmap2[layer],
+                           prm) != cudaSuccess ||
+            cudaGetLastError() != cudaSuccess)
+            return SEMIPD_ERR_CUDA;
         pool->launches += 1;
         return SEMIPD_OK;
     }
@@ -1384,8 +1394,8 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
             if (e != cudaSuccess) return;
             attr_set[ai] = true;
         }
-        kern<<<grid, nthreads, smem, st>>>(pool->dkmap[layer], pool->dvmap[layer], prm);
-        e = cudaGetLastError();
+        e = spd_launch_pdl(kern, dim3(grid), dim3(nthreads), smem, st, pool->dkmap[layer], pool->dvmap[layer], prm);
+        if (e == cudaSuccess) e = cudaGetLastError();
     };
     if (lg_r == 4) swap ? launch(decode_bf16_kernel<4, true>) : launch(decode_bf16_kernel<4, false>);
     else if (lg_r == 5) swap ? launch(decode_bf16_kernel<5, true>) : launch(decode_bf16_kernel<5, false>);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <utility>
 #include <vector>
 
 #include "semipd.h"
@@ -209,3 +210,24 @@ semipd_status spd_launch_simt_attn(semipd_pool_t p, int layer, const void* q, co
                                    const int* req_ids, const int* pos0, int n, int total_rows,
                                    int mode, int Hq, float scale, void* out, int out_head_major,
                                    int budget, int* status_dev, cudaStream_t s);
+
+// Launch `k` on st with programmatic stream serialization (PDL): the kernel's prologue may
+// overlap the previous kernel's tail; every kernel launched this way calls pdl_wait() before
+// its first dependent global access.  SEMIPD_NO_PDL=1 in the environment launches plainly (A/B).
+bool spd_pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t spd_launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                           Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = spd_pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+

@@ -411,3 +411,9 @@ extern "C" semipd_status semipd_debug_set_timeline(semipd_pool_t pool, void* buf
     return SEMIPD_OK;
 }
 #endif
+
+bool spd_pdl_enabled() {
+    static const bool on = getenv("SEMIPD_NO_PDL") == nullptr;
+    return on;
+}
+

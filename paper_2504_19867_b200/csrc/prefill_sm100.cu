@@ -210,7 +210,6 @@ __global__ void __launch_bounds__(NT, 1)
             mbar_init(&sm.uempty[s], 1 + 8 + 1);  // MMA warp + 8 softmax warps + V producer
         }
         fence_mbar_init();
-        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -227,6 +226,8 @@ __global__ void __launch_bounds__(NT, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();  // PDL: the previous kernel on this stream is complete (sched counters, pool)
+    if (threadIdx.x == 0) span_begin(p.span);
     const uint32_t tmem = sm.tmem_base;
 
     if (warp < 4) {
@@ -285,7 +286,10 @@ __global__ void __launch_bounds__(NT, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.uempty[us]);
             }
-            if (d.i < 0) break;
+            if (d.i < 0) {  // no more units: the next kernel on the stream may be scheduled
+                pdl_trigger();
+                break;
+            }
             if (!kv && lane == 0) {
                 // Q tiles A and B (rows = tokens x G heads of kv head g)
                 [[maybe_unused]] const long long tq0 = TL_NOW();
@@ -995,10 +999,12 @@ extern "C" semipd_status semipd_prefill_attn(
     }
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;
-    if (prm.n_peers > 0)
-        prefill_tc_kernel<true><<<grid, NT, smem, st>>>(qmap, *pkmap, *pvmap, kcmap, vcmap, omap, prm);
-    else
-        prefill_tc_kernel<false><<<grid, NT, smem, st>>>(qmap, *pkmap, *pvmap, kcmap, vcmap, omap, prm);
+    const cudaError_t le = prm.n_peers > 0
+        ? spd_launch_pdl(prefill_tc_kernel<true>, dim3(grid), dim3(NT), smem, st, qmap, *pkmap, *pvmap, kcmap,
+                         vcmap, omap, prm)
+        : spd_launch_pdl(prefill_tc_kernel<false>, dim3(grid), dim3(NT), smem, st, qmap, *pkmap, *pvmap, kcmap,
+                         vcmap, omap, prm);
+    if (le != cudaSuccess) return SEMIPD_ERR_CUDA;
     pool->launches += 1;
     return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }

@@ -216,7 +216,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(bar.q_empty + i, 1);
         }
         fence_mbar_init();
-        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -234,6 +233,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();  // PDL: the previous kernel on this stream is complete (workspace counters, pool)
+    if (threadIdx.x == 0) span_begin(p.span);
     const uint32_t tmem = *tmem_base;
 
     if (warp == 0) {
@@ -280,7 +281,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             __syncwarp();
             ++nunit;
-            if (d.b < 0) break;
+            if (d.b < 0) {  // no more units: the next kernel on the stream may be scheduled
+                pdl_trigger();
+                break;
+            }
             const int* btr = p.bt + (size_t)rid * p.MBR;
             const int last_page = ctx / PAGE;
             // fused append (last split only): the step's latent row (576 bf16 = 72 x 16 B) goes
@@ -961,8 +965,8 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
     }
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;
-    decode_mla_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(pool->mla_lo[layer], pool->mla_hi[layer],
-                                                             qmap, prm);
+    const cudaError_t le = spd_launch_pdl(decode_mla_tc_kernel, dim3(grid), dim3(NTHREADS), SMEM_BYTES, st,
+                                          pool->mla_lo[layer], pool->mla_hi[layer], qmap, prm);
     pool->launches += 1;
-    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+    return le == cudaSuccess && cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }

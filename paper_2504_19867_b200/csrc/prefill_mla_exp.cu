@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(1024) mla_exp_prep_kernel(XPrep p) {
     __shared__ int s_P[XMAXN];
     __shared__ int s_rid[XMAXN];
     __shared__ int s_warp[32];
+    pdl_wait();  // PDL: the previous kernel on this stream (it may read this workspace) is complete
     if (threadIdx.x == 0) span_begin(p.span);
     for (int i = threadIdx.x; i <= p.n; i += blockDim.x) {
         s_cu[i] = __ldg(p.cu + i);
@@ -264,6 +265,7 @@ __global__ void __launch_bounds__(1024) mla_exp_prep_kernel(XPrep p) {
             }
         }
     }
+    pdl_trigger();
     __syncthreads();
     if (threadIdx.x == 0) span_end(p.span);
 }
@@ -301,7 +303,6 @@ __device__ __forceinline__ uint64_t xk_desc(uint32_t addr) { return umma_desc_sw
 __global__ void __launch_bounds__(GNT, 1)
     mla_exp_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap ukmap,
                         const __grid_constant__ CUtensorMap uvmap, XGemm p) {
-    if ((long long)__ldg(p.hdr + p.n) * XBM > p.rows_cap) return;  // INVALID (set by the prep kernel)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     GSmem& sm = *reinterpret_cast<GSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = (int)warp_id(), lane = (int)lane_id();
@@ -315,16 +316,18 @@ __global__ void __launch_bounds__(GNT, 1)
             mbar_init(&sm.acce[s], 128);
         }
         fence_mbar_init();
-        span_begin(p.span);
     }
     if (warp == 1) tmem_alloc(&sm.tmem_base, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();  // PDL: the prep kernel (Lat, hdr) is complete
+    if (threadIdx.x == 0) span_begin(p.span);
     const uint32_t tmem = sm.tmem_base;
     const int MT = __ldg(p.hdr + p.n);
     const int NTN = p.H;  // n tiles of 256 columns: H / 2 head pairs of K_nope, then of V
-    const int total = MT * NTN;
+    // rows beyond the workspace: INVALID was set by the prep kernel; no tiles
+    const int total = (long long)MT * XBM > p.rows_cap ? 0 : MT * NTN;
     auto off = [&](int k) { return __ldg(p.hdr + k); };
 
     if (warp == 0) {
@@ -351,6 +354,7 @@ __global__ void __launch_bounds__(GNT, 1)
                 __syncwarp();
             }
         }
+        pdl_trigger();  // every tile's loads issued: the attention kernel may be scheduled
     } else if (warp == 1) {
         // ================================ MMA issuer ================================
         const uint32_t idesc = umma_idesc_bf16_f32(XBM, 256, 0);
@@ -454,7 +458,6 @@ struct TSmem {
 __global__ void __launch_bounds__(GNT, 1)
     mla_exp_gemm_ta_kernel(const __grid_constant__ CUtensorMap ukmap, const __grid_constant__ CUtensorMap uvmap,
                            const uint4* __restrict__ lat, XGemm p) {
-    if ((long long)__ldg(p.hdr + p.n) * XBM > p.rows_cap) return;  // INVALID (set by the prep kernel)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     TSmem& sm = *reinterpret_cast<TSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = (int)warp_id(), lane = (int)lane_id();
@@ -470,16 +473,17 @@ __global__ void __launch_bounds__(GNT, 1)
         mbar_init(&sm.a_full, 128);
         mbar_init(&sm.a_free, 1);
         fence_mbar_init();
-        span_begin(p.span);
     }
     if (warp == 1) tmem_alloc(&sm.tmem_base, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();
+    if (threadIdx.x == 0) span_begin(p.span);
     const uint32_t tmem = sm.tmem_base;
     const int MT = __ldg(p.hdr + p.n);
     const int NG = 2 * p.H / XG;  // items per m-tile
-    const int total = MT * NG;
+    const int total = (long long)MT * XBM > p.rows_cap ? 0 : MT * NG;
     constexpr int KS = XDC / (64 * TCB);  // B stages per n-tile
 
     if (warp == 0) {
@@ -772,7 +776,6 @@ __global__ void __launch_bounds__(ANT, 1)
             mbar_init(&sm.uempty[s], 1 + 8);  // MMA warp + 8 softmax warps
         }
         fence_mbar_init();
-        span_begin(p.span);
         if (p.trace.buf) {
             int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -784,6 +787,8 @@ __global__ void __launch_bounds__(ANT, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();  // PDL: the GEMM (K_exp, V_exp) and prep (Kpe, hdr) are complete
+    if (threadIdx.x == 0) span_begin(p.span);
     const uint32_t tmem = sm.tmem_base;
 
     if (warp < 4) {
@@ -845,7 +850,10 @@ __global__ void __launch_bounds__(ANT, 1)
                     mbar_arrive(&sm.ufull[us]);
                 }
                 __syncwarp();
-                if (d.i < 0) break;
+                if (d.i < 0) {  // no more units: the next kernel on the stream may be scheduled
+                    pdl_trigger();
+                    break;
+                }
                 if (lane == 0) {
                     mbar_wait(&sm.q_empty, (nunit & 1) ^ 1);
                     // (64 cols, head h, 256 tokens, 3 chunks) -> [chunk][A rows | B rows][128 B]
@@ -1245,7 +1253,8 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     int gprep = budget > 0 ? budget : pool->num_sms;
     const int prep_need = (int)((rows + 63) / 64);  // 32 warps x 2 rows per CTA and step
     if (gprep > prep_need) gprep = prep_need;
-    mla_exp_prep_kernel<<<gprep, 1024, 0, st>>>(pp);
+    if (spd_launch_pdl(mla_exp_prep_kernel, dim3(gprep), dim3(1024), 0, st, pp) != cudaSuccess)
+        return SEMIPD_ERR_CUDA;
     pool->launches += 1;
     if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
 
@@ -1313,12 +1322,16 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
         const long long items = (long long)max_mt * (2 * H / XG);
         int tgrid = budget > 0 ? budget : (int)(items < (1 << 30) ? items : (1 << 30));
         if (tgrid > items) tgrid = (int)items;
-        mla_exp_gemm_ta_kernel<<<tgrid, GNT, tsm, st>>>(tuk, tuv, reinterpret_cast<const uint4*>(lat), gp);
+        if (spd_launch_pdl(mla_exp_gemm_ta_kernel, dim3(tgrid), dim3(GNT), tsm, st, tuk, tuv,
+                           reinterpret_cast<const uint4*>(lat), gp) != cudaSuccess)
+            return SEMIPD_ERR_CUDA;
     } else {
         const long long gtiles = (long long)max_mt * H;
         int ggrid = budget > 0 ? budget : (int)(gtiles < (1 << 30) ? gtiles : (1 << 30));
         if (ggrid > gtiles) ggrid = (int)gtiles;
-        mla_exp_gemm_kernel<<<ggrid, GNT, gsm, st>>>(amap, ukmap, uvmap, gp);
+        if (spd_launch_pdl(mla_exp_gemm_kernel, dim3(ggrid), dim3(GNT), gsm, st, amap, ukmap, uvmap, gp) !=
+            cudaSuccess)
+            return SEMIPD_ERR_CUDA;
     }
     pool->launches += 1;
     if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
@@ -1362,7 +1375,9 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
         return SEMIPD_ERR_CUDA;
     int grid = budget > 0 ? budget : ap.n_units;
     if (grid > ap.n_units) grid = ap.n_units;
-    mla_exp_attn_kernel<<<grid, ANT, asm_, st>>>(qmap, kxmap, vxmap, pemap, ap);
+    if (spd_launch_pdl(mla_exp_attn_kernel, dim3(grid), dim3(ANT), asm_, st, qmap, kxmap, vxmap, pemap, ap) !=
+        cudaSuccess)
+        return SEMIPD_ERR_CUDA;
     pool->launches += 1;
     return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }

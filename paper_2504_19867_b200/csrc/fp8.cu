@@ -312,7 +312,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(uempty + i, 2 * NCW);
         }
         fence_mbar_init();
-        span_begin(p.span);
         if (p.trace.buf) {
             const int slot = atomicAdd(p.trace.ctr, 1);
             if (slot < p.trace.cap)
@@ -321,6 +320,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     }
     __syncthreads();
+    pdl_wait();  // PDL: the previous kernel on this stream is complete (workspace, pool)
+    if (threadIdx.x == 0) span_begin(p.span);
 
     if (warp == 2 * NCW) {
         // =========================== producer ===========================
@@ -388,7 +389,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             __syncwarp();
             ++nunit;
-            if (d.b < 0) break;
+            if (d.b < 0) {  // no more units: the next kernel on the stream may be scheduled
+                pdl_trigger();
+                break;
+            }
             const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
             const int last_page = ctx / BS;
             if (d.k0 <= ctx && ctx < d.k1) {
@@ -874,7 +878,9 @@ semipd_status spd_launch_decode_fp8(semipd_pool_t pool, int layer, const void* q
     }
     int grid = budget > 0 ? budget : prm.n_units;
     if (grid > prm.n_units) grid = prm.n_units;
-    decode_fp8_kernel<<<grid, NTHREADS, smem, st>>>(pool->f8kmap[layer], pool->f8vmap[layer], prm);
+    if (spd_launch_pdl(decode_fp8_kernel, dim3(grid), dim3(NTHREADS), smem, st, pool->f8kmap[layer],
+                       pool->f8vmap[layer], prm) != cudaSuccess)
+        return SEMIPD_ERR_CUDA;
     if (cudaGetLastError() != cudaSuccess) return SEMIPD_ERR_CUDA;
     pool->launches += 1;
     return SEMIPD_OK;

@@ -71,7 +71,13 @@ constexpr uint32_t Q_BYTES = NCB * NH * 128;            // 18 KiB
 constexpr uint32_t P_BYTES = NH * 128;                  // 2 KiB per buffer (2 buffers)
 constexpr int NTHREADS = 192;
 constexpr int NSOFT = 128;
-constexpr int SPLIT_PAGES = 20;  // a split spans at most 20 pages (1280 keys, 1.4 MiB)
+// SPD_MLA_SPLIT_PAGES: finer splits (8 / 12 / 16 pages) shorten the longest units' chains but
+// their partial write-back and merge cost more at every budget (cfg-5 lognormal batch at 104 SMs:
+// 0.052 / 0.048 / 0.044 vs 0.042 ms; profiles/r2_mla_decode_split_pages_ab.log).  Default 20.
+#ifndef SPD_MLA_SPLIT_PAGES
+#define SPD_MLA_SPLIT_PAGES 20
+#endif
+constexpr int SPLIT_PAGES = SPD_MLA_SPLIT_PAGES;  // a split spans at most this many pages (20: 1280 keys)
 
 // number of splits of a request with ctx cached tokens (ctx + 1 keys): a function of the
 // shape only (R26).  At least ceil(pages / 20) (1025 keys = 17 pages stay one unit).  The

@@ -146,6 +146,14 @@ __device__ __forceinline__ uint32_t pair_off(int key, int h) {
         return kv_off<LG_R>(key, h);
 }
 
+// SPD_DEC_KSPLIT = 1: separate barriers for a stage's K and V halves (see KS below).  Parity-
+// green (62 decode / co-run tests) but measured SLOWER (isolated, bs 64: 3274 / 5437 / 6032 vs
+// 3604 / 5702 / 6076 GB/s at 44 / 74 / 89 SMs; profiles/r2_decode_ksplit_ab.log): the one
+// producer lane now blocks on the V slot of every stage after issuing its K, so the next
+// stage's K goes out no earlier than before and the extra waits cost.  Default 0.
+#ifndef SPD_DEC_KSPLIT
+#define SPD_DEC_KSPLIT 0
+#endif
 template <int LG_R, bool SWAP>
 __global__ void __launch_bounds__(4 * 32, 1)
     decode_bf16_kernel(const __grid_constant__ CUtensorMap kmap,
@@ -156,6 +164,10 @@ __global__ void __launch_bounds__(4 * 32, 1)
     // 16 KiB one, so the producer warp streams them with 16-byte cp.async (LDGSTS) instead,
     // into the same 128-B-swizzled stage layout, 32 lanes arriving on the stage barrier
     constexpr bool CPA = LG_R == 4 && SPD_DEC_CPASYNC;
+    // KS: a stage's K and V halves have their own full / empty barriers, so a consumer hands
+    // the K half back to the producer as soon as S is computed (before softmax and P V): one
+    // more half-stage of loads in flight per held stage (SPD_DEC_KSPLIT, TMA path only)
+    constexpr bool KS = SPD_DEC_KSPLIT && !CPA;
     // consumer warps and scratch rows (the swap-AB partials have G <= 8 rows); 6 swap-AB
     // consumer warps measured 2-5 % slower than 3 (more padding stages and merge work)
     constexpr int CW = 3;
@@ -168,7 +180,9 @@ __global__ void __launch_bounds__(4 * 32, 1)
     float* scr_ml = scr_acc + CW * SR * HD;                       // [CW][16][2]
     uint64_t* full = reinterpret_cast<uint64_t*>(scr_ml + CW * SR * 2);
     uint64_t* empty = full + NSTAGE;
-    uint64_t* ufull = empty + NSTAGE;
+    uint64_t* fullV = KS ? empty + NSTAGE : full;   // V half (KS), else the stage barrier
+    uint64_t* emptyV = KS ? fullV + NSTAGE : empty;
+    uint64_t* ufull = KS ? emptyV + NSTAGE : empty + NSTAGE;
     uint64_t* uempty = ufull + 2;
     UnitDesc* units = reinterpret_cast<UnitDesc*>(uempty + 2);
     int* s_last = reinterpret_cast<int*>(units + 2);
@@ -180,6 +194,10 @@ __global__ void __launch_bounds__(4 * 32, 1)
         for (int i = 0; i < NSTAGE; ++i) {
             mbar_init(full + i, CPA ? 32 : 1);
             mbar_init(empty + i, 1);
+            if (KS) {
+                mbar_init(fullV + i, 1);
+                mbar_init(emptyV + i, 1);
+            }
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(ufull + i, 1);
@@ -331,6 +349,10 @@ __global__ void __launch_bounds__(4 * 32, 1)
                     if (lane == 0) mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
                     __syncwarp();
                     if (CPA || lane == 0) mbar_arrive(full + st);
+                    if (KS && lane == 0) {
+                        mbar_wait(emptyV + st, ((gstage / NSTAGE) & 1) ^ 1);
+                        mbar_arrive(fullV + st);
+                    }
                     ++gstage;
                 }
                 __syncwarp();
@@ -404,7 +426,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 if (lane == 0) {
                     mbar_wait(empty + st, ((gstage / NSTAGE) & 1) ^ 1);
                     tp1 = TL_NOW();
-                    if (!CPA) mbar_arrive_expect_tx(full + st, STAGE_BYTES);
+                    if (!CPA) mbar_arrive_expect_tx(full + st, KS ? KV_BYTES : STAGE_BYTES);
                 }
                 if constexpr (CPA) {
                     // every lane copies 8 of the 256 16-byte chunks of each 4 KiB K and V page
@@ -432,16 +454,30 @@ __global__ void __launch_bounds__(4 * 32, 1)
                     }
                     cp_async_mbar_arrive_noinc(full + st);
                 } else {
+                int zb[NB];
 #pragma unroll
                 for (int b = 0; b < NB; ++b) {
                     const int blk = __shfl_sync(0xffffffffu, zc, (bb0 & 31) + b);
-                    if (lane == 0) {
-                        int z = oob_z;
-                        if (blk >= 0 && blk < p.N_B) z = blk * p.Hkv + d.g;
-                        else if (blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                    zb[b] = oob_z;
+                    if (blk >= 0 && blk < p.N_B) zb[b] = blk * p.Hkv + d.g;
+                    else if (lane == 0 && blk != -2 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                }
+                if (lane == 0) {
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
                         const int y = (d.k0 + i * KPS + b * R) & bs_mask;
-                        tma_load_4d_hint(kst + b * (R * 256), &kmap, full + st, 0, y, 0, z, kv_pol);
-                        tma_load_4d_hint(kst + KV_BYTES + b * (R * 256), &vmap, full + st, 0, y, 0, z, kv_pol);
+                        tma_load_4d_hint(kst + b * (R * 256), &kmap, full + st, 0, y, 0, zb[b], kv_pol);
+                        if (!KS)
+                            tma_load_4d_hint(kst + KV_BYTES + b * (R * 256), &vmap, full + st, 0, y, 0, zb[b], kv_pol);
+                    }
+                    if (KS) {  // the V half goes out once its own slot is free
+                        mbar_wait(emptyV + st, ((gstage / NSTAGE) & 1) ^ 1);
+                        mbar_arrive_expect_tx(fullV + st, KV_BYTES);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) {
+                            const int y = (d.k0 + i * KPS + b * R) & bs_mask;
+                            tma_load_4d_hint(kst + KV_BYTES + b * (R * 256), &vmap, fullV + st, 0, y, 0, zb[b], kv_pol);
+                        }
                     }
                 }
                 if constexpr (SPD_DEC_PF > 0) {
@@ -501,8 +537,12 @@ __global__ void __launch_bounds__(4 * 32, 1)
             while (next_gs < d.base) {
                 const int st = next_gs % NSTAGE;
                 mbar_wait(full + st, (next_gs / NSTAGE) & 1);
+                if (KS) mbar_wait(fullV + st, (next_gs / NSTAGE) & 1);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(empty + st);
+                if (lane == 0) {
+                    mbar_arrive(empty + st);
+                    if (KS) mbar_arrive(emptyV + st);
+                }
                 next_gs += CW;
             }
             next_gs = d.base + (warp < d.nst ? warp + ((d.nst - 1 - warp) / CW + 1) * CW : warp);
@@ -529,6 +569,10 @@ __global__ void __launch_bounds__(4 * 32, 1)
                                 a2, a3);
                         mma_bf16_16816(s[kt], a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
                     }
+                }
+                if (KS) {  // every K ldmatrix of this stage has retired: hand the K half back
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + st);
                 }
                 // ---- mask + online softmax over keys, per head (log2 domain)
                 const int kbase = d.k0 + i * KPS;
@@ -578,6 +622,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                         acc[dt][3] *= alpha[1];
                     }
                 }
+                if (KS) mbar_wait(fullV + st, (gs / NSTAGE) & 1);
                 // ---- O^T += V^T P^T: 8 dv tiles x 4 key steps; A = V^T via ldmatrix.trans
 #pragma unroll
                 for (int kt = 0; kt < 4; ++kt) {
@@ -592,7 +637,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(empty + st);
+                if (lane == 0) mbar_arrive(KS ? emptyV + st : empty + st);
                 if (lane == 0) TL_REC(2, gs, tc0, tc1, TL_NOW());
             }
             // ---- per-warp partial -> shared scratch (rows = heads)
@@ -661,8 +706,12 @@ __global__ void __launch_bounds__(4 * 32, 1)
             while (next_gs < d.base) {
                 const int st = next_gs % NSTAGE;
                 mbar_wait(full + st, (next_gs / NSTAGE) & 1);
+                if (KS) mbar_wait(fullV + st, (next_gs / NSTAGE) & 1);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(empty + st);
+                if (lane == 0) {
+                    mbar_arrive(empty + st);
+                    if (KS) mbar_arrive(emptyV + st);
+                }
                 next_gs += CW;
             }
             next_gs = d.base + (warp < d.nst ? warp + ((d.nst - 1 - warp) / CW + 1) * CW : warp);
@@ -689,6 +738,10 @@ __global__ void __launch_bounds__(4 * 32, 1)
                         mma_bf16_16816(s[nt], qa[kk + 1][0], qa[kk + 1][1], qa[kk + 1][2],
                                        qa[kk + 1][3], b2, b3);
                     }
+                }
+                if (KS) {  // every K ldmatrix of this stage has retired: hand the K half back
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + st);
                 }
                 // ---- mask + online softmax (log2 domain); rows r0 (idx 0,1) and r0+8 (2,3)
                 const int kbase = d.k0 + i * KPS;
@@ -737,6 +790,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                         acc[nd][3] *= alpha[1];
                     }
                 }
+                if (KS) mbar_wait(fullV + st, (gs / NSTAGE) & 1);
                 // ---- O += P V : 16 dv n-tiles x 4 k-steps of 16 keys
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
@@ -753,7 +807,7 @@ __global__ void __launch_bounds__(4 * 32, 1)
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(empty + st);
+                if (lane == 0) mbar_arrive(KS ? emptyV + st : empty + st);
             }
             // ---- per-warp partial -> shared scratch
 #pragma unroll
@@ -1214,7 +1268,7 @@ size_t decode_pair_smem_bytes() {
 size_t decode_smem_bytes(bool swap) {
     const int cw = 3, sr = swap ? 8 : 16;
     return 1024 + NSTAGE * STAGE_BYTES + cw * sr * HD * 4 + cw * sr * 2 * 4 +
-           (2 * NSTAGE + 4) * 8 + 2 * sizeof(UnitDesc) + 16;
+           (4 * NSTAGE + 4) * 8 + 2 * sizeof(UnitDesc) + 16;  // (K, V) full / empty + unit barriers
 }
 
 bool fast_path_ok(const semipd_pool* p, int Hq) {

@@ -25,11 +25,18 @@ spd._build.up_to_date = lambda: True
 L = spd.lib()
 budget = int(sys.argv[1]) if len(sys.argv) > 1 else 148
 B, ctx = int(os.environ.get("TL_B", "256")), int(os.environ.get("TL_CTX", "1000"))
+if os.environ.get("TL_LOGN"):  # the bench's cfg-5 batch: lognormal around ctx, longest first
+    import numpy as np
+    rng = np.random.default_rng(5005)
+    ctxs = sorted((int(c) for c in np.clip(rng.lognormal(math.log(ctx) - 0.125, 0.5, B), 64, 4096)), reverse=True)
+else:
+    ctxs = [ctx] * B
+ctx = max(ctxs)
 dev = torch.device("cuda", 0)
 nb = ctx // 64 + 1
 pool = spd.KVPool(spd.PoolConfig(1, B * nb + 4, 64, 1, 576, 512, B + 1, nb + 1, kv_shared=True), dev)
 i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)
-pool.alloc_blocks(i32(list(range(B))), i32([nb] * B))
+pool.alloc_blocks(i32(list(range(B))), i32([c // 64 + 1 for c in ctxs]))
 K, _, _, _ = pool.views(0)
 K.normal_()
 q = torch.randn(B, 16, 576, device=dev).bfloat16()
@@ -43,7 +50,7 @@ for it in range(3):
     ctr.fill_(tl_cta)
     buf.zero_()
     L.semipd_debug_set_timeline(pool.h, ctypes.c_void_p(buf.data_ptr()), ctypes.c_void_p(ctr.data_ptr()))
-    pool.decode_attn(0, q, kn, None, i32(list(range(B))), i32([ctx] * B), ctx, 1 / math.sqrt(192), out, ws,
+    pool.decode_attn(0, q, kn, None, i32(list(range(B))), i32(ctxs), ctx, 1 / math.sqrt(192), out, ws,
                      sm_budget=budget)
     torch.cuda.synchronize()
 rec = [r for r in buf.view(-1, 8)[:, :5].cpu().tolist() if r[0] != 0]
@@ -58,6 +65,7 @@ if cta:
     ends = sorted(r[3] for r in cta)
     starts = sorted(r[2] for r in cta)
     print("CTA start ns: min %d max %d; end ns: min %d median %d max %d" % (starts[0], starts[-1], ends[0], ends[len(ends)//2], ends[-1]))
+    print("CTA end ns deciles:", [ends[int(len(ends) * k / 10)] for k in range(10)] + [ends[-1]])
     json.dump(cta, open(os.path.join(ROOT, "gpurun_out", "cta_times.json"), "w"))
 t0 = min(r[2] for r in rec)
 for r in rec:

@@ -150,7 +150,11 @@ __device__ __forceinline__ uint32_t pair_off(int key, int h) {
 // green (62 decode / co-run tests) but measured SLOWER (isolated, bs 64: 3274 / 5437 / 6032 vs
 // 3604 / 5702 / 6076 GB/s at 44 / 74 / 89 SMs; profiles/r2_decode_ksplit_ab.log): the one
 // producer lane now blocks on the V slot of every stage after issuing its K, so the next
-// stage's K goes out no earlier than before and the extra waits cost.  Default 0.
+// stage's K goes out no earlier than before and the extra waits cost.  = 2 issues each V half
+// after the next stage's K (no producer blocking): parity-green (62 tests), slower still (3068 /
+// 5111 / 5864 GB/s at 44 / 74 / 89 SMs; profiles/r2_decode_ksplit_ab.log).  At 89 SMs the
+// isolated kernel already streams 6.0 TB/s (0.92 of the copy peak): the ring is not what limits
+// it there.  Default 0.
 #ifndef SPD_DEC_KSPLIT
 #define SPD_DEC_KSPLIT 0
 #endif
@@ -168,6 +172,9 @@ __global__ void __launch_bounds__(4 * 32, 1)
     // the K half back to the producer as soon as S is computed (before softmax and P V): one
     // more half-stage of loads in flight per held stage (SPD_DEC_KSPLIT, TMA path only)
     constexpr bool KS = SPD_DEC_KSPLIT && !CPA;
+    // KS2 (SPD_DEC_KSPLIT = 2): the V half of stage i is issued after the K half of stage i + 1,
+    // so the producer never blocks on a V slot before the next K goes out
+    constexpr bool KS2 = KS && SPD_DEC_KSPLIT == 2;
     // consumer warps and scratch rows (the swap-AB partials have G <= 8 rows); 6 swap-AB
     // consumer warps measured 2-5 % slower than 3 (more padding stages and merge work)
     constexpr int CW = 3;
@@ -405,6 +412,17 @@ __global__ void __launch_bounds__(4 * 32, 1)
             prev_k0 = d.k0;
             zc0 = zc;
             zn0 = zn;
+            // KS2: the V half of the latest stage, issued after the next stage's K
+            bool pv_ok = false;
+            int pv_st = 0, pv_gs = 0, pv_y[NB], pv_z[NB];
+            auto issue_v = [&]() {
+                mbar_wait(emptyV + pv_st, ((pv_gs / NSTAGE) & 1) ^ 1);
+                mbar_arrive_expect_tx(fullV + pv_st, KV_BYTES);
+                unsigned char* vst_p = ring + pv_st * STAGE_BYTES + KV_BYTES;
+#pragma unroll
+                for (int b = 0; b < NB; ++b)
+                    tma_load_4d_hint(vst_p + b * (R * 256), &vmap, fullV + pv_st, 0, pv_y[b], 0, pv_z[b], kv_pol);
+            };
             for (int i = 0; i < d.nst; ++i, ++gstage) {
                 const int bb0 = i * NB;
                 if (bb0 > 0 && (bb0 & 31) == 0) {
@@ -470,7 +488,17 @@ __global__ void __launch_bounds__(4 * 32, 1)
                         if (!KS)
                             tma_load_4d_hint(kst + KV_BYTES + b * (R * 256), &vmap, full + st, 0, y, 0, zb[b], kv_pol);
                     }
-                    if (KS) {  // the V half goes out once its own slot is free
+                    if (KS2) {  // the previous stage's V, then remember this one's
+                        if (pv_ok) issue_v();
+                        pv_ok = true;
+                        pv_st = st;
+                        pv_gs = gstage;
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) {
+                            pv_y[b] = (d.k0 + i * KPS + b * R) & bs_mask;
+                            pv_z[b] = zb[b];
+                        }
+                    } else if (KS) {  // the V half goes out once its own slot is free
                         mbar_wait(emptyV + st, ((gstage / NSTAGE) & 1) ^ 1);
                         mbar_arrive_expect_tx(fullV + st, KV_BYTES);
 #pragma unroll
@@ -499,6 +527,8 @@ __global__ void __launch_bounds__(4 * 32, 1)
                 if (lane == 0) TL_REC(1, gstage, tp0, tp1, TL_NOW());
                 __syncwarp();
             }
+            if (KS2 && lane == 0 && pv_ok) issue_v();  // the unit's last V
+            __syncwarp();
         }
     } else if (SWAP) {
         // ================= consumers, swap-AB (G <= 8): heads are the MMA N =================

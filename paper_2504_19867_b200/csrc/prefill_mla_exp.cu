@@ -162,6 +162,7 @@ struct XPrep {
     int* hdr;
     int* status;
     int n, lg_bs, MBR, N_B, H;
+    int T;               // total_q: chunk rows of kv_new
     long long rows_cap;  // workspace rows (max_total_keys + 128 n)
     long long slots_cap; // split slots of the workspace
     int* cnt;            // split counters / flags [slots][2][2]
@@ -238,6 +239,10 @@ __global__ void __launch_bounds__(1024) mla_exp_prep_kernel(XPrep p) {
             const int blk = page < p.MBR ? __ldg(p.bt + (size_t)s_rid[i] * p.MBR + page) : -1;
             if (blk < 0 || blk >= p.N_B) {
                 if (lane == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+                continue;
+            }
+            if (j >= P && c0 + j - P >= p.T) {  // cu_seqlens_q beyond the host's total_q
+                if (lane == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_INVALID);
                 continue;
             }
             prow[u] = reinterpret_cast<uint4*>(p.pool + ((size_t)blk * (bs_mask + 1) + (j & bs_mask)) * (XDL * 2));
@@ -1125,7 +1130,8 @@ __global__ void __launch_bounds__(ANT, 1)
             if (lane == 0) mbar_arrive(&sm.uempty[us]);
             float la, lb;
             f2_split(l2, la, lb);
-            const bool valid = r < d.tv[t];
+            // rows past total_q (a cu_seqlens_q[n] larger than the host's total_q) are not stored
+            const bool valid = r < d.tv[t] && d.qrow0 + t * XBM + r < p.T;
             uint4* dst = reinterpret_cast<uint4*>(p.out + ((size_t)(d.qrow0 + t * XBM + r) * p.H + d.h) * XDV);
             if (d.slot < 0) {
                 const float inv = 1.f / (la + lb);
@@ -1248,6 +1254,7 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     pp.slots_cap = (long long)slots;
     pp.cnt = cnt;
     pp.H = H;
+    pp.T = total_q;
     pp.span = spd_next_span(pool);
     const int max_mt = (int)((rows + XBM - 1) / XBM);
     int gprep = budget > 0 ? budget : pool->num_sms;

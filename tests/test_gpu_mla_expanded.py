@@ -165,3 +165,26 @@ def test_mla_expanded_kernel_kind_and_unsupported_pool():
     with pytest.raises(SemipdError):
         gpool.prefill_mla_expanded(0, q, kn, w, w, i32([0, 100]), i32([0]), i32([0]), 100, 100, 100,
                                    0.07, out, ws)
+
+
+def test_mla_expanded_total_q_smaller_than_cu():
+    """A cu_seqlens_q[n] beyond the host's total_q: status INVALID, nothing read past kv_new and
+    nothing stored past out (a guard region after the output stays untouched)."""
+    from paper_2504_19867_b200 import KVPool, PoolConfig
+    dev = torch.device("cuda", 0)
+    pool = KVPool(PoolConfig(1, 8, 64, 1, 576, 512, 2, 4, kv_shared=True), dev)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    pool.alloc_blocks(i32([0]), i32([2]))
+    T = 60  # the host says 60 rows; cu says 100
+    q = torch.randn(T, H, 192, device=dev).bfloat16()
+    kn = torch.randn(T, 576, device=dev).bfloat16()
+    w = (torch.randn(H, 128, 512, device=dev) / 22.6).bfloat16()
+    buf = torch.full((T + 64, H, 128), 7.0, dtype=torch.bfloat16, device=dev)
+    out = buf[:T]
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = pool.new_mla_expanded_workspace(1, 100, H)
+    pool.prefill_mla_expanded(0, q, kn, w, w, i32([0, 100]), i32([0]), i32([0]), T, 100, 100, 0.07,
+                              out, ws, status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 1
+    assert torch.all(buf[T:] == 7.0)

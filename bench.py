@@ -1124,6 +1124,18 @@ def main(argv=None):
     pure = [r for r in sweep if r["tail_p"] == 0 and r["tail_d"] == 0]
     best_pure = max(pure, key=lambda r: r["tokens_per_s"]) if pure else None
     x, y, tp, td = best["x"], best["y"], best["tail_p"], best["tail_d"]
+    # the sweep's 3 replays per split can misorder splits within ~2 %: re-time the three best
+    # schedules with 10 replays each and run the timed region at the fastest of those
+    reselect = []
+    if args.split is None and len(sweep) > 1:
+        top = sorted(sweep, key=lambda r: -r["tokens_per_s"])[:3]
+        for r in top:
+            st_ = run.capture(lambda r=r: w.corun_step(r["x"], r["y"], r["tail_p"], r["tail_d"]))
+            t_, _ = run.time(st_, 10)
+            reselect.append({"x": r["x"], "tail_p": r["tail_p"], "tail_d": r["tail_d"],
+                             "sweep_ms": r["ms"], "ms_10_replays": t_ * 1e3})
+        pick = min(reselect, key=lambda r: r["ms_10_replays"])
+        x, y, tp, td = pick["x"], 100 - pick["x"], pick["tail_p"], pick["tail_d"]
     # library launches of one step (an eager step; graph replays launch the same kernels)
     c0 = w.pool.launch_count()
     w.corun_step(x, y, tp, td)
@@ -1280,6 +1292,7 @@ def main(argv=None):
                                  f"layers on all {w.pool.num_sms} SMs once the other worker is "
                                  f"done (R30)"}},
             "best_pure_split": best_pure,
+            "split_reselect": reselect,
             "roofline": roof_dec if dominant == "decode" else roof_pre,
             "roofline_decode": roof_dec, "roofline_prefill": roof_pre, "roofline_step": roof_step,
             "kernel_time_check": consistency,

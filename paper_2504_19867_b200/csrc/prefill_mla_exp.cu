@@ -648,6 +648,7 @@ struct XUnit {
     int kv0;            // first kv tile of this part
     int slot;           // split slot (-1: unsplit unit)
     int part;
+    int single;         // 1: tile A alone (a q tile of a split row); tile B idle
 };
 
 struct ASmem {
@@ -671,6 +672,7 @@ struct XAttn {
     int* status;
     unsigned long long* span;
     unsigned* sched;
+    int single_rows;  // the longest `single_rows` pair rows run as two single-tile units each
     float* part;  // split partials [slots][2 tiles][128 rows][XPROW]
     int* cnt;     // split counters [slots][2 tiles][role counter, flag]
     int n, T, H, pairs_max, n_units;
@@ -817,20 +819,27 @@ __global__ void __launch_bounds__(ANT, 1)
                 if (u < p.n_units) {
                     // u -> (slot v = (pair, part), request, head); LPT: last pairs first
                     const int per_pair = p.n * p.H;
-                    const int v = u / per_pair;
-                    const int pair = p.pairs_max - 1 - (kXSplit ? v >> 1 : v);
-                    const int part = kXSplit ? v & 1 : 0;
-                    d.i = (u / p.H) % p.n;
-                    d.h = u % p.H;
+                    // units: first the q tiles of the `single_rows` longest pair rows as single-
+                    // tile units (last tile first), then the remaining pair rows (last first)
+                    const int ns = 2 * p.single_rows * per_pair;
+                    const bool single = u < ns;
+                    const int uu = single ? u : u - ns;
+                    const int v = uu / per_pair;
+                    const int pair = single ? p.pairs_max - 1 - (v >> 1)
+                                            : p.pairs_max - 1 - p.single_rows - (kXSplit ? v >> 1 : v);
+                    const int part = kXSplit && !single ? v & 1 : 0;
+                    d.i = (uu / p.H) % p.n;
+                    d.h = uu % p.H;
                     const int c0 = __ldg(p.cu + d.i), C = __ldg(p.cu + d.i + 1) - c0;
-                    d.t0 = pair * 2 * XBM;
-                    if (d.t0 >= C) continue;  // pair past this request's chunk (warp-uniform)
+                    d.t0 = single ? (2 * pair + 1 - (v & 1)) * XBM : pair * 2 * XBM;
+                    if (d.t0 >= C) continue;  // tile / pair past this request's chunk (warp-uniform)
+                    d.single = single;
                     d.tv[0] = min(XBM, C - d.t0);
-                    d.tv[1] = max(0, min(XBM, C - d.t0 - XBM));
+                    d.tv[1] = single ? 0 : max(0, min(XBM, C - d.t0 - XBM));
                     d.P = __ldg(p.prefix + d.i);
                     const int nA = (d.P + d.t0 + d.tv[0] - 1) / XBM + 1;
                     const int nB = d.tv[1] > 0 ? (d.P + d.t0 + XBM + d.tv[1] - 1) / XBM + 1 : nA;
-                    const bool split = x_pair_nkv(d.P, C, pair) >= XSPLIT_MIN;
+                    const bool split = !single && x_pair_nkv(d.P, C, pair) >= XSPLIT_MIN;
                     if (!split && part) continue;
                     d.part = part;
                     if (split) {  // nB >= 10 and nA >= nB - 1: both tiles keep >= 1 kv tile per part
@@ -892,6 +901,7 @@ __global__ void __launch_bounds__(ANT, 1)
             const uint32_t idesc_o = umma_idesc_bf16_f32(XBM, XDV, 1);
             const uint32_t idesc_o64 = umma_idesc_bf16_f32(XBM, 64, 1);
             int sc = 0, nunit = 0, cnt_a = 0, cnt_b = 0;
+            int npair = 0;  // pair units so far: the phase of tile B's o_empty (single units skip B)
             auto wait_slot = [&](int c) { mbar_wait(&sm.full[c & (NSLOT - 1)], (c / NSLOT) & 1); };
             auto release = [&](int c0, int k) {
                 for (int e = 0; e < k; ++e) umma_commit_warp(&sm.empty[(c0 + e) & (NSLOT - 1)]);
@@ -958,6 +968,35 @@ __global__ void __launch_bounds__(ANT, 1)
                     ++cnt;
                 };
                 const int c0 = sc, j0 = d.kv0;
+                if (d.single) {  // tile A alone: S(j) -> softmax -> PV(j) -> S(j + 1)
+                    for (int e = 0; e < 3; ++e) wait_slot(c0 + e);
+                    tc_fence_after();
+                    issue_s(0, c0);
+                    release(c0, 3);
+                    if (nA == 1) umma_commit_warp(&sm.q_empty);
+                    for (int j = 0; j < nA; ++j) {
+                        const int vc = c0 + 5 * j + 3;
+                        wait_slot(vc);
+                        wait_slot(vc + 1);
+                        tc_fence_after();
+                        if (j == 0) mbar_wait(&sm.o_empty[0], (nunit & 1) ^ 1);
+                        issue_pv(0, cnt_a, vc, j == 0);
+                        release(vc, 2);
+                        if (j == nA - 1) {
+                            umma_commit_warp(&sm.o_full[0]);
+                        } else {
+                            const int kn = c0 + 5 * (j + 1);
+                            for (int e = 0; e < 3; ++e) wait_slot(kn + e);
+                            tc_fence_after();
+                            issue_s(0, kn);
+                            release(kn, 3);
+                            if (j + 1 == nA - 1) umma_commit_warp(&sm.q_empty);
+                        }
+                    }
+                    sc = c0 + 5 * nA;
+                    ++nunit;
+                    continue;
+                }
                 for (int e = 0; e < 3; ++e) wait_slot(c0 + e);
                 tc_fence_after();
                 issue_s(0, c0);
@@ -981,7 +1020,7 @@ __global__ void __launch_bounds__(ANT, 1)
                         tc_fence_after();
                     }
                     if (j + 1 < nA) issue_s(0, kn);
-                    if (j == j0) mbar_wait(&sm.o_empty[1], (nunit & 1) ^ 1);
+                    if (j == j0) mbar_wait(&sm.o_empty[1], (npair & 1) ^ 1);
                     issue_pv(1, cnt_b, vc, j == j0);
                     release(vc, 2);
                     if (j == nB - 1) umma_commit_warp(&sm.o_full[1]);
@@ -992,6 +1031,7 @@ __global__ void __launch_bounds__(ANT, 1)
                     }
                 }
                 sc = c0 + 5 * (nB - j0);
+                ++npair;
                 ++nunit;
             }
         }
@@ -1007,6 +1047,7 @@ __global__ void __launch_bounds__(ANT, 1)
         const uint32_t o_tmem = tmem + lane_base + 256u + (uint32_t)(t * XDV);
         const float tsc = p.scale_log2;
         int cnt = 0, nunit = 0;
+        int nown = 0;  // units this warpgroup computed (tile B skips single units): o_full phase
         for (;;) {
             const int us = nunit & 1;
             mbar_wait(&sm.ufull[us], (nunit >> 1) & 1);
@@ -1017,6 +1058,12 @@ __global__ void __launch_bounds__(ANT, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.uempty[us]);
                 break;
+            }
+            if (t == 1 && du.single) {  // a single-tile unit: tile B has no work
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.uempty[us]);
+                ++nunit;
+                continue;
             }
             const int kv0 = du.kv0, dP = du.P;
             const int trel = du.t0 + t * XBM + r;  // chunk-relative token of this row
@@ -1118,7 +1165,8 @@ __global__ void __launch_bounds__(ANT, 1)
                 l2 = fadd2(l2, f2(ls[0] + ls[2], ls[1] + ls[3]));
             }
             // ---- epilogue: O / l -> bf16 -> out [T][H][128] (each thread its 256-byte row)
-            mbar_wait(&sm.o_full[t], nunit & 1);
+            mbar_wait(&sm.o_full[t], nown & 1);
+            ++nown;
             tc_fence_after();
             XUnit d;
             d.tv[t] = du.tv[t];
@@ -1177,6 +1225,50 @@ __global__ void __launch_bounds__(ANT, 1)
             __threadfence();
         }
     }
+}
+
+// SPD_X_SINGLE: the host picks how many of the longest pair rows run as single-tile units, by a
+// makespan model in pair-step units (a pair row r costs 2 r + 2 steps, a lone tile k costs
+// SPD_X_SINGLE_COST x (k + 1): one tile's chain without a partner to overlap), minimising
+// max(longest unit, total work / grid); a chunk without prefix is assumed.
+// Measured (profiles/r2_mla_expanded_single_ab.log): a lone tile's kv step takes about as long
+// as a pair step (the S -> softmax -> P V -> S chain is the same; pairing only fills the tensor
+// pipe's idle time with the other tile), so single-tile rows shorten the critical path only when
+// nothing else is running: -19 % at 148 SMs for a chunk without prefix, +10-15 % at 89-118 SMs and
+// +46 % at 148 SMs with a 4096-token prefix (the model's cost 0.7 is wrong; ~1.1 would never
+// split).  Default 0.
+#ifndef SPD_X_SINGLE
+#define SPD_X_SINGLE 0
+#endif
+#ifndef SPD_X_SINGLE_COST
+#define SPD_X_SINGLE_COST 0.7
+#endif
+constexpr bool kXSingle = SPD_X_SINGLE != 0;
+int x_single_rows(int pairs_max, int units_per_row, int grid) {
+    int best_ks = 0;
+    double best = 1e300;
+    for (int ks = 0; ks <= pairs_max; ++ks) {
+        double total = 0.0, crit = 0.0;
+        for (int r = 0; r < pairs_max; ++r) {
+            if (r >= pairs_max - ks) {
+                for (int k = 2 * r; k <= 2 * r + 1; ++k) {
+                    const double c = SPD_X_SINGLE_COST * (k + 1);
+                    total += c * units_per_row;
+                    crit = c > crit ? c : crit;
+                }
+            } else {
+                const double c = 2.0 * r + 2.0;
+                total += c * units_per_row;
+                crit = c > crit ? c : crit;
+            }
+        }
+        const double mk = crit > total / grid ? crit : total / grid;
+        if (mk < best - 1e-9) {
+            best = mk;
+            best_ks = ks;
+        }
+    }
+    return best_ks;
 }
 
 bool x_pool_ok(const semipd_pool* pl) {
@@ -1357,7 +1449,13 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     ap.H = H;
     ap.pairs_max = (max_chunk_len + 2 * XBM - 1) / (2 * XBM);
     if (ap.pairs_max < 1) return SEMIPD_OK;
-    const long long units = (long long)n * ap.pairs_max * H * (kXSplit ? 2 : 1);  // x 2: split parts
+    // single-tile rows: when the grid is wide enough that the longest pair rows would set the
+    // kernel's critical path, their two q tiles run as separate units (R26 holds: a tile's
+    // arithmetic does not depend on being paired; only the K / V loads were shared)
+    const int grid0 = budget > 0 ? budget : 1 << 30;
+    ap.single_rows = kXSingle ? x_single_rows(ap.pairs_max, n * H, grid0) : 0;
+    const long long units = (long long)n * H * (2 * ap.single_rows + (long long)(ap.pairs_max - ap.single_rows) *
+                                                                           (kXSplit ? 2 : 1));
     if (units > (1LL << 30)) return SEMIPD_ERR_UNSUPPORTED;
     ap.n_units = (int)units;
     ap.scale_log2 = softmax_scale * XLOG2E;

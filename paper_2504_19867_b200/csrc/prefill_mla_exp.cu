@@ -641,6 +641,11 @@ constexpr int NSLOT = 8;
 constexpr uint32_t SLOT = XBM * 128;          // 16 KiB: 128 rows x 64 columns
 constexpr uint32_t QCH = 2 * SLOT;            // one 64-column chunk of the Q pair (tiles A, B)
 constexpr int kXPvParts = 4;
+// exp2 pairs of each 32-column S block on the FMA pipe (bit i = columns 2i, 2i + 1), as the GQA
+// prefill kernel's SPD_POLY_MASK
+#ifndef SPD_X_POLY
+#define SPD_X_POLY 0x1111u
+#endif
 
 struct XUnit {
     int i, h, t0, P, qrow0, krow0;
@@ -1145,7 +1150,7 @@ __global__ void __launch_bounds__(ANT, 1)
                     for (int e = 0; e < 32; e += 2) {
                         const uint64_t x2 = ffma2(f2(__uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1])), sc2, nm2);
                         float p0, p1;
-                        if ((0x1111u >> (e >> 1)) & 1u) {
+                        if ((SPD_X_POLY >> (e >> 1)) & 1u) {
                             f2_split(exp2_poly3(x2), p0, p1);
                         } else {
                             float x0, x1;

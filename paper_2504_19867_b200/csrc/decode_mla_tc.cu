@@ -185,6 +185,81 @@ __device__ __forceinline__ void split_range(int ctx, int S, int s, int& k0, int&
     k1 = min(nk, k0 + pps * PAGE);
 }
 
+// SPD_MLA_MERGE_FN = 1 (default): the last split's merge as a separate (non-inlined) function,
+// so its registers do not enter the page loop's allocation (255 -> 244 registers, no spill),
+// with (m, l) loaded by 8 threads per head at once and two splits' partials in flight (instead
+// of 2 S + S serialised L2 round trips).  +1-2 % on the lognormal cfg-5 batch, neutral on split
+// batches (profiles/r2_mla_decode_merge_fn_ab.log); finer splits stay slower with it.
+#ifndef SPD_MLA_MERGE_FN
+#define SPD_MLA_MERGE_FN 1
+#endif
+__device__ __noinline__ void mla_split_merge(const float* ws_m, const float* ws_l, const float* ws_acc,
+                                             __nv_bfloat16* out, int* ws_cnt, int b, int S, int S_max, int G,
+                                             int B, int out_head_major, int tid, float* wsm) {
+    // pass 1: w[h][s] = 2^(m_s - M_h) / L_h into smem, 8 threads per head (S <= 32: 4 splits each)
+    const int h1 = tid >> 3, j8 = tid & 7;
+    const size_t pb1 = ((size_t)b * NH + h1) * S_max;
+    float mv[4], lv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int sI = j8 + 8 * k;
+        const bool ok = h1 < G && sI < S;
+        mv[k] = ok ? __ldcg(ws_m + pb1 + sI) : -INFINITY;
+        lv[k] = ok ? __ldcg(ws_l + pb1 + sI) : 0.f;
+    }
+    float M = fmaxf(fmaxf(mv[0], mv[1]), fmaxf(mv[2], mv[3]));
+    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
+    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
+    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 4));
+    float f[4], Ls = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        f[k] = j8 + 8 * k < S ? fast_exp2(mv[k] - M) : 0.f;
+        Ls += f[k] * lv[k];
+    }
+    Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
+    Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
+    Ls += __shfl_xor_sync(0xffffffffu, Ls, 4);
+    const float inv = 1.f / Ls;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (h1 < G && j8 + 8 * k < S) wsm[h1 * 32 + j8 + 8 * k] = f[k] * inv;
+    named_bar_sync(1, NSOFT);
+    // pass 2: each thread owns 16 float4 columns; two splits' loads in flight
+    constexpr int PER = NH * (DV / 4) / NSOFT;
+    float4 o[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 2
+    for (int sI = 0; sI < S; ++sI) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int idx = tid + j * NSOFT;
+            const int h = idx / (DV / 4), c = (idx % (DV / 4)) * 4;
+            if (h < G) {
+                const float w = wsm[h * 32 + sI];
+                const float4 a = __ldcg(reinterpret_cast<const float4*>(ws_acc + (((size_t)b * NH + h) * S_max + sI) * DV + c));
+                o[j].x += w * a.x;
+                o[j].y += w * a.y;
+                o[j].z += w * a.z;
+                o[j].w += w * a.w;
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int idx = tid + j * NSOFT;
+        const int h = idx / (DV / 4), c = (idx % (DV / 4)) * 4;
+        if (h >= G) continue;
+        const size_t off = out_head_major ? (((size_t)h * B + b) * DV + c) : (((size_t)b * G + h) * DV + c);
+        uint2 v;
+        v.x = pack_bf16(o[j].x, o[j].y);
+        v.y = pack_bf16(o[j].z, o[j].w);
+        *reinterpret_cast<uint2*>(out + off) = v;
+    }
+    if (tid == 0) ws_cnt[b] = 0;
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     decode_mla_tc_kernel(const __grid_constant__ CUtensorMap map_lo,
                          const __grid_constant__ CUtensorMap map_hi,
@@ -768,6 +843,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 named_bar_sync(1, NSOFT);
                 if (*s_last) {
                     __threadfence();
+#if SPD_MLA_MERGE_FN
+                    mla_split_merge(p.ws_m, p.ws_l, p.ws_acc, p.out, p.ws_cnt, d.b, d.S, p.S_max, p.G, p.B,
+                                    p.out_head_major, tid, reinterpret_cast<float*>(ps));
+#else
                     // merge in split-index order.  Pass 1 (one thread per head): weights
                     // w[h][s] = 2^(m_s - M) / L into smem (the P buffer is idle here: PV of
                     // the unit's last tile completed).  Pass 2: each thread owns 16 float4
@@ -848,6 +927,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         }
                     }
                     if (tid == 0) p.ws_cnt[d.b] = 0;
+#endif
                 }
             }
             [[maybe_unused]] const long long te2 = TL_NOW();

@@ -125,6 +125,23 @@ struct TUnit {
     int b, s, S, k0, k1, nt;  // b < 0: done
 };
 
+// SPD_MLA_SORT = 1: the launch's real units in longest-first order, built in shared memory by
+// every CTA before its first unit (mla_unit_order).  The default enumeration walks the
+// (split level, request) grid, S_max x B entries, and a request with fewer splits than S_max
+// leaves empty entries that each cost the producer a counter atomic and a context load before
+// the next real unit (cfg-5 lognormal batch: 253 of 512 entries empty, most of them handed out
+// first).  Used when S_max x B <= SORT_CAP (uint16 entries b | s << 11, so B <= 2048, S <= 32).
+// Measured (profiles/r2_mla_decode_sort_ab.log, MLA parity 70/70): 2-5 % SLOWER at every shape
+// (cfg-5 lognormal batch 0.0410 vs 0.0391 ms at 148 SMs, 0.0684 vs 0.0668 at 44; uniform
+// ctx 1000, where the order is unchanged, +2 %: the prologue's context loads and barriers delay
+// every CTA's first TMA by about as much as the empty entries cost).  Finer splits stay slower
+// with it (SPLIT_PAGES 10 / 14: +12-70 %).  With the builder out of line (__noinline__) the MMA
+// warp's descriptors left the uniform datapath (R2UR per MMA, +25-30 %).  Default 0.
+#ifndef SPD_MLA_SORT
+#define SPD_MLA_SORT 0
+#endif
+constexpr int SORT_CAP = 1024;
+
 struct TcParams {
     const uint4* k_new;       // [B][1][576]
     const int* req_ids;
@@ -141,6 +158,7 @@ struct TcParams {
     unsigned long long* span;  // semipd_set_spans record of this launch (or null)
     int skip_append;           // 1: the step's latent row is already in the pool (RoPE pre-pass)
     int B, MBR, N_B, S_max, n_units, out_head_major, G, S_fill;
+    int sorted;  // 1: units come from the in-smem longest-first order (SPD_MLA_SORT)
     float scale_log2;
     SpdTrace trace;
     long long* tl;  // SPD_TIMELINE builds only: pipeline clock64 stamps of CTA 0
@@ -173,7 +191,8 @@ constexpr uint32_t OFF_RED = OFF_P + 2 * P_BYTES;            // [2][64] maxima, 
 constexpr uint32_t OFF_BARS = OFF_RED + 5 * 64 * 4;
 constexpr uint32_t OFF_UNITS = OFF_BARS + sizeof(Bars);
 constexpr uint32_t OFF_MISC = OFF_UNITS + 2 * sizeof(TUnit);
-constexpr uint32_t SMEM_BYTES = 1024 + OFF_MISC + 16;
+constexpr uint32_t OFF_PERM = OFF_MISC + 16;                 // [SORT_CAP] uint16 unit order
+constexpr uint32_t SMEM_BYTES = 1024 + OFF_PERM + (SPD_MLA_SORT ? SORT_CAP * 2 : 0);
 static_assert(OFF_Q % 1024 == 0 && OFF_P % 1024 == 0, "UMMA operands need 1 KiB alignment");
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KiB opt-in shared memory");
 
@@ -260,6 +279,108 @@ __device__ __noinline__ void mla_split_merge(const float* ws_m, const float* ws_
     if (tid == 0) ws_cnt[b] = 0;
 }
 
+// Longest-first order of the launch's real (request, split) units (SPD_MLA_SORT): a stable
+// counting sort by page count, descending, ties in (b, s) order.  A function of the shapes only,
+// so every CTA builds the same list and outputs stay bitwise identical for every sm_budget (R26;
+// the order only decides which CTA runs a unit, never its arithmetic).  All NTHREADS threads;
+// the scratch is the still-idle ring.  Needs B <= 6 * NTHREADS (implied by S_max x B <= SORT_CAP).
+__device__ __forceinline__ void mla_unit_order(const int* ctx_lens, int B, int S_fill, unsigned char* scratch,
+                                            uint16_t* perm, int* s_ntot) {
+    constexpr int NW = NTHREADS / 32;
+    constexpr int PER = 6;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    int* wsum = reinterpret_cast<int*>(scratch);                      // [8]
+    int* wcnt = wsum + 8;                                             // [NW][32]: counts, then bases
+    uint16_t* ccode = reinterpret_cast<uint16_t*>(wcnt + NW * 32);    // [SORT_CAP] canonical units
+    uint8_t* ckey = reinterpret_cast<uint8_t*>(ccode + SORT_CAP);     // [SORT_CAP] their page counts
+    for (int i = tid; i < NW * 32; i += NTHREADS) wcnt[i] = 0;
+    // 1. splits of this thread's consecutive requests; block exclusive scan -> canonical offsets
+    const int per = (B + NTHREADS - 1) / NTHREADS;
+    int cl[PER], sl[PER], loc = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int b = tid * per + j;
+        cl[j] = (j < per && b < B) ? __ldg(ctx_lens + b) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        sl[j] = cl[j] >= 0 ? n_splits(cl[j], S_fill) : 0;
+        loc += sl[j];
+    }
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    int c = inc - loc, tot = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        const int v = wsum[i];
+        if (i < w) c += v;
+        tot += v;
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        for (int sI = 0; sI < sl[j]; ++sI, ++c) {
+            int k0, k1;
+            split_range(cl[j], sl[j], sI, k0, k1);
+            const int nt = (k1 - k0 + PAGE - 1) / PAGE;
+            ccode[c] = (uint16_t)((tid * per + j) | (sI << 11));
+            ckey[c] = (uint8_t)(nt < 31 ? nt : 31);
+        }
+    }
+    __syncthreads();
+    // 2. per-warp key counts over warp w's canonical range
+    const int L = ((tot + NW - 1) / NW + 31) & ~31;
+    const int r0 = w * L, r1 = min(tot, r0 + L);
+    for (int c0 = r0; c0 < r1; c0 += 32) {
+        const int cc = c0 + lane;
+        const int key = cc < r1 ? (int)ckey[cc] : -1;
+        const unsigned m = __match_any_sync(0xffffffffu, key);
+        if (key >= 0 && lane == __ffs(m) - 1) wcnt[w * 32 + key] += __popc(m);
+        __syncwarp();
+    }
+    __syncthreads();
+    // 3. bases: keys in descending order, warps in canonical order within a key
+    if (w == 0) {
+        int pw[NW], t = 0;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            pw[i] = wcnt[i * 32 + lane];
+            t += pw[i];
+        }
+        int suf = t;  // sum over keys >= lane
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_down_sync(0xffffffffu, suf, o);
+            if (lane + o < 32) suf += v;
+        }
+        int base = suf - t;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            wcnt[i * 32 + lane] = base;
+            base += pw[i];
+        }
+    }
+    __syncthreads();
+    // 4. placement: rank among equal keys, stable within the warp's range
+    for (int c0 = r0; c0 < r1; c0 += 32) {
+        const int cc = c0 + lane;
+        const int key = cc < r1 ? (int)ckey[cc] : -1;
+        const unsigned m = __match_any_sync(0xffffffffu, key);
+        if (key >= 0) perm[wcnt[w * 32 + key] + __popc(m & ((1u << lane) - 1u))] = ccode[cc];
+        __syncwarp();
+        if (key >= 0 && lane == __ffs(m) - 1) wcnt[w * 32 + key] += __popc(m);
+        __syncwarp();
+    }
+    if (tid == 0) *s_ntot = tot;
+    fence_proxy_async_smem();  // the ring's generic scratch writes before its TMA fills
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     decode_mla_tc_kernel(const __grid_constant__ CUtensorMap map_lo,
                          const __grid_constant__ CUtensorMap map_hi,
@@ -317,6 +438,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     pdl_wait();  // PDL: the previous kernel on this stream is complete (workspace counters, pool)
     if (threadIdx.x == 0) span_begin(p.span);
     const uint32_t tmem = *tmem_base;
+    uint16_t* perm = reinterpret_cast<uint16_t*>(base + OFF_PERM);
+    int* s_ntot = reinterpret_cast<int*>(base + OFF_MISC + 8);
+    const bool sorted = SPD_MLA_SORT && p.sorted;
+    if (sorted) mla_unit_order(p.ctx_lens, p.B, p.S_fill, ring, perm, s_ntot);
+    const int n_lim = sorted ? *s_ntot : p.n_units;
 
     if (warp == 0) {
         // =========================== producer ===========================
@@ -340,13 +466,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             TUnit d;
             int ctx = 0, rid = 0;
             const bool have_la = SPD_MLA_LOOKAHEAD && u == la_u;
-            if (u >= p.n_units) {
+            if (u >= n_lim) {
                 d.b = -1;
             } else {
-                // longest-first: units of the highest split index (full-length splits of the
-                // longest requests) are handed out first
-                d.s = p.S_max - 1 - u / p.B;
-                d.b = u % p.B;
+                if (sorted) {
+                    const unsigned code = perm[u];
+                    d.b = (int)(code & 2047u);
+                    d.s = (int)(code >> 11);
+                } else {
+                    // longest-first: units of the highest split index (full-length splits of
+                    // the longest requests) are handed out first
+                    d.s = p.S_max - 1 - u / p.B;
+                    d.b = u % p.B;
+                }
                 ctx = have_la ? la_ctx : __ldg(p.ctx_lens + d.b);
                 rid = have_la ? la_rid : __ldg(p.req_ids + d.b);
                 d.S = n_splits(ctx, p.S_fill);
@@ -435,7 +567,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                 }
                 // after this page's TMA issue, so no lookahead load delays it
-                if (SPD_MLA_LOOKAHEAD && i == 0 && u_next < p.n_units) {
+                if (SPD_MLA_LOOKAHEAD && !sorted && i == 0 && u_next < p.n_units) {
                     // step 1: the next unit's context and request id (consumed at step 2)
                     la_u = u_next;
                     const int b2 = u_next % p.B;
@@ -1036,6 +1168,7 @@ semipd_status spd_launch_decode_mla_tc(semipd_pool_t pool, int layer, const void
     prm.S_max = S_max;
     prm.S_fill = S_fill;
     prm.n_units = batch * S_max;
+    prm.sorted = (SPD_MLA_SORT && prm.n_units <= SORT_CAP && S_max <= 32) ? 1 : 0;
     prm.out_head_major = out_head_major;
     prm.G = Hq;
     prm.scale_log2 = scale * LOG2E;

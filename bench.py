@@ -89,6 +89,9 @@ def parse(argv=None):
                          "the worker that finishes second run on all SMs once the other is done); "
                          "0:0 = the pure split")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sustained", type=float, default=1.0,
+                    help="seconds of back-to-back replays after all fields (the power-capped "
+                         "rate; 0 = skip)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every kernel from Python instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
@@ -154,7 +157,8 @@ def _clock_sampler_proc(index, period: float, stop, out):
     out.put(("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)))
     while not stop.is_set():
         rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
-                     pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                     pynvml.nvmlDeviceGetCurrentClocksEventReasons(h),
+                     pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0))
         time.sleep(period)
     out.put(("rows", rows))
 
@@ -201,10 +205,12 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
                     "error": self.err}
         import pynvml as nv
-        reasons = sorted({name for _, rs in self.rows for name, attr in self.REASONS.items()
-                          if rs & getattr(nv, attr)})
+        reasons = sorted({name for r in self.rows for name, attr in self.REASONS.items()
+                          if r[1] & getattr(nv, attr)})
         return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.rows), "source": "nvml, 5 ms, child process"}
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_median": round(statistics.median(r[2] for r in self.rows), 1),
+                "source": f"nvml, {self.period * 1e3:g} ms, child process"}
 
 
 def dist_info():
@@ -1275,6 +1281,29 @@ def main(argv=None):
                 secondary[name] = {"error": repr(e)[:300]}
             torch.cuda.synchronize(dev)
             torch.cuda.empty_cache()
+    sustained = None
+    if ws == 1 and args.sustained > 0:
+        # the same step replayed back to back for ~args.sustained seconds, after everything
+        # else: a B200 at this load reaches its 1000 W cap within ~0.2 s and lowers the SM
+        # clock (sw_power_cap), so this is the power-capped rate a long-running job sees; the
+        # headline's K steps mostly run before the cap engages (their clocks say which)
+        rs = Runner(w, dev, None, not args.no_graph, 1)
+        st_ = rs.capture(lambda: w.corun_step(x, y, tp, td))
+        n_win = 10
+        per_win = max(1, int(round(args.sustained / n_win / (ms_step / 1e3))))
+        wins = []
+        with ClockSampler(nvml_id(dev), period_s=0.02) as ck:
+            for _ in range(n_win):
+                wins.append(time_steps(st_, per_win, dev) / per_win * 1e3)
+        late = wins[n_win // 2:]
+        sustained = {"seconds": round(sum(wins) * per_win / 1e3, 3), "steps": n_win * per_win,
+                     "ms_per_step_windows": [round(v, 4) for v in wins],
+                     "ms_per_step_last_half": statistics.mean(late),
+                     "tokens_per_s_last_half": w.tokens_per_step() / (statistics.mean(late) / 1e3),
+                     "split": {"x": x, "y": y}, "clocks": ck.summary(),
+                     "note": "not the headline: the same captured step, back to back after all "
+                             "other fields; shows the power-capped steady state"}
+        del rs, st_
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_baseline(shape)
@@ -1303,7 +1332,7 @@ def main(argv=None):
             "target_met": bool(tgt and tgt["target_score"] >= 1.0),
             "sweep": sweep, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
             "gpu_launches": launches, "cuda_graph": graph_used, "graph_error": graph_error,
-            "dp_replicas": dp, "extra": extra or None, **secondary,
+            "dp_replicas": dp, "extra": extra or None, "sustained": sustained, **secondary,
         }
         if ws > 1:
             line["tp"] = {"mode": args.tp_mode, "gather": args.gather,

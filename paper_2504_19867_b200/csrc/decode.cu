@@ -60,7 +60,13 @@ constexpr int KPS = 64;           // keys per stage
 constexpr int NSTAGE = 6;
 constexpr int KV_BYTES = KPS * HD * 2;         // 16 KiB of K (or V) per stage
 constexpr int STAGE_BYTES = 2 * KV_BYTES;      // K + V
-constexpr int SPLIT_KEYS = 4096;  // maximum keys per split (shape-only decomposition)
+// SPD_DEC_SPLIT_KEYS: finer splits of the cfg-2 contexts (1024 / 2048 keys, with or without the
+// head-pair wide boxes, SEMIPD_DECODE_PAIR64=1) are 10-70 % slower than whole-context units at
+// 74-148 SMs (isolated, B 64 ctx 2048; profiles/r2_decode_split_pair_ab.log).  Default 4096.
+#ifndef SPD_DEC_SPLIT_KEYS
+#define SPD_DEC_SPLIT_KEYS 4096
+#endif
+constexpr int SPLIT_KEYS = SPD_DEC_SPLIT_KEYS;  // maximum keys per split (shape-only decomposition)
 constexpr float LOG2E = 1.4426950408889634f;
 
 struct UnitDesc {

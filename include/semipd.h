@@ -179,7 +179,9 @@ int32_t semipd_num_sms(semipd_pool_t pool);
  * FP8 pools (reading R31): step 1 quantises the rows; in step 2 keys j < P_i are the pool's
  * dequantised values (staged through the FP8 prefill scratch) and keys j >= P_i the chunk's
  * own bf16 rows; the tcgen05 kernel runs as for bf16.  Needs the scratch
- * (semipd_set_fp8_prefill_scratch) and no fused RoPE / peer epilogue (else UNSUPPORTED). */
+ * (semipd_set_fp8_prefill_scratch) and no peer epilogue (else UNSUPPORTED); with RoPE set
+ * (semipd_set_rope) step 1 rotates q / k_new in place and writes the rotated rows' codes in the
+ * same pass. */
 semipd_status semipd_prefill_attn(semipd_pool_t pool, int32_t layer, const void* q,
                                   const void* k_new, const void* v_new,
                                   const int32_t* cu_seqlens_q, const int32_t* req_ids,
@@ -202,8 +204,9 @@ semipd_status semipd_prefill_attn(semipd_pool_t pool, int32_t layer, const void*
  *   ZERO-FILLED before its first use (the kernels leave their counters at zero);
  *   sm_budget as in semipd_prefill_attn (0 = partition's decode budget).
  * FP8 pools (reading R31): the appended row is quantised and every key / value (the appended
- * one included) is read back dequantised; num_q_heads / Hkv <= 8; no fused RoPE / peer
- * epilogue (else UNSUPPORTED).  Kernel: head-pair E4M3 boxes converted to f16 in registers,
+ * one included) is read back dequantised; num_q_heads / Hkv <= 8; no peer epilogue (else
+ * UNSUPPORTED); with RoPE set the rotation pass writes the quantised rows and the kernel skips
+ * its own append.  Kernel: head-pair E4M3 boxes converted to f16 in registers,
  * f16 mma.sync with fp32 accumulation (kernel kind 9). */
 semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* q,
                                  const void* k_new, const void* v_new, const int32_t* req_ids,
@@ -350,7 +353,9 @@ semipd_status semipd_rope(void* q, void* k, const int32_t* positions, int32_t nu
  * and in the SAME pass writes the rotated k rows (and v) into the pool slots of those
  * positions, replacing both the separate semipd_rope pass and the attention kernels' own
  * K/V write / append (one pass over q / k / v instead of two; R28).  q and k_new
- * are rotated IN PLACE (the attention then reads the rotated rows).  cfg = NULL turns it off.
+ * are rotated IN PLACE (the attention then reads the rotated rows).  On an FP8 (E4M3) pool the
+ * pass writes the rows as codes with the pool's write rule (R31), the bytes the FP8 calls' own
+ * write would store from the rotated rows.  cfg = NULL turns it off.
  * cfg fields as semipd_rope's arguments; head_dim = the pool's head_dim_k.  Errors: INVALID /
  * UNSUPPORTED as semipd_rope, plus INVALID for a NULL pool. */
 typedef struct {

@@ -2,6 +2,7 @@
 // ldmatrix / mma.sync, proxy fences.  Part of the CUDA path only (no oracle code).
 #pragma once
 #include <cuda.h>
+#include <cuda_fp8.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -517,6 +518,23 @@ SPD_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::
 // named barrier among `nthreads` threads (id 1..15; 0 is __syncthreads)
 SPD_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// E4M3 pages (reading R31) write rule: code = E4M3_rne_satfinite(fl32(x / s)) of two floats;
+// lo -> low byte (fp8.cu's quantised writes and the fused RoPE write in rope.cu)
+SPD_DEV uint32_t quant2(float lo, float hi, float s) {
+    const float2 v = make_float2(__fdiv_rn(lo, s), __fdiv_rn(hi, s));
+    return (uint32_t)__nv_cvt_float2_to_fp8x2(v, __NV_SATFINITE, __NV_E4M3);
+}
+
+// 8 bf16 (one uint4) -> 8 codes (one uint2), element order kept
+SPD_DEV uint2 quant8(uint4 x, float s) {
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    uint32_t b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        b[i] = quant2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u), s);
+    return make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
 }
 
 }  // namespace spd

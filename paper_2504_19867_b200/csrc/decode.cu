@@ -1363,7 +1363,15 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     // at wrong head / token positions or past a peer's buffer
     if (pool->dec_n_peers > 0 && batch != pool->dec_peer_tokens) return SEMIPD_ERR_INVALID;
     if (c.dtype == SEMIPD_FP8_E4M3) {  // E4M3 pages (reading R31): quantised append + decode
-        if (pool->rope_on || pool->dec_n_peers > 0) return SEMIPD_ERR_UNSUPPORTED;
+        if (pool->dec_n_peers > 0) return SEMIPD_ERR_UNSUPPORTED;
+        if (pool->rope_on) {
+            // RoPE of q / k_new in place at ctx, fused with the quantised append of the rotated
+            // rows (R28 + R31); the FP8 kernel skips its own append
+            semipd_status r = spd_launch_rope_write(pool, layer, const_cast<void*>(q),
+                                                    const_cast<void*>(k_new), v_new, nullptr, req_ids,
+                                                    ctx_lens, batch, batch, num_q_heads, status_dev, st);
+            if (r != SEMIPD_OK) return r;
+        }
         return spd_launch_decode_fp8(pool, layer, q, k_new, v_new, req_ids, ctx_lens, batch,
                                      max_ctx_len, num_q_heads, softmax_scale, out, out_head_major,
                                      workspace, ws_bytes, budget, status_dev, st);

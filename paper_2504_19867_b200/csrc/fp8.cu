@@ -95,21 +95,7 @@ SPD_DEV void f8x4_to_h2x2_alu(uint32_t q, uint32_t& even, uint32_t& odd) {
     even = (q8 & 0x80008000u) | ((q8 & 0x7F007F00u) >> 1);
 }
 
-// E4M3_rne_satfinite(fl32(x / s)) of two floats; lo -> low byte
-SPD_DEV uint32_t quant2(float lo, float hi, float s) {
-    const float2 v = make_float2(__fdiv_rn(lo, s), __fdiv_rn(hi, s));
-    return (uint32_t)__nv_cvt_float2_to_fp8x2(v, __NV_SATFINITE, __NV_E4M3);
-}
-
-// 8 bf16 (one uint4) -> 8 codes (one uint2), element order kept
-SPD_DEV uint2 quant8(uint4 x, float s) {
-    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-    uint32_t b[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        b[i] = quant2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u), s);
-    return make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
-}
+// quant2 / quant8 (the write rule above) live in common.cuh: the fused RoPE write uses them too
 
 // 16 codes -> 16 bf16 of s * value(code) (2 x uint4 per 16 B of codes)
 SPD_DEV void dequant16(uint4 c, float s, uint4& lo, uint4& hi) {
@@ -278,6 +264,7 @@ struct DecParams {
     int* status;
     unsigned long long* span;
     int B, Hq, Hkv, G, MBR, N_B, S_max, n_units, out_head_major;
+    int skip_append;  // 1: the step's rows are already in the pool (fused RoPE write, R28)
     float scale_log2;            // softmax_scale * k_scale * log2(e)
     float ks, vs;                // write scales (append)
     float v_out;                 // v_scale, applied with 1 / l
@@ -395,7 +382,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             const int* btr = p.bt + (size_t)__ldg(p.req_ids + d.b) * p.MBR;
             const int last_page = ctx / BS;
-            if (d.k0 <= ctx && ctx < d.k1) {
+            if (!p.skip_append && d.k0 <= ctx && ctx < d.k1) {
                 // fused quantised append of both heads' K and V rows at slot ctx, by the
                 // unit whose key range holds slot ctx (no other unit reads that slot): lane
                 // = (tensor, head e, 16-element chunk c)
@@ -863,6 +850,7 @@ semipd_status spd_launch_decode_fp8(semipd_pool_t pool, int layer, const void* q
     prm.S_max = S0_max;  // unit enumeration; partial rows are indexed [B][Hq][S_max * NPIECE]
     prm.n_units = NPIECE * S0_max * batch * (c.num_kv_heads / 2);
     prm.out_head_major = out_head_major;
+    prm.skip_append = pool->rope_on ? 1 : 0;
     prm.scale_log2 = scale * pool->k_scale[layer] * LOG2E * (SPD_F8_KALU ? 256.f : 1.f);
     prm.ks = pool->k_scale[layer];
     prm.vs = pool->v_scale[layer];

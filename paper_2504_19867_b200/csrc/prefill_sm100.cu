@@ -870,10 +870,16 @@ extern "C" semipd_status semipd_prefill_attn(
         // E4M3 pages (reading R31): quantised K/V write of the chunk, then the call's prefix pages
         // dequantised into the bf16 staging scratch, which the tcgen05 kernel reads as it reads a
         // bf16 pool; the chunk's own keys come from k_new / v_new (bf16) as always
-        if (rope || pool->pre_n_peers > 0 || !fast_path_ok(pool, num_q_heads)) return SEMIPD_ERR_UNSUPPORTED;
+        // (with RoPE set, the rotation of q / k_new in place and the quantised write of the
+        // rotated rows are one pass, R28 + R31)
+        if (pool->pre_n_peers > 0 || !fast_path_ok(pool, num_q_heads)) return SEMIPD_ERR_UNSUPPORTED;
         if (!pool->have_f8s_maps || n > pool->f8s_cap) return SEMIPD_ERR_INVALID;
-        semipd_status r = spd_launch_kv_write_fp8(pool, layer, k_new, v_new, cu_seqlens_q, req_ids,
-                                                  prefix_lens, n, total_q, status_dev, st);
+        semipd_status r =
+            rope ? spd_launch_rope_write(pool, layer, const_cast<void*>(q), const_cast<void*>(k_new),
+                                         v_new, cu_seqlens_q, req_ids, prefix_lens, n, total_q,
+                                         num_q_heads, status_dev, st)
+                 : spd_launch_kv_write_fp8(pool, layer, k_new, v_new, cu_seqlens_q, req_ids,
+                                           prefix_lens, n, total_q, status_dev, st);
         if (r == SEMIPD_OK)
             r = spd_launch_dequant_prefix(pool, layer, req_ids, prefix_lens, n, budget, status_dev, st);
         if (r != SEMIPD_OK) return r;

@@ -23,9 +23,12 @@
 
 #include <cmath>
 
+#include "common.cuh"
 #include "internal.h"
 
 namespace {
+
+using spd::quant8;
 
 constexpr int MAX_HALF = 128;  // head_dim <= 256 (Llama 128, MLA rope part 64)
 
@@ -152,11 +155,16 @@ struct RopeWriteParams {
     const int* bt;
     int* status;
     int n, Hq, Hkv, dk, dv, off, rd, lg_bs, MBR, N_B;
+    float ks, vs;  // E4M3 pools (F8): the layer's scales of the quantised write (R31)
     double inv_freq[MAX_HALF];
 };
 
-template <typename T, bool INTER>
+// F8: E4M3 pages — the rotated k rows, the unrotated k columns and the v rows are written as
+// codes with fp8.cu's rule (quant8), exactly the bytes its own quantised append / chunk write
+// would store from the rotated k_new (so fused and composed paths leave identical pages)
+template <typename T, bool INTER, bool F8>
 __global__ void __launch_bounds__(256) rope_write_kernel(const __grid_constant__ RopeWriteParams p) {
+    static_assert(!F8 || sizeof(T) == 2, "E4M3 pools take bf16 activations");
     constexpr int VEC = 16 / sizeof(T);
     extern __shared__ float cs[];  // [rd/2] cos, [rd/2] sin
     const int t = blockIdx.x;
@@ -217,9 +225,15 @@ __global__ void __launch_bounds__(256) rope_write_kernel(const __grid_constant__
             *reinterpret_cast<uint4*>(row + i0) = a;
             if (!INTER) *reinterpret_cast<uint4*>(row + half + i0) = b;
             if (!is_q && ok) {
-                T* dst = reinterpret_cast<T*>(p.kpool) + slot(h) * p.dk + p.off;
-                *reinterpret_cast<uint4*>(dst + i0) = a;
-                if (!INTER) *reinterpret_cast<uint4*>(dst + half + i0) = b;
+                if constexpr (F8) {
+                    unsigned char* dst = p.kpool + slot(h) * p.dk + p.off;
+                    *reinterpret_cast<uint2*>(dst + i0) = quant8(a, p.ks);
+                    if (!INTER) *reinterpret_cast<uint2*>(dst + half + i0) = quant8(b, p.ks);
+                } else {
+                    T* dst = reinterpret_cast<T*>(p.kpool) + slot(h) * p.dk + p.off;
+                    *reinterpret_cast<uint4*>(dst + i0) = a;
+                    if (!INTER) *reinterpret_cast<uint4*>(dst + half + i0) = b;
+                }
             }
         } else if (it < n_q + n_kr + n_kp) {
             if (!ok) continue;
@@ -227,15 +241,23 @@ __global__ void __launch_bounds__(256) rope_write_kernel(const __grid_constant__
             const int h = j / nkp, c0 = (j % nkp) * VEC;
             const int c = c0 < p.off ? c0 : c0 + p.rd;  // columns outside [off, off + rd)
             const T* src = reinterpret_cast<const T*>(p.k) + ((size_t)t * p.Hkv + h) * p.dk + c;
-            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.kpool) + slot(h) * p.dk + c) =
-                *reinterpret_cast<const uint4*>(src);
+            if constexpr (F8)
+                *reinterpret_cast<uint2*>(p.kpool + slot(h) * p.dk + c) =
+                    quant8(*reinterpret_cast<const uint4*>(src), p.ks);
+            else
+                *reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.kpool) + slot(h) * p.dk + c) =
+                    *reinterpret_cast<const uint4*>(src);
         } else {
             if (!ok) continue;
             const int j = it - n_q - n_kr - n_kp;
             const int h = j / nv, c = (j % nv) * VEC;
             const T* src = reinterpret_cast<const T*>(p.v) + ((size_t)t * p.Hkv + h) * p.dv + c;
-            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.vpool) + slot(h) * p.dv + c) =
-                __ldg(reinterpret_cast<const uint4*>(src));
+            if constexpr (F8)
+                *reinterpret_cast<uint2*>(p.vpool + slot(h) * p.dv + c) =
+                    quant8(__ldg(reinterpret_cast<const uint4*>(src)), p.vs);
+            else
+                *reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.vpool) + slot(h) * p.dv + c) =
+                    __ldg(reinterpret_cast<const uint4*>(src));
         }
     }
 }
@@ -285,13 +307,19 @@ semipd_status spd_launch_rope_write(semipd_pool_t pool, int layer, void* q, void
     p.MBR = c.max_blocks_per_req;
     p.N_B = c.num_blocks;
     for (int i = 0; i < MAX_HALF; ++i) p.inv_freq[i] = pool->rope_inv_freq[i];
+    const bool f8 = c.dtype == SEMIPD_FP8_E4M3;
+    p.ks = f8 ? pool->k_scale[layer] : 1.f;
+    p.vs = f8 ? pool->v_scale[layer] : 1.f;
     const size_t smem = (size_t)rc.rot_dim * sizeof(float);
-    if (c.dtype == SEMIPD_BF16)
-        rc.interleaved ? rope_write_kernel<__nv_bfloat16, true><<<T, 256, smem, st>>>(p)
-                       : rope_write_kernel<__nv_bfloat16, false><<<T, 256, smem, st>>>(p);
+    if (f8)
+        rc.interleaved ? rope_write_kernel<__nv_bfloat16, true, true><<<T, 256, smem, st>>>(p)
+                       : rope_write_kernel<__nv_bfloat16, false, true><<<T, 256, smem, st>>>(p);
+    else if (c.dtype == SEMIPD_BF16)
+        rc.interleaved ? rope_write_kernel<__nv_bfloat16, true, false><<<T, 256, smem, st>>>(p)
+                       : rope_write_kernel<__nv_bfloat16, false, false><<<T, 256, smem, st>>>(p);
     else
-        rc.interleaved ? rope_write_kernel<float, true><<<T, 256, smem, st>>>(p)
-                       : rope_write_kernel<float, false><<<T, 256, smem, st>>>(p);
+        rc.interleaved ? rope_write_kernel<float, true, false><<<T, 256, smem, st>>>(p)
+                       : rope_write_kernel<float, false, false><<<T, 256, smem, st>>>(p);
     pool->launches += 1;
     return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }
@@ -303,12 +331,13 @@ extern "C" semipd_status semipd_set_rope(semipd_pool_t pool, const semipd_rope_c
         return SEMIPD_OK;
     }
     const auto& c = pool->cfg;
-    if (c.dtype == SEMIPD_FP8_E4M3) return SEMIPD_ERR_UNSUPPORTED;  // no fused quantised RoPE write
-    const semipd_status e = rope_check(c.head_dim_k, cfg->rot_offset, cfg->rot_dim, c.dtype,
+    // E4M3 pools carry bf16 activations (q / k_new); the fused write quantises (R31)
+    const int act = c.dtype == SEMIPD_FP8_E4M3 ? SEMIPD_BF16 : c.dtype;
+    const semipd_status e = rope_check(c.head_dim_k, cfg->rot_offset, cfg->rot_dim, act,
                                        cfg->theta, cfg->factor, cfg->low_freq_factor,
                                        cfg->high_freq_factor, cfg->original_max_pos);
     if (e != SEMIPD_OK) return e;
-    const int vec = c.dtype == SEMIPD_BF16 ? 8 : 4;
+    const int vec = act == SEMIPD_BF16 ? 8 : 4;
     const int half = cfg->rot_dim / 2;
     if ((cfg->interleaved ? cfg->rot_dim : half) % vec || cfg->rot_offset % vec ||
         c.head_dim_k % vec || c.head_dim_v % vec || half > MAX_HALF)

@@ -228,8 +228,10 @@ def test_fp8_host_errors():
         KVPool(PoolConfig(1, 8, 16, 8, 128, 128, 2, 4, dtype=F8), 0)
     rig = F8Rig(SHAPE, 8, 4, 4)
     rig.alloc([0, 1], [1, 1])
-    with pytest.raises(SemipdError, match="UNSUPPORTED"):
-        rig.pool.set_rope(RopeConfig(theta=500000.0))
+    rig.pool.set_rope(RopeConfig(theta=500000.0))  # E4M3 pools take fused RoPE (R28 + R31)
+    with pytest.raises(SemipdError, match="INVALID"):
+        rig.pool.set_rope(RopeConfig(theta=1.0))
+    rig.pool.set_rope(None)
     with pytest.raises(SemipdError, match="INVALID"):
         rig.pool.set_kv_scales(0.0, 1.0)
     q = torch.zeros(2, 32, 128, dtype=torch.bfloat16, device=rig.dev)

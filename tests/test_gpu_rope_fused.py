@@ -171,6 +171,74 @@ def test_fused_rope_fp32_generic_path_bitwise():
     assert np.array_equal(Kf, Kc) and np.array_equal(Vf, Vc)
 
 
+@pytest.mark.parametrize("inter", [False, True], ids=["half_split", "interleaved"])
+def test_fused_rope_fp8_decode_and_prefill_bitwise(inter):
+    """E4M3 pools (R31): with RoPE set, one pass rotates q / k_new and writes the rotated K and
+    the V rows as E4M3 codes; the FP8 kernels skip their own quantised write.  The pool codes,
+    the rotated rows and the outputs must equal the composed path's (semipd_rope, then the plain
+    FP8 call, whose own write applies the same rule to the rotated k_new) bit for bit."""
+    from test_gpu_fp8 import SHAPE, F8Rig
+    cfg, rk = LLAMA31, dict(interleaved=inter)
+    bs = SHAPE.block_size
+    # decode
+    ctx = [0, 15, 64, 700, 4097, 2048]
+    case = synth.decode_case(SHAPE, ctx, 63, synth.NEEDLE)
+    res = []
+    for fused in (True, False):
+        nb = [c // bs + 1 for c in ctx]
+        rig = F8Rig(SHAPE, sum(nb) + 3, len(ctx) + 1, max(nb) + 1)
+        rig.alloc(range(len(ctx)), nb)
+        for b in range(len(ctx)):
+            rig.put(0, b, case.k_ctx[b], case.v_ctx[b])
+        dev = rig.dev
+        q, k, v = (t.to(dev).contiguous() for t in (case.q, case.k_new, case.v_new))
+        out = torch.empty(len(ctx), 32, 128, dtype=torch.bfloat16, device=dev)
+        if fused:
+            rig.pool.set_rope(cfg, **rk)
+        else:
+            rope_(q, k, rig.i32(ctx), cfg, **rk)
+        rig.pool.decode_attn(0, q, k, v, rig.i32(range(len(ctx))), rig.i32(ctx), max(ctx),
+                             SHAPE.softmax_scale, out,
+                             rig.pool.new_decode_workspace(len(ctx), 32, max(ctx)), status=rig.status)
+        torch.cuda.synchronize()
+        assert int(rig.status.item()) == 0
+        res.append((out, q, k, rig.host_pool(0)))
+    (of, qf, kf, (Kf, Vf)), (oc, qc, kc, (Kc, Vc)) = res
+    assert _bitwise(qf, qc) and _bitwise(kf, kc), "decode: rotated rows differ"
+    assert np.array_equal(Kf, Kc) and np.array_equal(Vf, Vc), "decode: pool codes differ"
+    assert _bitwise(of, oc), "decode: fused output differs from the composed path"
+    # prefill (two requests with prefixes, one starting mid-page)
+    chunks, prefixes = [130, 77], [64, 500]
+    case = synth.prefill_case(SHAPE, chunks, prefixes, 64, synth.FLAT)
+    cu = np.concatenate([[0], np.cumsum(chunks)]).astype(np.int32)
+    pos = np.concatenate([np.arange(p, p + c) for c, p in zip(chunks, prefixes)]).astype(np.int32)
+    res = []
+    for fused in (True, False):
+        nb = [(p + c + bs - 1) // bs for p, c in zip(prefixes, chunks)]
+        rig = F8Rig(SHAPE, sum(nb) + 2, len(chunks) + 1, max(nb) + 1)
+        rig.alloc(range(len(chunks)), nb)
+        rig.pool.attach_fp8_prefill_scratch(len(chunks))
+        for i in range(len(chunks)):
+            rig.put(0, i, case.k_prefix[i], case.v_prefix[i])
+        dev = rig.dev
+        q, k, v = (t.to(dev).contiguous() for t in (case.q, case.k_new, case.v_new))
+        T = sum(chunks)
+        out = torch.empty(T, 32, 128, dtype=torch.bfloat16, device=dev)
+        if fused:
+            rig.pool.set_rope(cfg, **rk)
+        else:
+            rope_(q, k, torch.from_numpy(pos).to(dev), cfg, **rk)
+        rig.pool.prefill_attn(0, q, k, v, rig.i32(cu), rig.i32(range(len(chunks))), rig.i32(prefixes),
+                              T, max(chunks), SHAPE.softmax_scale, out, status=rig.status)
+        torch.cuda.synchronize()
+        assert int(rig.status.item()) == 0
+        res.append((out, q, k, rig.host_pool(0)))
+    (of, qf, kf, (Kf, Vf)), (oc, qc, kc, (Kc, Vc)) = res
+    assert _bitwise(qf, qc) and _bitwise(kf, kc), "prefill: rotated rows differ"
+    assert np.array_equal(Kf, Kc) and np.array_equal(Vf, Vc), "prefill: pool codes differ"
+    assert _bitwise(of, oc), "prefill: fused output differs from the composed path"
+
+
 def test_set_rope_validation_and_off():
     from paper_2504_19867_b200 import SemipdError
     shape = _shape(synth.CFG2_LLAMA8B, block_size=64)

@@ -408,7 +408,10 @@ semipd_status semipd_set_fp8_prefill_scratch(semipd_pool_t pool, void* mem, size
  *   sm_budget as in semipd_prefill_attn (caps each of the three persistent grids).
  * Pool: bf16, kv_shared, one KV head, head_dim_k 576, block_size in {16, 32, 64, 128}; H even,
  * <= 128 (else UNSUPPORTED / INVALID).  A block-table entry outside [0, N_B) sets BAD_BLOCK and
- * that key's latent is read as zeros.  No fused RoPE / peer epilogue (UNSUPPORTED).
+ * that key's latent is read as zeros.  No peer epilogue (UNSUPPORTED).  With RoPE set
+ * (semipd_set_rope, rot_offset >= 512: MLA's decoupled k_pe columns, else UNSUPPORTED) the call
+ * first rotates q_pe = q[..., 128 + (rot_offset - 512) ...] and kv_new's rope columns in place
+ * at prefix_lens[r] + t, with the same frequencies, before the prep writes the latent rows.
  * Kernels: a prep pass (copies), a tcgen05 up-projection GEMM over TMA-gathered pool pages, a
  * tcgen05 causal attention kernel with dqk 192 / dv 128 (trace kernel kind 10); three launches,
  * each with a launch span (semipd_set_spans) in that order. */

@@ -186,6 +186,12 @@ semipd_status spd_launch_rope_write(semipd_pool_t p, int layer, void* q, void* k
                                     const void* v_new, const int* cu_seqlens, const int* req_ids,
                                     const int* base_pos, int n, int T, int Hq, int* status_dev,
                                     cudaStream_t s);
+// the same pass with q rows of q_dk columns rotated from column q_off (the pool's k columns from
+// its rot_offset); write_pool = 0 rotates q / k_new in place only
+semipd_status spd_launch_rope_write_ex(semipd_pool_t p, int layer, void* q, int q_dk, int q_off,
+                                       void* k_new, const void* v_new, const int* cu_seqlens,
+                                       const int* req_ids, const int* base_pos, int n, int T, int Hq,
+                                       int write_pool, int* status_dev, cudaStream_t s);
 semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new, const void* v_new,
                                   const int* cu_seqlens, const int* req_ids, const int* pos0,
                                   int n, int total_rows, int mode, int* status_dev,

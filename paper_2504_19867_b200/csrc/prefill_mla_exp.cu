@@ -1305,7 +1305,11 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     if (num_heads <= 0 || num_heads % 2 || num_heads > 128) return SEMIPD_ERR_INVALID;
     if (sm_budget < -1 || sm_budget > pool->num_sms) return SEMIPD_ERR_INVALID;
     if (!x_pool_ok(pool)) return SEMIPD_ERR_UNSUPPORTED;
-    if (pool->rope_on || pool->pre_n_peers > 0) return SEMIPD_ERR_UNSUPPORTED;
+    if (pool->pre_n_peers > 0) return SEMIPD_ERR_UNSUPPORTED;
+    // RoPE (semipd_set_rope) on the decoupled columns only: k_pe = latent columns [512, 576)
+    // carry the rotation, q_pe = q columns [128, 192) the same frequencies (MLA's decoupled RoPE)
+    const int rope_qoff = pool->rope_on ? XDN + (pool->rope.rot_offset - XDC) : 0;
+    if (pool->rope_on && pool->rope.rot_offset < XDC) return SEMIPD_ERR_UNSUPPORTED;
     cudaStream_t st = static_cast<cudaStream_t>(s);
     if (status_dev && cudaMemsetAsync(status_dev, 0, sizeof(int), st) != cudaSuccess) return SEMIPD_ERR_CUDA;
     if (n == 0 || total_q == 0) return SEMIPD_OK;
@@ -1331,6 +1335,14 @@ extern "C" semipd_status semipd_prefill_mla_expanded(
     float* part = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(cnt) + x_cnt_bytes(slots));
     const int lg_bs = __builtin_ctz((unsigned)c.block_size);
 
+    // 0. with RoPE set: q_pe and the chunk's k_pe rotated in place at prefix + t (R4, R28); the
+    //    prep below then writes the rotated latent rows into the pool and Kpe
+    if (pool->rope_on) {
+        const semipd_status r = spd_launch_rope_write_ex(
+            pool, layer, const_cast<void*>(q), XDN + XDR, rope_qoff, const_cast<void*>(kv_new), nullptr,
+            cu_seqlens_q, req_ids, prefix_lens, n, total_q, H, 0, status_dev, st);
+        if (r != SEMIPD_OK) return r;
+    }
     // 1. prep: chunk latent rows -> pool, k_pe -> Kpe, row offsets -> hdr
     XPrep pp;
     pp.cu = cu_seqlens_q;

@@ -156,6 +156,9 @@ struct RopeWriteParams {
     int* status;
     int n, Hq, Hkv, dk, dv, off, rd, lg_bs, MBR, N_B;
     float ks, vs;  // E4M3 pools (F8): the layer's scales of the quantised write (R31)
+    int qdk, qoff;  // q row length and the first rotated q column (the pool's dk / off unless
+                    // q is narrower, as the expanded MLA prefill's [q_nope | q_pe] rows)
+    int write_pool; // 0: rotate q / k in place only (the caller's next pass writes the pool)
     double inv_freq[MAX_HALF];
 };
 
@@ -181,9 +184,9 @@ __global__ void __launch_bounds__(256) rope_write_kernel(const __grid_constant__
         pos = __ldg(p.base + t);
     }
     const int page = pos >> p.lg_bs;
-    const int blk = page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + r) * p.MBR + page) : -1;
+    const int blk = p.write_pool && page < p.MBR ? __ldg(p.bt + (size_t)__ldg(p.req_ids + r) * p.MBR + page) : -1;
     const bool ok = blk >= 0 && blk < p.N_B;
-    if (!ok && threadIdx.x == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
+    if (p.write_pool && !ok && threadIdx.x == 0 && p.status) atomicMax(p.status, SEMIPD_ERR_BAD_BLOCK);
     const int half = p.rd >> 1;
     for (int i = threadIdx.x; i < half; i += blockDim.x) {
         double s, c;
@@ -193,8 +196,8 @@ __global__ void __launch_bounds__(256) rope_write_kernel(const __grid_constant__
     }
     __syncthreads();
     const int nrot = (INTER ? p.rd : half) / VEC;  // rotation items per head row
-    const int nkp = (p.dk - p.rd) / VEC;           // unrotated k vectors per head row
-    const int nv = p.vpool ? p.dv / VEC : 0;
+    const int nkp = p.write_pool ? (p.dk - p.rd) / VEC : 0;  // unrotated k vectors per head row
+    const int nv = p.write_pool && p.vpool ? p.dv / VEC : 0;
     const int n_q = p.Hq * nrot, n_kr = p.Hkv * nrot, n_kp = p.Hkv * nkp, n_v = p.Hkv * nv;
     const int total = n_q + n_kr + n_kp + n_v;
     const size_t bs_mask = ((size_t)1 << p.lg_bs) - 1;
@@ -204,9 +207,8 @@ __global__ void __launch_bounds__(256) rope_write_kernel(const __grid_constant__
             const bool is_q = it < n_q;
             const int j = is_q ? it : it - n_q;
             const int h = j / nrot, i0 = (j % nrot) * VEC;
-            T* row = is_q ? reinterpret_cast<T*>(p.q) + ((size_t)t * p.Hq + h) * p.dk
-                          : reinterpret_cast<T*>(p.k) + ((size_t)t * p.Hkv + h) * p.dk;
-            row += p.off;
+            T* row = is_q ? reinterpret_cast<T*>(p.q) + ((size_t)t * p.Hq + h) * p.qdk + p.qoff
+                          : reinterpret_cast<T*>(p.k) + ((size_t)t * p.Hkv + h) * p.dk + p.off;
             uint4 a = *reinterpret_cast<const uint4*>(row + i0);
             T* xa = reinterpret_cast<T*>(&a);
             uint4 b = a;
@@ -279,6 +281,15 @@ semipd_status spd_launch_rope_write(semipd_pool_t pool, int layer, void* q, void
                                     const void* v_new, const int* cu_seqlens, const int* req_ids,
                                     const int* base_pos, int n, int T, int Hq, int* status_dev,
                                     cudaStream_t st) {
+    return spd_launch_rope_write_ex(pool, layer, q, pool->cfg.head_dim_k, pool->rope.rot_offset,
+                                    k_new, v_new, cu_seqlens, req_ids, base_pos, n, T, Hq, 1,
+                                    status_dev, st);
+}
+
+semipd_status spd_launch_rope_write_ex(semipd_pool_t pool, int layer, void* q, int q_dk, int q_off,
+                                       void* k_new, const void* v_new, const int* cu_seqlens,
+                                       const int* req_ids, const int* base_pos, int n, int T, int Hq,
+                                       int write_pool, int* status_dev, cudaStream_t st) {
     const auto& c = pool->cfg;
     const auto& rc = pool->rope;
     if (T <= 0) return SEMIPD_OK;
@@ -303,6 +314,9 @@ semipd_status spd_launch_rope_write(semipd_pool_t pool, int layer, void* q, void
     p.dv = c.head_dim_v;
     p.off = rc.rot_offset;
     p.rd = rc.rot_dim;
+    p.qdk = q_dk;
+    p.qoff = q_off;
+    p.write_pool = write_pool;
     p.lg_bs = __builtin_ctz((unsigned)c.block_size);
     p.MBR = c.max_blocks_per_req;
     p.N_B = c.num_blocks;

@@ -188,3 +188,59 @@ def test_mla_expanded_total_q_smaller_than_cu():
     torch.cuda.synchronize()
     assert int(st.item()) == 1
     assert torch.all(buf[T:] == 7.0)
+
+
+@pytest.mark.parametrize("inter", [True, False], ids=["interleaved", "half_split"])
+def test_mla_expanded_fused_rope_bitwise(inter):
+    """RoPE set on the pool (semipd_set_rope, R28) on the decoupled columns: the call rotates
+    q_pe = q[..., 128:192] and k_pe = kv_new[..., 512:576] in place at prefix + t before the
+    prep writes the chunk's latent rows.  q, kv_new, the pool and the output equal the composed
+    path (semipd_rope on the two column ranges, then the plain call) bit for bit, and the output
+    matches the oracle over the rotated rows."""
+    from paper_2504_19867_b200 import RopeConfig, rope_
+    ds = RopeConfig(theta=10000.0, factor=0.0)
+    chunks, prefixes = [100, 37], [0, 70]
+    case = synth.mla_expanded_case(chunks, prefixes, 91, H, synth.FLAT)
+    n, bs = len(chunks), 64
+    need = [-(-(p + c) // bs) for p, c in zip(prefixes, chunks)]
+    pos = np.concatenate([np.arange(p, p + c) for c, p in zip(chunks, prefixes)]).astype(np.int32)
+    res = []
+    for fused in (True, False):
+        rig = Rig(_shape(bs), num_blocks=sum(need) + 3, max_reqs=n, mbr=max(need) + 1)
+        for i in range(n):
+            rig.alloc([i], [need[i]])
+        K, _, BT, _ = rig.pool.views(0)
+        bt = BT.cpu().numpy().copy()
+        K.zero_()
+        for i in range(n):
+            for j in range(prefixes[i]):
+                K[bt[i, j // bs], 0, j % bs] = case.lat[i][j].to(rig.dev)
+        pool_ref = np_bits(K)
+        dev = rig.dev
+        q, kv = case.q.to(dev).contiguous(), case.kv_new.to(dev).contiguous()
+        T = case.cu[-1]
+        if fused:
+            rig.pool.set_rope(ds, rot_offset=512, rot_dim=64, interleaved=inter)
+        else:
+            p32 = torch.from_numpy(pos).to(dev)
+            rope_(q, None, p32, ds, rot_offset=128, rot_dim=64, interleaved=inter)
+            rope_(None, kv.view(T, 1, 576), p32, ds, rot_offset=512, rot_dim=64, interleaved=inter)
+        ws = rig.pool.new_mla_expanded_workspace(n, sum(need) * bs, H)
+        out = torch.empty((T, H, 128), dtype=torch.bfloat16, device=dev)
+        rig.pool.prefill_mla_expanded(0, q, kv, case.w_uk.to(dev), case.w_uv.to(dev), rig.i32(case.cu),
+                                      rig.i32(range(n)), rig.i32(prefixes), T, max(chunks),
+                                      sum(need) * bs, case.scale, out, ws, status=rig.status)
+        torch.cuda.synchronize()
+        assert int(rig.status.item()) == 0
+        res.append((out, q, kv, np_bits(K), pool_ref, bt))
+    (of, qf, kf, Kf, pref, bt), (oc, qc, kc, Kc, _, _) = res
+    eq = lambda a, b: torch.equal(a.contiguous().view(torch.uint8), b.contiguous().view(torch.uint8))  # noqa: E731
+    assert eq(qf, qc) and eq(kf, kc), "rotated rows differ from semipd_rope's"
+    assert not eq(qf.cpu(), case.q), "q was not rotated"
+    assert eq(qf[..., :128].cpu(), case.q[..., :128]) and eq(kf[..., :512].cpu(), case.kv_new[..., :512])
+    np.testing.assert_array_equal(Kf, Kc)
+    assert eq(of, oc), "fused output differs from the composed path"
+    ref = oracle.prefill_mla_expanded(np_bits(qf), np_bits(kf), pref, bt, np.array(case.cu, np.int32),
+                                      np.arange(n, dtype=np.int32), np.array(prefixes, np.int32),
+                                      np_bits(case.w_uk), np_bits(case.w_uv), case.scale)
+    compare(of.float().cpu().double().numpy(), ref, torch.bfloat16, "mla_expanded + rope vs oracle")

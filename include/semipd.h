@@ -204,9 +204,9 @@ semipd_status semipd_prefill_attn(semipd_pool_t pool, int32_t layer, const void*
  *   ZERO-FILLED before its first use (the kernels leave their counters at zero);
  *   sm_budget as in semipd_prefill_attn (0 = partition's decode budget).
  * FP8 pools (reading R31): the appended row is quantised and every key / value (the appended
- * one included) is read back dequantised; num_q_heads / Hkv <= 8; no peer epilogue (else
- * UNSUPPORTED); with RoPE set the rotation pass writes the quantised rows and the kernel skips
- * its own append.  Kernel: head-pair E4M3 boxes converted to f16 in registers,
+ * one included) is read back dequantised; num_q_heads / Hkv <= 8; the peer epilogue
+ * (semipd_set_decode_peers) is supported as for bf16; with RoPE set the rotation pass writes
+ * the quantised rows and the kernel skips its own append.  Kernel: head-pair E4M3 boxes converted to f16 in registers,
  * f16 mma.sync with fp32 accumulation (kernel kind 9). */
 semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* q,
                                  const void* k_new, const void* v_new, const int32_t* req_ids,
@@ -297,8 +297,8 @@ semipd_status semipd_peer_gather(const void* src, size_t bytes, void* const* dst
  * epilogue performs this rank's part of the all-gather itself (posted NVLink stores, no
  * copies).  Bracket each such decode call with semipd_peer_handshake: which = 0 ("ready")
  * before it, so no peer is still reading the buffer, and which = 1 ("landed") after it, which
- * fences the kernel's stores and waits until every peer's have landed here.  Only the bf16
- * split-K decode kernels support peers: other decode paths return UNSUPPORTED, row-major
+ * fences the kernel's stores and waits until every peer's have landed here.  Only the split-K
+ * decode kernels (bf16 and E4M3 pages) support peers: other decode paths return UNSUPPORTED, row-major
  * output INVALID.  `tokens` (> 0 when n > 0) is the token count B the gathered buffers were
  * sized for ([Hq, tokens, dv]): the peer offsets depend on it, so a later decode call whose
  * batch differs returns INVALID (and launches nothing) instead of storing at wrong offsets or

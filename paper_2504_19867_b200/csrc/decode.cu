@@ -1355,15 +1355,16 @@ semipd_status semipd_decode_attn(semipd_pool_t pool, int32_t layer, const void* 
     if (!q || !k_new || (!v_new && !c.kv_shared) || !req_ids || !ctx_lens || !out)
         return SEMIPD_ERR_INVALID;
     const int budget = spd_resolve_budget(pool, sm_budget, false);
-    if (pool->dec_n_peers > 0 && (!out_head_major || !fast_path_ok(pool, num_q_heads) ||
+    // the split-K kernels (bf16 and E4M3 pages) support peers
+    const bool f8_pool = c.dtype == SEMIPD_FP8_E4M3;
+    if (pool->dec_n_peers > 0 && (!out_head_major || (!f8_pool && !fast_path_ok(pool, num_q_heads)) ||
                                   spd_mla_tc_ok(pool, num_q_heads) ||
                                   spd_mla_decode_ok(pool, num_q_heads)))
         return pool->dec_n_peers > 0 && !out_head_major ? SEMIPD_ERR_INVALID : SEMIPD_ERR_UNSUPPORTED;
     // the peer offsets were fixed for the gathered buffers' batch: any other batch would store
     // at wrong head / token positions or past a peer's buffer
     if (pool->dec_n_peers > 0 && batch != pool->dec_peer_tokens) return SEMIPD_ERR_INVALID;
-    if (c.dtype == SEMIPD_FP8_E4M3) {  // E4M3 pages (reading R31): quantised append + decode
-        if (pool->dec_n_peers > 0) return SEMIPD_ERR_UNSUPPORTED;
+    if (f8_pool) {  // E4M3 pages (reading R31): quantised append + decode
         if (pool->rope_on) {
             // RoPE of q / k_new in place at ctx, fused with the quantised append of the rotated
             // rows (R28 + R31); the FP8 kernel skips its own append

@@ -269,7 +269,19 @@ struct DecParams {
     float ks, vs;                // write scales (append)
     float v_out;                 // v_scale, applied with 1 / l
     SpdTrace trace;
+    // TP head all-gather fused into the epilogue (N2, as decode.cu): every output vector is also
+    // stored to each peer's gathered buffer (peer-mapped, already offset to this rank's shard)
+    __nv_bfloat16* peers[SEMIPD_MAX_PEERS - 1];
+    int n_peers;
 };
+
+// one bf16x4 output vector: local buffer, then every peer's gathered buffer
+__device__ __forceinline__ void f8_store_out(const DecParams& p, size_t off, uint2 v) {
+    *reinterpret_cast<uint2*>(p.out + off) = v;
+#pragma unroll
+    for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k)
+        if (k < p.n_peers) *reinterpret_cast<uint2*>(p.peers[k] + off) = v;
+}
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     decode_fp8_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
@@ -630,7 +642,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     uint2 v;
                     v.x = pack_bf16(o.x * inv, o.y * inv);
                     v.y = pack_bf16(o.z * inv, o.w * inv);
-                    *reinterpret_cast<uint2*>(p.out + off) = v;
+                    f8_store_out(p, off, v);
                 } else {
                     const size_t pi = ((size_t)d.b * p.Hq + hq) * (p.S_max * NPIECE) + d.s;
                     *reinterpret_cast<float4*>(p.ws_acc + pi * HD + c) = o;
@@ -672,7 +684,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         uint2 v;
                         v.x = pack_bf16(o.x * inv, o.y * inv);
                         v.y = pack_bf16(o.z * inv, o.w * inv);
-                        *reinterpret_cast<uint2*>(p.out + off) = v;
+                        f8_store_out(p, off, v);
                     }
                     if (tid == 0) p.ws_cnt[d.b * p.Hkv + d.g] = 0;  // ready for the next call
                 }
@@ -851,6 +863,9 @@ semipd_status spd_launch_decode_fp8(semipd_pool_t pool, int layer, const void* q
     prm.n_units = NPIECE * S0_max * batch * (c.num_kv_heads / 2);
     prm.out_head_major = out_head_major;
     prm.skip_append = pool->rope_on ? 1 : 0;
+    prm.n_peers = pool->dec_n_peers;
+    for (int k = 0; k < SEMIPD_MAX_PEERS - 1; ++k)
+        prm.peers[k] = k < pool->dec_n_peers ? static_cast<__nv_bfloat16*>(pool->dec_peers[k]) : nullptr;
     prm.scale_log2 = scale * pool->k_scale[layer] * LOG2E * (SPD_F8_KALU ? 256.f : 1.f);
     prm.ks = pool->k_scale[layer];
     prm.vs = pool->v_scale[layer];

@@ -359,3 +359,90 @@ def test_prefill_epilogue_peer_stores_emulated(tpn):
                               vs[:C - 1].contiguous(), i32([0, C - 1]), rid, pre, C - 1, C - 1, sc,
                               outs[0][ql:qh, :C - 1], out_head_major=True)
     assert ei.value.status == INVALID
+
+
+def _decode_pool_f8(shape, ctx, case, heads_kv, dev, ks, vs):
+    """An E4M3 pool (R31) holding kv heads [heads_kv) of the cached contexts as the oracle's codes."""
+    from paper_2504_19867_b200 import KVPool, PoolConfig
+    kl, kh = heads_kv
+    bs = shape.block_size
+    nb = [c // bs + 1 for c in ctx]
+    pool = KVPool(PoolConfig(1, sum(nb) + 2, bs, kh - kl, 128, 128, len(ctx), max(nb),
+                             dtype=torch.float8_e4m3fn), dev)
+    pool.set_kv_scales(ks, vs)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    for b, n in enumerate(nb):
+        pool.alloc_blocks(i32([b]), i32([n]))
+    K, V, BT, _ = pool.views(0)
+    bt = BT.cpu()
+    for b, c in enumerate(ctx):
+        pos = torch.arange(c)
+        blk = bt[b].long()[pos // bs].to(dev)
+        kc = torch.from_numpy(oracle.e4m3_quantize(np_bits(case.k_ctx[b][:, kl:kh]), ks))
+        vc = torch.from_numpy(oracle.e4m3_quantize(np_bits(case.v_ctx[b][:, kl:kh]), vs))
+        K[blk, :, (pos % bs).to(dev)] = kc.to(dev)
+        V[blk, :, (pos % bs).to(dev)] = vc.to(dev)
+    return pool
+
+
+@pytest.mark.parametrize("tpn", [2, 4])
+def test_decode_epilogue_peer_stores_fp8_emulated(tpn):
+    """The fused TP head gather on E4M3 pools (N2 x R31): rank r's FP8 decode kernel stores its
+    head slice into every rank's gathered buffer; each gathered buffer equals the unsharded FP8
+    decode bitwise and the oracle's FP8 decode within the bf16 bar.  (FP8 decode units are head
+    pairs, so every rank keeps an even number of kv heads: TP <= 4 for 8 kv heads.)"""
+    import ctypes
+
+    import synth
+    from paper_2504_19867_b200 import lib, tp
+    dev = torch.device("cuda", 0)
+    shape = synth.AttnShape("llama3-70b-fp8", 64, 8, 128, 128, 64, torch.bfloat16)
+    ks, vs = 0.05, 0.02
+    ctx = [300, 2048, 4500, 64]
+    B = len(ctx)
+    cd = synth.decode_case(shape, ctx, seed=3041)
+    i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+    sc = shape.softmax_scale
+    full_pool = _decode_pool_f8(shape, ctx, cd, (0, 8), dev, ks, vs)
+    kp, vp = (t.cpu().numpy().copy() for t in full_pool.views(0)[:2])
+    ref = torch.empty(64, B, 128, dtype=torch.bfloat16, device=dev)
+    full_pool.decode_attn(0, cd.q.to(dev), cd.k_new.to(dev), cd.v_new.to(dev), i32(list(range(B))),
+                          i32(ctx), max(ctx), sc, ref, full_pool.new_decode_workspace(B, 64, max(ctx)),
+                          out_head_major=True)
+    torch.cuda.synchronize()
+    pools, outs, flags, streams, wss, ins = [], [], [], [], [], []
+    hq = 64 // tpn
+    for r in range(tpn):
+        pools.append(_decode_pool_f8(shape, ctx, cd, tp.head_range(8, tpn, r), dev, ks, vs))
+        outs.append(torch.full((64, B, 128), float("nan"), dtype=torch.bfloat16, device=dev))
+        flags.append(torch.zeros(2 * tpn, dtype=torch.int32, device=dev))
+        streams.append(torch.cuda.Stream(dev))
+        wss.append(pools[r].new_decode_workspace(B, hq, max(ctx)))
+        ql, qh = tp.head_range(64, tpn, r)
+        kl, kh = tp.head_range(8, tpn, r)
+        ins.append((cd.q[:, ql:qh].contiguous().to(dev), cd.k_new[:, kl:kh].contiguous().to(dev),
+                    cd.v_new[:, kl:kh].contiguous().to(dev), ql, qh))
+    fl = (ctypes.c_void_p * tpn)(*[f.data_ptr() for f in flags])
+    L = lib()
+    rid, ctx_d = i32(list(range(B))), i32(ctx)
+    torch.cuda.synchronize()
+    shard = hq * B * 128 * 2
+    for r in range(tpn):
+        pools[r].set_decode_peers([outs[k].data_ptr() + r * shard for k in range(tpn) if k != r], B)
+    for r in range(tpn):
+        qs, kn, vn, ql, qh = ins[r]
+        cs = ctypes.c_void_p(streams[r].cuda_stream)
+        assert L.semipd_peer_handshake(fl, ctypes.c_void_p(flags[r].data_ptr()), tpn, r, 0, cs) == 0
+        pools[r].decode_attn(0, qs, kn, vn, rid, ctx_d, max(ctx), sc, outs[r][ql:qh], wss[r],
+                             out_head_major=True, stream=streams[r])
+        assert L.semipd_peer_handshake(fl, ctypes.c_void_p(flags[r].data_ptr()), tpn, r, 1, cs) == 0
+    torch.cuda.synchronize()
+    for r in range(tpn):
+        assert torch.equal(outs[r].view(torch.int16), ref.view(torch.int16)), r
+    ref64 = oracle.decode_fp8(np_bits(cd.q), np_bits(cd.k_new), np_bits(cd.v_new), kp, vp,
+                              full_pool.views(0)[2].cpu().numpy(), np.arange(B), ctx, sc, ks, vs)
+    for r in range(tpn):
+        compare(outs[r].float().cpu().double().numpy().transpose(1, 0, 2), ref64, torch.bfloat16,
+                f"fused fp8 decode gather tp{tpn} rank {r}")
+    for p in pools:
+        p.set_decode_peers([])

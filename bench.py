@@ -764,7 +764,8 @@ class E2E:
         self.qp, self.kp, self.vp = list(w.qp), list(w.kp), list(w.vp)
         self.qd, self.kd, self.vd = list(w.qd), list(w.kd), list(w.vd)
         self.op, self.od = list(w.op), list(w.od)
-        self.packed = not w.fused
+        # (TP > 1 gathers the workload's own output buffers, so it keeps the per-tensor copies)
+        self.packed = not w.fused and w.tp == 1
         if self.packed:
             # one pinned buffer and one device buffer per layer holding all six inputs (and one
             # pair for the two outputs): one H2D and one D2H copy per layer instead of six and

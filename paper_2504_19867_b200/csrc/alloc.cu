@@ -117,6 +117,10 @@ __global__ void __launch_bounds__(kThreads) alloc_kernel(AllocArgs a, const int*
     __shared__ int s_flag, s_top;
     __shared__ unsigned long long s_seq;
     const int tid = threadIdx.x;
+    // PDL: everything before this call on the stream is complete; the next kernel may launch
+    // now (its own griddepcontrol.wait holds it until this one has completed)
+    spd::pdl_wait();
+    spd::pdl_trigger();
     if (tid == 0) {
         lock_acquire(a.st);
         s_top = __ldcg(&a.st->top);
@@ -206,6 +210,10 @@ __global__ void __launch_bounds__(kThreads) free_kernel(AllocArgs a, const int* 
     __shared__ int s_flag, s_top;
     __shared__ unsigned long long s_seq;
     const int tid = threadIdx.x;
+    // PDL: everything before this call on the stream is complete; the next kernel may launch
+    // now (its own griddepcontrol.wait holds it until this one has completed)
+    spd::pdl_wait();
+    spd::pdl_trigger();
     if (tid == 0) {
         lock_acquire(a.st);
         s_top = __ldcg(&a.st->top);
@@ -294,9 +302,10 @@ semipd_status semipd_alloc_blocks(semipd_pool_t pool, const int32_t* req_ids,
         return SEMIPD_OK;
     }
     if (!req_ids || !n_blocks) return SEMIPD_ERR_INVALID;
-    alloc_kernel<<<1, kThreads, 0, st>>>(args_of(pool), req_ids, n_blocks, n, status_dev);
+    const cudaError_t le = spd_launch_pdl(alloc_kernel, dim3(1), dim3(kThreads), 0, st, args_of(pool),
+                                          req_ids, n_blocks, n, status_dev);
     pool->launches += 1;
-    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+    return le == cudaSuccess && cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }
 
 semipd_status semipd_free_blocks(semipd_pool_t pool, const int32_t* req_ids, int32_t n,
@@ -309,9 +318,10 @@ semipd_status semipd_free_blocks(semipd_pool_t pool, const int32_t* req_ids, int
         return SEMIPD_OK;
     }
     if (!req_ids) return SEMIPD_ERR_INVALID;
-    free_kernel<<<1, kThreads, 0, st>>>(args_of(pool), req_ids, n, status_dev);
+    const cudaError_t le = spd_launch_pdl(free_kernel, dim3(1), dim3(kThreads), 0, st, args_of(pool),
+                                          req_ids, n, status_dev);
     pool->launches += 1;
-    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+    return le == cudaSuccess && cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }
 
 }  // extern "C"

@@ -169,6 +169,8 @@ struct KvWriteArgs {
 constexpr int kWarps = 8;
 
 __global__ void __launch_bounds__(kWarps * 32) kv_write_fp8_kernel(KvWriteArgs a) {
+    pdl_wait();  // PDL: the previous kernel is complete; the next may launch (it waits itself)
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     const long long total = (long long)a.rows * a.Hkv;
     for (long long u = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5); u < total;
@@ -213,6 +215,8 @@ struct DequantArgs {
 };
 
 __global__ void __launch_bounds__(kWarps * 32) dequant_prefix_kernel(DequantArgs a) {
+    pdl_wait();  // PDL: the previous kernel is complete; the next may launch (it waits itself)
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     const long long total = (long long)a.n * a.MBR * a.Hkv * 2;
     for (long long u = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5); u < total;
@@ -781,9 +785,9 @@ semipd_status spd_launch_kv_write_fp8(semipd_pool_t p, int layer, const void* k_
     a.vs = p->v_scale[layer];
     long long grid = ((long long)total_rows * c.num_kv_heads + kWarps - 1) / kWarps;
     if (grid > 16LL * p->num_sms) grid = 16LL * p->num_sms;
-    kv_write_fp8_kernel<<<(unsigned)grid, kWarps * 32, 0, s>>>(a);
+    const cudaError_t le = spd_launch_pdl(kv_write_fp8_kernel, dim3((unsigned)grid), dim3(kWarps * 32), 0, s, a);
     p->launches += 1;
-    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+    return le == cudaSuccess && cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }
 
 semipd_status spd_launch_dequant_prefix(semipd_pool_t p, int layer, const int* req_ids,
@@ -811,9 +815,9 @@ semipd_status spd_launch_dequant_prefix(semipd_pool_t p, int layer, const int* r
     const long long cap = budget > 0 ? 4LL * budget : 4LL * p->num_sms;
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    dequant_prefix_kernel<<<(unsigned)grid, kWarps * 32, 0, s>>>(a);
+    const cudaError_t le = spd_launch_pdl(dequant_prefix_kernel, dim3((unsigned)grid), dim3(kWarps * 32), 0, s, a);
     p->launches += 1;
-    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+    return le == cudaSuccess && cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }
 
 void spd_fp8_prefill_view(const semipd_pool* p, const int** ids, const int** bt, int* n_pages_blocks) {

@@ -57,6 +57,10 @@ __global__ void __launch_bounds__(kKvWarps * 32)
                     const uint4* __restrict__ v_new, unsigned char* k_pool,
                     unsigned char* v_pool, const int* __restrict__ bt, int MBR, int N_B, int Hkv,
                     int bs, int k_vec, int v_vec, int* status) {
+    // PDL: the previous kernel is complete; the attention kernel that follows may launch now
+    // (its own griddepcontrol.wait holds its reads of these rows until this kernel completes)
+    spd::pdl_wait();
+    spd::pdl_trigger();
     const int lane = threadIdx.x & 31;
     const long long total = (long long)rows * Hkv;
     for (long long u = (long long)blockIdx.x * kKvWarps + (threadIdx.x >> 5); u < total;
@@ -211,13 +215,14 @@ semipd_status spd_launch_kv_write(semipd_pool_t p, int layer, const void* k_new,
     long long grid = (units + kKvWarps - 1) / kKvWarps;
     if (grid > 16LL * p->num_sms) grid = 16LL * p->num_sms;
     unsigned char* vpool = c.kv_shared ? nullptr : static_cast<unsigned char*>(p->v_layer(layer));
-    kv_write_kernel<<<(unsigned)grid, kKvWarps * 32, 0, s>>>(m, total_rows, static_cast<const uint4*>(k_new),
+    const cudaError_t le = spd_launch_pdl(kv_write_kernel, dim3((unsigned)grid), dim3(kKvWarps * 32), 0, s,
+                                          m, total_rows, static_cast<const uint4*>(k_new),
                                         static_cast<const uint4*>(v_new),
                                         static_cast<unsigned char*>(p->k_layer(layer)), vpool,
                                         p->bt, c.max_blocks_per_req, c.num_blocks,
                                         c.num_kv_heads, c.block_size, k_vec, v_vec, status_dev);
     p->launches += 1;
-    return cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
+    return le == cudaSuccess && cudaGetLastError() == cudaSuccess ? SEMIPD_OK : SEMIPD_ERR_CUDA;
 }
 
 semipd_status spd_launch_simt_attn(semipd_pool_t p, int layer, const void* q, const int* cu_seqlens,
